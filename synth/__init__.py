@@ -1,0 +1,322 @@
+"""Seeded synthetic workloads shaped like the paper's test cases.
+
+This module is shared by the oracle tests and the CUDA path.  It holds NO part of
+the method's arithmetic (no kernel, no neighbour search, no pressure solve): it
+only lays particles on lattices, applies the seeded jitter, evaluates the
+*initial conditions* the paper prints, and records the scheme parameters each
+case uses.  Everything returned is plain numpy (fp64 / int32).
+
+Case recipes (SURVEY.md §8(d) "Synthetic inputs"):
+
+* ``tgv2d``   — PAPER.md:931-946 §4.1 eq:tgv (BASELINE configs[0]).
+* ``hydrostatic`` — BASELINE configs[1]; wall layout of PAPER.md:808-813 §3.4.
+* ``dambreak2d``  — PAPER.md:1352-1371 §4.5 (BASELINE configs[2]).
+* ``tgv3d``   — BASELINE configs[3] (not in the paper; standard 3D TG field).
+* ``dambreak3d``  — PAPER.md:1407-1428 §4.6, per-GPU slab of BASELINE configs[4].
+
+Lattice sites sit at (i + 1/2) dx with x fastest; jitter is
+``numpy.random.default_rng(seed).uniform(-a, a, (N, dim))`` in lattice order,
+then wrapped into periodic boxes.  Masses are rho0 * dx**dim for every particle
+(fluid and wall); initial density is rho0.  Tags: 0 fluid, 1 wall.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+FLUID = 0
+WALL = 1
+
+# pressure-gradient forms (PAPER.md:320-339 eq:mom:sph:press:symm / :pij)
+PGRAD_SYMM = 0
+PGRAD_ASYMM = 1
+
+
+@dataclass
+class Case:
+    """A synthetic workload: particles, domain, scheme parameters, timestep."""
+
+    name: str
+    dim: int
+    h: float
+    dx: float
+    dt: float
+    steps: int
+    lo: list
+    hi: list
+    periodic: list
+    x: np.ndarray          # (n, dim) fp64
+    u: np.ndarray          # (n, dim) fp64
+    m: np.ndarray          # (n,) fp64
+    rho: np.ndarray        # (n,) fp64
+    p: np.ndarray          # (n,) fp64
+    tag: np.ndarray        # (n,) int32
+    params: dict = field(default_factory=dict)
+
+    @property
+    def n(self) -> int:
+        return int(self.x.shape[0])
+
+    @property
+    def n_fluid(self) -> int:
+        return int((self.tag == FLUID).sum())
+
+    @property
+    def n_wall(self) -> int:
+        return int((self.tag == WALL).sum())
+
+
+def default_params(**kw) -> dict:
+    """Scheme parameters with the paper's defaults.
+
+    omega=0.5, tol=1e-2, max_iter=1000 and
+    min_iter=2, eta=0.01, free-surface
+    ratio 0.8, K=10 GTVF sub-steps (reading R22).
+    """
+    p = dict(
+        rho0=1.0, nu=0.0, g=[0.0, 0.0, 0.0], alpha=0.0, c_ref=0.0,
+        omega=0.5, tol=1e-2, max_iter=1000, min_iter=2, K=10,
+        pgrad=PGRAD_SYMM, h_tilde_factor=1.0, pref_external=0, p_ref=0.0,
+        ustar_noslip=0, clamp_wall_p=0, fs_ratio=0.8, eta=0.01, precision=64,
+    )
+    p.update(kw)
+    return p
+
+
+def _lattice(counts, dx, origin):
+    """Sites (i + 1/2) dx + origin, x fastest.  counts = (nx, ny[, nz])."""
+    axes = [origin[a] + (np.arange(c) + 0.5) * dx for a, c in enumerate(counts)]
+    grids = np.meshgrid(*axes[::-1], indexing="ij")  # slowest first
+    pts = np.stack([g.ravel() for g in grids[::-1]], axis=1)
+    return pts
+
+
+def _jitter(x, amp, seed, lo, hi, periodic):
+    if amp <= 0:
+        return x
+    rng = np.random.default_rng(seed)
+    x = x + rng.uniform(-amp, amp, x.shape)
+    for a in range(x.shape[1]):
+        if periodic[a]:
+            L = hi[a] - lo[a]
+            x[:, a] = np.where(x[:, a] >= hi[a], x[:, a] - L, x[:, a])
+            x[:, a] = np.where(x[:, a] < lo[a], x[:, a] + L, x[:, a])
+    return x
+
+
+def _pad3(v):
+    v = list(v)
+    return v + [0.0] * (3 - len(v))
+
+
+# --------------------------------------------------------------------------
+# C1  2D Taylor-Green vortex (§4.1, eq:tgv)
+# --------------------------------------------------------------------------
+def tgv2d(n: int = 50, re: float = 100.0, jitter: float = 0.1, seed: int = 101,
+          steps: int = 10, tol: float = 1e-4, K: int = 10, precision: int = 64) -> Case:
+    L, U, rho0 = 1.0, 1.0, 1.0
+    dx = L / n
+    h = dx  # h/dx = 1.0
+    nu = U * L / re
+    lo, hi, per = [0.0, 0.0], [L, L], [1, 1]
+    x = _lattice((n, n), dx, lo)
+    x = _jitter(x, jitter * dx, seed, lo, hi, per)
+    X, Y = x[:, 0], x[:, 1]
+    # eq:tgv at t = 0
+    u = np.stack([-U * np.cos(2 * np.pi * X) * np.sin(2 * np.pi * Y),
+                  U * np.sin(2 * np.pi * X) * np.cos(2 * np.pi * Y)], axis=1)
+    p = -U * U * (np.cos(4 * np.pi * X) + np.cos(4 * np.pi * Y)) / 4.0
+    npart = x.shape[0]
+    # fixed dt = min(0.25 h/U, 0.25 h^2/nu)
+    dt = min(0.25 * h / U, 0.25 * h * h / nu)
+    # internal flow: p_ref = 2 max(p) (reading R22); max p = U^2/2
+    params = default_params(rho0=rho0, nu=nu, pgrad=PGRAD_ASYMM, h_tilde_factor=1.0,
+                            pref_external=0, p_ref=2.0 * 0.5 * rho0 * U * U, tol=tol, K=K,
+                            precision=precision)
+    return Case("tgv2d", 2, h, dx, dt, steps, _pad3(lo), _pad3(hi), per + [0], x, u,
+                np.full(npart, rho0 * dx * dx), np.full(npart, rho0), p,
+                np.zeros(npart, np.int32), params)
+
+
+# --------------------------------------------------------------------------
+# walled 2D tanks (hydrostatic column, dam break)
+# --------------------------------------------------------------------------
+def _tank2d(nfx, nfy, tank_nx, wall_ny, layers, dx):
+    """Fluid block nfx x nfy at the tank's lower-left corner; walls: floor
+    (spanning the whole tank incl. corners) and both sides up to wall_ny rows."""
+    fluid = _lattice((nfx, nfy), dx, (0.0, 0.0))
+    walls = []
+    # floor: y = -(l + 1/2) dx, x = (i + 1/2) dx for i in [-layers, tank_nx + layers)
+    xs = (np.arange(-layers, tank_nx + layers) + 0.5) * dx
+    for l in range(layers):
+        walls.append(np.stack([xs, np.full_like(xs, -(l + 0.5) * dx)], axis=1))
+    ys = (np.arange(wall_ny) + 0.5) * dx
+    for l in range(layers):
+        walls.append(np.stack([np.full_like(ys, -(l + 0.5) * dx), ys], axis=1))
+        walls.append(np.stack([np.full_like(ys, tank_nx * dx + (l + 0.5) * dx), ys], axis=1))
+    return fluid, np.concatenate(walls, axis=0)
+
+
+def hydrostatic(nx: int = 200, ny: int = 400, dx: float = 0.005, layers: int = 3,
+                steps: int = 500, tol: float = 1e-3, K: int = 10, precision: int = 32,
+                gtvf: bool = False) -> Case:
+    """BASELINE configs[1]: 1.0 x 2.0 column at dx=0.005, 3 dummy-wall layers."""
+    rho0, gmag = 1000.0, 9.81
+    h = dx
+    H = ny * dx
+    wall_ny = int(round(1.05 * H / dx))  # side walls up to 1.05 H (2.1 m for H = 2)
+    fluid, wall = _tank2d(nx, ny, nx, wall_ny, layers, dx)
+    x = np.concatenate([fluid, wall])
+    nf, nw = fluid.shape[0], wall.shape[0]
+    tag = np.concatenate([np.zeros(nf, np.int32), np.ones(nw, np.int32)])
+    c_ref = 10.0 * math.sqrt(2 * gmag * H)     # c = 10 |u|max, |u|max ~ sqrt(2 g H)
+    dt = 0.125 * h / math.sqrt(2 * gmag * H)   # PAPER.md:1365-1366 formula
+    # BASELINE configs[1] asks for no background-pressure homogenisation: p_ref = 0
+    # (p0 = min(10|p|, 0) = 0, so the GTVF shift vanishes; reading R22a)
+    params = default_params(rho0=rho0, g=[0.0, -gmag, 0.0], alpha=0.05, c_ref=c_ref,
+                            pgrad=PGRAD_SYMM, h_tilde_factor=0.5, pref_external=1,
+                            p_ref=0.0 if not gtvf else rho0 * c_ref * c_ref, ustar_noslip=0,
+                            clamp_wall_p=1, tol=tol, K=K, precision=precision)
+    lo = [-(layers + 0.5) * dx, -(layers + 0.5) * dx, 0.0]
+    hi = [nx * dx + (layers + 0.5) * dx, 1.1 * H + 4 * dx, 0.0]
+    n = nf + nw
+    return Case("hydrostatic", 2, h, dx, dt, steps, lo, hi, [0, 0, 0], x,
+                np.zeros((n, 2)), np.full(n, rho0 * dx * dx), np.full(n, rho0),
+                np.zeros(n), tag, params)
+
+
+def dambreak2d(nx: int = 500, ny: int = 1000, dx: float = 0.002, tank: float = 4.0,
+               layers: int = 4, steps: int = 1000, tol: float = 1e-2, K: int = 10,
+               precision: int = 32) -> Case:
+    """BASELINE configs[2] / PAPER.md:1352-1371: 1 x 2 block in a 4 x 4 tank."""
+    rho0, gmag = 1000.0, 9.81
+    h = 1.3 * dx                     # h/dx = 1.3
+    hw = ny * dx
+    tank_nx = int(round(tank / dx))
+    fluid, wall = _tank2d(nx, ny, tank_nx, tank_nx, layers, dx)
+    x = np.concatenate([fluid, wall])
+    nf, nw = fluid.shape[0], wall.shape[0]
+    tag = np.concatenate([np.zeros(nf, np.int32), np.ones(nw, np.int32)])
+    p = np.concatenate([rho0 * gmag * (hw - fluid[:, 1]), np.zeros(nw)])  # reading R29
+    c_ref = 10.0 * math.sqrt(2 * gmag * hw)
+    dt = 0.125 * h / math.sqrt(2 * gmag * hw)
+    params = default_params(rho0=rho0, g=[0.0, -gmag, 0.0], alpha=0.05, c_ref=c_ref,
+                            pgrad=PGRAD_SYMM, h_tilde_factor=0.5, pref_external=1,
+                            p_ref=rho0 * c_ref * c_ref, ustar_noslip=0, clamp_wall_p=1,
+                            tol=tol, K=K, precision=precision)
+    lo = [-(layers + 0.5) * dx, -(layers + 0.5) * dx, 0.0]
+    hi = [tank_nx * dx + (layers + 0.5) * dx, tank_nx * dx + 4 * dx, 0.0]
+    n = nf + nw
+    return Case("dambreak2d", 2, h, dx, dt, steps, lo, hi, [0, 0, 0], x,
+                np.zeros((n, 2)), np.full(n, rho0 * dx * dx), np.full(n, rho0), p, tag, params)
+
+
+# --------------------------------------------------------------------------
+# C4  3D Taylor-Green vortex (BASELINE configs[3])
+# --------------------------------------------------------------------------
+def tgv3d(n: int = 128, re: float = 100.0, jitter: float = 0.05, seed: int = 104,
+          steps: int = 100, tol: float = 1e-3, K: int = 10, precision: int = 32) -> Case:
+    L, U, rho0 = 2.0 * np.pi, 1.0, 1.0
+    dx = L / n
+    h = dx
+    nu = 0.01 if re == 100.0 else U * 1.0 / re
+    lo, hi, per = [0.0] * 3, [L] * 3, [1, 1, 1]
+    x = _lattice((n, n, n), dx, lo)
+    x = _jitter(x, jitter * dx, seed, lo, hi, per)
+    X, Y, Z = x[:, 0], x[:, 1], x[:, 2]
+    u = np.stack([np.sin(X) * np.cos(Y) * np.cos(Z),
+                  -np.cos(X) * np.sin(Y) * np.cos(Z),
+                  np.zeros_like(X)], axis=1)
+    p = rho0 / 16.0 * (np.cos(2 * X) + np.cos(2 * Y)) * (np.cos(2 * Z) + 2.0)  # reading R29
+    npart = x.shape[0]
+    dt = min(0.25 * h / U, 0.25 * h * h / nu)
+    # internal flow: p_ref = 2 max(p) (reading R22); max p = 3/16 rho U^2
+    params = default_params(rho0=rho0, nu=nu, pgrad=PGRAD_ASYMM, h_tilde_factor=1.0,
+                            pref_external=0, p_ref=2.0 * 3.0 / 16.0 * rho0 * U * U, tol=tol,
+                            K=K, precision=precision)
+    return Case("tgv3d", 3, h, dx, dt, steps, lo, hi, per, x, u,
+                np.full(npart, rho0 * dx ** 3), np.full(npart, rho0), p,
+                np.zeros(npart, np.int32), params)
+
+
+# --------------------------------------------------------------------------
+# C5  3D dam break, per-GPU slab (BASELINE configs[4])
+# --------------------------------------------------------------------------
+def dambreak3d(nfx: int = 256, nfy: int = 64, nfz: int = 128, dx: float = 1.0 / 256,
+               tank_nx: int = 824, wall_nz: int = 154, layers: int = 3, ranks: int = 1,
+               steps: int = 100, tol: float = 1e-2, K: int = 10, precision: int = 32) -> Case:
+    """Water block nfx*dx x (ranks*nfy*dx) x nfz*dx at the x=0 end of a tank of
+    length tank_nx*dx, open top, y periodic (spanwise; the slab axis).  Walls:
+    floor under the whole tank and both x-end walls up to wall_nz rows."""
+    rho0, gmag = 1000.0, 9.81
+    h = dx                                   # h/dx = 1.0
+    ny = nfy * ranks
+    Ly = ny * dx
+    hw = nfz * dx
+    fluid = _lattice((nfx, ny, nfz), dx, (0.0, 0.0, 0.0))
+    walls = []
+    ys = (np.arange(ny) + 0.5) * dx
+    xs = (np.arange(-layers, tank_nx + layers) + 0.5) * dx
+    for l in range(layers):                  # floor z = -(l + 1/2) dx
+        X, Y = np.meshgrid(xs, ys, indexing="xy")
+        walls.append(np.stack([X.ravel(), Y.ravel(), np.full(X.size, -(l + 0.5) * dx)], 1))
+    zs = (np.arange(wall_nz) + 0.5) * dx
+    for l in range(layers):                  # end walls x = -(l+1/2)dx and L + (l+1/2)dx
+        for xw in (-(l + 0.5) * dx, tank_nx * dx + (l + 0.5) * dx):
+            Y, Z = np.meshgrid(ys, zs, indexing="xy")
+            walls.append(np.stack([np.full(Y.size, xw), Y.ravel(), Z.ravel()], 1))
+    wall = np.concatenate(walls)
+    x = np.concatenate([fluid, wall])
+    nf, nw = fluid.shape[0], wall.shape[0]
+    tag = np.concatenate([np.zeros(nf, np.int32), np.ones(nw, np.int32)])
+    p = np.concatenate([rho0 * gmag * (hw - fluid[:, 2]), np.zeros(nw)])  # reading R29
+    v_ref = math.sqrt(2 * gmag * hw)
+    c_ref = 10.0 * v_ref
+    dt = h / (8.0 * v_ref)
+    params = default_params(rho0=rho0, g=[0.0, 0.0, -gmag], alpha=0.25, c_ref=c_ref,
+                            pgrad=PGRAD_SYMM, h_tilde_factor=0.5, pref_external=1,
+                            p_ref=rho0 * c_ref * c_ref, ustar_noslip=0, clamp_wall_p=1,
+                            tol=tol, K=K, precision=precision)
+    lo = [-(layers + 0.5) * dx, 0.0, -(layers + 0.5) * dx]
+    hi = [tank_nx * dx + (layers + 0.5) * dx, Ly, 2.0 * hw + 4 * dx]
+    n = nf + nw
+    return Case("dambreak3d", 3, h, dx, dt, steps, lo, hi, [0, 1, 0], x,
+                np.zeros((n, 3)), np.full(n, rho0 * dx ** 3), np.full(n, rho0), p, tag, params)
+
+
+def lattice_periodic(dim: int, n: int, dx: float = 1.0, h_ratio: float = 1.0,
+                     jitter: float = 0.0, seed: int = 7, rho0: float = 1.0) -> Case:
+    """A resting periodic lattice (used for lattice identities and invariants)."""
+    L = n * dx
+    lo, hi, per = [0.0] * dim, [L] * dim, [1] * dim
+    x = _lattice((n,) * dim, dx, lo)
+    x = _jitter(x, jitter * dx, seed, lo, hi, per)
+    npart = x.shape[0]
+    params = default_params(rho0=rho0, p_ref=0.0, K=1)
+    return Case(f"lattice{dim}d", dim, h_ratio * dx, dx, 1e-3, 1, _pad3(lo), _pad3(hi),
+                per + [0] * (3 - dim), x, np.zeros((npart, dim)),
+                np.full(npart, rho0 * dx ** dim), np.full(npart, rho0), np.zeros(npart),
+                np.zeros(npart, np.int32), params)
+
+
+def random_box(dim: int, n: int, L: float, h: float, seed: int, periodic) -> Case:
+    """Uniform random particles in [0, L)^dim (neighbour-search fuzzing)."""
+    rng = np.random.default_rng(seed)
+    x = rng.uniform(0.0, L, (n, dim))
+    lo, hi = [0.0] * dim, [L] * dim
+    per = list(periodic)[:dim]
+    params = default_params()
+    return Case("random", dim, h, L / max(n, 1) ** (1.0 / dim), 1e-3, 1, _pad3(lo), _pad3(hi),
+                per + [0] * (3 - dim), x, np.zeros((n, dim)), np.ones(n), np.ones(n),
+                np.zeros(n), np.zeros(n, np.int32), params)
+
+
+CASES = {
+    "tgv2d": tgv2d,
+    "hydrostatic": hydrostatic,
+    "dambreak2d": dambreak2d,
+    "tgv3d": tgv3d,
+    "dambreak3d": dambreak3d,
+}
