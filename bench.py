@@ -1,0 +1,312 @@
+#!/usr/bin/env python
+"""SISPH hot-path benchmark (BASELINE.json metric: PPE Jacobi sweeps x particles / s
+and ms / timestep; % HBM roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl sisph|reference]
+
+A step is one full SISPH step (Algorithm 1: two neighbour
+builds, density, wall BCs, forces + predictors, RHS/D_ii, the iterated PPE,
+pressure-gradient correction, K GTVF sub-steps, advance) on the per-GPU slab of
+BASELINE configs[4] (3D dam break, fp32).  Inputs are synthetic (synth/).
+
+value = (sum over the K timed steps of PPE sweeps x fluid particles) x n_gpus
+        / (device time of the K whole steps)       [particle-sweeps / s]
+ms_per_step = device time of one whole step.
+The oracle (oracle/, fp64 C) is timed on the host as cpu_baseline, and is the
+--impl reference arm.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PPE Jacobi particle-sweeps/s (sweeps x fluid particles per second of whole SISPH-step time)"
+UNIT = "particle-sweeps/s"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="sisph", choices=["sisph", "reference"])
+    ap.add_argument("--workload", default="dambreak3d", choices=["dambreak3d", "tgv3d", "dambreak2d", "hydrostatic"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    return ap.parse_args()
+
+
+def workload(name, ranks=1):
+    import synth
+    if name == "dambreak3d":
+        c = synth.dambreak3d(ranks=ranks)
+        desc = ("3D dam break per-GPU slab (BASELINE configs[4]): fluid 256x64x128 at dx=1/256, "
+                "3 wall layers, y periodic, fp32, tol 1e-2, K=10")
+    elif name == "tgv3d":
+        c = synth.tgv3d()
+        desc = "3D Taylor-Green 128^3 periodic (BASELINE configs[3]), fp32, tol 1e-3"
+    elif name == "dambreak2d":
+        c = synth.dambreak2d()
+        desc = "2D dam break 500x1000 fluid in a 4x4 tank (BASELINE configs[2]), fp32, tol 1e-2"
+    else:
+        c = synth.hydrostatic()
+        desc = "2D hydrostatic column 200x400 (BASELINE configs[1]), fp32, tol 1e-3"
+    return c, desc
+
+
+def sample_case(name, frac=8):
+    """Bounded CPU sample of the same workload (1/frac spanwise slab)."""
+    import synth
+    if name == "dambreak3d":
+        return synth.dambreak3d(nfy=64 // frac), f"1/{frac} spanwise slab of the per-GPU workload (nfy={64 // frac})"
+    if name == "tgv3d":
+        return synth.tgv3d(n=64), "64^3 instance of the same TGV-3D recipe"
+    if name == "dambreak2d":
+        return synth.dambreak2d(nx=250, ny=500, dx=0.004), "dx=0.004 instance of the same dam break"
+    return synth.hydrostatic(), "the full workload"
+
+
+class ClockSampler:
+    """SM clock + throttle reasons via NVML every 20 ms while the timed region runs."""
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": len(self.samples)}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def sweep_traffic():
+    """dram bytes per sweep launch from the committed ncu --set full capture, if any."""
+    p = os.path.join(ROOT, "profiles", "sweep_traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    return None
+
+
+def cpu_baseline(name, max_seconds=15.0):
+    """The oracle as it stands, on a bounded sample, on all host cores (fp64)."""
+    import oracle
+    import synth  # noqa: F401
+    oracle.build()
+    case, desc = sample_case(name)
+    o = oracle.Sim(case)
+    o.predict(case.dt)
+    t0 = time.perf_counter()
+    o.solve(0.0, 1)
+    t1 = time.perf_counter() - t0
+    S = int(max(1, min(20, max_seconds / max(t1, 1e-6))))
+    o.predict(case.dt)
+    t0 = time.perf_counter()
+    it, _, _ = o.solve(0.0, S)
+    t = time.perf_counter() - t0
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count()))
+    return {"value": it * case.n_fluid / t, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{desc}: {it} Jacobi sweeps (PPE phase only) over {case.n_fluid} fluid particles, "
+                      f"{t:.1f} s, fp64"}
+
+
+def emit(d):
+    print(json.dumps(d), flush=True)
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    case, sdesc = sample_case(args.workload)
+    _, desc = workload(args.workload)
+    o = oracle.Sim(case)
+    for _ in range(args.warmup):
+        o.step(case.dt)
+    t0 = time.perf_counter()
+    sweeps = 0
+    for _ in range(args.steps):
+        it, _, _ = o.step(case.dt)
+        sweeps += it
+    t = time.perf_counter() - t0
+    v = sweeps * case.n_fluid / t
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count()))
+    emit({"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+          "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+          "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+          "data": "synthetic", "config": {"workload": desc, "reference_sample": sdesc,
+                                          "n_fluid_sample": case.n_fluid},
+          "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                           "sample": f"{sdesc}: {args.steps} full SISPH steps, fp64"},
+          "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
+
+
+def run_sisph(args):
+    import numpy as np
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        raise SystemExit("multi-GPU slab decomposition is not available in this build (N=1 only)")
+    torch.cuda.set_device(local)
+    from paper_1908_01762_b200 import Simulation
+
+    case, desc = workload(args.workload)
+    stream = torch.cuda.current_stream()
+    sim = Simulation.from_case(case, stream=stream.cuda_stream, device=local)
+    sim.set_timing(True)
+    nf, n = sim.n_fluid, sim.n
+    for _ in range(args.warmup):
+        sim.step(case.dt)
+    torch.cuda.synchronize()
+    reps = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            reps.append(sim.step(case.dt))
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    sweeps = sum(r.iters for r in reps)
+    value = sweeps * nf * world / (ms / 1e3)
+    ms_solve = sum(r.ms_solve for r in reps)
+    # roofline of the dominant hot-path kernel: the Jacobi sweep (A12)
+    ms_sw = sum(r.ms_sweeps for r in reps)
+    n_sw = sum(r.sweeps_timed for r in reps)
+    pairs = reps[-1].pairs
+    b_per = 24 * n + 17 * nf + 4 * pairs    # every state array once + the neighbour list
+    avg_s = ms_sw / max(n_sw, 1) / 1e3
+    achieved = b_per / avg_s / 1e9
+    peak, peak_src = peaks()
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32" if case.params["precision"] == 32 else "f64",
+        "data": "synthetic",
+        "config": {"workload": desc, "n_fluid": nf, "n_wall": n - nf, "dt": case.dt,
+                   "l2": "inputs larger than L2 (neighbour list %.2f GB, state %.0f MB per GPU)"
+                         % (4 * pairs / 1e9, 24 * n / 1e6),
+                   "parallelism": f"slab x{world}"},
+        "ppe_phase_particle_sweeps_per_s": sweeps * nf * world / (ms_solve / 1e3),
+        "sweeps_per_step": sweeps / args.steps,
+        "ms_per_step_phases": {"predict": sum(r.ms_predict for r in reps) / args.steps,
+                               "solve": ms_solve / args.steps,
+                               "correct": sum(r.ms_correct for r in reps) / args.steps},
+        "roofline": {"kernel": "k_sweep (A12 Jacobi sweep + fused residual reduction)", "bound": "hbm",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": sweep_traffic(), "bytes_per_launch": b_per, "pairs_per_launch": pairs,
+                     "avg_launch_us": avg_s * 1e6, "launches_timed": n_sw, "peak_source": peak_src},
+        "gpu_launches": int(sum(r.launches for r in reps)),
+        "clocks": clk.summary(),
+    }
+    # end to end through the public API with host buffers
+    if not args.no_e2e:
+        dim = case.dim
+        pin = lambda shape: torch.empty(shape, dtype=torch.float64, pin_memory=True)
+        hx, hu, hut, hp = pin((n, dim)), pin((n, dim)), pin((n, dim)), pin((n,))
+        sim.get_ptr("POSITION", hx.data_ptr(), n * dim)
+        sim.get_ptr("VELOCITY", hu.data_ptr(), n * dim)
+        sim.get_ptr("TRANSPORT_VELOCITY", hut.data_ptr(), n * dim)
+        sim.get_ptr("PRESSURE", hp.data_ptr(), n)
+        out_p = pin((n,))
+        torch.cuda.synchronize()
+        K2 = args.e2e_steps
+        sw2 = 0
+        t0 = time.perf_counter()
+        for _ in range(K2):
+            sim.set_ptr("POSITION", hx.data_ptr(), n * dim)
+            sim.set_ptr("VELOCITY", hu.data_ptr(), n * dim)
+            sim.set_ptr("TRANSPORT_VELOCITY", hut.data_ptr(), n * dim)
+            sim.set_ptr("PRESSURE", hp.data_ptr(), n)
+            sw2 += sim.step(case.dt).iters
+            sim.get_ptr("PRESSURE", out_p.data_ptr(), n)
+        torch.cuda.synchronize()
+        t = time.perf_counter() - t0
+        out["e2e"] = {"value": sw2 * nf * world / t, "unit": UNIT, "h2d_bytes_per_step": 8 * n * (3 * dim + 1),
+                      "d2h_bytes_per_step": 8 * n, "steps": K2, "ms_per_step": 1e3 * t / K2}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args.workload)
+    del np
+    emit(out)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_sisph(args)
+
+
+if __name__ == "__main__":
+    main()

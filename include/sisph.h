@@ -1,0 +1,197 @@
+/*
+ * sisph.h — C ABI of the B200-native SISPH hot path (libsisph.so).
+ *
+ * SISPH is the iterative, matrix-free incompressible SPH scheme of Muta,
+ * Ramachandran & Negi (arXiv 1908.01762).  Citations "P:a-b" are lines of the
+ * paper's LaTeX source; "Rn" are the readings listed in DESIGN.md.
+ *
+ * Conventions (all entry points):
+ *   - Every pointer argument is a HOST pointer owned by the caller; the library
+ *     copies in or out and never keeps it.  The handle owns all device memory,
+ *     its CUDA stream (unless one is supplied in sisph_params.stream), and its
+ *     NCCL communicator (distributed handles).
+ *   - Vectors are row-major n x dim (dim = domain->dim) doubles.
+ *   - Values passed in or returned are in CREATION-ID order: particle k is the
+ *     k-th particle given to sisph_create.  Internally particles are kept in
+ *     cell-sorted order (fluid and wall sets separately).
+ *   - Calls are stream-ordered on the handle's stream; calls that return host
+ *     values (solve, step, getters) synchronise the stream.
+ *   - One handle per GPU; a handle is not thread-safe.
+ *   - Return value: SISPH_OK (0) or one of the error codes below; the message
+ *     of the last error is returned by sisph_last_error().  After
+ *     SISPH_ENONFINITE or SISPH_ECUDA the state of the handle is undefined.
+ */
+#ifndef SISPH_H
+#define SISPH_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SISPH_OK 0
+#define SISPH_EINVAL 1      /* invalid argument (see each call) */
+#define SISPH_ENOMEM 2      /* device or host allocation failed */
+#define SISPH_ECUDA 3       /* a CUDA runtime call or kernel failed */
+#define SISPH_ENCCL 4       /* an NCCL call failed (distributed handles) */
+#define SISPH_ENONFINITE 5  /* a non-finite pressure appeared in the PPE sweep */
+#define SISPH_EOVERFLOW 6   /* a particle has more neighbours than the list capacity */
+
+#define SISPH_TAG_FLUID 0
+#define SISPH_TAG_WALL 1
+
+typedef struct sisph sisph_t;
+
+/* Simulation box.  Axes a < dim are used.  A periodic axis wraps positions
+ * into [lo, hi) and uses the minimum image (R26); a bounded axis clamps cell
+ * coordinates into the grid (R27). */
+typedef struct {
+    int dim;            /* 2 or 3 */
+    double lo[3];
+    double hi[3];
+    int periodic[3];    /* 0 or 1 per axis */
+} sisph_domain;
+
+/* Scheme parameters.  sisph_params_default() fills the paper's defaults. */
+typedef struct {
+    int precision;          /* 32: fp32 state and arithmetic; 64: fp64 (default 64) */
+    double rho0;            /* rest density rho0 */
+    double nu;              /* kinematic viscosity (eq:mom:sph:visc) */
+    double g[3];            /* body force per unit mass */
+    double alpha;           /* artificial viscosity coefficient (eq:mom:sph:av, R20) */
+    double c_ref;           /* reference sound speed c */
+    double omega;           /* SOR factor, default 0.5 (eq:p-sor) */
+    double eta;             /* regulariser eta h^2 with eta = 0.01 (R6) */
+    double fs_ratio;        /* free surface if rho/rho0 < fs_ratio, default 0.8 */
+    double h_tilde_factor;  /* GTVF kernel length h~ = factor h */
+    double p_ref;           /* GTVF reference background pressure */
+    int pgrad;              /* 0 symm (eq:mom:sph:press:symm), 1 asymm (eq:...:pij) */
+    int pref_external;      /* 1: p0 = min(10|p|, p_ref); 0: p0 = p_ref */
+    int ustar_noslip;       /* 1 no-slip, 0 slip wall u* (R16) */
+    int clamp_wall_p;       /* 1: negative wall pressure -> 0 */
+    int K;                  /* GTVF sub-steps (R22), default 10 */
+    int min_iter;           /* minimum PPE sweeps, default 2 */
+    int max_iter;           /* maximum PPE sweeps, default 1000 */
+    double tol;             /* epsilon of eq:convergence used by sisph_step, default 1e-2 */
+    int wall_rho_summation; /* 1: walls get summation density; 0: walls keep rho0 (R4) */
+    int nbr_cap;            /* neighbour-list capacity per particle, 0 = automatic */
+    int device;             /* CUDA device ordinal, -1 = current device */
+    void* stream;           /* cudaStream_t to run on, NULL = the handle creates one */
+} sisph_params;
+
+/* Per-step report (sisph_step).  Timings are device milliseconds measured
+ * with CUDA events on the handle's stream when timing is enabled. */
+typedef struct {
+    double dt;
+    int iters;              /* PPE sweeps executed */
+    double residual;        /* final value of eq:convergence's left side */
+    double lambda;          /* Lambda = max |RHS_i / D_ii| (eq:convergence, R12) */
+    double ms_predict, ms_solve, ms_correct;
+    int64_t pairs;          /* directed neighbour pairs with a fluid destination, r* build */
+    int max_neighbors;      /* largest neighbour count of the r* build */
+    double ms_sweeps;       /* device ms of the Jacobi sweep kernels that did work (timing mode) */
+    int sweeps_timed;       /* number of sweep launches ms_sweeps covers */
+    int64_t launches;       /* kernel launches this step issued (speculative no-op sweeps included) */
+} sisph_step_report;
+
+typedef enum {
+    SISPH_FIELD_POSITION = 0,           /* n x dim; r^n (after a step: r^{n+1}) */
+    SISPH_FIELD_VELOCITY = 1,           /* n x dim; fluid u, wall ghost velocity u_w */
+    SISPH_FIELD_TRANSPORT_VELOCITY = 2, /* n x dim; fluid u~ (walls: 0) */
+    SISPH_FIELD_PRESSURE = 3,           /* n; fluid p, wall p_w */
+    SISPH_FIELD_DENSITY = 4,            /* n; rho of the last density pass */
+    SISPH_FIELD_MASS = 5,               /* n */
+    SISPH_FIELD_USTAR = 6,              /* n x dim; u* (walls: wall u*) */
+    SISPH_FIELD_RSTAR = 7,              /* n x dim; r* of the last predict (walls: r) */
+    SISPH_FIELD_RHS = 8,                /* n; RHS_i of eq:sph-ppe (walls: 0) */
+    SISPH_FIELD_DIAG = 9,               /* n; D_ii of eq:coeff (walls: 0) */
+    SISPH_FIELD_NORMAL = 10,            /* n x dim; wall unit normals (fluid: 0) */
+    SISPH_FIELD_FREE_SURFACE = 11,      /* n; 1 if free-surface fluid particle */
+    SISPH_FIELD_TAG = 12                /* n; 0 fluid, 1 wall (read only) */
+} sisph_field;
+
+/* Fill *p with the paper's defaults (precision 64, omega 0.5, eta 0.01,
+ * fs_ratio 0.8, K 10, min_iter 2, max_iter 1000, tol 1e-2, h~ = h, slip u*,
+ * walls keep rho0; everything else 0). */
+void sisph_params_default(sisph_params* p);
+
+/* Create a simulation on one GPU.
+ *   positions, velocities: n x dim; masses, densities: n; tags: n (0 fluid,
+ *   1 wall); h: uniform smoothing length, support 3h.
+ * Copies the inputs to the device, computes the cell grid (R26/R27), sorts
+ * walls once, builds the neighbour lists, computes the wall normals
+ * (§3.4.1) and sets u~ = u (R23), p = 0.
+ * Errors: SISPH_EINVAL if n <= 0, h <= 0, dim not 2 or 3, a non-finite input,
+ * a tag not 0/1, no fluid particle, a particle outside a bounded axis' box by
+ * more than the box size, a periodic axis with fewer than 3 cells (L < 9h),
+ * rho <= 0 or m <= 0, precision not 32/64; SISPH_ENOMEM; SISPH_ECUDA. */
+int sisph_create(const double* positions, const double* velocities, const double* masses,
+                 const double* densities, const int32_t* tags, int64_t n, double h,
+                 const sisph_domain* domain, const sisph_params* params, sisph_t** out);
+
+/* Release the handle and all its device memory.  NULL is ignored. */
+void sisph_destroy(sisph_t* s);
+
+/* Neighbour build at the current positions (A1-A5): cell hash, counting
+ * (radix = cell key) sort with a stable per-cell fix-up, reorder of the fluid
+ * state, cell start table, neighbour lists N(i) = { j != i : r_ij^2 < (3h)^2 }
+ * (R2, decided in fp64).  Errors: SISPH_ECUDA, SISPH_EOVERFLOW. */
+int sisph_build_neighbors(sisph_t* s);
+
+/* Algorithm 1 lines 2-6 plus the PPE set-up: build at r^n,
+ * summation density + free-surface flags (A6), wall ghost velocity (A7),
+ * forces and predictors u*, r* (A8), build at r* (A9), wall u* (A10),
+ * RHS_i, D_ii and Lambda (A11).  Errors: SISPH_EINVAL if dt <= 0. */
+int sisph_predict(sisph_t* s, double dt);
+
+/* The PPE solve (Algorithm 1 lines 7-10; eq:p-sor, eq:convergence): damped
+ * Jacobi from p^0 = current p, walls refreshed from p^k every sweep (R14),
+ * until (k >= min(min_iter, max_iter) and residual < tol) or k == max_iter.
+ * Needs a preceding sisph_predict.  Non-convergence is NOT an error: it
+ * returns SISPH_OK with *iters_out == max_iter and *residual_out >= tol.
+ * iters_out / residual_out may be NULL.  Errors: SISPH_EINVAL if tol < 0 or
+ * max_iter < 1 or no predict was done; SISPH_ENONFINITE. */
+int sisph_ppe_solve(sisph_t* s, double tol, int max_iter, int* iters_out, double* residual_out);
+
+/* Algorithm 1 lines 11-19: final wall pressure, pressure gradient and
+ * corrector u^{n+1} (eq:int:vnp1), K GTVF sub-steps with the pair set frozen
+ * at r* (eq:int:gtvf:pos/vel:tmp), transport velocity (eq:int:vhatnp2) and
+ * positions (eq:int:rnp2).  Errors: SISPH_EINVAL if dt <= 0 or no solve. */
+int sisph_correct(sisph_t* s, double dt);
+
+/* One full SISPH step = predict + ppe_solve(params.tol, params.max_iter) +
+ * correct.  rep may be NULL. */
+int sisph_step(sisph_t* s, double dt, sisph_step_report* rep);
+
+/* Copy a field out / in, creation-id order.  count must equal n (scalars) or
+ * n * dim (vectors), else SISPH_EINVAL.  TAG is read only. */
+int sisph_get_field(sisph_t* s, sisph_field f, double* out, int64_t count);
+int sisph_set_field(sisph_t* s, sisph_field f, const double* in, int64_t count);
+
+/* Creation ids in internal order: ids[0 .. n_fluid) are the fluid particles
+ * in cell-sorted order, ids[n_fluid .. n) the walls.  n must equal the
+ * particle count. */
+int sisph_get_order(sisph_t* s, int64_t* ids, int64_t n);
+
+/* The current neighbour sets as CSR in creation-id order, each row sorted by
+ * id: offsets[n + 1], ids[*total].  If cap < total only offsets and *total
+ * are written and SISPH_EINVAL is returned. */
+int sisph_get_neighbors(sisph_t* s, int64_t* offsets, int64_t* ids, int64_t cap, int64_t* total);
+
+/* Counts: particles, fluid particles, wall particles. */
+int sisph_get_counts(const sisph_t* s, int64_t* n, int64_t* n_fluid, int64_t* n_wall);
+
+/* Enable (1) / disable (0) per-phase CUDA-event timing in sisph_step. */
+int sisph_set_timing(sisph_t* s, int enable);
+
+/* Wait for all work queued on the handle's stream. */
+int sisph_sync(sisph_t* s);
+
+/* Message of the last error of s (or of the calling thread if s is NULL). */
+const char* sisph_last_error(const sisph_t* s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SISPH_H */

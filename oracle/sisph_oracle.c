@@ -377,7 +377,8 @@ static void clip_normal(int dim, double* uw, const double* n)
 
 /* Wall normals, §3.4.1 eq:normal-approx / eq:normal, reading R17:
  * sources are wall particles; |n*| < 1/(4h) -> 0 else normalised; then the
- * SPH-smoothed sum (self included) is normalised (zero stays zero). */
+ * SPH-smoothed sum (self included) is normalised, and a smoothed vector
+ * shorter than 0.01 is set to zero. */
 static void compute_normals(or_sim* s)
 {
     const or_cfg* c = &s->c;
@@ -417,8 +418,11 @@ static void compute_normals(or_sim* s)
             double wv = or_W(dim, r, h) * s->m[j] / s->rho[j];
             for (int a = 0; a < dim; a++) acc[a] += wv * ns[3 * j + a];
         }
+        /* R17: a smoothed normal this short (e.g. the middle of three wall
+         * layers, where the layers above and below cancel) has no direction;
+         * it stays zero instead of normalising rounding noise */
         double mag = sqrt(dot(dim, acc, acc));
-        for (int a = 0; a < 3; a++) s->nrm[3 * i + a] = mag > 0.0 ? acc[a] / mag : 0.0;
+        for (int a = 0; a < 3; a++) s->nrm[3 * i + a] = mag >= 0.01 ? acc[a] / mag : 0.0;
     }
     free(ns);
 }

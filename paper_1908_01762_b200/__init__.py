@@ -1,0 +1,9 @@
+"""B200-native SISPH hot path (arXiv 1908.01762): sm_100a CUDA kernels behind a
+C ABI (include/sisph.h), with a thin ctypes binding.
+
+    from paper_1908_01762_b200 import Simulation
+"""
+from .sisph import (EXPORTED, FIELDS, Simulation, SisphError, domain, lib,  # noqa: F401
+                    params_from_dict, sisph_domain, sisph_params, sisph_step_report)
+
+__all__ = ["Simulation", "SisphError", "domain", "params_from_dict", "lib", "FIELDS", "EXPORTED"]

@@ -1,0 +1,208 @@
+// sisph_device.cuh — device-side types and per-pair arithmetic of the SISPH
+// hot path (sm_100a).  Citations "P:a-b" are PAPER.md lines; "Rn" DESIGN.md
+// readings.  Nothing here is shared with the oracle (oracle/).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sb {
+
+// ---------------------------------------------------------------------------
+// Vector types.  Particle positions are packed (x, y, z, m) so one 16-byte
+// (fp32) or 32-byte (fp64) load brings everything a neighbour gather needs
+// besides rho_j and p_j.
+// ---------------------------------------------------------------------------
+struct __align__(32) dbl4 {
+    double x, y, z, w;
+};
+
+template <class T> struct V4T;
+template <> struct V4T<float> { using type = float4; };
+template <> struct V4T<double> { using type = dbl4; };
+template <class T> using V4 = typename V4T<T>::type;
+
+__device__ __forceinline__ float4 ld4(const float4* p) { return __ldg(p); }
+__device__ __forceinline__ dbl4 ld4(const dbl4* p)
+{
+    const double2* q = reinterpret_cast<const double2*>(p);
+    double2 a = __ldg(q), b = __ldg(q + 1);
+    return dbl4{a.x, a.y, b.x, b.y};
+}
+template <class T> __device__ __forceinline__ V4<T> mk4(T x, T y, T z, T w);
+template <> __device__ __forceinline__ float4 mk4<float>(float x, float y, float z, float w)
+{
+    return make_float4(x, y, z, w);
+}
+template <> __device__ __forceinline__ dbl4 mk4<double>(double x, double y, double z, double w)
+{
+    return dbl4{x, y, z, w};
+}
+
+// ---------------------------------------------------------------------------
+// Kernel-argument block: geometry + scheme constants, passed by value.
+// ---------------------------------------------------------------------------
+template <class T> struct Params {
+    // sizes
+    int Nf, Nw, Ntot, cap;
+    // cell grid (R26/R27): decisions in fp64
+    int dim;
+    int nc[3];
+    int per[3];
+    double lo[3], hi[3], cell[3], Ld[3], halfLd[3];
+    double R2d;            // (3h)^2 in fp64 (R2)
+    float R2lo, R2hi;      // fp32 prefilter band around R^2
+    float Lf[3], halfLf[3];
+    // working-precision constants
+    T L[3], halfL[3];
+    T h, sig, dwk;         // W = sig * poly5(q), dW/dr = dwk * poly4(q), q = r / h
+    T inv_h;
+    T h2, sig2, dwk2, inv_h2;   // kernel at h/2 (Shepard of eq:vf)
+    T ht, dwkt, inv_ht;         // kernel at h~ (GTVF, eq:mom:sph:gtvf)
+    T w0;                  // W(0)
+    T eta_h2;              // eta h^2 (R6)
+    T rho0, nu, alpha, c_ref, omega, fs_ratio, p_ref;
+    T g[3];
+    int pgrad, pref_external, ustar_noslip, clamp_wall_p, wall_rho_summation;
+};
+
+// ---------------------------------------------------------------------------
+// M6 quintic spline (reading R1), branch-free: each truncated power is
+// max(k - q, 0)^n, identical to the piecewise definition.
+// ---------------------------------------------------------------------------
+template <class T> __device__ __forceinline__ T quintic4(T q)
+{
+    T a = fmax(T(3) - q, T(0)), b = fmax(T(2) - q, T(0)), c = fmax(T(1) - q, T(0));
+    T a2 = a * a, b2 = b * b, c2 = c * c;
+    return a2 * a2 - T(6) * (b2 * b2) + T(15) * (c2 * c2);
+}
+template <class T> __device__ __forceinline__ T quintic5(T q)
+{
+    T a = fmax(T(3) - q, T(0)), b = fmax(T(2) - q, T(0)), c = fmax(T(1) - q, T(0));
+    T a2 = a * a, b2 = b * b, c2 = c * c;
+    return a2 * a2 * a - T(6) * (b2 * b2 * b) + T(15) * (c2 * c2 * c);
+}
+
+__device__ __forceinline__ float my_sqrt(float x) { return sqrtf(x); }
+__device__ __forceinline__ double my_sqrt(double x) { return sqrt(x); }
+
+// minimum-image difference on a periodic axis (R26)
+template <class T> __device__ __forceinline__ T wrapd(T d, T L, T halfL)
+{
+    if (d > halfL) d -= L;
+    else if (d < -halfL) d += L;
+    return d;
+}
+
+// r_ij = r_i - r_j in working precision (minimum image), returns r^2
+template <class T, int D>
+__device__ __forceinline__ T pair_vec(const Params<T>& P, const V4<T>& a, const V4<T>& b, T d[3])
+{
+    d[0] = a.x - b.x;
+    d[1] = a.y - b.y;
+    d[2] = D == 3 ? a.z - b.z : T(0);
+    if (P.per[0]) d[0] = wrapd(d[0], P.L[0], P.halfL[0]);
+    if (P.per[1]) d[1] = wrapd(d[1], P.L[1], P.halfL[1]);
+    if (D == 3 && P.per[2]) d[2] = wrapd(d[2], P.L[2], P.halfL[2]);
+    T r2 = d[0] * d[0] + d[1] * d[1];
+    if (D == 3) r2 += d[2] * d[2];
+    return r2;
+}
+
+// ---------------------------------------------------------------------------
+// Exact neighbour decision (R2): r^2 < R^2 evaluated in fp64 exactly as the
+// definition is written (difference, minimum image, products and sums in
+// order, no contraction).  Working in fp32, a cheap prefilter with a
+// relative band of 2^-12 decides all pairs whose fp32 r^2 is clearly inside
+// or outside; only the band goes to fp64 (it is also the whole decision in
+// fp64 mode).
+// ---------------------------------------------------------------------------
+template <int D>
+__device__ __forceinline__ bool exact_inside(const Params<float>& P, double xi, double yi, double zi,
+                                             double xj, double yj, double zj)
+{
+    double d0 = __dadd_rn(xi, -xj), d1 = __dadd_rn(yi, -yj), d2 = D == 3 ? __dadd_rn(zi, -zj) : 0.0;
+    if (P.per[0]) d0 = d0 > P.halfLd[0] ? __dadd_rn(d0, -P.Ld[0]) : (d0 < -P.halfLd[0] ? __dadd_rn(d0, P.Ld[0]) : d0);
+    if (P.per[1]) d1 = d1 > P.halfLd[1] ? __dadd_rn(d1, -P.Ld[1]) : (d1 < -P.halfLd[1] ? __dadd_rn(d1, P.Ld[1]) : d1);
+    if (D == 3 && P.per[2])
+        d2 = d2 > P.halfLd[2] ? __dadd_rn(d2, -P.Ld[2]) : (d2 < -P.halfLd[2] ? __dadd_rn(d2, P.Ld[2]) : d2);
+    double r2 = __dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1));
+    if (D == 3) r2 = __dadd_rn(r2, __dmul_rn(d2, d2));
+    return r2 < P.R2d;
+}
+
+template <int D>
+__device__ __forceinline__ bool exact_inside(const Params<double>& P, double xi, double yi, double zi,
+                                             double xj, double yj, double zj)
+{
+    double d0 = __dadd_rn(xi, -xj), d1 = __dadd_rn(yi, -yj), d2 = D == 3 ? __dadd_rn(zi, -zj) : 0.0;
+    if (P.per[0]) d0 = d0 > P.halfLd[0] ? __dadd_rn(d0, -P.Ld[0]) : (d0 < -P.halfLd[0] ? __dadd_rn(d0, P.Ld[0]) : d0);
+    if (P.per[1]) d1 = d1 > P.halfLd[1] ? __dadd_rn(d1, -P.Ld[1]) : (d1 < -P.halfLd[1] ? __dadd_rn(d1, P.Ld[1]) : d1);
+    if (D == 3 && P.per[2])
+        d2 = d2 > P.halfLd[2] ? __dadd_rn(d2, -P.Ld[2]) : (d2 < -P.halfLd[2] ? __dadd_rn(d2, P.Ld[2]) : d2);
+    double r2 = __dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1));
+    if (D == 3) r2 = __dadd_rn(r2, __dmul_rn(d2, d2));
+    return r2 < P.R2d;
+}
+
+// is j a neighbour of i?  fp32: prefilter + fp64 band; fp64: exact.
+template <int D>
+__device__ __forceinline__ bool is_neighbor(const Params<float>& P, const float4& a, const float4& b)
+{
+    float d0 = a.x - b.x, d1 = a.y - b.y, d2 = D == 3 ? a.z - b.z : 0.f;
+    if (P.per[0]) d0 = wrapd(d0, P.Lf[0], P.halfLf[0]);
+    if (P.per[1]) d1 = wrapd(d1, P.Lf[1], P.halfLf[1]);
+    if (D == 3 && P.per[2]) d2 = wrapd(d2, P.Lf[2], P.halfLf[2]);
+    float r2 = d0 * d0 + d1 * d1;
+    if (D == 3) r2 += d2 * d2;
+    if (r2 < P.R2lo) return true;
+    if (r2 > P.R2hi) return false;
+    return exact_inside<D>(P, (double)a.x, (double)a.y, (double)a.z, (double)b.x, (double)b.y, (double)b.z);
+}
+template <int D>
+__device__ __forceinline__ bool is_neighbor(const Params<double>& P, const dbl4& a, const dbl4& b)
+{
+    return exact_inside<D>(P, a.x, a.y, a.z, b.x, b.y, b.z);
+}
+
+// cell coordinates of a position, fp64 with IEEE division (R27): identical
+// to floor((x - lo) / cell) then clamp
+template <class T>
+__device__ __forceinline__ int cell_coord(const Params<T>& P, int a, double x)
+{
+    double f = floor(__ddiv_rn(__dadd_rn(x, -P.lo[a]), P.cell[a]));
+    if (f < 0.0) return 0;
+    if (f > (double)(P.nc[a] - 1)) return P.nc[a] - 1;
+    return (int)f;
+}
+
+template <class T, int D>
+__device__ __forceinline__ void cell_of(const Params<T>& P, const V4<T>& x, int c[3])
+{
+    c[0] = cell_coord(P, 0, (double)x.x);
+    c[1] = cell_coord(P, 1, (double)x.y);
+    c[2] = D == 3 ? cell_coord(P, 2, (double)x.z) : 0;
+}
+
+template <class T>
+__device__ __forceinline__ int cell_key(const Params<T>& P, const int c[3])
+{
+    return c[0] + P.nc[0] * (c[1] + P.nc[1] * c[2]);
+}
+
+// ---------------------------------------------------------------------------
+// warp / block reductions
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double warp_sum(double v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ double warp_max(double v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+}  // namespace sb

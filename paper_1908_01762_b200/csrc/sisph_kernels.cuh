@@ -1,0 +1,863 @@
+// sisph_kernels.cuh — the hand-written sm_100a kernels of the SISPH per-step
+// hot path.  One thread per destination particle for the neighbour passes
+// (particles are cell-sorted, so a warp's neighbour rows overlap and the
+// gathers hit L1/L2); warp-shuffle + block reductions with a last-block
+// finish for the device-wide sums.  Citations: PAPER.md lines (P:a-b) and
+// DESIGN.md readings (Rn).
+#pragma once
+#include "sisph_device.cuh"
+
+namespace sb {
+
+// device-side control block of one handle
+struct Ctl {
+    unsigned int ticket;       // last-block election of the sweep reduction
+    int iter;                  // sweeps completed in the current solve
+    int done;                  // 1 once eq:convergence holds or max_iter is reached
+    int nonfinite;             // a non-finite p^{k+1} was produced
+    double residual;           // last value of eq:convergence's left side
+    unsigned long long lambda_bits;  // Lambda as ordered bits of a non-negative double
+    int max_count;             // largest neighbour count of the last build
+    int overflow;              // a row exceeded the list capacity
+    unsigned long long pairs_fluid;  // sum of neighbour counts over fluid rows of the last build
+};
+
+// ===========================================================================
+// A1: cell hash + per-cell counts.  rank = arrival order inside the cell
+// (made deterministic later by the stable fix-up, A2).  Warp-aggregated:
+// lanes with equal keys elect one atomic.
+// ===========================================================================
+template <class T, int D>
+__global__ void k_hash_count(Params<T> P, const V4<T>* __restrict__ pos, int n,
+                             int* __restrict__ keys, int* __restrict__ rank, int* __restrict__ ccount)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    bool act = i < n;
+    int key = -1;
+    if (act) {
+        V4<T> x = ld4(pos + i);
+        int c[3];
+        cell_of<T, D>(P, x, c);
+        key = cell_key(P, c);
+        keys[i] = key;
+    }
+    unsigned mask = __ballot_sync(0xffffffffu, act);
+    if (!act) return;
+    unsigned peers = __match_any_sync(mask, key);
+    int lane = threadIdx.x & 31;
+    int leader = __ffs(peers) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(ccount + key, __popc(peers));
+    base = __shfl_sync(peers, base, leader);
+    rank[i] = base + __popc(peers & ((1u << lane) - 1u));
+}
+
+// ===========================================================================
+// exclusive scan of ints (3-phase: per-block scan, scan of block sums,
+// add-back).  1024 items per block of 256 threads.
+// ===========================================================================
+constexpr int SCAN_T = 256, SCAN_IPT = 4, SCAN_B = SCAN_T * SCAN_IPT;
+
+__device__ __forceinline__ int block_excl_scan(int v, int* sm, int& total)
+{
+    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) sm[w] = x;
+    __syncthreads();
+    if (w == 0) {
+        int s = lane < (blockDim.x >> 5) ? sm[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s += y;
+        }
+        if (lane < (blockDim.x >> 5)) sm[lane] = s;
+    }
+    __syncthreads();
+    total = sm[(blockDim.x >> 5) - 1];
+    int pre = (w > 0 ? sm[w - 1] : 0) + x - v;
+    __syncthreads();
+    return pre;
+}
+
+__global__ void k_scan_local(const int* __restrict__ in, int* __restrict__ out, int n, int* __restrict__ bsum)
+{
+    __shared__ int sm[32];
+    int base = blockIdx.x * SCAN_B + threadIdx.x * SCAN_IPT;
+    int v[SCAN_IPT];
+    int s = 0;
+#pragma unroll
+    for (int k = 0; k < SCAN_IPT; k++) {
+        v[k] = base + k < n ? in[base + k] : 0;
+        s += v[k];
+    }
+    int tot;
+    int pre = block_excl_scan(s, sm, tot);
+#pragma unroll
+    for (int k = 0; k < SCAN_IPT; k++) {
+        if (base + k < n) out[base + k] = pre;
+        pre += v[k];
+    }
+    if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+
+// single block: exclusive scan of nb block sums (loops over chunks)
+__global__ void k_scan_sums(int* __restrict__ bsum, int nb)
+{
+    __shared__ int sm[32];
+    int carry = 0;
+    for (int c0 = 0; c0 < nb; c0 += blockDim.x) {
+        int i = c0 + threadIdx.x;
+        int v = i < nb ? bsum[i] : 0;
+        int tot;
+        int pre = block_excl_scan(v, sm, tot);
+        if (i < nb) bsum[i] = pre + carry;
+        carry += tot;
+    }
+}
+
+__global__ void k_scan_add(int* __restrict__ out, int n, const int* __restrict__ bsum)
+{
+    int base = blockIdx.x * SCAN_B + threadIdx.x * SCAN_IPT;
+    int add = bsum[blockIdx.x];
+#pragma unroll
+    for (int k = 0; k < SCAN_IPT; k++)
+        if (base + k < n) out[base + k] += add;
+}
+
+// ===========================================================================
+// A2: counting sort by the full cell key (a single radix pass, radix =
+// number of cells), then a stable per-cell fix-up: within a cell, elements
+// are re-ranked by their previous slot, so the result equals a stable sort
+// of the current order by key (bit-exact with the oracle's counting sort).
+// ===========================================================================
+__global__ void k_scatter(const int* __restrict__ keys, const int* __restrict__ rank,
+                          const int* __restrict__ start, int* __restrict__ perm, int n)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) perm[start[keys[i]] + rank[i]] = i;
+}
+
+__global__ void k_stabilize(const int* __restrict__ perm, const int* __restrict__ keys,
+                            const int* __restrict__ start, int* __restrict__ perm2, int n)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    int o = perm[t];
+    int key = keys[o];
+    int a = start[key], b = start[key + 1];
+    int r = 0;
+    for (int u = a; u < b; u++) r += perm[u] < o;
+    perm2[a + r] = o;
+}
+
+// ===========================================================================
+// A3: reorder (gather) of the per-particle state by the permutation.
+// ===========================================================================
+struct GatherList {
+    int nf;
+    const void* src[14];
+    void* dst[14];
+    int size[14];   // element bytes
+    int n[14];      // elements to move (fluid only, or fluid + walls with an identity tail)
+};
+
+__global__ void k_gather(GatherList G, const int* __restrict__ perm, int n)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    int o = perm[t];
+#pragma unroll 1
+    for (int f = 0; f < G.nf; f++) {
+        if (t >= G.n[f]) continue;
+        switch (G.size[f]) {
+            case 32: {
+                const double2* s = (const double2*)G.src[f] + 2 * (size_t)o;
+                double2* d = (double2*)G.dst[f] + 2 * (size_t)t;
+                d[0] = __ldg(s);
+                d[1] = __ldg(s + 1);
+            } break;
+            case 16: ((float4*)G.dst[f])[t] = __ldg((const float4*)G.src[f] + o); break;
+            case 8: ((double*)G.dst[f])[t] = __ldg((const double*)G.src[f] + o); break;
+            case 4: ((int*)G.dst[f])[t] = __ldg((const int*)G.src[f] + o); break;
+            case 1: ((uint8_t*)G.dst[f])[t] = ((const uint8_t*)G.src[f])[o]; break;
+        }
+    }
+}
+
+// ===========================================================================
+// A5: neighbour lists.  Destination i scans the 3^d stencil of its cell; in
+// each stencil row the cells (cx-1 .. cx+1) are consecutive keys, so their
+// fluid particles form ONE contiguous slot range (likewise the walls').
+// Slot-major ELL: nbr[k * Ntot + i], k < cnt[i] (coalesced per warp).
+// ===========================================================================
+template <class T, int D>
+__device__ __forceinline__ void scan_range(const Params<T>& P, const V4<T>* __restrict__ pos, const V4<T>& xi,
+                                           int i, int a, int b, int* __restrict__ nbr, int& k)
+{
+    for (int j = a; j < b; j++) {
+        if (j == i) continue;
+        V4<T> xj = ld4(pos + j);
+        if (is_neighbor<D>(P, xi, xj)) {
+            if (k < P.cap) nbr[(size_t)k * P.Ntot + i] = j;
+            k++;
+        }
+    }
+}
+
+template <class T, int D>
+__global__ void __launch_bounds__(128) k_build_list(Params<T> P, const V4<T>* __restrict__ pos,
+                                                    const int* __restrict__ fstart, const int* __restrict__ wstart,
+                                                    int* __restrict__ nbr, int* __restrict__ cnt, Ctl* ctl)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    int k = 0;
+    if (i < P.Ntot) {
+        V4<T> xi = ld4(pos + i);
+        int c[3];
+        cell_of<T, D>(P, xi, c);
+        const int zlo = D == 3 ? -1 : 0, zhi = D == 3 ? 1 : 0;
+        for (int dz = zlo; dz <= zhi; dz++) {
+            int cz = c[2] + dz;
+            if (D == 3) {
+                if (P.per[2]) cz = (cz + P.nc[2]) % P.nc[2];
+                else if (cz < 0 || cz >= P.nc[2]) continue;
+            }
+            for (int dy = -1; dy <= 1; dy++) {
+                int cy = c[1] + dy;
+                if (P.per[1]) cy = (cy + P.nc[1]) % P.nc[1];
+                else if (cy < 0 || cy >= P.nc[1]) continue;
+                int row = P.nc[0] * (cy + P.nc[1] * cz);
+                int x0 = c[0] - 1, x1 = c[0] + 1;
+                if (P.per[0] && (x0 < 0 || x1 >= P.nc[0])) {
+                    // wrapped row: three separate cells
+                    for (int dx = -1; dx <= 1; dx++) {
+                        int cx = (c[0] + dx + P.nc[0]) % P.nc[0];
+                        int key = row + cx;
+                        scan_range<T, D>(P, pos, xi, i, fstart[key], fstart[key + 1], nbr, k);
+                        scan_range<T, D>(P, pos, xi, i, P.Nf + wstart[key], P.Nf + wstart[key + 1], nbr, k);
+                    }
+                } else {
+                    x0 = max(x0, 0);
+                    x1 = min(x1, P.nc[0] - 1);
+                    scan_range<T, D>(P, pos, xi, i, fstart[row + x0], fstart[row + x1 + 1], nbr, k);
+                    scan_range<T, D>(P, pos, xi, i, P.Nf + wstart[row + x0], P.Nf + wstart[row + x1 + 1], nbr, k);
+                }
+            }
+        }
+        cnt[i] = k < P.cap ? k : P.cap;
+    }
+    // warp max of counts and warp sum of fluid-row counts -> one atomic each
+    int m = k;
+    unsigned sfl = (i < P.Nf) ? (unsigned)min(k, P.cap) : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+        sfl += __shfl_xor_sync(0xffffffffu, sfl, o);
+    }
+    if ((threadIdx.x & 31) == 0 && m > 0) {
+        atomicMax(&ctl->max_count, m);
+        if (m > P.cap) atomicExch(&ctl->overflow, 1);
+        if (sfl) atomicAdd(&ctl->pairs_fluid, (unsigned long long)sfl);
+    }
+}
+
+// ===========================================================================
+// A6: summation density, eq:summation_density, self included;
+// walls keep rho0 unless wall_rho_summation (R4).  Free surface flag
+// rho_i / rho0 < 0.8 for fluid.
+// ===========================================================================
+template <class T, int D>
+__global__ void __launch_bounds__(256) k_density(Params<T> P, const V4<T>* __restrict__ pos,
+                                                 const int* __restrict__ nbr, const int* __restrict__ cnt,
+                                                 T* __restrict__ rho, uint8_t* __restrict__ fs)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.Ntot) return;
+    V4<T> xi = ld4(pos + i);
+    if (i >= P.Nf && !P.wall_rho_summation) {
+        rho[i] = P.rho0;
+        return;
+    }
+    T s = xi.w * P.w0;
+    int n = cnt[i];
+    for (int k = 0; k < n; k++) {
+        int j = __ldg(nbr + (size_t)k * P.Ntot + i);
+        V4<T> xj = ld4(pos + j);
+        T d[3];
+        T r = my_sqrt(pair_vec<T, D>(P, xi, xj, d));
+        s += xj.w * (P.sig * quintic5(r * P.inv_h));
+    }
+    rho[i] = s;
+    if (i < P.Nf) fs[i] = (s / P.rho0 < P.fs_ratio) ? 1 : 0;
+}
+
+// ===========================================================================
+// A7 / A10: wall velocities from a Shepard average of a fluid vector field
+// with W(r, h/2) (eq:vf), then eq:vg-adami (u_wall = 0) or the
+// slip reading (R16), then eq:vg-no-normal's clip.
+//   mode 0: mirror (ghost velocity, no-slip u*): u_w = -Shepard
+//   mode 1: slip u*: u_w = +Shepard
+// ===========================================================================
+template <class T, int D>
+__global__ void __launch_bounds__(256) k_wall_velocity(Params<T> P, const V4<T>* __restrict__ pos,
+                                                       const int* __restrict__ nbr, const int* __restrict__ cnt,
+                                                       const V4<T>* __restrict__ nrm, V4<T>* __restrict__ vel, int mode)
+{
+    int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= P.Nw) return;
+    int i = P.Nf + w;
+    V4<T> xi = ld4(pos + i);
+    T sw = 0, ax = 0, ay = 0, az = 0;
+    int n = cnt[i];
+    for (int k = 0; k < n; k++) {
+        int j = __ldg(nbr + (size_t)k * P.Ntot + i);
+        if (j >= P.Nf) continue;
+        V4<T> xj = ld4(pos + j);
+        T d[3];
+        T r = my_sqrt(pair_vec<T, D>(P, xi, xj, d));
+        T wv = P.sig2 * quintic5(r * P.inv_h2);
+        V4<T> uj = ld4(vel + j);
+        ax += uj.x * wv;
+        ay += uj.y * wv;
+        if (D == 3) az += uj.z * wv;
+        sw += wv;
+    }
+    T ux = 0, uy = 0, uz = 0;
+    if (sw > 0) {
+        ux = ax / sw;
+        uy = ay / sw;
+        uz = D == 3 ? az / sw : T(0);
+    }
+    if (mode == 0) {
+        ux = -ux;
+        uy = -uy;
+        uz = -uz;
+    }
+    V4<T> nn = ld4(nrm + w);
+    T un = ux * nn.x + uy * nn.y;
+    if (D == 3) un += uz * nn.z;
+    if (un < 0) {
+        ux -= un * nn.x;
+        uy -= un * nn.y;
+        if (D == 3) uz -= un * nn.z;
+    }
+    vel[i] = mk4<T>(ux, uy, uz, T(0));
+}
+
+// ===========================================================================
+// A8: non-pressure forces + predictors (Alg. 1 lines 3-5):
+//   f_visc  eq:mom:sph:visc, fluid + wall sources (R19)
+//   f_avisc eq:mom:sph:av (R20), fluid + wall (ghost velocities)
+//   f_astress eq:mom:sph:gtvf:stress (R21), fluid sources
+//   u* = u + dt (f_visc + f_avisc + f_astress + g)   (eq:int:vint)
+//   r* = r + dt u~                                    (eq:int:rnp1)
+// ===========================================================================
+template <class T, int D>
+__global__ void __launch_bounds__(128) k_forces_predict(Params<T> P, T dt, const V4<T>* __restrict__ pos,
+                                                        const V4<T>* __restrict__ vel, const V4<T>* __restrict__ vt,
+                                                        const T* __restrict__ rho, const int* __restrict__ nbr,
+                                                        const int* __restrict__ cnt, V4<T>* __restrict__ us,
+                                                        V4<T>* __restrict__ rstar)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.Nf) return;
+    V4<T> xi = ld4(pos + i), ui = ld4(vel + i), uti = ld4(vt + i);
+    T rhoi = rho[i];
+    T ax = P.g[0], ay = P.g[1], az = D == 3 ? P.g[2] : T(0);
+    T dux = uti.x - ui.x, duy = uti.y - ui.y, duz = D == 3 ? uti.z - ui.z : T(0);
+    const T nu4 = T(4) * P.nu;
+    const T avf = P.alpha * P.h * P.c_ref;
+    int n = cnt[i];
+    for (int k = 0; k < n; k++) {
+        int j = __ldg(nbr + (size_t)k * P.Ntot + i);
+        V4<T> xj = ld4(pos + j), uj = ld4(vel + j);
+        T rhoj = __ldg(rho + j);
+        T d[3];
+        T r2 = pair_vec<T, D>(P, xi, xj, d);
+        T r = my_sqrt(r2);
+        T dwdr = P.dwk * quintic4(r * P.inv_h);
+        T gf = r > T(0) ? dwdr / r : T(0);           // grad W = gf * r_ij
+        T mj = xj.w;
+        T uijx = ui.x - uj.x, uijy = ui.y - uj.y, uijz = D == 3 ? ui.z - uj.z : T(0);
+        T den = r2 + P.eta_h2;
+        if (P.nu > T(0)) {
+            T f = mj * nu4 / (rhoi + rhoj) * (r * dwdr) / den;
+            ax += f * uijx;
+            ay += f * uijy;
+            if (D == 3) az += f * uijz;
+        }
+        if (P.alpha > T(0)) {
+            T vr = uijx * d[0] + uijy * d[1];
+            if (D == 3) vr += uijz * d[2];
+            if (vr < T(0)) {
+                T phi = vr / den;
+                T Pi = -avf * phi / (T(0.5) * (rhoi + rhoj));
+                T f = mj * Pi * gf;
+                ax -= f * d[0];
+                ay -= f * d[1];
+                if (D == 3) az -= f * d[2];
+            }
+        }
+        if (j < P.Nf) {
+            V4<T> utj = ld4(vt + j);
+            T gx = gf * d[0], gy = gf * d[1], gz = D == 3 ? gf * d[2] : T(0);
+            T ai = (dux * gx + duy * gy + (D == 3 ? duz * gz : T(0))) / rhoi;
+            T aj = ((utj.x - uj.x) * gx + (utj.y - uj.y) * gy + (D == 3 ? (utj.z - uj.z) * gz : T(0))) / rhoj;
+            ax += mj * (ui.x * ai + uj.x * aj);
+            ay += mj * (ui.y * ai + uj.y * aj);
+            if (D == 3) az += mj * (ui.z * ai + uj.z * aj);
+        }
+    }
+    us[i] = mk4<T>(ui.x + dt * ax, ui.y + dt * ay, D == 3 ? ui.z + dt * az : T(0), T(0));
+    T rx = xi.x + dt * uti.x, ry = xi.y + dt * uti.y, rz = D == 3 ? xi.z + dt * uti.z : xi.z;
+    if (P.per[0]) { if (rx >= P.hi[0]) rx -= P.L[0]; else if (rx < P.lo[0]) rx += P.L[0]; }
+    if (P.per[1]) { if (ry >= P.hi[1]) ry -= P.L[1]; else if (ry < P.lo[1]) ry += P.L[1]; }
+    if (D == 3 && P.per[2]) { if (rz >= P.hi[2]) rz -= P.L[2]; else if (rz < P.lo[2]) rz += P.L[2]; }
+    rstar[i] = mk4<T>(rx, ry, rz, xi.w);
+}
+
+// ===========================================================================
+// A11: RHS_i (eq:sph-ppe right side, R8), D_ii (eq:coeff, R6/R7) and the
+// device-wide Lambda = max |RHS_i / D_ii| over non-free-surface fluid with
+// D_ii != 0 (eq:convergence, R12).
+// ===========================================================================
+template <class T, int D>
+__global__ void __launch_bounds__(128) k_rhs_diag(Params<T> P, T inv_dt, const V4<T>* __restrict__ pos,
+                                                  const V4<T>* __restrict__ us, const T* __restrict__ rho,
+                                                  const uint8_t* __restrict__ fs, const int* __restrict__ nbr,
+                                                  const int* __restrict__ cnt, T* __restrict__ rhs,
+                                                  T* __restrict__ diag, Ctl* ctl)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    double lam = 0.0;
+    if (i < P.Nf) {
+        V4<T> xi = ld4(pos + i), ui = ld4(us + i);
+        T rhoi = rho[i];
+        T sr = 0, sd = 0;
+        int n = cnt[i];
+        for (int k = 0; k < n; k++) {
+            int j = __ldg(nbr + (size_t)k * P.Ntot + i);
+            V4<T> xj = ld4(pos + j), uj = ld4(us + j);
+            T rhoj = __ldg(rho + j);
+            T d[3];
+            T r2 = pair_vec<T, D>(P, xi, xj, d);
+            T r = my_sqrt(r2);
+            T dwdr = P.dwk * quintic4(r * P.inv_h);
+            T gf = r > T(0) ? dwdr / r : T(0);
+            T mj = xj.w;
+            T ud = (ui.x - uj.x) * d[0] + (ui.y - uj.y) * d[1];
+            if (D == 3) ud += (ui.z - uj.z) * d[2];
+            sr -= mj / rhoj * inv_dt * (ud * gf);
+            sd += T(4) * mj / (rhoi * (rhoi + rhoj)) * (r * dwdr) / (r2 + P.eta_h2);
+        }
+        rhs[i] = sr;
+        diag[i] = sd;
+        if (!fs[i] && sd != T(0)) lam = (double)fabs(sr / sd);
+    }
+    lam = warp_max(lam);
+    if ((threadIdx.x & 31) == 0 && lam > 0.0)
+        atomicMax(&ctl->lambda_bits, (unsigned long long)__double_as_longlong(lam));
+}
+
+// ===========================================================================
+// A12(i): wall pressure, eq:p-shepard (R14): fluid sources, a_w = 0,
+// sum W = 0 -> 0, optional clamp of negative values.  In a solve it reads
+// p^k from the buffer selected by the device iteration counter.
+// ===========================================================================
+template <class T, int D>
+__global__ void __launch_bounds__(256) k_wall_pressure(Params<T> P, const V4<T>* __restrict__ pos,
+                                                       const T* __restrict__ rho, const int* __restrict__ nbr,
+                                                       const int* __restrict__ cnt, T* pA, T* pB, const Ctl* ctl)
+{
+    T* p = pA;
+    if (ctl) {
+        if (ctl->done) return;
+        p = (ctl->iter & 1) ? pB : pA;
+    }
+    int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= P.Nw) return;
+    int i = P.Nf + w;
+    V4<T> xi = ld4(pos + i);
+    T sw = 0, sp = 0, sx = 0, sy = 0, sz = 0;
+    int n = cnt[i];
+    for (int k = 0; k < n; k++) {
+        int j = __ldg(nbr + (size_t)k * P.Ntot + i);
+        if (j >= P.Nf) continue;
+        V4<T> xj = ld4(pos + j);
+        T d[3];
+        T r = my_sqrt(pair_vec<T, D>(P, xi, xj, d));
+        T wv = P.sig * quintic5(r * P.inv_h);
+        T rw = __ldg(rho + j) * wv;
+        sp += p[j] * wv;
+        sx += rw * d[0];
+        sy += rw * d[1];
+        if (D == 3) sz += rw * d[2];
+        sw += wv;
+    }
+    T pw = 0;
+    if (sw > T(0)) {
+        T gr = P.g[0] * sx + P.g[1] * sy;
+        if (D == 3) gr += P.g[2] * sz;
+        pw = (sp + gr) / sw;
+    }
+    if (P.clamp_wall_p && pw < T(0)) pw = T(0);
+    p[i] = pw;
+}
+
+// ===========================================================================
+// A12(ii, iii): one damped-Jacobi sweep, eq:p-sor with
+// fac_ij = 4 m_j / (rho_i (rho_i + rho_j)) r_ij.gradW_ij / (r^2 + eta h^2)
+// recomputed matrix-free from the positions, the special cases
+// of P:530-534, and the fused device-wide fp64 reduction of eq:convergence
+// (sum |p^{k+1} - p^k|, sum |p^{k+1}|) finished by the last block, which also
+// takes the stop decision (R12, R13) on the device.
+// ===========================================================================
+constexpr int SWEEP_T = 256;
+
+template <class T, int D>
+__global__ void __launch_bounds__(SWEEP_T) k_sweep(Params<T> P, const V4<T>* __restrict__ pos,
+                                                   const T* __restrict__ rho, const T* __restrict__ rhs,
+                                                   const T* __restrict__ diag, const uint8_t* __restrict__ fs,
+                                                   const int* __restrict__ nbr, const int* __restrict__ cnt,
+                                                   T* pA, T* pB, Ctl* ctl, double* __restrict__ partials,
+                                                   double tol, int min_it, int max_it)
+{
+    if (ctl->done) return;
+    const int kit = ctl->iter;
+    const T* __restrict__ pin = (kit & 1) ? pB : pA;
+    T* __restrict__ pout = (kit & 1) ? pA : pB;
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    double dn = 0.0, dd = 0.0;
+    bool bad = false;
+    if (i < P.Nf) {
+        T pold = pin[i];
+        T pnew = T(0);
+        T di = diag[i];
+        if (!fs[i] && di != T(0)) {
+            V4<T> xi = ld4(pos + i);
+            T rhoi = rho[i];
+            T s = 0;
+            int n = cnt[i];
+            for (int k = 0; k < n; k++) {
+                int j = __ldg(nbr + (size_t)k * P.Ntot + i);
+                V4<T> xj = ld4(pos + j);
+                T rhoj = __ldg(rho + j);
+                T pj = pin[j];
+                T d[3];
+                T r2 = pair_vec<T, D>(P, xi, xj, d);
+                T r = my_sqrt(r2);
+                T dwdr = P.dwk * quintic4(r * P.inv_h);
+                T fac = T(4) * xj.w / (rhoi * (rhoi + rhoj)) * (r * dwdr) / (r2 + P.eta_h2);
+                s += fac * pj;
+            }
+            pnew = P.omega * (rhs[i] + s) / di + (T(1) - P.omega) * pold;
+        }
+        pout[i] = pnew;
+        dn = fabs((double)pnew - (double)pold);
+        dd = fabs((double)pnew);
+        bad = !isfinite((double)pnew);
+    }
+    // block reduction (fixed order)
+    __shared__ double sn[SWEEP_T / 32], sd[SWEEP_T / 32];
+    __shared__ int last;
+    dn = warp_sum(dn);
+    dd = warp_sum(dd);
+    int anybad = __any_sync(0xffffffffu, bad);
+    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) {
+        sn[w] = dn;
+        sd[w] = dd;
+        if (anybad) atomicExch(&ctl->nonfinite, 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0, b = 0;
+        for (int q = 0; q < SWEEP_T / 32; q++) {
+            a += sn[q];
+            b += sd[q];
+        }
+        partials[2 * blockIdx.x] = a;
+        partials[2 * blockIdx.x + 1] = b;
+        __threadfence();
+        unsigned t = atomicAdd(&ctl->ticket, 1u);
+        last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    // the last block: fixed-assignment sum of all partials -> deterministic
+    double a = 0, b = 0;
+    for (int q = threadIdx.x; q < (int)gridDim.x; q += blockDim.x) {
+        a += ((volatile double*)partials)[2 * q];
+        b += ((volatile double*)partials)[2 * q + 1];
+    }
+    a = warp_sum(a);
+    b = warp_sum(b);
+    if (lane == 0) {
+        sn[w] = a;
+        sd[w] = b;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double num = 0, den = 0;
+        for (int q = 0; q < SWEEP_T / 32; q++) {
+            num += sn[q];
+            den += sd[q];
+        }
+        double lam = __longlong_as_double((long long)ctl->lambda_bits);
+        double dmax = den > lam ? den : lam;
+        double res = num == 0.0 ? 0.0 : (dmax > 0.0 ? num / dmax : INFINITY);
+        int k1 = kit + 1;
+        ctl->residual = res;
+        ctl->iter = k1;
+        ctl->done = ((k1 >= min_it && res < tol) || k1 >= max_it || ctl->nonfinite) ? 1 : 0;
+        ctl->ticket = 0;
+    }
+}
+
+// ===========================================================================
+// A13: pressure gradient (eq:mom:sph:press:symm / :pij, R18) and corrector
+// u^{n+1} = u* + dt f_p (eq:int:vnp1).  Sources fluid + wall.
+// ===========================================================================
+template <class T, int D>
+__global__ void __launch_bounds__(128) k_pgrad_correct(Params<T> P, T dt, const V4<T>* __restrict__ pos,
+                                                       const T* __restrict__ rho, const T* __restrict__ p,
+                                                       const V4<T>* __restrict__ us, const int* __restrict__ nbr,
+                                                       const int* __restrict__ cnt, V4<T>* __restrict__ vel)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.Nf) return;
+    V4<T> xi = ld4(pos + i);
+    T rhoi = rho[i], pi = p[i];
+    T pir = pi / (rhoi * rhoi);
+    T ax = 0, ay = 0, az = 0;
+    int n = cnt[i];
+    for (int k = 0; k < n; k++) {
+        int j = __ldg(nbr + (size_t)k * P.Ntot + i);
+        V4<T> xj = ld4(pos + j);
+        T rhoj = __ldg(rho + j), pj = __ldg(p + j);
+        T d[3];
+        T r = my_sqrt(pair_vec<T, D>(P, xi, xj, d));
+        T dwdr = P.dwk * quintic4(r * P.inv_h);
+        T gf = r > T(0) ? dwdr / r : T(0);
+        T f = P.pgrad == 0 ? xj.w * (pir + pj / (rhoj * rhoj)) : xj.w / (rhoi * rhoj) * (pj - pi);
+        f *= gf;
+        ax -= f * d[0];
+        ay -= f * d[1];
+        if (D == 3) az -= f * d[2];
+    }
+    V4<T> u = ld4(us + i);
+    vel[i] = mk4<T>(u.x + dt * ax, u.y + dt * ay, D == 3 ? u.z + dt * az : T(0), T(0));
+}
+
+// ===========================================================================
+// A14: one modified-GTVF sub-step (eq:int:gtvf:pos, eq:int:gtvf:vel:tmp) with
+// f_GTVF(r^k) = -p0_i sum_j m_j / rho_j^2 gradW(r^k_ij, h~) (eq:mom:sph:gtvf)
+// over the pair set frozen at r* (P:454-456).  p0 per P:389-390 / R22.
+// ===========================================================================
+template <class T, int D>
+__global__ void __launch_bounds__(128) k_gtvf_substep(Params<T> P, T dtau, const V4<T>* __restrict__ rk,
+                                                      V4<T>* __restrict__ rk1, V4<T>* __restrict__ vk,
+                                                      const T* __restrict__ rho, const T* __restrict__ p,
+                                                      const int* __restrict__ nbr, const int* __restrict__ cnt,
+                                                      int first)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.Nf) return;
+    V4<T> xi = ld4(rk + i);
+    T ax = 0, ay = 0, az = 0;
+    int n = cnt[i];
+    for (int k = 0; k < n; k++) {
+        int j = __ldg(nbr + (size_t)k * P.Ntot + i);
+        V4<T> xj = ld4(rk + j);
+        T rhoj = __ldg(rho + j);
+        T d[3];
+        T r = my_sqrt(pair_vec<T, D>(P, xi, xj, d));
+        T dwdr = P.dwkt * quintic4(r * P.inv_ht);
+        T gf = r > T(0) ? dwdr / r : T(0);
+        T f = xj.w / (rhoj * rhoj) * gf;
+        ax += f * d[0];
+        ay += f * d[1];
+        if (D == 3) az += f * d[2];
+    }
+    T p0 = P.p_ref;
+    if (P.pref_external) {
+        T v = T(10) * fabs(p[i]);
+        p0 = v < P.p_ref ? v : P.p_ref;
+    }
+    ax *= -p0;
+    ay *= -p0;
+    az *= -p0;
+    V4<T> v = first ? mk4<T>(T(0), T(0), T(0), T(0)) : ld4(vk + i);
+    T h2 = T(0.5) * dtau * dtau;
+    rk1[i] = mk4<T>(xi.x + dtau * v.x + h2 * ax, xi.y + dtau * v.y + h2 * ay,
+                    D == 3 ? xi.z + dtau * v.z + h2 * az : xi.z, xi.w);
+    vk[i] = mk4<T>(v.x + dtau * ax, v.y + dtau * ay, D == 3 ? v.z + dtau * az : T(0), T(0));
+}
+
+// ===========================================================================
+// A15: transport velocity (eq:int:vhatnp2) and positions from r^n
+// (eq:int:rnp2, R24), periodic wrap.
+// ===========================================================================
+template <class T, int D>
+__global__ void k_advance(Params<T> P, T dt, const V4<T>* __restrict__ rK, const V4<T>* __restrict__ rn,
+                          const V4<T>* __restrict__ vel, V4<T>* __restrict__ pos, V4<T>* __restrict__ vt)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.Nf) return;
+    V4<T> r0 = ld4(pos + i), rk = ld4(rK + i), x = ld4(rn + i), u = ld4(vel + i), ut = ld4(vt + i);
+    T tx = u.x + (rk.x - r0.x) / dt, ty = u.y + (rk.y - r0.y) / dt;
+    T tz = D == 3 ? u.z + (rk.z - r0.z) / dt : T(0);
+    T hd = T(0.5) * dt;
+    T X = x.x + hd * (tx + ut.x), Y = x.y + hd * (ty + ut.y), Z = D == 3 ? x.z + hd * (tz + ut.z) : x.z;
+    if (P.per[0]) { if (X >= P.hi[0]) X -= P.L[0]; else if (X < P.lo[0]) X += P.L[0]; }
+    if (P.per[1]) { if (Y >= P.hi[1]) Y -= P.L[1]; else if (Y < P.lo[1]) Y += P.L[1]; }
+    if (D == 3 && P.per[2]) { if (Z >= P.hi[2]) Z -= P.L[2]; else if (Z < P.lo[2]) Z += P.L[2]; }
+    pos[i] = mk4<T>(X, Y, Z, x.w);
+    vt[i] = mk4<T>(tx, ty, tz, T(0));
+}
+
+// ===========================================================================
+// A0: wall normals (§3.4.1, eq:normal-approx / eq:normal, R17), at create.
+// ===========================================================================
+template <class T, int D>
+__global__ void k_normals_raw(Params<T> P, const V4<T>* __restrict__ pos, const T* __restrict__ rho,
+                              const int* __restrict__ nbr, const int* __restrict__ cnt, V4<T>* __restrict__ ns)
+{
+    int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= P.Nw) return;
+    int i = P.Nf + w;
+    V4<T> xi = ld4(pos + i);
+    T ax = 0, ay = 0, az = 0;
+    int n = cnt[i];
+    for (int k = 0; k < n; k++) {
+        int j = nbr[(size_t)k * P.Ntot + i];
+        if (j < P.Nf) continue;
+        V4<T> xj = ld4(pos + j);
+        T d[3];
+        T r = my_sqrt(pair_vec<T, D>(P, xi, xj, d));
+        T gf = r > T(0) ? P.dwk * quintic4(r * P.inv_h) / r : T(0);
+        T v = xj.w / rho[j] * gf;
+        ax -= v * d[0];
+        ay -= v * d[1];
+        if (D == 3) az -= v * d[2];
+    }
+    T mag = my_sqrt(ax * ax + ay * ay + az * az);
+    if (mag < T(1) / (T(4) * P.h)) ax = ay = az = T(0);
+    else {
+        ax /= mag;
+        ay /= mag;
+        az /= mag;
+    }
+    ns[w] = mk4<T>(ax, ay, az, T(0));
+}
+
+template <class T, int D>
+__global__ void k_normals_smooth(Params<T> P, const V4<T>* __restrict__ pos, const T* __restrict__ rho,
+                                 const int* __restrict__ nbr, const int* __restrict__ cnt,
+                                 const V4<T>* __restrict__ ns, V4<T>* __restrict__ nrm)
+{
+    int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= P.Nw) return;
+    int i = P.Nf + w;
+    V4<T> xi = ld4(pos + i);
+    T v0 = xi.w / rho[i] * P.w0;
+    V4<T> n0 = ns[w];
+    T ax = v0 * n0.x, ay = v0 * n0.y, az = v0 * n0.z;
+    int n = cnt[i];
+    for (int k = 0; k < n; k++) {
+        int j = nbr[(size_t)k * P.Ntot + i];
+        if (j < P.Nf) continue;
+        V4<T> xj = ld4(pos + j);
+        T d[3];
+        T r = my_sqrt(pair_vec<T, D>(P, xi, xj, d));
+        T v = xj.w / rho[j] * (P.sig * quintic5(r * P.inv_h));
+        V4<T> nj = ns[j - P.Nf];
+        ax += v * nj.x;
+        ay += v * nj.y;
+        az += v * nj.z;
+    }
+    // R17: a smoothed vector shorter than 0.01 (layers cancelling) has no direction -> 0
+    T mag = my_sqrt(ax * ax + ay * ay + az * az);
+    if (mag >= T(0.01)) {
+        ax /= mag;
+        ay /= mag;
+        az /= mag;
+    } else {
+        ax = ay = az = T(0);
+    }
+    nrm[w] = mk4<T>(ax, ay, az, T(0));
+}
+
+// ===========================================================================
+// host <-> device marshalling in creation-id order
+// ===========================================================================
+// vector field: dst[slot] = src[id[slot]] (id order -> internal order)
+template <class T>
+__global__ void k_from_ids_vec(const double* __restrict__ src, const int* __restrict__ id, int n, int dim,
+                               V4<T>* __restrict__ dst, int keep_w)
+{
+    int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    const double* v = src + (size_t)id[s] * dim;
+    V4<T> o = dst[s];
+    o.x = (T)v[0];
+    o.y = (T)v[1];
+    o.z = dim == 3 ? (T)v[2] : T(0);
+    if (!keep_w) o.w = T(0);
+    dst[s] = o;
+}
+template <class T>
+__global__ void k_to_ids_vec(const V4<T>* __restrict__ src, const int* __restrict__ id, int n, int dim,
+                             double* __restrict__ dst)
+{
+    int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    V4<T> o = src[s];
+    double* v = dst + (size_t)id[s] * dim;
+    v[0] = (double)o.x;
+    v[1] = (double)o.y;
+    if (dim == 3) v[2] = (double)o.z;
+}
+template <class T>
+__global__ void k_from_ids_w(const double* __restrict__ src, const int* __restrict__ id, int n,
+                             V4<T>* __restrict__ dst)
+{
+    int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    dst[s].w = (T)src[id[s]];
+}
+template <class T>
+__global__ void k_to_ids_w(const V4<T>* __restrict__ src, const int* __restrict__ id, int n, double* __restrict__ dst)
+{
+    int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    dst[id[s]] = (double)src[s].w;
+}
+template <class T, class S>
+__global__ void k_from_ids_sc(const double* __restrict__ src, const int* __restrict__ id, int n, S* __restrict__ dst)
+{
+    int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    dst[s] = (S)src[id[s]];
+}
+template <class S>
+__global__ void k_to_ids_sc(const S* __restrict__ src, const int* __restrict__ id, int n, double* __restrict__ dst)
+{
+    int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    dst[id[s]] = (double)src[s];
+}
+__global__ void k_iota(int* __restrict__ a, int n, int base)
+{
+    int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s < n) a[s] = base + s;
+}
+
+}  // namespace sb

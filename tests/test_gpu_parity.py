@@ -1,0 +1,238 @@
+"""GPU (libsisph.so, sm_100a) vs the fp64 oracle, on identical seeded inputs.
+
+Every call goes through the C ABI (ctypes binding).  Discrete results (cell
+order, neighbour sets, sweep counts) must be bit-exact; fields must be within
+the north_star tolerances (parity_util.TOL).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from parity_util import TOL, assert_close, gpu_sim, oracle_from_gpu, resync, small_cases
+
+pytestmark = pytest.mark.gpu
+
+CASES = small_cases()
+
+
+def _prec(case):
+    return case.params["precision"]
+
+
+# ------------------------------------------------------------------ A1-A4
+@pytest.mark.parametrize("name", list(CASES))
+def test_cell_order_is_the_stable_sort(name):
+    case = CASES[name]
+    sim = gpu_sim(case)
+    nf = case.n_fluid
+    cfg = oracle.case_cfg(case)
+    x = sim.get("POSITION")
+    # walls: sorted once at create, stable in creation order
+    order0 = sim.order()
+    wid = np.flatnonzero(case.tag == 1)
+    if wid.size:
+        o, _ = oracle.cell_order(cfg, x[wid])
+        assert np.array_equal(order0[nf:], wid[o])
+    # move the fluid, rebuild: new order = stable sort of the CURRENT order by key
+    rng = np.random.default_rng(3)
+    x2 = x.copy()
+    f = case.tag == 0
+    x2[f] += rng.uniform(-0.7, 0.7, (nf, case.dim)) * case.h
+    for a in range(case.dim):
+        if case.periodic[a]:
+            L = case.hi[a] - case.lo[a]
+            x2[:, a] = np.where(x2[:, a] >= case.hi[a], x2[:, a] - L, x2[:, a])
+            x2[:, a] = np.where(x2[:, a] < case.lo[a], x2[:, a] + L, x2[:, a])
+    sim.set("POSITION", x2)
+    x2 = sim.get("POSITION")            # precision-rounded
+    cur = sim.order()[:nf]
+    sim.build_neighbors()
+    new = sim.order()
+    o, keys = oracle.cell_order(cfg, x2[cur])
+    assert np.array_equal(new[:nf], cur[o])
+    assert np.array_equal(new[nf:], order0[nf:])
+
+
+# ------------------------------------------------------------------ A5
+@pytest.mark.parametrize("name", list(CASES))
+def test_neighbor_sets_bit_exact(name):
+    case = CASES[name]
+    sim = gpu_sim(case)
+    x = sim.get("POSITION")
+    off, ids = sim.neighbors()
+    roff, rids = oracle.neighbors(oracle.case_cfg(case), x)
+    assert np.array_equal(off, roff)
+    assert np.array_equal(ids, rids)
+
+
+def test_neighbor_sets_with_exact_ties_fp64():
+    # hydrostatic lattice: every lattice pair at exactly 3h is a tie and must be excluded
+    case = synth.hydrostatic(nx=30, ny=30, dx=0.02, precision=64)
+    sim = gpu_sim(case)
+    off, ids = sim.neighbors()
+    roff, rids = oracle.neighbors(oracle.case_cfg(case), sim.get("POSITION"))
+    assert np.array_equal(off, roff) and np.array_equal(ids, rids)
+    interior = np.diff(off)[(case.tag == 0)]
+    assert np.median(interior) == 24
+
+
+# ------------------------------------------------------------------ A6-A11
+@pytest.mark.parametrize("name", list(CASES))
+def test_predict_parity(name):
+    case = CASES[name]
+    prec = _prec(case)
+    sim = gpu_sim(case)
+    o = oracle_from_gpu(case, sim)
+    f, w = case.tag == 0, case.tag == 1
+    if w.any():
+        assert_close("normal", sim.get("NORMAL")[w], o.get("normal")[w], prec, scale=1.0)
+    sim.predict(case.dt)
+    o.predict(case.dt)
+    rho_o = o.get("rho")
+    assert_close("rho", sim.get("DENSITY"), rho_o, prec)
+    # free-surface flags: exact, except hazards within 1e-6 of the threshold
+    haz = np.abs(rho_o / case.params["rho0"] - case.params["fs_ratio"]) < 1e-6
+    assert np.array_equal(sim.get("FREE_SURFACE")[~haz], o.get("fs")[~haz])
+    assert_close("rstar", sim.get("RSTAR")[f], o.get("xs")[f], prec, scale=np.abs(case.x).max())
+    assert_close("ustar", sim.get("USTAR"), o.get("us"), prec, scale=max(np.abs(o.get("us")).max(), 1e-3))
+    if w.any():
+        assert_close("ghost u", sim.get("VELOCITY")[w], o.get("u")[w], prec,
+                     scale=max(np.abs(o.get("u")).max(), 1e-3))
+    assert_close("diag", sim.get("DIAG")[f], o.get("diag")[f], prec)
+    assert_close("rhs", sim.get("RHS")[f], o.get("rhs")[f], prec, scale=max(np.abs(o.get("rhs")).max(), 1e-9))
+
+
+# ------------------------------------------------------------------ A12
+@pytest.mark.parametrize("name", [n for n in CASES if n.endswith("f64")])
+def test_solve_parity_fp64_iteration_count(name):
+    case = CASES[name]
+    sim = gpu_sim(case)
+    o = oracle_from_gpu(case, sim)
+    sim.predict(case.dt)
+    o.predict(case.dt)
+    tol, mx = case.params["tol"], case.params["max_iter"]
+    it_g, res_g = sim.ppe_solve(tol, mx)
+    it_o, res_o, lam = o.solve(tol, mx)
+    hazard = abs(res_o - tol) <= 1e-9 * tol
+    if not hazard:
+        assert it_g == it_o, (it_g, it_o, res_g, res_o)
+    assert res_g == pytest.approx(res_o, rel=1e-8, abs=1e-14)
+    f = case.tag == 0
+    assert_close("p", sim.get("PRESSURE")[f], o.get("p")[f], 64)
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_fixed_sweeps_parity(name):
+    # tol = 0, max_iter = S: both sides do exactly S sweeps (SURVEY §8(c) fp32 contract)
+    case = CASES[name]
+    prec = _prec(case)
+    sim = gpu_sim(case)
+    o = oracle_from_gpu(case, sim)
+    sim.predict(case.dt)
+    o.predict(case.dt)
+    S = 7
+    it_g, _ = sim.ppe_solve(0.0, S)
+    it_o, _, _ = o.solve(0.0, S)
+    assert it_g == it_o == S
+    assert_close("p", sim.get("PRESSURE"), o.get("p"), prec)
+
+
+# ------------------------------------------------------------------ A13-A15
+@pytest.mark.parametrize("name", list(CASES))
+def test_full_step_parity_resynced(name):
+    """Several full Algorithm-1 steps; before each step the oracle is loaded with
+    the GPU's state, so both sides step from identical inputs."""
+    case = CASES[name]
+    prec = _prec(case)
+    sim = gpu_sim(case)
+    o = oracle_from_gpu(case, sim)
+    f = case.tag == 0
+    steps = 3 if case.dim == 3 else 4
+    over = {} if prec == 64 else {"tol": 0.0, "max_iter": 5}
+    tol = over.get("tol", case.params["tol"])
+    mx = over.get("max_iter", case.params["max_iter"])
+    for s in range(steps):
+        resync(case, sim, o)
+        sim.predict(case.dt)
+        o.predict(case.dt)
+        it_g, _ = sim.ppe_solve(tol, mx)
+        it_o, res_o, _ = o.solve(tol, mx)
+        if prec == 64 and abs(res_o - tol) > 1e-9 * tol:
+            assert it_g == it_o, (s, it_g, it_o)
+        sim.correct(case.dt)
+        o.correct(case.dt)
+        assert_close(f"p step {s}", sim.get("PRESSURE")[f], o.get("p")[f], prec)
+        assert_close(f"u step {s}", sim.get("VELOCITY")[f], o.get("u")[f], prec,
+                     scale=max(np.abs(o.get("u")[f]).max(), 1e-3))
+        assert_close(f"ut step {s}", sim.get("TRANSPORT_VELOCITY")[f], o.get("ut")[f], prec,
+                     scale=max(np.abs(o.get("ut")[f]).max(), 1e-3))
+        dxg = sim.get("POSITION")[f] - o.get("x")[f]
+        for a in range(case.dim):
+            if case.periodic[a]:
+                L = case.hi[a] - case.lo[a]
+                dxg[:, a] = (dxg[:, a] + 0.5 * L) % L - 0.5 * L
+        rel, ab = TOL[prec]
+        assert np.abs(dxg).max() <= rel * np.abs(case.x).max() + ab
+
+
+def test_tgv2d_ten_steps_free_running():
+    """C1 exactly as configured (fp64, tol 1e-4, 10 steps), both sides free
+    running from the same inputs: sweep counts equal each step, fields close,
+    and the decay matches exp(b t)."""
+    case = synth.tgv2d()
+    sim = gpu_sim(case)
+    o = oracle_from_gpu(case, sim)
+    for s in range(case.steps):
+        rep = sim.step(case.dt)
+        it_o, res_o, _ = o.step(case.dt)
+        if abs(res_o - case.params["tol"]) > 1e-9 * case.params["tol"]:
+            assert rep.iters == it_o, (s, rep.iters, it_o)
+    f = case.tag == 0
+    u = sim.get("VELOCITY")[f]
+    assert np.abs(u - o.get("u")[f]).max() < 1e-8
+    umax = np.linalg.norm(u, axis=1).max()
+    assert umax == pytest.approx(np.exp(-8 * np.pi ** 2 / 100 * case.steps * case.dt), rel=1e-2)
+
+
+# ------------------------------------------------------------------ properties
+def test_step_is_deterministic():
+    case = CASES["db3d_f32"]
+    a, b = gpu_sim(case), gpu_sim(case)
+    for _ in range(3):
+        ra, rb = a.step(case.dt), b.step(case.dt)
+        assert ra.iters == rb.iters and ra.residual == rb.residual
+    for fld in ("POSITION", "VELOCITY", "PRESSURE"):
+        assert np.array_equal(a.get(fld), b.get(fld))
+
+
+def test_edge_single_fluid_particle():
+    # no neighbours: D_ii = 0 -> p = 0; the step still runs
+    from paper_1908_01762_b200 import Simulation, domain, params_from_dict
+    x = np.array([[0.5, 0.5]])
+    sim = Simulation(x, np.zeros((1, 2)), np.ones(1), np.ones(1), np.zeros(1, np.int32), 0.01,
+                     domain(2, [0, 0], [1, 1], [0, 0]), params_from_dict({"precision": 64, "rho0": 1e-9}))
+    sim.set("PRESSURE", np.array([3.0]))
+    rep = sim.step(1e-3)
+    assert rep.iters == 2
+    assert sim.get("PRESSURE")[0] == 0.0
+
+
+def test_edge_fluid_only_ragged_and_max_iter_cap():
+    case = synth.tgv2d(n=23)   # 529 particles: ragged against 128/256-thread blocks
+    sim = gpu_sim(case)
+    o = oracle_from_gpu(case, sim)
+    sim.predict(case.dt)
+    o.predict(case.dt)
+    it_g, res_g = sim.ppe_solve(1e-15, 3)     # non-convergence is not an error
+    it_o, res_o, _ = o.solve(1e-15, 3)
+    assert it_g == it_o == 3 and res_g >= 1e-15
+    assert_close("p", sim.get("PRESSURE"), o.get("p"), 64)
+
+
+def test_eisph_single_sweep():
+    case = CASES["hydro_f64"]
+    sim = gpu_sim(case)
+    sim.predict(case.dt)
+    it, _ = sim.ppe_solve(1e-2, 1)
+    assert it == 1

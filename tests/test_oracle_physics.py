@@ -236,6 +236,9 @@ def test_wall_normals_point_into_fluid(orc):
     assert np.allclose(n[floor1], [0.0, 1.0], atol=1e-12)
     left1 = w & np.isclose(x[:, 0], -0.5 * dx) & (x[:, 1] > 4 * dx) & (x[:, 1] < 0.8 - 4 * dx)
     assert np.allclose(n[left1], [1.0, 0.0], atol=1e-12)
+    # the middle of three layers: the layers above and below cancel -> no normal (R17)
+    floor2 = w & np.isclose(x[:, 1], -1.5 * dx) & (x[:, 0] > 4 * dx) & (x[:, 0] < 0.8 - 4 * dx)
+    assert (n[floor2] == 0).all()
     mag = np.linalg.norm(n[w], axis=1)
     assert np.all((np.abs(mag - 1) < 1e-12) | (mag == 0))
 
