@@ -63,6 +63,10 @@ template <class T> struct Params {
     T rho0, nu, alpha, c_ref, omega, fs_ratio, p_ref;
     T g[3];
     int pgrad, pref_external, ustar_noslip, clamp_wall_p, wall_rho_summation;
+    // GTVF inner list (pairs with r* < 3 h~ + skin; used when h~ < h)
+    int cap_in;
+    float Rin2f;           // (3 h~ + skin)^2 (1 + 2^-10): generous inclusion
+    T skin_half2;          // (skin / 2)^2: allowed squared displacement per particle
 };
 
 // ---------------------------------------------------------------------------
@@ -116,18 +120,24 @@ __device__ __forceinline__ T pair_vec(const Params<T>& P, const V4<T>& a, const 
 // or outside; only the band goes to fp64 (it is also the whole decision in
 // fp64 mode).
 // ---------------------------------------------------------------------------
-template <int D>
-__device__ __forceinline__ bool exact_inside(const Params<float>& P, double xi, double yi, double zi,
-                                             double xj, double yj, double zj)
+// the rare fp32 band case, out of line so the candidate loop stays small;
+// scalars by value (a reference to the kernel-parameter block would force
+// a local copy of it)
+__device__ __forceinline__ double wrap_exact(double d, double L)
 {
-    double d0 = __dadd_rn(xi, -xj), d1 = __dadd_rn(yi, -yj), d2 = D == 3 ? __dadd_rn(zi, -zj) : 0.0;
-    if (P.per[0]) d0 = d0 > P.halfLd[0] ? __dadd_rn(d0, -P.Ld[0]) : (d0 < -P.halfLd[0] ? __dadd_rn(d0, P.Ld[0]) : d0);
-    if (P.per[1]) d1 = d1 > P.halfLd[1] ? __dadd_rn(d1, -P.Ld[1]) : (d1 < -P.halfLd[1] ? __dadd_rn(d1, P.Ld[1]) : d1);
-    if (D == 3 && P.per[2])
-        d2 = d2 > P.halfLd[2] ? __dadd_rn(d2, -P.Ld[2]) : (d2 < -P.halfLd[2] ? __dadd_rn(d2, P.Ld[2]) : d2);
+    double hl = 0.5 * L;
+    return d > hl ? __dadd_rn(d, -L) : (d < -hl ? __dadd_rn(d, L) : d);
+}
+__device__ __noinline__ bool exact_band(double xi, double yi, double zi, double xj, double yj, double zj, double L0,
+                                        double L1, double L2, int pmask, int three, double R2)
+{
+    double d0 = __dadd_rn(xi, -xj), d1 = __dadd_rn(yi, -yj), d2 = three ? __dadd_rn(zi, -zj) : 0.0;
+    if (pmask & 1) d0 = wrap_exact(d0, L0);
+    if (pmask & 2) d1 = wrap_exact(d1, L1);
+    if (three && (pmask & 4)) d2 = wrap_exact(d2, L2);
     double r2 = __dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1));
-    if (D == 3) r2 = __dadd_rn(r2, __dmul_rn(d2, d2));
-    return r2 < P.R2d;
+    if (three) r2 = __dadd_rn(r2, __dmul_rn(d2, d2));
+    return r2 < R2;
 }
 
 template <int D>
@@ -142,26 +152,6 @@ __device__ __forceinline__ bool exact_inside(const Params<double>& P, double xi,
     double r2 = __dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1));
     if (D == 3) r2 = __dadd_rn(r2, __dmul_rn(d2, d2));
     return r2 < P.R2d;
-}
-
-// is j a neighbour of i?  fp32: prefilter + fp64 band; fp64: exact.
-template <int D>
-__device__ __forceinline__ bool is_neighbor(const Params<float>& P, const float4& a, const float4& b)
-{
-    float d0 = a.x - b.x, d1 = a.y - b.y, d2 = D == 3 ? a.z - b.z : 0.f;
-    if (P.per[0]) d0 = wrapd(d0, P.Lf[0], P.halfLf[0]);
-    if (P.per[1]) d1 = wrapd(d1, P.Lf[1], P.halfLf[1]);
-    if (D == 3 && P.per[2]) d2 = wrapd(d2, P.Lf[2], P.halfLf[2]);
-    float r2 = d0 * d0 + d1 * d1;
-    if (D == 3) r2 += d2 * d2;
-    if (r2 < P.R2lo) return true;
-    if (r2 > P.R2hi) return false;
-    return exact_inside<D>(P, (double)a.x, (double)a.y, (double)a.z, (double)b.x, (double)b.y, (double)b.z);
-}
-template <int D>
-__device__ __forceinline__ bool is_neighbor(const Params<double>& P, const dbl4& a, const dbl4& b)
-{
-    return exact_inside<D>(P, a.x, a.y, a.z, b.x, b.y, b.z);
 }
 
 // cell coordinates of a position, fp64 with IEEE division (R27): identical
@@ -203,6 +193,70 @@ __device__ __forceinline__ double warp_max(double v)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
     return v;
+}
+
+// ---------------------------------------------------------------------------
+// Per-pair arithmetic.  fp32: hardware approximations (MUFU rsqrt / rcp,
+// relative error ~2^-22), which is well inside the fp32 parity tolerance;
+// fp64: correctly rounded operations (parity 1e-10 against the oracle).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float frsqrt(float x)
+{
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ double frsqrt(double x) { return 1.0 / sqrt(x); }
+__device__ __forceinline__ float frcp(float x)
+{
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ double frcp(double x) { return 1.0 / x; }
+
+// r and 1/r from r^2 (> 0 for every listed pair; clamped for coincident particles)
+__device__ __forceinline__ void r_of(float r2, float& r, float& ri)
+{
+    float x = fmaxf(r2, 1e-30f);
+    ri = frsqrt(x);
+    r = x * ri;
+}
+__device__ __forceinline__ void r_of(double r2, double& r, double& ri)
+{
+    r = sqrt(r2);
+    ri = r > 0.0 ? 1.0 / r : 0.0;
+}
+
+// neighbour test that also returns an approximation of r^2 (for the inner list)
+template <int D>
+__device__ __forceinline__ bool nb_test(const Params<float>& P, const float4& a, const float4& b, float& r2o)
+{
+    float d0 = a.x - b.x, d1 = a.y - b.y, d2 = D == 3 ? a.z - b.z : 0.f;
+    if (P.per[0]) d0 = wrapd(d0, P.Lf[0], P.halfLf[0]);
+    if (P.per[1]) d1 = wrapd(d1, P.Lf[1], P.halfLf[1]);
+    if (D == 3 && P.per[2]) d2 = wrapd(d2, P.Lf[2], P.halfLf[2]);
+    float r2 = d0 * d0 + d1 * d1;
+    if (D == 3) r2 += d2 * d2;
+    r2o = r2;
+    if (r2 < P.R2lo) return true;
+    if (r2 > P.R2hi) return false;
+    return exact_band((double)a.x, (double)a.y, (double)a.z, (double)b.x, (double)b.y, (double)b.z, P.Ld[0], P.Ld[1],
+                      P.Ld[2], P.per[0] | (P.per[1] << 1) | (P.per[2] << 2), D == 3, P.R2d);
+}
+template <int D>
+__device__ __forceinline__ bool nb_test(const Params<double>& P, const dbl4& a, const dbl4& b, float& r2o)
+{
+    double d0 = a.x - b.x, d1 = a.y - b.y, d2 = D == 3 ? a.z - b.z : 0.0;
+    if (P.per[0]) d0 = wrapd(d0, P.Ld[0], P.halfLd[0]);
+    if (P.per[1]) d1 = wrapd(d1, P.Ld[1], P.halfLd[1]);
+    if (D == 3 && P.per[2]) d2 = wrapd(d2, P.Ld[2], P.halfLd[2]);
+    double r2 = d0 * d0 + d1 * d1;
+    if (D == 3) r2 += d2 * d2;
+    r2o = (float)r2;
+    if (r2 < P.R2d * (1.0 - 1e-9)) return true;
+    if (r2 > P.R2d * (1.0 + 1e-9)) return false;
+    return exact_inside<D>(P, a.x, a.y, a.z, b.x, b.y, b.z);
 }
 
 }  // namespace sb

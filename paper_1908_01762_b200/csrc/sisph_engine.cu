@@ -87,13 +87,16 @@ template <class T, int D> struct Engine : EngineBase {
     // device state
     V *pos = nullptr, *pos_alt = nullptr, *vel = nullptr, *vel_alt = nullptr, *us = nullptr, *us_alt = nullptr;
     V *vt = nullptr, *vt_alt = nullptr, *rn = nullptr, *rstar = nullptr, *nrm = nullptr, *nstmp = nullptr;
-    V *rkA = nullptr, *rkB = nullptr, *vk = nullptr;
+    V *rkA = nullptr, *rkB = nullptr, *vk = nullptr, *dk = nullptr;
     T *p = nullptr, *p_alt = nullptr, *rho = nullptr, *rho_alt = nullptr, *rhs = nullptr, *diag = nullptr;
     uint8_t *fs = nullptr, *fs_alt = nullptr;
     int *pid = nullptr, *pid_alt = nullptr;
     int *keys = nullptr, *rank = nullptr, *perm0 = nullptr, *perm = nullptr;
     int *ccount = nullptr, *fstart = nullptr, *wstart = nullptr, *bsum = nullptr;
     int *nbr = nullptr, *cnt = nullptr;
+    int *nbr_in = nullptr, *cnt_in = nullptr;  // GTVF inner list (h~ < h)
+    bool use_inner = false, inner_valid = false;
+    int64_t gtvf_fallbacks = 0;
     Ctl* ctl = nullptr;
     Ctl* hctl = nullptr;  // pinned host mirror
     double* partials = nullptr;
@@ -103,9 +106,9 @@ template <class T, int D> struct Engine : EngineBase {
 
     ~Engine() override
     {
-        void* ptrs[] = {pos, pos_alt, vel, vel_alt, us, us_alt, vt, vt_alt, rn, rstar, nrm, nstmp, rkA, rkB, vk,
+        void* ptrs[] = {pos, pos_alt, vel, vel_alt, us, us_alt, vt, vt_alt, rn, rstar, nrm, nstmp, rkA, rkB, vk, dk,
                         p, p_alt, rho, rho_alt, rhs, diag, fs, fs_alt, pid, pid_alt, keys, rank, perm0, perm,
-                        ccount, fstart, wstart, bsum, nbr, cnt, ctl, partials, dtmp};
+                        ccount, fstart, wstart, bsum, nbr, cnt, ctl, partials, dtmp, nbr_in, cnt_in};
         if (st) cudaStreamSynchronize(st);
         for (void* q : ptrs)
             if (q) cudaFree(q);
@@ -212,6 +215,14 @@ template <class T, int D> struct Engine : EngineBase {
         max_iter = prm->max_iter;
         tol = prm->tol;
         K = prm->K;
+        // GTVF inner list: worth it when the GTVF kernel support 3 h~ is well inside 3 h
+        {
+            const double ht = prm->h_tilde_factor * h, skin = 0.25 * h;
+            const double rin = 3.0 * ht + skin;
+            use_inner = rin < 0.85 * R && prm->p_ref != 0.0 && prm->K > 0;
+            P.Rin2f = (float)(rin * rin * (1.0 + 1.0 / 1024.0));
+            P.skin_half2 = (T)(0.25 * skin * skin);
+        }
         // ------------------------------------------------ allocation
         int rc = 0;
         size_t NT = (size_t)Ntot, NF = (size_t)std::max(Nf, 1), NW = (size_t)std::max(Nw, 1);
@@ -220,12 +231,12 @@ template <class T, int D> struct Engine : EngineBase {
     if (rc) return rc;
         AL(pos, V, NT) AL(pos_alt, V, NT) AL(vel, V, NT) AL(vel_alt, V, NT) AL(us, V, NT) AL(us_alt, V, NT)
         AL(vt, V, NF) AL(vt_alt, V, NF) AL(rn, V, NF) AL(rstar, V, NF) AL(nrm, V, NW) AL(nstmp, V, NW)
-        AL(rkA, V, NT) AL(rkB, V, NT) AL(vk, V, NF)
+        AL(rkA, V, NT) AL(rkB, V, NT) AL(vk, V, NF) AL(dk, V, NF)
         AL(p, T, NT) AL(p_alt, T, NT) AL(rho, T, NT) AL(rho_alt, T, NT) AL(rhs, T, NF) AL(diag, T, NF)
         AL(fs, uint8_t, NF) AL(fs_alt, uint8_t, NF) AL(pid, int, NT) AL(pid_alt, int, NT)
         AL(keys, int, NT) AL(rank, int, NT) AL(perm0, int, NT) AL(perm, int, NT)
         AL(ccount, int, (size_t)ncells + 1) AL(fstart, int, (size_t)ncells + 1) AL(wstart, int, (size_t)ncells + 1)
-        AL(bsum, int, (size_t)nblk(ncells + 1, SCAN_B) + 1) AL(cnt, int, NT) AL(ctl, Ctl, 1)
+        AL(bsum, int, (size_t)nblk(ncells + 1, SCAN_B) + 1) AL(cnt, int, NT) AL(ctl, Ctl, 1) AL(cnt_in, int, NF)
         AL(partials, double, 2 * (size_t)nblk(Nf, SWEEP_T) + 2) AL(dtmp, double, 3 * (size_t)n)
 #undef AL
         SCK(cudaHostAlloc((void**)&hctl, sizeof(Ctl), cudaHostAllocDefault));
@@ -296,11 +307,18 @@ template <class T, int D> struct Engine : EngineBase {
     int alloc_list(int cap)
     {
         if (nbr) cudaFree(nbr);
-        nbr = nullptr;
+        if (nbr_in) cudaFree(nbr_in);
+        nbr = nbr_in = nullptr;
         int rc = 0;
         nbr = dalloc<int>((size_t)cap * Ntot, err, rc);
         if (rc) return rc;
         P.cap = cap;
+        if (use_inner) {
+            // the inner list holds a subset of each fluid row: the full capacity is an upper bound
+            P.cap_in = cap;
+            nbr_in = dalloc<int>((size_t)cap * std::max(Nf, 1), err, rc);
+            if (rc) return rc;
+        }
         return SISPH_OK;
     }
 
@@ -361,11 +379,14 @@ template <class T, int D> struct Engine : EngineBase {
         G.nf++;
     }
 
-    int build_list()
+    int build_list(bool inner = false)
     {
-        SCK(cudaMemsetAsync(&ctl->max_count, 0, 2 * sizeof(int) + sizeof(unsigned long long), st));
-        ++nlaunch, k_build_list<T, D><<<nblk(Ntot, 128), 128, 0, st>>>(P, pos, fstart, wstart, nbr, cnt, ctl);
+        SCK(cudaMemsetAsync(&ctl->max_count, 0, 2 * sizeof(int) + 2 * sizeof(unsigned long long), st));
+        int* ni = inner && nbr_in ? nbr_in : nullptr;
+        ++nlaunch, k_build_cells<T, D><<<nblk(ncells, BL_WARPS), 32 * BL_WARPS, 0, st>>>(
+            P, ncells, pos, fstart, wstart, nbr, cnt, ni, cnt_in, ctl);
         SCK(cudaGetLastError());
+        inner_valid = ni != nullptr;
         return SISPH_OK;
     }
 
@@ -487,7 +508,7 @@ template <class T, int D> struct Engine : EngineBase {
         std::swap(fs, fs_alt);
         std::swap(p, p_alt);
         std::swap(pid, pid_alt);
-        SRET(build_list());
+        SRET(build_list(true));   // + GTVF inner list
         // A10
         if (Nw) ++nlaunch, k_wall_velocity<T, D><<<nblk(Nw, 256), 256, 0, st>>>(P, pos, nbr, cnt, nrm, us, P.ustar_noslip ? 0 : 1);
         // A11
@@ -559,6 +580,10 @@ template <class T, int D> struct Engine : EngineBase {
         }
         int k = hctl->iter;
         if (k & 1) std::swap(p, p_alt);
+        // p^k's buffer holds fluid p^k; the wall values of the last sweep (from
+        // p^{k-1}, R14) are in the other buffer
+        if (Nw && k > 0)
+            SCK(cudaMemcpyAsync(p + Nf, p_alt + Nf, Nw * sizeof(T), cudaMemcpyDeviceToDevice, st));
         last_ms_sweeps = 0;
         last_sweeps_timed = std::min(k, nrec);
         for (int q = 0; q < last_sweeps_timed; q++) {
@@ -576,6 +601,27 @@ template <class T, int D> struct Engine : EngineBase {
         return SISPH_OK;
     }
 
+    // K modified-GTVF sub-steps (A14) from r* = pos; returns the final positions in rK
+    int gtvf_substeps(T dtau, bool inner, const V*& rK)
+    {
+        ++nlaunch, k_gtvf_prep<T><<<nblk(Ntot, 256), 256, 0, st>>>(pos, rho, Ntot, rkA, rkB);
+        if (inner) SCK(cudaMemsetAsync(&ctl->gtvf_far, 0, sizeof(int), st));
+        const V* src = rkB;
+        for (int k = 0; k < K; k++) {
+            V* dst = (k & 1) ? rkB : rkA;
+            if (inner)
+                ++nlaunch, k_gtvf_substep<T, D><<<nblk(Nf, 128), 128, 0, st>>>(P, dtau, src, dst, vk, dk, p, nbr_in, Nf,
+                                                                               cnt_in, k == 0, pos, 1, ctl);
+            else
+                ++nlaunch, k_gtvf_substep<T, D><<<nblk(Nf, 128), 128, 0, st>>>(P, dtau, src, dst, vk, dk, p, nbr, Ntot,
+                                                                               cnt, k == 0, pos, 0, ctl);
+            src = dst;
+        }
+        SCK(cudaGetLastError());
+        rK = dk;
+        return SISPH_OK;
+    }
+
     int correct(double dt) override
     {
         if (phase != SOLVED) {
@@ -590,16 +636,18 @@ template <class T, int D> struct Engine : EngineBase {
         if (Nw) ++nlaunch, k_wall_pressure<T, D><<<nblk(Nw, 256), 256, 0, st>>>(P, pos, rho, nbr, cnt, p, p_alt, nullptr);
         if (Nf) ++nlaunch, k_pgrad_correct<T, D><<<nblk(Nf, 128), 128, 0, st>>>(P, (T)dt, pos, rho, p, us, nbr, cnt, vel);
         // A14: K sub-steps (p0 = 0 everywhere when p_ref == 0: the shift is exactly zero)
-        const V* rK = pos;
+        const V* rK = nullptr;   // GTVF displacement r^K - r^0 (none when p0 = 0)
         if (P.p_ref != T(0) && K > 0 && Nf) {
-            T dtau = (T)(dt / K);
-            const V* src = pos;
-            for (int k = 0; k < K; k++) {
-                V* dst = (k & 1) ? rkB : rkA;
-                ++nlaunch, k_gtvf_substep<T, D><<<nblk(Nf, 128), 128, 0, st>>>(P, dtau, src, dst, vk, rho, p, nbr, cnt, k == 0);
-                src = dst;
+            SRET(gtvf_substeps((T)(dt / K), inner_valid, rK));
+            if (inner_valid) {
+                // the inner list is exact only while no particle moved more than skin/2
+                SCK(cudaMemcpyAsync(&hctl->gtvf_far, &ctl->gtvf_far, sizeof(int), cudaMemcpyDeviceToHost, st));
+                SCK(cudaStreamSynchronize(st));
+                if (hctl->gtvf_far) {
+                    gtvf_fallbacks++;
+                    SRET(gtvf_substeps((T)(dt / K), false, rK));
+                }
             }
-            rK = src;
         }
         // A15
         if (Nf) ++nlaunch, k_advance<T, D><<<nblk(Nf, 256), 256, 0, st>>>(P, (T)dt, rK, rn, vel, pos, vt);

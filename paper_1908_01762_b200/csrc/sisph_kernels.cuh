@@ -20,6 +20,9 @@ struct Ctl {
     int max_count;             // largest neighbour count of the last build
     int overflow;              // a row exceeded the list capacity
     unsigned long long pairs_fluid;  // sum of neighbour counts over fluid rows of the last build
+    unsigned long long pairs_inner;  // sum of GTVF inner-list counts of the last build
+    int gtvf_far;              // a particle moved more than skin/2 during the GTVF sub-steps
+    int pad2;
 };
 
 // ===========================================================================
@@ -196,74 +199,131 @@ __global__ void k_gather(GatherList G, const int* __restrict__ perm, int n)
 // fluid particles form ONE contiguous slot range (likewise the walls').
 // Slot-major ELL: nbr[k * Ntot + i], k < cnt[i] (coalesced per warp).
 // ===========================================================================
+// One warp per cell: the lanes are the cell's destinations (fluid, then
+// walls, 32 at a time); candidates of each stencil row are staged 32 at a
+// time in shared memory and read back as broadcasts, so every lane tests the
+// same candidate in lockstep (no divergence, one LDS per candidate).
+// Optionally also writes the GTVF inner list (fluid rows; pairs with
+// r^2 < Rin2f, slot-major with stride Nf).
+constexpr int BL_WARPS = 4;
+
 template <class T, int D>
-__device__ __forceinline__ void scan_range(const Params<T>& P, const V4<T>* __restrict__ pos, const V4<T>& xi,
-                                           int i, int a, int b, int* __restrict__ nbr, int& k)
+__device__ __forceinline__ void bl_range(const Params<T>& P, const V4<T>* __restrict__ pos, V4<T>* sm,
+                                         const V4<T>& xi, int i, bool act, int a, int b,
+                                         int* __restrict__ nbr, int& k, int* __restrict__ nbr_in, int& k2)
 {
-    for (int j = a; j < b; j++) {
-        if (j == i) continue;
-        V4<T> xj = ld4(pos + j);
-        if (is_neighbor<D>(P, xi, xj)) {
-            if (k < P.cap) nbr[(size_t)k * P.Ntot + i] = j;
-            k++;
+    const int lane = threadIdx.x & 31;
+    for (int j0 = a; j0 < b; j0 += 32) {
+        int jj = j0 + lane;
+        if (jj < b) sm[lane] = ld4(pos + jj);
+        __syncwarp();
+        int nn = min(32, b - j0);
+        for (int q = 0; q < nn; q++) {
+            V4<T> xj = sm[q];
+            int j = j0 + q;
+            float r2f;
+            bool ok = nb_test<D>(P, xi, xj, r2f);
+            if (act && ok && j != i) {
+                if (k < P.cap) nbr[(size_t)k * P.Ntot + i] = j;
+                k++;
+                if (nbr_in && r2f < P.Rin2f) {
+                    if (k2 < P.cap_in) nbr_in[(size_t)k2 * P.Nf + i] = j;
+                    k2++;
+                }
+            }
         }
+        __syncwarp();
     }
 }
 
 template <class T, int D>
-__global__ void __launch_bounds__(128) k_build_list(Params<T> P, const V4<T>* __restrict__ pos,
-                                                    const int* __restrict__ fstart, const int* __restrict__ wstart,
-                                                    int* __restrict__ nbr, int* __restrict__ cnt, Ctl* ctl)
+__global__ void __launch_bounds__(32 * BL_WARPS) k_build_cells(Params<T> P, int ncells, const V4<T>* __restrict__ pos,
+                                                              const int* __restrict__ fstart,
+                                                              const int* __restrict__ wstart, int* __restrict__ nbr,
+                                                              int* __restrict__ cnt, int* __restrict__ nbr_in,
+                                                              int* __restrict__ cnt_in, Ctl* ctl)
 {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    int k = 0;
-    if (i < P.Ntot) {
-        V4<T> xi = ld4(pos + i);
-        int c[3];
-        cell_of<T, D>(P, xi, c);
-        const int zlo = D == 3 ? -1 : 0, zhi = D == 3 ? 1 : 0;
-        for (int dz = zlo; dz <= zhi; dz++) {
-            int cz = c[2] + dz;
-            if (D == 3) {
-                if (P.per[2]) cz = (cz + P.nc[2]) % P.nc[2];
-                else if (cz < 0 || cz >= P.nc[2]) continue;
-            }
-            for (int dy = -1; dy <= 1; dy++) {
-                int cy = c[1] + dy;
-                if (P.per[1]) cy = (cy + P.nc[1]) % P.nc[1];
-                else if (cy < 0 || cy >= P.nc[1]) continue;
-                int row = P.nc[0] * (cy + P.nc[1] * cz);
-                int x0 = c[0] - 1, x1 = c[0] + 1;
-                if (P.per[0] && (x0 < 0 || x1 >= P.nc[0])) {
-                    // wrapped row: three separate cells
-                    for (int dx = -1; dx <= 1; dx++) {
-                        int cx = (c[0] + dx + P.nc[0]) % P.nc[0];
-                        int key = row + cx;
-                        scan_range<T, D>(P, pos, xi, i, fstart[key], fstart[key + 1], nbr, k);
-                        scan_range<T, D>(P, pos, xi, i, P.Nf + wstart[key], P.Nf + wstart[key + 1], nbr, k);
-                    }
-                } else {
-                    x0 = max(x0, 0);
-                    x1 = min(x1, P.nc[0] - 1);
-                    scan_range<T, D>(P, pos, xi, i, fstart[row + x0], fstart[row + x1 + 1], nbr, k);
-                    scan_range<T, D>(P, pos, xi, i, P.Nf + wstart[row + x0], P.Nf + wstart[row + x1 + 1], nbr, k);
+    constexpr int NROW = D == 3 ? 9 : 3;
+    constexpr int NRNG = NROW * 6;   // per row: up to 3 fluid + 3 wall slot ranges
+    __shared__ V4<T> smem[BL_WARPS][32];
+    __shared__ int2 rng[BL_WARPS][NRNG];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int c = blockIdx.x * BL_WARPS + warp;
+    if (c >= ncells) return;
+    const int fa = fstart[c], nfc = fstart[c + 1] - fa;
+    const int wa = wstart[c], nwc = wstart[c + 1] - wa;
+    const int nd = nfc + nwc;
+    if (nd == 0) return;
+    V4<T>* sm = smem[warp];
+    // lane r < NROW: slot ranges of stencil row r = (dy, dz); in a row the cells
+    // cx-1 .. cx+1 are consecutive keys, so they form one contiguous range
+    // (three separate cells only where a periodic x axis wraps)
+    if (lane < NROW) {
+        const int c0 = c % P.nc[0], c1 = (c / P.nc[0]) % P.nc[1], c2 = c / (P.nc[0] * P.nc[1]);
+        const int dy = lane % 3 - 1, dz = D == 3 ? lane / 3 - 1 : 0;
+        int2* o = rng[warp] + 6 * lane;
+        for (int q = 0; q < 6; q++) o[q] = make_int2(0, 0);
+        int cy = c1 + dy, cz = c2 + dz;
+        bool ok = true;
+        if (P.per[1]) cy = (cy + P.nc[1]) % P.nc[1];
+        else ok = ok && cy >= 0 && cy < P.nc[1];
+        if (D == 3) {
+            if (P.per[2]) cz = (cz + P.nc[2]) % P.nc[2];
+            else ok = ok && cz >= 0 && cz < P.nc[2];
+        }
+        if (ok) {
+            const int row = P.nc[0] * (cy + P.nc[1] * cz);
+            int x0 = c0 - 1, x1 = c0 + 1;
+            if (P.per[0] && (x0 < 0 || x1 >= P.nc[0])) {
+                for (int dx = 0; dx < 3; dx++) {
+                    const int key = row + (c0 + dx - 1 + P.nc[0]) % P.nc[0];
+                    o[dx] = make_int2(fstart[key], fstart[key + 1]);
+                    o[3 + dx] = make_int2(P.Nf + wstart[key], P.Nf + wstart[key + 1]);
                 }
+            } else {
+                x0 = max(x0, 0);
+                x1 = min(x1, P.nc[0] - 1);
+                o[0] = make_int2(fstart[row + x0], fstart[row + x1 + 1]);
+                o[3] = make_int2(P.Nf + wstart[row + x0], P.Nf + wstart[row + x1 + 1]);
             }
         }
-        cnt[i] = k < P.cap ? k : P.cap;
     }
-    // warp max of counts and warp sum of fluid-row counts -> one atomic each
-    int m = k;
-    unsigned sfl = (i < P.Nf) ? (unsigned)min(k, P.cap) : 0u;
+    __syncwarp();
+    int mmax = 0;
+    unsigned sfl = 0, sin_ = 0;
+    for (int base = 0; base < nd; base += 32) {
+        const int t = base + lane;
+        const bool act = t < nd;
+        const int i = !act ? -1 : (t < nfc ? fa + t : P.Nf + wa + (t - nfc));
+        V4<T> xi = ld4(pos + (act ? i : fa));
+        int k = 0, k2 = 0;
+        int* nin = (nbr_in && i < P.Nf) ? nbr_in : nullptr;
+#pragma unroll 1
+        for (int q = 0; q < NRNG; q++) {
+            const int2 ab = rng[warp][q];
+            if (ab.x < ab.y) bl_range<T, D>(P, pos, sm, xi, i, act, ab.x, ab.y, nbr, k, nin, k2);
+        }
+        if (act) {
+            cnt[i] = min(k, P.cap);
+            if (nin) cnt_in[i] = min(k2, P.cap_in);
+            mmax = max(mmax, max(k, nin && k2 > P.cap_in ? P.cap + 1 : 0));
+            if (i < P.Nf) {
+                sfl += (unsigned)min(k, P.cap);
+                sin_ += (unsigned)k2;
+            }
+        }
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-        m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+        mmax = max(mmax, __shfl_xor_sync(0xffffffffu, mmax, o));
         sfl += __shfl_xor_sync(0xffffffffu, sfl, o);
+        sin_ += __shfl_xor_sync(0xffffffffu, sin_, o);
     }
-    if ((threadIdx.x & 31) == 0 && m > 0) {
-        atomicMax(&ctl->max_count, m);
-        if (m > P.cap) atomicExch(&ctl->overflow, 1);
+    if (lane == 0) {
+        atomicMax(&ctl->max_count, mmax);
+        if (mmax > P.cap) atomicExch(&ctl->overflow, 1);
         if (sfl) atomicAdd(&ctl->pairs_fluid, (unsigned long long)sfl);
+        if (sin_) atomicAdd(&ctl->pairs_inner, (unsigned long long)sin_);
     }
 }
 
@@ -284,15 +344,16 @@ __global__ void __launch_bounds__(256) k_density(Params<T> P, const V4<T>* __res
         rho[i] = P.rho0;
         return;
     }
-    T s = xi.w * P.w0;
+    T s = 0;
     int n = cnt[i];
     for (int k = 0; k < n; k++) {
         int j = __ldg(nbr + (size_t)k * P.Ntot + i);
         V4<T> xj = ld4(pos + j);
-        T d[3];
-        T r = my_sqrt(pair_vec<T, D>(P, xi, xj, d));
-        s += xj.w * (P.sig * quintic5(r * P.inv_h));
+        T d[3], r, ri;
+        r_of(pair_vec<T, D>(P, xi, xj, d), r, ri);
+        s += xj.w * quintic5(r * P.inv_h);
     }
+    s = xi.w * P.w0 + P.sig * s;
     rho[i] = s;
     if (i < P.Nf) fs[i] = (s / P.rho0 < P.fs_ratio) ? 1 : 0;
 }
@@ -319,8 +380,8 @@ __global__ void __launch_bounds__(256) k_wall_velocity(Params<T> P, const V4<T>*
         int j = __ldg(nbr + (size_t)k * P.Ntot + i);
         if (j >= P.Nf) continue;
         V4<T> xj = ld4(pos + j);
-        T d[3];
-        T r = my_sqrt(pair_vec<T, D>(P, xi, xj, d));
+        T d[3], r, ri;
+        r_of(pair_vec<T, D>(P, xi, xj, d), r, ri);
         T wv = P.sig2 * quintic5(r * P.inv_h2);
         V4<T> uj = ld4(vel + j);
         ax += uj.x * wv;
@@ -372,22 +433,23 @@ __global__ void __launch_bounds__(128) k_forces_predict(Params<T> P, T dt, const
     T ax = P.g[0], ay = P.g[1], az = D == 3 ? P.g[2] : T(0);
     T dux = uti.x - ui.x, duy = uti.y - ui.y, duz = D == 3 ? uti.z - ui.z : T(0);
     const T nu4 = T(4) * P.nu;
-    const T avf = P.alpha * P.h * P.c_ref;
+    const T avf2 = T(2) * P.alpha * P.h * P.c_ref;   // Pi = -avf phi / rhobar, rhobar = (rho_i + rho_j) / 2
+    const T irhoi = frcp(rhoi);
     int n = cnt[i];
     for (int k = 0; k < n; k++) {
         int j = __ldg(nbr + (size_t)k * P.Ntot + i);
         V4<T> xj = ld4(pos + j), uj = ld4(vel + j);
         T rhoj = __ldg(rho + j);
-        T d[3];
+        T d[3], r, ri;
         T r2 = pair_vec<T, D>(P, xi, xj, d);
-        T r = my_sqrt(r2);
+        r_of(r2, r, ri);
         T dwdr = P.dwk * quintic4(r * P.inv_h);
-        T gf = r > T(0) ? dwdr / r : T(0);           // grad W = gf * r_ij
+        T gf = dwdr * ri;                            // grad_i W_ij = gf * r_ij
         T mj = xj.w;
         T uijx = ui.x - uj.x, uijy = ui.y - uj.y, uijz = D == 3 ? ui.z - uj.z : T(0);
-        T den = r2 + P.eta_h2;
+        T iden = frcp((rhoi + rhoj) * (r2 + P.eta_h2));  // shared by f_visc and f_avisc
         if (P.nu > T(0)) {
-            T f = mj * nu4 / (rhoi + rhoj) * (r * dwdr) / den;
+            T f = mj * nu4 * (r * dwdr) * iden;          // eq:mom:sph:visc
             ax += f * uijx;
             ay += f * uijy;
             if (D == 3) az += f * uijz;
@@ -395,20 +457,19 @@ __global__ void __launch_bounds__(128) k_forces_predict(Params<T> P, T dt, const
         if (P.alpha > T(0)) {
             T vr = uijx * d[0] + uijy * d[1];
             if (D == 3) vr += uijz * d[2];
-            if (vr < T(0)) {
-                T phi = vr / den;
-                T Pi = -avf * phi / (T(0.5) * (rhoi + rhoj));
+            if (vr < T(0)) {                             // eq:mom:sph:av:params (R20)
+                T Pi = -avf2 * vr * iden;
                 T f = mj * Pi * gf;
                 ax -= f * d[0];
                 ay -= f * d[1];
                 if (D == 3) az -= f * d[2];
             }
         }
-        if (j < P.Nf) {
+        if (j < P.Nf) {                                  // eq:mom:sph:gtvf:stress (R21)
             V4<T> utj = ld4(vt + j);
             T gx = gf * d[0], gy = gf * d[1], gz = D == 3 ? gf * d[2] : T(0);
-            T ai = (dux * gx + duy * gy + (D == 3 ? duz * gz : T(0))) / rhoi;
-            T aj = ((utj.x - uj.x) * gx + (utj.y - uj.y) * gy + (D == 3 ? (utj.z - uj.z) * gz : T(0))) / rhoj;
+            T ai = (dux * gx + duy * gy + (D == 3 ? duz * gz : T(0))) * irhoi;
+            T aj = ((utj.x - uj.x) * gx + (utj.y - uj.y) * gy + (D == 3 ? (utj.z - uj.z) * gz : T(0))) * frcp(rhoj);
             ax += mj * (ui.x * ai + uj.x * aj);
             ay += mj * (ui.y * ai + uj.y * aj);
             if (D == 3) az += mj * (ui.z * ai + uj.z * aj);
@@ -445,17 +506,18 @@ __global__ void __launch_bounds__(128) k_rhs_diag(Params<T> P, T inv_dt, const V
             int j = __ldg(nbr + (size_t)k * P.Ntot + i);
             V4<T> xj = ld4(pos + j), uj = ld4(us + j);
             T rhoj = __ldg(rho + j);
-            T d[3];
+            T d[3], r, ri;
             T r2 = pair_vec<T, D>(P, xi, xj, d);
-            T r = my_sqrt(r2);
-            T dwdr = P.dwk * quintic4(r * P.inv_h);
-            T gf = r > T(0) ? dwdr / r : T(0);
+            r_of(r2, r, ri);
+            T p4 = quintic4(r * P.inv_h);
             T mj = xj.w;
             T ud = (ui.x - uj.x) * d[0] + (ui.y - uj.y) * d[1];
             if (D == 3) ud += (ui.z - uj.z) * d[2];
-            sr -= mj / rhoj * inv_dt * (ud * gf);
-            sd += T(4) * mj / (rhoi * (rhoi + rhoj)) * (r * dwdr) / (r2 + P.eta_h2);
+            sr += mj * frcp(rhoj) * (ud * p4 * ri);                        // * (-dwk / dt) below
+            sd += mj * (r * p4) * frcp((rhoi + rhoj) * (r2 + P.eta_h2));   // * 4 dwk / rho_i below
         }
+        sr *= -P.dwk * inv_dt;
+        sd *= T(4) * P.dwk * frcp(rhoi);
         rhs[i] = sr;
         diag[i] = sd;
         if (!fs[i] && sd != T(0)) lam = (double)fabs(sr / sd);
@@ -490,8 +552,8 @@ __global__ void __launch_bounds__(256) k_wall_pressure(Params<T> P, const V4<T>*
         int j = __ldg(nbr + (size_t)k * P.Ntot + i);
         if (j >= P.Nf) continue;
         V4<T> xj = ld4(pos + j);
-        T d[3];
-        T r = my_sqrt(pair_vec<T, D>(P, xi, xj, d));
+        T d[3], r, ri;
+        r_of(pair_vec<T, D>(P, xi, xj, d), r, ri);
         T wv = P.sig * quintic5(r * P.inv_h);
         T rw = __ldg(rho + j) * wv;
         sp += p[j] * wv;
@@ -544,19 +606,20 @@ __global__ void __launch_bounds__(SWEEP_T) k_sweep(Params<T> P, const V4<T>* __r
             T rhoi = rho[i];
             T s = 0;
             int n = cnt[i];
+            const int* __restrict__ row = nbr + i;
             for (int k = 0; k < n; k++) {
-                int j = __ldg(nbr + (size_t)k * P.Ntot + i);
+                int j = __ldg(row + (size_t)k * P.Ntot);
                 V4<T> xj = ld4(pos + j);
                 T rhoj = __ldg(rho + j);
                 T pj = pin[j];
-                T d[3];
+                T d[3], r, ri;
                 T r2 = pair_vec<T, D>(P, xi, xj, d);
-                T r = my_sqrt(r2);
-                T dwdr = P.dwk * quintic4(r * P.inv_h);
-                T fac = T(4) * xj.w / (rhoi * (rhoi + rhoj)) * (r * dwdr) / (r2 + P.eta_h2);
-                s += fac * pj;
+                r_of(r2, r, ri);
+                // fac_ij / (4 dW/dr-scale / rho_i): m_j r poly4(q) / ((rho_i + rho_j)(r^2 + eta h^2))
+                s += (xj.w * r * quintic4(r * P.inv_h) * pj) * frcp((rhoi + rhoj) * (r2 + P.eta_h2));
             }
-            pnew = P.omega * (rhs[i] + s) / di + (T(1) - P.omega) * pold;
+            s *= T(4) * P.dwk * frcp(rhoi);       // S_i = sum_j fac_ij p_j = -sum_j OD_ij p_j
+            pnew = P.omega * (rhs[i] + s) * frcp(di) + (T(1) - P.omega) * pold;
         }
         pout[i] = pnew;
         dn = fabs((double)pnew - (double)pold);
@@ -635,23 +698,27 @@ __global__ void __launch_bounds__(128) k_pgrad_correct(Params<T> P, T dt, const 
     if (i >= P.Nf) return;
     V4<T> xi = ld4(pos + i);
     T rhoi = rho[i], pi = p[i];
-    T pir = pi / (rhoi * rhoi);
+    T irhoi = frcp(rhoi);
+    T pir = pi * irhoi * irhoi;
     T ax = 0, ay = 0, az = 0;
     int n = cnt[i];
     for (int k = 0; k < n; k++) {
         int j = __ldg(nbr + (size_t)k * P.Ntot + i);
         V4<T> xj = ld4(pos + j);
         T rhoj = __ldg(rho + j), pj = __ldg(p + j);
-        T d[3];
-        T r = my_sqrt(pair_vec<T, D>(P, xi, xj, d));
-        T dwdr = P.dwk * quintic4(r * P.inv_h);
-        T gf = r > T(0) ? dwdr / r : T(0);
-        T f = P.pgrad == 0 ? xj.w * (pir + pj / (rhoj * rhoj)) : xj.w / (rhoi * rhoj) * (pj - pi);
+        T d[3], r, ri;
+        r_of(pair_vec<T, D>(P, xi, xj, d), r, ri);
+        T gf = quintic4(r * P.inv_h) * ri;       // * dwk below
+        T irj = frcp(rhoj);
+        T f = P.pgrad == 0 ? xj.w * (pir + pj * irj * irj) : xj.w * irhoi * irj * (pj - pi);
         f *= gf;
         ax -= f * d[0];
         ay -= f * d[1];
         if (D == 3) az -= f * d[2];
     }
+    ax *= P.dwk;
+    ay *= P.dwk;
+    az *= P.dwk;
     V4<T> u = ld4(us + i);
     vel[i] = mk4<T>(u.x + dt * ax, u.y + dt * ay, D == 3 ? u.z + dt * az : T(0), T(0));
 }
@@ -661,27 +728,49 @@ __global__ void __launch_bounds__(128) k_pgrad_correct(Params<T> P, T dt, const 
 // f_GTVF(r^k) = -p0_i sum_j m_j / rho_j^2 gradW(r^k_ij, h~) (eq:mom:sph:gtvf)
 // over the pair set frozen at r* (P:454-456).  p0 per P:389-390 / R22.
 // ===========================================================================
+// rk0 = (r*, m / rho^2) for all particles: the GTVF weight of a source is
+// constant through the sub-steps (rho frozen at stage 1, R5), so it rides in
+// the position vector's 4th lane and costs no extra gather.
+template <class T>
+__global__ void k_gtvf_prep(const V4<T>* __restrict__ pos, const T* __restrict__ rho, int n, V4<T>* __restrict__ a,
+                            V4<T>* __restrict__ b)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    V4<T> x = ld4(pos + i);
+    T r = rho[i];
+    x.w = x.w / (r * r);
+    a[i] = x;
+    if (b) b[i] = x;
+}
+
+// nbr/stride/cnt select the full r* list or the inner list (pairs with
+// r* < 3 h~ + skin).  With the inner list, a particle that has moved more
+// than skin/2 from r* raises ctl->gtvf_far and the host repeats the
+// sub-steps on the full list (exact either way).
+// The displacement delta^k = r^k - r^0 is carried explicitly (same recursion
+// as eq:int:gtvf:pos), so that eq:int:vhatnp2's (r^K - r^0)/dt does not lose
+// its digits to a difference of two positions in fp32.
 template <class T, int D>
 __global__ void __launch_bounds__(128) k_gtvf_substep(Params<T> P, T dtau, const V4<T>* __restrict__ rk,
                                                       V4<T>* __restrict__ rk1, V4<T>* __restrict__ vk,
-                                                      const T* __restrict__ rho, const T* __restrict__ p,
-                                                      const int* __restrict__ nbr, const int* __restrict__ cnt,
-                                                      int first)
+                                                      V4<T>* __restrict__ dk, const T* __restrict__ p,
+                                                      const int* __restrict__ nbr, int stride,
+                                                      const int* __restrict__ cnt, int first,
+                                                      const V4<T>* __restrict__ rstar, int check, Ctl* ctl)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= P.Nf) return;
     V4<T> xi = ld4(rk + i);
     T ax = 0, ay = 0, az = 0;
     int n = cnt[i];
+    const int* __restrict__ row = nbr + i;
     for (int k = 0; k < n; k++) {
-        int j = __ldg(nbr + (size_t)k * P.Ntot + i);
+        int j = __ldg(row + (size_t)k * stride);
         V4<T> xj = ld4(rk + j);
-        T rhoj = __ldg(rho + j);
-        T d[3];
-        T r = my_sqrt(pair_vec<T, D>(P, xi, xj, d));
-        T dwdr = P.dwkt * quintic4(r * P.inv_ht);
-        T gf = r > T(0) ? dwdr / r : T(0);
-        T f = xj.w / (rhoj * rhoj) * gf;
+        T d[3], r, ri;
+        r_of(pair_vec<T, D>(P, xi, xj, d), r, ri);
+        T f = xj.w * quintic4(r * P.inv_ht) * ri;   // m_j / rho_j^2 * |gradW| / r (dwkt below)
         ax += f * d[0];
         ay += f * d[1];
         if (D == 3) az += f * d[2];
@@ -691,14 +780,21 @@ __global__ void __launch_bounds__(128) k_gtvf_substep(Params<T> P, T dtau, const
         T v = T(10) * fabs(p[i]);
         p0 = v < P.p_ref ? v : P.p_ref;
     }
-    ax *= -p0;
-    ay *= -p0;
-    az *= -p0;
-    V4<T> v = first ? mk4<T>(T(0), T(0), T(0), T(0)) : ld4(vk + i);
+    const T s = -p0 * P.dwkt;
+    ax *= s;
+    ay *= s;
+    az *= s;
+    const V4<T> zero = mk4<T>(T(0), T(0), T(0), T(0));
+    V4<T> v = first ? zero : ld4(vk + i);
+    V4<T> dl = first ? zero : ld4(dk + i);
     T h2 = T(0.5) * dtau * dtau;
-    rk1[i] = mk4<T>(xi.x + dtau * v.x + h2 * ax, xi.y + dtau * v.y + h2 * ay,
-                    D == 3 ? xi.z + dtau * v.z + h2 * az : xi.z, xi.w);
+    dl = mk4<T>(dl.x + dtau * v.x + h2 * ax, dl.y + dtau * v.y + h2 * ay, D == 3 ? dl.z + dtau * v.z + h2 * az : T(0),
+                T(0));
+    V4<T> r0 = ld4(rstar + i);
+    rk1[i] = mk4<T>(r0.x + dl.x, r0.y + dl.y, D == 3 ? r0.z + dl.z : xi.z, xi.w);
+    dk[i] = dl;
     vk[i] = mk4<T>(v.x + dtau * ax, v.y + dtau * ay, D == 3 ? v.z + dtau * az : T(0), T(0));
+    if (check && dl.x * dl.x + dl.y * dl.y + dl.z * dl.z > P.skin_half2) atomicExch(&ctl->gtvf_far, 1);
 }
 
 // ===========================================================================
@@ -706,14 +802,15 @@ __global__ void __launch_bounds__(128) k_gtvf_substep(Params<T> P, T dtau, const
 // (eq:int:rnp2, R24), periodic wrap.
 // ===========================================================================
 template <class T, int D>
-__global__ void k_advance(Params<T> P, T dt, const V4<T>* __restrict__ rK, const V4<T>* __restrict__ rn,
+__global__ void k_advance(Params<T> P, T dt, const V4<T>* __restrict__ dK, const V4<T>* __restrict__ rn,
                           const V4<T>* __restrict__ vel, V4<T>* __restrict__ pos, V4<T>* __restrict__ vt)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= P.Nf) return;
-    V4<T> r0 = ld4(pos + i), rk = ld4(rK + i), x = ld4(rn + i), u = ld4(vel + i), ut = ld4(vt + i);
-    T tx = u.x + (rk.x - r0.x) / dt, ty = u.y + (rk.y - r0.y) / dt;
-    T tz = D == 3 ? u.z + (rk.z - r0.z) / dt : T(0);
+    V4<T> x = ld4(rn + i), u = ld4(vel + i), ut = ld4(vt + i);
+    V4<T> dl = dK ? ld4(dK + i) : mk4<T>(T(0), T(0), T(0), T(0));   // r^K - r^0
+    T tx = u.x + dl.x / dt, ty = u.y + dl.y / dt;
+    T tz = D == 3 ? u.z + dl.z / dt : T(0);
     T hd = T(0.5) * dt;
     T X = x.x + hd * (tx + ut.x), Y = x.y + hd * (ty + ut.y), Z = D == 3 ? x.z + hd * (tz + ut.z) : x.z;
     if (P.per[0]) { if (X >= P.hi[0]) X -= P.L[0]; else if (X < P.lo[0]) X += P.L[0]; }
