@@ -128,7 +128,7 @@ __device__ __forceinline__ double wrap_exact(double d, double L)
     double hl = 0.5 * L;
     return d > hl ? __dadd_rn(d, -L) : (d < -hl ? __dadd_rn(d, L) : d);
 }
-__device__ __noinline__ bool exact_band(double xi, double yi, double zi, double xj, double yj, double zj, double L0,
+__device__ __forceinline__ bool exact_band(double xi, double yi, double zi, double xj, double yj, double zj, double L0,
                                         double L1, double L2, int pmask, int three, double R2)
 {
     double d0 = __dadd_rn(xi, -xj), d1 = __dadd_rn(yi, -yj), d2 = three ? __dadd_rn(zi, -zj) : 0.0;

@@ -207,30 +207,63 @@ __global__ void k_gather(GatherList G, const int* __restrict__ perm, int n)
 // r^2 < Rin2f, slot-major with stride Nf).
 constexpr int BL_WARPS = 4;
 
+// Candidates of one slot range are staged 32 at a time with the range's
+// periodic image shift (sx, sy, sz) already applied, so the fast test is a
+// plain difference.  Pairs whose fp32 r^2 falls in the +-2^-12 band around
+// R^2 (or every pair in fp64 mode) are decided exactly (R2) from the
+// unshifted positions with the oracle's minimum-image arithmetic.
+struct BLState {
+    int k, k2;          // list lengths so far
+    int off, off2;      // running store offsets k * Ntot, k2 * Nf
+};
+
 template <class T, int D>
-__device__ __forceinline__ void bl_range(const Params<T>& P, const V4<T>* __restrict__ pos, V4<T>* sm,
-                                         const V4<T>& xi, int i, bool act, int a, int b,
-                                         int* __restrict__ nbr, int& k, int* __restrict__ nbr_in, int& k2)
+__device__ __forceinline__ void bl_range(const Params<T>& P, const V4<T>* __restrict__ pos, V4<T>* sm, V4<T>* smo,
+                                         const V4<T>& xi, int i, bool act, int a, int b, T sx, T sy, T sz,
+                                         int* __restrict__ nbr, int* __restrict__ nbr_in, BLState& S,
+                                         float R2lo, float R2hi, float Rin2)
 {
     const int lane = threadIdx.x & 31;
+    const int cap = P.cap, cap_in = P.cap_in, Ntot = P.Ntot, Nf = P.Nf;
+    const int pmask = P.per[0] | (P.per[1] << 1) | (P.per[2] << 2);
+    const double xid = (double)xi.x, yid = (double)xi.y, zid = (double)xi.z;
     for (int j0 = a; j0 < b; j0 += 32) {
         int jj = j0 + lane;
-        if (jj < b) sm[lane] = ld4(pos + jj);
+        if (jj < b) {
+            V4<T> v = ld4(pos + jj);
+            smo[lane] = v;
+            v.x += sx;
+            v.y += sy;
+            if (D == 3) v.z += sz;
+            sm[lane] = v;
+        }
         __syncwarp();
-        int nn = min(32, b - j0);
+        const int nn = min(32, b - j0);
         for (int q = 0; q < nn; q++) {
-            V4<T> xj = sm[q];
-            int j = j0 + q;
-            float r2f;
-            bool ok = nb_test<D>(P, xi, xj, r2f);
-            if (act && ok && j != i) {
-                if (k < P.cap) nbr[(size_t)k * P.Ntot + i] = j;
-                k++;
-                if (nbr_in && r2f < P.Rin2f) {
-                    if (k2 < P.cap_in) nbr_in[(size_t)k2 * P.Nf + i] = j;
-                    k2++;
-                }
+            const V4<T> xj = sm[q];
+            const int j = j0 + q;
+            const float dx = (float)(xi.x - xj.x), dy = (float)(xi.y - xj.y);
+            const float dz = D == 3 ? (float)(xi.z - xj.z) : 0.f;
+            float r2 = dx * dx + dy * dy;
+            if (D == 3) r2 += dz * dz;
+            bool in = r2 < R2lo;
+            const bool band = !in && r2 <= R2hi;
+            // exact ties (lattices!) are common: the fp64 decision on the unshifted
+            // positions runs inline and predicated, once per candidate for the warp
+            if (__any_sync(0xffffffffu, band)) {
+                const V4<T> o = smo[q];
+                const bool ex = exact_band(xid, yid, zid, (double)o.x, (double)o.y, (double)o.z, P.Ld[0], P.Ld[1],
+                                           P.Ld[2], pmask, D == 3, P.R2d);
+                in = band ? ex : in;
             }
+            const bool acc = act && in && j != i;
+            if (acc && S.k < cap) nbr[S.off + i] = j;
+            S.k += acc ? 1 : 0;
+            S.off += acc ? Ntot : 0;
+            const bool ai = acc && r2 < Rin2;
+            if (ai && S.k2 < cap_in) nbr_in[S.off2 + i] = j;
+            S.k2 += ai ? 1 : 0;
+            S.off2 += ai ? Nf : 0;
         }
         __syncwarp();
     }
@@ -245,8 +278,8 @@ __global__ void __launch_bounds__(32 * BL_WARPS) k_build_cells(Params<T> P, int 
 {
     constexpr int NROW = D == 3 ? 9 : 3;
     constexpr int NRNG = NROW * 6;   // per row: up to 3 fluid + 3 wall slot ranges
-    __shared__ V4<T> smem[BL_WARPS][32];
-    __shared__ int2 rng[BL_WARPS][NRNG];
+    __shared__ V4<T> smem[BL_WARPS][32], smemo[BL_WARPS][32];
+    __shared__ int4 rng[BL_WARPS][NRNG];   // (first slot, end slot, image shift code, -)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c = blockIdx.x * BL_WARPS + warp;
     if (c >= ncells) return;
@@ -255,36 +288,46 @@ __global__ void __launch_bounds__(32 * BL_WARPS) k_build_cells(Params<T> P, int 
     const int nd = nfc + nwc;
     if (nd == 0) return;
     V4<T>* sm = smem[warp];
+    V4<T>* smo = smemo[warp];
     // lane r < NROW: slot ranges of stencil row r = (dy, dz); in a row the cells
     // cx-1 .. cx+1 are consecutive keys, so they form one contiguous range
     // (three separate cells only where a periodic x axis wraps)
+    // image shift code: 2 bits per axis, value s + 1 for a shift of s L (s in -1, 0, 1)
     if (lane < NROW) {
         const int c0 = c % P.nc[0], c1 = (c / P.nc[0]) % P.nc[1], c2 = c / (P.nc[0] * P.nc[1]);
         const int dy = lane % 3 - 1, dz = D == 3 ? lane / 3 - 1 : 0;
-        int2* o = rng[warp] + 6 * lane;
-        for (int q = 0; q < 6; q++) o[q] = make_int2(0, 0);
+        int4* o = rng[warp] + 6 * lane;
+        for (int q = 0; q < 6; q++) o[q] = make_int4(0, 0, 0, 0);
         int cy = c1 + dy, cz = c2 + dz;
+        int code = 1 | (1 << 2) | (1 << 4);
         bool ok = true;
-        if (P.per[1]) cy = (cy + P.nc[1]) % P.nc[1];
-        else ok = ok && cy >= 0 && cy < P.nc[1];
+        if (P.per[1]) {
+            if (cy < 0) { cy += P.nc[1]; code += (-1) << 2; }        // candidate row is the image below
+            else if (cy >= P.nc[1]) { cy -= P.nc[1]; code += 1 << 2; }
+        } else ok = ok && cy >= 0 && cy < P.nc[1];
         if (D == 3) {
-            if (P.per[2]) cz = (cz + P.nc[2]) % P.nc[2];
-            else ok = ok && cz >= 0 && cz < P.nc[2];
+            if (P.per[2]) {
+                if (cz < 0) { cz += P.nc[2]; code += (-1) << 4; }
+                else if (cz >= P.nc[2]) { cz -= P.nc[2]; code += 1 << 4; }
+            } else ok = ok && cz >= 0 && cz < P.nc[2];
         }
         if (ok) {
             const int row = P.nc[0] * (cy + P.nc[1] * cz);
             int x0 = c0 - 1, x1 = c0 + 1;
             if (P.per[0] && (x0 < 0 || x1 >= P.nc[0])) {
                 for (int dx = 0; dx < 3; dx++) {
-                    const int key = row + (c0 + dx - 1 + P.nc[0]) % P.nc[0];
-                    o[dx] = make_int2(fstart[key], fstart[key + 1]);
-                    o[3 + dx] = make_int2(P.Nf + wstart[key], P.Nf + wstart[key + 1]);
+                    int cx = c0 + dx - 1, cd = code;
+                    if (cx < 0) { cx += P.nc[0]; cd -= 1; }
+                    else if (cx >= P.nc[0]) { cx -= P.nc[0]; cd += 1; }
+                    const int key = row + cx;
+                    o[dx] = make_int4(fstart[key], fstart[key + 1], cd, 0);
+                    o[3 + dx] = make_int4(P.Nf + wstart[key], P.Nf + wstart[key + 1], cd, 0);
                 }
             } else {
                 x0 = max(x0, 0);
                 x1 = min(x1, P.nc[0] - 1);
-                o[0] = make_int2(fstart[row + x0], fstart[row + x1 + 1]);
-                o[3] = make_int2(P.Nf + wstart[row + x0], P.Nf + wstart[row + x1 + 1]);
+                o[0] = make_int4(fstart[row + x0], fstart[row + x1 + 1], code, 0);
+                o[3] = make_int4(P.Nf + wstart[row + x0], P.Nf + wstart[row + x1 + 1], code, 0);
             }
         }
     }
@@ -296,16 +339,25 @@ __global__ void __launch_bounds__(32 * BL_WARPS) k_build_cells(Params<T> P, int 
         const bool act = t < nd;
         const int i = !act ? -1 : (t < nfc ? fa + t : P.Nf + wa + (t - nfc));
         V4<T> xi = ld4(pos + (act ? i : fa));
-        int k = 0, k2 = 0;
-        int* nin = (nbr_in && i < P.Nf) ? nbr_in : nullptr;
+        BLState S{0, 0, 0, 0};
+        // wall destinations get no inner list (a warp's lanes may mix fluid and walls:
+        // the pointer stays uniform, the per-lane test below excludes wall rows)
+        int* nin = nbr_in;
+        const float Rin2 = (nin && i < P.Nf) ? P.Rin2f : -1.f;
+        const float R2lo = P.R2lo, R2hi = P.R2hi;
 #pragma unroll 1
         for (int q = 0; q < NRNG; q++) {
-            const int2 ab = rng[warp][q];
-            if (ab.x < ab.y) bl_range<T, D>(P, pos, sm, xi, i, act, ab.x, ab.y, nbr, k, nin, k2);
+            const int4 ab = rng[warp][q];
+            if (ab.x < ab.y) {
+                const T sx = (T)((ab.z & 3) - 1) * P.L[0], sy = (T)(((ab.z >> 2) & 3) - 1) * P.L[1];
+                const T sz = (T)(((ab.z >> 4) & 3) - 1) * P.L[2];
+                bl_range<T, D>(P, pos, sm, smo, xi, i, act, ab.x, ab.y, sx, sy, sz, nbr, nin, S, R2lo, R2hi, Rin2);
+            }
         }
+        const int k = S.k, k2 = S.k2;
         if (act) {
             cnt[i] = min(k, P.cap);
-            if (nin) cnt_in[i] = min(k2, P.cap_in);
+            if (nin && i < P.Nf) cnt_in[i] = min(k2, P.cap_in);
             mmax = max(mmax, max(k, nin && k2 > P.cap_in ? P.cap + 1 : 0));
             if (i < P.Nf) {
                 sfl += (unsigned)min(k, P.cap);
