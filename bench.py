@@ -153,26 +153,28 @@ def sweep_traffic():
     return None
 
 
-def cpu_baseline(name, max_seconds=15.0):
-    """The oracle as it stands, on a bounded sample, on all host cores (fp64)."""
+def cpu_baseline(name, max_seconds=20.0):
+    """The oracle as it stands, on a bounded sample, on all host cores (fp64):
+    whole SISPH steps, same metric definition as `value`."""
     import oracle
-    import synth  # noqa: F401
     oracle.build()
     case, desc = sample_case(name)
     o = oracle.Sim(case)
-    o.predict(case.dt)
+    o.step(case.dt)   # untimed first step (allocations)
+    sweeps, steps = 0, 0
     t0 = time.perf_counter()
-    o.solve(0.0, 1)
-    t1 = time.perf_counter() - t0
-    S = int(max(1, min(20, max_seconds / max(t1, 1e-6))))
-    o.predict(case.dt)
-    t0 = time.perf_counter()
-    it, _, _ = o.solve(0.0, S)
-    t = time.perf_counter() - t0
+    while True:
+        it, _, _ = o.step(case.dt)
+        sweeps += it
+        steps += 1
+        t = time.perf_counter() - t0
+        if t > max_seconds or steps >= 50:
+            break
     cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count()))
-    return {"value": it * case.n_fluid / t, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{desc}: {it} Jacobi sweeps (PPE phase only) over {case.n_fluid} fluid particles, "
-                      f"{t:.1f} s, fp64"}
+    return {"value": sweeps * case.n_fluid / t, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "ms_per_step": 1e3 * t / steps,
+            "sample": f"{desc}: {steps} full SISPH steps ({sweeps} PPE sweeps) over {case.n_fluid} fluid "
+                      f"particles, {t:.1f} s, fp64"}
 
 
 def emit(d):
