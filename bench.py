@@ -261,6 +261,7 @@ def run_sisph(args):
                    "parallelism": f"slab x{world}"},
         "ppe_phase_particle_sweeps_per_s": sweeps * nf * world / (ms_solve / 1e3),
         "sweeps_per_step": sweeps / args.steps,
+        "single_build_steps": sum(r.single_build for r in reps),
         "ms_per_step_phases": {"predict": sum(r.ms_predict for r in reps) / args.steps,
                                "solve": ms_solve / args.steps,
                                "correct": sum(r.ms_correct for r in reps) / args.steps},

@@ -78,6 +78,9 @@ typedef struct {
     int nbr_cap;            /* neighbour-list capacity per particle, 0 = automatic */
     int device;             /* CUDA device ordinal, -1 = current device */
     void* stream;           /* cudaStream_t to run on, NULL = the handle creates one */
+    int rebuild_mode;       /* 0 (default): one build per step at r^n with a skin of
+                               2 dt max|u~| and the r* sets filtered out of it (R3) when the
+                               skin fits the grid; 1: two exact builds (at r^n and r*) */
 } sisph_params;
 
 /* Per-step report (sisph_step).  Timings are device milliseconds measured
@@ -93,6 +96,8 @@ typedef struct {
     double ms_sweeps;       /* device ms of the Jacobi sweep kernels that did work (timing mode) */
     int sweeps_timed;       /* number of sweep launches ms_sweeps covers */
     int64_t launches;       /* kernel launches this step issued (speculative no-op sweeps included) */
+    int single_build;       /* 1 if this step used the single build + filter (R3) */
+    double skin_radius;     /* loose radius 3h + skin of that build (0 otherwise) */
 } sisph_step_report;
 
 typedef enum {
@@ -141,7 +146,9 @@ int sisph_build_neighbors(sisph_t* s);
 
 /* Algorithm 1 lines 2-6 plus the PPE set-up: build at r^n,
  * summation density + free-surface flags (A6), wall ghost velocity (A7),
- * forces and predictors u*, r* (A8), build at r* (A9), wall u* (A10),
+ * forces and predictors u*, r* (A8), neighbour sets at r* (A9: a second exact
+ * build, or — default, R3 — the exact r* sets filtered out of a loose list
+ * built once at r^n with radius 3h + 2 dt max|u~|), wall u* (A10),
  * RHS_i, D_ii and Lambda (A11).  Errors: SISPH_EINVAL if dt <= 0. */
 int sisph_predict(sisph_t* s, double dt);
 

@@ -67,6 +67,9 @@ template <class T> struct Params {
     int cap_in;
     float Rin2f;           // (3 h~ + skin)^2 (1 + 2^-10): generous inclusion
     T skin_half2;          // (skin / 2)^2: allowed squared displacement per particle
+    // loose (superset) radius^2 of the single per-step build at r^n (R3):
+    // (3h + 2 dt max|u~| + margin)^2 (1 + 2^-10), working precision
+    T Rs2;
 };
 
 // ---------------------------------------------------------------------------

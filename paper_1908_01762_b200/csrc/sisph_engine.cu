@@ -95,6 +95,17 @@ template <class T, int D> struct Engine : EngineBase {
     int *ccount = nullptr, *fstart = nullptr, *wstart = nullptr, *bsum = nullptr;
     int *nbr = nullptr, *cnt = nullptr;
     int *nbr_in = nullptr, *cnt_in = nullptr;  // GTVF inner list (h~ < h)
+    // single per-step build (R3): loose list at r^n on the skin geometry PS,
+    // walls binned for PS through wperm_s / wstart_s (recomputed when PS's grid changes)
+    int *nbs = nullptr, *cnt_s = nullptr;
+    int cap_s = 0;
+    int *wperm_s = nullptr, *wstart_s = nullptr;
+    int wnc_s[3] = {-1, -1, -1};
+    Params<T> PS;
+    int rebuild_mode = 0;   // 0: single build + filter when the skin fits, 1: always two exact builds
+    bool skin_used = false;
+    double skin_radius = 0;
+    double extent = 0;      // max |coordinate| of the domain (rounding margin of the skin)
     bool use_inner = false, inner_valid = false;
     int64_t gtvf_fallbacks = 0;
     Ctl* ctl = nullptr;
@@ -108,7 +119,8 @@ template <class T, int D> struct Engine : EngineBase {
     {
         void* ptrs[] = {pos, pos_alt, vel, vel_alt, us, us_alt, vt, vt_alt, rn, rstar, nrm, nstmp, rkA, rkB, vk, dk,
                         p, p_alt, rho, rho_alt, rhs, diag, fs, fs_alt, pid, pid_alt, keys, rank, perm0, perm,
-                        ccount, fstart, wstart, bsum, nbr, cnt, ctl, partials, dtmp, nbr_in, cnt_in};
+                        ccount, fstart, wstart, bsum, nbr, cnt, ctl, partials, dtmp, nbr_in, cnt_in,
+                        nbs, cnt_s, wperm_s, wstart_s};
         if (st) cudaStreamSynchronize(st);
         for (void* q : ptrs)
             if (q) cudaFree(q);
@@ -211,6 +223,8 @@ template <class T, int D> struct Engine : EngineBase {
         P.ustar_noslip = prm->ustar_noslip;
         P.clamp_wall_p = prm->clamp_wall_p;
         P.wall_rho_summation = prm->wall_rho_summation;
+        rebuild_mode = prm->rebuild_mode;
+        for (int a = 0; a < D; a++) extent = std::max(extent, std::max(fabs(dom->lo[a]), fabs(dom->hi[a])));
         min_iter = prm->min_iter;
         max_iter = prm->max_iter;
         tol = prm->tol;
@@ -230,13 +244,14 @@ template <class T, int D> struct Engine : EngineBase {
     ptr = dalloc<Ty>((cntx), err, rc);       \
     if (rc) return rc;
         AL(pos, V, NT) AL(pos_alt, V, NT) AL(vel, V, NT) AL(vel_alt, V, NT) AL(us, V, NT) AL(us_alt, V, NT)
-        AL(vt, V, NF) AL(vt_alt, V, NF) AL(rn, V, NF) AL(rstar, V, NF) AL(nrm, V, NW) AL(nstmp, V, NW)
+        AL(vt, V, NF) AL(vt_alt, V, NF) AL(rn, V, NT) AL(rstar, V, NT) AL(nrm, V, NW) AL(nstmp, V, NW)
         AL(rkA, V, NT) AL(rkB, V, NT) AL(vk, V, NF) AL(dk, V, NF)
         AL(p, T, NT) AL(p_alt, T, NT) AL(rho, T, NT) AL(rho_alt, T, NT) AL(rhs, T, NF) AL(diag, T, NF)
         AL(fs, uint8_t, NF) AL(fs_alt, uint8_t, NF) AL(pid, int, NT) AL(pid_alt, int, NT)
         AL(keys, int, NT) AL(rank, int, NT) AL(perm0, int, NT) AL(perm, int, NT)
         AL(ccount, int, (size_t)ncells + 1) AL(fstart, int, (size_t)ncells + 1) AL(wstart, int, (size_t)ncells + 1)
         AL(bsum, int, (size_t)nblk(ncells + 1, SCAN_B) + 1) AL(cnt, int, NT) AL(ctl, Ctl, 1) AL(cnt_in, int, NF)
+        AL(cnt_s, int, NT) AL(wperm_s, int, NW) AL(wstart_s, int, (size_t)ncells + 1)
         AL(partials, double, 2 * (size_t)nblk(Nf, SWEEP_T) + 2) AL(dtmp, double, 3 * (size_t)n)
 #undef AL
         SCK(cudaHostAlloc((void**)&hctl, sizeof(Ctl), cudaHostAllocDefault));
@@ -277,6 +292,7 @@ template <class T, int D> struct Engine : EngineBase {
         // ------------------------------------------------ capacity, walls, first build, normals
         int cap = prm->nbr_cap;
         if (cap <= 0) cap = D == 2 ? 48 : 160;
+        cap = (cap + 3) / 4 * 4;   // blocked ELL stores 16-byte chunks of 4 entries
         SRET(alloc_list(cap));
         SRET(setup_walls());
         if (prm->nbr_cap <= 0) {
@@ -310,17 +326,19 @@ template <class T, int D> struct Engine : EngineBase {
         if (nbr_in) cudaFree(nbr_in);
         nbr = nbr_in = nullptr;
         int rc = 0;
-        nbr = dalloc<int>((size_t)cap * Ntot, err, rc);
+        nbr = dalloc<int>((size_t)cap * rows32(Ntot), err, rc);
         if (rc) return rc;
         P.cap = cap;
         if (use_inner) {
             // the inner list holds a subset of each fluid row: the full capacity is an upper bound
             P.cap_in = cap;
-            nbr_in = dalloc<int>((size_t)cap * std::max(Nf, 1), err, rc);
+            nbr_in = dalloc<int>((size_t)cap * rows32(Nf), err, rc);
             if (rc) return rc;
         }
         return SISPH_OK;
     }
+
+    static size_t rows32(int n) { return ((size_t)std::max(n, 1) + 31) / 32 * 32; }
 
     int check_overflow()
     {
@@ -347,14 +365,18 @@ template <class T, int D> struct Engine : EngineBase {
 
     // A1 + A2 + A4: stable counting sort of n particles at xs by cell key;
     // writes start[0..ncells] and perm_out[0..n) (relative slots)
-    int sort_set(const V* xs, int nn, int* start, int* perm_out)
+    static int ncells_of(const Params<T>& G) { return G.nc[0] * G.nc[1] * G.nc[2]; }
+
+    int sort_set(const V* xs, int nn, int* start, int* perm_out) { return sort_set(P, xs, nn, start, perm_out); }
+    int sort_set(const Params<T>& G, const V* xs, int nn, int* start, int* perm_out)
     {
-        SCK(cudaMemsetAsync(ccount, 0, ((size_t)ncells + 1) * sizeof(int), st));
+        const int nc = ncells_of(G);
+        SCK(cudaMemsetAsync(ccount, 0, ((size_t)nc + 1) * sizeof(int), st));
         if (nn > 0) {
-            ++nlaunch, k_hash_count<T, D><<<nblk(nn, 256), 256, 0, st>>>(P, xs, nn, keys, rank, ccount);
+            ++nlaunch, k_hash_count<T, D><<<nblk(nn, 256), 256, 0, st>>>(G, xs, nn, keys, rank, ccount);
             SCK(cudaGetLastError());
         }
-        SRET(scan(ccount, start, ncells + 1));
+        SRET(scan(ccount, start, nc + 1));
         if (nn > 0) {
             ++nlaunch, k_scatter<<<nblk(nn, 256), 256, 0, st>>>(keys, rank, start, perm0, nn);
             ++nlaunch, k_stabilize<<<nblk(nn, 256), 256, 0, st>>>(perm0, keys, start, perm_out, nn);
@@ -384,9 +406,92 @@ template <class T, int D> struct Engine : EngineBase {
         SCK(cudaMemsetAsync(&ctl->max_count, 0, 2 * sizeof(int) + 2 * sizeof(unsigned long long), st));
         int* ni = inner && nbr_in ? nbr_in : nullptr;
         ++nlaunch, k_build_cells<T, D><<<nblk(ncells, BL_WARPS), 32 * BL_WARPS, 0, st>>>(
-            P, ncells, pos, fstart, wstart, nbr, cnt, ni, cnt_in, ctl);
+            P, ncells, pos, fstart, wstart, nullptr, nbr, cnt, ni, cnt_in, ctl);
         SCK(cudaGetLastError());
         inner_valid = ni != nullptr;
+        return SISPH_OK;
+    }
+
+    // loose list at the current positions on the skin geometry PS (R3)
+    int build_loose()
+    {
+        SCK(cudaMemsetAsync(&ctl->max_count, 0, 2 * sizeof(int) + 2 * sizeof(unsigned long long), st));
+        const int nc = ncells_of(PS);
+        ++nlaunch, k_build_loose<T, D><<<nblk(nc, BL_WARPS), 32 * BL_WARPS, 0, st>>>(
+            PS, nc, pos, fstart, wstart_s, Nw ? wperm_s : nullptr, nbs, cnt_s, ctl);
+        SCK(cudaGetLastError());
+        return SISPH_OK;
+    }
+
+    // exact sets at the current positions out of the loose list (+ GTVF inner list)
+    int filter_list()
+    {
+        // keep the overflow flag of the loose build; reset the statistics
+        SCK(cudaMemsetAsync(&ctl->max_count, 0, sizeof(int), st));
+        SCK(cudaMemsetAsync(&ctl->pairs_fluid, 0, 2 * sizeof(unsigned long long), st));
+        int* ni = nbr_in;
+        ++nlaunch, k_filter<T, D><<<nblk(Ntot, 128), 128, 0, st>>>(P, pos, nbs, cnt_s, cap_s, nbr, cnt, ni, cnt_in, ctl);
+        SCK(cudaGetLastError());
+        inner_valid = ni != nullptr;
+        return SISPH_OK;
+    }
+
+    // Decide whether this step can use the single build: skin s = 2 dt max|u~|
+    // (+ a rounding margin); the skin geometry has cells >= 3h + s, at least 3
+    // per periodic axis, and 3h + s <= 1.3 * 3h (list capacity).  Sets PS.
+    int plan_skin(double dt, bool& ok)
+    {
+        ok = false;
+        skin_used = false;
+        skin_radius = 0;
+        if (rebuild_mode != 0 || Nf == 0) return SISPH_OK;
+        SCK(cudaMemsetAsync(&ctl->umax2_bits, 0, sizeof(unsigned long long), st));
+        ++nlaunch, k_max_speed<T, D><<<std::min(nblk(Nf, 256), 148 * 8), 256, 0, st>>>(vt, Nf, ctl);
+        SCK(cudaGetLastError());
+        SCK(cudaMemcpyAsync(&hctl->umax2_bits, &ctl->umax2_bits, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                            st));
+        SCK(cudaStreamSynchronize(st));
+        double um2;
+        unsigned long long b = hctl->umax2_bits;
+        memcpy(&um2, &b, sizeof(double));
+        if (!std::isfinite(um2)) return SISPH_OK;
+        const double R = 3.0 * (double)P.h;
+        const double eps = std::is_same<T, float>::value ? 1e-6 : 1e-14;
+        const double Rs = R + 2.0 * dt * sqrt(um2) * (1.0 + 1e-6) + eps * (extent + R) + 1e-9 * R;
+        if (Rs > 1.3 * R) return SISPH_OK;
+        Params<T> G = P;
+        for (int a = 0; a < D; a++) {
+            int nc = (int)floor(P.Ld[a] / (Rs * (1.0 + 1.0 / (1 << 20))));
+            if (nc < 1) nc = 1;
+            if (P.per[a] && nc < 3) return SISPH_OK;
+            if (nc > P.nc[a]) nc = P.nc[a];
+            G.nc[a] = nc;
+            G.cell[a] = P.Ld[a] / nc;
+        }
+        G.Rs2 = (T)(Rs * Rs * (1.0 + 1.0 / 1024.0));
+        // loose-list capacity: the exact capacity scaled by the volume ratio
+        int want = (int)ceil(P.cap * pow(Rs / R, D)) + 8;
+        want = (want + 7) / 8 * 8;
+        if (want > cap_s) {
+            if (nbs) cudaFree(nbs);
+            nbs = nullptr;
+            int rc = 0;
+            nbs = dalloc<int>((size_t)want * rows32(Ntot), err, rc);
+            if (rc) return rc;
+            cap_s = want;
+        }
+        G.cap = cap_s;
+        PS = G;
+        // walls binned on the skin grid (static: only when the grid changes)
+        if (Nw && (G.nc[0] != wnc_s[0] || G.nc[1] != wnc_s[1] || G.nc[2] != wnc_s[2])) {
+            SRET(sort_set(G, pos + Nf, Nw, wstart_s, wperm_s));
+            for (int a = 0; a < 3; a++) wnc_s[a] = G.nc[a];
+        } else if (!Nw) {
+            SCK(cudaMemsetAsync(wstart_s, 0, ((size_t)ncells_of(G) + 1) * sizeof(int), st));
+        }
+        ok = true;
+        skin_used = true;
+        skin_radius = Rs;
         return SISPH_OK;
     }
 
@@ -413,13 +518,16 @@ template <class T, int D> struct Engine : EngineBase {
             SCK(cudaMemcpyAsync(p + Nf, p_alt + Nf, Nw * sizeof(T), cudaMemcpyDeviceToDevice, st));
             SCK(cudaMemcpyAsync(rkA + Nf, pos + Nf, Nw * sizeof(V), cudaMemcpyDeviceToDevice, st));
             SCK(cudaMemcpyAsync(rkB + Nf, pos + Nf, Nw * sizeof(V), cudaMemcpyDeviceToDevice, st));
+            SCK(cudaMemcpyAsync(rn + Nf, pos + Nf, Nw * sizeof(V), cudaMemcpyDeviceToDevice, st));
+            SCK(cudaMemcpyAsync(rstar + Nf, pos + Nf, Nw * sizeof(V), cudaMemcpyDeviceToDevice, st));
+            wnc_s[0] = wnc_s[1] = wnc_s[2] = -1;
         } else {
             SCK(cudaMemsetAsync(wstart, 0, ((size_t)ncells + 1) * sizeof(int), st));
         }
         SRET(build_fluid());
         if (Nw > 0) {
-            ++nlaunch, k_normals_raw<T, D><<<nblk(Nw, 128), 128, 0, st>>>(P, pos, rho, nbr, cnt, nstmp);
-            ++nlaunch, k_normals_smooth<T, D><<<nblk(Nw, 128), 128, 0, st>>>(P, pos, rho, nbr, cnt, nstmp, nrm);
+            ++nlaunch, k_normals_raw<T, D><<<nblk(Nw, 128), 128, 0, st>>>(P, pos, rho, nbr, cnt, P.cap, nstmp);
+            ++nlaunch, k_normals_smooth<T, D><<<nblk(Nw, 128), 128, 0, st>>>(P, pos, rho, nbr, cnt, P.cap, nstmp, nrm);
             SCK(cudaGetLastError());
         }
         return SISPH_OK;
@@ -427,9 +535,9 @@ template <class T, int D> struct Engine : EngineBase {
 
     // build at the current fluid positions: sort, reorder the carried state,
     // neighbour lists.
-    int build_fluid()
+    int build_fluid(bool loose = false)
     {
-        SRET(sort_set(pos, Nf, fstart, perm));
+        SRET(sort_set(loose ? PS : P, pos, Nf, fstart, perm));
         GatherList G{};
         gl_add(G, pos, pos_alt, sizeof(V), Nf);
         gl_add(G, vel, vel_alt, sizeof(V), Nf);
@@ -448,7 +556,7 @@ template <class T, int D> struct Engine : EngineBase {
         std::swap(pid, pid_alt);
         std::swap(rho, rho_alt);
         std::swap(fs, fs_alt);
-        return build_list();
+        return loose ? build_loose() : build_list();
     }
 
     int copy_walls_to_alt()
@@ -477,43 +585,56 @@ template <class T, int D> struct Engine : EngineBase {
             return SISPH_EINVAL;
         }
         last_dt = dt;
-        // A1-A5 at r^n
-        SRET(build_fluid());
-        // A6
-        ++nlaunch, k_density<T, D><<<nblk(Ntot, 256), 256, 0, st>>>(P, pos, nbr, cnt, rho, fs);
+        bool single = false;
+        SRET(plan_skin(dt, single));
+        // A1-A5 at r^n (single build: the loose list on the skin grid)
+        SRET(build_fluid(single));
+        const int* nb1 = single ? nbs : nbr;
+        const int* cn1 = single ? cnt_s : cnt;
+        const int cap1 = single ? cap_s : P.cap;
+        // A6 (loose pairs beyond 3h contribute exactly 0: W, dW/dr vanish for q >= 3)
+        ++nlaunch, k_density<T, D><<<nblk(Ntot, 256), 256, 0, st>>>(P, pos, nb1, cn1, cap1, rho, fs);
         // A7
-        if (Nw) ++nlaunch, k_wall_velocity<T, D><<<nblk(Nw, 256), 256, 0, st>>>(P, pos, nbr, cnt, nrm, vel, 0);
+        if (Nw) ++nlaunch, k_wall_velocity<T, D><<<nblk(Nw, 256), 256, 0, st>>>(P, pos, nb1, cn1, cap1, nrm, vel, 0);
         // A8
-        if (Nf) ++nlaunch, k_forces_predict<T, D><<<nblk(Nf, 128), 128, 0, st>>>(P, (T)dt, pos, vel, vt, rho, nbr, cnt, us, rstar);
+        if (Nf) ++nlaunch, k_forces_predict<T, D><<<nblk(Nf, 128), 128, 0, st>>>(P, (T)dt, pos, vel, vt, rho, nb1, cn1, cap1, us, rstar);
         SCK(cudaGetLastError());
-        // A9: build at r*; carry r^n along as rn
-        SRET(sort_set(rstar, Nf, fstart, perm));
-        GatherList G{};
-        gl_add(G, rstar, pos_alt, sizeof(V), Nf);
-        gl_add(G, pos, rn, sizeof(V), Nf);
-        gl_add(G, vel, vel_alt, sizeof(V), Nf);
-        gl_add(G, vt, vt_alt, sizeof(V), Nf);
-        gl_add(G, us, us_alt, sizeof(V), Nf);
-        gl_add(G, rho, rho_alt, sizeof(T), Nf);
-        gl_add(G, fs, fs_alt, 1, Nf);
-        gl_add(G, p, p_alt, sizeof(T), Nf);
-        gl_add(G, pid, pid_alt, sizeof(int), Nf);
-        SRET(gather(G, perm, Nf));
-        SRET(copy_walls_to_alt());
-        std::swap(pos, pos_alt);
-        std::swap(vel, vel_alt);
-        std::swap(vt, vt_alt);
-        std::swap(us, us_alt);
-        std::swap(rho, rho_alt);
-        std::swap(fs, fs_alt);
-        std::swap(p, p_alt);
-        std::swap(pid, pid_alt);
-        SRET(build_list(true));   // + GTVF inner list
+        if (single) {
+            // A9 (R3): r* becomes the current position set (walls are in every buffer),
+            // r^n is kept as rn; exact sets at r* filtered out of the loose list
+            std::swap(pos, rstar);
+            std::swap(rn, rstar);
+            SRET(filter_list());
+        } else {
+            // A9: build at r*; carry r^n along as rn
+            SRET(sort_set(rstar, Nf, fstart, perm));
+            GatherList G{};
+            gl_add(G, rstar, pos_alt, sizeof(V), Nf);
+            gl_add(G, pos, rn, sizeof(V), Nf);
+            gl_add(G, vel, vel_alt, sizeof(V), Nf);
+            gl_add(G, vt, vt_alt, sizeof(V), Nf);
+            gl_add(G, us, us_alt, sizeof(V), Nf);
+            gl_add(G, rho, rho_alt, sizeof(T), Nf);
+            gl_add(G, fs, fs_alt, 1, Nf);
+            gl_add(G, p, p_alt, sizeof(T), Nf);
+            gl_add(G, pid, pid_alt, sizeof(int), Nf);
+            SRET(gather(G, perm, Nf));
+            SRET(copy_walls_to_alt());
+            std::swap(pos, pos_alt);
+            std::swap(vel, vel_alt);
+            std::swap(vt, vt_alt);
+            std::swap(us, us_alt);
+            std::swap(rho, rho_alt);
+            std::swap(fs, fs_alt);
+            std::swap(p, p_alt);
+            std::swap(pid, pid_alt);
+            SRET(build_list(true));   // + GTVF inner list
+        }
         // A10
-        if (Nw) ++nlaunch, k_wall_velocity<T, D><<<nblk(Nw, 256), 256, 0, st>>>(P, pos, nbr, cnt, nrm, us, P.ustar_noslip ? 0 : 1);
+        if (Nw) ++nlaunch, k_wall_velocity<T, D><<<nblk(Nw, 256), 256, 0, st>>>(P, pos, nbr, cnt, P.cap, nrm, us, P.ustar_noslip ? 0 : 1);
         // A11
         SCK(cudaMemsetAsync(&ctl->lambda_bits, 0, sizeof(unsigned long long), st));
-        if (Nf) ++nlaunch, k_rhs_diag<T, D><<<nblk(Nf, 128), 128, 0, st>>>(P, (T)(1.0 / dt), pos, us, rho, fs, nbr, cnt, rhs, diag, ctl);
+        if (Nf) ++nlaunch, k_rhs_diag<T, D><<<nblk(Nf, 128), 128, 0, st>>>(P, (T)(1.0 / dt), pos, us, rho, fs, nbr, cnt, P.cap, rhs, diag, ctl);
         SCK(cudaGetLastError());
         phase = PREDICTED;
         return SISPH_OK;
@@ -528,7 +649,7 @@ template <class T, int D> struct Engine : EngineBase {
     int launch_sweeps(int count, double tl, int mi, int mx)
     {
         for (int c = 0; c < count; c++) {
-            if (Nw) ++nlaunch, k_wall_pressure<T, D><<<nblk(Nw, 256), 256, 0, st>>>(P, pos, rho, nbr, cnt, p, p_alt, ctl);
+            if (Nw) ++nlaunch, k_wall_pressure<T, D><<<nblk(Nw, 256), 256, 0, st>>>(P, pos, rho, nbr, cnt, P.cap, p, p_alt, ctl);
             bool rec = timing && nrec < MAXREC;
             if (rec) {
                 if (!sev[2 * nrec]) {
@@ -537,7 +658,7 @@ template <class T, int D> struct Engine : EngineBase {
                 }
                 SCK(cudaEventRecord(sev[2 * nrec], st));
             }
-            ++nlaunch, k_sweep<T, D><<<nblk(Nf, SWEEP_T), SWEEP_T, 0, st>>>(P, pos, rho, rhs, diag, fs, nbr, cnt, p, p_alt, ctl,
+            ++nlaunch, k_sweep<T, D><<<nblk(Nf, SWEEP_T), SWEEP_T, 0, st>>>(P, pos, rho, rhs, diag, fs, nbr, cnt, P.cap, p, p_alt, ctl,
                                                                   partials, tl, mi, mx);
             if (rec) {
                 SCK(cudaEventRecord(sev[2 * nrec + 1], st));
@@ -610,10 +731,10 @@ template <class T, int D> struct Engine : EngineBase {
         for (int k = 0; k < K; k++) {
             V* dst = (k & 1) ? rkB : rkA;
             if (inner)
-                ++nlaunch, k_gtvf_substep<T, D><<<nblk(Nf, 128), 128, 0, st>>>(P, dtau, src, dst, vk, dk, p, nbr_in, Nf,
+                ++nlaunch, k_gtvf_substep<T, D><<<nblk(Nf, 128), 128, 0, st>>>(P, dtau, src, dst, vk, dk, p, nbr_in, P.cap_in,
                                                                                cnt_in, k == 0, pos, 1, ctl);
             else
-                ++nlaunch, k_gtvf_substep<T, D><<<nblk(Nf, 128), 128, 0, st>>>(P, dtau, src, dst, vk, dk, p, nbr, Ntot,
+                ++nlaunch, k_gtvf_substep<T, D><<<nblk(Nf, 128), 128, 0, st>>>(P, dtau, src, dst, vk, dk, p, nbr, P.cap,
                                                                                cnt, k == 0, pos, 0, ctl);
             src = dst;
         }
@@ -633,8 +754,8 @@ template <class T, int D> struct Engine : EngineBase {
             return SISPH_EINVAL;
         }
         // A13
-        if (Nw) ++nlaunch, k_wall_pressure<T, D><<<nblk(Nw, 256), 256, 0, st>>>(P, pos, rho, nbr, cnt, p, p_alt, nullptr);
-        if (Nf) ++nlaunch, k_pgrad_correct<T, D><<<nblk(Nf, 128), 128, 0, st>>>(P, (T)dt, pos, rho, p, us, nbr, cnt, vel);
+        if (Nw) ++nlaunch, k_wall_pressure<T, D><<<nblk(Nw, 256), 256, 0, st>>>(P, pos, rho, nbr, cnt, P.cap, p, p_alt, nullptr);
+        if (Nf) ++nlaunch, k_pgrad_correct<T, D><<<nblk(Nf, 128), 128, 0, st>>>(P, (T)dt, pos, rho, p, us, nbr, cnt, P.cap, vel);
         // A14: K sub-steps (p0 = 0 everywhere when p_ref == 0: the shift is exactly zero)
         const V* rK = nullptr;   // GTVF displacement r^K - r^0 (none when p0 = 0)
         if (P.p_ref != T(0) && K > 0 && Nf) {
@@ -680,6 +801,8 @@ template <class T, int D> struct Engine : EngineBase {
             rep->ms_sweeps = last_ms_sweeps;
             rep->sweeps_timed = last_sweeps_timed;
             rep->launches = nlaunch - l0;
+            rep->single_build = skin_used ? 1 : 0;
+            rep->skin_radius = skin_radius;
             if (timing) {
                 SCK(cudaEventSynchronize(ev[3]));
                 float a, b, c;
@@ -847,7 +970,7 @@ template <class T, int D> struct Engine : EngineBase {
 
     int get_neighbors(int64_t* off, int64_t* ids, int64_t cap, int64_t* total) override
     {
-        std::vector<int> hc(Ntot), hp(Ntot), hn((size_t)P.cap * Ntot);
+        std::vector<int> hc(Ntot), hp(Ntot), hn((size_t)P.cap * rows32(Ntot));
         SCK(cudaMemcpyAsync(hc.data(), cnt, Ntot * sizeof(int), cudaMemcpyDeviceToHost, st));
         SCK(cudaMemcpyAsync(hp.data(), pid, Ntot * sizeof(int), cudaMemcpyDeviceToHost, st));
         SCK(cudaMemcpyAsync(hn.data(), nbr, hn.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -864,7 +987,9 @@ template <class T, int D> struct Engine : EngineBase {
         for (int64_t k = 0; k < n; k++) {
             int s = slot_of[k];
             int64_t* row = ids + off[k];
-            for (int q = 0; q < hc[s]; q++) row[q] = hp[hn[(size_t)q * Ntot + s]];
+            // blocked ELL (see sisph_kernels.cuh): (s / 32) 32 cap + (q / 4) 128 + (s % 32) 4 + q % 4
+            const size_t b = (size_t)(s >> 5) * ((size_t)P.cap << 5) + ((s & 31) << 2);
+            for (int q = 0; q < hc[s]; q++) row[q] = hp[hn[b + ((size_t)(q >> 2) << 7) + (q & 3)]];
             std::sort(row, row + hc[s]);
         }
         return SISPH_OK;

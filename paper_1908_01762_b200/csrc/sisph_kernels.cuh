@@ -23,7 +23,26 @@ struct Ctl {
     unsigned long long pairs_inner;  // sum of GTVF inner-list counts of the last build
     int gtvf_far;              // a particle moved more than skin/2 during the GTVF sub-steps
     int pad2;
+    unsigned long long umax2_bits;   // max |u~|^2 over fluid (ordered bits of a non-negative double)
 };
+
+// ===========================================================================
+// max |u~_i|^2 over fluid particles: sizes the skin of the single per-step
+// build (R3: |r*_ij| <= |r^n_ij| + dt |u~_i| + dt |u~_j|, eq:int:rnp1).
+// ===========================================================================
+template <class T, int D>
+__global__ void __launch_bounds__(256) k_max_speed(const V4<T>* __restrict__ vt, int n, Ctl* ctl)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    double v = 0.0;
+    for (; i < n; i += gridDim.x * blockDim.x) {
+        V4<T> u = ld4(vt + i);
+        double a = (double)u.x * u.x + (double)u.y * u.y + (D == 3 ? (double)u.z * u.z : 0.0);
+        v = fmax(v, a);
+    }
+    v = warp_max(v);
+    if ((threadIdx.x & 31) == 0 && v > 0.0) atomicMax(&ctl->umax2_bits, (unsigned long long)__double_as_longlong(v));
+}
 
 // ===========================================================================
 // A1: cell hash + per-cell counts.  rank = arrival order inside the cell
@@ -197,106 +216,96 @@ __global__ void k_gather(GatherList G, const int* __restrict__ perm, int n)
 // A5: neighbour lists.  Destination i scans the 3^d stencil of its cell; in
 // each stencil row the cells (cx-1 .. cx+1) are consecutive keys, so their
 // fluid particles form ONE contiguous slot range (likewise the walls').
-// Slot-major ELL: nbr[k * Ntot + i], k < cnt[i] (coalesced per warp).
+//
+// Storage: blocked ELL.  Rows in groups of 32; inside a group the entries k
+// .. k+3 of each row form one 16-byte chunk and the 32 rows' chunks are
+// contiguous:
+//     index(i, k) = (i / 32) 32 cap + (k / 4) 128 + (i % 32) 4 + k % 4
+// (cap a multiple of 4, rows padded to a multiple of 32).  A warp of 32
+// consecutive destinations reads 4 entries each with ONE coalesced 512-byte
+// int4 load; a builder lane fills its own row's chunks in order, so every
+// 16-byte chunk is written by one lane and every 512-byte block by one warp
+// (the L2 merges them before write-back: no partial-sector traffic).
 // ===========================================================================
-// One warp per cell: the lanes are the cell's destinations (fluid, then
-// walls, 32 at a time); candidates of each stencil row are staged 32 at a
-// time in shared memory and read back as broadcasts, so every lane tests the
-// same candidate in lockstep (no divergence, one LDS per candidate).
-// Optionally also writes the GTVF inner list (fluid rows; pairs with
-// r^2 < Rin2f, slot-major with stride Nf).
-constexpr int BL_WARPS = 4;
-
-// Candidates of one slot range are staged 32 at a time with the range's
-// periodic image shift (sx, sy, sz) already applied, so the fast test is a
-// plain difference.  Pairs whose fp32 r^2 falls in the +-2^-12 band around
-// R^2 (or every pair in fp64 mode) are decided exactly (R2) from the
-// unshifted positions with the oracle's minimum-image arithmetic.
-struct BLState {
-    int k, k2;          // list lengths so far
-    int off, off2;      // running store offsets k * Ntot, k2 * Nf
-};
-
-template <class T, int D>
-__device__ __forceinline__ void bl_range(const Params<T>& P, const V4<T>* __restrict__ pos, V4<T>* sm, V4<T>* smo,
-                                         const V4<T>& xi, int i, bool act, int a, int b, T sx, T sy, T sz,
-                                         int* __restrict__ nbr, int* __restrict__ nbr_in, BLState& S,
-                                         float R2lo, float R2hi, float Rin2)
+__device__ __forceinline__ size_t nb_base(int i, int cap)
 {
-    const int lane = threadIdx.x & 31;
-    const int cap = P.cap, cap_in = P.cap_in, Ntot = P.Ntot, Nf = P.Nf;
-    const int pmask = P.per[0] | (P.per[1] << 1) | (P.per[2] << 2);
-    const double xid = (double)xi.x, yid = (double)xi.y, zid = (double)xi.z;
-    for (int j0 = a; j0 < b; j0 += 32) {
-        int jj = j0 + lane;
-        if (jj < b) {
-            V4<T> v = ld4(pos + jj);
-            smo[lane] = v;
-            v.x += sx;
-            v.y += sy;
-            if (D == 3) v.z += sz;
-            sm[lane] = v;
-        }
-        __syncwarp();
-        const int nn = min(32, b - j0);
-        for (int q = 0; q < nn; q++) {
-            const V4<T> xj = sm[q];
-            const int j = j0 + q;
-            const float dx = (float)(xi.x - xj.x), dy = (float)(xi.y - xj.y);
-            const float dz = D == 3 ? (float)(xi.z - xj.z) : 0.f;
-            float r2 = dx * dx + dy * dy;
-            if (D == 3) r2 += dz * dz;
-            bool in = r2 < R2lo;
-            const bool band = !in && r2 <= R2hi;
-            // exact ties (lattices!) are common: the fp64 decision on the unshifted
-            // positions runs inline and predicated, once per candidate for the warp
-            if (__any_sync(0xffffffffu, band)) {
-                const V4<T> o = smo[q];
-                const bool ex = exact_band(xid, yid, zid, (double)o.x, (double)o.y, (double)o.z, P.Ld[0], P.Ld[1],
-                                           P.Ld[2], pmask, D == 3, P.R2d);
-                in = band ? ex : in;
-            }
-            const bool acc = act && in && j != i;
-            if (acc && S.k < cap) nbr[S.off + i] = j;
-            S.k += acc ? 1 : 0;
-            S.off += acc ? Ntot : 0;
-            const bool ai = acc && r2 < Rin2;
-            if (ai && S.k2 < cap_in) nbr_in[S.off2 + i] = j;
-            S.k2 += ai ? 1 : 0;
-            S.off2 += ai ? Nf : 0;
-        }
-        __syncwarp();
+    return (size_t)(i >> 5) * ((size_t)cap << 5) + (size_t)((i & 31) << 2);
+}
+// offset of entry k + 1 relative to entry k
+__device__ __forceinline__ int nb_adv(int k) { return (k & 3) == 3 ? 125 : 1; }
+
+// for every neighbour j of row i (n entries), in list order
+template <class F>
+__device__ __forceinline__ void for_nbrs(const int* __restrict__ nbr, int cap, int i, int n, F&& f)
+{
+    const int4* __restrict__ q = reinterpret_cast<const int4*>(nbr + nb_base(i, cap));
+    for (int c = 0; c < n; c += 4) {
+        const int4 v = __ldg(q + (size_t)(c >> 2) * 32);
+        f(v.x);
+        if (c + 1 < n) f(v.y);
+        if (c + 2 < n) f(v.z);
+        if (c + 3 < n) f(v.w);
     }
 }
 
+// a builder lane's append cursor into its row
+struct NbCursor {
+    int* row;   // nbr + nb_base(i, cap)
+    int off;    // offset of entry k
+    int k;      // entries so far (may exceed cap: overflow is counted, not stored)
+    __device__ __forceinline__ void init(int* nbr, int cap, int i)
+    {
+        row = nbr + nb_base(i, cap);
+        off = 0;
+        k = 0;
+    }
+    __device__ __forceinline__ void push(bool acc, int j, int cap)
+    {
+        if (acc && k < cap) row[off] = j;
+        off += acc ? nb_adv(k) : 0;
+        k += acc ? 1 : 0;
+    }
+};
+
+// One warp per cell: the lanes are the cell's destinations; candidates of
+// each stencil row are staged 32 at a time in shared memory (with the range's
+// periodic image shift applied) and read back as broadcasts, so every lane
+// tests the same candidate in lockstep.
+//
+// Two kernels:
+//  * k_build_cells (exact): N(i) = { j != i : r_ij^2 < (3h)^2 } decided as R2
+//    prescribes (fp32 prefilter with a +-2^-12 band decided in fp64 from the
+//    unshifted positions with the oracle's minimum-image arithmetic; every
+//    pair in fp64 mode), optionally also the GTVF inner list (fluid rows;
+//    pairs with r^2 < Rin2f);
+//  * k_build_loose: a superset list of every pair with r^2 < Rs2 in working
+//    precision (Rs = 3h + skin, inflated), no exact decision: the single
+//    per-step build at r^n (R3) whose exact r* sets k_filter extracts.
+//    A lane takes up to two destinations (cells of 33..64 particles in one
+//    pass over the candidates).
+// Walls are static: their slots keep the order of the base geometry, and a
+// build on another cell geometry reads them through wperm (wall slots sorted
+// by that geometry's key); wperm == nullptr means identity.
+constexpr int BL_WARPS = 4;
+
+__device__ __forceinline__ int wslot(const int* __restrict__ wperm, int Nf, int u)
+{
+    return (wperm && u >= Nf) ? Nf + __ldg(wperm + (u - Nf)) : u;
+}
+
+// slot ranges of the 3^d stencil of cell c: lane r < NROW fills row r = (dy, dz)
+// with up to 3 fluid + 3 wall ranges (x, y) and the image shift code z
+// (2 bits per axis, s + 1 for a shift of s L).  Returns after __syncwarp.
 template <class T, int D>
-__global__ void __launch_bounds__(32 * BL_WARPS) k_build_cells(Params<T> P, int ncells, const V4<T>* __restrict__ pos,
-                                                              const int* __restrict__ fstart,
-                                                              const int* __restrict__ wstart, int* __restrict__ nbr,
-                                                              int* __restrict__ cnt, int* __restrict__ nbr_in,
-                                                              int* __restrict__ cnt_in, Ctl* ctl)
+__device__ __forceinline__ void stencil_ranges(const Params<T>& P, int c, const int* __restrict__ fstart,
+                                               const int* __restrict__ wstart, int4* o6)
 {
     constexpr int NROW = D == 3 ? 9 : 3;
-    constexpr int NRNG = NROW * 6;   // per row: up to 3 fluid + 3 wall slot ranges
-    __shared__ V4<T> smem[BL_WARPS][32], smemo[BL_WARPS][32];
-    __shared__ int4 rng[BL_WARPS][NRNG];   // (first slot, end slot, image shift code, -)
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int c = blockIdx.x * BL_WARPS + warp;
-    if (c >= ncells) return;
-    const int fa = fstart[c], nfc = fstart[c + 1] - fa;
-    const int wa = wstart[c], nwc = wstart[c + 1] - wa;
-    const int nd = nfc + nwc;
-    if (nd == 0) return;
-    V4<T>* sm = smem[warp];
-    V4<T>* smo = smemo[warp];
-    // lane r < NROW: slot ranges of stencil row r = (dy, dz); in a row the cells
-    // cx-1 .. cx+1 are consecutive keys, so they form one contiguous range
-    // (three separate cells only where a periodic x axis wraps)
-    // image shift code: 2 bits per axis, value s + 1 for a shift of s L (s in -1, 0, 1)
+    const int lane = threadIdx.x & 31;
     if (lane < NROW) {
         const int c0 = c % P.nc[0], c1 = (c / P.nc[0]) % P.nc[1], c2 = c / (P.nc[0] * P.nc[1]);
         const int dy = lane % 3 - 1, dz = D == 3 ? lane / 3 - 1 : 0;
-        int4* o = rng[warp] + 6 * lane;
+        int4* o = o6 + 6 * lane;
         for (int q = 0; q < 6; q++) o[q] = make_int4(0, 0, 0, 0);
         int cy = c1 + dy, cz = c2 + dz;
         int code = 1 | (1 << 2) | (1 << 4);
@@ -332,36 +341,117 @@ __global__ void __launch_bounds__(32 * BL_WARPS) k_build_cells(Params<T> P, int 
         }
     }
     __syncwarp();
+}
+
+template <class T>
+__device__ __forceinline__ void shift_of(const Params<T>& P, int code, T& sx, T& sy, T& sz)
+{
+    sx = (T)((code & 3) - 1) * P.L[0];
+    sy = (T)(((code >> 2) & 3) - 1) * P.L[1];
+    sz = (T)(((code >> 4) & 3) - 1) * P.L[2];
+}
+
+// stage candidates [j0, min(j0 + 32, b)) of a range: shifted copy, unshifted
+// copy (exact mode only) and slot
+template <class T, int D, bool ORIG>
+__device__ __forceinline__ void stage32(const V4<T>* __restrict__ pos, const int* __restrict__ wperm, int Nf, int j0,
+                                        int b, T sx, T sy, T sz, V4<T>* sm, V4<T>* smo, int* smj)
+{
+    const int lane = threadIdx.x & 31;
+    const int jj = j0 + lane;
+    if (jj < b) {
+        const int slot = wslot(wperm, Nf, jj);
+        V4<T> v = ld4(pos + slot);
+        if (ORIG) smo[lane] = v;
+        smj[lane] = slot;
+        v.x += sx;
+        v.y += sy;
+        if (D == 3) v.z += sz;
+        sm[lane] = v;
+    }
+    __syncwarp();
+}
+
+template <class T, int D>
+__global__ void __launch_bounds__(32 * BL_WARPS) k_build_cells(Params<T> P, int ncells, const V4<T>* __restrict__ pos,
+                                                              const int* __restrict__ fstart,
+                                                              const int* __restrict__ wstart,
+                                                              const int* __restrict__ wperm, int* __restrict__ nbr,
+                                                              int* __restrict__ cnt, int* __restrict__ nbr_in,
+                                                              int* __restrict__ cnt_in, Ctl* ctl)
+{
+    constexpr int NROW = D == 3 ? 9 : 3;
+    constexpr int NRNG = NROW * 6;
+    __shared__ V4<T> smem[BL_WARPS][32], smemo[BL_WARPS][32];
+    __shared__ int smemj[BL_WARPS][32];
+    __shared__ int4 rng[BL_WARPS][NRNG];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int c = blockIdx.x * BL_WARPS + warp;
+    if (c >= ncells) return;
+    const int fa = fstart[c], nfc = fstart[c + 1] - fa;
+    const int wa = wstart[c], nwc = wstart[c + 1] - wa;
+    const int nd = nfc + nwc;
+    if (nd == 0) return;
+    V4<T>* sm = smem[warp];
+    V4<T>* smo = smemo[warp];
+    int* smj = smemj[warp];
+    stencil_ranges<T, D>(P, c, fstart, wstart, rng[warp]);
+    const int Nf = P.Nf, cap = P.cap, cap_in = P.cap_in;
+    const int pmask = P.per[0] | (P.per[1] << 1) | (P.per[2] << 2);
     int mmax = 0;
     unsigned sfl = 0, sin_ = 0;
     for (int base = 0; base < nd; base += 32) {
         const int t = base + lane;
         const bool act = t < nd;
-        const int i = !act ? -1 : (t < nfc ? fa + t : P.Nf + wa + (t - nfc));
-        V4<T> xi = ld4(pos + (act ? i : fa));
-        BLState S{0, 0, 0, 0};
-        // wall destinations get no inner list (a warp's lanes may mix fluid and walls:
-        // the pointer stays uniform, the per-lane test below excludes wall rows)
-        int* nin = nbr_in;
-        const float Rin2 = (nin && i < P.Nf) ? P.Rin2f : -1.f;
-        const float R2lo = P.R2lo, R2hi = P.R2hi;
+        const int i = !act ? -1 : (t < nfc ? fa + t : wslot(wperm, Nf, Nf + wa + (t - nfc)));
+        const V4<T> xi = ld4(pos + (act ? i : fa));
+        const double xid = (double)xi.x, yid = (double)xi.y, zid = (double)xi.z;
+        NbCursor A, B;
+        A.init(nbr, cap, act ? i : 0);
+        // wall destinations get no inner list
+        const bool inner = nbr_in && act && i < Nf;
+        B.init(nbr_in ? nbr_in : nbr, cap_in, inner ? i : 0);
+        const float Rin2 = inner ? P.Rin2f : -1.f;
 #pragma unroll 1
         for (int q = 0; q < NRNG; q++) {
             const int4 ab = rng[warp][q];
-            if (ab.x < ab.y) {
-                const T sx = (T)((ab.z & 3) - 1) * P.L[0], sy = (T)(((ab.z >> 2) & 3) - 1) * P.L[1];
-                const T sz = (T)(((ab.z >> 4) & 3) - 1) * P.L[2];
-                bl_range<T, D>(P, pos, sm, smo, xi, i, act, ab.x, ab.y, sx, sy, sz, nbr, nin, S, R2lo, R2hi, Rin2);
+            if (ab.x >= ab.y) continue;
+            T sx, sy, sz;
+            shift_of(P, ab.z, sx, sy, sz);
+            for (int j0 = ab.x; j0 < ab.y; j0 += 32) {
+                stage32<T, D, true>(pos, wperm, Nf, j0, ab.y, sx, sy, sz, sm, smo, smj);
+                const int nn = min(32, ab.y - j0);
+                for (int u = 0; u < nn; u++) {
+                    const V4<T> xj = sm[u];
+                    const int j = smj[u];
+                    const float dx = (float)(xi.x - xj.x), dy = (float)(xi.y - xj.y);
+                    const float dz = D == 3 ? (float)(xi.z - xj.z) : 0.f;
+                    float r2 = dx * dx + dy * dy;
+                    if (D == 3) r2 += dz * dz;
+                    bool in = r2 < P.R2lo;
+                    const bool band = !in && r2 <= P.R2hi;
+                    // exact ties (lattices!) are common: the fp64 decision on the unshifted
+                    // positions runs inline and predicated, once per candidate for the warp
+                    if (__any_sync(0xffffffffu, band)) {
+                        const V4<T> o = smo[u];
+                        const bool ex = exact_band(xid, yid, zid, (double)o.x, (double)o.y, (double)o.z, P.Ld[0],
+                                                   P.Ld[1], P.Ld[2], pmask, D == 3, P.R2d);
+                        in = band ? ex : in;
+                    }
+                    const bool acc = act && in && j != i;
+                    A.push(acc, j, cap);
+                    B.push(acc && r2 < Rin2, j, cap_in);
+                }
+                __syncwarp();
             }
         }
-        const int k = S.k, k2 = S.k2;
         if (act) {
-            cnt[i] = min(k, P.cap);
-            if (nin && i < P.Nf) cnt_in[i] = min(k2, P.cap_in);
-            mmax = max(mmax, max(k, nin && k2 > P.cap_in ? P.cap + 1 : 0));
-            if (i < P.Nf) {
-                sfl += (unsigned)min(k, P.cap);
-                sin_ += (unsigned)k2;
+            cnt[i] = min(A.k, cap);
+            if (inner) cnt_in[i] = min(B.k, cap_in);
+            mmax = max(mmax, max(A.k, inner && B.k > cap_in ? cap + 1 : 0));
+            if (i < Nf) {
+                sfl += (unsigned)min(A.k, cap);
+                sin_ += (unsigned)B.k;
             }
         }
     }
@@ -373,7 +463,177 @@ __global__ void __launch_bounds__(32 * BL_WARPS) k_build_cells(Params<T> P, int 
     }
     if (lane == 0) {
         atomicMax(&ctl->max_count, mmax);
-        if (mmax > P.cap) atomicExch(&ctl->overflow, 1);
+        if (mmax > cap) atomicExch(&ctl->overflow, 1);
+        if (sfl) atomicAdd(&ctl->pairs_fluid, (unsigned long long)sfl);
+        if (sin_) atomicAdd(&ctl->pairs_inner, (unsigned long long)sin_);
+    }
+}
+
+// loose candidate loop over one staged chunk for DPL destinations per lane
+template <class T, int D, int DPL>
+__device__ __forceinline__ void loose_chunk(const V4<T>* sm, const int* smj, int nn, const V4<T> (&xi)[2],
+                                            const int (&i)[2], const bool (&act)[2], NbCursor (&A)[2], T Rs2, int cap)
+{
+#pragma unroll 4
+    for (int u = 0; u < nn; u++) {
+        const V4<T> xj = sm[u];
+        const int j = smj[u];
+#pragma unroll
+        for (int d = 0; d < DPL; d++) {
+            const T dx = xi[d].x - xj.x, dy = xi[d].y - xj.y;
+            T r2 = dx * dx + dy * dy;
+            if (D == 3) {
+                const T dz = xi[d].z - xj.z;
+                r2 += dz * dz;
+            }
+            A[d].push(act[d] && r2 < Rs2 && j != i[d], j, cap);
+        }
+    }
+}
+
+template <class T, int D>
+__global__ void __launch_bounds__(32 * BL_WARPS) k_build_loose(Params<T> P, int ncells, const V4<T>* __restrict__ pos,
+                                                              const int* __restrict__ fstart,
+                                                              const int* __restrict__ wstart,
+                                                              const int* __restrict__ wperm, int* __restrict__ nbr,
+                                                              int* __restrict__ cnt, Ctl* ctl)
+{
+    constexpr int NROW = D == 3 ? 9 : 3;
+    constexpr int NRNG = NROW * 6;
+    __shared__ V4<T> smem[BL_WARPS][32];
+    __shared__ int smemj[BL_WARPS][32];
+    __shared__ int4 rng[BL_WARPS][NRNG];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int c = blockIdx.x * BL_WARPS + warp;
+    if (c >= ncells) return;
+    const int fa = fstart[c], nfc = fstart[c + 1] - fa;
+    const int wa = wstart[c], nwc = wstart[c + 1] - wa;
+    const int nd = nfc + nwc;
+    if (nd == 0) return;
+    V4<T>* sm = smem[warp];
+    int* smj = smemj[warp];
+    stencil_ranges<T, D>(P, c, fstart, wstart, rng[warp]);
+    const int Nf = P.Nf, cap = P.cap;
+    const T Rs2 = P.Rs2;
+    int mmax = 0;
+    for (int base = 0; base < nd; base += 64) {
+        const bool two = nd - base > 32;   // warp-uniform
+        V4<T> xi[2];
+        int i[2];
+        bool act[2];
+        NbCursor A[2];
+#pragma unroll
+        for (int d = 0; d < 2; d++) {
+            const int t = base + 32 * d + lane;
+            act[d] = t < nd;
+            i[d] = !act[d] ? -1 : (t < nfc ? fa + t : wslot(wperm, Nf, Nf + wa + (t - nfc)));
+            xi[d] = ld4(pos + (act[d] ? i[d] : fa));
+            A[d].init(nbr, cap, act[d] ? i[d] : 0);
+        }
+#pragma unroll 1
+        for (int q = 0; q < NRNG; q++) {
+            const int4 ab = rng[warp][q];
+            if (ab.x >= ab.y) continue;
+            T sx, sy, sz;
+            shift_of(P, ab.z, sx, sy, sz);
+            for (int j0 = ab.x; j0 < ab.y; j0 += 32) {
+                stage32<T, D, false>(pos, wperm, Nf, j0, ab.y, sx, sy, sz, sm, nullptr, smj);
+                const int nn = min(32, ab.y - j0);
+                if (two)
+                    loose_chunk<T, D, 2>(sm, smj, nn, xi, i, act, A, Rs2, cap);
+                else
+                    loose_chunk<T, D, 1>(sm, smj, nn, xi, i, act, A, Rs2, cap);
+                __syncwarp();
+            }
+        }
+#pragma unroll
+        for (int d = 0; d < 2; d++)
+            if (act[d]) {
+                cnt[i[d]] = min(A[d].k, cap);
+                mmax = max(mmax, A[d].k);
+            }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mmax = max(mmax, __shfl_xor_sync(0xffffffffu, mmax, o));
+    if (lane == 0 && mmax > cap) atomicExch(&ctl->overflow, 1);
+}
+
+// ===========================================================================
+// A9 (single-build form, R3): the exact neighbour sets at r* filtered out of
+// the loose list built at r^n.  Every pair with |r*_ij| < 3h has
+// |r^n_ij| < 3h + dt|u~_i| + dt|u~_j| <= Rs, so it is in the loose list; the
+// decision itself is R2's (fp32 prefilter + fp64 band, as the exact build).
+// The filtered rows keep the loose list's order (deterministic).  Also
+// writes the GTVF inner list of fluid rows.  The warp walks to its longest
+// row so that the fp64 band decision can be taken warp-wide.
+// ===========================================================================
+template <class T, int D>
+__global__ void __launch_bounds__(128) k_filter(Params<T> P, const V4<T>* __restrict__ pos,
+                                                const int* __restrict__ nbs, const int* __restrict__ cnts, int cap_s,
+                                                int* __restrict__ nbr, int* __restrict__ cnt,
+                                                int* __restrict__ nbr_in, int* __restrict__ cnt_in, Ctl* ctl)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int Ntot = P.Ntot, Nf = P.Nf, cap = P.cap, cap_in = P.cap_in;
+    const bool act = i < Ntot;
+    const bool inner = act && nbr_in && i < Nf;
+    const V4<T> xi = ld4(pos + (act ? i : 0));
+    const int n = act ? cnts[i] : 0;
+    int nmax = n;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
+    const float Rin2 = inner ? P.Rin2f : -1.f;
+    const int pmask = P.per[0] | (P.per[1] << 1) | (P.per[2] << 2);
+    NbCursor A, B;
+    A.init(nbr, cap, act ? i : 0);
+    B.init(nbr_in ? nbr_in : nbr, cap_in, inner ? i : 0);
+    const int4* __restrict__ src = reinterpret_cast<const int4*>(nbs + nb_base(act ? i : 0, cap_s));
+    for (int c = 0; c < nmax; c += 4) {
+        const int4 v = c < n ? __ldg(src + (size_t)(c >> 2) * 32) : make_int4(0, 0, 0, 0);
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+            const bool valid = c + e < n;
+            const int j = e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
+            const V4<T> xj = ld4(pos + (valid ? j : 0));
+            float r2;
+            bool in;
+            if constexpr (std::is_same<T, float>::value) {
+                float d0 = xi.x - xj.x, d1 = xi.y - xj.y, d2 = D == 3 ? xi.z - xj.z : 0.f;
+                if (P.per[0]) d0 = wrapd(d0, P.Lf[0], P.halfLf[0]);
+                if (P.per[1]) d1 = wrapd(d1, P.Lf[1], P.halfLf[1]);
+                if (D == 3 && P.per[2]) d2 = wrapd(d2, P.Lf[2], P.halfLf[2]);
+                r2 = d0 * d0 + d1 * d1;
+                if (D == 3) r2 += d2 * d2;
+                in = r2 < P.R2lo;
+                const bool band = valid && !in && r2 <= P.R2hi;
+                if (__any_sync(0xffffffffu, band)) {
+                    const bool ex = exact_band((double)xi.x, (double)xi.y, (double)xi.z, (double)xj.x, (double)xj.y,
+                                               (double)xj.z, P.Ld[0], P.Ld[1], P.Ld[2], pmask, D == 3, P.R2d);
+                    in = band ? ex : in;
+                }
+            } else {
+                in = nb_test<D>(P, xi, xj, r2);
+            }
+            in = in && valid;
+            A.push(in, j, cap);
+            B.push(in && r2 < Rin2, j, cap_in);
+        }
+    }
+    if (act) {
+        cnt[i] = min(A.k, cap);
+        if (inner) cnt_in[i] = min(B.k, cap_in);
+    }
+    int mmax = act ? max(A.k, inner && B.k > cap_in ? cap + 1 : 0) : 0;
+    unsigned sfl = act && i < Nf ? (unsigned)min(A.k, cap) : 0u, sin_ = inner ? (unsigned)B.k : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mmax = max(mmax, __shfl_xor_sync(0xffffffffu, mmax, o));
+        sfl += __shfl_xor_sync(0xffffffffu, sfl, o);
+        sin_ += __shfl_xor_sync(0xffffffffu, sin_, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(&ctl->max_count, mmax);
+        if (mmax > cap) atomicExch(&ctl->overflow, 1);
         if (sfl) atomicAdd(&ctl->pairs_fluid, (unsigned long long)sfl);
         if (sin_) atomicAdd(&ctl->pairs_inner, (unsigned long long)sin_);
     }
@@ -386,7 +646,7 @@ __global__ void __launch_bounds__(32 * BL_WARPS) k_build_cells(Params<T> P, int 
 // ===========================================================================
 template <class T, int D>
 __global__ void __launch_bounds__(256) k_density(Params<T> P, const V4<T>* __restrict__ pos,
-                                                 const int* __restrict__ nbr, const int* __restrict__ cnt,
+                                                 const int* __restrict__ nbr, const int* __restrict__ cnt, int ncap,
                                                  T* __restrict__ rho, uint8_t* __restrict__ fs)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -398,13 +658,12 @@ __global__ void __launch_bounds__(256) k_density(Params<T> P, const V4<T>* __res
     }
     T s = 0;
     int n = cnt[i];
-    for (int k = 0; k < n; k++) {
-        int j = __ldg(nbr + (size_t)k * P.Ntot + i);
+    for_nbrs(nbr, ncap, i, n, [&](int j) {
         V4<T> xj = ld4(pos + j);
         T d[3], r, ri;
         r_of(pair_vec<T, D>(P, xi, xj, d), r, ri);
         s += xj.w * quintic5(r * P.inv_h);
-    }
+    });
     s = xi.w * P.w0 + P.sig * s;
     rho[i] = s;
     if (i < P.Nf) fs[i] = (s / P.rho0 < P.fs_ratio) ? 1 : 0;
@@ -419,7 +678,7 @@ __global__ void __launch_bounds__(256) k_density(Params<T> P, const V4<T>* __res
 // ===========================================================================
 template <class T, int D>
 __global__ void __launch_bounds__(256) k_wall_velocity(Params<T> P, const V4<T>* __restrict__ pos,
-                                                       const int* __restrict__ nbr, const int* __restrict__ cnt,
+                                                       const int* __restrict__ nbr, const int* __restrict__ cnt, int ncap,
                                                        const V4<T>* __restrict__ nrm, V4<T>* __restrict__ vel, int mode)
 {
     int w = blockIdx.x * blockDim.x + threadIdx.x;
@@ -428,9 +687,8 @@ __global__ void __launch_bounds__(256) k_wall_velocity(Params<T> P, const V4<T>*
     V4<T> xi = ld4(pos + i);
     T sw = 0, ax = 0, ay = 0, az = 0;
     int n = cnt[i];
-    for (int k = 0; k < n; k++) {
-        int j = __ldg(nbr + (size_t)k * P.Ntot + i);
-        if (j >= P.Nf) continue;
+    for_nbrs(nbr, ncap, i, n, [&](int j) {
+        if (j >= P.Nf) return;
         V4<T> xj = ld4(pos + j);
         T d[3], r, ri;
         r_of(pair_vec<T, D>(P, xi, xj, d), r, ri);
@@ -440,7 +698,7 @@ __global__ void __launch_bounds__(256) k_wall_velocity(Params<T> P, const V4<T>*
         ay += uj.y * wv;
         if (D == 3) az += uj.z * wv;
         sw += wv;
-    }
+    });
     T ux = 0, uy = 0, uz = 0;
     if (sw > 0) {
         ux = ax / sw;
@@ -475,7 +733,7 @@ template <class T, int D>
 __global__ void __launch_bounds__(128) k_forces_predict(Params<T> P, T dt, const V4<T>* __restrict__ pos,
                                                         const V4<T>* __restrict__ vel, const V4<T>* __restrict__ vt,
                                                         const T* __restrict__ rho, const int* __restrict__ nbr,
-                                                        const int* __restrict__ cnt, V4<T>* __restrict__ us,
+                                                        const int* __restrict__ cnt, int ncap, V4<T>* __restrict__ us,
                                                         V4<T>* __restrict__ rstar)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -488,8 +746,7 @@ __global__ void __launch_bounds__(128) k_forces_predict(Params<T> P, T dt, const
     const T avf2 = T(2) * P.alpha * P.h * P.c_ref;   // Pi = -avf phi / rhobar, rhobar = (rho_i + rho_j) / 2
     const T irhoi = frcp(rhoi);
     int n = cnt[i];
-    for (int k = 0; k < n; k++) {
-        int j = __ldg(nbr + (size_t)k * P.Ntot + i);
+    for_nbrs(nbr, ncap, i, n, [&](int j) {
         V4<T> xj = ld4(pos + j), uj = ld4(vel + j);
         T rhoj = __ldg(rho + j);
         T d[3], r, ri;
@@ -526,7 +783,7 @@ __global__ void __launch_bounds__(128) k_forces_predict(Params<T> P, T dt, const
             ay += mj * (ui.y * ai + uj.y * aj);
             if (D == 3) az += mj * (ui.z * ai + uj.z * aj);
         }
-    }
+    });
     us[i] = mk4<T>(ui.x + dt * ax, ui.y + dt * ay, D == 3 ? ui.z + dt * az : T(0), T(0));
     T rx = xi.x + dt * uti.x, ry = xi.y + dt * uti.y, rz = D == 3 ? xi.z + dt * uti.z : xi.z;
     if (P.per[0]) { if (rx >= P.hi[0]) rx -= P.L[0]; else if (rx < P.lo[0]) rx += P.L[0]; }
@@ -544,7 +801,7 @@ template <class T, int D>
 __global__ void __launch_bounds__(128) k_rhs_diag(Params<T> P, T inv_dt, const V4<T>* __restrict__ pos,
                                                   const V4<T>* __restrict__ us, const T* __restrict__ rho,
                                                   const uint8_t* __restrict__ fs, const int* __restrict__ nbr,
-                                                  const int* __restrict__ cnt, T* __restrict__ rhs,
+                                                  const int* __restrict__ cnt, int ncap, T* __restrict__ rhs,
                                                   T* __restrict__ diag, Ctl* ctl)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -554,8 +811,7 @@ __global__ void __launch_bounds__(128) k_rhs_diag(Params<T> P, T inv_dt, const V
         T rhoi = rho[i];
         T sr = 0, sd = 0;
         int n = cnt[i];
-        for (int k = 0; k < n; k++) {
-            int j = __ldg(nbr + (size_t)k * P.Ntot + i);
+        for_nbrs(nbr, ncap, i, n, [&](int j) {
             V4<T> xj = ld4(pos + j), uj = ld4(us + j);
             T rhoj = __ldg(rho + j);
             T d[3], r, ri;
@@ -567,7 +823,7 @@ __global__ void __launch_bounds__(128) k_rhs_diag(Params<T> P, T inv_dt, const V
             if (D == 3) ud += (ui.z - uj.z) * d[2];
             sr += mj * frcp(rhoj) * (ud * p4 * ri);                        // * (-dwk / dt) below
             sd += mj * (r * p4) * frcp((rhoi + rhoj) * (r2 + P.eta_h2));   // * 4 dwk / rho_i below
-        }
+        });
         sr *= -P.dwk * inv_dt;
         sd *= T(4) * P.dwk * frcp(rhoi);
         rhs[i] = sr;
@@ -587,7 +843,7 @@ __global__ void __launch_bounds__(128) k_rhs_diag(Params<T> P, T inv_dt, const V
 template <class T, int D>
 __global__ void __launch_bounds__(256) k_wall_pressure(Params<T> P, const V4<T>* __restrict__ pos,
                                                        const T* __restrict__ rho, const int* __restrict__ nbr,
-                                                       const int* __restrict__ cnt, T* pA, T* pB, const Ctl* ctl)
+                                                       const int* __restrict__ cnt, int ncap, T* pA, T* pB, const Ctl* ctl)
 {
     T* p = pA;
     if (ctl) {
@@ -600,9 +856,8 @@ __global__ void __launch_bounds__(256) k_wall_pressure(Params<T> P, const V4<T>*
     V4<T> xi = ld4(pos + i);
     T sw = 0, sp = 0, sx = 0, sy = 0, sz = 0;
     int n = cnt[i];
-    for (int k = 0; k < n; k++) {
-        int j = __ldg(nbr + (size_t)k * P.Ntot + i);
-        if (j >= P.Nf) continue;
+    for_nbrs(nbr, ncap, i, n, [&](int j) {
+        if (j >= P.Nf) return;
         V4<T> xj = ld4(pos + j);
         T d[3], r, ri;
         r_of(pair_vec<T, D>(P, xi, xj, d), r, ri);
@@ -613,7 +868,7 @@ __global__ void __launch_bounds__(256) k_wall_pressure(Params<T> P, const V4<T>*
         sy += rw * d[1];
         if (D == 3) sz += rw * d[2];
         sw += wv;
-    }
+    });
     T pw = 0;
     if (sw > T(0)) {
         T gr = P.g[0] * sx + P.g[1] * sy;
@@ -638,7 +893,7 @@ template <class T, int D>
 __global__ void __launch_bounds__(SWEEP_T) k_sweep(Params<T> P, const V4<T>* __restrict__ pos,
                                                    const T* __restrict__ rho, const T* __restrict__ rhs,
                                                    const T* __restrict__ diag, const uint8_t* __restrict__ fs,
-                                                   const int* __restrict__ nbr, const int* __restrict__ cnt,
+                                                   const int* __restrict__ nbr, const int* __restrict__ cnt, int ncap,
                                                    T* pA, T* pB, Ctl* ctl, double* __restrict__ partials,
                                                    double tol, int min_it, int max_it)
 {
@@ -658,9 +913,7 @@ __global__ void __launch_bounds__(SWEEP_T) k_sweep(Params<T> P, const V4<T>* __r
             T rhoi = rho[i];
             T s = 0;
             int n = cnt[i];
-            const int* __restrict__ row = nbr + i;
-            for (int k = 0; k < n; k++) {
-                int j = __ldg(row + (size_t)k * P.Ntot);
+            for_nbrs(nbr, ncap, i, n, [&](int j) {
                 V4<T> xj = ld4(pos + j);
                 T rhoj = __ldg(rho + j);
                 T pj = pin[j];
@@ -669,7 +922,7 @@ __global__ void __launch_bounds__(SWEEP_T) k_sweep(Params<T> P, const V4<T>* __r
                 r_of(r2, r, ri);
                 // fac_ij / (4 dW/dr-scale / rho_i): m_j r poly4(q) / ((rho_i + rho_j)(r^2 + eta h^2))
                 s += (xj.w * r * quintic4(r * P.inv_h) * pj) * frcp((rhoi + rhoj) * (r2 + P.eta_h2));
-            }
+            });
             s *= T(4) * P.dwk * frcp(rhoi);       // S_i = sum_j fac_ij p_j = -sum_j OD_ij p_j
             pnew = P.omega * (rhs[i] + s) * frcp(di) + (T(1) - P.omega) * pold;
         }
@@ -744,7 +997,7 @@ template <class T, int D>
 __global__ void __launch_bounds__(128) k_pgrad_correct(Params<T> P, T dt, const V4<T>* __restrict__ pos,
                                                        const T* __restrict__ rho, const T* __restrict__ p,
                                                        const V4<T>* __restrict__ us, const int* __restrict__ nbr,
-                                                       const int* __restrict__ cnt, V4<T>* __restrict__ vel)
+                                                       const int* __restrict__ cnt, int ncap, V4<T>* __restrict__ vel)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= P.Nf) return;
@@ -754,8 +1007,7 @@ __global__ void __launch_bounds__(128) k_pgrad_correct(Params<T> P, T dt, const 
     T pir = pi * irhoi * irhoi;
     T ax = 0, ay = 0, az = 0;
     int n = cnt[i];
-    for (int k = 0; k < n; k++) {
-        int j = __ldg(nbr + (size_t)k * P.Ntot + i);
+    for_nbrs(nbr, ncap, i, n, [&](int j) {
         V4<T> xj = ld4(pos + j);
         T rhoj = __ldg(rho + j), pj = __ldg(p + j);
         T d[3], r, ri;
@@ -767,7 +1019,7 @@ __global__ void __launch_bounds__(128) k_pgrad_correct(Params<T> P, T dt, const 
         ax -= f * d[0];
         ay -= f * d[1];
         if (D == 3) az -= f * d[2];
-    }
+    });
     ax *= P.dwk;
     ay *= P.dwk;
     az *= P.dwk;
@@ -807,7 +1059,7 @@ template <class T, int D>
 __global__ void __launch_bounds__(128) k_gtvf_substep(Params<T> P, T dtau, const V4<T>* __restrict__ rk,
                                                       V4<T>* __restrict__ rk1, V4<T>* __restrict__ vk,
                                                       V4<T>* __restrict__ dk, const T* __restrict__ p,
-                                                      const int* __restrict__ nbr, int stride,
+                                                      const int* __restrict__ nbr, int ncap,
                                                       const int* __restrict__ cnt, int first,
                                                       const V4<T>* __restrict__ rstar, int check, Ctl* ctl)
 {
@@ -816,9 +1068,7 @@ __global__ void __launch_bounds__(128) k_gtvf_substep(Params<T> P, T dtau, const
     V4<T> xi = ld4(rk + i);
     T ax = 0, ay = 0, az = 0;
     int n = cnt[i];
-    const int* __restrict__ row = nbr + i;
-    for (int k = 0; k < n; k++) {
-        int j = __ldg(row + (size_t)k * stride);
+    for_nbrs(nbr, ncap, i, n, [&](int j) {
         V4<T> xj = ld4(rk + j);
         T d[3], r, ri;
         r_of(pair_vec<T, D>(P, xi, xj, d), r, ri);
@@ -826,7 +1076,7 @@ __global__ void __launch_bounds__(128) k_gtvf_substep(Params<T> P, T dtau, const
         ax += f * d[0];
         ay += f * d[1];
         if (D == 3) az += f * d[2];
-    }
+    });
     T p0 = P.p_ref;
     if (P.pref_external) {
         T v = T(10) * fabs(p[i]);
@@ -877,7 +1127,7 @@ __global__ void k_advance(Params<T> P, T dt, const V4<T>* __restrict__ dK, const
 // ===========================================================================
 template <class T, int D>
 __global__ void k_normals_raw(Params<T> P, const V4<T>* __restrict__ pos, const T* __restrict__ rho,
-                              const int* __restrict__ nbr, const int* __restrict__ cnt, V4<T>* __restrict__ ns)
+                              const int* __restrict__ nbr, const int* __restrict__ cnt, int ncap, V4<T>* __restrict__ ns)
 {
     int w = blockIdx.x * blockDim.x + threadIdx.x;
     if (w >= P.Nw) return;
@@ -885,9 +1135,8 @@ __global__ void k_normals_raw(Params<T> P, const V4<T>* __restrict__ pos, const 
     V4<T> xi = ld4(pos + i);
     T ax = 0, ay = 0, az = 0;
     int n = cnt[i];
-    for (int k = 0; k < n; k++) {
-        int j = nbr[(size_t)k * P.Ntot + i];
-        if (j < P.Nf) continue;
+    for_nbrs(nbr, ncap, i, n, [&](int j) {
+        if (j < P.Nf) return;
         V4<T> xj = ld4(pos + j);
         T d[3];
         T r = my_sqrt(pair_vec<T, D>(P, xi, xj, d));
@@ -896,7 +1145,7 @@ __global__ void k_normals_raw(Params<T> P, const V4<T>* __restrict__ pos, const 
         ax -= v * d[0];
         ay -= v * d[1];
         if (D == 3) az -= v * d[2];
-    }
+    });
     T mag = my_sqrt(ax * ax + ay * ay + az * az);
     if (mag < T(1) / (T(4) * P.h)) ax = ay = az = T(0);
     else {
@@ -909,7 +1158,7 @@ __global__ void k_normals_raw(Params<T> P, const V4<T>* __restrict__ pos, const 
 
 template <class T, int D>
 __global__ void k_normals_smooth(Params<T> P, const V4<T>* __restrict__ pos, const T* __restrict__ rho,
-                                 const int* __restrict__ nbr, const int* __restrict__ cnt,
+                                 const int* __restrict__ nbr, const int* __restrict__ cnt, int ncap,
                                  const V4<T>* __restrict__ ns, V4<T>* __restrict__ nrm)
 {
     int w = blockIdx.x * blockDim.x + threadIdx.x;
@@ -920,9 +1169,8 @@ __global__ void k_normals_smooth(Params<T> P, const V4<T>* __restrict__ pos, con
     V4<T> n0 = ns[w];
     T ax = v0 * n0.x, ay = v0 * n0.y, az = v0 * n0.z;
     int n = cnt[i];
-    for (int k = 0; k < n; k++) {
-        int j = nbr[(size_t)k * P.Ntot + i];
-        if (j < P.Nf) continue;
+    for_nbrs(nbr, ncap, i, n, [&](int j) {
+        if (j < P.Nf) return;
         V4<T> xj = ld4(pos + j);
         T d[3];
         T r = my_sqrt(pair_vec<T, D>(P, xi, xj, d));
@@ -931,7 +1179,7 @@ __global__ void k_normals_smooth(Params<T> P, const V4<T>* __restrict__ pos, con
         ax += v * nj.x;
         ay += v * nj.y;
         az += v * nj.z;
-    }
+    });
     // R17: a smoothed vector shorter than 0.01 (layers cancelling) has no direction -> 0
     T mag = my_sqrt(ax * ax + ay * ay + az * az);
     if (mag >= T(0.01)) {

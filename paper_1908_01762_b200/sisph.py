@@ -41,7 +41,7 @@ class sisph_params(C.Structure):
         ("pgrad", C.c_int), ("pref_external", C.c_int), ("ustar_noslip", C.c_int),
         ("clamp_wall_p", C.c_int), ("K", C.c_int), ("min_iter", C.c_int), ("max_iter", C.c_int),
         ("tol", C.c_double), ("wall_rho_summation", C.c_int), ("nbr_cap", C.c_int),
-        ("device", C.c_int), ("stream", C.c_void_p),
+        ("device", C.c_int), ("stream", C.c_void_p), ("rebuild_mode", C.c_int),
     ]
 
 
@@ -49,7 +49,8 @@ class sisph_step_report(C.Structure):
     _fields_ = [("dt", C.c_double), ("iters", C.c_int), ("residual", C.c_double),
                 ("lambda_", C.c_double), ("ms_predict", C.c_double), ("ms_solve", C.c_double),
                 ("ms_correct", C.c_double), ("pairs", C.c_int64), ("max_neighbors", C.c_int),
-                ("ms_sweeps", C.c_double), ("sweeps_timed", C.c_int), ("launches", C.c_int64)]
+                ("ms_sweeps", C.c_double), ("sweeps_timed", C.c_int), ("launches", C.c_int64),
+                ("single_build", C.c_int), ("skin_radius", C.c_double)]
 
 
 class SisphError(RuntimeError):

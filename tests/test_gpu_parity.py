@@ -77,6 +77,47 @@ def test_neighbor_sets_with_exact_ties_fp64():
     assert np.median(interior) == 24
 
 
+def _moving(case, frac=0.4, seed=5):
+    """Transport velocities of |u~| ~ frac h / dt on the fluid: a skin of ~2 frac h."""
+    rng = np.random.default_rng(seed)
+    ut = np.zeros((case.n, case.dim))
+    f = case.tag == 0
+    ut[f] = rng.uniform(-1, 1, (f.sum(), case.dim)) * frac * case.h / case.dt / np.sqrt(case.dim)
+    return ut
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_rstar_sets_of_the_single_build(name):
+    """A9 by the single build (R3): the r* sets filtered out of the loose r^n
+    list equal the oracle's exact sets at r*, bit for bit."""
+    case = CASES[name]
+    sim = gpu_sim(case)
+    sim.set("TRANSPORT_VELOCITY", _moving(case))
+    sim.predict(case.dt)
+    xs = sim.get("RSTAR")
+    off, ids = sim.neighbors()
+    roff, rids = oracle.neighbors(oracle.case_cfg(case), xs)
+    assert np.array_equal(off, roff)
+    assert np.array_equal(ids, rids)
+
+
+@pytest.mark.parametrize("name", ["tgv2d_f64", "db2d_f64", "tgv3d_f64", "db3d_f64", "db3d_f32"])
+def test_single_build_equals_two_builds(name):
+    case = CASES[name]
+    a, b = gpu_sim(case), gpu_sim(case, rebuild_mode=1)
+    # db3d_f64's periodic y axis has 3.3 cells of 3h: only a thin skin keeps 3 cells
+    ut = _moving(case, 0.05 if name == "db3d_f64" else 0.3)
+    for s in (a, b):
+        s.set("TRANSPORT_VELOCITY", ut)
+    ra, rb = a.step(case.dt), b.step(case.dt)
+    assert ra.single_build == 1 and rb.single_build == 0
+    assert ra.iters == rb.iters and ra.pairs == rb.pairs
+    prec = _prec(case)
+    for fld in ("PRESSURE", "VELOCITY", "POSITION", "TRANSPORT_VELOCITY"):
+        ref = b.get(fld)
+        assert_close(fld, a.get(fld), ref, prec, scale=max(np.abs(ref).max(), 1e-3))
+
+
 # ------------------------------------------------------------------ A6-A11
 @pytest.mark.parametrize("name", list(CASES))
 def test_predict_parity(name):
