@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--matrix-free", action="store_true",
+                    help="ablation: the sweep recomputes fac_ij every sweep (PAPER.md:785-801)")
     return ap.parse_args()
 
 
@@ -224,7 +226,8 @@ def run_sisph(args):
 
     case, desc = workload(args.workload)
     stream = torch.cuda.current_stream()
-    sim = Simulation.from_case(case, stream=stream.cuda_stream, device=local)
+    sim = Simulation.from_case(case, stream=stream.cuda_stream, device=local,
+                               matrix_free=1 if args.matrix_free else 0)
     sim.set_timing(True)
     nf, n = sim.n_fluid, sim.n
     for _ in range(args.warmup):
@@ -246,7 +249,15 @@ def run_sisph(args):
     ms_sw = sum(r.ms_sweeps for r in reps)
     n_sw = sum(r.sweeps_timed for r in reps)
     pairs = reps[-1].pairs
-    b_per = 24 * n + 17 * nf + 4 * pairs    # every state array once + the neighbour list
+    tb = 4 if case.params["precision"] == 32 else 8
+    if args.matrix_free:
+        # pos (x, y, z, m), rho, p^k of every particle; rhs, diag, cnt, p^{k+1} (+ 1-byte fs) of
+        # every fluid particle; the 4-byte neighbour index of every pair
+        b_per = (6 * tb) * n + (3 * tb + 5) * nf + 4 * pairs
+    else:
+        # p^k of every particle; rho, rhs, diag, cnt, p^{k+1} (+ fs) of every fluid particle;
+        # per pair the 4-byte index and the stored factor of fac_ij
+        b_per = tb * n + (4 * tb + 5) * nf + (4 + tb) * pairs
     avg_s = ms_sw / max(n_sw, 1) / 1e3
     achieved = b_per / avg_s / 1e9
     peak, peak_src = peaks()
@@ -265,7 +276,9 @@ def run_sisph(args):
         "ms_per_step_phases": {"predict": sum(r.ms_predict for r in reps) / args.steps,
                                "solve": ms_solve / args.steps,
                                "correct": sum(r.ms_correct for r in reps) / args.steps},
-        "roofline": {"kernel": "k_sweep (A12 Jacobi sweep + fused residual reduction)", "bound": "hbm",
+        "roofline": {"kernel": "k_sweep (A12 Jacobi sweep + fused residual reduction, "
+                               + ("fac_ij recomputed per sweep)" if args.matrix_free else "stored fac_ij streamed)"),
+                     "bound": "hbm",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": sweep_traffic(), "bytes_per_launch": b_per, "pairs_per_launch": pairs,
                      "avg_launch_us": avg_s * 1e6, "launches_timed": n_sw, "peak_source": peak_src},

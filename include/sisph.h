@@ -81,6 +81,10 @@ typedef struct {
     int rebuild_mode;       /* 0 (default): one build per step at r^n with a skin of
                                2 dt max|u~| and the r* sets filtered out of it (R3) when the
                                skin fits the grid; 1: two exact builds (at r^n and r*) */
+    int matrix_free;        /* 0 (default): A11 stores the per-pair factor of fac_ij (eq:coeff)
+                               once per solve and every sweep streams it (particles do not move
+                               during the iterations); 1: every sweep recomputes it from
+                               the positions, as the paper's listing */
 } sisph_params;
 
 /* Per-step report (sisph_step).  Timings are device milliseconds measured

@@ -102,7 +102,9 @@ template <class T, int D> struct Engine : EngineBase {
     int *wperm_s = nullptr, *wstart_s = nullptr;
     int wnc_s[3] = {-1, -1, -1};
     Params<T> PS;
-    int rebuild_mode = 0;   // 0: single build + filter when the skin fits, 1: always two exact builds
+    int rebuild_mode = 0;
+    int matrix_free = 0;    // 1: the sweep recomputes fac_ij from positions; 0: A11 stores it per pair
+    T* coef = nullptr;      // stored per-pair part of fac_ij, blocked-ELL layout of nbr (fluid rows)   // 0: single build + filter when the skin fits, 1: always two exact builds
     bool skin_used = false;
     double skin_radius = 0;
     double extent = 0;      // max |coordinate| of the domain (rounding margin of the skin)
@@ -120,7 +122,7 @@ template <class T, int D> struct Engine : EngineBase {
         void* ptrs[] = {pos, pos_alt, vel, vel_alt, us, us_alt, vt, vt_alt, rn, rstar, nrm, nstmp, rkA, rkB, vk, dk,
                         p, p_alt, rho, rho_alt, rhs, diag, fs, fs_alt, pid, pid_alt, keys, rank, perm0, perm,
                         ccount, fstart, wstart, bsum, nbr, cnt, ctl, partials, dtmp, nbr_in, cnt_in,
-                        nbs, cnt_s, wperm_s, wstart_s};
+                        nbs, cnt_s, wperm_s, wstart_s, coef};
         if (st) cudaStreamSynchronize(st);
         for (void* q : ptrs)
             if (q) cudaFree(q);
@@ -224,6 +226,7 @@ template <class T, int D> struct Engine : EngineBase {
         P.clamp_wall_p = prm->clamp_wall_p;
         P.wall_rho_summation = prm->wall_rho_summation;
         rebuild_mode = prm->rebuild_mode;
+        matrix_free = prm->matrix_free;
         for (int a = 0; a < D; a++) extent = std::max(extent, std::max(fabs(dom->lo[a]), fabs(dom->hi[a])));
         min_iter = prm->min_iter;
         max_iter = prm->max_iter;
@@ -324,10 +327,16 @@ template <class T, int D> struct Engine : EngineBase {
     {
         if (nbr) cudaFree(nbr);
         if (nbr_in) cudaFree(nbr_in);
+        if (coef) cudaFree(coef);
         nbr = nbr_in = nullptr;
+        coef = nullptr;
         int rc = 0;
         nbr = dalloc<int>((size_t)cap * rows32(Ntot), err, rc);
         if (rc) return rc;
+        if (!matrix_free) {
+            coef = dalloc<T>((size_t)cap * rows32(Nf), err, rc);
+            if (rc) return rc;
+        }
         P.cap = cap;
         if (use_inner) {
             // the inner list holds a subset of each fluid row: the full capacity is an upper bound
@@ -634,7 +643,7 @@ template <class T, int D> struct Engine : EngineBase {
         if (Nw) ++nlaunch, k_wall_velocity<T, D><<<nblk(Nw, 256), 256, 0, st>>>(P, pos, nbr, cnt, P.cap, nrm, us, P.ustar_noslip ? 0 : 1);
         // A11
         SCK(cudaMemsetAsync(&ctl->lambda_bits, 0, sizeof(unsigned long long), st));
-        if (Nf) ++nlaunch, k_rhs_diag<T, D><<<nblk(Nf, 128), 128, 0, st>>>(P, (T)(1.0 / dt), pos, us, rho, fs, nbr, cnt, P.cap, rhs, diag, ctl);
+        if (Nf) ++nlaunch, k_rhs_diag<T, D><<<nblk(Nf, 128), 128, 0, st>>>(P, (T)(1.0 / dt), pos, us, rho, fs, nbr, cnt, P.cap, rhs, diag, coef, ctl);
         SCK(cudaGetLastError());
         phase = PREDICTED;
         return SISPH_OK;
@@ -658,8 +667,12 @@ template <class T, int D> struct Engine : EngineBase {
                 }
                 SCK(cudaEventRecord(sev[2 * nrec], st));
             }
-            ++nlaunch, k_sweep<T, D><<<nblk(Nf, SWEEP_T), SWEEP_T, 0, st>>>(P, pos, rho, rhs, diag, fs, nbr, cnt, P.cap, p, p_alt, ctl,
-                                                                  partials, tl, mi, mx);
+            if (coef)
+                ++nlaunch, k_sweep<T, D, true><<<nblk(Nf, SWEEP_T), SWEEP_T, 0, st>>>(
+                               P, pos, rho, rhs, diag, fs, nbr, cnt, P.cap, coef, p, p_alt, ctl, partials, tl, mi, mx);
+            else
+                ++nlaunch, k_sweep<T, D, false><<<nblk(Nf, SWEEP_T), SWEEP_T, 0, st>>>(
+                               P, pos, rho, rhs, diag, fs, nbr, cnt, P.cap, nullptr, p, p_alt, ctl, partials, tl, mi, mx);
             if (rec) {
                 SCK(cudaEventRecord(sev[2 * nrec + 1], st));
                 nrec++;

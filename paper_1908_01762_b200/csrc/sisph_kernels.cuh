@@ -248,6 +248,38 @@ __device__ __forceinline__ void for_nbrs(const int* __restrict__ nbr, int cap, i
     }
 }
 
+// same, also passing the entry number k
+template <class F>
+__device__ __forceinline__ void for_nbrs_k(const int* __restrict__ nbr, int cap, int i, int n, F&& f)
+{
+    const int4* __restrict__ q = reinterpret_cast<const int4*>(nbr + nb_base(i, cap));
+    for (int c = 0; c < n; c += 4) {
+        const int4 v = __ldg(q + (size_t)(c >> 2) * 32);
+        f(v.x, c);
+        if (c + 1 < n) f(v.y, c + 1);
+        if (c + 2 < n) f(v.z, c + 2);
+        if (c + 3 < n) f(v.w, c + 3);
+    }
+}
+__device__ __forceinline__ size_t nb_off(int k) { return ((size_t)(k >> 2) << 7) + (k & 3); }
+// one 4-entry chunk of a per-pair array in the same layout (16 / 32 bytes)
+__device__ __forceinline__ void ld_chunk4(const float* p, float (&f)[4])
+{
+    const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+    f[0] = v.x;
+    f[1] = v.y;
+    f[2] = v.z;
+    f[3] = v.w;
+}
+__device__ __forceinline__ void ld_chunk4(const double* p, double (&f)[4])
+{
+    const double2 a = __ldg(reinterpret_cast<const double2*>(p)), b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+    f[0] = a.x;
+    f[1] = a.y;
+    f[2] = b.x;
+    f[3] = b.y;
+}
+
 // a builder lane's append cursor into its row
 struct NbCursor {
     int* row;   // nbr + nb_base(i, cap)
@@ -802,7 +834,7 @@ __global__ void __launch_bounds__(128) k_rhs_diag(Params<T> P, T inv_dt, const V
                                                   const V4<T>* __restrict__ us, const T* __restrict__ rho,
                                                   const uint8_t* __restrict__ fs, const int* __restrict__ nbr,
                                                   const int* __restrict__ cnt, int ncap, T* __restrict__ rhs,
-                                                  T* __restrict__ diag, Ctl* ctl)
+                                                  T* __restrict__ diag, T* __restrict__ coef, Ctl* ctl)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     double lam = 0.0;
@@ -811,7 +843,8 @@ __global__ void __launch_bounds__(128) k_rhs_diag(Params<T> P, T inv_dt, const V
         T rhoi = rho[i];
         T sr = 0, sd = 0;
         int n = cnt[i];
-        for_nbrs(nbr, ncap, i, n, [&](int j) {
+        T* __restrict__ crow = coef ? coef + nb_base(i, ncap) : nullptr;
+        for_nbrs_k(nbr, ncap, i, n, [&](int j, int k) {
             V4<T> xj = ld4(pos + j), uj = ld4(us + j);
             T rhoj = __ldg(rho + j);
             T d[3], r, ri;
@@ -822,7 +855,11 @@ __global__ void __launch_bounds__(128) k_rhs_diag(Params<T> P, T inv_dt, const V
             T ud = (ui.x - uj.x) * d[0] + (ui.y - uj.y) * d[1];
             if (D == 3) ud += (ui.z - uj.z) * d[2];
             sr += mj * frcp(rhoj) * (ud * p4 * ri);                        // * (-dwk / dt) below
-            sd += mj * (r * p4) * frcp((rhoi + rhoj) * (r2 + P.eta_h2));   // * 4 dwk / rho_i below
+            const T f = mj * (r * p4) * frcp((rhoi + rhoj) * (r2 + P.eta_h2));   // * 4 dwk / rho_i below
+            sd += f;
+            // stored per-pair part of fac_ij (particles do not move during the solve):
+            // the sweep then reads it instead of recomputing it (same value, same layout as nbr)
+            if (crow) crow[nb_off(k)] = f;
         });
         sr *= -P.dwk * inv_dt;
         sd *= T(4) * P.dwk * frcp(rhoi);
@@ -889,13 +926,17 @@ __global__ void __launch_bounds__(256) k_wall_pressure(Params<T> P, const V4<T>*
 // ===========================================================================
 constexpr int SWEEP_T = 256;
 
-template <class T, int D>
+// STORED: the per-pair part of fac_ij written by k_rhs_diag is streamed
+// alongside the neighbour index (an ELL SpMV: 4 + 4 bytes per pair from HBM,
+// p_j gathered); otherwise it is recomputed from the positions every sweep,
+// as the paper's listing does.
+template <class T, int D, bool STORED>
 __global__ void __launch_bounds__(SWEEP_T) k_sweep(Params<T> P, const V4<T>* __restrict__ pos,
                                                    const T* __restrict__ rho, const T* __restrict__ rhs,
                                                    const T* __restrict__ diag, const uint8_t* __restrict__ fs,
                                                    const int* __restrict__ nbr, const int* __restrict__ cnt, int ncap,
-                                                   T* pA, T* pB, Ctl* ctl, double* __restrict__ partials,
-                                                   double tol, int min_it, int max_it)
+                                                   const T* __restrict__ coef, T* pA, T* pB, Ctl* ctl,
+                                                   double* __restrict__ partials, double tol, int min_it, int max_it)
 {
     if (ctl->done) return;
     const int kit = ctl->iter;
@@ -909,20 +950,36 @@ __global__ void __launch_bounds__(SWEEP_T) k_sweep(Params<T> P, const V4<T>* __r
         T pnew = T(0);
         T di = diag[i];
         if (!fs[i] && di != T(0)) {
-            V4<T> xi = ld4(pos + i);
             T rhoi = rho[i];
             T s = 0;
             int n = cnt[i];
-            for_nbrs(nbr, ncap, i, n, [&](int j) {
-                V4<T> xj = ld4(pos + j);
-                T rhoj = __ldg(rho + j);
-                T pj = pin[j];
-                T d[3], r, ri;
-                T r2 = pair_vec<T, D>(P, xi, xj, d);
-                r_of(r2, r, ri);
-                // fac_ij / (4 dW/dr-scale / rho_i): m_j r poly4(q) / ((rho_i + rho_j)(r^2 + eta h^2))
-                s += (xj.w * r * quintic4(r * P.inv_h) * pj) * frcp((rhoi + rhoj) * (r2 + P.eta_h2));
-            });
+            if (STORED) {
+                const size_t b = nb_base(i, ncap);
+                const int4* __restrict__ qi = reinterpret_cast<const int4*>(nbr + b);
+                for (int c = 0; c < n; c += 4) {
+                    const size_t o = (size_t)(c >> 2) * 32;
+                    const int4 v = __ldg(qi + o);
+                    T f[4];
+                    ld_chunk4(coef + b + (o << 2), f);
+                    s += f[0] * pin[v.x];
+                    if (c + 1 < n) s += f[1] * pin[v.y];
+                    if (c + 2 < n) s += f[2] * pin[v.z];
+                    if (c + 3 < n) s += f[3] * pin[v.w];
+                }
+            } else {
+                V4<T> xi = ld4(pos + i);
+                for_nbrs(nbr, ncap, i, n, [&](int j) {
+                    V4<T> xj = ld4(pos + j);
+                    T rhoj = __ldg(rho + j);
+                    T pj = pin[j];
+                    T d[3], r, ri;
+                    T r2 = pair_vec<T, D>(P, xi, xj, d);
+                    r_of(r2, r, ri);
+                    // fac_ij / (4 dW/dr-scale / rho_i): m_j r poly4(q) / ((rho_i + rho_j)(r^2 + eta h^2))
+                    // (the expression of k_rhs_diag's stored value, so both modes agree bit for bit)
+                    s += xj.w * (r * quintic4(r * P.inv_h)) * frcp((rhoi + rhoj) * (r2 + P.eta_h2)) * pj;
+                });
+            }
             s *= T(4) * P.dwk * frcp(rhoi);       // S_i = sum_j fac_ij p_j = -sum_j OD_ij p_j
             pnew = P.omega * (rhs[i] + s) * frcp(di) + (T(1) - P.omega) * pold;
         }

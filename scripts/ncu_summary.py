@@ -55,7 +55,11 @@ if __name__ == "__main__":
     out = sys.argv[1]
     allines = []
     for rep in sys.argv[2:]:
-        name, lines, extra = summarise(rep)
+        try:
+            name, lines, extra = summarise(rep)
+        except (ValueError, IndexError) as e:
+            print(f"skip {rep}: {e}", file=sys.stderr)
+            continue
         allines += [f"# {rep}"] + lines + [""]
         if "k_sweep" in name and "dram__bytes_read.sum" in extra:
             b = to_bytes(*extra["dram__bytes_read.sum"]) + to_bytes(*extra["dram__bytes_write.sum"])

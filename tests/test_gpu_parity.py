@@ -163,6 +163,24 @@ def test_solve_parity_fp64_iteration_count(name):
     assert_close("p", sim.get("PRESSURE")[f], o.get("p")[f], 64)
 
 
+@pytest.mark.parametrize("name", ["tgv2d_f64", "hydro_f64", "db3d_f64", "tgv3d_f32", "db2d_f32"])
+def test_stored_coefficients_equal_matrix_free(name):
+    """The sweep streaming the per-pair factor stored by A11 and the sweep
+    recomputing it from the positions take the same decisions
+    and agree to rounding (the factor is the same expression)."""
+    case = CASES[name]
+    a, b = gpu_sim(case), gpu_sim(case, matrix_free=1)
+    for s in (a, b):
+        s.predict(case.dt)
+    tol, mx = case.params["tol"], case.params["max_iter"]
+    ia, ra = a.ppe_solve(tol, mx)
+    ib, rb = b.ppe_solve(tol, mx)
+    assert ia == ib
+    assert ra == pytest.approx(rb, rel=1e-12, abs=1e-300)
+    pa, pb = a.get("PRESSURE"), b.get("PRESSURE")
+    assert np.abs(pa - pb).max() <= 1e-13 * max(np.abs(pb).max(), 1e-300) * (1 if _prec(case) == 64 else 1e7)
+
+
 @pytest.mark.parametrize("name", list(CASES))
 def test_fixed_sweeps_parity(name):
     # tol = 0, max_iter = S: both sides do exactly S sweeps (SURVEY §8(c) fp32 contract)
