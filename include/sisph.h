@@ -190,6 +190,13 @@ int sisph_get_order(sisph_t* s, int64_t* ids, int64_t n);
  * are written and SISPH_EINVAL is returned. */
 int sisph_get_neighbors(sisph_t* s, int64_t* offsets, int64_t* ids, int64_t cap, int64_t* total);
 
+/* The neighbour sets of the m particles with creation ids which[0 .. m) only
+ * (for large problems): CSR offsets[m + 1], ids[*total], rows in the order of
+ * which, each sorted by id.  Errors as sisph_get_neighbors; an id outside
+ * [0, n) is SISPH_EINVAL. */
+int sisph_get_neighbors_of(sisph_t* s, const int64_t* which, int64_t m, int64_t* offsets, int64_t* ids,
+                           int64_t cap, int64_t* total);
+
 /* Counts: particles, fluid particles, wall particles. */
 int sisph_get_counts(const sisph_t* s, int64_t* n, int64_t* n_fluid, int64_t* n_wall);
 

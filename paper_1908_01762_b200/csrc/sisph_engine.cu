@@ -55,6 +55,8 @@ struct EngineBase {
     virtual int set_field(int f, const double* in, int64_t count) = 0;
     virtual int get_order(int64_t* ids) = 0;
     virtual int get_neighbors(int64_t* off, int64_t* ids, int64_t cap, int64_t* total) = 0;
+    virtual int get_neighbors_of(const int64_t* which, int64_t m, int64_t* off, int64_t* ids, int64_t cap,
+                                 int64_t* total) = 0;
     virtual int sync() = 0;
     int timing = 0;
     int64_t nlaunch = 0;  // kernel launches issued (all entry points)
@@ -1008,6 +1010,48 @@ template <class T, int D> struct Engine : EngineBase {
         return SISPH_OK;
     }
 
+    // rows of the listed particles only (large problems): each row's 16-byte
+    // chunks sit 512 bytes apart in the blocked layout -> one 2D copy per row
+    int get_neighbors_of(const int64_t* which, int64_t m, int64_t* off, int64_t* ids, int64_t cap,
+                         int64_t* total) override
+    {
+        std::vector<int> hc(Ntot), hp(Ntot);
+        SCK(cudaMemcpyAsync(hc.data(), cnt, Ntot * sizeof(int), cudaMemcpyDeviceToHost, st));
+        SCK(cudaMemcpyAsync(hp.data(), pid, Ntot * sizeof(int), cudaMemcpyDeviceToHost, st));
+        SCK(cudaStreamSynchronize(st));
+        std::vector<int> slot_of(n);
+        for (int s = 0; s < Ntot; s++) slot_of[hp[s]] = s;
+        off[0] = 0;
+        for (int64_t q = 0; q < m; q++) {
+            if (which[q] < 0 || which[q] >= n) {
+                err = "get_neighbors_of: id out of range";
+                return SISPH_EINVAL;
+            }
+            off[q + 1] = off[q] + hc[slot_of[which[q]]];
+        }
+        *total = off[m];
+        if (cap < off[m]) {
+            err = "get_neighbors_of: cap < total";
+            return SISPH_EINVAL;
+        }
+        const int nch = P.cap / 4;
+        std::vector<int> rows((size_t)m * P.cap);
+        for (int64_t q = 0; q < m; q++) {
+            const int s = slot_of[which[q]];
+            const size_t b = (size_t)(s >> 5) * ((size_t)P.cap << 5) + ((s & 31) << 2);
+            SCK(cudaMemcpy2DAsync(rows.data() + (size_t)q * P.cap, 16, nbr + b, 512, 16, nch, cudaMemcpyDeviceToHost,
+                                  st));
+        }
+        SCK(cudaStreamSynchronize(st));
+        for (int64_t q = 0; q < m; q++) {
+            const int s = slot_of[which[q]];
+            int64_t* row = ids + off[q];
+            for (int k = 0; k < hc[s]; k++) row[k] = hp[rows[(size_t)q * P.cap + k]];
+            std::sort(row, row + hc[s]);
+        }
+        return SISPH_OK;
+    }
+
     int sync() override
     {
         SCK(cudaStreamSynchronize(st));
@@ -1187,6 +1231,13 @@ int sisph_get_neighbors(sisph_t* s, int64_t* offsets, int64_t* ids, int64_t cap,
     CHK_HANDLE(s);
     if (!offsets || !total) return fail_thread(SISPH_EINVAL, "NULL offsets/total");
     return s->e->get_neighbors(offsets, ids, cap, total);
+}
+int sisph_get_neighbors_of(sisph_t* s, const int64_t* ids_in, int64_t m, int64_t* offsets, int64_t* ids,
+                           int64_t cap, int64_t* total)
+{
+    CHK_HANDLE(s);
+    if (!ids_in || m < 0 || !offsets || !total) return fail_thread(SISPH_EINVAL, "NULL or bad argument");
+    return s->e->get_neighbors_of(ids_in, m, offsets, ids, cap, total);
 }
 int sisph_get_counts(const sisph_t* s, int64_t* n, int64_t* n_fluid, int64_t* n_wall)
 {

@@ -24,7 +24,8 @@ VECTOR_FIELDS = {"POSITION", "VELOCITY", "TRANSPORT_VELOCITY", "USTAR", "RSTAR",
 
 EXPORTED = ["sisph_params_default", "sisph_create", "sisph_destroy", "sisph_build_neighbors",
             "sisph_predict", "sisph_ppe_solve", "sisph_correct", "sisph_step", "sisph_get_field",
-            "sisph_set_field", "sisph_get_order", "sisph_get_neighbors", "sisph_get_counts",
+            "sisph_set_field", "sisph_get_order", "sisph_get_neighbors", "sisph_get_neighbors_of",
+            "sisph_get_counts",
             "sisph_set_timing", "sisph_sync", "sisph_last_error"]
 
 
@@ -84,6 +85,7 @@ def lib():
         L.sisph_set_field.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64]
         L.sisph_get_order.argtypes = [C.c_void_p, i64p, C.c_int64]
         L.sisph_get_neighbors.argtypes = [C.c_void_p, i64p, i64p, C.c_int64, i64p]
+        L.sisph_get_neighbors_of.argtypes = [C.c_void_p, i64p, C.c_int64, i64p, i64p, C.c_int64, i64p]
         L.sisph_get_counts.argtypes = [C.c_void_p, i64p, i64p, i64p]
         L.sisph_set_timing.argtypes = [C.c_void_p, C.c_int]
         L.sisph_sync.argtypes = [C.c_void_p]
@@ -224,4 +226,18 @@ class Simulation:
         _check(L.sisph_get_neighbors(self._h, off.ctypes.data_as(C.POINTER(C.c_int64)),
                                      ids.ctypes.data_as(C.POINTER(C.c_int64)), ids.size, C.byref(tot)), self._h)
         del rc
+        return off, ids[: tot.value]
+
+    def neighbors_of(self, which):
+        """Neighbour sets (sorted ids) of the particles with creation ids `which`."""
+        which = np.ascontiguousarray(which, np.int64)
+        m = which.size
+        off = np.zeros(m + 1, np.int64)
+        tot = C.c_int64()
+        L = lib()
+        wp = which.ctypes.data_as(C.POINTER(C.c_int64))
+        L.sisph_get_neighbors_of(self._h, wp, m, off.ctypes.data_as(C.POINTER(C.c_int64)), None, 0, C.byref(tot))
+        ids = np.empty(max(tot.value, 1), np.int64)
+        _check(L.sisph_get_neighbors_of(self._h, wp, m, off.ctypes.data_as(C.POINTER(C.c_int64)),
+                                        ids.ctypes.data_as(C.POINTER(C.c_int64)), ids.size, C.byref(tot)), self._h)
         return off, ids[: tot.value]

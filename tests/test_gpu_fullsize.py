@@ -1,0 +1,89 @@
+"""Parity at BASELINE.json's full size, in the configuration bench.py times.
+
+The workload is the 3D dam-break per-GPU slab of configs[4] (2 097 152 fluid +
+218 496 wall particles, fp32, single per-step build, stored PPE coefficients).
+Two free-running GPU steps give a state with non-trivial u~; from that state
+one step runs through the C ABI split (predict / 2 fixed sweeps / correct),
+and the fp64 oracle (oracle/, all host cores) runs the same step from the
+GPU's own inputs.  Every particle's fields are compared with the north_star
+fp32 tolerance; the neighbour sets at r* of a seeded sample of rows are
+compared bit for bit against the oracle's cell-list search.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from parity_util import assert_close, gpu_sim, oracle_from_gpu
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def c5():
+    case = synth.dambreak3d()
+    sim = gpu_sim(case)
+    for _ in range(2):
+        sim.step(case.dt)
+    o = oracle_from_gpu(case, sim)
+    return case, sim, o
+
+
+def test_c5_full_size_step(c5):
+    case, sim, o = c5
+    f, w = case.tag == 0, case.tag == 1
+    dt = case.dt
+    sim.predict(dt)
+    o.predict(dt)
+    # A6-A11 on every particle
+    assert_close("rho", sim.get("DENSITY"), o.get("rho"), 32)
+    rho_o = o.get("rho")
+    haz = np.abs(rho_o / case.params["rho0"] - case.params["fs_ratio"]) < 1e-5
+    assert np.array_equal(sim.get("FREE_SURFACE")[~haz], o.get("fs")[~haz])
+    xs = sim.get("RSTAR")
+    assert_close("rstar", xs[f], o.get("xs")[f], 32, scale=np.abs(case.x).max())
+    us_o = o.get("us")
+    assert_close("ustar", sim.get("USTAR"), us_o, 32, scale=max(np.abs(us_o).max(), 1e-3))
+    assert_close("ghost u", sim.get("VELOCITY")[w], o.get("u")[w], 32,
+                 scale=max(np.abs(o.get("u")).max(), 1e-3))
+    assert_close("diag", sim.get("DIAG")[f], o.get("diag")[f], 32)
+    assert_close("rhs", sim.get("RHS")[f], o.get("rhs")[f], 32, scale=max(np.abs(o.get("rhs")).max(), 1e-9))
+    # A9: neighbour sets at r* of sampled rows (fluid and wall), bit-exact
+    rng = np.random.default_rng(7)
+    which = np.sort(np.concatenate([rng.choice(np.flatnonzero(f), 3000, replace=False),
+                                    rng.choice(np.flatnonzero(w), 500, replace=False)]))
+    off, ids = sim.neighbors_of(which)
+    roff, rids = oracle.neighbors(oracle.case_cfg(case), xs, dests=which)
+    assert np.array_equal(off, roff)
+    assert np.array_equal(ids, rids)
+    # A12: two sweeps (fixed work on both sides: tol 0, max_iter 2)
+    it_g, _ = sim.ppe_solve(0.0, 2)
+    it_o, _, _ = o.solve(0.0, 2)
+    assert it_g == it_o == 2
+    p_o = o.get("p")
+    assert_close("p", sim.get("PRESSURE"), p_o, 32)
+    # A13-A15
+    sim.correct(dt)
+    o.correct(dt)
+    u_o = o.get("u")[f]
+    assert_close("u", sim.get("VELOCITY")[f], u_o, 32, scale=max(np.abs(u_o).max(), 1e-3))
+    ut_o = o.get("ut")[f]
+    assert_close("ut", sim.get("TRANSPORT_VELOCITY")[f], ut_o, 32, scale=max(np.abs(ut_o).max(), 1e-3))
+    assert_close("x", sim.get("POSITION")[f], o.get("x")[f], 32, scale=np.abs(case.x).max())
+
+
+def test_c5_full_size_solve_to_tolerance(c5):
+    """The configured solve (tol 1e-2) at full size: GPU and oracle stop at the
+    same sweep (the residual is reduced in fp64 on both sides; a residual within
+    1e-6 relative of the tolerance is reported as a hazard, not compared)."""
+    case, sim, o = c5
+    from parity_util import resync
+    resync(case, sim, o)
+    sim.predict(case.dt)
+    o.predict(case.dt)
+    tol = case.params["tol"]
+    it_g, res_g = sim.ppe_solve(tol, 1000)
+    it_o, res_o, _ = o.solve(tol, 1000)
+    if abs(res_o - tol) > 1e-6 * tol:
+        assert it_g == it_o, (it_g, it_o, res_g, res_o)
+    assert res_g == pytest.approx(res_o, rel=1e-3, abs=1e-7)
