@@ -102,6 +102,9 @@ typedef struct {
     int64_t launches;       /* kernel launches this step issued (speculative no-op sweeps included) */
     int single_build;       /* 1 if this step used the single build + filter (R3) */
     double skin_radius;     /* loose radius 3h + skin of that build (0 otherwise) */
+    int64_t n_owned_fluid;  /* fluid particles this handle owns (all of them on one GPU) */
+    int64_t n_ghost_fluid;  /* halo copies of neighbour slabs' fluid (slab ranks) */
+    int64_t halo_bytes;     /* bytes this rank sent in halo / migration exchanges this step */
 } sisph_step_report;
 
 typedef enum {
@@ -196,6 +199,60 @@ int sisph_get_neighbors(sisph_t* s, int64_t* offsets, int64_t* ids, int64_t cap,
  * [0, n) is SISPH_EINVAL. */
 int sisph_get_neighbors_of(sisph_t* s, const int64_t* which, int64_t m, int64_t* offsets, int64_t* ids,
                            int64_t cap, int64_t* total);
+
+/* ---------------------------------------------------------------------------
+ * Slab decomposition over several GPUs.  The domain is cut
+ * into nranks slabs of equal width along slab_axis; rank r owns the particles
+ * whose slab_axis coordinate lies in its slab (sisph_slab_bounds) and keeps
+ * read-only halo copies of the neighbour slabs' particles within 1.3 x 3h of
+ * its faces.  Per step: fluid particles that left the slab migrate to the
+ * neighbour rank; halos are refreshed before every pass that reads them (the
+ * PPE sweep: wall pressure and p^{k+1} every sweep); Lambda, the two sums of
+ * eq:convergence and the skin are allreduced, so every rank runs the same
+ * number of sweeps.  One process (or, for tests, one thread) per rank; every
+ * rank calls every entry point collectively, in the same order.
+ * ------------------------------------------------------------------------- */
+typedef struct sisph_local_group sisph_local_group_t;
+
+typedef struct {
+    int nranks;              /* >= 1 (1: same as sisph_create) */
+    int rank;                /* 0 .. nranks - 1 */
+    int slab_axis;           /* 0 .. dim - 1; slabs must be at least 1.3 x 3h wide */
+    uint8_t nccl_id[128];    /* NCCL unique id from sisph_nccl_unique_id on one rank,
+                                broadcast to all ranks by the caller (e.g. torch.distributed) */
+    const char* nccl_lib;    /* NCCL library to dlopen (NULL: "libnccl.so.2") */
+    sisph_local_group_t* local_group;  /* non-NULL: ranks are threads of THIS process sharing
+                                          one GPU, exchanging through device copies at host
+                                          barriers (tests; no NCCL) */
+} sisph_dist;
+
+/* A fresh NCCL unique id (ncclGetUniqueId of the library nccl_lib, NULL for
+ * "libnccl.so.2").  Errors: SISPH_EINVAL (NULL id), SISPH_ENCCL. */
+int sisph_nccl_unique_id(const char* nccl_lib, uint8_t id[128]);
+
+/* An in-process group of nranks ranks (see sisph_dist.local_group).  Destroy
+ * after every handle of the group. */
+int sisph_local_group_create(int nranks, sisph_local_group_t** out);
+void sisph_local_group_destroy(sisph_local_group_t* group);
+
+/* [lo, hi) of rank's slab: lo + L r / nranks .. lo + L (r + 1) / nranks along axis. */
+int sisph_slab_bounds(const sisph_domain* domain, int axis, int nranks, int rank, double* lo, double* hi);
+
+/* Collective create of one rank of a slab-decomposed simulation.  Every rank
+ * passes the same GLOBAL arrays (as sisph_create) and keeps its slab and
+ * halos.  Field getters of a rank fill the entries of the particles it owns
+ * (others are left 0: summing the ranks' arrays gives the whole field);
+ * setters take those entries.  The wall geometry is fixed at create.
+ * Errors: as sisph_create; SISPH_EINVAL for bad rank / axis or slabs thinner
+ * than the halo; SISPH_ENCCL; a step whose skin 2 dt max|u~| exceeds 0.3 x 3h
+ * returns SISPH_EINVAL (reduce dt). */
+int sisph_create_dist(const double* positions, const double* velocities, const double* masses,
+                      const double* densities, const int32_t* tags, int64_t n, double h,
+                      const sisph_domain* domain, const sisph_params* params, const sisph_dist* dist,
+                      sisph_t** out);
+
+/* Particles owned by this handle (= sisph_get_counts' fluid / wall counts on one GPU). */
+int sisph_get_owned_counts(sisph_t* s, int64_t* n_fluid, int64_t* n_wall);
 
 /* Counts: particles, fluid particles, wall particles. */
 int sisph_get_counts(const sisph_t* s, int64_t* n, int64_t* n_fluid, int64_t* n_wall);

@@ -3,7 +3,9 @@ C ABI (include/sisph.h), with a thin ctypes binding.
 
     from paper_1908_01762_b200 import Simulation
 """
-from .sisph import (EXPORTED, FIELDS, Simulation, SisphError, domain, lib,  # noqa: F401
-                    params_from_dict, sisph_domain, sisph_params, sisph_step_report)
+from .sisph import (EXPORTED, FIELDS, LocalGroup, Simulation, SisphError, default_nccl_lib,  # noqa: F401
+                    domain, lib, make_dist, nccl_unique_id, params_from_dict, sisph_dist, sisph_domain,
+                    sisph_params, sisph_step_report, slab_bounds)
 
-__all__ = ["Simulation", "SisphError", "domain", "params_from_dict", "lib", "FIELDS", "EXPORTED"]
+__all__ = ["Simulation", "SisphError", "domain", "params_from_dict", "lib", "FIELDS", "EXPORTED", "LocalGroup",
+           "make_dist", "nccl_unique_id", "slab_bounds", "default_nccl_lib"]

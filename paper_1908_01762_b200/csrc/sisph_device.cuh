@@ -42,8 +42,11 @@ template <> __device__ __forceinline__ dbl4 mk4<double>(double x, double y, doub
 // Kernel-argument block: geometry + scheme constants, passed by value.
 // ---------------------------------------------------------------------------
 template <class T> struct Params {
-    // sizes
+    // sizes: fluid slots [0, Nf) = owned [0, Nfo) + ghosts [Nfo, Nf); wall slots
+    // [Nf, Ntot) = owned [Nf, Nf + Nwo) + ghosts.  Single GPU: Nfo = Nf, Nwo = Nw.
     int Nf, Nw, Ntot, cap;
+    int Nfo, Nwo;
+    int ghosts;            // 1: keys of ghost particles are offset by the cell count (slab halos)
     // cell grid (R26/R27): decisions in fp64
     int dim;
     int nc[3];

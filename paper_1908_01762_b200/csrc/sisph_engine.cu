@@ -6,17 +6,33 @@
 // kernels of sisph_kernels.cuh on one stream, and keeps the PPE stop decision
 // on the device (the host only polls a pinned copy of the control block
 // between speculative batches of sweeps).
+//
+// Slab ranks (sisph_create_dist): the domain is cut into
+// nranks slabs along one axis; a rank owns the particles of its slab and
+// holds read-only halo copies ("ghosts") of the neighbour slabs' particles
+// within Gw = 1.3 x 3h of its faces.  Slots: owned fluid [0, Nfo), ghost
+// fluid [Nfo, Nf), owned walls [Nf, Nf + Nwo), ghost walls [Nf + Nwo, Ntot);
+// ghosts carry the cell key + ncells, so one stable sort keeps each set
+// cell-sorted and contiguous.  Every kernel computes owned rows only; each
+// ghost value a kernel reads is refreshed from its owner first (halo
+// exchange of the transport, sisph_comm.cuh), the sweep's residual sums and
+// Lambda are allreduced, and every rank takes the same decisions from the
+// same bits.  Migration of fluid particles to the neighbour slab happens at
+// the start of each step.
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
-#include <type_traits>
+#include <map>
 #include <string>
+#include <type_traits>
+#include <utility>
 #include <vector>
 
 #include "../../include/sisph.h"
+#include "sisph_comm.cuh"
 #include "sisph_kernels.cuh"
 
 namespace sb {
@@ -41,6 +57,12 @@ static inline int nblk(long n, int bs) { return (int)((n + bs - 1) / bs); }
 
 enum Phase { IDLE = 0, PREDICTED = 1, SOLVED = 2 };
 
+// distribution of a handle over slab ranks (resolved from sisph_dist)
+struct DistInfo {
+    int nranks = 1, rank = 0, axis = 0;
+    Transport* tp = nullptr;   // owned by the engine
+};
+
 struct EngineBase {
     std::string err;
     int64_t n = 0, nf = 0, nw = 0;
@@ -57,6 +79,7 @@ struct EngineBase {
     virtual int get_neighbors(int64_t* off, int64_t* ids, int64_t cap, int64_t* total) = 0;
     virtual int get_neighbors_of(const int64_t* which, int64_t m, int64_t* off, int64_t* ids, int64_t cap,
                                  int64_t* total) = 0;
+    virtual int owned_counts(int64_t* nfo, int64_t* nwo) = 0;
     virtual int sync() = 0;
     int timing = 0;
     int64_t nlaunch = 0;  // kernel launches issued (all entry points)
@@ -81,6 +104,8 @@ template <class T, int D> struct Engine : EngineBase {
     cudaStream_t st = nullptr;
     bool own_stream = false;
     int Nf = 0, Nw = 0, Ntot = 0, ncells = 0;
+    int Nfo = 0, Nwo = 0;          // owned fluid / walls (= Nf / Nw on one GPU)
+    int capT = 0, capF = 0;        // slot capacities (total, fluid)
     int phase = IDLE;
     int min_iter = 2, max_iter = 1000, K = 10;
     double tol = 1e-2;
@@ -97,6 +122,8 @@ template <class T, int D> struct Engine : EngineBase {
     int *ccount = nullptr, *fstart = nullptr, *wstart = nullptr, *bsum = nullptr;
     int *nbr = nullptr, *cnt = nullptr;
     int *nbr_in = nullptr, *cnt_in = nullptr;  // GTVF inner list (h~ < h)
+    bool use_inner = false, inner_valid = false;
+    int64_t gtvf_fallbacks = 0;
     // single per-step build (R3): loose list at r^n on the skin geometry PS,
     // walls binned for PS through wperm_s / wstart_s (recomputed when PS's grid changes)
     int *nbs = nullptr, *cnt_s = nullptr;
@@ -104,14 +131,12 @@ template <class T, int D> struct Engine : EngineBase {
     int *wperm_s = nullptr, *wstart_s = nullptr;
     int wnc_s[3] = {-1, -1, -1};
     Params<T> PS;
-    int rebuild_mode = 0;
+    int rebuild_mode = 0;   // 0: single build + filter when the skin fits, 1: always two exact builds
     int matrix_free = 0;    // 1: the sweep recomputes fac_ij from positions; 0: A11 stores it per pair
-    T* coef = nullptr;      // stored per-pair part of fac_ij, blocked-ELL layout of nbr (fluid rows)   // 0: single build + filter when the skin fits, 1: always two exact builds
+    T* coef = nullptr;      // stored per-pair part of fac_ij, blocked-ELL layout of nbr (fluid rows)
     bool skin_used = false;
     double skin_radius = 0;
     double extent = 0;      // max |coordinate| of the domain (rounding margin of the skin)
-    bool use_inner = false, inner_valid = false;
-    int64_t gtvf_fallbacks = 0;
     Ctl* ctl = nullptr;
     Ctl* hctl = nullptr;  // pinned host mirror
     double* partials = nullptr;
@@ -119,37 +144,66 @@ template <class T, int D> struct Engine : EngineBase {
     std::vector<int> tags_host;  // creation-order tags
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
 
+    // ---------------------------------------------------------------- slab ranks
+    Transport* tp = nullptr;
+    int axis = 0;
+    double slab_lo = 0, slab_hi = 0, glo = 0, ghi = 0;  // own slab and the global box along the axis
+    int gper = 0;                                       // the axis is periodic globally
+    double Gw = 0;                                      // halo width (>= every loose radius)
+    int *dflag = nullptr, *dflag2 = nullptr, *dpre = nullptr, *dlist[3] = {nullptr, nullptr, nullptr};
+    int *dcnt = nullptr, *hcnt = nullptr;               // small count exchanges (device / pinned host)
+    int *fsend[2] = {nullptr, nullptr}, *fsend_pre[2] = {nullptr, nullptr};
+    int nfs[2] = {0, 0}, nfr[2] = {0, 0};
+    int* grecv = nullptr;                               // fluid halo record q -> ghost slot
+    int *wsend[2] = {nullptr, nullptr};                 // owned-wall halo lists (relative slots)
+    int nws[2] = {0, 0}, nwr[2] = {0, 0};
+    int* wrecv = nullptr;                               // wall halo record q -> ghost wall (relative)
+    int* inv = nullptr;
+    char *sbuf[2] = {nullptr, nullptr}, *rbuf[2] = {nullptr, nullptr};
+    size_t bufcap[2] = {0, 0};
+    V* wtmp = nullptr;                                  // wall-block relocation staging
+    int64_t halo_bytes = 0;                             // bytes sent by halo / migration exchanges
+
+    bool dist() const { return tp != nullptr; }
+
     ~Engine() override
     {
         void* ptrs[] = {pos, pos_alt, vel, vel_alt, us, us_alt, vt, vt_alt, rn, rstar, nrm, nstmp, rkA, rkB, vk, dk,
                         p, p_alt, rho, rho_alt, rhs, diag, fs, fs_alt, pid, pid_alt, keys, rank, perm0, perm,
                         ccount, fstart, wstart, bsum, nbr, cnt, ctl, partials, dtmp, nbr_in, cnt_in,
-                        nbs, cnt_s, wperm_s, wstart_s, coef};
+                        nbs, cnt_s, wperm_s, wstart_s, coef, dflag, dflag2, dpre, dlist[0], dlist[1], dlist[2],
+                        dcnt, fsend[0], fsend[1], fsend_pre[0], fsend_pre[1], grecv, wsend[0], wsend[1], wrecv,
+                        inv, sbuf[0], sbuf[1], rbuf[0], rbuf[1], wtmp};
         if (st) cudaStreamSynchronize(st);
         for (void* q : ptrs)
             if (q) cudaFree(q);
         if (hctl) cudaFreeHost(hctl);
+        if (hcnt) cudaFreeHost(hcnt);
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
         for (auto& e : sev)
             if (e) cudaEventDestroy(e);
+        delete tp;
         if (own_stream && st) cudaStreamDestroy(st);
     }
 
     // ------------------------------------------------------------------ setup
-    int init(const double* x, const double* u, const double* m, const double* r0, const int32_t* tags, int64_t n_,
-             double h, const sisph_domain* dom, const sisph_params* prm)
+    // Local particle arrays: fluid (tag 0) first, then walls; the first nwo
+    // walls are owned (all of them on one GPU).  gid: creation id of each
+    // local particle (NULL: its index).  n_glob: particle count of the whole
+    // problem (size of the creation-id-order arrays of get/set_field).
+    int init(const double* x, const double* u, const double* m, const double* r0, const int32_t* tags,
+             const int64_t* gid, int64_t nloc, int64_t n_glob, const int32_t* tags_glob, double h,
+             const sisph_domain* dom, const sisph_params* prm, const DistInfo* di, const double* slab)
     {
-        n = n_;
+        n = n_glob;
         dim = D;
-        tags_host.assign(tags, tags + n);
+        tags_host.assign(tags_glob, tags_glob + n);
         std::vector<int> fid, wid;
-        for (int64_t k = 0; k < n; k++) (tags[k] == SISPH_TAG_FLUID ? fid : wid).push_back((int)k);
-        Nf = (int)fid.size();
+        for (int64_t k = 0; k < nloc; k++) (tags[k] == SISPH_TAG_FLUID ? fid : wid).push_back((int)k);
+        Nf = Nfo = (int)fid.size();
         Nw = (int)wid.size();
-        Ntot = Nf + Nw;
-        nf = Nf;
-        nw = Nw;
+        Nwo = Nw;
         if (prm->device >= 0) SCK(cudaSetDevice(prm->device));
         if (prm->stream) {
             st = (cudaStream_t)prm->stream;
@@ -158,13 +212,20 @@ template <class T, int D> struct Engine : EngineBase {
             own_stream = true;
         }
         for (auto& e : ev) SCK(cudaEventCreate(&e));
+        const double R = 3.0 * h;
+        if (di && di->nranks > 1) {
+            tp = di->tp;
+            axis = di->axis;
+            glo = dom->lo[axis];
+            ghi = dom->hi[axis];
+            gper = dom->periodic[axis] ? 1 : 0;
+            slab_lo = slab[0];
+            slab_hi = slab[1];
+            Gw = 1.3 * R * (1.0 + 1e-6);
+        }
         // ------------------------------------------------ parameters
         memset(&P, 0, sizeof(P));
-        P.Nf = Nf;
-        P.Nw = Nw;
-        P.Ntot = Ntot;
         P.dim = D;
-        const double R = 3.0 * h;
         for (int a = 0; a < 3; a++) {
             P.nc[a] = 1;
             P.cell[a] = 1.0;
@@ -173,16 +234,26 @@ template <class T, int D> struct Engine : EngineBase {
             P.per[a] = 0;
         }
         for (int a = 0; a < D; a++) {
-            double L = dom->hi[a] - dom->lo[a];
+            double lo = dom->lo[a], hi = dom->hi[a];
+            int per = dom->periodic[a] ? 1 : 0;
+            if (dist() && a == axis) {
+                // the local box of a slab rank: its slab plus the halo layers, bounded
+                lo = slab_lo - Gw;
+                hi = slab_hi + Gw;
+                per = 0;
+            }
+            double L = hi - lo;
             int nc = (int)floor(L / R);
             if (nc < 1) nc = 1;
-            if (dom->periodic[a] && nc < 3) {
+            if (per && nc < 3) {
                 err = "periodic axis " + std::to_string(a) + " has fewer than 3 cells of size >= 3h";
                 return SISPH_EINVAL;
             }
+            P.lo[a] = lo;
+            P.hi[a] = hi;
             P.nc[a] = nc;
             P.cell[a] = L / nc;
-            P.per[a] = dom->periodic[a] ? 1 : 0;
+            P.per[a] = per;
             P.Ld[a] = L;
             P.halfLd[a] = 0.5 * L;
             P.Lf[a] = (float)L;
@@ -191,7 +262,7 @@ template <class T, int D> struct Engine : EngineBase {
             P.halfL[a] = (T)(0.5 * L);
         }
         long long nc_tot = (long long)P.nc[0] * P.nc[1] * P.nc[2];
-        if (nc_tot > (1ll << 30)) {
+        if (nc_tot > (1ll << 29)) {
             err = "cell grid too large";
             return SISPH_EINVAL;
         }
@@ -200,10 +271,10 @@ template <class T, int D> struct Engine : EngineBase {
         P.R2lo = (float)(R * R * (1.0 - 1.0 / 4096.0));
         P.R2hi = (float)(R * R * (1.0 + 1.0 / 4096.0));
         const double sigd = D == 2 ? 7.0 / (478.0 * M_PI) : 1.0 / (120.0 * M_PI);
-        auto hd = [&](double hh, T& sig, T& dwk, T& inv) {
+        auto hd = [&](double hh, T& sig, T& dwk, T& inv_) {
             sig = (T)(sigd / pow(hh, D));
             dwk = (T)(-5.0 * sigd / pow(hh, D + 1));
-            inv = (T)(1.0 / hh);
+            inv_ = (T)(1.0 / hh);
         };
         P.h = (T)h;
         hd(h, P.sig, P.dwk, P.inv_h);
@@ -227,6 +298,7 @@ template <class T, int D> struct Engine : EngineBase {
         P.ustar_noslip = prm->ustar_noslip;
         P.clamp_wall_p = prm->clamp_wall_p;
         P.wall_rho_summation = prm->wall_rho_summation;
+        P.ghosts = dist() ? 1 : 0;
         rebuild_mode = prm->rebuild_mode;
         matrix_free = prm->matrix_free;
         for (int a = 0; a < D; a++) extent = std::max(extent, std::max(fabs(dom->lo[a]), fabs(dom->hi[a])));
@@ -242,9 +314,34 @@ template <class T, int D> struct Engine : EngineBase {
             P.Rin2f = (float)(rin * rin * (1.0 + 1.0 / 1024.0));
             P.skin_half2 = (T)(0.25 * skin * skin);
         }
+        // slab ranks: the owned walls' halo lists are chosen on the host (same
+        // arithmetic as k_halo_flags on the working-precision positions) so that
+        // the ghost-wall count is known before the allocation
+        std::vector<int> hws[2];
+        if (dist()) {
+            SCK(cudaHostAlloc((void**)&hcnt, 8 * sizeof(int), cudaHostAllocDefault));
+            int rc = 0;
+            dcnt = dalloc<int>(8, err, rc);
+            if (rc) return rc;
+            for (int w = 0; w < Nw; w++) {
+                const double y = (double)(T)x[(size_t)wid[w] * D + axis];
+                if (tp->nb[0] >= 0 && y < slab_lo + Gw) hws[0].push_back(w);
+                if (tp->nb[1] >= 0 && y >= slab_hi - Gw) hws[1].push_back(w);
+            }
+            for (int f = 0; f < 2; f++) nws[f] = (int)hws[f].size();
+            SRET(exchange_counts(nws, nwr));
+            Nw = Nwo + nwr[0] + nwr[1];
+        }
+        Ntot = Nf + Nw;
+        nf = Nfo;
+        nw = Nwo;
+        capF = dist() ? (int)(1.6 * Nfo) + 4096 : Nf;
+        capT = capF + Nw;
+        SRET(sync_counts());
         // ------------------------------------------------ allocation
         int rc = 0;
-        size_t NT = (size_t)Ntot, NF = (size_t)std::max(Nf, 1), NW = (size_t)std::max(Nw, 1);
+        size_t NT = (size_t)std::max(capT, 1), NF = (size_t)std::max(capF, 1), NW = (size_t)std::max(Nw, 1);
+        size_t NCT = 2 * (size_t)ncells + 2;   // cell tables: owned keys + ghost keys (+ end)
 #define AL(ptr, Ty, cntx)                    \
     ptr = dalloc<Ty>((cntx), err, rc);       \
     if (rc) return rc;
@@ -254,10 +351,16 @@ template <class T, int D> struct Engine : EngineBase {
         AL(p, T, NT) AL(p_alt, T, NT) AL(rho, T, NT) AL(rho_alt, T, NT) AL(rhs, T, NF) AL(diag, T, NF)
         AL(fs, uint8_t, NF) AL(fs_alt, uint8_t, NF) AL(pid, int, NT) AL(pid_alt, int, NT)
         AL(keys, int, NT) AL(rank, int, NT) AL(perm0, int, NT) AL(perm, int, NT)
-        AL(ccount, int, (size_t)ncells + 1) AL(fstart, int, (size_t)ncells + 1) AL(wstart, int, (size_t)ncells + 1)
-        AL(bsum, int, (size_t)nblk(ncells + 1, SCAN_B) + 1) AL(cnt, int, NT) AL(ctl, Ctl, 1) AL(cnt_in, int, NF)
-        AL(cnt_s, int, NT) AL(wperm_s, int, NW) AL(wstart_s, int, (size_t)ncells + 1)
-        AL(partials, double, 2 * (size_t)nblk(Nf, SWEEP_T) + 2) AL(dtmp, double, 3 * (size_t)n)
+        AL(ccount, int, NCT) AL(fstart, int, NCT) AL(wstart, int, NCT)
+        AL(bsum, int, (size_t)nblk(NCT, SCAN_B) + 1) AL(cnt, int, NT) AL(ctl, Ctl, 1) AL(cnt_in, int, NF)
+        AL(cnt_s, int, NT) AL(wperm_s, int, NW) AL(wstart_s, int, NCT)
+        AL(partials, double, 2 * (size_t)nblk(NF, SWEEP_T) + 2) AL(dtmp, double, 3 * (size_t)n)
+        if (dist()) {
+            AL(dflag, int, NT) AL(dflag2, int, NT) AL(dpre, int, NT + 1) AL(dlist[0], int, NF) AL(dlist[1], int, NF)
+            AL(dlist[2], int, NF) AL(fsend[0], int, NF) AL(fsend[1], int, NF) AL(fsend_pre[0], int, NF)
+            AL(fsend_pre[1], int, NF) AL(grecv, int, NF) AL(wsend[0], int, NW) AL(wsend[1], int, NW)
+            AL(wrecv, int, NW) AL(inv, int, NT) AL(wtmp, V, NW)
+        }
 #undef AL
         SCK(cudaHostAlloc((void**)&hctl, sizeof(Ctl), cudaHostAllocDefault));
         SCK(cudaMemsetAsync(ctl, 0, sizeof(Ctl), st));
@@ -270,46 +373,47 @@ template <class T, int D> struct Engine : EngineBase {
         SCK(cudaMemsetAsync(nrm, 0, NW * sizeof(V), st));
         SCK(cudaMemsetAsync(rhs, 0, NF * sizeof(T), st));
         SCK(cudaMemsetAsync(diag, 0, NF * sizeof(T), st));
-        // ------------------------------------------------ upload (fluid ids, then wall ids, ascending)
+        // ------------------------------------------------ upload (fluid, then owned walls, given order)
         std::vector<V> hpos(NT), hvel(NT);
         std::vector<T> hrho(NT);
         std::vector<int> hid(NT);
-        for (int s = 0; s < Ntot; s++) {
+        const int nup = Nf + Nwo;
+        for (int s = 0; s < nup; s++) {
             int k = s < Nf ? fid[s] : wid[s - Nf];
-            hid[s] = k;
+            hid[s] = gid ? (int)gid[k] : k;
             const double* xk = x + (size_t)k * D;
             const double* uk = u + (size_t)k * D;
             hpos[s] = mkh(xk[0], xk[1], D == 3 ? xk[2] : 0.0, m[k]);
             hvel[s] = mkh(uk[0], uk[1], D == 3 ? uk[2] : 0.0, 0.0);
             hrho[s] = (T)r0[k];
         }
-        SCK(cudaMemcpyAsync(pos, hpos.data(), NT * sizeof(V), cudaMemcpyHostToDevice, st));
-        SCK(cudaMemcpyAsync(vel, hvel.data(), NT * sizeof(V), cudaMemcpyHostToDevice, st));
+        SCK(cudaMemcpyAsync(pos, hpos.data(), nup * sizeof(V), cudaMemcpyHostToDevice, st));
+        SCK(cudaMemcpyAsync(vel, hvel.data(), nup * sizeof(V), cudaMemcpyHostToDevice, st));
         SCK(cudaMemcpyAsync(vt, hvel.data(), (size_t)Nf * sizeof(V), cudaMemcpyHostToDevice, st));  // R23
-        SCK(cudaMemcpyAsync(rho, hrho.data(), NT * sizeof(T), cudaMemcpyHostToDevice, st));
-        SCK(cudaMemcpyAsync(pid, hid.data(), NT * sizeof(int), cudaMemcpyHostToDevice, st));
+        SCK(cudaMemcpyAsync(rho, hrho.data(), nup * sizeof(T), cudaMemcpyHostToDevice, st));
+        SCK(cudaMemcpyAsync(pid, hid.data(), nup * sizeof(int), cudaMemcpyHostToDevice, st));
+        if (dist())
+            for (int f = 0; f < 2; f++)
+                if (nws[f]) SCK(cudaMemcpyAsync(wsend[f], hws[f].data(), nws[f] * sizeof(int), cudaMemcpyHostToDevice, st));
         SCK(cudaStreamSynchronize(st));  // host vectors go out of scope
-        // identity tails of the permutations (walls are gathered in place)
-        if (Nw) {
-            ++nlaunch, k_iota<<<nblk(Nw, 256), 256, 0, st>>>(perm + Nf, Nw, Nf);
-            SCK(cudaGetLastError());
-        }
-        // ------------------------------------------------ capacity, walls, first build, normals
+        // ------------------------------------------------ walls, first build, normals, capacity
         int cap = prm->nbr_cap;
         if (cap <= 0) cap = D == 2 ? 48 : 160;
         cap = (cap + 3) / 4 * 4;   // blocked ELL stores 16-byte chunks of 4 entries
         SRET(alloc_list(cap));
-        SRET(setup_walls());
+        SRET(sort_walls(true));
+        SRET(first_build());
         if (prm->nbr_cap <= 0) {
-            // automatic capacity: 1.5 x the largest count of the first build
+            // automatic capacity: 1.5 x the largest count of the first build (slab ranks: of all ranks)
             SCK(cudaMemcpyAsync(hctl, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
             SCK(cudaStreamSynchronize(st));
             int mc = hctl->max_count;
+            if (dist()) SRET(allreduce_host(&mc, 1));
             int want = std::max((int)ceil(1.5 * mc) + 8, D == 2 ? 48 : 128);
             want = (want + 7) / 8 * 8;
             if (want != P.cap) {
                 SRET(alloc_list(want));
-                SRET(setup_walls());
+                SRET(first_build());
             }
         }
         return check_overflow();
@@ -325,6 +429,23 @@ template <class T, int D> struct Engine : EngineBase {
         return v;
     }
 
+    static size_t rows32(int n_) { return ((size_t)std::max(n_, 1) + 31) / 32 * 32; }
+
+    int sync_counts()
+    {
+        P.Nf = Nf;
+        P.Nw = Nw;
+        P.Ntot = Ntot;
+        P.Nfo = Nfo;
+        P.Nwo = Nwo;
+        PS.Nf = Nf;
+        PS.Nw = Nw;
+        PS.Ntot = Ntot;
+        PS.Nfo = Nfo;
+        PS.Nwo = Nwo;
+        return SISPH_OK;
+    }
+
     int alloc_list(int cap)
     {
         if (nbr) cudaFree(nbr);
@@ -333,23 +454,21 @@ template <class T, int D> struct Engine : EngineBase {
         nbr = nbr_in = nullptr;
         coef = nullptr;
         int rc = 0;
-        nbr = dalloc<int>((size_t)cap * rows32(Ntot), err, rc);
+        nbr = dalloc<int>((size_t)cap * rows32(capT), err, rc);
         if (rc) return rc;
         if (!matrix_free) {
-            coef = dalloc<T>((size_t)cap * rows32(Nf), err, rc);
+            coef = dalloc<T>((size_t)cap * rows32(capF), err, rc);
             if (rc) return rc;
         }
         P.cap = cap;
         if (use_inner) {
             // the inner list holds a subset of each fluid row: the full capacity is an upper bound
             P.cap_in = cap;
-            nbr_in = dalloc<int>((size_t)cap * rows32(Nf), err, rc);
+            nbr_in = dalloc<int>((size_t)cap * rows32(capF), err, rc);
             if (rc) return rc;
         }
         return SISPH_OK;
     }
-
-    static size_t rows32(int n) { return ((size_t)std::max(n, 1) + 31) / 32 * 32; }
 
     int check_overflow()
     {
@@ -374,20 +493,20 @@ template <class T, int D> struct Engine : EngineBase {
         return SISPH_OK;
     }
 
-    // A1 + A2 + A4: stable counting sort of n particles at xs by cell key;
-    // writes start[0..ncells] and perm_out[0..n) (relative slots)
     static int ncells_of(const Params<T>& G) { return G.nc[0] * G.nc[1] * G.nc[2]; }
 
-    int sort_set(const V* xs, int nn, int* start, int* perm_out) { return sort_set(P, xs, nn, start, perm_out); }
-    int sort_set(const Params<T>& G, const V* xs, int nn, int* start, int* perm_out)
+    // A1 + A2 + A4: stable counting sort of n particles at xs by cell key
+    // (elements at i >= nown are ghosts: key + ncells); writes
+    // start[0 .. 2 ncells] (ghosts present) and perm_out[0..n) (relative slots)
+    int sort_set(const Params<T>& G, const V* xs, int nn, int nown, int* start, int* perm_out)
     {
-        const int nc = ncells_of(G);
-        SCK(cudaMemsetAsync(ccount, 0, ((size_t)nc + 1) * sizeof(int), st));
+        const int nk = ncells_of(G) * (G.ghosts ? 2 : 1);
+        SCK(cudaMemsetAsync(ccount, 0, ((size_t)nk + 1) * sizeof(int), st));
         if (nn > 0) {
-            ++nlaunch, k_hash_count<T, D><<<nblk(nn, 256), 256, 0, st>>>(G, xs, nn, keys, rank, ccount);
+            ++nlaunch, k_hash_count<T, D><<<nblk(nn, 256), 256, 0, st>>>(G, xs, nn, nown, keys, rank, ccount);
             SCK(cudaGetLastError());
         }
-        SRET(scan(ccount, start, nc + 1));
+        SRET(scan(ccount, start, nk + 1));
         if (nn > 0) {
             ++nlaunch, k_scatter<<<nblk(nn, 256), 256, 0, st>>>(keys, rank, start, perm0, nn);
             ++nlaunch, k_stabilize<<<nblk(nn, 256), 256, 0, st>>>(perm0, keys, start, perm_out, nn);
@@ -441,7 +560,7 @@ template <class T, int D> struct Engine : EngineBase {
         SCK(cudaMemsetAsync(&ctl->max_count, 0, sizeof(int), st));
         SCK(cudaMemsetAsync(&ctl->pairs_fluid, 0, 2 * sizeof(unsigned long long), st));
         int* ni = nbr_in;
-        ++nlaunch, k_filter<T, D><<<nblk(Ntot, 128), 128, 0, st>>>(P, pos, nbs, cnt_s, cap_s, nbr, cnt, ni, cnt_in, ctl);
+        if (Ntot) ++nlaunch, k_filter<T, D><<<nblk(Ntot, 128), 128, 0, st>>>(P, pos, nbs, cnt_s, cap_s, nbr, cnt, ni, cnt_in, ctl);
         SCK(cudaGetLastError());
         inner_valid = ni != nullptr;
         return SISPH_OK;
@@ -449,16 +568,20 @@ template <class T, int D> struct Engine : EngineBase {
 
     // Decide whether this step can use the single build: skin s = 2 dt max|u~|
     // (+ a rounding margin); the skin geometry has cells >= 3h + s, at least 3
-    // per periodic axis, and 3h + s <= 1.3 * 3h (list capacity).  Sets PS.
+    // per periodic axis, and 3h + s <= 1.3 * 3h (list capacity; slab ranks:
+    // the halo width).  Slab ranks take the max over all ranks' owned fluid
+    // (ghosts are not present yet).  Sets PS.
     int plan_skin(double dt, bool& ok)
     {
         ok = false;
         skin_used = false;
         skin_radius = 0;
-        if (rebuild_mode != 0 || Nf == 0) return SISPH_OK;
+        if (rebuild_mode != 0 || (Nf == 0 && !dist())) return SISPH_OK;
         SCK(cudaMemsetAsync(&ctl->umax2_bits, 0, sizeof(unsigned long long), st));
-        ++nlaunch, k_max_speed<T, D><<<std::min(nblk(Nf, 256), 148 * 8), 256, 0, st>>>(vt, Nf, ctl);
+        const int nmax = dist() ? Nfo : Nf;
+        if (nmax) ++nlaunch, k_max_speed<T, D><<<std::min(nblk(nmax, 256), 148 * 8), 256, 0, st>>>(vt, nmax, ctl);
         SCK(cudaGetLastError());
+        if (dist()) SRET(xallreduce(reinterpret_cast<double*>(&ctl->umax2_bits), 1, 1));
         SCK(cudaMemcpyAsync(&hctl->umax2_bits, &ctl->umax2_bits, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                             st));
         SCK(cudaStreamSynchronize(st));
@@ -487,34 +610,325 @@ template <class T, int D> struct Engine : EngineBase {
             if (nbs) cudaFree(nbs);
             nbs = nullptr;
             int rc = 0;
-            nbs = dalloc<int>((size_t)want * rows32(Ntot), err, rc);
+            nbs = dalloc<int>((size_t)want * rows32(capT), err, rc);
             if (rc) return rc;
             cap_s = want;
         }
         G.cap = cap_s;
         PS = G;
-        // walls binned on the skin grid (static: only when the grid changes)
-        if (Nw && (G.nc[0] != wnc_s[0] || G.nc[1] != wnc_s[1] || G.nc[2] != wnc_s[2])) {
-            SRET(sort_set(G, pos + Nf, Nw, wstart_s, wperm_s));
-            for (int a = 0; a < 3; a++) wnc_s[a] = G.nc[a];
-        } else if (!Nw) {
-            SCK(cudaMemsetAsync(wstart_s, 0, ((size_t)ncells_of(G) + 1) * sizeof(int), st));
-        }
         ok = true;
         skin_used = true;
         skin_radius = Rs;
         return SISPH_OK;
     }
 
-    // walls: stable sort by cell (once, or when wall positions change), wall
-    // cell table, copies of the wall positions into every position buffer,
-    // then a full build and the normals (A0).
-    int setup_walls()
+    // walls binned on the skin grid (static: only when the grid changes)
+    int bin_walls_skin()
     {
+        const Params<T>& G = PS;
+        if (Nw && (G.nc[0] != wnc_s[0] || G.nc[1] != wnc_s[1] || G.nc[2] != wnc_s[2])) {
+            SRET(sort_set(G, pos + Nf, Nw, Nwo, wstart_s, wperm_s));
+            for (int a = 0; a < 3; a++) wnc_s[a] = G.nc[a];
+        } else if (!Nw) {
+            SCK(cudaMemsetAsync(wstart_s, 0, (2 * (size_t)ncells_of(G) + 2) * sizeof(int), st));
+        }
+        return SISPH_OK;
+    }
+
+    // ------------------------------------------------------------------ slab-rank plumbing
+    int tperr()
+    {
+        err = "transport: " + tp->err;
+        return SISPH_ENCCL;
+    }
+    int xallreduce(double* dbuf, int count, int op)
+    {
+        if (tp->allreduce(dbuf, count, op, st)) return tperr();
+        return SISPH_OK;
+    }
+    // host ints -> max over ranks (through the device)
+    int allreduce_host(int* v, int count)
+    {
+        std::vector<double> h(count);
+        for (int q = 0; q < count; q++) h[q] = v[q];
+        double* d = partials;   // scratch (>= 2 doubles)
+        SCK(cudaMemcpyAsync(d, h.data(), count * sizeof(double), cudaMemcpyHostToDevice, st));
+        SRET(xallreduce(d, count, 1));
+        SCK(cudaMemcpyAsync(h.data(), d, count * sizeof(double), cudaMemcpyDeviceToHost, st));
+        SCK(cudaStreamSynchronize(st));
+        for (int q = 0; q < count; q++) v[q] = (int)h[q];
+        return SISPH_OK;
+    }
+    // send s[f] to the face-f neighbour, receive r[f] from it (host ints)
+    int exchange_counts(const int s[2], int r[2])
+    {
+        hcnt[0] = s[0];
+        hcnt[1] = s[1];
+        hcnt[2] = hcnt[3] = 0;
+        SCK(cudaMemcpyAsync(dcnt, hcnt, 4 * sizeof(int), cudaMemcpyHostToDevice, st));
+        const void* sb[2] = {dcnt, dcnt + 1};
+        void* rb[2] = {dcnt + 2, dcnt + 3};
+        const size_t sz[2] = {sizeof(int), sizeof(int)};
+        if (tp->sendrecv(sb, sz, rb, sz, st)) return tperr();
+        SCK(cudaMemcpyAsync(hcnt, dcnt, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
+        SCK(cudaStreamSynchronize(st));
+        r[0] = tp->nb[0] >= 0 ? hcnt[2] : 0;
+        r[1] = tp->nb[1] >= 0 ? hcnt[3] : 0;
+        return SISPH_OK;
+    }
+    int ensure_buf(int f, size_t bytes)
+    {
+        if (bytes <= bufcap[f]) return SISPH_OK;
+        size_t want = bytes + bytes / 4 + 4096;
+        if (sbuf[f]) cudaFree(sbuf[f]);
+        if (rbuf[f]) cudaFree(rbuf[f]);
+        sbuf[f] = rbuf[f] = nullptr;
+        int rc = 0;
+        sbuf[f] = dalloc<char>(want, err, rc);
+        if (rc) return rc;
+        rbuf[f] = dalloc<char>(want, err, rc);
+        if (rc) return rc;
+        bufcap[f] = want;
+        return SISPH_OK;
+    }
+    static void pl_add(PackList& L, void* ptr, int size, int shift = 0)
+    {
+        L.ptr[L.nf] = ptr;
+        L.size[L.nf] = size;
+        L.sh[L.nf] = shift;
+        L.nf++;
+        L.rec += size;
+    }
+    // periodic image shift of records crossing face f of this rank
+    double face_shift(int f) const
+    {
+        if (!gper) return 0.0;
+        if (f == 0 && tp->rank == 0) return ghi - glo;                  // to the last slab, above its top
+        if (f == 1 && tp->rank == tp->nranks - 1) return -(ghi - glo);  // to the first slab, below its bottom
+        return 0.0;
+    }
+    // One face exchange: pack list[f] (count ns[f]; NULL list = slots base +
+    // q) of the fields of L, send, unpack the received records (counts nr[f])
+    // to map (NULL: base_r + q), face-0 records first.  L.ptr are the arrays
+    // (for pack and unpack alike: a halo refresh writes the same arrays).
+    int exchange(PackList L, int* const list[2], const int ns[2], const int nr[2], const int* map, int base_r)
+    {
+        L.rec = (L.rec + 15) / 16 * 16;
+        L.axis = axis;
+        for (int f = 0; f < 2; f++) {
+            SRET(ensure_buf(f, (size_t)std::max(ns[f], nr[f]) * L.rec));
+        }
+        for (int f = 0; f < 2; f++) {
+            if (!ns[f]) continue;
+            PackList Lf = L;
+            Lf.shift = face_shift(f);
+            ++nlaunch, k_pack<T><<<nblk(ns[f], 256), 256, 0, st>>>(Lf, list[f], 0, ns[f], sbuf[f]);
+            halo_bytes += (int64_t)ns[f] * L.rec;
+        }
+        SCK(cudaGetLastError());
+        const void* sb[2] = {sbuf[0], sbuf[1]};
+        void* rb[2] = {rbuf[0], rbuf[1]};
+        const size_t sz[2] = {(size_t)ns[0] * L.rec, (size_t)ns[1] * L.rec};
+        const size_t rz[2] = {(size_t)nr[0] * L.rec, (size_t)nr[1] * L.rec};
+        if (tp->sendrecv(sb, sz, rb, rz, st)) return tperr();
+        int off = 0;
+        for (int f = 0; f < 2; f++) {
+            if (nr[f])
+                ++nlaunch, k_unpack<T><<<nblk(nr[f], 256), 256, 0, st>>>(L, map ? map + off : nullptr, base_r + off,
+                                                                          nr[f], rbuf[f]);
+            off += nr[f];
+        }
+        SCK(cudaGetLastError());
+        return SISPH_OK;
+    }
+    // halo refresh of fluid fields (owned rows -> the neighbours' ghost rows)
+    int halo_fluid(PackList L) { return exchange(L, fsend, nfs, nfr, grecv, 0); }
+    // halo refresh of wall fields; L.ptr point at the wall blocks (relative slots)
+    int halo_walls(PackList L) { return exchange(L, wsend, nws, nwr, wrecv, 0); }
+    // the p^k buffer of a solve is chosen on the device (iteration parity):
+    // refresh both, the copy of the unused one is harmless
+    int halo_p(bool walls)
+    {
+        PackList L{};
+        pl_add(L, walls ? (void*)(p + Nf) : (void*)p, sizeof(T));
+        pl_add(L, walls ? (void*)(p_alt + Nf) : (void*)p_alt, sizeof(T));
+        return walls ? halo_walls(L) : halo_fluid(L);
+    }
+
+    // stable compaction of flag == v (or flag != 0 with v < 0) over n items
+    // into out; the count reaches the host
+    int compact(const int* flag, int nn, int v, int* out, int& count)
+    {
+        count = 0;
+        if (nn <= 0) return SISPH_OK;
+        const int* f01 = flag;
+        if (v >= 0) {
+            ++nlaunch, k_flag_eq<<<nblk(nn, 256), 256, 0, st>>>(flag, nn, v, dflag2);
+            f01 = dflag2;
+        }
+        SRET(scan(f01, dpre, nn));
+        ++nlaunch, k_compact<<<nblk(nn, 256), 256, 0, st>>>(f01, dpre, nn, out, dcnt + 4);
+        SCK(cudaGetLastError());
+        SCK(cudaMemcpyAsync(hcnt + 4, dcnt + 4, sizeof(int), cudaMemcpyDeviceToHost, st));
+        SCK(cudaStreamSynchronize(st));
+        count = hcnt[4];
+        return SISPH_OK;
+    }
+
+    // move the wall block of every wall-carrying array from [Nf, ...) to [newNf, ...)
+    int relocate_walls(int newNf)
+    {
+        if (newNf + Nw > capT) {
+            err = "slab rank: fluid slot capacity exceeded (" + std::to_string(newNf) + " fluid + halo slots)";
+            return SISPH_ENOMEM;
+        }
+        if (newNf == Nf) return SISPH_OK;
+        if (Nw == 0) {
+            Nf = newNf;
+            Ntot = Nf;
+            return sync_counts();
+        }
+        auto mv = [&](void* base, size_t esz) -> int {
+            char* b = (char*)base;
+            SCK(cudaMemcpyAsync(wtmp, b + (size_t)Nf * esz, (size_t)Nw * esz, cudaMemcpyDeviceToDevice, st));
+            SCK(cudaMemcpyAsync(b + (size_t)newNf * esz, wtmp, (size_t)Nw * esz, cudaMemcpyDeviceToDevice, st));
+            return SISPH_OK;
+        };
+        void* vecs[] = {pos, pos_alt, rn, rstar, rkA, rkB, vel, vel_alt, us, us_alt};
+        for (void* q : vecs) SRET(mv(q, sizeof(V)));
+        void* scs[] = {p, p_alt, rho, rho_alt};
+        for (void* q : scs) SRET(mv(q, sizeof(T)));
+        SRET(mv(pid, sizeof(int)));
+        SRET(mv(pid_alt, sizeof(int)));
+        Nf = newNf;
+        Ntot = Nf + Nw;
+        return sync_counts();
+    }
+
+    // Slab ranks, step start: owned fluid particles that left the slab move
+    // to the neighbour rank (whole carried state: r, m, u, u~, p, id).
+    int migrate()
+    {
+        const int has[2] = {tp->nb[0] >= 0, tp->nb[1] >= 0};
+        if (Nfo) ++nlaunch, k_classify<T><<<nblk(Nfo, 256), 256, 0, st>>>(pos, Nfo, axis, slab_lo, slab_hi, glo, ghi, gper,
+                                                                          has[0], has[1], dflag);
+        SCK(cudaGetLastError());
+        int nstay = 0, nout[2] = {0, 0}, nin[2] = {0, 0};
+        SRET(compact(dflag, Nfo, 0, dlist[0], nstay));
+        SRET(compact(dflag, Nfo, 1, dlist[1], nout[0]));
+        SRET(compact(dflag, Nfo, 2, dlist[2], nout[1]));
+        SRET(exchange_counts(nout, nin));
+        const int nnew = nstay + nin[0] + nin[1];
+        // ghosts of the previous step are dropped: the fluid block is owned only
+        if (nnew + Nw > capT) {
+            err = "slab rank: fluid slot capacity exceeded by migration";
+            return SISPH_ENOMEM;
+        }
+        // stayers -> alternates [0, nstay)
+        GatherList G{};
+        gl_add(G, pos, pos_alt, sizeof(V), nstay);
+        gl_add(G, vel, vel_alt, sizeof(V), nstay);
+        gl_add(G, vt, vt_alt, sizeof(V), nstay);
+        gl_add(G, p, p_alt, sizeof(T), nstay);
+        gl_add(G, pid, pid_alt, sizeof(int), nstay);
+        SRET(gather(G, dlist[0], nstay));
+        // migrants: pack from the current arrays, unpack behind the stayers
+        PackList L{};
+        pl_add(L, pos, sizeof(V));
+        pl_add(L, vel, sizeof(V));
+        pl_add(L, vt, sizeof(V));
+        pl_add(L, p, sizeof(T));
+        pl_add(L, pid, sizeof(int));
+        L.rec = (L.rec + 15) / 16 * 16;
+        L.axis = axis;
+        for (int f = 0; f < 2; f++) SRET(ensure_buf(f, (size_t)std::max(nout[f], nin[f]) * L.rec));
+        int* lists[2] = {dlist[1], dlist[2]};
+        for (int f = 0; f < 2; f++)
+            if (nout[f]) {
+                ++nlaunch, k_pack<T><<<nblk(nout[f], 256), 256, 0, st>>>(L, lists[f], 0, nout[f], sbuf[f]);
+                halo_bytes += (int64_t)nout[f] * L.rec;
+            }
+        SCK(cudaGetLastError());
+        {
+            const void* sb[2] = {sbuf[0], sbuf[1]};
+            void* rb[2] = {rbuf[0], rbuf[1]};
+            const size_t sz[2] = {(size_t)nout[0] * L.rec, (size_t)nout[1] * L.rec};
+            const size_t rz[2] = {(size_t)nin[0] * L.rec, (size_t)nin[1] * L.rec};
+            if (tp->sendrecv(sb, sz, rb, rz, st)) return tperr();
+        }
+        PackList U{};
+        pl_add(U, pos_alt, sizeof(V));
+        pl_add(U, vel_alt, sizeof(V));
+        pl_add(U, vt_alt, sizeof(V));
+        pl_add(U, p_alt, sizeof(T));
+        pl_add(U, pid_alt, sizeof(int));
+        U.rec = L.rec;
+        int off = nstay;
+        for (int f = 0; f < 2; f++) {
+            if (nin[f]) ++nlaunch, k_unpack<T><<<nblk(nin[f], 256), 256, 0, st>>>(U, nullptr, off, nin[f], rbuf[f]);
+            off += nin[f];
+        }
+        SCK(cudaGetLastError());
+        SRET(copy_walls_to_alt());
+        std::swap(pos, pos_alt);
+        std::swap(vel, vel_alt);
+        std::swap(vt, vt_alt);
+        std::swap(p, p_alt);
+        std::swap(pid, pid_alt);
+        // the alternates' wall blocks are at Nf: the position buffers keep theirs
+        SRET(copy_pos_walls(pos_alt, pos));
+        Nfo = nnew;
+        // the fluid block is now [0, Nfo): walls move down to Nfo
+        SRET(relocate_walls(Nfo));
+        return sync_counts();
+    }
+    int copy_pos_walls(V* dst, const V* src)
+    {
+        if (Nw) SCK(cudaMemcpyAsync(dst + Nf, src + Nf, Nw * sizeof(V), cudaMemcpyDeviceToDevice, st));
+        return SISPH_OK;
+    }
+
+    // Slab ranks: halo selection on the owned fluid, exchange of the ghost
+    // records (r with the periodic image shift, m, u, u~, p, rho, id) into
+    // [Nfo, Nf).  The lists refer to pre-sort slots (remapped after the sort).
+    int fetch_ghosts()
+    {
+        const int has[2] = {tp->nb[0] >= 0, tp->nb[1] >= 0};
+        if (Nfo) ++nlaunch, k_halo_flags<T><<<nblk(Nfo, 256), 256, 0, st>>>(pos, Nfo, axis, slab_lo, slab_hi, Gw, has[0],
+                                                                            has[1], dflag, dflag2);
+        SCK(cudaGetLastError());
+        SRET(compact(dflag, Nfo, -1, fsend_pre[0], nfs[0]));
+        SRET(compact(dflag2, Nfo, -1, fsend_pre[1], nfs[1]));
+        SRET(exchange_counts(nfs, nfr));
+        const int ng = nfr[0] + nfr[1];
+        SRET(relocate_walls(Nfo + ng));
+        PackList L{};
+        pl_add(L, pos, sizeof(V), 1);
+        pl_add(L, vel, sizeof(V));
+        pl_add(L, vt, sizeof(V));
+        pl_add(L, p, sizeof(T));
+        pl_add(L, rho, sizeof(T));
+        pl_add(L, pid, sizeof(int));
+        return exchange(L, fsend_pre, nfs, nfr, nullptr, Nfo);
+    }
+
+    // walls (create): sort owned + ghost walls by cell; slab ranks first fetch
+    // the ghost walls (static) from the neighbours and keep the halo maps
+    int sort_walls(bool fetch)
+    {
+        if (dist() && fetch) {
+            // ghost walls appended behind the owned ones (relative slots Nwo + q)
+            PackList L{};
+            pl_add(L, pos + Nf, sizeof(V), 1);
+            pl_add(L, vel + Nf, sizeof(V));
+            pl_add(L, rho + Nf, sizeof(T));
+            pl_add(L, pid + Nf, sizeof(int));
+            SRET(exchange(L, wsend, nws, nwr, nullptr, Nwo));
+        }
         if (Nw > 0) {
             // relative wall slots go to rank[] (free after the sort): gather through it
             int* wp = rank + Nf;
-            SRET(sort_set(pos + Nf, Nw, wstart, wp));
+            SRET(sort_set(P, pos + Nf, Nw, Nwo, wstart, wp));
             GatherList G{};
             gl_add(G, pos + Nf, pos_alt + Nf, sizeof(V), Nw);
             gl_add(G, vel + Nf, vel_alt + Nf, sizeof(V), Nw);
@@ -527,37 +941,56 @@ template <class T, int D> struct Engine : EngineBase {
             SCK(cudaMemcpyAsync(rho + Nf, rho_alt + Nf, Nw * sizeof(T), cudaMemcpyDeviceToDevice, st));
             SCK(cudaMemcpyAsync(pid + Nf, pid_alt + Nf, Nw * sizeof(int), cudaMemcpyDeviceToDevice, st));
             SCK(cudaMemcpyAsync(p + Nf, p_alt + Nf, Nw * sizeof(T), cudaMemcpyDeviceToDevice, st));
-            SCK(cudaMemcpyAsync(rkA + Nf, pos + Nf, Nw * sizeof(V), cudaMemcpyDeviceToDevice, st));
-            SCK(cudaMemcpyAsync(rkB + Nf, pos + Nf, Nw * sizeof(V), cudaMemcpyDeviceToDevice, st));
-            SCK(cudaMemcpyAsync(rn + Nf, pos + Nf, Nw * sizeof(V), cudaMemcpyDeviceToDevice, st));
-            SCK(cudaMemcpyAsync(rstar + Nf, pos + Nf, Nw * sizeof(V), cudaMemcpyDeviceToDevice, st));
-            wnc_s[0] = wnc_s[1] = wnc_s[2] = -1;
+            V* bufs[] = {pos_alt, rkA, rkB, rn, rstar};
+            for (V* q : bufs) SCK(cudaMemcpyAsync(q + Nf, pos + Nf, Nw * sizeof(V), cudaMemcpyDeviceToDevice, st));
+            if (dist()) {
+                // new relative slot of every pre-sort wall slot
+                ++nlaunch, k_invperm<<<nblk(Nw, 256), 256, 0, st>>>(wp, Nw, inv);
+                for (int f = 0; f < 2; f++)
+                    if (nws[f]) ++nlaunch, k_remap<<<nblk(nws[f], 256), 256, 0, st>>>(wsend[f], 0, nws[f], inv, wsend[f]);
+                const int ngw = nwr[0] + nwr[1];
+                if (ngw) ++nlaunch, k_remap<<<nblk(ngw, 256), 256, 0, st>>>(nullptr, Nwo, ngw, inv, wrecv);
+                SCK(cudaGetLastError());
+            }
         } else {
-            SCK(cudaMemsetAsync(wstart, 0, ((size_t)ncells + 1) * sizeof(int), st));
+            SCK(cudaMemsetAsync(wstart, 0, (2 * (size_t)ncells + 2) * sizeof(int), st));
         }
+        wnc_s[0] = wnc_s[1] = wnc_s[2] = -1;
+        return SISPH_OK;
+    }
+
+    // first build at create (exact) and the wall normals (A0)
+    int first_build()
+    {
         SRET(build_fluid());
         if (Nw > 0) {
-            ++nlaunch, k_normals_raw<T, D><<<nblk(Nw, 128), 128, 0, st>>>(P, pos, rho, nbr, cnt, P.cap, nstmp);
-            ++nlaunch, k_normals_smooth<T, D><<<nblk(Nw, 128), 128, 0, st>>>(P, pos, rho, nbr, cnt, P.cap, nstmp, nrm);
+            if (Nwo) ++nlaunch, k_normals_raw<T, D><<<nblk(Nwo, 128), 128, 0, st>>>(P, pos, rho, nbr, cnt, P.cap, nstmp);
+            SCK(cudaGetLastError());
+            if (dist()) {
+                PackList L{};
+                pl_add(L, nstmp, sizeof(V));
+                SRET(halo_walls(L));
+            }
+            if (Nwo) ++nlaunch, k_normals_smooth<T, D><<<nblk(Nwo, 128), 128, 0, st>>>(P, pos, rho, nbr, cnt, P.cap, nstmp, nrm);
             SCK(cudaGetLastError());
         }
         return SISPH_OK;
     }
 
-    // build at the current fluid positions: sort, reorder the carried state,
-    // neighbour lists.
-    int build_fluid(bool loose = false)
+    // sort the fluid block [0, Nf) on geometry G (owned first, ghosts after),
+    // reorder the carried state; slab ranks remap their halo lists
+    int sort_fluid(const Params<T>& G)
     {
-        SRET(sort_set(loose ? PS : P, pos, Nf, fstart, perm));
-        GatherList G{};
-        gl_add(G, pos, pos_alt, sizeof(V), Nf);
-        gl_add(G, vel, vel_alt, sizeof(V), Nf);
-        gl_add(G, vt, vt_alt, sizeof(V), Nf);
-        gl_add(G, p, p_alt, sizeof(T), Nf);
-        gl_add(G, pid, pid_alt, sizeof(int), Nf);
-        gl_add(G, rho, rho_alt, sizeof(T), Nf);
-        gl_add(G, fs, fs_alt, 1, Nf);
-        SRET(gather(G, perm, Nf));
+        SRET(sort_set(G, pos, Nf, Nfo, fstart, perm));
+        GatherList L{};
+        gl_add(L, pos, pos_alt, sizeof(V), Nf);
+        gl_add(L, vel, vel_alt, sizeof(V), Nf);
+        gl_add(L, vt, vt_alt, sizeof(V), Nf);
+        gl_add(L, p, p_alt, sizeof(T), Nf);
+        gl_add(L, pid, pid_alt, sizeof(int), Nf);
+        gl_add(L, rho, rho_alt, sizeof(T), Nf);
+        gl_add(L, fs, fs_alt, 1, Nf);
+        SRET(gather(L, perm, Nf));
         // wall parts of the alternates
         SRET(copy_walls_to_alt());
         std::swap(pos, pos_alt);
@@ -567,6 +1000,27 @@ template <class T, int D> struct Engine : EngineBase {
         std::swap(pid, pid_alt);
         std::swap(rho, rho_alt);
         std::swap(fs, fs_alt);
+        if (dist() && Nf) {
+            ++nlaunch, k_invperm<<<nblk(Nf, 256), 256, 0, st>>>(perm, Nf, inv);
+            for (int f = 0; f < 2; f++)
+                if (nfs[f]) ++nlaunch, k_remap<<<nblk(nfs[f], 256), 256, 0, st>>>(fsend_pre[f], 0, nfs[f], inv, fsend[f]);
+            const int ng = nfr[0] + nfr[1];
+            if (ng) ++nlaunch, k_remap<<<nblk(ng, 256), 256, 0, st>>>(nullptr, Nfo, ng, inv, grecv);
+            SCK(cudaGetLastError());
+        }
+        return SISPH_OK;
+    }
+
+    // build at the current fluid positions: (slab ranks: migrate, halos,)
+    // sort, reorder the carried state, neighbour lists
+    int build_fluid(bool loose = false)
+    {
+        if (dist()) {
+            SRET(migrate());
+            SRET(fetch_ghosts());
+        }
+        if (loose) SRET(bin_walls_skin());
+        SRET(sort_fluid(loose ? PS : P));
         return loose ? build_loose() : build_list();
     }
 
@@ -597,19 +1051,56 @@ template <class T, int D> struct Engine : EngineBase {
         }
         last_dt = dt;
         bool single = false;
-        SRET(plan_skin(dt, single));
-        // A1-A5 at r^n (single build: the loose list on the skin grid)
-        SRET(build_fluid(single));
+        if (dist()) {
+            // migrate first: the skin is the max over the owned fluid of all ranks
+            SRET(migrate());
+            SRET(plan_skin(dt, single));
+            if (!single) {
+                err = "slab ranks need the single per-step build: 2 dt max|u~| exceeds 0.3 x 3h (reduce dt)";
+                return SISPH_EINVAL;
+            }
+            SRET(fetch_ghosts());
+            SRET(bin_walls_skin());
+            SRET(sort_fluid(PS));
+            SRET(build_loose());
+        } else {
+            SRET(plan_skin(dt, single));
+            // A1-A5 at r^n (single build: the loose list on the skin grid)
+            SRET(build_fluid(single));
+        }
         const int* nb1 = single ? nbs : nbr;
         const int* cn1 = single ? cnt_s : cnt;
         const int cap1 = single ? cap_s : P.cap;
         // A6 (loose pairs beyond 3h contribute exactly 0: W, dW/dr vanish for q >= 3)
-        ++nlaunch, k_density<T, D><<<nblk(Ntot, 256), 256, 0, st>>>(P, pos, nb1, cn1, cap1, rho, fs);
-        // A7
-        if (Nw) ++nlaunch, k_wall_velocity<T, D><<<nblk(Nw, 256), 256, 0, st>>>(P, pos, nb1, cn1, cap1, nrm, vel, 0);
-        // A8
-        if (Nf) ++nlaunch, k_forces_predict<T, D><<<nblk(Nf, 128), 128, 0, st>>>(P, (T)dt, pos, vel, vt, rho, nb1, cn1, cap1, us, rstar);
+        if (Ntot) ++nlaunch, k_density<T, D><<<nblk(Ntot, 256), 256, 0, st>>>(P, pos, nb1, cn1, cap1, rho, fs);
         SCK(cudaGetLastError());
+        if (dist()) {
+            PackList L{};
+            pl_add(L, rho, sizeof(T));
+            SRET(halo_fluid(L));
+            if (P.wall_rho_summation) {
+                PackList W{};
+                pl_add(W, rho + Nf, sizeof(T));
+                SRET(halo_walls(W));
+            }
+        }
+        // A7
+        if (Nwo) ++nlaunch, k_wall_velocity<T, D><<<nblk(Nwo, 256), 256, 0, st>>>(P, pos, nb1, cn1, cap1, nrm, vel, 0);
+        SCK(cudaGetLastError());
+        if (dist()) {
+            PackList W{};
+            pl_add(W, vel + Nf, sizeof(V));
+            SRET(halo_walls(W));
+        }
+        // A8
+        if (Nfo) ++nlaunch, k_forces_predict<T, D><<<nblk(Nfo, 128), 128, 0, st>>>(P, (T)dt, pos, vel, vt, rho, nb1, cn1, cap1, us, rstar);
+        SCK(cudaGetLastError());
+        if (dist()) {
+            PackList L{};
+            pl_add(L, rstar, sizeof(V), 1);
+            pl_add(L, us, sizeof(V));
+            SRET(halo_fluid(L));
+        }
         if (single) {
             // A9 (R3): r* becomes the current position set (walls are in every buffer),
             // r^n is kept as rn; exact sets at r* filtered out of the loose list
@@ -618,7 +1109,7 @@ template <class T, int D> struct Engine : EngineBase {
             SRET(filter_list());
         } else {
             // A9: build at r*; carry r^n along as rn
-            SRET(sort_set(rstar, Nf, fstart, perm));
+            SRET(sort_set(P, rstar, Nf, Nf, fstart, perm));
             GatherList G{};
             gl_add(G, rstar, pos_alt, sizeof(V), Nf);
             gl_add(G, pos, rn, sizeof(V), Nf);
@@ -642,11 +1133,19 @@ template <class T, int D> struct Engine : EngineBase {
             SRET(build_list(true));   // + GTVF inner list
         }
         // A10
-        if (Nw) ++nlaunch, k_wall_velocity<T, D><<<nblk(Nw, 256), 256, 0, st>>>(P, pos, nbr, cnt, P.cap, nrm, us, P.ustar_noslip ? 0 : 1);
+        if (Nwo) ++nlaunch, k_wall_velocity<T, D><<<nblk(Nwo, 256), 256, 0, st>>>(P, pos, nbr, cnt, P.cap, nrm, us, P.ustar_noslip ? 0 : 1);
+        SCK(cudaGetLastError());
+        if (dist()) {
+            PackList W{};
+            pl_add(W, us + Nf, sizeof(V));
+            SRET(halo_walls(W));
+        }
         // A11
         SCK(cudaMemsetAsync(&ctl->lambda_bits, 0, sizeof(unsigned long long), st));
-        if (Nf) ++nlaunch, k_rhs_diag<T, D><<<nblk(Nf, 128), 128, 0, st>>>(P, (T)(1.0 / dt), pos, us, rho, fs, nbr, cnt, P.cap, rhs, diag, coef, ctl);
+        if (Nfo) ++nlaunch, k_rhs_diag<T, D><<<nblk(Nfo, 128), 128, 0, st>>>(P, (T)(1.0 / dt), pos, us, rho, fs, nbr, cnt, P.cap, rhs, diag, coef, ctl);
         SCK(cudaGetLastError());
+        // Lambda is global (eq:convergence): the bits of a non-negative double order as the value
+        if (dist()) SRET(xallreduce(reinterpret_cast<double*>(&ctl->lambda_bits), 1, 1));
         phase = PREDICTED;
         return SISPH_OK;
     }
@@ -660,7 +1159,8 @@ template <class T, int D> struct Engine : EngineBase {
     int launch_sweeps(int count, double tl, int mi, int mx)
     {
         for (int c = 0; c < count; c++) {
-            if (Nw) ++nlaunch, k_wall_pressure<T, D><<<nblk(Nw, 256), 256, 0, st>>>(P, pos, rho, nbr, cnt, P.cap, p, p_alt, ctl);
+            if (Nwo) ++nlaunch, k_wall_pressure<T, D><<<nblk(Nwo, 256), 256, 0, st>>>(P, pos, rho, nbr, cnt, P.cap, p, p_alt, ctl);
+            if (dist()) SRET(halo_p(true));
             bool rec = timing && nrec < MAXREC;
             if (rec) {
                 if (!sev[2 * nrec]) {
@@ -669,15 +1169,23 @@ template <class T, int D> struct Engine : EngineBase {
                 }
                 SCK(cudaEventRecord(sev[2 * nrec], st));
             }
+            const int defer = dist() ? 1 : 0;
+            const int nb = std::max(nblk(Nfo, SWEEP_T), 1);   // one block at least: the last block decides
             if (coef)
-                ++nlaunch, k_sweep<T, D, true><<<nblk(Nf, SWEEP_T), SWEEP_T, 0, st>>>(
-                               P, pos, rho, rhs, diag, fs, nbr, cnt, P.cap, coef, p, p_alt, ctl, partials, tl, mi, mx);
+                ++nlaunch, k_sweep<T, D, true><<<nb, SWEEP_T, 0, st>>>(
+                               P, pos, rho, rhs, diag, fs, nbr, cnt, P.cap, coef, p, p_alt, ctl, partials, tl, mi, mx, defer);
             else
-                ++nlaunch, k_sweep<T, D, false><<<nblk(Nf, SWEEP_T), SWEEP_T, 0, st>>>(
-                               P, pos, rho, rhs, diag, fs, nbr, cnt, P.cap, nullptr, p, p_alt, ctl, partials, tl, mi, mx);
+                ++nlaunch, k_sweep<T, D, false><<<nb, SWEEP_T, 0, st>>>(
+                               P, pos, rho, rhs, diag, fs, nbr, cnt, P.cap, nullptr, p, p_alt, ctl, partials, tl, mi, mx, defer);
             if (rec) {
                 SCK(cudaEventRecord(sev[2 * nrec + 1], st));
                 nrec++;
+            }
+            if (dist()) {
+                // eq:convergence over all ranks: allreduce the local sums, decide, refresh p^{k+1}
+                SRET(xallreduce(ctl->red, 3, 0));
+                ++nlaunch, k_decide<<<1, 1, 0, st>>>(ctl, tl, mi, mx);
+                SRET(halo_p(false));
             }
         }
         SCK(cudaGetLastError());
@@ -698,8 +1206,9 @@ template <class T, int D> struct Engine : EngineBase {
         SCK(cudaMemsetAsync(ctl, 0, 4 * sizeof(int), st));  // ticket, iter, done, nonfinite
         int launched = 0;
         nrec = 0;
-        if (Nf > 0) {
+        if (Nf > 0 || dist()) {
             // speculative batches: sweeps after convergence are no-ops on the device
+            // (slab ranks take the same decisions, so they run the same batches)
             int batch = std::min(mx, std::max(mi, 2) + 1);
             for (;;) {
                 SRET(launch_sweeps(batch, tl, mi, mx));
@@ -740,17 +1249,25 @@ template <class T, int D> struct Engine : EngineBase {
     // K modified-GTVF sub-steps (A14) from r* = pos; returns the final positions in rK
     int gtvf_substeps(T dtau, bool inner, const V*& rK)
     {
-        ++nlaunch, k_gtvf_prep<T><<<nblk(Ntot, 256), 256, 0, st>>>(pos, rho, Ntot, rkA, rkB);
+        if (Ntot) ++nlaunch, k_gtvf_prep<T><<<nblk(Ntot, 256), 256, 0, st>>>(pos, rho, Ntot, rkA, rkB);
         if (inner) SCK(cudaMemsetAsync(&ctl->gtvf_far, 0, sizeof(int), st));
         const V* src = rkB;
         for (int k = 0; k < K; k++) {
             V* dst = (k & 1) ? rkB : rkA;
-            if (inner)
-                ++nlaunch, k_gtvf_substep<T, D><<<nblk(Nf, 128), 128, 0, st>>>(P, dtau, src, dst, vk, dk, p, nbr_in, P.cap_in,
-                                                                               cnt_in, k == 0, pos, 1, ctl);
-            else
-                ++nlaunch, k_gtvf_substep<T, D><<<nblk(Nf, 128), 128, 0, st>>>(P, dtau, src, dst, vk, dk, p, nbr, P.cap,
-                                                                               cnt, k == 0, pos, 0, ctl);
+            if (Nfo) {
+                if (inner)
+                    ++nlaunch, k_gtvf_substep<T, D><<<nblk(Nfo, 128), 128, 0, st>>>(P, dtau, src, dst, vk, dk, p, nbr_in,
+                                                                                    P.cap_in, cnt_in, k == 0, pos, 1, ctl);
+                else
+                    ++nlaunch, k_gtvf_substep<T, D><<<nblk(Nfo, 128), 128, 0, st>>>(P, dtau, src, dst, vk, dk, p, nbr,
+                                                                                    P.cap, cnt, k == 0, pos, 0, ctl);
+            }
+            SCK(cudaGetLastError());
+            if (dist()) {
+                PackList L{};
+                pl_add(L, dst, sizeof(V), 1);
+                SRET(halo_fluid(L));
+            }
             src = dst;
         }
         SCK(cudaGetLastError());
@@ -769,16 +1286,32 @@ template <class T, int D> struct Engine : EngineBase {
             return SISPH_EINVAL;
         }
         // A13
-        if (Nw) ++nlaunch, k_wall_pressure<T, D><<<nblk(Nw, 256), 256, 0, st>>>(P, pos, rho, nbr, cnt, P.cap, p, p_alt, nullptr);
-        if (Nf) ++nlaunch, k_pgrad_correct<T, D><<<nblk(Nf, 128), 128, 0, st>>>(P, (T)dt, pos, rho, p, us, nbr, cnt, P.cap, vel);
+        if (Nwo) ++nlaunch, k_wall_pressure<T, D><<<nblk(Nwo, 256), 256, 0, st>>>(P, pos, rho, nbr, cnt, P.cap, p, p_alt, nullptr);
+        SCK(cudaGetLastError());
+        if (dist()) {
+            PackList W{};
+            pl_add(W, p + Nf, sizeof(T));
+            SRET(halo_walls(W));
+        }
+        if (Nfo) ++nlaunch, k_pgrad_correct<T, D><<<nblk(Nfo, 128), 128, 0, st>>>(P, (T)dt, pos, rho, p, us, nbr, cnt, P.cap, vel);
         // A14: K sub-steps (p0 = 0 everywhere when p_ref == 0: the shift is exactly zero)
         const V* rK = nullptr;   // GTVF displacement r^K - r^0 (none when p0 = 0)
-        if (P.p_ref != T(0) && K > 0 && Nf) {
+        if (P.p_ref != T(0) && K > 0 && (Nf || dist())) {
             SRET(gtvf_substeps((T)(dt / K), inner_valid, rK));
             if (inner_valid) {
                 // the inner list is exact only while no particle moved more than skin/2
-                SCK(cudaMemcpyAsync(&hctl->gtvf_far, &ctl->gtvf_far, sizeof(int), cudaMemcpyDeviceToHost, st));
-                SCK(cudaStreamSynchronize(st));
+                // (slab ranks: if any rank's did, all repeat)
+                if (dist()) {
+                    int far = 0;
+                    SCK(cudaMemcpyAsync(&hctl->gtvf_far, &ctl->gtvf_far, sizeof(int), cudaMemcpyDeviceToHost, st));
+                    SCK(cudaStreamSynchronize(st));
+                    far = hctl->gtvf_far;
+                    SRET(allreduce_host(&far, 1));
+                    hctl->gtvf_far = far;
+                } else {
+                    SCK(cudaMemcpyAsync(&hctl->gtvf_far, &ctl->gtvf_far, sizeof(int), cudaMemcpyDeviceToHost, st));
+                    SCK(cudaStreamSynchronize(st));
+                }
                 if (hctl->gtvf_far) {
                     gtvf_fallbacks++;
                     SRET(gtvf_substeps((T)(dt / K), false, rK));
@@ -786,7 +1319,7 @@ template <class T, int D> struct Engine : EngineBase {
             }
         }
         // A15
-        if (Nf) ++nlaunch, k_advance<T, D><<<nblk(Nf, 256), 256, 0, st>>>(P, (T)dt, rK, rn, vel, pos, vt);
+        if (Nfo) ++nlaunch, k_advance<T, D><<<nblk(Nfo, 256), 256, 0, st>>>(P, (T)dt, rK, rn, vel, pos, vt);
         SCK(cudaGetLastError());
         phase = IDLE;
         return SISPH_OK;
@@ -795,6 +1328,7 @@ template <class T, int D> struct Engine : EngineBase {
     int step(double dt, sisph_step_report* rep) override
     {
         int64_t l0 = nlaunch;
+        int64_t hb0 = halo_bytes;
         if (timing) SCK(cudaEventRecord(ev[0], st));
         SRET(predict(dt));
         if (timing) SCK(cudaEventRecord(ev[1], st));
@@ -818,6 +1352,9 @@ template <class T, int D> struct Engine : EngineBase {
             rep->launches = nlaunch - l0;
             rep->single_build = skin_used ? 1 : 0;
             rep->skin_radius = skin_radius;
+            rep->n_owned_fluid = Nfo;
+            rep->n_ghost_fluid = Nf - Nfo;
+            rep->halo_bytes = halo_bytes - hb0;
             if (timing) {
                 SCK(cudaEventSynchronize(ev[3]));
                 float a, b, c;
@@ -854,6 +1391,7 @@ template <class T, int D> struct Engine : EngineBase {
         return -1;
     }
 
+    // owned particles only (slab ranks: the entries of other ranks' particles stay 0)
     int get_field(int f, double* out, int64_t count) override
     {
         int nc = ncomp(f);
@@ -880,25 +1418,39 @@ template <class T, int D> struct Engine : EngineBase {
         };
         switch (f) {
             case SISPH_FIELD_POSITION:
-                vec(mid ? rn - 0 : pos, 0, Nf);
-                vec(pos, Nf, Nw);
+                vec(mid ? rn : pos, 0, Nfo);
+                vec(pos, Nf, Nwo);
                 break;
             case SISPH_FIELD_RSTAR:
-                vec(pos, 0, Ntot);
+                vec(pos, 0, Nfo);
+                vec(pos, Nf, Nwo);
                 break;
-            case SISPH_FIELD_VELOCITY: vec(vel, 0, Ntot); break;
-            case SISPH_FIELD_TRANSPORT_VELOCITY: vec(vt, 0, Nf); break;
-            case SISPH_FIELD_USTAR: vec(us, 0, Ntot); break;
+            case SISPH_FIELD_VELOCITY:
+                vec(vel, 0, Nfo);
+                vec(vel, Nf, Nwo);
+                break;
+            case SISPH_FIELD_TRANSPORT_VELOCITY: vec(vt, 0, Nfo); break;
+            case SISPH_FIELD_USTAR:
+                vec(us, 0, Nfo);
+                vec(us, Nf, Nwo);
+                break;
             case SISPH_FIELD_NORMAL:
-                if (Nw) ++nlaunch, k_to_ids_vec<T><<<nblk(Nw, B), B, 0, st>>>(nrm, pid + Nf, Nw, D, dtmp);
+                if (Nwo) ++nlaunch, k_to_ids_vec<T><<<nblk(Nwo, B), B, 0, st>>>(nrm, pid + Nf, Nwo, D, dtmp);
                 break;
-            case SISPH_FIELD_PRESSURE: sc(p, 0, Ntot); break;
-            case SISPH_FIELD_DENSITY: sc(rho, 0, Ntot); break;
-            case SISPH_FIELD_RHS: sc(rhs, 0, Nf); break;
-            case SISPH_FIELD_DIAG: sc(diag, 0, Nf); break;
-            case SISPH_FIELD_FREE_SURFACE: sc(fs, 0, Nf); break;
+            case SISPH_FIELD_PRESSURE:
+                sc(p, 0, Nfo);
+                sc(p, Nf, Nwo);
+                break;
+            case SISPH_FIELD_DENSITY:
+                sc(rho, 0, Nfo);
+                sc(rho, Nf, Nwo);
+                break;
+            case SISPH_FIELD_RHS: sc(rhs, 0, Nfo); break;
+            case SISPH_FIELD_DIAG: sc(diag, 0, Nfo); break;
+            case SISPH_FIELD_FREE_SURFACE: sc(fs, 0, Nfo); break;
             case SISPH_FIELD_MASS:
-                if (Ntot) ++nlaunch, k_to_ids_w<T><<<nblk(Ntot, B), B, 0, st>>>(pos, pid, Ntot, dtmp);
+                if (Nfo) ++nlaunch, k_to_ids_w<T><<<nblk(Nfo, B), B, 0, st>>>(pos, pid, Nfo, dtmp);
+                if (Nwo) ++nlaunch, k_to_ids_w<T><<<nblk(Nwo, B), B, 0, st>>>(pos + Nf, pid + Nf, Nwo, dtmp);
                 break;
         }
         SCK(cudaGetLastError());
@@ -926,37 +1478,59 @@ template <class T, int D> struct Engine : EngineBase {
         switch (f) {
             case SISPH_FIELD_POSITION: {
                 bool mid = phase != IDLE;
-                vec(mid ? rn : pos, 0, Nf, 1);
+                vec(mid ? rn : pos, 0, Nfo, 1);
                 if (Nw) {
                     // wall geometry is static; re-sort walls + normals only if it changed
                     std::vector<double> oldw((size_t)count);
                     SRET(get_field_walls_pos(oldw.data()));
                     bool changed = false;
+                    std::vector<char> mine(n, 0);
+                    std::vector<int> hp(Nwo);
+                    if (Nwo) SCK(cudaMemcpy(hp.data(), pid + Nf, Nwo * sizeof(int), cudaMemcpyDeviceToHost));
+                    for (int w = 0; w < Nwo; w++) mine[hp[w]] = 1;
                     for (int64_t k = 0; k < n && !changed; k++)
-                        if (tags_host[k] == SISPH_TAG_WALL)
+                        if (mine[k])
                             for (int a = 0; a < D; a++)
                                 if ((T)in[k * D + a] != (T)oldw[k * D + a]) changed = true;
                     if (changed) {
+                        if (dist()) {
+                            err = "set_field: slab ranks keep the wall geometry of sisph_create_dist";
+                            return SISPH_EINVAL;
+                        }
                         SCK(cudaMemcpyAsync(dtmp, in, (size_t)count * sizeof(double), cudaMemcpyDefault, st));
                         vec(pos, Nf, Nw, 1);
-                        SRET(setup_walls());
+                        SRET(sort_walls(false));
+                        SRET(first_build());
                         phase = IDLE;
                     }
                 }
             } break;
-            case SISPH_FIELD_VELOCITY: vec(vel, 0, Ntot, 0); break;
-            case SISPH_FIELD_TRANSPORT_VELOCITY: vec(vt, 0, Nf, 0); break;
-            case SISPH_FIELD_USTAR: vec(us, 0, Ntot, 0); break;
-            case SISPH_FIELD_NORMAL:
-                if (Nw) ++nlaunch, k_from_ids_vec<T><<<nblk(Nw, B), B, 0, st>>>(dtmp, pid + Nf, Nw, D, nrm, 0);
+            case SISPH_FIELD_VELOCITY:
+                vec(vel, 0, Nfo, 0);
+                vec(vel, Nf, Nwo, 0);
                 break;
-            case SISPH_FIELD_PRESSURE: sc(p, 0, Ntot); break;
-            case SISPH_FIELD_DENSITY: sc(rho, 0, Ntot); break;
-            case SISPH_FIELD_RHS: sc(rhs, 0, Nf); break;
-            case SISPH_FIELD_DIAG: sc(diag, 0, Nf); break;
-            case SISPH_FIELD_FREE_SURFACE: sc(fs, 0, Nf); break;
+            case SISPH_FIELD_TRANSPORT_VELOCITY: vec(vt, 0, Nfo, 0); break;
+            case SISPH_FIELD_USTAR:
+                vec(us, 0, Nfo, 0);
+                vec(us, Nf, Nwo, 0);
+                break;
+            case SISPH_FIELD_NORMAL:
+                if (Nwo) ++nlaunch, k_from_ids_vec<T><<<nblk(Nwo, B), B, 0, st>>>(dtmp, pid + Nf, Nwo, D, nrm, 0);
+                break;
+            case SISPH_FIELD_PRESSURE:
+                sc(p, 0, Nfo);
+                sc(p, Nf, Nwo);
+                break;
+            case SISPH_FIELD_DENSITY:
+                sc(rho, 0, Nfo);
+                sc(rho, Nf, Nwo);
+                break;
+            case SISPH_FIELD_RHS: sc(rhs, 0, Nfo); break;
+            case SISPH_FIELD_DIAG: sc(diag, 0, Nfo); break;
+            case SISPH_FIELD_FREE_SURFACE: sc(fs, 0, Nfo); break;
             case SISPH_FIELD_MASS:
-                if (Ntot) ++nlaunch, k_from_ids_w<T><<<nblk(Ntot, B), B, 0, st>>>(dtmp, pid, Ntot, pos);
+                if (Nfo) ++nlaunch, k_from_ids_w<T><<<nblk(Nfo, B), B, 0, st>>>(dtmp, pid, Nfo, pos);
+                if (Nwo) ++nlaunch, k_from_ids_w<T><<<nblk(Nwo, B), B, 0, st>>>(dtmp, pid + Nf, Nwo, pos + Nf);
                 break;
         }
         SCK(cudaGetLastError());
@@ -967,33 +1541,51 @@ template <class T, int D> struct Engine : EngineBase {
     int get_field_walls_pos(double* out)
     {
         SCK(cudaMemsetAsync(dtmp, 0, (size_t)n * D * sizeof(double), st));
-        if (Nw) ++nlaunch, k_to_ids_vec<T><<<nblk(Nw, 256), 256, 0, st>>>(pos + Nf, pid + Nf, Nw, D, dtmp);
+        if (Nwo) ++nlaunch, k_to_ids_vec<T><<<nblk(Nwo, 256), 256, 0, st>>>(pos + Nf, pid + Nf, Nwo, D, dtmp);
         SCK(cudaGetLastError());
         SCK(cudaMemcpyAsync(out, dtmp, (size_t)n * D * sizeof(double), cudaMemcpyDefault, st));
         SCK(cudaStreamSynchronize(st));
         return SISPH_OK;
     }
 
+    // owned slots: fluid [0, Nfo), walls [Nf, Nf + Nwo)
+    bool owned_slot(int s) const { return s < Nfo || (s >= Nf && s < Nf + Nwo); }
+
     int get_order(int64_t* ids) override
     {
         std::vector<int> h(Ntot);
         SCK(cudaMemcpyAsync(h.data(), pid, Ntot * sizeof(int), cudaMemcpyDeviceToHost, st));
         SCK(cudaStreamSynchronize(st));
-        for (int s = 0; s < Ntot; s++) ids[s] = h[s];
+        int64_t q = 0;
+        for (int s = 0; s < Ntot; s++)
+            if (owned_slot(s)) ids[q++] = h[s];
+        for (; q < n; q++) ids[q] = -1;
+        return SISPH_OK;
+    }
+
+    // id -> owned slot (-1: not owned here)
+    int slot_map(std::vector<int>& hc, std::vector<int>& hp, std::vector<int>& slot_of)
+    {
+        hc.resize(Ntot);
+        hp.resize(Ntot);
+        SCK(cudaMemcpyAsync(hc.data(), cnt, Ntot * sizeof(int), cudaMemcpyDeviceToHost, st));
+        SCK(cudaMemcpyAsync(hp.data(), pid, Ntot * sizeof(int), cudaMemcpyDeviceToHost, st));
+        SCK(cudaStreamSynchronize(st));
+        slot_of.assign(n, -1);
+        for (int s = 0; s < Ntot; s++)
+            if (owned_slot(s)) slot_of[hp[s]] = s;
         return SISPH_OK;
     }
 
     int get_neighbors(int64_t* off, int64_t* ids, int64_t cap, int64_t* total) override
     {
-        std::vector<int> hc(Ntot), hp(Ntot), hn((size_t)P.cap * rows32(Ntot));
-        SCK(cudaMemcpyAsync(hc.data(), cnt, Ntot * sizeof(int), cudaMemcpyDeviceToHost, st));
-        SCK(cudaMemcpyAsync(hp.data(), pid, Ntot * sizeof(int), cudaMemcpyDeviceToHost, st));
+        std::vector<int> hc, hp, slot_of;
+        SRET(slot_map(hc, hp, slot_of));
+        std::vector<int> hn((size_t)P.cap * rows32(Ntot));
         SCK(cudaMemcpyAsync(hn.data(), nbr, hn.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
         SCK(cudaStreamSynchronize(st));
-        std::vector<int> slot_of(n);
-        for (int s = 0; s < Ntot; s++) slot_of[hp[s]] = s;
         off[0] = 0;
-        for (int64_t k = 0; k < n; k++) off[k + 1] = off[k] + hc[slot_of[k]];
+        for (int64_t k = 0; k < n; k++) off[k + 1] = off[k] + (slot_of[k] >= 0 ? hc[slot_of[k]] : 0);
         *total = off[n];
         if (cap < off[n]) {
             err = "get_neighbors: cap < total";
@@ -1001,6 +1593,7 @@ template <class T, int D> struct Engine : EngineBase {
         }
         for (int64_t k = 0; k < n; k++) {
             int s = slot_of[k];
+            if (s < 0) continue;
             int64_t* row = ids + off[k];
             // blocked ELL (see sisph_kernels.cuh): (s / 32) 32 cap + (q / 4) 128 + (s % 32) 4 + q % 4
             const size_t b = (size_t)(s >> 5) * ((size_t)P.cap << 5) + ((s & 31) << 2);
@@ -1011,23 +1604,21 @@ template <class T, int D> struct Engine : EngineBase {
     }
 
     // rows of the listed particles only (large problems): each row's 16-byte
-    // chunks sit 512 bytes apart in the blocked layout -> one 2D copy per row
+    // chunks sit 512 bytes apart in the blocked layout -> one 2D copy per row.
+    // Particles not owned by this handle get an empty row.
     int get_neighbors_of(const int64_t* which, int64_t m, int64_t* off, int64_t* ids, int64_t cap,
                          int64_t* total) override
     {
-        std::vector<int> hc(Ntot), hp(Ntot);
-        SCK(cudaMemcpyAsync(hc.data(), cnt, Ntot * sizeof(int), cudaMemcpyDeviceToHost, st));
-        SCK(cudaMemcpyAsync(hp.data(), pid, Ntot * sizeof(int), cudaMemcpyDeviceToHost, st));
-        SCK(cudaStreamSynchronize(st));
-        std::vector<int> slot_of(n);
-        for (int s = 0; s < Ntot; s++) slot_of[hp[s]] = s;
+        std::vector<int> hc, hp, slot_of;
+        SRET(slot_map(hc, hp, slot_of));
         off[0] = 0;
         for (int64_t q = 0; q < m; q++) {
             if (which[q] < 0 || which[q] >= n) {
                 err = "get_neighbors_of: id out of range";
                 return SISPH_EINVAL;
             }
-            off[q + 1] = off[q] + hc[slot_of[which[q]]];
+            const int s = slot_of[which[q]];
+            off[q + 1] = off[q] + (s >= 0 ? hc[s] : 0);
         }
         *total = off[m];
         if (cap < off[m]) {
@@ -1038,6 +1629,7 @@ template <class T, int D> struct Engine : EngineBase {
         std::vector<int> rows((size_t)m * P.cap);
         for (int64_t q = 0; q < m; q++) {
             const int s = slot_of[which[q]];
+            if (s < 0) continue;
             const size_t b = (size_t)(s >> 5) * ((size_t)P.cap << 5) + ((s & 31) << 2);
             SCK(cudaMemcpy2DAsync(rows.data() + (size_t)q * P.cap, 16, nbr + b, 512, 16, nch, cudaMemcpyDeviceToHost,
                                   st));
@@ -1045,10 +1637,18 @@ template <class T, int D> struct Engine : EngineBase {
         SCK(cudaStreamSynchronize(st));
         for (int64_t q = 0; q < m; q++) {
             const int s = slot_of[which[q]];
+            if (s < 0) continue;
             int64_t* row = ids + off[q];
             for (int k = 0; k < hc[s]; k++) row[k] = hp[rows[(size_t)q * P.cap + k]];
             std::sort(row, row + hc[s]);
         }
+        return SISPH_OK;
+    }
+
+    int owned_counts(int64_t* nfo, int64_t* nwo) override
+    {
+        if (nfo) *nfo = Nfo;
+        if (nwo) *nwo = Nwo;
         return SISPH_OK;
     }
 
@@ -1067,9 +1667,12 @@ struct sisph {
     EngineBase* e;
 };
 
-extern "C" {
+struct sisph_local_group {
+    LocalHub hub;
+    explicit sisph_local_group(int n) : hub(n) {}
+};
 
-void sisph_params_default(sisph_params* p)
+extern "C" void sisph_params_default(sisph_params* p)
 {
     if (!p) return;
     memset(p, 0, sizeof(*p));
@@ -1092,19 +1695,16 @@ static int fail_thread(int code, const std::string& m)
     return code;
 }
 
-int sisph_create(const double* positions, const double* velocities, const double* masses, const double* densities,
-                 const int32_t* tags, int64_t n, double h, const sisph_domain* domain, const sisph_params* params,
-                 sisph_t** out)
+static int validate(const double* positions, const double* velocities, const double* masses, const double* densities,
+                    const int32_t* tags, int64_t n, double h, const sisph_domain* domain, sisph_params& prm,
+                    const sisph_params* params)
 {
-    if (!out) return fail_thread(SISPH_EINVAL, "out is NULL");
-    *out = nullptr;
     if (!positions || !velocities || !masses || !densities || !tags || !domain)
         return fail_thread(SISPH_EINVAL, "NULL input array");
     if (n <= 0 || n > (1ll << 30)) return fail_thread(SISPH_EINVAL, "n must be in [1, 2^30]");
     if (!(h > 0) || !std::isfinite(h)) return fail_thread(SISPH_EINVAL, "h must be finite and > 0");
     int dim = domain->dim;
     if (dim != 2 && dim != 3) return fail_thread(SISPH_EINVAL, "dim must be 2 or 3");
-    sisph_params prm;
     if (params) prm = *params;
     else sisph_params_default(&prm);
     if (prm.precision != 32 && prm.precision != 64) return fail_thread(SISPH_EINVAL, "precision must be 32 or 64");
@@ -1136,32 +1736,177 @@ int sisph_create(const double* positions, const double* velocities, const double
         }
     }
     if (nfl == 0) return fail_thread(SISPH_EINVAL, "no fluid particle");
-    EngineBase* e = nullptr;
-    int rc;
-    if (prm.precision == 32) {
-        if (dim == 2) {
-            auto* x = new Engine<float, 2>();
-            e = x;
-            rc = x->init(positions, velocities, masses, densities, tags, n, h, domain, &prm);
-        } else {
-            auto* x = new Engine<float, 3>();
-            e = x;
-            rc = x->init(positions, velocities, masses, densities, tags, n, h, domain, &prm);
-        }
-    } else {
-        if (dim == 2) {
-            auto* x = new Engine<double, 2>();
-            e = x;
-            rc = x->init(positions, velocities, masses, densities, tags, n, h, domain, &prm);
-        } else {
-            auto* x = new Engine<double, 3>();
-            e = x;
-            rc = x->init(positions, velocities, masses, densities, tags, n, h, domain, &prm);
-        }
+    return SISPH_OK;
+}
+
+static EngineBase* new_engine(int prec, int dim)
+{
+    if (prec == 32) {
+        if (dim == 2) return new Engine<float, 2>();
+        return new Engine<float, 3>();
     }
+    if (dim == 2) return new Engine<double, 2>();
+    return new Engine<double, 3>();
+}
+
+template <class E>
+static int init_as(EngineBase* e, const double* x, const double* u, const double* m, const double* r0,
+                   const int32_t* tags, const int64_t* gid, int64_t nloc, int64_t n, const int32_t* tags_glob, double h,
+                   const sisph_domain* dom, const sisph_params* prm, const DistInfo* di, const double* slab)
+{
+    return static_cast<E*>(e)->init(x, u, m, r0, tags, gid, nloc, n, tags_glob, h, dom, prm, di, slab);
+}
+
+static int init_engine(EngineBase* e, int prec, int dim, const double* x, const double* u, const double* m,
+                       const double* r0, const int32_t* tags, const int64_t* gid, int64_t nloc, int64_t n,
+                       const int32_t* tags_glob, double h, const sisph_domain* dom, const sisph_params* prm,
+                       const DistInfo* di, const double* slab)
+{
+    if (prec == 32) {
+        if (dim == 2) return init_as<Engine<float, 2>>(e, x, u, m, r0, tags, gid, nloc, n, tags_glob, h, dom, prm, di, slab);
+        return init_as<Engine<float, 3>>(e, x, u, m, r0, tags, gid, nloc, n, tags_glob, h, dom, prm, di, slab);
+    }
+    if (dim == 2) return init_as<Engine<double, 2>>(e, x, u, m, r0, tags, gid, nloc, n, tags_glob, h, dom, prm, di, slab);
+    return init_as<Engine<double, 3>>(e, x, u, m, r0, tags, gid, nloc, n, tags_glob, h, dom, prm, di, slab);
+}
+
+extern "C" {
+
+int sisph_create(const double* positions, const double* velocities, const double* masses, const double* densities,
+                 const int32_t* tags, int64_t n, double h, const sisph_domain* domain, const sisph_params* params,
+                 sisph_t** out)
+{
+    if (!out) return fail_thread(SISPH_EINVAL, "out is NULL");
+    *out = nullptr;
+    sisph_params prm;
+    int rc = validate(positions, velocities, masses, densities, tags, n, h, domain, prm, params);
+    if (rc) return rc;
+    EngineBase* e = new_engine(prm.precision, domain->dim);
+    rc = init_engine(e, prm.precision, domain->dim, positions, velocities, masses, densities, tags, nullptr, n, n, tags,
+                     h, domain, &prm, nullptr, nullptr);
     if (rc) {
         g_thread_err = e->err;
         delete e;
+        return rc;
+    }
+    sisph_t* s = new sisph;
+    s->e = e;
+    *out = s;
+    return SISPH_OK;
+}
+
+int sisph_nccl_unique_id(const char* nccl_lib, uint8_t id[128])
+{
+    if (!id) return fail_thread(SISPH_EINVAL, "NULL id");
+    std::string err;
+    NcclApi& a = nccl_api();
+    if (!a.load(nccl_lib, err)) return fail_thread(SISPH_ENCCL, err);
+    ncclUniqueId u;
+    ncclResult_t r = a.GetUniqueId(&u);
+    if (r != ncclSuccess) return fail_thread(SISPH_ENCCL, std::string("ncclGetUniqueId: ") + a.GetErrorString(r));
+    memcpy(id, u.internal, 128);
+    return SISPH_OK;
+}
+
+int sisph_local_group_create(int nranks, sisph_local_group_t** out)
+{
+    if (!out || nranks < 1) return fail_thread(SISPH_EINVAL, "bad arguments");
+    *out = new sisph_local_group(nranks);
+    return SISPH_OK;
+}
+
+void sisph_local_group_destroy(sisph_local_group_t* g) { delete g; }
+
+int sisph_slab_bounds(const sisph_domain* domain, int axis, int nranks, int rank, double* lo, double* hi)
+{
+    if (!domain || !lo || !hi || axis < 0 || axis >= domain->dim || nranks < 1 || rank < 0 || rank >= nranks)
+        return fail_thread(SISPH_EINVAL, "bad arguments");
+    const double a = domain->lo[axis], b = domain->hi[axis], L = b - a;
+    *lo = rank == 0 ? a : a + L * rank / nranks;
+    *hi = rank == nranks - 1 ? b : a + L * (rank + 1) / nranks;
+    return SISPH_OK;
+}
+
+int sisph_create_dist(const double* positions, const double* velocities, const double* masses,
+                      const double* densities, const int32_t* tags, int64_t n, double h, const sisph_domain* domain,
+                      const sisph_params* params, const sisph_dist* dist, sisph_t** out)
+{
+    if (!out) return fail_thread(SISPH_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (!dist) return fail_thread(SISPH_EINVAL, "NULL dist");
+    sisph_params prm;
+    int rc = validate(positions, velocities, masses, densities, tags, n, h, domain, prm, params);
+    if (rc) return rc;
+    const int P_ = dist->nranks, r = dist->rank, ax = dist->slab_axis, dim = domain->dim;
+    if (P_ < 1 || r < 0 || r >= P_ || ax < 0 || ax >= dim) return fail_thread(SISPH_EINVAL, "bad nranks / rank / slab_axis");
+    if (P_ == 1)
+        return sisph_create(positions, velocities, masses, densities, tags, n, h, domain, params, out);
+    const double L = domain->hi[ax] - domain->lo[ax];
+    if (L / P_ < 1.3 * 3.0 * h * 1.01)
+        return fail_thread(SISPH_EINVAL, "slabs thinner than the halo width 1.3 x 3h");
+    double slab[2];
+    sisph_slab_bounds(domain, ax, P_, r, &slab[0], &slab[1]);
+    // ownership of the global particles: slab-axis coordinate in [lo, hi) (the
+    // first / last slab also own what lies below / above a bounded box)
+    std::vector<int64_t> own;
+    for (int pass = 0; pass < 2; pass++)   // fluid, then walls
+        for (int64_t k = 0; k < n; k++) {
+            if ((tags[k] == SISPH_TAG_WALL) != (pass == 1)) continue;
+            const double y = positions[k * dim + ax];
+            const bool lo_ok = r == 0 ? (domain->periodic[ax] ? y >= slab[0] : true) : y >= slab[0];
+            const bool hi_ok = r == P_ - 1 ? (domain->periodic[ax] ? y < slab[1] : true) : y < slab[1];
+            if (lo_ok && hi_ok) own.push_back(k);
+        }
+    const int64_t nl = (int64_t)own.size();
+    std::vector<double> x(nl * dim), u(nl * dim), m(nl), r0(nl);
+    std::vector<int32_t> tg(nl);
+    for (int64_t q = 0; q < nl; q++) {
+        const int64_t k = own[q];
+        for (int a = 0; a < dim; a++) {
+            x[q * dim + a] = positions[k * dim + a];
+            u[q * dim + a] = velocities[k * dim + a];
+        }
+        m[q] = masses[k];
+        r0[q] = densities[k];
+        tg[q] = tags[k];
+    }
+    // transport
+    DistInfo di;
+    di.nranks = P_;
+    di.rank = r;
+    di.axis = ax;
+    Transport* t = nullptr;
+    if (dist->local_group) {
+        auto* lt = new LocalTransport();
+        lt->hub = &dist->local_group->hub;
+        if (lt->hub->nranks != P_) {
+            delete lt;
+            return fail_thread(SISPH_EINVAL, "local group size != nranks");
+        }
+        t = lt;
+    } else {
+        if (prm.device >= 0 && cudaSetDevice(prm.device) != cudaSuccess)
+            return fail_thread(SISPH_ECUDA, "cudaSetDevice failed");
+        auto* nt = new NcclTransport();
+        if (nt->init(dist->nccl_lib, dist->nccl_id, P_, r)) {
+            std::string m_ = nt->err;
+            delete nt;
+            return fail_thread(SISPH_ENCCL, m_);
+        }
+        t = nt;
+    }
+    t->rank = r;
+    t->nranks = P_;
+    const bool per = domain->periodic[ax] != 0;
+    t->nb[0] = r > 0 ? r - 1 : (per ? P_ - 1 : -1);
+    t->nb[1] = r < P_ - 1 ? r + 1 : (per ? 0 : -1);
+    di.tp = t;
+    EngineBase* e = new_engine(prm.precision, dim);
+    rc = init_engine(e, prm.precision, dim, x.data(), u.data(), m.data(), r0.data(), tg.data(), own.data(), nl, n,
+                     tags, h, domain, &prm, &di, slab);
+    if (rc) {
+        g_thread_err = e->err;
+        delete e;   // owns the transport once init has taken it
         return rc;
     }
     sisph_t* s = new sisph;
@@ -1246,6 +1991,11 @@ int sisph_get_counts(const sisph_t* s, int64_t* n, int64_t* n_fluid, int64_t* n_
     if (n_fluid) *n_fluid = s->e->nf;
     if (n_wall) *n_wall = s->e->nw;
     return SISPH_OK;
+}
+int sisph_get_owned_counts(sisph_t* s, int64_t* n_fluid, int64_t* n_wall)
+{
+    CHK_HANDLE(s);
+    return s->e->owned_counts(n_fluid, n_wall);
 }
 int sisph_set_timing(sisph_t* s, int enable)
 {

@@ -24,6 +24,7 @@ struct Ctl {
     int gtvf_far;              // a particle moved more than skin/2 during the GTVF sub-steps
     int pad2;
     unsigned long long umax2_bits;   // max |u~|^2 over fluid (ordered bits of a non-negative double)
+    double red[4];             // slab ranks: local (sum |dp|, sum |p|, nonfinite) of a sweep, allreduced
 };
 
 // ===========================================================================
@@ -49,8 +50,11 @@ __global__ void __launch_bounds__(256) k_max_speed(const V4<T>* __restrict__ vt,
 // (made deterministic later by the stable fix-up, A2).  Warp-aggregated:
 // lanes with equal keys elect one atomic.
 // ===========================================================================
+// Slab halos: particles at i >= nown are ghosts; their key is offset by the
+// cell count, so a stable sort keeps the owned set first (and both sets
+// cell-sorted) and the cell table has 2 x ncells + 1 entries.
 template <class T, int D>
-__global__ void k_hash_count(Params<T> P, const V4<T>* __restrict__ pos, int n,
+__global__ void k_hash_count(Params<T> P, const V4<T>* __restrict__ pos, int n, int nown,
                              int* __restrict__ keys, int* __restrict__ rank, int* __restrict__ ccount)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -60,7 +64,7 @@ __global__ void k_hash_count(Params<T> P, const V4<T>* __restrict__ pos, int n,
         V4<T> x = ld4(pos + i);
         int c[3];
         cell_of<T, D>(P, x, c);
-        key = cell_key(P, c);
+        key = cell_key(P, c) + (i >= nown ? P.nc[0] * P.nc[1] * P.nc[2] : 0);
         keys[i] = key;
     }
     unsigned mask = __ballot_sync(0xffffffffu, act);
@@ -326,19 +330,23 @@ __device__ __forceinline__ int wslot(const int* __restrict__ wperm, int Nf, int 
 }
 
 // slot ranges of the 3^d stencil of cell c: lane r < NROW fills row r = (dy, dz)
-// with up to 3 fluid + 3 wall ranges (x, y) and the image shift code z
-// (2 bits per axis, s + 1 for a shift of s L).  Returns after __syncwarp.
+// with up to 3 ranges for each candidate set (x, y) and the image shift code z
+// (2 bits per axis, s + 1 for a shift of s L): entries 0-2 owned fluid, 3-5
+// owned walls, 6-8 ghost fluid, 9-11 ghost walls (slab halos: keys + ncells).
+// Returns after __syncwarp.
+constexpr int RNG_PER_ROW = 12;
 template <class T, int D>
 __device__ __forceinline__ void stencil_ranges(const Params<T>& P, int c, const int* __restrict__ fstart,
-                                               const int* __restrict__ wstart, int4* o6)
+                                               const int* __restrict__ wstart, int4* o12)
 {
     constexpr int NROW = D == 3 ? 9 : 3;
     const int lane = threadIdx.x & 31;
     if (lane < NROW) {
+        const int NC = P.nc[0] * P.nc[1] * P.nc[2];
         const int c0 = c % P.nc[0], c1 = (c / P.nc[0]) % P.nc[1], c2 = c / (P.nc[0] * P.nc[1]);
         const int dy = lane % 3 - 1, dz = D == 3 ? lane / 3 - 1 : 0;
-        int4* o = o6 + 6 * lane;
-        for (int q = 0; q < 6; q++) o[q] = make_int4(0, 0, 0, 0);
+        int4* o = o12 + RNG_PER_ROW * lane;
+        for (int q = 0; q < RNG_PER_ROW; q++) o[q] = make_int4(0, 0, 0, 0);
         int cy = c1 + dy, cz = c2 + dz;
         int code = 1 | (1 << 2) | (1 << 4);
         bool ok = true;
@@ -354,21 +362,26 @@ __device__ __forceinline__ void stencil_ranges(const Params<T>& P, int c, const 
         }
         if (ok) {
             const int row = P.nc[0] * (cy + P.nc[1] * cz);
-            int x0 = c0 - 1, x1 = c0 + 1;
-            if (P.per[0] && (x0 < 0 || x1 >= P.nc[0])) {
-                for (int dx = 0; dx < 3; dx++) {
-                    int cx = c0 + dx - 1, cd = code;
-                    if (cx < 0) { cx += P.nc[0]; cd -= 1; }
-                    else if (cx >= P.nc[0]) { cx -= P.nc[0]; cd += 1; }
-                    const int key = row + cx;
-                    o[dx] = make_int4(fstart[key], fstart[key + 1], cd, 0);
-                    o[3 + dx] = make_int4(P.Nf + wstart[key], P.Nf + wstart[key + 1], cd, 0);
+            const int nset = P.ghosts ? 2 : 1;
+            for (int g = 0; g < nset; g++) {
+                const int kb = row + g * NC;   // ghost keys are offset by the cell count
+                int4* og = o + 6 * g;
+                int x0 = c0 - 1, x1 = c0 + 1;
+                if (P.per[0] && (x0 < 0 || x1 >= P.nc[0])) {
+                    for (int dx = 0; dx < 3; dx++) {
+                        int cx = c0 + dx - 1, cd = code;
+                        if (cx < 0) { cx += P.nc[0]; cd -= 1; }
+                        else if (cx >= P.nc[0]) { cx -= P.nc[0]; cd += 1; }
+                        const int key = kb + cx;
+                        og[dx] = make_int4(fstart[key], fstart[key + 1], cd, 0);
+                        og[3 + dx] = make_int4(P.Nf + wstart[key], P.Nf + wstart[key + 1], cd, 0);
+                    }
+                } else {
+                    x0 = max(x0, 0);
+                    x1 = min(x1, P.nc[0] - 1);
+                    og[0] = make_int4(fstart[kb + x0], fstart[kb + x1 + 1], code, 0);
+                    og[3] = make_int4(P.Nf + wstart[kb + x0], P.Nf + wstart[kb + x1 + 1], code, 0);
                 }
-            } else {
-                x0 = max(x0, 0);
-                x1 = min(x1, P.nc[0] - 1);
-                o[0] = make_int4(fstart[row + x0], fstart[row + x1 + 1], code, 0);
-                o[3] = make_int4(P.Nf + wstart[row + x0], P.Nf + wstart[row + x1 + 1], code, 0);
             }
         }
     }
@@ -413,7 +426,7 @@ __global__ void __launch_bounds__(32 * BL_WARPS) k_build_cells(Params<T> P, int 
                                                               int* __restrict__ cnt_in, Ctl* ctl)
 {
     constexpr int NROW = D == 3 ? 9 : 3;
-    constexpr int NRNG = NROW * 6;
+    constexpr int NRNG = NROW * RNG_PER_ROW;
     __shared__ V4<T> smem[BL_WARPS][32], smemo[BL_WARPS][32];
     __shared__ int smemj[BL_WARPS][32];
     __shared__ int4 rng[BL_WARPS][NRNG];
@@ -531,7 +544,7 @@ __global__ void __launch_bounds__(32 * BL_WARPS) k_build_loose(Params<T> P, int 
                                                               int* __restrict__ cnt, Ctl* ctl)
 {
     constexpr int NROW = D == 3 ? 9 : 3;
-    constexpr int NRNG = NROW * 6;
+    constexpr int NRNG = NROW * RNG_PER_ROW;
     __shared__ V4<T> smem[BL_WARPS][32];
     __shared__ int smemj[BL_WARPS][32];
     __shared__ int4 rng[BL_WARPS][NRNG];
@@ -607,7 +620,7 @@ __global__ void __launch_bounds__(128) k_filter(Params<T> P, const V4<T>* __rest
 {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int Ntot = P.Ntot, Nf = P.Nf, cap = P.cap, cap_in = P.cap_in;
-    const bool act = i < Ntot;
+    const bool act = i < P.Nfo || (i >= Nf && i < Nf + P.Nwo);   // owned rows
     const bool inner = act && nbr_in && i < Nf;
     const V4<T> xi = ld4(pos + (act ? i : 0));
     const int n = act ? cnts[i] : 0;
@@ -682,7 +695,7 @@ __global__ void __launch_bounds__(256) k_density(Params<T> P, const V4<T>* __res
                                                  T* __restrict__ rho, uint8_t* __restrict__ fs)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= P.Ntot) return;
+    if (i >= P.Ntot || (i >= P.Nfo && i < P.Nf) || i >= P.Nf + P.Nwo) return;   // owned rows
     V4<T> xi = ld4(pos + i);
     if (i >= P.Nf && !P.wall_rho_summation) {
         rho[i] = P.rho0;
@@ -714,7 +727,7 @@ __global__ void __launch_bounds__(256) k_wall_velocity(Params<T> P, const V4<T>*
                                                        const V4<T>* __restrict__ nrm, V4<T>* __restrict__ vel, int mode)
 {
     int w = blockIdx.x * blockDim.x + threadIdx.x;
-    if (w >= P.Nw) return;
+    if (w >= P.Nwo) return;
     int i = P.Nf + w;
     V4<T> xi = ld4(pos + i);
     T sw = 0, ax = 0, ay = 0, az = 0;
@@ -769,7 +782,7 @@ __global__ void __launch_bounds__(128) k_forces_predict(Params<T> P, T dt, const
                                                         V4<T>* __restrict__ rstar)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= P.Nf) return;
+    if (i >= P.Nfo) return;
     V4<T> xi = ld4(pos + i), ui = ld4(vel + i), uti = ld4(vt + i);
     T rhoi = rho[i];
     T ax = P.g[0], ay = P.g[1], az = D == 3 ? P.g[2] : T(0);
@@ -838,7 +851,7 @@ __global__ void __launch_bounds__(128) k_rhs_diag(Params<T> P, T inv_dt, const V
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     double lam = 0.0;
-    if (i < P.Nf) {
+    if (i < P.Nfo) {
         V4<T> xi = ld4(pos + i), ui = ld4(us + i);
         T rhoi = rho[i];
         T sr = 0, sd = 0;
@@ -888,7 +901,7 @@ __global__ void __launch_bounds__(256) k_wall_pressure(Params<T> P, const V4<T>*
         p = (ctl->iter & 1) ? pB : pA;
     }
     int w = blockIdx.x * blockDim.x + threadIdx.x;
-    if (w >= P.Nw) return;
+    if (w >= P.Nwo) return;
     int i = P.Nf + w;
     V4<T> xi = ld4(pos + i);
     T sw = 0, sp = 0, sx = 0, sy = 0, sz = 0;
@@ -936,7 +949,8 @@ __global__ void __launch_bounds__(SWEEP_T) k_sweep(Params<T> P, const V4<T>* __r
                                                    const T* __restrict__ diag, const uint8_t* __restrict__ fs,
                                                    const int* __restrict__ nbr, const int* __restrict__ cnt, int ncap,
                                                    const T* __restrict__ coef, T* pA, T* pB, Ctl* ctl,
-                                                   double* __restrict__ partials, double tol, int min_it, int max_it)
+                                                   double* __restrict__ partials, double tol, int min_it, int max_it,
+                                                   int defer)
 {
     if (ctl->done) return;
     const int kit = ctl->iter;
@@ -945,7 +959,7 @@ __global__ void __launch_bounds__(SWEEP_T) k_sweep(Params<T> P, const V4<T>* __r
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     double dn = 0.0, dd = 0.0;
     bool bad = false;
-    if (i < P.Nf) {
+    if (i < P.Nfo) {
         T pold = pin[i];
         T pnew = T(0);
         T di = diag[i];
@@ -1035,6 +1049,14 @@ __global__ void __launch_bounds__(SWEEP_T) k_sweep(Params<T> P, const V4<T>* __r
             num += sn[q];
             den += sd[q];
         }
+        if (defer) {
+            // slab ranks: the local sums go through an allreduce, k_decide finishes
+            ctl->red[0] = num;
+            ctl->red[1] = den;
+            ctl->red[2] = ctl->nonfinite ? 1.0 : 0.0;
+            ctl->ticket = 0;
+            return;
+        }
         double lam = __longlong_as_double((long long)ctl->lambda_bits);
         double dmax = den > lam ? den : lam;
         double res = num == 0.0 ? 0.0 : (dmax > 0.0 ? num / dmax : INFINITY);
@@ -1044,6 +1066,22 @@ __global__ void __launch_bounds__(SWEEP_T) k_sweep(Params<T> P, const V4<T>* __r
         ctl->done = ((k1 >= min_it && res < tol) || k1 >= max_it || ctl->nonfinite) ? 1 : 0;
         ctl->ticket = 0;
     }
+}
+
+// eq:convergence on the allreduced sums (slab ranks; every rank takes the
+// same decision from the same bits).  A no-op once the solve is done.
+__global__ void k_decide(Ctl* ctl, double tol, int min_it, int max_it)
+{
+    if (ctl->done) return;
+    const double num = ctl->red[0], den = ctl->red[1];
+    const double lam = __longlong_as_double((long long)ctl->lambda_bits);
+    const double dmax = den > lam ? den : lam;
+    const double res = num == 0.0 ? 0.0 : (dmax > 0.0 ? num / dmax : INFINITY);
+    const int k1 = ctl->iter + 1;
+    if (ctl->red[2] > 0.0) ctl->nonfinite = 1;
+    ctl->residual = res;
+    ctl->iter = k1;
+    ctl->done = ((k1 >= min_it && res < tol) || k1 >= max_it || ctl->nonfinite) ? 1 : 0;
 }
 
 // ===========================================================================
@@ -1057,7 +1095,7 @@ __global__ void __launch_bounds__(128) k_pgrad_correct(Params<T> P, T dt, const 
                                                        const int* __restrict__ cnt, int ncap, V4<T>* __restrict__ vel)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= P.Nf) return;
+    if (i >= P.Nfo) return;
     V4<T> xi = ld4(pos + i);
     T rhoi = rho[i], pi = p[i];
     T irhoi = frcp(rhoi);
@@ -1121,7 +1159,7 @@ __global__ void __launch_bounds__(128) k_gtvf_substep(Params<T> P, T dtau, const
                                                       const V4<T>* __restrict__ rstar, int check, Ctl* ctl)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= P.Nf) return;
+    if (i >= P.Nfo) return;
     V4<T> xi = ld4(rk + i);
     T ax = 0, ay = 0, az = 0;
     int n = cnt[i];
@@ -1165,7 +1203,7 @@ __global__ void k_advance(Params<T> P, T dt, const V4<T>* __restrict__ dK, const
                           const V4<T>* __restrict__ vel, V4<T>* __restrict__ pos, V4<T>* __restrict__ vt)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= P.Nf) return;
+    if (i >= P.Nfo) return;
     V4<T> x = ld4(rn + i), u = ld4(vel + i), ut = ld4(vt + i);
     V4<T> dl = dK ? ld4(dK + i) : mk4<T>(T(0), T(0), T(0), T(0));   // r^K - r^0
     T tx = u.x + dl.x / dt, ty = u.y + dl.y / dt;
@@ -1187,7 +1225,7 @@ __global__ void k_normals_raw(Params<T> P, const V4<T>* __restrict__ pos, const 
                               const int* __restrict__ nbr, const int* __restrict__ cnt, int ncap, V4<T>* __restrict__ ns)
 {
     int w = blockIdx.x * blockDim.x + threadIdx.x;
-    if (w >= P.Nw) return;
+    if (w >= P.Nwo) return;
     int i = P.Nf + w;
     V4<T> xi = ld4(pos + i);
     T ax = 0, ay = 0, az = 0;
@@ -1219,7 +1257,7 @@ __global__ void k_normals_smooth(Params<T> P, const V4<T>* __restrict__ pos, con
                                  const V4<T>* __restrict__ ns, V4<T>* __restrict__ nrm)
 {
     int w = blockIdx.x * blockDim.x + threadIdx.x;
-    if (w >= P.Nw) return;
+    if (w >= P.Nwo) return;
     int i = P.Nf + w;
     V4<T> xi = ld4(pos + i);
     T v0 = xi.w / rho[i] * P.w0;
@@ -1247,6 +1285,126 @@ __global__ void k_normals_smooth(Params<T> P, const V4<T>* __restrict__ pos, con
         ax = ay = az = T(0);
     }
     nrm[w] = mk4<T>(ax, ay, az, T(0));
+}
+
+// ===========================================================================
+// Slab decomposition: classification, compaction and
+// pack / unpack of halo and migration records.
+// ===========================================================================
+// wrap the slab-axis coordinate of owned fluid into the global periodic box
+// and classify: 0 stays, 1 leaves across the low face, 2 across the high face
+template <class T>
+__global__ void k_classify(V4<T>* __restrict__ pos, int n, int axis, double slab_lo, double slab_hi, double glo,
+                           double ghi, int gper, int has_lo, int has_hi, int* __restrict__ flag)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    V4<T> x = ld4(pos + i);
+    T* c = reinterpret_cast<T*>(&x);
+    // the face is decided on the unwrapped coordinate (a particle leaving the
+    // first slab downwards goes to the last slab), the stored position is wrapped
+    const double y = (double)c[axis];
+    flag[i] = (has_lo && y < slab_lo) ? 1 : ((has_hi && y >= slab_hi) ? 2 : 0);
+    if (gper) {
+        const T L = (T)(ghi - glo);
+        if (y >= ghi) c[axis] -= L;
+        else if (y < glo) c[axis] += L;
+        pos[i] = x;
+    }
+}
+
+// halo selection: owned particles within G of the low / high face
+template <class T>
+__global__ void k_halo_flags(const V4<T>* __restrict__ pos, int n, int axis, double slab_lo, double slab_hi, double G,
+                             int has_lo, int has_hi, int* __restrict__ flo, int* __restrict__ fhi)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    V4<T> x = ld4(pos + i);
+    const double y = (double)reinterpret_cast<const T*>(&x)[axis];
+    flo[i] = has_lo && y < slab_lo + G ? 1 : 0;
+    fhi[i] = has_hi && y >= slab_hi - G ? 1 : 0;
+}
+
+__global__ void k_flag_eq(const int* __restrict__ flag, int n, int v, int* __restrict__ out)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = flag[i] == v ? 1 : 0;
+}
+
+// stable compaction: out[pre[i]] = i for flagged i (pre = exclusive scan of f)
+__global__ void k_compact(const int* __restrict__ f, const int* __restrict__ pre, int n, int* __restrict__ out,
+                          int* __restrict__ count)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (f[i]) out[pre[i]] = i;
+    if (i == n - 1) *count = pre[i] + f[i];
+}
+
+__global__ void k_invperm(const int* __restrict__ perm, int n, int* __restrict__ inv)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n) inv[perm[t]] = t;
+}
+
+// out[q] = inv[list ? list[q] : base + q]
+__global__ void k_remap(const int* __restrict__ list, int base, int n, const int* __restrict__ inv, int* __restrict__ out)
+{
+    int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < n) out[q] = inv[list ? list[q] : base + q];
+}
+
+// records of up to 8 fields (4-byte multiples first, 1-byte fields last);
+// a field marked shift is a position vector whose slab-axis component gets
+// the face's periodic image shift
+struct PackList {
+    int nf, rec, axis;
+    double shift;
+    void* ptr[8];
+    int size[8];
+    int sh[8];
+};
+
+template <class T>
+__global__ void k_pack(PackList L, const int* __restrict__ idx, int base, int n, char* __restrict__ buf)
+{
+    int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n) return;
+    const int s = idx ? idx[q] : base + q;
+    char* r = buf + (size_t)q * L.rec;
+    int off = 0;
+    for (int f = 0; f < L.nf; f++) {
+        const int sz = L.size[f];
+        const char* src = (const char*)L.ptr[f] + (size_t)s * sz;
+        if (sz == 1) {
+            r[off] = *src;
+        } else {
+            for (int w = 0; w < sz / 4; w++) reinterpret_cast<int*>(r + off)[w] = reinterpret_cast<const int*>(src)[w];
+            if (L.sh[f]) reinterpret_cast<T*>(r + off)[L.axis] += (T)L.shift;
+        }
+        off += sz;
+    }
+}
+
+template <class T>
+__global__ void k_unpack(PackList L, const int* __restrict__ map, int base, int n, const char* __restrict__ buf)
+{
+    int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n) return;
+    const int s = map ? map[q] : base + q;
+    const char* r = buf + (size_t)q * L.rec;
+    int off = 0;
+    for (int f = 0; f < L.nf; f++) {
+        const int sz = L.size[f];
+        char* dst = (char*)L.ptr[f] + (size_t)s * sz;
+        if (sz == 1) {
+            *dst = r[off];
+        } else {
+            for (int w = 0; w < sz / 4; w++) reinterpret_cast<int*>(dst)[w] = reinterpret_cast<const int*>(r + off)[w];
+        }
+        off += sz;
+    }
 }
 
 // ===========================================================================

@@ -25,7 +25,8 @@ VECTOR_FIELDS = {"POSITION", "VELOCITY", "TRANSPORT_VELOCITY", "USTAR", "RSTAR",
 EXPORTED = ["sisph_params_default", "sisph_create", "sisph_destroy", "sisph_build_neighbors",
             "sisph_predict", "sisph_ppe_solve", "sisph_correct", "sisph_step", "sisph_get_field",
             "sisph_set_field", "sisph_get_order", "sisph_get_neighbors", "sisph_get_neighbors_of",
-            "sisph_get_counts",
+            "sisph_get_counts", "sisph_get_owned_counts", "sisph_nccl_unique_id", "sisph_local_group_create",
+            "sisph_local_group_destroy", "sisph_slab_bounds", "sisph_create_dist",
             "sisph_set_timing", "sisph_sync", "sisph_last_error"]
 
 
@@ -52,7 +53,13 @@ class sisph_step_report(C.Structure):
                 ("lambda_", C.c_double), ("ms_predict", C.c_double), ("ms_solve", C.c_double),
                 ("ms_correct", C.c_double), ("pairs", C.c_int64), ("max_neighbors", C.c_int),
                 ("ms_sweeps", C.c_double), ("sweeps_timed", C.c_int), ("launches", C.c_int64),
-                ("single_build", C.c_int), ("skin_radius", C.c_double)]
+                ("single_build", C.c_int), ("skin_radius", C.c_double), ("n_owned_fluid", C.c_int64),
+                ("n_ghost_fluid", C.c_int64), ("halo_bytes", C.c_int64)]
+
+
+class sisph_dist(C.Structure):
+    _fields_ = [("nranks", C.c_int), ("rank", C.c_int), ("slab_axis", C.c_int), ("nccl_id", C.c_uint8 * 128),
+                ("nccl_lib", C.c_char_p), ("local_group", C.c_void_p)]
 
 
 class SisphError(RuntimeError):
@@ -87,6 +94,14 @@ def lib():
         L.sisph_get_neighbors.argtypes = [C.c_void_p, i64p, i64p, C.c_int64, i64p]
         L.sisph_get_neighbors_of.argtypes = [C.c_void_p, i64p, C.c_int64, i64p, i64p, C.c_int64, i64p]
         L.sisph_get_counts.argtypes = [C.c_void_p, i64p, i64p, i64p]
+        L.sisph_get_owned_counts.argtypes = [C.c_void_p, i64p, i64p]
+        L.sisph_nccl_unique_id.argtypes = [C.c_char_p, C.POINTER(C.c_uint8)]
+        L.sisph_local_group_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
+        L.sisph_local_group_destroy.argtypes = [C.c_void_p]
+        L.sisph_slab_bounds.argtypes = [C.POINTER(sisph_domain), C.c_int, C.c_int, C.c_int, dp, dp]
+        L.sisph_create_dist.argtypes = [dp, dp, dp, dp, C.POINTER(C.c_int32), C.c_int64, C.c_double,
+                                        C.POINTER(sisph_domain), C.POINTER(sisph_params), C.POINTER(sisph_dist),
+                                        C.POINTER(C.c_void_p)]
         L.sisph_set_timing.argtypes = [C.c_void_p, C.c_int]
         L.sisph_sync.argtypes = [C.c_void_p]
         L.sisph_last_error.argtypes = [C.c_void_p]
@@ -130,10 +145,66 @@ def domain(dim, lo, hi, periodic) -> sisph_domain:
     return d
 
 
-class Simulation:
-    """Owns one sisph_t handle.  Methods map 1:1 onto the C entry points."""
+def default_nccl_lib():
+    """The NCCL library torch itself loads (nvidia-nccl wheel), else None (loader search)."""
+    try:
+        import nvidia.nccl
+        for d in nvidia.nccl.__path__:
+            p = os.path.join(d, "lib", "libnccl.so.2")
+            if os.path.exists(p):
+                return p
+    except ImportError:
+        pass
+    return None
 
-    def __init__(self, x, u, m, rho, tag, h, dom: sisph_domain, params: sisph_params):
+
+def nccl_unique_id(nccl_lib=None) -> bytes:
+    """sisph_nccl_unique_id: 128 bytes to broadcast to every rank."""
+    buf = (C.c_uint8 * 128)()
+    _check(lib().sisph_nccl_unique_id(nccl_lib.encode() if nccl_lib else None, buf), None)
+    return bytes(buf)
+
+
+def slab_bounds(dom: sisph_domain, axis: int, nranks: int, rank: int):
+    lo, hi = C.c_double(), C.c_double()
+    _check(lib().sisph_slab_bounds(C.byref(dom), axis, nranks, rank, C.byref(lo), C.byref(hi)), None)
+    return lo.value, hi.value
+
+
+class LocalGroup:
+    """sisph_local_group_create: ranks as threads of this process on one GPU (tests)."""
+
+    def __init__(self, nranks):
+        self._g = C.c_void_p()
+        _check(lib().sisph_local_group_create(int(nranks), C.byref(self._g)), None)
+        self.nranks = nranks
+
+    def close(self):
+        if getattr(self, "_g", None):
+            lib().sisph_local_group_destroy(self._g)
+            self._g = None
+
+    __del__ = close
+
+
+def make_dist(nranks, rank, axis, nccl_id: bytes | None = None, nccl_lib=None, local_group: LocalGroup | None = None):
+    d = sisph_dist()
+    d.nranks, d.rank, d.slab_axis = int(nranks), int(rank), int(axis)
+    if nccl_id is not None:
+        for k in range(128):
+            d.nccl_id[k] = nccl_id[k]
+    d.nccl_lib = nccl_lib.encode() if nccl_lib else None
+    d.local_group = local_group._g if local_group is not None else None
+    d._keep = (local_group, nccl_lib)
+    return d
+
+
+class Simulation:
+    """Owns one sisph_t handle.  Methods map 1:1 onto the C entry points.
+    With dist (make_dist(...)), the handle is one rank of a slab-decomposed
+    simulation (sisph_create_dist): every rank passes the same global arrays."""
+
+    def __init__(self, x, u, m, rho, tag, h, dom: sisph_domain, params: sisph_params, dist=None):
         L = lib()
         self.dim = dom.dim
         x = np.ascontiguousarray(x, np.float64)
@@ -143,8 +214,14 @@ class Simulation:
         tag = np.ascontiguousarray(tag, np.int32)
         self.n = int(x.shape[0])
         h_out = C.c_void_p()
-        rc = L.sisph_create(_dp(x), _dp(u), _dp(m), _dp(rho), tag.ctypes.data_as(C.POINTER(C.c_int32)),
-                            self.n, float(h), C.byref(dom), C.byref(params), C.byref(h_out))
+        self.dist = dist
+        if dist is None:
+            rc = L.sisph_create(_dp(x), _dp(u), _dp(m), _dp(rho), tag.ctypes.data_as(C.POINTER(C.c_int32)),
+                                self.n, float(h), C.byref(dom), C.byref(params), C.byref(h_out))
+        else:
+            rc = L.sisph_create_dist(_dp(x), _dp(u), _dp(m), _dp(rho), tag.ctypes.data_as(C.POINTER(C.c_int32)),
+                                     self.n, float(h), C.byref(dom), C.byref(params), C.byref(dist),
+                                     C.byref(h_out))
         _check(rc, None)
         self._h = h_out
         nn, nf, nw = C.c_int64(), C.c_int64(), C.c_int64()
@@ -152,14 +229,19 @@ class Simulation:
         self.n_fluid, self.n_wall = nf.value, nw.value
 
     @classmethod
-    def from_case(cls, case, **overrides):
+    def from_case(cls, case, dist=None, **overrides):
         prm = dict(case.params)
         prm.update(overrides)
         sim = cls(case.x, case.u, case.m, case.rho, case.tag, case.h,
-                  domain(case.dim, case.lo, case.hi, case.periodic), params_from_dict(prm))
+                  domain(case.dim, case.lo, case.hi, case.periodic), params_from_dict(prm), dist=dist)
         if np.any(case.p != 0):
             sim.set("PRESSURE", case.p)
         return sim
+
+    def owned_counts(self):
+        nf, nw = C.c_int64(), C.c_int64()
+        _check(lib().sisph_get_owned_counts(self._h, C.byref(nf), C.byref(nw)), self._h)
+        return nf.value, nw.value
 
     def close(self):
         if getattr(self, "_h", None):

@@ -1,0 +1,139 @@
+"""Slab decomposition of the CUDA path, on one GPU.
+
+R ranks run as threads of this process sharing the GPU through the
+in-process transport (sisph_local_group): every exchange synchronises the
+rank's stream and meets the other ranks at a host barrier, so no kernel ever
+waits on another rank's kernel (B200_PROFILING.md).  The same engine code
+runs over NCCL in production; only the transport differs.
+
+Each case runs a few free SISPH steps decomposed over R slabs and on a single
+handle, from the same inputs: the PPE sweep counts must be equal (the
+residual sums and Lambda are allreduced) and the fields must agree to the
+north_star tolerance (summation order differs across decompositions).
+"""
+import threading
+
+import numpy as np
+import pytest
+
+import synth
+from parity_util import TOL, gpu_sim
+
+pytestmark = pytest.mark.gpu
+
+
+def run_ranks(case, R, axis, nsteps, **over):
+    from paper_1908_01762_b200 import LocalGroup, Simulation, make_dist
+    g = LocalGroup(R)
+    sims, reps, errs = [None] * R, [[] for _ in range(R)], [None] * R
+
+    def work(r):
+        try:
+            s = Simulation.from_case(case, dist=make_dist(R, r, axis, local_group=g), **over)
+            sims[r] = s
+            for _ in range(nsteps):
+                reps[r].append(s.step(case.dt))
+        except Exception as e:  # noqa: BLE001 - reported below
+            errs[r] = e
+
+    th = [threading.Thread(target=work, args=(r,), daemon=True) for r in range(R)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not any(t.is_alive() for t in th), "a rank hung"
+    for e in errs:
+        if e is not None:
+            raise e
+    return sims, reps, g
+
+
+def gathered(sims, field):
+    return sum(s.get(field) for s in sims)
+
+
+CASES = {
+    # periodic both ways, jittered: slabs along x (R = 2, 4) and y (R = 3)
+    "tgv2d_f64_x2": (lambda: synth.tgv2d(), 2, 0),
+    "tgv2d_f64_y3": (lambda: synth.tgv2d(), 3, 1),
+    "tgv2d_f64_x4": (lambda: synth.tgv2d(), 4, 0),
+    # walls, free surface, bounded slab axis (x across the tank)
+    "db2d_f64_x2": (lambda: synth.dambreak2d(nx=30, ny=60, dx=0.0333333, precision=64), 2, 0),
+    "hydro_f64_x3": (lambda: synth.hydrostatic(nx=40, ny=80, dx=0.025, precision=64), 3, 0),
+    # the bench family: periodic spanwise y is the slab axis
+    "db3d_f64_y2": (lambda: synth.dambreak3d(nfx=16, nfy=10, nfz=12, dx=1.0 / 32, tank_nx=40, wall_nz=16,
+                                             precision=64), 2, 1),
+    "db3d_f32_y2": (lambda: synth.dambreak3d(nfx=24, nfy=12, nfz=16, dx=1.0 / 32, tank_nx=60, wall_nz=24,
+                                             precision=32), 2, 1),
+    "tgv3d_f32_z3": (lambda: synth.tgv3d(n=20, precision=32), 3, 2),
+}
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_slab_ranks_equal_single_gpu(name):
+    mk, R, axis = CASES[name]
+    case = mk()
+    prec = case.params["precision"]
+    steps = 3
+    # fp32: fixed sweeps so both decompositions do identical work
+    over = {} if prec == 64 else {"tol": 0.0, "max_iter": 4}
+    single = gpu_sim(case, **over)
+    rs = [single.step(case.dt) for _ in range(steps)]
+    sims, reps, g = run_ranks(case, R, axis, steps, **over)
+    for s in range(steps):
+        its = {reps[r][s].iters for r in range(R)}
+        assert len(its) == 1, f"ranks disagree on the sweep count at step {s}: {its}"
+        assert its.pop() == rs[s].iters, (s, rs[s].iters, [reps[r][s].iters for r in range(R)])
+    # every particle owned by exactly one rank
+    own = sum(s.owned_counts()[0] for s in sims)
+    assert own == case.n_fluid
+    rel, ab = TOL[prec]
+    for fld in ("PRESSURE", "VELOCITY", "TRANSPORT_VELOCITY", "POSITION"):
+        a, b = gathered(sims, fld), single.get(fld)
+        if fld == "POSITION":
+            d = a - b
+            for k in range(case.dim):
+                if case.periodic[k]:
+                    L = case.hi[k] - case.lo[k]
+                    d[:, k] = (d[:, k] + 0.5 * L) % L - 0.5 * L
+            err, scale = np.abs(d).max(), np.abs(case.x).max()
+        else:
+            err, scale = np.abs(a - b).max(), max(np.abs(b).max(), 1e-3)
+        assert err <= rel * scale + ab, f"{fld}: {err:.3e} > {rel * scale + ab:.3e}"
+    # halos were exchanged (and ghosts were present where fluid borders fluid)
+    assert sum(reps[r][-1].halo_bytes for r in range(R)) > 0
+    if not name.startswith("db2d"):      # db2d: the water column lies in one slab
+        assert all(reps[r][-1].n_ghost_fluid > 0 for r in range(R))
+    for s in sims:
+        s.close()
+    g.close()
+
+
+def test_migration_moves_ownership():
+    """Particles pushed across a slab face change owner at the next step and
+    every particle stays owned exactly once."""
+    case = synth.tgv2d()
+    R, axis = 2, 0
+    case.u[:, 0] = 0.9          # uniform drift along the slab axis: particles cross both faces
+    case.u[:, 1] = 0.0
+    sims, reps, g = run_ranks(case, R, axis, 4, tol=1e-3)
+    own = [s.owned_counts()[0] for s in sims]
+    assert sum(own) == case.n_fluid
+    ids = [np.flatnonzero(np.abs(s.get("MASS")) > 0) for s in sims]
+    assert len(np.intersect1d(ids[0], ids[1])) == 0
+    assert len(ids[0]) + len(ids[1]) == case.n
+    x = gathered(sims, "POSITION")
+    from paper_1908_01762_b200 import domain, slab_bounds
+    dom = domain(case.dim, case.lo, case.hi, case.periodic)
+    for r, s in enumerate(sims):
+        lo, hi = slab_bounds(dom, axis, R, r)
+        mine = ids[r][case.tag[ids[r]] == 0]
+        # owned at the start of the last step: at most one step's motion outside the slab
+        xs = x[mine, axis]
+        L = case.hi[axis] - case.lo[axis]
+        d = np.minimum(np.abs(((xs - lo) + 0.5 * L) % L - 0.5 * L), np.abs(((xs - hi) + 0.5 * L) % L - 0.5 * L))
+        outside = ~((xs >= lo) & (xs < hi))
+        assert np.all(d[outside] < 0.9 * case.dt * 2)
+    for s in sims:
+        s.close()
+    g.close()
