@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--slab-self", action="store_true",
+                    help="ablation on one GPU: the slab path (halos over NCCL to itself across the periodic y)")
     ap.add_argument("--matrix-free", action="store_true",
                     help="ablation: the sweep recomputes fac_ij every sweep (PAPER.md:785-801)")
     return ap.parse_args()
@@ -54,6 +56,8 @@ def workload(name, ranks=1):
         c = synth.dambreak3d(ranks=ranks)
         desc = ("3D dam break per-GPU slab (BASELINE configs[4]): fluid 256x64x128 at dx=1/256, "
                 "3 wall layers, y periodic, fp32, tol 1e-2, K=10")
+        if ranks > 1:
+            desc += f"; {ranks} slabs along y, global fluid 256x{64 * ranks}x128 = {c.n_fluid} particles"
     elif name == "tgv3d":
         c = synth.tgv3d()
         desc = "3D Taylor-Green 128^3 periodic (BASELINE configs[3]), fp32, tol 1e-3"
@@ -212,27 +216,52 @@ def run_reference(args):
           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
 
 
+SLAB_AXIS = {"dambreak3d": 1, "tgv3d": 0, "dambreak2d": 0, "hydrostatic": 0}
+
+
 def run_sisph(args):
     import numpy as np
     import torch
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        raise SystemExit("multi-GPU slab decomposition is not available in this build (N=1 only)")
-    torch.cuda.set_device(local)
-    from paper_1908_01762_b200 import Simulation
+    from paper_1908_01762_b200 import Simulation, default_nccl_lib
+    from paper_1908_01762_b200 import dist as D
 
-    case, desc = workload(args.workload)
+    rank, world, local = D.env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    # weak scaling: the per-GPU problem is fixed, the global problem has `world` slabs
+    case, desc = workload(args.workload, ranks=world)
     stream = torch.cuda.current_stream()
-    sim = Simulation.from_case(case, stream=stream.cuda_stream, device=local,
-                               matrix_free=1 if args.matrix_free else 0)
+    over = dict(stream=stream.cuda_stream, device=local, matrix_free=1 if args.matrix_free else 0)
+    if world > 1:
+        # one process per GPU: torch.distributed (NCCL) carries the NCCL id; the halo
+        # exchanges and per-sweep allreduce run inside libsisph over NCCL
+        D.init_process_group("nccl")
+        nccl_lib = default_nccl_lib()
+        uid = D.share_nccl_id(rank, nccl_lib)
+        sim = D.create_rank(case, SLAB_AXIS[args.workload], rank, world, uid, nccl_lib, **over)
+    elif args.slab_self:
+        from paper_1908_01762_b200 import make_dist, nccl_unique_id
+        nccl_lib = default_nccl_lib()
+        d = make_dist(1, 0, SLAB_AXIS[args.workload], nccl_id=nccl_unique_id(nccl_lib), nccl_lib=nccl_lib,
+                      always_slab=True)
+        sim = Simulation.from_case(case, dist=d, **over)
+    else:
+        sim = Simulation.from_case(case, **over)
     sim.set_timing(True)
-    nf, n = sim.n_fluid, sim.n
+    nf, n = sim.n_fluid, sim.n            # global counts
+    nf_own = sim.owned_counts()[0]
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            import torch.distributed as td
+            td.barrier()
+        torch.cuda.synchronize()
+
     for _ in range(args.warmup):
         sim.step(case.dt)
-    torch.cuda.synchronize()
+    barrier()
     reps = []
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
@@ -240,37 +269,42 @@ def run_sisph(args):
         for _ in range(args.steps):
             reps.append(sim.step(case.dt))
         e1.record(stream)
-        torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
-    sweeps = sum(r.iters for r in reps)
-    value = sweeps * nf * world / (ms / 1e3)
+        barrier()
+    ms_rank = e0.elapsed_time(e1)
+    ms = D.max_over_ranks(ms_rank, dev) if world > 1 else ms_rank   # the job's time: its slowest rank
+    sweeps = sum(r.iters for r in reps)   # identical on every rank (allreduced decision)
+    value = sweeps * nf / (ms / 1e3)      # all ranks' fluid particles
     ms_solve = sum(r.ms_solve for r in reps)
     # roofline of the dominant hot-path kernel: the Jacobi sweep (A12)
     ms_sw = sum(r.ms_sweeps for r in reps)
     n_sw = sum(r.sweeps_timed for r in reps)
     pairs = reps[-1].pairs
+    n_loc = nf_own + (n - nf) // world if world > 1 else n     # this rank's rows (roofline: per-GPU kernel)
+    nf_loc = nf_own
     tb = 4 if case.params["precision"] == 32 else 8
     if args.matrix_free:
         # pos (x, y, z, m), rho, p^k of every particle; rhs, diag, cnt, p^{k+1} (+ 1-byte fs) of
         # every fluid particle; the 4-byte neighbour index of every pair
-        b_per = (6 * tb) * n + (3 * tb + 5) * nf + 4 * pairs
+        b_per = (6 * tb) * n_loc + (3 * tb + 5) * nf_loc + 4 * pairs
     else:
         # p^k of every particle; rho, rhs, diag, cnt, p^{k+1} (+ fs) of every fluid particle;
         # per pair the 4-byte index and the stored factor of fac_ij
-        b_per = tb * n + (4 * tb + 5) * nf + (4 + tb) * pairs
+        b_per = tb * n_loc + (4 * tb + 5) * nf_loc + (4 + tb) * pairs
     avg_s = ms_sw / max(n_sw, 1) / 1e3
     achieved = b_per / avg_s / 1e9
     peak, peak_src = peaks()
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32" if case.params["precision"] == 32 else "f64",
+        "scaling": "weak" if args.workload == "dambreak3d" else "strong",
+        "vs_baseline": None, "dtype": "f32" if case.params["precision"] == 32 else "f64",
         "data": "synthetic",
         "config": {"workload": desc, "n_fluid": nf, "n_wall": n - nf, "dt": case.dt,
                    "l2": "inputs larger than L2 (neighbour list %.2f GB, state %.0f MB per GPU)"
-                         % (4 * pairs / 1e9, 24 * n / 1e6),
-                   "parallelism": f"slab x{world}"},
-        "ppe_phase_particle_sweeps_per_s": sweeps * nf * world / (ms_solve / 1e3),
+                         % (4 * pairs / 1e9, 24 * n_loc / 1e6),
+                   "parallelism": f"slab x{world}" + (f" along axis {SLAB_AXIS[args.workload]}, NCCL halos + "
+                                                      "per-sweep allreduce" if world > 1 else "")},
+        "ppe_phase_particle_sweeps_per_s": sweeps * nf / (ms_solve / 1e3),
         "sweeps_per_step": sweeps / args.steps,
         "single_build_steps": sum(r.single_build for r in reps),
         "ms_per_step_phases": {"predict": sum(r.ms_predict for r in reps) / args.steps,
@@ -283,6 +317,9 @@ def run_sisph(args):
                      "traffic": sweep_traffic(), "bytes_per_launch": b_per, "pairs_per_launch": pairs,
                      "avg_launch_us": avg_s * 1e6, "launches_timed": n_sw, "peak_source": peak_src},
         "gpu_launches": int(sum(r.launches for r in reps)),
+        "halo": {"ghost_fluid_per_rank": int(reps[-1].n_ghost_fluid),
+                 "bytes_sent_per_step_rank0": int(sum(r.halo_bytes for r in reps) / args.steps)}
+                if (world > 1 or args.slab_self) else None,
         "clocks": clk.summary(),
     }
     # end to end through the public API with host buffers
@@ -294,8 +331,16 @@ def run_sisph(args):
         sim.get_ptr("VELOCITY", hu.data_ptr(), n * dim)
         sim.get_ptr("TRANSPORT_VELOCITY", hut.data_ptr(), n * dim)
         sim.get_ptr("PRESSURE", hp.data_ptr(), n)
+        if world > 1:
+            # each rank filled its own particles: sum the ranks' arrays into the whole state,
+            # so that every rank can feed any particle it comes to own
+            import torch.distributed as td
+            for hbuf in (hx, hu, hut, hp):
+                t = hbuf.to(dev)
+                td.all_reduce(t)
+                hbuf.copy_(t.cpu())
         out_p = pin((n,))
-        torch.cuda.synchronize()
+        barrier()
         K2 = args.e2e_steps
         sw2 = 0
         t0 = time.perf_counter()
@@ -308,12 +353,20 @@ def run_sisph(args):
             sim.get_ptr("PRESSURE", out_p.data_ptr(), n)
         torch.cuda.synchronize()
         t = time.perf_counter() - t0
-        out["e2e"] = {"value": sw2 * nf * world / t, "unit": UNIT, "h2d_bytes_per_step": 8 * n * (3 * dim + 1),
+        if world > 1:
+            t = D.max_over_ranks(t, dev)
+        out["e2e"] = {"value": sw2 * nf / t, "unit": UNIT, "h2d_bytes_per_step": 8 * n * (3 * dim + 1),
                       "d2h_bytes_per_step": 8 * n, "steps": K2, "ms_per_step": 1e3 * t / K2}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args.workload)
     del np
-    emit(out)
+    if rank == 0:
+        emit(out)
+    if world > 1:
+        sim.close()
+        import torch.distributed as td
+        td.barrier()
+        td.destroy_process_group()
 
 
 def main():

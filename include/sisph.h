@@ -224,6 +224,8 @@ typedef struct {
     sisph_local_group_t* local_group;  /* non-NULL: ranks are threads of THIS process sharing
                                           one GPU, exchanging through device copies at host
                                           barriers (tests; no NCCL) */
+    int always_slab;         /* 1: the slab path even for nranks == 1 (a periodic slab axis then
+                                takes its halo from the rank itself, through the transport) */
 } sisph_dist;
 
 /* A fresh NCCL unique id (ncclGetUniqueId of the library nccl_lib, NULL for
@@ -237,6 +239,10 @@ void sisph_local_group_destroy(sisph_local_group_t* group);
 
 /* [lo, hi) of rank's slab: lo + L r / nranks .. lo + L (r + 1) / nranks along axis. */
 int sisph_slab_bounds(const sisph_domain* domain, int axis, int nranks, int rank, double* lo, double* hi);
+
+/* The rank owning slab-axis coordinate y: the slab whose [lo, hi) holds it;
+ * below / above a bounded box: the first / last slab.  -1 on bad arguments. */
+int sisph_slab_owner(const sisph_domain* domain, int axis, int nranks, double y);
 
 /* Collective create of one rank of a slab-decomposed simulation.  Every rank
  * passes the same GLOBAL arrays (as sisph_create) and keeps its slab and

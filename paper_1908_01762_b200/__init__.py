@@ -5,7 +5,7 @@ C ABI (include/sisph.h), with a thin ctypes binding.
 """
 from .sisph import (EXPORTED, FIELDS, LocalGroup, Simulation, SisphError, default_nccl_lib,  # noqa: F401
                     domain, lib, make_dist, nccl_unique_id, params_from_dict, sisph_dist, sisph_domain,
-                    sisph_params, sisph_step_report, slab_bounds)
+                    sisph_params, sisph_step_report, slab_bounds, slab_owner)
 
 __all__ = ["Simulation", "SisphError", "domain", "params_from_dict", "lib", "FIELDS", "EXPORTED", "LocalGroup",
-           "make_dist", "nccl_unique_id", "slab_bounds", "default_nccl_lib"]
+           "make_dist", "nccl_unique_id", "slab_bounds", "slab_owner", "default_nccl_lib"]

@@ -60,7 +60,7 @@ enum Phase { IDLE = 0, PREDICTED = 1, SOLVED = 2 };
 // distribution of a handle over slab ranks (resolved from sisph_dist)
 struct DistInfo {
     int nranks = 1, rank = 0, axis = 0;
-    Transport* tp = nullptr;   // owned by the engine
+    Transport* tp = nullptr;   // owned by the engine (nranks > 1, or the slab path forced)
 };
 
 struct EngineBase {
@@ -213,7 +213,7 @@ template <class T, int D> struct Engine : EngineBase {
         }
         for (auto& e : ev) SCK(cudaEventCreate(&e));
         const double R = 3.0 * h;
-        if (di && di->nranks > 1) {
+        if (di && di->tp) {
             tp = di->tp;
             axis = di->axis;
             glo = dom->lo[axis];
@@ -1827,6 +1827,19 @@ int sisph_slab_bounds(const sisph_domain* domain, int axis, int nranks, int rank
     return SISPH_OK;
 }
 
+int sisph_slab_owner(const sisph_domain* domain, int axis, int nranks, double y)
+{
+    if (!domain || axis < 0 || axis >= domain->dim || nranks < 1) return -1;
+    // the slab whose [lo, hi) holds y; below the box -> first, above -> last
+    // (a periodic axis has its inputs inside [lo, hi) already)
+    for (int r = 0; r < nranks; r++) {
+        double lo, hi;
+        sisph_slab_bounds(domain, axis, nranks, r, &lo, &hi);
+        if ((r == 0 || y >= lo) && (r == nranks - 1 || y < hi)) return r;
+    }
+    return nranks - 1;
+}
+
 int sisph_create_dist(const double* positions, const double* velocities, const double* masses,
                       const double* densities, const int32_t* tags, int64_t n, double h, const sisph_domain* domain,
                       const sisph_params* params, const sisph_dist* dist, sisph_t** out)
@@ -1839,7 +1852,7 @@ int sisph_create_dist(const double* positions, const double* velocities, const d
     if (rc) return rc;
     const int P_ = dist->nranks, r = dist->rank, ax = dist->slab_axis, dim = domain->dim;
     if (P_ < 1 || r < 0 || r >= P_ || ax < 0 || ax >= dim) return fail_thread(SISPH_EINVAL, "bad nranks / rank / slab_axis");
-    if (P_ == 1)
+    if (P_ == 1 && !dist->always_slab)
         return sisph_create(positions, velocities, masses, densities, tags, n, h, domain, params, out);
     const double L = domain->hi[ax] - domain->lo[ax];
     if (L / P_ < 1.3 * 3.0 * h * 1.01)
@@ -1852,10 +1865,7 @@ int sisph_create_dist(const double* positions, const double* velocities, const d
     for (int pass = 0; pass < 2; pass++)   // fluid, then walls
         for (int64_t k = 0; k < n; k++) {
             if ((tags[k] == SISPH_TAG_WALL) != (pass == 1)) continue;
-            const double y = positions[k * dim + ax];
-            const bool lo_ok = r == 0 ? (domain->periodic[ax] ? y >= slab[0] : true) : y >= slab[0];
-            const bool hi_ok = r == P_ - 1 ? (domain->periodic[ax] ? y < slab[1] : true) : y < slab[1];
-            if (lo_ok && hi_ok) own.push_back(k);
+            if (sisph_slab_owner(domain, ax, P_, positions[k * dim + ax]) == r) own.push_back(k);
         }
     const int64_t nl = (int64_t)own.size();
     std::vector<double> x(nl * dim), u(nl * dim), m(nl), r0(nl);

@@ -26,7 +26,7 @@ EXPORTED = ["sisph_params_default", "sisph_create", "sisph_destroy", "sisph_buil
             "sisph_predict", "sisph_ppe_solve", "sisph_correct", "sisph_step", "sisph_get_field",
             "sisph_set_field", "sisph_get_order", "sisph_get_neighbors", "sisph_get_neighbors_of",
             "sisph_get_counts", "sisph_get_owned_counts", "sisph_nccl_unique_id", "sisph_local_group_create",
-            "sisph_local_group_destroy", "sisph_slab_bounds", "sisph_create_dist",
+            "sisph_local_group_destroy", "sisph_slab_bounds", "sisph_slab_owner", "sisph_create_dist",
             "sisph_set_timing", "sisph_sync", "sisph_last_error"]
 
 
@@ -59,7 +59,7 @@ class sisph_step_report(C.Structure):
 
 class sisph_dist(C.Structure):
     _fields_ = [("nranks", C.c_int), ("rank", C.c_int), ("slab_axis", C.c_int), ("nccl_id", C.c_uint8 * 128),
-                ("nccl_lib", C.c_char_p), ("local_group", C.c_void_p)]
+                ("nccl_lib", C.c_char_p), ("local_group", C.c_void_p), ("always_slab", C.c_int)]
 
 
 class SisphError(RuntimeError):
@@ -99,6 +99,7 @@ def lib():
         L.sisph_local_group_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
         L.sisph_local_group_destroy.argtypes = [C.c_void_p]
         L.sisph_slab_bounds.argtypes = [C.POINTER(sisph_domain), C.c_int, C.c_int, C.c_int, dp, dp]
+        L.sisph_slab_owner.argtypes = [C.POINTER(sisph_domain), C.c_int, C.c_int, C.c_double]
         L.sisph_create_dist.argtypes = [dp, dp, dp, dp, C.POINTER(C.c_int32), C.c_int64, C.c_double,
                                         C.POINTER(sisph_domain), C.POINTER(sisph_params), C.POINTER(sisph_dist),
                                         C.POINTER(C.c_void_p)]
@@ -187,9 +188,15 @@ class LocalGroup:
     __del__ = close
 
 
-def make_dist(nranks, rank, axis, nccl_id: bytes | None = None, nccl_lib=None, local_group: LocalGroup | None = None):
+def slab_owner(dom: sisph_domain, axis: int, nranks: int, y: float) -> int:
+    return lib().sisph_slab_owner(C.byref(dom), axis, nranks, float(y))
+
+
+def make_dist(nranks, rank, axis, nccl_id: bytes | None = None, nccl_lib=None, local_group: LocalGroup | None = None,
+              always_slab=False):
     d = sisph_dist()
     d.nranks, d.rank, d.slab_axis = int(nranks), int(rank), int(axis)
+    d.always_slab = 1 if always_slab else 0
     if nccl_id is not None:
         for k in range(128):
             d.nccl_id[k] = nccl_id[k]
