@@ -1072,10 +1072,11 @@ template <class T, int D> struct Engine : EngineBase {
         const int* cn1 = single ? cnt_s : cnt;
         const int cap1 = single ? cap_s : P.cap;
         // A6 (loose pairs beyond 3h contribute exactly 0: W, dW/dr vanish for q >= 3)
-        if (Ntot) ++nlaunch, k_density<T, D><<<nblk(Ntot, 256), 256, 0, st>>>(P, pos, nb1, cn1, cap1, rho, fs);
+        if (Ntot) ++nlaunch, k_density<T, D><<<nblk(Ntot, 256), 256, 0, st>>>(P, pos, nb1, cn1, cap1, rho, fs, vel);
         SCK(cudaGetLastError());
         if (dist()) {
             PackList L{};
+            pl_add(L, vel, sizeof(V));   // rho rides in the 4th lane
             pl_add(L, rho, sizeof(T));
             SRET(halo_fluid(L));
             if (P.wall_rho_summation) {
@@ -1085,7 +1086,7 @@ template <class T, int D> struct Engine : EngineBase {
             }
         }
         // A7
-        if (Nwo) ++nlaunch, k_wall_velocity<T, D><<<nblk(Nwo, 256), 256, 0, st>>>(P, pos, nb1, cn1, cap1, nrm, vel, 0);
+        if (Nwo) ++nlaunch, k_wall_velocity<T, D><<<nblk(Nwo, 256), 256, 0, st>>>(P, pos, nb1, cn1, cap1, nrm, rho, vel, 0);
         SCK(cudaGetLastError());
         if (dist()) {
             PackList W{};
@@ -1133,7 +1134,7 @@ template <class T, int D> struct Engine : EngineBase {
             SRET(build_list(true));   // + GTVF inner list
         }
         // A10
-        if (Nwo) ++nlaunch, k_wall_velocity<T, D><<<nblk(Nwo, 256), 256, 0, st>>>(P, pos, nbr, cnt, P.cap, nrm, us, P.ustar_noslip ? 0 : 1);
+        if (Nwo) ++nlaunch, k_wall_velocity<T, D><<<nblk(Nwo, 256), 256, 0, st>>>(P, pos, nbr, cnt, P.cap, nrm, rho, us, P.ustar_noslip ? 0 : 1);
         SCK(cudaGetLastError());
         if (dist()) {
             PackList W{};

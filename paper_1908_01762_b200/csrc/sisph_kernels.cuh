@@ -297,7 +297,10 @@ struct NbCursor {
     }
     __device__ __forceinline__ void push(bool acc, int j, int cap)
     {
-        if (acc && k < cap) row[off] = j;
+        // predicated store, no branch: the candidate loop stays straight-line
+        const int pr = (acc && k < cap) ? 1 : 0;
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.b32 [%0], %1;\n\t}"
+                     :: "l"(row + off), "r"(j), "r"(pr) : "memory");
         off += acc ? nb_adv(k) : 0;
         k += acc ? 1 : 0;
     }
@@ -692,7 +695,8 @@ __global__ void __launch_bounds__(128) k_filter(Params<T> P, const V4<T>* __rest
 template <class T, int D>
 __global__ void __launch_bounds__(256) k_density(Params<T> P, const V4<T>* __restrict__ pos,
                                                  const int* __restrict__ nbr, const int* __restrict__ cnt, int ncap,
-                                                 T* __restrict__ rho, uint8_t* __restrict__ fs)
+                                                 T* __restrict__ rho, uint8_t* __restrict__ fs,
+                                                 V4<T>* __restrict__ vel)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= P.Ntot || (i >= P.Nfo && i < P.Nf) || i >= P.Nf + P.Nwo) return;   // owned rows
@@ -711,7 +715,11 @@ __global__ void __launch_bounds__(256) k_density(Params<T> P, const V4<T>* __res
     });
     s = xi.w * P.w0 + P.sig * s;
     rho[i] = s;
-    if (i < P.Nf) fs[i] = (s / P.rho0 < P.fs_ratio) ? 1 : 0;
+    if (i < P.Nf) {
+        fs[i] = (s / P.rho0 < P.fs_ratio) ? 1 : 0;
+        // rho_i rides in the 4th lane of u_i: the force pass gathers one vector less per pair
+        reinterpret_cast<T*>(vel + i)[3] = s;
+    }
 }
 
 // ===========================================================================
@@ -724,7 +732,8 @@ __global__ void __launch_bounds__(256) k_density(Params<T> P, const V4<T>* __res
 template <class T, int D>
 __global__ void __launch_bounds__(256) k_wall_velocity(Params<T> P, const V4<T>* __restrict__ pos,
                                                        const int* __restrict__ nbr, const int* __restrict__ cnt, int ncap,
-                                                       const V4<T>* __restrict__ nrm, V4<T>* __restrict__ vel, int mode)
+                                                       const V4<T>* __restrict__ nrm, const T* __restrict__ rho,
+                                                       V4<T>* __restrict__ vel, int mode)
 {
     int w = blockIdx.x * blockDim.x + threadIdx.x;
     if (w >= P.Nwo) return;
@@ -763,7 +772,7 @@ __global__ void __launch_bounds__(256) k_wall_velocity(Params<T> P, const V4<T>*
         uy -= un * nn.y;
         if (D == 3) uz -= un * nn.z;
     }
-    vel[i] = mk4<T>(ux, uy, uz, T(0));
+    vel[i] = mk4<T>(ux, uy, uz, rho[i]);   // rho_w in the 4th lane (as the fluid's, see k_density)
 }
 
 // ===========================================================================
@@ -793,7 +802,7 @@ __global__ void __launch_bounds__(128) k_forces_predict(Params<T> P, T dt, const
     int n = cnt[i];
     for_nbrs(nbr, ncap, i, n, [&](int j) {
         V4<T> xj = ld4(pos + j), uj = ld4(vel + j);
-        T rhoj = __ldg(rho + j);
+        T rhoj = uj.w;                               // k_density / k_wall_velocity put rho_j there
         T d[3], r, ri;
         T r2 = pair_vec<T, D>(P, xi, xj, d);
         r_of(r2, r, ri);
@@ -829,7 +838,7 @@ __global__ void __launch_bounds__(128) k_forces_predict(Params<T> P, T dt, const
             if (D == 3) az += mj * (ui.z * ai + uj.z * aj);
         }
     });
-    us[i] = mk4<T>(ui.x + dt * ax, ui.y + dt * ay, D == 3 ? ui.z + dt * az : T(0), T(0));
+    us[i] = mk4<T>(ui.x + dt * ax, ui.y + dt * ay, D == 3 ? ui.z + dt * az : T(0), rhoi);   // rho_i in lane 4
     T rx = xi.x + dt * uti.x, ry = xi.y + dt * uti.y, rz = D == 3 ? xi.z + dt * uti.z : xi.z;
     if (P.per[0]) { if (rx >= P.hi[0]) rx -= P.L[0]; else if (rx < P.lo[0]) rx += P.L[0]; }
     if (P.per[1]) { if (ry >= P.hi[1]) ry -= P.L[1]; else if (ry < P.lo[1]) ry += P.L[1]; }
@@ -859,7 +868,7 @@ __global__ void __launch_bounds__(128) k_rhs_diag(Params<T> P, T inv_dt, const V
         T* __restrict__ crow = coef ? coef + nb_base(i, ncap) : nullptr;
         for_nbrs_k(nbr, ncap, i, n, [&](int j, int k) {
             V4<T> xj = ld4(pos + j), uj = ld4(us + j);
-            T rhoj = __ldg(rho + j);
+            T rhoj = uj.w;                           // rho_j rides in u*_j's 4th lane
             T d[3], r, ri;
             T r2 = pair_vec<T, D>(P, xi, xj, d);
             r_of(r2, r, ri);
