@@ -73,6 +73,9 @@ template <class T> struct Params {
     // loose (superset) radius^2 of the single per-step build at r^n (R3):
     // (3h + 2 dt max|u~| + margin)^2 (1 + 2^-10), working precision
     T Rs2;
+    // (3h)^2 (1 + 2^-10): a pair at or beyond it contributes exactly 0 to every
+    // kernel sum (W, dW/dr vanish for q >= 3): passes over the loose list skip it
+    T R2cut;
 };
 
 // ---------------------------------------------------------------------------

@@ -270,6 +270,7 @@ template <class T, int D> struct Engine : EngineBase {
         P.R2d = R * R;
         P.R2lo = (float)(R * R * (1.0 - 1.0 / 4096.0));
         P.R2hi = (float)(R * R * (1.0 + 1.0 / 4096.0));
+        P.R2cut = (T)(R * R * (1.0 + 1.0 / 1024.0));
         const double sigd = D == 2 ? 7.0 / (478.0 * M_PI) : 1.0 / (120.0 * M_PI);
         auto hd = [&](double hh, T& sig, T& dwk, T& inv_) {
             sig = (T)(sigd / pow(hh, D));
@@ -560,7 +561,11 @@ template <class T, int D> struct Engine : EngineBase {
         SCK(cudaMemsetAsync(&ctl->max_count, 0, sizeof(int), st));
         SCK(cudaMemsetAsync(&ctl->pairs_fluid, 0, 2 * sizeof(unsigned long long), st));
         int* ni = nbr_in;
-        if (Ntot) ++nlaunch, k_filter<T, D><<<nblk(Ntot, 128), 128, 0, st>>>(P, pos, nbs, cnt_s, cap_s, nbr, cnt, ni, cnt_in, ctl);
+        const int rows = Nfo + Nwo;
+        if (rows)
+            ++nlaunch, k_filter<T, D, false><<<nblk(rows, 128), 128, 0, st>>>(
+                           P, -1, rows, pos, nbs, cnt_s, cap_s, nbr, cnt, ni, cnt_in, us, fs, T(0), nullptr, nullptr,
+                           nullptr, ctl);
         SCK(cudaGetLastError());
         inner_valid = ni != nullptr;
         return SISPH_OK;

@@ -615,17 +615,28 @@ __global__ void __launch_bounds__(32 * BL_WARPS) k_build_loose(Params<T> P, int 
 // writes the GTVF inner list of fluid rows.  The warp walks to its longest
 // row so that the fp64 band decision can be taken warp-wide.
 // ===========================================================================
-template <class T, int D>
-__global__ void __launch_bounds__(128) k_filter(Params<T> P, const V4<T>* __restrict__ pos,
+//
+// RHS = true (fluid rows): A11 fused in (the contributions to RHS_i, D_ii
+// and the stored factor of fac_ij computed for every kept pair, as
+// k_rhs_diag).  Measured on C5 it is SLOWER than filter + k_rhs_diag (96
+// registers: occupancy halves), so the engine runs RHS = false; kept for
+// the record.
+template <class T, int D, bool RHS>
+__global__ void __launch_bounds__(128) k_filter(Params<T> P, int row0, int nrows, const V4<T>* __restrict__ pos,
                                                 const int* __restrict__ nbs, const int* __restrict__ cnts, int cap_s,
                                                 int* __restrict__ nbr, int* __restrict__ cnt,
-                                                int* __restrict__ nbr_in, int* __restrict__ cnt_in, Ctl* ctl)
+                                                int* __restrict__ nbr_in, int* __restrict__ cnt_in,
+                                                const V4<T>* __restrict__ us, const uint8_t* __restrict__ fs, T inv_dt,
+                                                T* __restrict__ rhs, T* __restrict__ diag, T* __restrict__ coef,
+                                                Ctl* ctl)
 {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    const int Ntot = P.Ntot, Nf = P.Nf, cap = P.cap, cap_in = P.cap_in;
-    const bool act = i < P.Nfo || (i >= Nf && i < Nf + P.Nwo);   // owned rows
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int Nf = P.Nf, cap = P.cap, cap_in = P.cap_in;
+    // rows row0 + t; row0 < 0: every owned row (fluid [0, Nfo), then walls [Nf, Nf + Nwo))
+    const bool act = t < nrows;
+    const int i = row0 >= 0 ? row0 + (act ? t : 0) : (!act ? 0 : (t < P.Nfo ? t : Nf + (t - P.Nfo)));
     const bool inner = act && nbr_in && i < Nf;
-    const V4<T> xi = ld4(pos + (act ? i : 0));
+    const V4<T> xi = ld4(pos + i);
     const int n = act ? cnts[i] : 0;
     int nmax = n;
 #pragma unroll
@@ -633,16 +644,32 @@ __global__ void __launch_bounds__(128) k_filter(Params<T> P, const V4<T>* __rest
     const float Rin2 = inner ? P.Rin2f : -1.f;
     const int pmask = P.per[0] | (P.per[1] << 1) | (P.per[2] << 2);
     NbCursor A, B;
-    A.init(nbr, cap, act ? i : 0);
+    A.init(nbr, cap, i);
     B.init(nbr_in ? nbr_in : nbr, cap_in, inner ? i : 0);
-    const int4* __restrict__ src = reinterpret_cast<const int4*>(nbs + nb_base(act ? i : 0, cap_s));
+    // A11 state
+    V4<T> ui;
+    T rhoi = T(1), sr = T(0), sd = T(0);
+    T* __restrict__ crow = nullptr;
+    if (RHS) {
+        ui = ld4(us + i);
+        rhoi = ui.w;                    // rho_i rides in u*'s 4th lane (k_forces_predict)
+        crow = coef ? coef + nb_base(i, cap) : nullptr;
+    }
+    const int4* __restrict__ src = reinterpret_cast<const int4*>(nbs + nb_base(i, cap_s));
+    int4 vnext = n > 0 ? __ldg(src) : make_int4(i, i, i, i);
     for (int c = 0; c < nmax; c += 4) {
-        const int4 v = c < n ? __ldg(src + (size_t)(c >> 2) * 32) : make_int4(0, 0, 0, 0);
+        const int4 v = vnext;
+        // prefetch the next chunk of indices while this one is tested
+        vnext = c + 4 < n ? __ldg(src + (size_t)((c + 4) >> 2) * 32) : make_int4(i, i, i, i);
+        V4<T> xj4[4];
+        int j4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int e = 0; e < 4; e++) xj4[e] = ld4(pos + (c + e < n ? j4[e] : i));
 #pragma unroll
         for (int e = 0; e < 4; e++) {
             const bool valid = c + e < n;
-            const int j = e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
-            const V4<T> xj = ld4(pos + (valid ? j : 0));
+            const int j = j4[e];
+            const V4<T> xj = xj4[e];
             float r2;
             bool in;
             if constexpr (std::is_same<T, float>::value) {
@@ -663,13 +690,38 @@ __global__ void __launch_bounds__(128) k_filter(Params<T> P, const V4<T>* __rest
                 in = nb_test<D>(P, xi, xj, r2);
             }
             in = in && valid;
+            if (RHS) {
+                // eq:sph-ppe right side (R8) and eq:coeff (R6/R7), as k_rhs_diag
+                const V4<T> uj = in ? ld4(us + j) : ui;
+                const T rhoj = in ? uj.w : T(1);
+                T d[3], r, ri;
+                const T rr2 = pair_vec<T, D>(P, xi, xj, d);
+                r_of(rr2, r, ri);
+                const T p4 = quintic4(r * P.inv_h);
+                const T mj = xj.w;
+                T ud = (ui.x - uj.x) * d[0] + (ui.y - uj.y) * d[1];
+                if (D == 3) ud += (ui.z - uj.z) * d[2];
+                const T fr = mj * frcp(rhoj) * (ud * p4 * ri);
+                const T f = mj * (r * p4) * frcp((rhoi + rhoj) * (rr2 + P.eta_h2));
+                sr += in ? fr : T(0);
+                sd += in ? f : T(0);
+                if (crow && in && A.k < cap) crow[nb_off(A.k)] = f;
+            }
             A.push(in, j, cap);
             B.push(in && r2 < Rin2, j, cap_in);
         }
     }
+    double lam = 0.0;
     if (act) {
         cnt[i] = min(A.k, cap);
         if (inner) cnt_in[i] = min(B.k, cap_in);
+        if (RHS) {
+            sr *= -P.dwk * inv_dt;
+            sd *= T(4) * P.dwk * frcp(rhoi);
+            rhs[i] = sr;
+            diag[i] = sd;
+            if (!fs[i] && sd != T(0)) lam = (double)fabs(sr / sd);
+        }
     }
     int mmax = act ? max(A.k, inner && B.k > cap_in ? cap + 1 : 0) : 0;
     unsigned sfl = act && i < Nf ? (unsigned)min(A.k, cap) : 0u, sin_ = inner ? (unsigned)B.k : 0u;
@@ -679,11 +731,13 @@ __global__ void __launch_bounds__(128) k_filter(Params<T> P, const V4<T>* __rest
         sfl += __shfl_xor_sync(0xffffffffu, sfl, o);
         sin_ += __shfl_xor_sync(0xffffffffu, sin_, o);
     }
+    if (RHS) lam = warp_max(lam);
     if ((threadIdx.x & 31) == 0) {
         atomicMax(&ctl->max_count, mmax);
         if (mmax > cap) atomicExch(&ctl->overflow, 1);
         if (sfl) atomicAdd(&ctl->pairs_fluid, (unsigned long long)sfl);
         if (sin_) atomicAdd(&ctl->pairs_inner, (unsigned long long)sin_);
+        if (RHS && lam > 0.0) atomicMax(&ctl->lambda_bits, (unsigned long long)__double_as_longlong(lam));
     }
 }
 
@@ -711,7 +765,7 @@ __global__ void __launch_bounds__(256) k_density(Params<T> P, const V4<T>* __res
         V4<T> xj = ld4(pos + j);
         T d[3], r, ri;
         r_of(pair_vec<T, D>(P, xi, xj, d), r, ri);
-        s += xj.w * quintic5(r * P.inv_h);
+        s += xj.w * quintic5(r * P.inv_h);           // W = 0 exactly beyond 3h (loose-list pairs)
     });
     s = xi.w * P.w0 + P.sig * s;
     rho[i] = s;
@@ -745,7 +799,9 @@ __global__ void __launch_bounds__(256) k_wall_velocity(Params<T> P, const V4<T>*
         if (j >= P.Nf) return;
         V4<T> xj = ld4(pos + j);
         T d[3], r, ri;
-        r_of(pair_vec<T, D>(P, xi, xj, d), r, ri);
+        const T r2 = pair_vec<T, D>(P, xi, xj, d);
+        if (r2 >= P.R2cut * T(0.25)) return;          // beyond 3 (h/2): W(r, h/2) = 0
+        r_of(r2, r, ri);
         T wv = P.sig2 * quintic5(r * P.inv_h2);
         V4<T> uj = ld4(vel + j);
         ax += uj.x * wv;
@@ -801,6 +857,8 @@ __global__ void __launch_bounds__(128) k_forces_predict(Params<T> P, T dt, const
     const T irhoi = frcp(rhoi);
     int n = cnt[i];
     for_nbrs(nbr, ncap, i, n, [&](int j) {
+        // (loose-list pairs beyond 3h contribute exactly 0: dW/dr = 0 for q >= 3; skipping
+        // them per lane measured slower -- divergence -- than computing the zeros)
         V4<T> xj = ld4(pos + j), uj = ld4(vel + j);
         T rhoj = uj.w;                               // k_density / k_wall_velocity put rho_j there
         T d[3], r, ri;
