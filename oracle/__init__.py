@@ -84,6 +84,7 @@ def lib():
         L.or_pass_sweep.argtypes = [C.c_void_p, dp, C.c_int64, ip64, dp]
         L.or_num_pairs.restype = C.c_int64
         L.or_num_pairs.argtypes = [C.c_void_p, C.c_int]
+        L.or_next_dt.argtypes = [C.c_void_p, dp, dp, dp]
         _lib = L
     return _lib
 
@@ -184,7 +185,7 @@ def neighbors(cfg, x, dests=None, brute=False):
 class Sim:
     """The oracle's simulation state, kept in creation-id order."""
 
-    VEC = ("x", "u", "ut", "xs", "us", "normal", "xk")
+    VEC = ("x", "u", "ut", "xs", "us", "normal", "xk", "ftot")
 
     def __init__(self, case=None, *, cfg=None, x=None, u=None, m=None, rho=None, p=None, tag=None):
         if case is not None:
@@ -237,6 +238,13 @@ class Sim:
 
     def correct(self, dt):
         lib().or_correct(self._h, float(dt))
+
+    def next_dt(self):
+        """Adaptive time step of the next step: (dt, dt_cfl, dt_force)."""
+        a, b, c = C.c_double(), C.c_double(), C.c_double()
+        if lib().or_next_dt(self._h, C.byref(a), C.byref(b), C.byref(c)) != 0:
+            raise RuntimeError("next_dt before any completed step")
+        return a.value, b.value, c.value
 
     def step(self, dt):
         r = Report()

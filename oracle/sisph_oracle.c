@@ -308,6 +308,9 @@ struct or_sim {
     double *rhs, *diag, *fs;            /* PPE scratch */
     double* nrm;                        /* wall unit normals */
     double* xk;                         /* GTVF sub-step positions r^K */
+    double* anp;                        /* f_visc + f_avisc + f_astress + f_body of the last predict */
+    double* ftot;                       /* f^n = anp + f_p of the last correct */
+    int stepped;                        /* a correct has completed (ftot valid) */
     double lambda;
     csr_t nb[2];                        /* 0: built at x (r^n), 1: built at xs (r*) */
 };
@@ -439,6 +442,7 @@ or_sim* or_create(const or_cfg* c, int64_t n, const double* x3, const double* u3
     s->xs = dalloc(3 * n); s->us = dalloc(3 * n); s->nrm = dalloc(3 * n); s->xk = dalloc(3 * n);
     s->m = dalloc(n); s->rho = dalloc(n); s->p = dalloc(n);
     s->rhs = dalloc(n); s->diag = dalloc(n); s->fs = dalloc(n);
+    s->anp = dalloc(3 * n); s->ftot = dalloc(3 * n);
     memcpy(s->x, x3, (size_t)(3 * n) * sizeof(double));
     memcpy(s->xs, x3, (size_t)(3 * n) * sizeof(double));
     memcpy(s->u, u3, (size_t)(3 * n) * sizeof(double));
@@ -461,6 +465,7 @@ void or_destroy(or_sim* s)
     free(s->tag); free(s->x); free(s->u); free(s->ut); free(s->xs); free(s->us);
     free(s->nrm); free(s->xk); free(s->m); free(s->rho); free(s->p);
     free(s->rhs); free(s->diag); free(s->fs);
+    free(s->anp); free(s->ftot);
     free(s);
 }
 
@@ -480,6 +485,7 @@ static double* field_ptr(or_sim* s, const char* f, int* ncomp)
     if (!strcmp(f, "rhs")) return s->rhs;
     if (!strcmp(f, "diag")) return s->diag;
     if (!strcmp(f, "fs")) return s->fs;
+    if (!strcmp(f, "ftot")) { *ncomp = 3; return s->ftot; }
     if (!strcmp(f, "lambda")) return &s->lambda;
     return NULL;
 }
@@ -626,6 +632,7 @@ static void pass_forces_predict(or_sim* s, double dt)
         for (int a = 0; a < 3; a++) {
             s->us[3 * i + a] = a < dim ? ui[a] + dt * acc[a] : 0.0;
             s->xs[3 * i + a] = a < dim ? s->x[3 * i + a] + dt * uti[a] : 0.0;
+            s->anp[3 * i + a] = a < dim ? acc[a] : 0.0;
         }
         wrap_pos(c, s->xs + 3 * i);
     }
@@ -827,8 +834,12 @@ void or_correct(or_sim* s, double dt)
             else f = mj / (rhoi * rhoj) * (pj - pi);
             for (int a = 0; a < dim; a++) acc[a] -= f * gw[a];
         }
-        for (int a = 0; a < dim; a++) unew[3 * i + a] = s->us[3 * i + a] + dt * acc[a];
+        for (int a = 0; a < dim; a++) {
+            unew[3 * i + a] = s->us[3 * i + a] + dt * acc[a];
+            s->ftot[3 * i + a] = s->anp[3 * i + a] + acc[a];   /* f^n = f_np + f_p */
+        }
     }
+    s->stepped = 1;
     /* GTVF background pressure p0 (R22) and K sub-steps */
     double* p0 = dalloc(n);
     for (int64_t i = 0; i < n; i++) {
@@ -884,6 +895,36 @@ void or_correct(or_sim* s, double dt)
         wrap_pos(c, s->x + 3 * i);
     }
     free(unew); free(p0); free(rn); free(vk); free(fk);
+}
+
+/* Adaptive time step:
+ *   dt_cfl   = 0.25 h / max_i |u_i^n|          (max over fluid, velocities after the step)
+ *   dt_force = 0.25 sqrt(h / max_i |f_i^n|),  f^n = f_p + f_visc + f_body + f_avisc + f_astress
+ *   dt^{n+1} = min(dt_cfl, dt_force)
+ * An unrestricted criterion (zero maximum) is +infinity.  Returns -1 if no
+ * step has completed. */
+int or_next_dt(or_sim* s, double* dt_next, double* dt_cfl, double* dt_force)
+{
+    if (!s->stepped) return -1;
+    int dim = s->c.dim;
+    double um = 0.0, fm = 0.0;
+    for (int64_t i = 0; i < s->n; i++) {
+        if (s->tag[i] != FLUID) continue;
+        double u2 = 0.0, f2 = 0.0;
+        for (int a = 0; a < dim; a++) {
+            u2 += s->u[3 * i + a] * s->u[3 * i + a];
+            f2 += s->ftot[3 * i + a] * s->ftot[3 * i + a];
+        }
+        if (u2 > um) um = u2;
+        if (f2 > fm) fm = f2;
+    }
+    double h = s->c.h;
+    double a = um > 0.0 ? 0.25 * h / sqrt(um) : INFINITY;
+    double b = fm > 0.0 ? 0.25 * sqrt(h / sqrt(fm)) : INFINITY;
+    if (dt_cfl) *dt_cfl = a;
+    if (dt_force) *dt_force = b;
+    if (dt_next) *dt_next = a < b ? a : b;
+    return 0;
 }
 
 void or_step(or_sim* s, double dt, or_report* rep)

@@ -83,4 +83,10 @@ void or_pass_wall_pressure(or_sim* s, const double* pk, double* pw_out);   /* at
 void or_pass_sweep(or_sim* s, const double* pk, int64_t nd, const int64_t* dests, double* out);
 int64_t or_num_pairs(or_sim* s, int which);  /* 0: build at x, 1: build at xs */
 
+/* adaptive time step of the next step from the last completed
+ * step: min(0.25 h / max|u|, 0.25 sqrt(h / max|f|)) over fluid, f = f_p +
+ * f_visc + f_body + f_avisc + f_astress; +inf for an unrestricted criterion;
+ * -1 if no step has completed */
+int or_next_dt(or_sim* s, double* dt_next, double* dt_cfl, double* dt_force);
+
 #endif

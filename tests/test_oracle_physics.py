@@ -330,3 +330,39 @@ def test_hydrostatic_column(orc):
     assert errs[:, 0].max() < 0.08 and errs[:, 1].max() < 0.05
     assert errs[-1, 0] < 0.06 and errs[-1, 1] < 0.02
     assert np.abs(s.get("u")[f]).max() < 0.1
+
+
+# ---------------------------------------------------------------- adaptive time step
+def test_adaptive_dt_free_fall_closed_form(orc):
+    # A periodic lattice translating uniformly under uniform gravity: the PPE
+    # source of a uniform u* vanishes, p stays uniform (0), so f_p = 0 exactly;
+    # viscosity, artificial viscosity and the artificial stress of a uniform
+    # field (u~ = u) vanish too.  Hence f^n = g exactly and u^{n+1} = U0 + dt g:
+    #   dt_cfl = 0.25 h / |U0 + dt g|,  dt_force = 0.25 sqrt(h / |g|),
+    # and dt^{n+1} is their minimum (a swapped ratio, a dropped sqrt or a missing
+    # force term fails one of the three).
+    g = np.array([0.0, -9.81])
+    U0 = np.array([0.3, 0.2])
+    case, s = _resting_lattice(orc, 2, 16, jitter=0.1, p_ref=0.0, g=[0.0, -9.81, 0.0], nu=0.01,
+                               alpha=0.05, c_ref=10.0, pgrad=1)
+    with pytest.raises(RuntimeError):
+        s.next_dt()
+    s.set("u", np.tile(U0, (case.n, 1)))
+    s.set("ut", np.tile(U0, (case.n, 1)))
+    dt = 1e-3
+    s.step(dt)
+    assert np.allclose(s.get("ftot"), g, rtol=0, atol=1e-9)
+    dtn, dtc, dtf = s.next_dt()
+    h = case.h
+    assert dtc == pytest.approx(0.25 * h / np.linalg.norm(U0 + dt * g), rel=1e-12)
+    assert dtf == pytest.approx(0.25 * np.sqrt(h / 9.81), rel=1e-9)
+    assert dtn == min(dtc, dtf)
+
+
+def test_adaptive_dt_unrestricted_at_rest(orc):
+    # a resting lattice without body force: no velocity and no force, both
+    # criteria are unrestricted (P:675-694 divides by the maxima)
+    case, s = _resting_lattice(orc, 2, 12, p_ref=0.0)
+    s.step(1e-3)
+    dtn, dtc, dtf = s.next_dt()
+    assert np.isinf(dtc) and np.isinf(dtf) and np.isinf(dtn)
