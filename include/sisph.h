@@ -178,6 +178,18 @@ int sisph_correct(sisph_t* s, double dt);
  * correct.  rep may be NULL. */
 int sisph_step(sisph_t* s, double dt, sisph_step_report* rep);
 
+/* Adaptive time step for the next step, from the step that last
+ * completed (sisph_step or sisph_correct):
+ *   dt_cfl   = 0.25 h / max_i |u_i|      (fluid velocities after that step)
+ *   dt_force = 0.25 sqrt(h / max_i |f_i|), f = f_p + f_visc + f_body + f_avisc + f_astress
+ *              of that step (the GTVF shift is not a force on u, eq:int:vnp1)
+ *   dt_next  = min(dt_cfl, dt_force)
+ * +INFINITY for an unrestricted criterion (zero maximum).  The maxima are
+ * reduced on the device inside the step (no extra pass); slab ranks allreduce
+ * them (collective call).  Output pointers may be NULL.  Errors: SISPH_EINVAL
+ * before the first completed step. */
+int sisph_next_dt(sisph_t* s, double* dt_next, double* dt_cfl, double* dt_force);
+
 /* Copy a field out / in, creation-id order.  count must equal n (scalars) or
  * n * dim (vectors), else SISPH_EINVAL.  TAG is read only. */
 int sisph_get_field(sisph_t* s, sisph_field f, double* out, int64_t count);

@@ -80,6 +80,7 @@ struct EngineBase {
     virtual int get_neighbors_of(const int64_t* which, int64_t m, int64_t* off, int64_t* ids, int64_t cap,
                                  int64_t* total) = 0;
     virtual int owned_counts(int64_t* nfo, int64_t* nwo) = 0;
+    virtual int next_dt(double* dtn, double* dtc, double* dtf) = 0;
     virtual int sync() = 0;
     int timing = 0;
     int64_t nlaunch = 0;  // kernel launches issued (all entry points)
@@ -115,6 +116,8 @@ template <class T, int D> struct Engine : EngineBase {
     V *pos = nullptr, *pos_alt = nullptr, *vel = nullptr, *vel_alt = nullptr, *us = nullptr, *us_alt = nullptr;
     V *vt = nullptr, *vt_alt = nullptr, *rn = nullptr, *rstar = nullptr, *nrm = nullptr, *nstmp = nullptr;
     V *rkA = nullptr, *rkB = nullptr, *vk = nullptr, *dk = nullptr;
+    V* fnp = nullptr;       // non-pressure acceleration of A8 (adaptive dt)
+    bool stepped = false;   // a correct has completed: next_dt is defined
     T *p = nullptr, *p_alt = nullptr, *rho = nullptr, *rho_alt = nullptr, *rhs = nullptr, *diag = nullptr;
     uint8_t *fs = nullptr, *fs_alt = nullptr;
     int *pid = nullptr, *pid_alt = nullptr;
@@ -173,7 +176,7 @@ template <class T, int D> struct Engine : EngineBase {
                         ccount, fstart, wstart, bsum, nbr, cnt, ctl, partials, dtmp, nbr_in, cnt_in,
                         nbs, cnt_s, wperm_s, wstart_s, coef, dflag, dflag2, dpre, dlist[0], dlist[1], dlist[2],
                         dcnt, fsend[0], fsend[1], fsend_pre[0], fsend_pre[1], grecv, wsend[0], wsend[1], wrecv,
-                        inv, sbuf[0], sbuf[1], rbuf[0], rbuf[1], wtmp};
+                        inv, sbuf[0], sbuf[1], rbuf[0], rbuf[1], wtmp, fnp};
         if (st) cudaStreamSynchronize(st);
         for (void* q : ptrs)
             if (q) cudaFree(q);
@@ -348,7 +351,7 @@ template <class T, int D> struct Engine : EngineBase {
     if (rc) return rc;
         AL(pos, V, NT) AL(pos_alt, V, NT) AL(vel, V, NT) AL(vel_alt, V, NT) AL(us, V, NT) AL(us_alt, V, NT)
         AL(vt, V, NF) AL(vt_alt, V, NF) AL(rn, V, NT) AL(rstar, V, NT) AL(nrm, V, NW) AL(nstmp, V, NW)
-        AL(rkA, V, NT) AL(rkB, V, NT) AL(vk, V, NF) AL(dk, V, NF)
+        AL(rkA, V, NT) AL(rkB, V, NT) AL(vk, V, NF) AL(dk, V, NF) AL(fnp, V, NF)
         AL(p, T, NT) AL(p_alt, T, NT) AL(rho, T, NT) AL(rho_alt, T, NT) AL(rhs, T, NF) AL(diag, T, NF)
         AL(fs, uint8_t, NF) AL(fs_alt, uint8_t, NF) AL(pid, int, NT) AL(pid_alt, int, NT)
         AL(keys, int, NT) AL(rank, int, NT) AL(perm0, int, NT) AL(perm, int, NT)
@@ -1099,7 +1102,7 @@ template <class T, int D> struct Engine : EngineBase {
             SRET(halo_walls(W));
         }
         // A8
-        if (Nfo) ++nlaunch, k_forces_predict<T, D><<<nblk(Nfo, 128), 128, 0, st>>>(P, (T)dt, pos, vel, vt, rho, nb1, cn1, cap1, us, rstar);
+        if (Nfo) ++nlaunch, k_forces_predict<T, D><<<nblk(Nfo, 128), 128, 0, st>>>(P, (T)dt, pos, vel, vt, rho, nb1, cn1, cap1, us, rstar, fnp);
         SCK(cudaGetLastError());
         if (dist()) {
             PackList L{};
@@ -1299,7 +1302,8 @@ template <class T, int D> struct Engine : EngineBase {
             pl_add(W, p + Nf, sizeof(T));
             SRET(halo_walls(W));
         }
-        if (Nfo) ++nlaunch, k_pgrad_correct<T, D><<<nblk(Nfo, 128), 128, 0, st>>>(P, (T)dt, pos, rho, p, us, nbr, cnt, P.cap, vel);
+        SCK(cudaMemsetAsync(&ctl->fmax2_bits, 0, 2 * sizeof(unsigned long long), st));
+        if (Nfo) ++nlaunch, k_pgrad_correct<T, D><<<nblk(Nfo, 128), 128, 0, st>>>(P, (T)dt, pos, rho, p, us, nbr, cnt, P.cap, vel, fnp, ctl);
         // A14: K sub-steps (p0 = 0 everywhere when p_ref == 0: the shift is exactly zero)
         const V* rK = nullptr;   // GTVF displacement r^K - r^0 (none when p0 = 0)
         if (P.p_ref != T(0) && K > 0 && (Nf || dist())) {
@@ -1325,9 +1329,10 @@ template <class T, int D> struct Engine : EngineBase {
             }
         }
         // A15
-        if (Nfo) ++nlaunch, k_advance<T, D><<<nblk(Nfo, 256), 256, 0, st>>>(P, (T)dt, rK, rn, vel, pos, vt);
+        if (Nfo) ++nlaunch, k_advance<T, D><<<nblk(Nfo, 256), 256, 0, st>>>(P, (T)dt, rK, rn, vel, pos, vt, ctl);
         SCK(cudaGetLastError());
         phase = IDLE;
+        stepped = true;
         return SISPH_OK;
     }
 
@@ -1648,6 +1653,30 @@ template <class T, int D> struct Engine : EngineBase {
             for (int k = 0; k < hc[s]; k++) row[k] = hp[rows[(size_t)q * P.cap + k]];
             std::sort(row, row + hc[s]);
         }
+        return SISPH_OK;
+    }
+
+    // adaptive time step of the next step from the maxima the last
+    // correct reduced on the device (slab ranks: allreduced)
+    int next_dt(double* dtn, double* dtc, double* dtf) override
+    {
+        if (!stepped) {
+            err = "next_dt needs a completed step";
+            return SISPH_EINVAL;
+        }
+        if (dist()) SRET(xallreduce(reinterpret_cast<double*>(&ctl->fmax2_bits), 2, 1));
+        SCK(cudaMemcpyAsync(&hctl->fmax2_bits, &ctl->fmax2_bits, 2 * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, st));
+        SCK(cudaStreamSynchronize(st));
+        double f2, v2;
+        memcpy(&f2, &hctl->fmax2_bits, sizeof(double));
+        memcpy(&v2, &hctl->vmax2_bits, sizeof(double));
+        const double hh = (double)P.h;
+        const double a = v2 > 0.0 ? 0.25 * hh / sqrt(v2) : INFINITY;
+        const double b = f2 > 0.0 ? 0.25 * sqrt(hh / sqrt(f2)) : INFINITY;
+        if (dtc) *dtc = a;
+        if (dtf) *dtf = b;
+        if (dtn) *dtn = a < b ? a : b;
         return SISPH_OK;
     }
 
@@ -2012,6 +2041,11 @@ int sisph_get_owned_counts(sisph_t* s, int64_t* n_fluid, int64_t* n_wall)
 {
     CHK_HANDLE(s);
     return s->e->owned_counts(n_fluid, n_wall);
+}
+int sisph_next_dt(sisph_t* s, double* dt_next, double* dt_cfl, double* dt_force)
+{
+    CHK_HANDLE(s);
+    return s->e->next_dt(dt_next, dt_cfl, dt_force);
 }
 int sisph_set_timing(sisph_t* s, int enable)
 {

@@ -25,7 +25,16 @@ struct Ctl {
     int pad2;
     unsigned long long umax2_bits;   // max |u~|^2 over fluid (ordered bits of a non-negative double)
     double red[4];             // slab ranks: local (sum |dp|, sum |p|, nonfinite) of a sweep, allreduced
+    unsigned long long fmax2_bits;   // max |f^n|^2 of the last correct (adaptive dt)
+    unsigned long long vmax2_bits;   // max |u^{n+1}|^2 of the last correct
 };
+
+// warp max of a non-negative double, one atomic per warp (all 32 lanes present)
+__device__ __forceinline__ void warp_max_to(double v, unsigned long long* dst)
+{
+    v = warp_max(v);
+    if ((threadIdx.x & 31) == 0 && v > 0.0) atomicMax(dst, (unsigned long long)__double_as_longlong(v));
+}
 
 // ===========================================================================
 // max |u~_i|^2 over fluid particles: sizes the skin of the single per-step
@@ -844,7 +853,7 @@ __global__ void __launch_bounds__(128) k_forces_predict(Params<T> P, T dt, const
                                                         const V4<T>* __restrict__ vel, const V4<T>* __restrict__ vt,
                                                         const T* __restrict__ rho, const int* __restrict__ nbr,
                                                         const int* __restrict__ cnt, int ncap, V4<T>* __restrict__ us,
-                                                        V4<T>* __restrict__ rstar)
+                                                        V4<T>* __restrict__ rstar, V4<T>* __restrict__ fnp)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= P.Nfo) return;
@@ -897,6 +906,7 @@ __global__ void __launch_bounds__(128) k_forces_predict(Params<T> P, T dt, const
         }
     });
     us[i] = mk4<T>(ui.x + dt * ax, ui.y + dt * ay, D == 3 ? ui.z + dt * az : T(0), rhoi);   // rho_i in lane 4
+    fnp[i] = mk4<T>(ax, ay, D == 3 ? az : T(0), T(0));   // f_visc + f_avisc + f_astress + f_body (adaptive dt)
     T rx = xi.x + dt * uti.x, ry = xi.y + dt * uti.y, rz = D == 3 ? xi.z + dt * uti.z : xi.z;
     if (P.per[0]) { if (rx >= P.hi[0]) rx -= P.L[0]; else if (rx < P.lo[0]) rx += P.L[0]; }
     if (P.per[1]) { if (ry >= P.hi[1]) ry -= P.L[1]; else if (ry < P.lo[1]) ry += P.L[1]; }
@@ -1159,34 +1169,42 @@ template <class T, int D>
 __global__ void __launch_bounds__(128) k_pgrad_correct(Params<T> P, T dt, const V4<T>* __restrict__ pos,
                                                        const T* __restrict__ rho, const T* __restrict__ p,
                                                        const V4<T>* __restrict__ us, const int* __restrict__ nbr,
-                                                       const int* __restrict__ cnt, int ncap, V4<T>* __restrict__ vel)
+                                                       const int* __restrict__ cnt, int ncap, V4<T>* __restrict__ vel,
+                                                       const V4<T>* __restrict__ fnp, Ctl* ctl)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= P.Nfo) return;
-    V4<T> xi = ld4(pos + i);
-    T rhoi = rho[i], pi = p[i];
-    T irhoi = frcp(rhoi);
-    T pir = pi * irhoi * irhoi;
-    T ax = 0, ay = 0, az = 0;
-    int n = cnt[i];
-    for_nbrs(nbr, ncap, i, n, [&](int j) {
-        V4<T> xj = ld4(pos + j);
-        T rhoj = __ldg(rho + j), pj = __ldg(p + j);
-        T d[3], r, ri;
-        r_of(pair_vec<T, D>(P, xi, xj, d), r, ri);
-        T gf = quintic4(r * P.inv_h) * ri;       // * dwk below
-        T irj = frcp(rhoj);
-        T f = P.pgrad == 0 ? xj.w * (pir + pj * irj * irj) : xj.w * irhoi * irj * (pj - pi);
-        f *= gf;
-        ax -= f * d[0];
-        ay -= f * d[1];
-        if (D == 3) az -= f * d[2];
-    });
-    ax *= P.dwk;
-    ay *= P.dwk;
-    az *= P.dwk;
-    V4<T> u = ld4(us + i);
-    vel[i] = mk4<T>(u.x + dt * ax, u.y + dt * ay, D == 3 ? u.z + dt * az : T(0), T(0));
+    double f2 = 0.0;
+    if (i < P.Nfo) {
+        V4<T> xi = ld4(pos + i);
+        T rhoi = rho[i], pi = p[i];
+        T irhoi = frcp(rhoi);
+        T pir = pi * irhoi * irhoi;
+        T ax = 0, ay = 0, az = 0;
+        int n = cnt[i];
+        for_nbrs(nbr, ncap, i, n, [&](int j) {
+            V4<T> xj = ld4(pos + j);
+            T rhoj = __ldg(rho + j), pj = __ldg(p + j);
+            T d[3], r, ri;
+            r_of(pair_vec<T, D>(P, xi, xj, d), r, ri);
+            T gf = quintic4(r * P.inv_h) * ri;       // * dwk below
+            T irj = frcp(rhoj);
+            T f = P.pgrad == 0 ? xj.w * (pir + pj * irj * irj) : xj.w * irhoi * irj * (pj - pi);
+            f *= gf;
+            ax -= f * d[0];
+            ay -= f * d[1];
+            if (D == 3) az -= f * d[2];
+        });
+        ax *= P.dwk;
+        ay *= P.dwk;
+        az *= P.dwk;
+        V4<T> u = ld4(us + i);
+        vel[i] = mk4<T>(u.x + dt * ax, u.y + dt * ay, D == 3 ? u.z + dt * az : T(0), T(0));
+        // f^n = f_p + f_visc + f_body + f_avisc + f_astress for the adaptive dt
+        const V4<T> a = ld4(fnp + i);
+        const double fx = (double)(a.x + ax), fy = (double)(a.y + ay), fz = D == 3 ? (double)(a.z + az) : 0.0;
+        f2 = fx * fx + fy * fy + fz * fz;
+    }
+    warp_max_to(f2, &ctl->fmax2_bits);
 }
 
 // ===========================================================================
@@ -1267,21 +1285,25 @@ __global__ void __launch_bounds__(128) k_gtvf_substep(Params<T> P, T dtau, const
 // ===========================================================================
 template <class T, int D>
 __global__ void k_advance(Params<T> P, T dt, const V4<T>* __restrict__ dK, const V4<T>* __restrict__ rn,
-                          const V4<T>* __restrict__ vel, V4<T>* __restrict__ pos, V4<T>* __restrict__ vt)
+                          const V4<T>* __restrict__ vel, V4<T>* __restrict__ pos, V4<T>* __restrict__ vt, Ctl* ctl)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= P.Nfo) return;
-    V4<T> x = ld4(rn + i), u = ld4(vel + i), ut = ld4(vt + i);
-    V4<T> dl = dK ? ld4(dK + i) : mk4<T>(T(0), T(0), T(0), T(0));   // r^K - r^0
-    T tx = u.x + dl.x / dt, ty = u.y + dl.y / dt;
-    T tz = D == 3 ? u.z + dl.z / dt : T(0);
-    T hd = T(0.5) * dt;
-    T X = x.x + hd * (tx + ut.x), Y = x.y + hd * (ty + ut.y), Z = D == 3 ? x.z + hd * (tz + ut.z) : x.z;
-    if (P.per[0]) { if (X >= P.hi[0]) X -= P.L[0]; else if (X < P.lo[0]) X += P.L[0]; }
-    if (P.per[1]) { if (Y >= P.hi[1]) Y -= P.L[1]; else if (Y < P.lo[1]) Y += P.L[1]; }
-    if (D == 3 && P.per[2]) { if (Z >= P.hi[2]) Z -= P.L[2]; else if (Z < P.lo[2]) Z += P.L[2]; }
-    pos[i] = mk4<T>(X, Y, Z, x.w);
-    vt[i] = mk4<T>(tx, ty, tz, T(0));
+    double v2 = 0.0;
+    if (i < P.Nfo) {
+        V4<T> x = ld4(rn + i), u = ld4(vel + i), ut = ld4(vt + i);
+        V4<T> dl = dK ? ld4(dK + i) : mk4<T>(T(0), T(0), T(0), T(0));   // r^K - r^0
+        T tx = u.x + dl.x / dt, ty = u.y + dl.y / dt;
+        T tz = D == 3 ? u.z + dl.z / dt : T(0);
+        T hd = T(0.5) * dt;
+        T X = x.x + hd * (tx + ut.x), Y = x.y + hd * (ty + ut.y), Z = D == 3 ? x.z + hd * (tz + ut.z) : x.z;
+        if (P.per[0]) { if (X >= P.hi[0]) X -= P.L[0]; else if (X < P.lo[0]) X += P.L[0]; }
+        if (P.per[1]) { if (Y >= P.hi[1]) Y -= P.L[1]; else if (Y < P.lo[1]) Y += P.L[1]; }
+        if (D == 3 && P.per[2]) { if (Z >= P.hi[2]) Z -= P.L[2]; else if (Z < P.lo[2]) Z += P.L[2]; }
+        pos[i] = mk4<T>(X, Y, Z, x.w);
+        vt[i] = mk4<T>(tx, ty, tz, T(0));
+        v2 = (double)u.x * u.x + (double)u.y * u.y + (D == 3 ? (double)u.z * u.z : 0.0);   // |u^{n+1}|^2
+    }
+    warp_max_to(v2, &ctl->vmax2_bits);
 }
 
 // ===========================================================================

@@ -163,3 +163,37 @@ def test_one_rank_periodic_self_halo(transport):
         a, b = sim.get(fld), single.get(fld)
         assert np.abs(a - b).max() <= 1e-10 * np.abs(b).max()
     sim.close()
+
+
+def test_adaptive_dt_over_slab_ranks():
+    """sisph_next_dt is collective: every rank returns the single GPU's value."""
+    case = synth.tgv2d()
+    single = gpu_sim(case)
+    single.step(case.dt)
+    ref = single.next_dt()
+    from paper_1908_01762_b200 import LocalGroup, Simulation, make_dist
+    R = 3
+    g = LocalGroup(R)
+    out, errs = [None] * R, [None] * R
+
+    def work(r):
+        try:
+            s = Simulation.from_case(case, dist=make_dist(R, r, 1, local_group=g))
+            s.step(case.dt)
+            out[r] = s.next_dt()
+            s.close()
+        except Exception as e:  # noqa: BLE001
+            errs[r] = e
+
+    th = [threading.Thread(target=work, args=(r,), daemon=True) for r in range(R)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=120)
+    for e in errs:
+        if e is not None:
+            raise e
+    for r in range(R):
+        for a, b in zip(out[r], ref):
+            assert a == pytest.approx(b, rel=1e-12)
+    g.close()

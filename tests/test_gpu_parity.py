@@ -295,3 +295,46 @@ def test_eisph_single_sweep():
     sim.predict(case.dt)
     it, _ = sim.ppe_solve(1e-2, 1)
     assert it == 1
+
+
+# ------------------------------------------------------------------ NEXT-1: adaptive dt
+@pytest.mark.parametrize("name", list(CASES))
+def test_adaptive_dt_parity(name):
+    """sisph_next_dt (device-reduced max|u|, max|f|) vs the oracle's P:675-694 rule."""
+    from paper_1908_01762_b200 import SisphError
+    case = CASES[name]
+    prec = _prec(case)
+    sim = gpu_sim(case)
+    o = oracle_from_gpu(case, sim)
+    with pytest.raises(SisphError):
+        sim.next_dt()
+    tol, mx = (case.params["tol"], case.params["max_iter"]) if prec == 64 else (0.0, 5)
+    sim.predict(case.dt)
+    o.predict(case.dt)
+    sim.ppe_solve(tol, mx)
+    o.solve(tol, mx)
+    sim.correct(case.dt)
+    o.correct(case.dt)
+    rel = 1e-9 if prec == 64 else 1e-4
+    for g, r in zip(sim.next_dt(), o.next_dt()):
+        if np.isinf(r):
+            assert np.isinf(g)
+        else:
+            assert g == pytest.approx(r, rel=rel)
+
+
+def test_adaptive_dt_free_fall_closed_form_gpu():
+    # f^n = g exactly and u^{n+1} = U0 + dt g for a uniformly translating periodic
+    # lattice under gravity (see the oracle pin): the device reductions must give
+    # 0.25 h / |U0 + dt g| and 0.25 sqrt(h / |g|)
+    case = synth.lattice_periodic(2, 16, dx=1.0 / 16, jitter=0.1)
+    case.params.update(p_ref=0.0, g=[0.0, -9.81, 0.0], nu=0.01, alpha=0.05, c_ref=10.0, pgrad=1)
+    U0 = np.array([0.3, 0.2])
+    case.u[:] = U0
+    sim = gpu_sim(case)
+    dt = 1e-3
+    sim.step(dt)
+    dtn, dtc, dtf = sim.next_dt()
+    assert dtc == pytest.approx(0.25 * case.h / np.linalg.norm(U0 + dt * np.array([0.0, -9.81])), rel=1e-12)
+    assert dtf == pytest.approx(0.25 * np.sqrt(case.h / 9.81), rel=1e-9)
+    assert dtn == min(dtc, dtf)
