@@ -1029,7 +1029,60 @@ template <class T, int D> struct Engine : EngineBase {
         }
         if (loose) SRET(bin_walls_skin());
         SRET(sort_fluid(loose ? PS : P));
-        return loose ? build_loose() : build_list();
+        return loose ? build_loose_grow() : build_list_grow();
+    }
+
+    // ---- list capacities grow instead of failing: after a build or filter
+    // the host reads the overflow flag (one small D2H); on overflow the list
+    // is reallocated at 1.25 x the largest row and the same pass is redone
+    // (the positions it reads have not changed).
+    int read_overflow(int& mc)
+    {
+        SCK(cudaMemcpyAsync(&hctl->max_count, &ctl->max_count, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+        SCK(cudaStreamSynchronize(st));
+        mc = hctl->max_count;
+        return SISPH_OK;
+    }
+    static int grown(int mc) { return ((int)ceil(1.25 * mc) + 8 + 7) / 8 * 8; }
+    int build_list_grow(bool inner = false)
+    {
+        SRET(build_list(inner));
+        int mc;
+        SRET(read_overflow(mc));
+        if (hctl->overflow) {
+            SRET(alloc_list(grown(mc)));
+            SRET(build_list(inner));
+        }
+        return SISPH_OK;
+    }
+    int build_loose_grow()
+    {
+        SRET(build_loose());
+        int mc;
+        SRET(read_overflow(mc));
+        if (hctl->overflow) {
+            const int want = grown(mc);
+            if (nbs) cudaFree(nbs);
+            nbs = nullptr;
+            int rc = 0;
+            nbs = dalloc<int>((size_t)want * rows32(capT), err, rc);
+            if (rc) return rc;
+            cap_s = PS.cap = want;
+            SRET(build_loose());
+        }
+        return SISPH_OK;
+    }
+    int filter_list_grow()
+    {
+        SRET(filter_list());
+        int mc;
+        SRET(read_overflow(mc));
+        if (hctl->overflow) {
+            SCK(cudaMemsetAsync(&ctl->overflow, 0, sizeof(int), st));
+            SRET(alloc_list(grown(mc)));
+            SRET(filter_list());
+        }
+        return SISPH_OK;
     }
 
     int copy_walls_to_alt()
@@ -1070,7 +1123,7 @@ template <class T, int D> struct Engine : EngineBase {
             SRET(fetch_ghosts());
             SRET(bin_walls_skin());
             SRET(sort_fluid(PS));
-            SRET(build_loose());
+            SRET(build_loose_grow());
         } else {
             SRET(plan_skin(dt, single));
             // A1-A5 at r^n (single build: the loose list on the skin grid)
@@ -1115,7 +1168,7 @@ template <class T, int D> struct Engine : EngineBase {
             // r^n is kept as rn; exact sets at r* filtered out of the loose list
             std::swap(pos, rstar);
             std::swap(rn, rstar);
-            SRET(filter_list());
+            SRET(filter_list_grow());
         } else {
             // A9: build at r*; carry r^n along as rn
             SRET(sort_set(P, rstar, Nf, Nf, fstart, perm));
@@ -1139,7 +1192,7 @@ template <class T, int D> struct Engine : EngineBase {
             std::swap(fs, fs_alt);
             std::swap(p, p_alt);
             std::swap(pid, pid_alt);
-            SRET(build_list(true));   // + GTVF inner list
+            SRET(build_list_grow(true));   // + GTVF inner list
         }
         // A10
         if (Nwo) ++nlaunch, k_wall_velocity<T, D><<<nblk(Nwo, 256), 256, 0, st>>>(P, pos, nbr, cnt, P.cap, nrm, rho, us, P.ustar_noslip ? 0 : 1);

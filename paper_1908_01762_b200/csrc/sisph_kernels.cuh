@@ -612,7 +612,10 @@ __global__ void __launch_bounds__(32 * BL_WARPS) k_build_loose(Params<T> P, int 
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mmax = max(mmax, __shfl_xor_sync(0xffffffffu, mmax, o));
-    if (lane == 0 && mmax > cap) atomicExch(&ctl->overflow, 1);
+    if (lane == 0) {
+        atomicMax(&ctl->max_count, mmax);
+        if (mmax > cap) atomicExch(&ctl->overflow, 1);
+    }
 }
 
 // ===========================================================================

@@ -338,3 +338,34 @@ def test_adaptive_dt_free_fall_closed_form_gpu():
     assert dtc == pytest.approx(0.25 * case.h / np.linalg.norm(U0 + dt * np.array([0.0, -9.81])), rel=1e-12)
     assert dtf == pytest.approx(0.25 * np.sqrt(case.h / 9.81), rel=1e-9)
     assert dtn == min(dtc, dtf)
+
+
+# ------------------------------------------------------------------ NEXT-2: method variants
+@pytest.mark.parametrize("name,over", [
+    ("tgv2d_f64", {"max_iter": 1, "min_iter": 1}),        # EISPH: one sweep, no minimum of two
+    ("hydro_f64", {"max_iter": 1, "min_iter": 1}),
+    ("hydro_f64", {"ustar_noslip": 1}),                   # no-slip wall u*
+    ("db2d_f64", {"pgrad": 1}),                           # asymm pressure gradient on a free surface
+    ("tgv2d_f64", {"pgrad": 0}),                          # symm on the TGV
+    ("db3d_f64", {"tol": 1e-3}),                          # a tighter tolerance (Table 1)
+])
+def test_variant_step_parity(name, over):
+    case = CASES[name]
+    sim = gpu_sim(case, **over)
+    o = oracle_from_gpu(case, sim, params=over)
+    f = case.tag == 0
+    tol = over.get("tol", case.params["tol"])
+    mx = over.get("max_iter", case.params["max_iter"])
+    for s in range(3):
+        resync(case, sim, o)
+        sim.predict(case.dt)
+        o.predict(case.dt)
+        it_g, _ = sim.ppe_solve(tol, mx)
+        it_o, res_o, _ = o.solve(tol, mx)
+        if abs(res_o - tol) > 1e-9 * tol:
+            assert it_g == it_o, (s, it_g, it_o)
+        sim.correct(case.dt)
+        o.correct(case.dt)
+        assert_close(f"p step {s}", sim.get("PRESSURE")[f], o.get("p")[f], 64)
+        assert_close(f"u step {s}", sim.get("VELOCITY")[f], o.get("u")[f], 64,
+                     scale=max(np.abs(o.get("u")[f]).max(), 1e-3))
