@@ -286,6 +286,48 @@ def dambreak3d(nfx: int = 256, nfy: int = 64, nfz: int = 128, dx: float = 1.0 / 
                 np.zeros((n, 3)), np.full(n, rho0 * dx ** 3), np.full(n, rho0), p, tag, params)
 
 
+# --------------------------------------------------------------------------
+# NEXT-3  square patch (§4.4, eq:sqp:vel, eq:sqp:p)
+# --------------------------------------------------------------------------
+def square_patch_pressure(x, y, L: float = 1.0, omega: float = 1.0, rho: float = 1.0, nterms: int = 80):
+    """Initial pressure of the rotating square patch, eq:sqp:p:
+        p0 = rho sum_{m, n odd} -32 omega^2 / (m n pi^2 [(n pi / L)^2 + (m pi / L)^2])
+                                 sin(m pi x* / L) sin(n pi y* / L),   x* = x + L/2, y* = y + L/2.
+    The printed (m pi^2 / L)^2 is read as (m pi / L)^2 (reading R30: the series must solve
+    lap p = 2 rho omega^2 with p = 0 on the patch boundary, which fixes the symmetric form).
+    nterms odd values of m and of n (the coefficients fall as 1/(m n (m^2 + n^2)))."""
+    k = 2 * np.arange(nterms) + 1.0                          # 1, 3, 5, ...
+    xs, ys = np.asarray(x) + L / 2, np.asarray(y) + L / 2
+    Sx = np.sin(np.pi * np.outer(xs, k) / L)                # (N, M)
+    Sy = np.sin(np.pi * np.outer(ys, k) / L)
+    C = -32.0 * omega ** 2 / (np.outer(k, k) * np.pi ** 2 * ((np.pi / L) ** 2 * (k[None, :] ** 2 + k[:, None] ** 2)))
+    return rho * np.einsum("im,mn,in->i", Sx, C, Sy)
+
+
+def square_patch(n: int = 100, L: float = 1.0, omega: float = 1.0, h_ratio: float = 1.3, alpha: float = 0.15,
+                 steps: int = 100, tol: float = 1e-2, K: int = 10, precision: int = 64,
+                 box: float = 4.0) -> Case:
+    """An L x L patch of fluid centred at the origin rotating rigidly (eq:sqp:vel:
+    u0 = omega y, v0 = -omega x) with the balancing pressure eq:sqp:p; no walls, free
+    surface everywhere (100 x 100, h/dx = 1.3, alpha = 0.15,
+    epsilon = 1e-2, asymm pressure gradient)."""
+    rho0 = 1.0
+    dx = L / n
+    h = h_ratio * dx
+    x = _lattice((n, n), dx, (-L / 2, -L / 2))
+    u = np.stack([omega * x[:, 1], -omega * x[:, 0]], axis=1)
+    p = square_patch_pressure(x[:, 0], x[:, 1], L, omega, rho0)
+    umax = omega * L / math.sqrt(2.0)
+    c_ref = 10.0 * umax                      # c = 10 |u|max (PAPER.md:393-394)
+    dt = 0.25 * h / umax                     # CFL (PAPER.md:655-659)
+    params = default_params(rho0=rho0, alpha=alpha, c_ref=c_ref, pgrad=PGRAD_ASYMM, h_tilde_factor=0.5,
+                            pref_external=1, p_ref=rho0 * c_ref * c_ref, tol=tol, K=K, precision=precision)
+    lo, hi = [-box * L / 2, -box * L / 2], [box * L / 2, box * L / 2]
+    npart = x.shape[0]
+    return Case("square_patch", 2, h, dx, dt, steps, _pad3(lo), _pad3(hi), [0, 0, 0], x, u,
+                np.full(npart, rho0 * dx * dx), np.full(npart, rho0), p, np.zeros(npart, np.int32), params)
+
+
 def lattice_periodic(dim: int, n: int, dx: float = 1.0, h_ratio: float = 1.0,
                      jitter: float = 0.0, seed: int = 7, rho0: float = 1.0) -> Case:
     """A resting periodic lattice (used for lattice identities and invariants)."""
