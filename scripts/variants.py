@@ -122,6 +122,27 @@ def main():
         print(f"| hydrostatic, {steps} steps | {label} | {np.mean(its):.2f} | mean abs(p - rho g (H - y)) / rho g H = {dev:.4f} |")
         sim.close()
     out["forms"] = forms
+    # ---------------------------------------------------------------- 4. square patch (NEXT-3)
+    print("\n## 4. Square patch (NEXT-3, P:1301-1350): 100 x 100, h/dx 1.3, alpha 0.15, eps 1e-2, t = 3 s\n")
+    print("| pgrad | steps | mean sweeps | angular momentum L(t)/L(0) | centre of mass | extent x | extent y |")
+    print("|---|---|---|---|---|---|---|")
+    sq = []
+    for pg, label in ((1, "asymm"), (0, "symm")):
+        case = synth.square_patch(precision=32)
+        steps = int(round((0.5 if q else 3.0) / case.dt))
+        sim = Simulation.from_case(case, pgrad=pg)
+        m = case.m
+        L0 = float(np.sum(m * (case.x[:, 0] * case.u[:, 1] - case.x[:, 1] * case.u[:, 0])))
+        its = [sim.step(case.dt).iters for _ in range(steps)]
+        x, u = sim.get("POSITION"), sim.get("VELOCITY")
+        Lt = float(np.sum(m * (x[:, 0] * u[:, 1] - x[:, 1] * u[:, 0])))
+        com = (m[:, None] * x).sum(0) / m.sum()
+        sq.append({"pgrad": label, "steps": steps, "mean": float(np.mean(its)), "L_ratio": Lt / L0,
+                   "com": com.tolist(), "extent": [float(np.ptp(x[:, 0])), float(np.ptp(x[:, 1]))]})
+        print(f"| {label} | {steps} | {np.mean(its):.2f} | {Lt / L0:.4f} | ({com[0]:.1e}, {com[1]:.1e}) | "
+              f"{np.ptp(x[:, 0]):.3f} | {np.ptp(x[:, 1]):.3f} |")
+        sim.close()
+    out["square_patch"] = sq
     with open(os.path.join(ROOT, "gpurun_out", "variants.json") if os.path.isdir(os.path.join(ROOT, "gpurun_out"))
               else "/tmp/variants.json", "w") as fh:
         json.dump(out, fh, indent=1)

@@ -369,3 +369,29 @@ def test_variant_step_parity(name, over):
         assert_close(f"p step {s}", sim.get("PRESSURE")[f], o.get("p")[f], 64)
         assert_close(f"u step {s}", sim.get("VELOCITY")[f], o.get("u")[f], 64,
                      scale=max(np.abs(o.get("u")[f]).max(), 1e-3))
+
+
+# ------------------------------------------------------------------ NEXT-3: square patch
+@pytest.mark.parametrize("prec", [64, 32])
+def test_square_patch_parity(prec):
+    """Free surface everywhere, no walls: full steps vs the oracle."""
+    case = synth.square_patch(n=30, precision=prec)
+    sim = gpu_sim(case)
+    o = oracle_from_gpu(case, sim)
+    over = {} if prec == 64 else {"tol": 0.0, "max_iter": 5}
+    tol = over.get("tol", case.params["tol"])
+    mx = over.get("max_iter", case.params["max_iter"])
+    for s in range(3):
+        resync(case, sim, o)
+        sim.predict(case.dt)
+        o.predict(case.dt)
+        haz = np.abs(o.get("rho") / case.params["rho0"] - case.params["fs_ratio"]) < 1e-6
+        assert np.array_equal(sim.get("FREE_SURFACE")[~haz], o.get("fs")[~haz])
+        it_g, _ = sim.ppe_solve(tol, mx)
+        it_o, res_o, _ = o.solve(tol, mx)
+        if prec == 64 and abs(res_o - tol) > 1e-9 * tol:
+            assert it_g == it_o
+        sim.correct(case.dt)
+        o.correct(case.dt)
+        assert_close(f"p {s}", sim.get("PRESSURE"), o.get("p"), prec)
+        assert_close(f"u {s}", sim.get("VELOCITY"), o.get("u"), prec, scale=max(np.abs(o.get("u")).max(), 1e-3))
