@@ -29,11 +29,20 @@ struct Ctl {
     unsigned long long vmax2_bits;   // max |u^{n+1}|^2 of the last correct
 };
 
-// warp max of a non-negative double, one atomic per warp (all 32 lanes present)
+// block max of a non-negative double, one atomic per block (every thread of
+// the block calls it; blockDim.x a multiple of 32, at most 1024)
 __device__ __forceinline__ void warp_max_to(double v, unsigned long long* dst)
 {
+    __shared__ double sm_max[32];
     v = warp_max(v);
-    if ((threadIdx.x & 31) == 0 && v > 0.0) atomicMax(dst, (unsigned long long)__double_as_longlong(v));
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) sm_max[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        v = lane < (int)(blockDim.x >> 5) ? sm_max[lane] : 0.0;
+        v = warp_max(v);
+        if (lane == 0 && v > 0.0) atomicMax(dst, (unsigned long long)__double_as_longlong(v));
+    }
 }
 
 // ===========================================================================
