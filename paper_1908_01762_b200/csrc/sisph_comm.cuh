@@ -136,7 +136,7 @@ struct NcclTransport : Transport {
     }
     int allreduce(double* buf, int count, int op, cudaStream_t st) override
     {
-        if (nranks == 1) return 0;
+        // also with one rank (the slab path forced on one GPU): the same NCCL call runs
         return check(api->AllReduce(buf, buf, (size_t)count, ncclDouble, op == 0 ? ncclSum : ncclMax, comm, st),
                      "ncclAllReduce");
     }

@@ -249,6 +249,9 @@ __global__ void k_gather(GatherList G, const int* __restrict__ perm, int n)
 // 16-byte chunk is written by one lane and every 512-byte block by one warp
 // (the L2 merges them before write-back: no partial-sector traffic).
 // ===========================================================================
+// List (and stored-coefficient) loads use the streaming cache policy
+// (__ldcs: evict-first in L1 and L2): each list is read once per pass and is
+// far larger than L2, so it must not evict the gathered per-particle arrays.
 __device__ __forceinline__ size_t nb_base(int i, int cap)
 {
     return (size_t)(i >> 5) * ((size_t)cap << 5) + (size_t)((i & 31) << 2);
@@ -262,7 +265,7 @@ __device__ __forceinline__ void for_nbrs(const int* __restrict__ nbr, int cap, i
 {
     const int4* __restrict__ q = reinterpret_cast<const int4*>(nbr + nb_base(i, cap));
     for (int c = 0; c < n; c += 4) {
-        const int4 v = __ldg(q + (size_t)(c >> 2) * 32);
+        const int4 v = __ldcs(q + (size_t)(c >> 2) * 32);
         f(v.x);
         if (c + 1 < n) f(v.y);
         if (c + 2 < n) f(v.z);
@@ -276,7 +279,7 @@ __device__ __forceinline__ void for_nbrs_k(const int* __restrict__ nbr, int cap,
 {
     const int4* __restrict__ q = reinterpret_cast<const int4*>(nbr + nb_base(i, cap));
     for (int c = 0; c < n; c += 4) {
-        const int4 v = __ldg(q + (size_t)(c >> 2) * 32);
+        const int4 v = __ldcs(q + (size_t)(c >> 2) * 32);
         f(v.x, c);
         if (c + 1 < n) f(v.y, c + 1);
         if (c + 2 < n) f(v.z, c + 2);
@@ -287,7 +290,7 @@ __device__ __forceinline__ size_t nb_off(int k) { return ((size_t)(k >> 2) << 7)
 // one 4-entry chunk of a per-pair array in the same layout (16 / 32 bytes)
 __device__ __forceinline__ void ld_chunk4(const float* p, float (&f)[4])
 {
-    const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+    const float4 v = __ldcs(reinterpret_cast<const float4*>(p));
     f[0] = v.x;
     f[1] = v.y;
     f[2] = v.z;
@@ -295,7 +298,7 @@ __device__ __forceinline__ void ld_chunk4(const float* p, float (&f)[4])
 }
 __device__ __forceinline__ void ld_chunk4(const double* p, double (&f)[4])
 {
-    const double2 a = __ldg(reinterpret_cast<const double2*>(p)), b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+    const double2 a = __ldcs(reinterpret_cast<const double2*>(p)), b = __ldcs(reinterpret_cast<const double2*>(p) + 1);
     f[0] = a.x;
     f[1] = a.y;
     f[2] = b.x;
@@ -305,21 +308,21 @@ __device__ __forceinline__ void ld_chunk4(const double* p, double (&f)[4])
 // a builder lane's append cursor into its row
 struct NbCursor {
     int* row;   // nbr + nb_base(i, cap)
-    int off;    // offset of entry k
     int k;      // entries so far (may exceed cap: overflow is counted, not stored)
     __device__ __forceinline__ void init(int* nbr, int cap, int i)
     {
         row = nbr + nb_base(i, cap);
-        off = 0;
         k = 0;
     }
     __device__ __forceinline__ void push(bool acc, int j, int cap)
     {
-        // predicated store, no branch: the candidate loop stays straight-line
+        // entry k sits at (k / 4) 128 + k % 4 = 32 (k & ~3) + (k & 3) ints from the row base;
+        // predicated store (no branch: the candidate loop stays straight-line)
+        const unsigned off = ((unsigned)(k & ~3) << 5) | (unsigned)(k & 3);
         const int pr = (acc && k < cap) ? 1 : 0;
-        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.b32 [%0], %1;\n\t}"
-                     :: "l"(row + off), "r"(j), "r"(pr) : "memory");
-        off += acc ? nb_adv(k) : 0;
+        asm volatile("{\n\t.reg .pred q;\n\t.reg .b64 a;\n\tsetp.ne.b32 q, %3, 0;\n\t"
+                     "mad.wide.u32 a, %1, 4, %0;\n\t@q st.global.b32 [a], %2;\n\t}"
+                     :: "l"(row), "r"(off), "r"(j), "r"(pr) : "memory");
         k += acc ? 1 : 0;
     }
 };
@@ -677,11 +680,11 @@ __global__ void __launch_bounds__(128) k_filter(Params<T> P, int row0, int nrows
         crow = coef ? coef + nb_base(i, cap) : nullptr;
     }
     const int4* __restrict__ src = reinterpret_cast<const int4*>(nbs + nb_base(i, cap_s));
-    int4 vnext = n > 0 ? __ldg(src) : make_int4(i, i, i, i);
+    int4 vnext = n > 0 ? __ldcs(src) : make_int4(i, i, i, i);
     for (int c = 0; c < nmax; c += 4) {
         const int4 v = vnext;
         // prefetch the next chunk of indices while this one is tested
-        vnext = c + 4 < n ? __ldg(src + (size_t)((c + 4) >> 2) * 32) : make_int4(i, i, i, i);
+        vnext = c + 4 < n ? __ldcs(src + (size_t)((c + 4) >> 2) * 32) : make_int4(i, i, i, i);
         V4<T> xj4[4];
         int j4[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
@@ -1061,7 +1064,7 @@ __global__ void __launch_bounds__(SWEEP_T) k_sweep(Params<T> P, const V4<T>* __r
                 const int4* __restrict__ qi = reinterpret_cast<const int4*>(nbr + b);
                 for (int c = 0; c < n; c += 4) {
                     const size_t o = (size_t)(c >> 2) * 32;
-                    const int4 v = __ldg(qi + o);
+                    const int4 v = __ldcs(qi + o);
                     T f[4];
                     ld_chunk4(coef + b + (o << 2), f);
                     s += f[0] * pin[v.x];
