@@ -118,6 +118,7 @@ template <class T, int D> struct Engine : EngineBase {
     V *rkA = nullptr, *rkB = nullptr, *vk = nullptr, *dk = nullptr;
     V* fnp = nullptr;       // non-pressure acceleration of A8 (adaptive dt)
     bool stepped = false;   // a correct has completed: next_dt is defined
+    bool pre_swept = false; // A11 ran the first Jacobi sweep (p^1 in p_alt, sums deferred)
     T *p = nullptr, *p_alt = nullptr, *rho = nullptr, *rho_alt = nullptr, *rhs = nullptr, *diag = nullptr;
     uint8_t *fs = nullptr, *fs_alt = nullptr;
     int *pid = nullptr, *pid_alt = nullptr;
@@ -358,7 +359,7 @@ template <class T, int D> struct Engine : EngineBase {
         AL(ccount, int, NCT) AL(fstart, int, NCT) AL(wstart, int, NCT)
         AL(bsum, int, (size_t)nblk(NCT, SCAN_B) + 1) AL(cnt, int, NT) AL(ctl, Ctl, 1) AL(cnt_in, int, NF)
         AL(cnt_s, int, NT) AL(wperm_s, int, NW) AL(wstart_s, int, NCT)
-        AL(partials, double, 2 * (size_t)nblk(NF, SWEEP_T) + 2) AL(dtmp, double, 3 * (size_t)n)
+        AL(partials, double, 2 * (size_t)nblk(NF, RHS_T) + 2) AL(dtmp, double, 3 * (size_t)n)
         if (dist()) {
             AL(dflag, int, NT) AL(dflag2, int, NT) AL(dpre, int, NT + 1) AL(dlist[0], int, NF) AL(dlist[1], int, NF)
             AL(dlist[2], int, NF) AL(fsend[0], int, NF) AL(fsend[1], int, NF) AL(fsend_pre[0], int, NF)
@@ -1202,10 +1203,20 @@ template <class T, int D> struct Engine : EngineBase {
             pl_add(W, us + Nf, sizeof(V));
             SRET(halo_walls(W));
         }
-        // A11
+        // A11 with the first PPE sweep fused (walls first get p^0, R14)
         SCK(cudaMemsetAsync(&ctl->lambda_bits, 0, sizeof(unsigned long long), st));
-        if (Nfo) ++nlaunch, k_rhs_diag<T, D><<<nblk(Nfo, 128), 128, 0, st>>>(P, (T)(1.0 / dt), pos, us, rho, fs, nbr, cnt, P.cap, rhs, diag, coef, ctl);
+        SCK(cudaMemsetAsync(ctl, 0, 4 * sizeof(int), st));  // ticket, iter, done, nonfinite
+        if (Nwo) ++nlaunch, k_wall_pressure<T, D><<<nblk(Nwo, 256), 256, 0, st>>>(P, pos, rho, nbr, cnt, P.cap, p, p_alt, nullptr);
         SCK(cudaGetLastError());
+        if (dist()) {
+            PackList W{};
+            pl_add(W, p + Nf, sizeof(T));
+            SRET(halo_walls(W));
+        }
+        ++nlaunch, k_rhs_diag<T, D><<<std::max(nblk(Nfo, RHS_T), 1), RHS_T, 0, st>>>(
+                       P, (T)(1.0 / dt), pos, us, rho, fs, nbr, cnt, P.cap, rhs, diag, coef, ctl, p, p_alt, partials);
+        SCK(cudaGetLastError());
+        pre_swept = true;
         // Lambda is global (eq:convergence): the bits of a non-negative double order as the value
         if (dist()) SRET(xallreduce(reinterpret_cast<double*>(&ctl->lambda_bits), 1, 1));
         phase = PREDICTED;
@@ -1265,20 +1276,34 @@ template <class T, int D> struct Engine : EngineBase {
             return SISPH_EINVAL;
         }
         int mi = std::min(min_iter, mx);
-        SCK(cudaMemsetAsync(ctl, 0, 4 * sizeof(int), st));  // ticket, iter, done, nonfinite
         int launched = 0;
         nrec = 0;
+        const bool pre = pre_swept;
+        pre_swept = false;
+        if (pre) {
+            // sweep 1 ran inside A11 as a deferred sweep: decide it now with this
+            // solve's tolerance and bounds (slab ranks: sums allreduced first)
+            if (dist()) SRET(xallreduce(ctl->red, 3, 0));
+            ++nlaunch, k_decide<<<1, 1, 0, st>>>(ctl, tl, mi, mx);
+            SCK(cudaGetLastError());
+            if (dist()) SRET(halo_p(false));
+            launched = 1;
+        } else {
+            SCK(cudaMemsetAsync(ctl, 0, 4 * sizeof(int), st));  // ticket, iter, done, nonfinite
+        }
         if (Nf > 0 || dist()) {
             // speculative batches: sweeps after convergence are no-ops on the device
             // (slab ranks take the same decisions, so they run the same batches)
-            int batch = std::min(mx, std::max(mi, 2) + 1);
+            int batch = std::min(mx - launched, std::max(mi, 2) + 1 - launched);
             for (;;) {
-                SRET(launch_sweeps(batch, tl, mi, mx));
-                launched += batch;
+                if (batch > 0) {
+                    SRET(launch_sweeps(batch, tl, mi, mx));
+                    launched += batch;
+                }
                 SCK(cudaMemcpyAsync(hctl, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
                 SCK(cudaStreamSynchronize(st));
                 if (hctl->done || launched >= mx) break;
-                batch = std::min(mx - launched, std::min(2 * batch, 32));
+                batch = std::min(mx - launched, std::min(2 * std::max(batch, 1), 32));
             }
         } else {
             hctl->iter = 0;
@@ -1292,7 +1317,7 @@ template <class T, int D> struct Engine : EngineBase {
         if (Nw && k > 0)
             SCK(cudaMemcpyAsync(p + Nf, p_alt + Nf, Nw * sizeof(T), cudaMemcpyDeviceToDevice, st));
         last_ms_sweeps = 0;
-        last_sweeps_timed = std::min(k, nrec);
+        last_sweeps_timed = std::min(k - (pre ? 1 : 0), nrec);   // the fused first sweep is not timed apart
         for (int q = 0; q < last_sweeps_timed; q++) {
             float ms = 0;
             SCK(cudaEventElapsedTime(&ms, sev[2 * q], sev[2 * q + 1]));
@@ -1530,6 +1555,7 @@ template <class T, int D> struct Engine : EngineBase {
             err = "set_field: unknown or read-only field, or count != n * components";
             return SISPH_EINVAL;
         }
+        pre_swept = false;   // the sweep fused into A11 used the old state: the solve redoes it
         SCK(cudaMemcpyAsync(dtmp, in, (size_t)count * sizeof(double), cudaMemcpyDefault, st));
         const int B = 256;
         auto vec = [&](V* dst, int base, int cntx, int keep_w) {

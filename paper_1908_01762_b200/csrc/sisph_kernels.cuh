@@ -934,19 +934,30 @@ __global__ void __launch_bounds__(128) k_forces_predict(Params<T> P, T dt, const
 // device-wide Lambda = max |RHS_i / D_ii| over non-free-surface fluid with
 // D_ii != 0 (eq:convergence, R12).
 // ===========================================================================
+//
+// pin != nullptr: the FIRST Jacobi sweep (eq:p-sor from p^0 = pin, walls
+// already refreshed from p^0, R14) is fused in: p^0_j is gathered with each
+// pair, so sum_j fac_ij p^0_j needs no second pass over the list; p^1 goes
+// to pout and the residual sums of eq:convergence are reduced as a deferred
+// sweep (k_decide takes the decision in the solve, once Lambda is complete).
+constexpr int RHS_T = 128;
+
 template <class T, int D>
-__global__ void __launch_bounds__(128) k_rhs_diag(Params<T> P, T inv_dt, const V4<T>* __restrict__ pos,
-                                                  const V4<T>* __restrict__ us, const T* __restrict__ rho,
-                                                  const uint8_t* __restrict__ fs, const int* __restrict__ nbr,
-                                                  const int* __restrict__ cnt, int ncap, T* __restrict__ rhs,
-                                                  T* __restrict__ diag, T* __restrict__ coef, Ctl* ctl)
+__global__ void __launch_bounds__(RHS_T) k_rhs_diag(Params<T> P, T inv_dt, const V4<T>* __restrict__ pos,
+                                                    const V4<T>* __restrict__ us, const T* __restrict__ rho,
+                                                    const uint8_t* __restrict__ fs, const int* __restrict__ nbr,
+                                                    const int* __restrict__ cnt, int ncap, T* __restrict__ rhs,
+                                                    T* __restrict__ diag, T* __restrict__ coef, Ctl* ctl,
+                                                    const T* __restrict__ pin, T* __restrict__ pout,
+                                                    double* __restrict__ partials)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
-    double lam = 0.0;
+    double lam = 0.0, dn = 0.0, dd = 0.0;
+    bool bad = false;
     if (i < P.Nfo) {
         V4<T> xi = ld4(pos + i), ui = ld4(us + i);
         T rhoi = rho[i];
-        T sr = 0, sd = 0;
+        T sr = 0, sd = 0, sp = 0;
         int n = cnt[i];
         T* __restrict__ crow = coef ? coef + nb_base(i, ncap) : nullptr;
         for_nbrs_k(nbr, ncap, i, n, [&](int j, int k) {
@@ -965,16 +976,84 @@ __global__ void __launch_bounds__(128) k_rhs_diag(Params<T> P, T inv_dt, const V
             // stored per-pair part of fac_ij (particles do not move during the solve):
             // the sweep then reads it instead of recomputing it (same value, same layout as nbr)
             if (crow) crow[nb_off(k)] = f;
+            if (pin) sp += f * pin[j];                   // first sweep: sum_j fac_ij p^0_j
         });
         sr *= -P.dwk * inv_dt;
-        sd *= T(4) * P.dwk * frcp(rhoi);
+        const T scale = T(4) * P.dwk * frcp(rhoi);
+        sd *= scale;
         rhs[i] = sr;
         diag[i] = sd;
-        if (!fs[i] && sd != T(0)) lam = (double)fabs(sr / sd);
+        const bool live = !fs[i] && sd != T(0);
+        if (live) lam = (double)fabs(sr / sd);
+        if (pin) {
+            // eq:p-sor with p^k = p^0, exactly as k_sweep (same expression order)
+            const T pold = pin[i];
+            T pnew = T(0);
+            if (live) {
+                sp *= scale;
+                pnew = P.omega * (sr + sp) * frcp(sd) + (T(1) - P.omega) * pold;
+            }
+            pout[i] = pnew;
+            dn = fabs((double)pnew - (double)pold);
+            dd = fabs((double)pnew);
+            bad = !isfinite((double)pnew);
+        }
     }
     lam = warp_max(lam);
     if ((threadIdx.x & 31) == 0 && lam > 0.0)
         atomicMax(&ctl->lambda_bits, (unsigned long long)__double_as_longlong(lam));
+    if (!pin) return;
+    // deferred sweep reduction (fixed order): block partials, the last block sums them
+    __shared__ double sn[RHS_T / 32], sdd[RHS_T / 32];
+    __shared__ int last;
+    dn = warp_sum(dn);
+    dd = warp_sum(dd);
+    const int anybad = __any_sync(0xffffffffu, bad);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) {
+        sn[w] = dn;
+        sdd[w] = dd;
+        if (anybad) atomicExch(&ctl->nonfinite, 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0, b = 0;
+        for (int q = 0; q < RHS_T / 32; q++) {
+            a += sn[q];
+            b += sdd[q];
+        }
+        partials[2 * blockIdx.x] = a;
+        partials[2 * blockIdx.x + 1] = b;
+        __threadfence();
+        const unsigned t = atomicAdd(&ctl->ticket, 1u);
+        last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double a = 0, b = 0;
+    for (int q = threadIdx.x; q < (int)gridDim.x; q += blockDim.x) {
+        a += ((volatile double*)partials)[2 * q];
+        b += ((volatile double*)partials)[2 * q + 1];
+    }
+    a = warp_sum(a);
+    b = warp_sum(b);
+    if (lane == 0) {
+        sn[w] = a;
+        sdd[w] = b;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double num = 0, den = 0;
+        for (int q = 0; q < RHS_T / 32; q++) {
+            num += sn[q];
+            den += sdd[q];
+        }
+        ctl->red[0] = num;
+        ctl->red[1] = den;
+        ctl->red[2] = ctl->nonfinite ? 1.0 : 0.0;
+        ctl->ticket = 0;
+    }
 }
 
 // ===========================================================================
