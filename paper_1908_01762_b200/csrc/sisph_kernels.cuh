@@ -863,6 +863,65 @@ __global__ void __launch_bounds__(256) k_wall_velocity(Params<T> P, const V4<T>*
 //   u* = u + dt (f_visc + f_avisc + f_astress + g)   (eq:int:vint)
 //   r* = r + dt u~                                    (eq:int:rnp1)
 // ===========================================================================
+// per-pair part of A8 (shared by the list pass and the staged cell pass):
+// d = r_i - r_j (already minimum-image / shifted), r2 = |d|^2
+template <class T, int D>
+__device__ __forceinline__ void forces_pair(const Params<T>& P, const V4<T>& ui, T rhoi, T irhoi, T dux, T duy, T duz,
+                                            const V4<T>& xj, const V4<T>& uj, const V4<T>& utj, bool fluid_j,
+                                            const T (&d)[3], T r2, T& ax, T& ay, T& az)
+{
+    const T nu4 = T(4) * P.nu;
+    const T avf2 = T(2) * P.alpha * P.h * P.c_ref;   // Pi = -avf phi / rhobar, rhobar = (rho_i + rho_j) / 2
+    T rhoj = uj.w;                                   // k_density / k_wall_velocity put rho_j there
+    T r, ri;
+    r_of(r2, r, ri);
+    T dwdr = P.dwk * quintic4(r * P.inv_h);
+    T gf = dwdr * ri;                                // grad_i W_ij = gf * r_ij
+    T mj = xj.w;
+    T uijx = ui.x - uj.x, uijy = ui.y - uj.y, uijz = D == 3 ? ui.z - uj.z : T(0);
+    T iden = frcp((rhoi + rhoj) * (r2 + P.eta_h2));  // shared by f_visc and f_avisc
+    if (P.nu > T(0)) {
+        T f = mj * nu4 * (r * dwdr) * iden;          // eq:mom:sph:visc
+        ax += f * uijx;
+        ay += f * uijy;
+        if (D == 3) az += f * uijz;
+    }
+    if (P.alpha > T(0)) {
+        T vr = uijx * d[0] + uijy * d[1];
+        if (D == 3) vr += uijz * d[2];
+        if (vr < T(0)) {                             // eq:mom:sph:av:params (R20)
+            T Pi = -avf2 * vr * iden;
+            T f = mj * Pi * gf;
+            ax -= f * d[0];
+            ay -= f * d[1];
+            if (D == 3) az -= f * d[2];
+        }
+    }
+    if (fluid_j) {                                   // eq:mom:sph:gtvf:stress (R21)
+        T gx = gf * d[0], gy = gf * d[1], gz = D == 3 ? gf * d[2] : T(0);
+        T ai = (dux * gx + duy * gy + (D == 3 ? duz * gz : T(0))) * irhoi;
+        T aj = ((utj.x - uj.x) * gx + (utj.y - uj.y) * gy + (D == 3 ? (utj.z - uj.z) * gz : T(0))) * frcp(rhoj);
+        ax += mj * (ui.x * ai + uj.x * aj);
+        ay += mj * (ui.y * ai + uj.y * aj);
+        if (D == 3) az += mj * (ui.z * ai + uj.z * aj);
+    }
+}
+
+// per-particle part of A8: u* = u + dt a (eq:int:vint), r* = r + dt u~ (eq:int:rnp1)
+template <class T, int D>
+__device__ __forceinline__ void forces_finish(const Params<T>& P, int i, T dt, const V4<T>& xi, const V4<T>& ui,
+                                              const V4<T>& uti, T rhoi, T ax, T ay, T az, V4<T>* __restrict__ us,
+                                              V4<T>* __restrict__ rstar, V4<T>* __restrict__ fnp)
+{
+    us[i] = mk4<T>(ui.x + dt * ax, ui.y + dt * ay, D == 3 ? ui.z + dt * az : T(0), rhoi);   // rho_i in lane 4
+    fnp[i] = mk4<T>(ax, ay, D == 3 ? az : T(0), T(0));   // f_visc + f_avisc + f_astress + f_body (adaptive dt)
+    T rx = xi.x + dt * uti.x, ry = xi.y + dt * uti.y, rz = D == 3 ? xi.z + dt * uti.z : xi.z;
+    if (P.per[0]) { if (rx >= P.hi[0]) rx -= P.L[0]; else if (rx < P.lo[0]) rx += P.L[0]; }
+    if (P.per[1]) { if (ry >= P.hi[1]) ry -= P.L[1]; else if (ry < P.lo[1]) ry += P.L[1]; }
+    if (D == 3 && P.per[2]) { if (rz >= P.hi[2]) rz -= P.L[2]; else if (rz < P.lo[2]) rz += P.L[2]; }
+    rstar[i] = mk4<T>(rx, ry, rz, xi.w);
+}
+
 template <class T, int D>
 __global__ void __launch_bounds__(128) k_forces_predict(Params<T> P, T dt, const V4<T>* __restrict__ pos,
                                                         const V4<T>* __restrict__ vel, const V4<T>* __restrict__ vt,
@@ -876,58 +935,20 @@ __global__ void __launch_bounds__(128) k_forces_predict(Params<T> P, T dt, const
     T rhoi = rho[i];
     T ax = P.g[0], ay = P.g[1], az = D == 3 ? P.g[2] : T(0);
     T dux = uti.x - ui.x, duy = uti.y - ui.y, duz = D == 3 ? uti.z - ui.z : T(0);
-    const T nu4 = T(4) * P.nu;
-    const T avf2 = T(2) * P.alpha * P.h * P.c_ref;   // Pi = -avf phi / rhobar, rhobar = (rho_i + rho_j) / 2
     const T irhoi = frcp(rhoi);
     int n = cnt[i];
     for_nbrs(nbr, ncap, i, n, [&](int j) {
-        // (loose-list pairs beyond 3h contribute exactly 0: dW/dr = 0 for q >= 3; skipping
-        // them per lane measured slower -- divergence -- than computing the zeros)
+        // (loose-list pairs beyond 3h contribute exactly 0: dW/dr = 0 for q >= 3)
         V4<T> xj = ld4(pos + j), uj = ld4(vel + j);
-        T rhoj = uj.w;                               // k_density / k_wall_velocity put rho_j there
-        T d[3], r, ri;
+        const bool fl = j < P.Nf;
+        V4<T> utj = fl ? ld4(vt + j) : uj;
+        T d[3];
         T r2 = pair_vec<T, D>(P, xi, xj, d);
-        r_of(r2, r, ri);
-        T dwdr = P.dwk * quintic4(r * P.inv_h);
-        T gf = dwdr * ri;                            // grad_i W_ij = gf * r_ij
-        T mj = xj.w;
-        T uijx = ui.x - uj.x, uijy = ui.y - uj.y, uijz = D == 3 ? ui.z - uj.z : T(0);
-        T iden = frcp((rhoi + rhoj) * (r2 + P.eta_h2));  // shared by f_visc and f_avisc
-        if (P.nu > T(0)) {
-            T f = mj * nu4 * (r * dwdr) * iden;          // eq:mom:sph:visc
-            ax += f * uijx;
-            ay += f * uijy;
-            if (D == 3) az += f * uijz;
-        }
-        if (P.alpha > T(0)) {
-            T vr = uijx * d[0] + uijy * d[1];
-            if (D == 3) vr += uijz * d[2];
-            if (vr < T(0)) {                             // eq:mom:sph:av:params (R20)
-                T Pi = -avf2 * vr * iden;
-                T f = mj * Pi * gf;
-                ax -= f * d[0];
-                ay -= f * d[1];
-                if (D == 3) az -= f * d[2];
-            }
-        }
-        if (j < P.Nf) {                                  // eq:mom:sph:gtvf:stress (R21)
-            V4<T> utj = ld4(vt + j);
-            T gx = gf * d[0], gy = gf * d[1], gz = D == 3 ? gf * d[2] : T(0);
-            T ai = (dux * gx + duy * gy + (D == 3 ? duz * gz : T(0))) * irhoi;
-            T aj = ((utj.x - uj.x) * gx + (utj.y - uj.y) * gy + (D == 3 ? (utj.z - uj.z) * gz : T(0))) * frcp(rhoj);
-            ax += mj * (ui.x * ai + uj.x * aj);
-            ay += mj * (ui.y * ai + uj.y * aj);
-            if (D == 3) az += mj * (ui.z * ai + uj.z * aj);
-        }
+        forces_pair<T, D>(P, ui, rhoi, irhoi, dux, duy, duz, xj, uj, utj, fl, d, r2, ax, ay, az);
     });
-    us[i] = mk4<T>(ui.x + dt * ax, ui.y + dt * ay, D == 3 ? ui.z + dt * az : T(0), rhoi);   // rho_i in lane 4
-    fnp[i] = mk4<T>(ax, ay, D == 3 ? az : T(0), T(0));   // f_visc + f_avisc + f_astress + f_body (adaptive dt)
-    T rx = xi.x + dt * uti.x, ry = xi.y + dt * uti.y, rz = D == 3 ? xi.z + dt * uti.z : xi.z;
-    if (P.per[0]) { if (rx >= P.hi[0]) rx -= P.L[0]; else if (rx < P.lo[0]) rx += P.L[0]; }
-    if (P.per[1]) { if (ry >= P.hi[1]) ry -= P.L[1]; else if (ry < P.lo[1]) ry += P.L[1]; }
-    if (D == 3 && P.per[2]) { if (rz >= P.hi[2]) rz -= P.L[2]; else if (rz < P.lo[2]) rz += P.L[2]; }
-    rstar[i] = mk4<T>(rx, ry, rz, xi.w);
+    forces_finish<T, D>(P, i, dt, xi, ui, uti, rhoi, ax, ay, az, us, rstar, fnp);
 }
+
 
 // ===========================================================================
 // A11: RHS_i (eq:sph-ppe right side, R8), D_ii (eq:coeff, R6/R7) and the
