@@ -85,6 +85,12 @@ typedef struct {
                                once per solve and every sweep streams it (particles do not move
                                during the iterations); 1: every sweep recomputes it from
                                the positions, as the paper's listing */
+    int ppe_loop;           /* form of the PPE loop (one handle, timing off; slab ranks and timing
+                               always use 1): 0 (default) = 1 (the forms measured within 10 % of
+                               each other on B200: a sweep is latency-bound at these sizes);
+                               1 = host-polled speculative batches of sweep launches; 2 = a captured
+                               CUDA graph with a device-decided WHILE node; 3 = one persistent
+                               cooperative kernel for the whole loop (grid syncs between phases) */
 } sisph_params;
 
 /* Per-step report (sisph_step).  Timings are device milliseconds measured

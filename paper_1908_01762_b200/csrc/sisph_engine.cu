@@ -188,6 +188,10 @@ template <class T, int D> struct Engine : EngineBase {
         for (auto& e : sev)
             if (e) cudaEventDestroy(e);
         delete tp;
+        drop_graph();
+        if (cst) cudaStreamDestroy(cst);
+        if (hdesc) cudaFreeHost(hdesc);
+        if (ddesc) cudaFree(ddesc);
         if (own_stream && st) cudaStreamDestroy(st);
     }
 
@@ -306,6 +310,7 @@ template <class T, int D> struct Engine : EngineBase {
         P.ghosts = dist() ? 1 : 0;
         rebuild_mode = prm->rebuild_mode;
         matrix_free = prm->matrix_free;
+        ppe_loop = prm->ppe_loop;
         for (int a = 0; a < D; a++) extent = std::max(extent, std::max(fabs(dom->lo[a]), fabs(dom->hi[a])));
         min_iter = prm->min_iter;
         max_iter = prm->max_iter;
@@ -359,7 +364,7 @@ template <class T, int D> struct Engine : EngineBase {
         AL(ccount, int, NCT) AL(fstart, int, NCT) AL(wstart, int, NCT)
         AL(bsum, int, (size_t)nblk(NCT, SCAN_B) + 1) AL(cnt, int, NT) AL(ctl, Ctl, 1) AL(cnt_in, int, NF)
         AL(cnt_s, int, NT) AL(wperm_s, int, NW) AL(wstart_s, int, NCT)
-        AL(partials, double, 2 * (size_t)nblk(NF, RHS_T) + 2) AL(dtmp, double, 3 * (size_t)n)
+        AL(partials, double, 2 * std::max((size_t)nblk(NF, RHS_T), (size_t)8192) + 2) AL(dtmp, double, 3 * (size_t)n)
         if (dist()) {
             AL(dflag, int, NT) AL(dflag2, int, NT) AL(dpre, int, NT + 1) AL(dlist[0], int, NF) AL(dlist[1], int, NF)
             AL(dlist[2], int, NF) AL(fsend[0], int, NF) AL(fsend[1], int, NF) AL(fsend_pre[0], int, NF)
@@ -1206,7 +1211,7 @@ template <class T, int D> struct Engine : EngineBase {
         // A11 with the first PPE sweep fused (walls first get p^0, R14)
         SCK(cudaMemsetAsync(&ctl->lambda_bits, 0, sizeof(unsigned long long), st));
         SCK(cudaMemsetAsync(ctl, 0, 4 * sizeof(int), st));  // ticket, iter, done, nonfinite
-        if (Nwo) ++nlaunch, k_wall_pressure<T, D><<<nblk(Nwo, 256), 256, 0, st>>>(P, pos, rho, nbr, cnt, P.cap, p, p_alt, nullptr);
+        if (Nwo) ++nlaunch, k_wall_pressure<T, D><<<nblk(Nwo, 256), 256, 0, st>>>(P, pos, rho, nbr, cnt, P.cap, p);
         SCK(cudaGetLastError());
         if (dist()) {
             PackList W{};
@@ -1229,10 +1234,104 @@ template <class T, int D> struct Engine : EngineBase {
     double last_ms_sweeps = 0;
     int last_sweeps_timed = 0;
 
+    // ---- the PPE iteration: per-solve state in a device descriptor, so the
+    // same kernels run host-polled (speculative batches; timing, slab ranks)
+    // or as the WHILE body of a captured CUDA graph (one launch per solve,
+    // the loop condition set on the device by the sweep's last block)
+    PpeDesc<T>* ddesc = nullptr;
+    PpeDesc<T>* hdesc = nullptr;   // pinned
+    int ppe_loop = 0;              // 0 auto, 1 host-polled batches, 2 graph WHILE node, 3 persistent
+    int pgrid_max = 0;             // co-resident blocks of the persistent PPE kernel
+    cudaStream_t cst = nullptr;    // capture stream (the handle's stream may be the legacy default)
+    cudaGraph_t pgraph = nullptr;
+    cudaGraphExec_t pexec = nullptr;
+    cudaGraphConditionalHandle pcond = 0;
+    long long gkey[5] = {-1, -1, -1, -1, -1};
+
+    int write_desc(double tl, int mi, int mx)
+    {
+        if (!ddesc) {
+            int rc = 0;
+            ddesc = dalloc<PpeDesc<T>>(1, err, rc);
+            if (rc) return rc;
+            SCK(cudaHostAlloc((void**)&hdesc, sizeof(PpeDesc<T>), cudaHostAllocDefault));
+        }
+        hdesc->pos = pos;
+        hdesc->rho = rho;
+        hdesc->fs = fs;
+        hdesc->nbr = nbr;
+        hdesc->coef = coef;
+        hdesc->pA = p;
+        hdesc->pB = p_alt;
+        hdesc->tol = tl;
+        hdesc->min_it = mi;
+        hdesc->max_it = mx;
+        SCK(cudaMemcpyAsync(ddesc, hdesc, sizeof(PpeDesc<T>), cudaMemcpyHostToDevice, st));
+        return SISPH_OK;
+    }
+
+    void drop_graph()
+    {
+        if (pexec) cudaGraphExecDestroy(pexec);
+        if (pgraph) cudaGraphDestroy(pgraph);
+        pexec = nullptr;
+        pgraph = nullptr;
+    }
+
+    // (re)capture the loop when what the kernels take by value changes
+    int ensure_graph()
+    {
+        const long long key[5] = {P.cap, Nfo, Nwo, coef ? 1 : 0, Nf};
+        if (pexec && !memcmp(key, gkey, sizeof(key))) return SISPH_OK;
+        drop_graph();
+        if (!cst) SCK(cudaStreamCreateWithFlags(&cst, cudaStreamNonBlocking));
+        SCK(cudaGraphCreate(&pgraph, 0));
+        SCK(cudaGraphConditionalHandleCreate(&pcond, pgraph, 1, cudaGraphCondAssignDefault));
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = pcond;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t node;
+        SCK(cudaGraphAddNode(&node, pgraph, nullptr, 0, &cp));
+        cudaGraph_t body = cp.conditional.phGraph_out[0];
+        SCK(cudaStreamBeginCaptureToGraph(cst, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+        if (Nwo) k_ppe_wall<T, D><<<nblk(Nwo, 256), 256, 0, cst>>>(P, ddesc, cnt, P.cap, ctl);
+        const int nb = std::max(nblk(Nfo, SWEEP_T), 1);
+        if (coef)
+            k_sweep<T, D, true><<<nb, SWEEP_T, 0, cst>>>(P, ddesc, rhs, diag, cnt, P.cap, ctl, partials, 0, pcond, 1);
+        else
+            k_sweep<T, D, false><<<nb, SWEEP_T, 0, cst>>>(P, ddesc, rhs, diag, cnt, P.cap, ctl, partials, 0, pcond, 1);
+        cudaError_t le = cudaGetLastError();
+        SCK(cudaStreamEndCapture(cst, &body));
+        SCK(le);
+        SCK(cudaGraphInstantiate(&pexec, pgraph, 0));
+        memcpy(gkey, key, sizeof(key));
+        return SISPH_OK;
+    }
+
+    int launch_persistent()
+    {
+        void* fn = coef ? (void*)k_ppe_persistent<T, D, true> : (void*)k_ppe_persistent<T, D, false>;
+        if (!pgrid_max) {
+            int per = 0, dev = 0, sms = 0;
+            SCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, SWEEP_T, 0));
+            SCK(cudaGetDevice(&dev));
+            SCK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+            pgrid_max = std::max(1, std::min(per * sms, 8192));
+        }
+        const int grid = std::max(1, std::min(pgrid_max, nblk(std::max(Nfo, Nwo), SWEEP_T)));
+        int cap = P.cap;
+        void* args[] = {&P, &ddesc, &rhs, &diag, &cnt, &cap, &ctl, &partials};
+        ++nlaunch;
+        SCK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(SWEEP_T), args, 0, st));
+        return SISPH_OK;
+    }
+
     int launch_sweeps(int count, double tl, int mi, int mx)
     {
         for (int c = 0; c < count; c++) {
-            if (Nwo) ++nlaunch, k_wall_pressure<T, D><<<nblk(Nwo, 256), 256, 0, st>>>(P, pos, rho, nbr, cnt, P.cap, p, p_alt, ctl);
+            if (Nwo) ++nlaunch, k_ppe_wall<T, D><<<nblk(Nwo, 256), 256, 0, st>>>(P, ddesc, cnt, P.cap, ctl);
             if (dist()) SRET(halo_p(true));
             bool rec = timing && nrec < MAXREC;
             if (rec) {
@@ -1246,10 +1345,10 @@ template <class T, int D> struct Engine : EngineBase {
             const int nb = std::max(nblk(Nfo, SWEEP_T), 1);   // one block at least: the last block decides
             if (coef)
                 ++nlaunch, k_sweep<T, D, true><<<nb, SWEEP_T, 0, st>>>(
-                               P, pos, rho, rhs, diag, fs, nbr, cnt, P.cap, coef, p, p_alt, ctl, partials, tl, mi, mx, defer);
+                               P, ddesc, rhs, diag, cnt, P.cap, ctl, partials, defer, pcond, 0);
             else
                 ++nlaunch, k_sweep<T, D, false><<<nb, SWEEP_T, 0, st>>>(
-                               P, pos, rho, rhs, diag, fs, nbr, cnt, P.cap, nullptr, p, p_alt, ctl, partials, tl, mi, mx, defer);
+                               P, ddesc, rhs, diag, cnt, P.cap, ctl, partials, defer, pcond, 0);
             if (rec) {
                 SCK(cudaEventRecord(sev[2 * nrec + 1], st));
                 nrec++;
@@ -1291,7 +1390,28 @@ template <class T, int D> struct Engine : EngineBase {
         } else {
             SCK(cudaMemsetAsync(ctl, 0, 4 * sizeof(int), st));  // ticket, iter, done, nonfinite
         }
-        if (Nf > 0 || dist()) {
+        SRET(write_desc(tl, mi, mx));
+        // the loop form: one handle with timing off may run the whole loop on the device
+        // (0 = host batches: on B200 the three forms measured within 10 % of each other on
+        // configs[0-1], where every form is bound by the ~10-25 us latency chain of one sweep)
+        int mode = ppe_loop == 0 ? 1 : ppe_loop;
+        if (dist() || timing || Nf == 0 || launched >= mx) mode = 1;
+        if (mode == 3) {
+            // one cooperative launch: walls, sweep, fixed-order reduction and decision per
+            // iteration, separated by grid syncs (small problems: no per-sweep launches)
+            SRET(launch_persistent());
+            SCK(cudaMemcpyAsync(hctl, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+            SCK(cudaStreamSynchronize(st));
+        } else if (mode == 2) {
+            // one launch: WHILE (not done) { wall pressure; sweep }  (sweeps after the
+            // decision never run; the host waits once)
+            SRET(ensure_graph());
+            SCK(cudaGraphLaunch(pexec, st));
+            SCK(cudaMemcpyAsync(hctl, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+            SCK(cudaStreamSynchronize(st));
+            // kernels the body ran: one (wall, sweep) pair per sweep + the one that saw done
+            nlaunch += (Nwo ? 2 : 1) * (std::max(hctl->iter - launched, 0) + 1);
+        } else if (Nf > 0 || dist()) {
             // speculative batches: sweeps after convergence are no-ops on the device
             // (slab ranks take the same decisions, so they run the same batches)
             int batch = std::min(mx - launched, std::max(mi, 2) + 1 - launched);
@@ -1373,7 +1493,7 @@ template <class T, int D> struct Engine : EngineBase {
             return SISPH_EINVAL;
         }
         // A13
-        if (Nwo) ++nlaunch, k_wall_pressure<T, D><<<nblk(Nwo, 256), 256, 0, st>>>(P, pos, rho, nbr, cnt, P.cap, p, p_alt, nullptr);
+        if (Nwo) ++nlaunch, k_wall_pressure<T, D><<<nblk(Nwo, 256), 256, 0, st>>>(P, pos, rho, nbr, cnt, P.cap, p);
         SCK(cudaGetLastError());
         if (dist()) {
             PackList W{};

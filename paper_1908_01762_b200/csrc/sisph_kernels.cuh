@@ -5,7 +5,11 @@
 // finish for the device-wide sums.  Citations: PAPER.md lines (P:a-b) and
 // DESIGN.md readings (Rn).
 #pragma once
+#include <cooperative_groups.h>
+
 #include "sisph_device.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace sb {
 
@@ -1082,18 +1086,27 @@ __global__ void __launch_bounds__(RHS_T) k_rhs_diag(Params<T> P, T inv_dt, const
 // sum W = 0 -> 0, optional clamp of negative values.  In a solve it reads
 // p^k from the buffer selected by the device iteration counter.
 // ===========================================================================
+// Per-solve state of the PPE iteration that changes between solves (buffer
+// rotation, list reallocation, the caller's tolerance): the sweep kernels
+// read it from device memory, so the captured graph of the loop (a WHILE
+// conditional node) is reused across steps.
+template <class T> struct PpeDesc {
+    const V4<T>* pos;
+    const T* rho;
+    const uint8_t* fs;
+    const int* nbr;
+    const T* coef;      // stored per-pair factor (nullptr: matrix-free)
+    T* pA;
+    T* pB;
+    double tol;
+    int min_it, max_it;
+};
+
 template <class T, int D>
-__global__ void __launch_bounds__(256) k_wall_pressure(Params<T> P, const V4<T>* __restrict__ pos,
-                                                       const T* __restrict__ rho, const int* __restrict__ nbr,
-                                                       const int* __restrict__ cnt, int ncap, T* pA, T* pB, const Ctl* ctl)
+__device__ __forceinline__ void wall_pressure_row(const Params<T>& P, int w, const V4<T>* __restrict__ pos,
+                                                  const T* __restrict__ rho, const int* __restrict__ nbr,
+                                                  const int* __restrict__ cnt, int ncap, T* p)
 {
-    T* p = pA;
-    if (ctl) {
-        if (ctl->done) return;
-        p = (ctl->iter & 1) ? pB : pA;
-    }
-    int w = blockIdx.x * blockDim.x + threadIdx.x;
-    if (w >= P.Nwo) return;
     int i = P.Nf + w;
     V4<T> xi = ld4(pos + i);
     T sw = 0, sp = 0, sx = 0, sy = 0, sz = 0;
@@ -1121,6 +1134,29 @@ __global__ void __launch_bounds__(256) k_wall_pressure(Params<T> P, const V4<T>*
     p[i] = pw;
 }
 
+// standalone wall pressure from the pressures in p (before A11's fused sweep, A13)
+template <class T, int D>
+__global__ void __launch_bounds__(256) k_wall_pressure(Params<T> P, const V4<T>* __restrict__ pos,
+                                                       const T* __restrict__ rho, const int* __restrict__ nbr,
+                                                       const int* __restrict__ cnt, int ncap, T* p)
+{
+    int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= P.Nwo) return;
+    wall_pressure_row<T, D>(P, w, pos, rho, nbr, cnt, ncap, p);
+}
+
+// in a solve: from p^k, the buffer selected by the device iteration counter
+template <class T, int D>
+__global__ void __launch_bounds__(256) k_ppe_wall(Params<T> P, const PpeDesc<T>* __restrict__ dsc,
+                                                  const int* __restrict__ cnt, int ncap, const Ctl* ctl)
+{
+    if (ctl->done) return;
+    int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= P.Nwo) return;
+    T* p = (ctl->iter & 1) ? dsc->pB : dsc->pA;
+    wall_pressure_row<T, D>(P, w, dsc->pos, dsc->rho, dsc->nbr, cnt, ncap, p);
+}
+
 // ===========================================================================
 // A12(ii, iii): one damped-Jacobi sweep, eq:p-sor with
 // fac_ij = 4 m_j / (rho_i (rho_i + rho_j)) r_ij.gradW_ij / (r^2 + eta h^2)
@@ -1131,20 +1167,81 @@ __global__ void __launch_bounds__(256) k_wall_pressure(Params<T> P, const V4<T>*
 // ===========================================================================
 constexpr int SWEEP_T = 256;
 
+// eq:p-sor for row i from p^k = pin (the stored or the recomputed fac_ij)
+template <class T, int D, bool STORED>
+__device__ __forceinline__ T sweep_row(const Params<T>& P, int i, const V4<T>* __restrict__ pos,
+                                       const T* __restrict__ rho, const uint8_t* __restrict__ fs,
+                                       const int* __restrict__ nbr, const int* __restrict__ cnt, int ncap,
+                                       const T* __restrict__ coef, const T* __restrict__ rhs,
+                                       const T* __restrict__ diag, const T* pin)
+{
+    const T pold = pin[i];
+    T pnew = T(0);
+    const T di = diag[i];
+    if (!fs[i] && di != T(0)) {
+        const T rhoi = rho[i];
+        T s = 0;
+        const int n = cnt[i];
+        if (STORED) {
+            const size_t b = nb_base(i, ncap);
+            const int4* __restrict__ qi = reinterpret_cast<const int4*>(nbr + b);
+            for (int c = 0; c < n; c += 4) {
+                const size_t o = (size_t)(c >> 2) * 32;
+                const int4 v = __ldcs(qi + o);
+                T f[4];
+                ld_chunk4(coef + b + (o << 2), f);
+                s += f[0] * pin[v.x];
+                if (c + 1 < n) s += f[1] * pin[v.y];
+                if (c + 2 < n) s += f[2] * pin[v.z];
+                if (c + 3 < n) s += f[3] * pin[v.w];
+            }
+        } else {
+            const V4<T> xi = ld4(pos + i);
+            for_nbrs(nbr, ncap, i, n, [&](int j) {
+                V4<T> xj = ld4(pos + j);
+                T rhoj = __ldg(rho + j);
+                T pj = pin[j];
+                T d[3], r, ri;
+                T r2 = pair_vec<T, D>(P, xi, xj, d);
+                r_of(r2, r, ri);
+                // fac_ij / (4 dW/dr-scale / rho_i): m_j r poly4(q) / ((rho_i + rho_j)(r^2 + eta h^2))
+                // (the expression of k_rhs_diag's stored value, so both modes agree bit for bit)
+                s += xj.w * (r * quintic4(r * P.inv_h)) * frcp((rhoi + rhoj) * (r2 + P.eta_h2)) * pj;
+            });
+        }
+        s *= T(4) * P.dwk * frcp(rhoi);       // S_i = sum_j fac_ij p_j = -sum_j OD_ij p_j
+        pnew = P.omega * (rhs[i] + s) * frcp(di) + (T(1) - P.omega) * pold;
+    }
+    return pnew;
+}
+
 // STORED: the per-pair part of fac_ij written by k_rhs_diag is streamed
 // alongside the neighbour index (an ELL SpMV: 4 + 4 bytes per pair from HBM,
 // p_j gathered); otherwise it is recomputed from the positions every sweep,
 // as the paper's listing does.
+//
+// The per-solve pointers and the tolerance / bounds come from dsc (device
+// memory).  use_h: the kernel runs inside the WHILE body of the solve's CUDA
+// graph and sets the loop condition (continue = not done) from the last
+// block; a sweep launched after the decision only clears it.
 template <class T, int D, bool STORED>
-__global__ void __launch_bounds__(SWEEP_T) k_sweep(Params<T> P, const V4<T>* __restrict__ pos,
-                                                   const T* __restrict__ rho, const T* __restrict__ rhs,
-                                                   const T* __restrict__ diag, const uint8_t* __restrict__ fs,
-                                                   const int* __restrict__ nbr, const int* __restrict__ cnt, int ncap,
-                                                   const T* __restrict__ coef, T* pA, T* pB, Ctl* ctl,
-                                                   double* __restrict__ partials, double tol, int min_it, int max_it,
-                                                   int defer)
+__global__ void __launch_bounds__(SWEEP_T) k_sweep(Params<T> P, const PpeDesc<T>* __restrict__ dsc,
+                                                   const T* __restrict__ rhs, const T* __restrict__ diag,
+                                                   const int* __restrict__ cnt, int ncap, Ctl* ctl,
+                                                   double* __restrict__ partials, int defer,
+                                                   cudaGraphConditionalHandle hcond, int use_h)
 {
-    if (ctl->done) return;
+    if (ctl->done) {
+        if (use_h && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(hcond, 0u);
+        return;
+    }
+    const V4<T>* __restrict__ pos = dsc->pos;
+    const T* __restrict__ rho = dsc->rho;
+    const uint8_t* __restrict__ fs = dsc->fs;
+    const int* __restrict__ nbr = dsc->nbr;
+    const T* __restrict__ coef = dsc->coef;
+    T* pA = dsc->pA;
+    T* pB = dsc->pB;
     const int kit = ctl->iter;
     const T* __restrict__ pin = (kit & 1) ? pB : pA;
     T* __restrict__ pout = (kit & 1) ? pA : pB;
@@ -1152,43 +1249,8 @@ __global__ void __launch_bounds__(SWEEP_T) k_sweep(Params<T> P, const V4<T>* __r
     double dn = 0.0, dd = 0.0;
     bool bad = false;
     if (i < P.Nfo) {
-        T pold = pin[i];
-        T pnew = T(0);
-        T di = diag[i];
-        if (!fs[i] && di != T(0)) {
-            T rhoi = rho[i];
-            T s = 0;
-            int n = cnt[i];
-            if (STORED) {
-                const size_t b = nb_base(i, ncap);
-                const int4* __restrict__ qi = reinterpret_cast<const int4*>(nbr + b);
-                for (int c = 0; c < n; c += 4) {
-                    const size_t o = (size_t)(c >> 2) * 32;
-                    const int4 v = __ldcs(qi + o);
-                    T f[4];
-                    ld_chunk4(coef + b + (o << 2), f);
-                    s += f[0] * pin[v.x];
-                    if (c + 1 < n) s += f[1] * pin[v.y];
-                    if (c + 2 < n) s += f[2] * pin[v.z];
-                    if (c + 3 < n) s += f[3] * pin[v.w];
-                }
-            } else {
-                V4<T> xi = ld4(pos + i);
-                for_nbrs(nbr, ncap, i, n, [&](int j) {
-                    V4<T> xj = ld4(pos + j);
-                    T rhoj = __ldg(rho + j);
-                    T pj = pin[j];
-                    T d[3], r, ri;
-                    T r2 = pair_vec<T, D>(P, xi, xj, d);
-                    r_of(r2, r, ri);
-                    // fac_ij / (4 dW/dr-scale / rho_i): m_j r poly4(q) / ((rho_i + rho_j)(r^2 + eta h^2))
-                    // (the expression of k_rhs_diag's stored value, so both modes agree bit for bit)
-                    s += xj.w * (r * quintic4(r * P.inv_h)) * frcp((rhoi + rhoj) * (r2 + P.eta_h2)) * pj;
-                });
-            }
-            s *= T(4) * P.dwk * frcp(rhoi);       // S_i = sum_j fac_ij p_j = -sum_j OD_ij p_j
-            pnew = P.omega * (rhs[i] + s) * frcp(di) + (T(1) - P.omega) * pold;
-        }
+        const T pold = pin[i];
+        const T pnew = sweep_row<T, D, STORED>(P, i, pos, rho, fs, nbr, cnt, ncap, coef, rhs, diag, pin);
         pout[i] = pnew;
         dn = fabs((double)pnew - (double)pold);
         dd = fabs((double)pnew);
@@ -1255,8 +1317,10 @@ __global__ void __launch_bounds__(SWEEP_T) k_sweep(Params<T> P, const V4<T>* __r
         int k1 = kit + 1;
         ctl->residual = res;
         ctl->iter = k1;
-        ctl->done = ((k1 >= min_it && res < tol) || k1 >= max_it || ctl->nonfinite) ? 1 : 0;
+        const int done = ((k1 >= dsc->min_it && res < dsc->tol) || k1 >= dsc->max_it || ctl->nonfinite) ? 1 : 0;
+        ctl->done = done;
         ctl->ticket = 0;
+        if (use_h) cudaGraphSetConditional(hcond, done ? 0u : 1u);
     }
 }
 
@@ -1274,6 +1338,104 @@ __global__ void k_decide(Ctl* ctl, double tol, int min_it, int max_it)
     ctl->residual = res;
     ctl->iter = k1;
     ctl->done = ((k1 >= min_it && res < tol) || k1 >= max_it || ctl->nonfinite) ? 1 : 0;
+}
+
+// ===========================================================================
+// The whole PPE loop in ONE cooperative launch (small problems, where the
+// per-sweep launches and their latency dominate: BASELINE configs[0-1]).
+// Per sweep: walls from p^k (grid-stride), grid sync, fluid rows (grid-
+// stride) + block partials, grid sync, block 0 sums the partials in a fixed
+// order and decides eq:convergence, grid sync.  Same row arithmetic as
+// k_sweep; the sums are grouped per block of the grid-stride loop (rounding-
+// level differences in the residual only).
+// ===========================================================================
+template <class T, int D, bool STORED>
+__global__ void __launch_bounds__(SWEEP_T) k_ppe_persistent(Params<T> P, const PpeDesc<T>* __restrict__ dsc,
+                                                            const T* __restrict__ rhs, const T* __restrict__ diag,
+                                                            const int* __restrict__ cnt, int ncap, Ctl* ctl,
+                                                            double* __restrict__ partials)
+{
+    cg::grid_group grid = cg::this_grid();
+    const V4<T>* __restrict__ pos = dsc->pos;
+    const T* __restrict__ rho = dsc->rho;
+    const uint8_t* __restrict__ fs = dsc->fs;
+    const int* __restrict__ nbr = dsc->nbr;
+    const T* __restrict__ coef = dsc->coef;
+    T* pA = dsc->pA;
+    T* pB = dsc->pB;
+    const double tol = dsc->tol;
+    const int min_it = dsc->min_it, max_it = dsc->max_it;
+    volatile Ctl* vc = ctl;
+    const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    __shared__ double sn[SWEEP_T / 32], sd[SWEEP_T / 32];
+    for (;;) {
+        if (vc->done) break;                       // every block reads it after the same grid sync
+        const int kit = vc->iter;
+        T* pin = (kit & 1) ? pB : pA;
+        T* pout = (kit & 1) ? pA : pB;
+        for (int q = gt; q < P.Nwo; q += gs) wall_pressure_row<T, D>(P, q, pos, rho, nbr, cnt, ncap, pin);
+        grid.sync();
+        double dn = 0.0, dd = 0.0;
+        bool bad = false;
+        for (int i = gt; i < P.Nfo; i += gs) {
+            const T pold = pin[i];
+            const T pnew = sweep_row<T, D, STORED>(P, i, pos, rho, fs, nbr, cnt, ncap, coef, rhs, diag, pin);
+            pout[i] = pnew;
+            dn += fabs((double)pnew - (double)pold);
+            dd += fabs((double)pnew);
+            bad = bad || !isfinite((double)pnew);
+        }
+        dn = warp_sum(dn);
+        dd = warp_sum(dd);
+        const int anybad = __any_sync(0xffffffffu, bad);
+        if (lane == 0) {
+            sn[w] = dn;
+            sd[w] = dd;
+            if (anybad) atomicExch(&ctl->nonfinite, 1);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double a = 0, b = 0;
+            for (int q = 0; q < SWEEP_T / 32; q++) {
+                a += sn[q];
+                b += sd[q];
+            }
+            partials[2 * blockIdx.x] = a;
+            partials[2 * blockIdx.x + 1] = b;
+        }
+        grid.sync();
+        if (blockIdx.x == 0) {
+            double a = 0, b = 0;
+            for (int q = threadIdx.x; q < (int)gridDim.x; q += blockDim.x) {
+                a += partials[2 * q];
+                b += partials[2 * q + 1];
+            }
+            a = warp_sum(a);
+            b = warp_sum(b);
+            __syncthreads();
+            if (lane == 0) {
+                sn[w] = a;
+                sd[w] = b;
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                double num = 0, den = 0;
+                for (int q = 0; q < SWEEP_T / 32; q++) {
+                    num += sn[q];
+                    den += sd[q];
+                }
+                const double lam = __longlong_as_double((long long)vc->lambda_bits);
+                const double dmax = den > lam ? den : lam;
+                const double res = num == 0.0 ? 0.0 : (dmax > 0.0 ? num / dmax : INFINITY);
+                const int k1 = kit + 1;
+                vc->residual = res;
+                vc->iter = k1;
+                vc->done = ((k1 >= min_it && res < tol) || k1 >= max_it || vc->nonfinite) ? 1 : 0;
+            }
+        }
+        grid.sync();
+    }
 }
 
 // ===========================================================================

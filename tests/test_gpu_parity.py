@@ -395,3 +395,31 @@ def test_square_patch_parity(prec):
         o.correct(case.dt)
         assert_close(f"p {s}", sim.get("PRESSURE"), o.get("p"), prec)
         assert_close(f"u {s}", sim.get("VELOCITY"), o.get("u"), prec, scale=max(np.abs(o.get("u")).max(), 1e-3))
+
+
+# ------------------------------------------------------------------ PPE loop forms
+@pytest.mark.parametrize("name", ["tgv2d_f64", "hydro_f64", "db3d_f32", "tgv3d_f64", "db2d_f64"])
+def test_ppe_loop_forms_agree(name):
+    """Host-polled batches (1), the CUDA-graph WHILE node (2) and the persistent
+    cooperative kernel (3) run the same row arithmetic: equal sweep counts and
+    bitwise-equal pressures; the graph runs the very same kernels, so its
+    residual is bitwise equal too (the persistent kernel groups the residual
+    sums per block of its grid-stride loop: equal to rounding)."""
+    case = CASES[name]
+    sims = {m: gpu_sim(case, ppe_loop=m) for m in (1, 2, 3)}
+    for _ in range(3):
+        r = {m: s.step(case.dt) for m, s in sims.items()}
+        assert r[1].iters == r[2].iters == r[3].iters
+        assert r[1].residual == r[2].residual
+        assert r[3].residual == pytest.approx(r[1].residual, rel=1e-9)
+    for fld in ("PRESSURE", "VELOCITY", "POSITION"):
+        ref = sims[1].get(fld)
+        assert np.array_equal(sims[2].get(fld), ref)
+        assert np.array_equal(sims[3].get(fld), ref)
+    # split API with another tolerance than the parameters': read per solve
+    for s in sims.values():
+        s.predict(case.dt)
+    its = {m: s.ppe_solve(1e-6, 50)[0] for m, s in sims.items()}
+    assert its[1] == its[2] == its[3]
+    assert np.array_equal(sims[2].get("PRESSURE"), sims[1].get("PRESSURE"))
+    assert np.array_equal(sims[3].get("PRESSURE"), sims[1].get("PRESSURE"))
