@@ -1,0 +1,34 @@
+"""TGV-2D long-run stability matrix (PAPER.md:1034-1110 settings): resolution, tolerance,
+pressure-gradient form, background pressure; L1 error / max|u| over exp(bt) at several t."""
+import sys
+sys.path.insert(0, "."); sys.path.insert(0, "scripts")
+import synth
+from paper_1908_01762_b200 import Simulation
+from variants import tgv_error
+T_OUT = (0.25, 0.5, 1.0, 2.0)
+def run(n, label, re=100.0, **over):
+    case = synth.tgv2d(n=n, re=re)
+    sim = Simulation.from_case(case, **over)
+    t, out, its = 0.0, [], 0
+    for t_end in T_OUT:
+        while t < t_end - 1e-9:
+            its += sim.step(case.dt).iters
+            t += case.dt
+        out.append(tgv_error(sim, case, t))
+    steps = round(t / case.dt)
+    print(f"n {n:3d} Re {re:5g} {label:28s} sweeps/step {its / steps:7.1f} |",
+          " ".join(f"t={tt}: {e:.3f}/{d:.2f}" for tt, (e, d) in zip(T_OUT, out)), flush=True)
+    sim.close()
+if __name__ != "__main__":
+    pass
+elif len(sys.argv) > 1 and sys.argv[1] == "tol":
+    # the paper's tolerance study: 100 x 100, asymm + GTVF
+    for tol in (0.1, 0.05, 1e-2, 5e-3, 1e-3, 5e-4, 2e-4, 1e-4):
+        run(100, f"asymm pref=1 tol {tol:g}", tol=tol)
+else:
+  for n in (50, 100):
+    for tol in (1e-2, 1e-4):
+        run(n, f"asymm pref=1 tol {tol:g}", tol=tol)
+        run(n, f"symm  pref=1 tol {tol:g}", tol=tol, pgrad=0)
+        run(n, f"symm  pref=0 tol {tol:g}", tol=tol, pgrad=0, p_ref=0.0)
+        run(n, f"asymm pref=0 tol {tol:g}", tol=tol, p_ref=0.0)
