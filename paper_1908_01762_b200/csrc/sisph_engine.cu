@@ -117,6 +117,7 @@ template <class T, int D> struct Engine : EngineBase {
     V *vt = nullptr, *vt_alt = nullptr, *rn = nullptr, *rstar = nullptr, *nrm = nullptr, *nstmp = nullptr;
     V *rkA = nullptr, *rkB = nullptr, *vk = nullptr, *dk = nullptr;
     V* fnp = nullptr;       // non-pressure acceleration of A8 (adaptive dt)
+    int* dcnt_w = nullptr;  // device flag of set_field's wall check
     bool stepped = false;   // a correct has completed: next_dt is defined
     bool pre_swept = false; // A11 ran the first Jacobi sweep (p^1 in p_alt, sums deferred)
     T *p = nullptr, *p_alt = nullptr, *rho = nullptr, *rho_alt = nullptr, *rhs = nullptr, *diag = nullptr;
@@ -177,7 +178,7 @@ template <class T, int D> struct Engine : EngineBase {
                         ccount, fstart, wstart, bsum, nbr, cnt, ctl, partials, dtmp, nbr_in, cnt_in,
                         nbs, cnt_s, wperm_s, wstart_s, coef, dflag, dflag2, dpre, dlist[0], dlist[1], dlist[2],
                         dcnt, fsend[0], fsend[1], fsend_pre[0], fsend_pre[1], grecv, wsend[0], wsend[1], wrecv,
-                        inv, sbuf[0], sbuf[1], rbuf[0], rbuf[1], wtmp, fnp};
+                        inv, sbuf[0], sbuf[1], rbuf[0], rbuf[1], wtmp, fnp, dcnt_w};
         if (st) cudaStreamSynchronize(st);
         for (void* q : ptrs)
             if (q) cudaFree(q);
@@ -357,7 +358,7 @@ template <class T, int D> struct Engine : EngineBase {
     if (rc) return rc;
         AL(pos, V, NT) AL(pos_alt, V, NT) AL(vel, V, NT) AL(vel_alt, V, NT) AL(us, V, NT) AL(us_alt, V, NT)
         AL(vt, V, NF) AL(vt_alt, V, NF) AL(rn, V, NT) AL(rstar, V, NT) AL(nrm, V, NW) AL(nstmp, V, NW)
-        AL(rkA, V, NT) AL(rkB, V, NT) AL(vk, V, NF) AL(dk, V, NF) AL(fnp, V, NF)
+        AL(rkA, V, NT) AL(rkB, V, NT) AL(vk, V, NF) AL(dk, V, NF) AL(fnp, V, NF) AL(dcnt_w, int, 4)
         AL(p, T, NT) AL(p_alt, T, NT) AL(rho, T, NT) AL(rho_alt, T, NT) AL(rhs, T, NF) AL(diag, T, NF)
         AL(fs, uint8_t, NF) AL(fs_alt, uint8_t, NF) AL(pid, int, NT) AL(pid_alt, int, NT)
         AL(keys, int, NT) AL(rank, int, NT) AL(perm0, int, NT) AL(perm, int, NT)
@@ -1689,25 +1690,19 @@ template <class T, int D> struct Engine : EngineBase {
             case SISPH_FIELD_POSITION: {
                 bool mid = phase != IDLE;
                 vec(mid ? rn : pos, 0, Nfo, 1);
-                if (Nw) {
+                if (Nwo) {
                     // wall geometry is static; re-sort walls + normals only if it changed
-                    std::vector<double> oldw((size_t)count);
-                    SRET(get_field_walls_pos(oldw.data()));
-                    bool changed = false;
-                    std::vector<char> mine(n, 0);
-                    std::vector<int> hp(Nwo);
-                    if (Nwo) SCK(cudaMemcpy(hp.data(), pid + Nf, Nwo * sizeof(int), cudaMemcpyDeviceToHost));
-                    for (int w = 0; w < Nwo; w++) mine[hp[w]] = 1;
-                    for (int64_t k = 0; k < n && !changed; k++)
-                        if (mine[k])
-                            for (int a = 0; a < D; a++)
-                                if ((T)in[k * D + a] != (T)oldw[k * D + a]) changed = true;
+                    // (compared on the device against the input, in working precision)
+                    SCK(cudaMemsetAsync(dcnt_w, 0, sizeof(int), st));
+                    ++nlaunch, k_walls_changed<T><<<nblk(Nwo, B), B, 0, st>>>(dtmp, pid + Nf, Nwo, D, pos + Nf, dcnt_w);
+                    int changed = 0;
+                    SCK(cudaMemcpyAsync(&changed, dcnt_w, sizeof(int), cudaMemcpyDeviceToHost, st));
+                    SCK(cudaStreamSynchronize(st));
                     if (changed) {
                         if (dist()) {
                             err = "set_field: slab ranks keep the wall geometry of sisph_create_dist";
                             return SISPH_EINVAL;
                         }
-                        SCK(cudaMemcpyAsync(dtmp, in, (size_t)count * sizeof(double), cudaMemcpyDefault, st));
                         vec(pos, Nf, Nw, 1);
                         SRET(sort_walls(false));
                         SRET(first_build());

@@ -1832,6 +1832,20 @@ __global__ void k_to_ids_sc(const S* __restrict__ src, const int* __restrict__ i
     if (s >= n) return;
     dst[id[s]] = (double)src[s];
 }
+// has any owned wall's position (creation-id order input, working precision)
+// changed?  (set_field(POSITION): the wall geometry is static unless it does)
+template <class T>
+__global__ void k_walls_changed(const double* __restrict__ src, const int* __restrict__ id, int n, int dim,
+                                const V4<T>* __restrict__ wpos, int* __restrict__ flag)
+{
+    int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    const double* v = src + (size_t)id[s] * dim;
+    const V4<T> o = wpos[s];
+    bool ch = (T)v[0] != o.x || (T)v[1] != o.y;
+    if (dim == 3) ch = ch || (T)v[2] != o.z;
+    if (ch) atomicOr(flag, 1);
+}
 __global__ void k_iota(int* __restrict__ a, int n, int base)
 {
     int s = blockIdx.x * blockDim.x + threadIdx.x;

@@ -32,3 +32,8 @@ else:
         run(n, f"symm  pref=1 tol {tol:g}", tol=tol, pgrad=0)
         run(n, f"symm  pref=0 tol {tol:g}", tol=tol, pgrad=0, p_ref=0.0)
         run(n, f"asymm pref=0 tol {tol:g}", tol=tol, p_ref=0.0)
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "pref":
+    for n in (50, 100):
+        for pref in (1.0, 10.0, 100.0):
+            for tol in (1e-2, 1e-3):
+                run(n, f"asymm pref={pref:g} tol {tol:g}", tol=tol, p_ref=pref)
