@@ -70,9 +70,14 @@ def workload(name, ranks=1):
     return c, desc
 
 
-def sample_case(name):
-    """Bounded CPU sample of the same workload."""
+def sample_case(name, small=False):
+    """Bounded CPU sample of the same workload.  small: the reference arm's per-step
+    sample, so that --steps K --warmup W of the oracle ends within a few minutes."""
     import synth
+    if name == "dambreak3d" and small:
+        # same dx, parameters and recipe; a 64 x 12 x 64 block in a quarter-length tank
+        return (synth.dambreak3d(nfx=64, nfy=12, nfz=64, tank_nx=206, wall_nz=77),
+                "64 x 12 x 64 block of the same dam-break recipe (dx = 1/256, quarter-length tank)")
     if name == "dambreak3d":
         # 12 of the 64 spanwise rows: the periodic y axis keeps 4 cells of 3h (>= 3, R26)
         return synth.dambreak3d(nfy=12), "12/64 spanwise slab of the per-GPU workload (nfy=12)"
@@ -193,7 +198,7 @@ def run_reference(args):
         return
     import oracle
     oracle.build()
-    case, sdesc = sample_case(args.workload)
+    case, sdesc = sample_case(args.workload, small=True)
     _, desc = workload(args.workload)
     o = oracle.Sim(case)
     for _ in range(args.warmup):
