@@ -284,6 +284,11 @@ int sisph_get_counts(const sisph_t* s, int64_t* n, int64_t* n_fluid, int64_t* n_
 /* Enable (1) / disable (0) per-phase CUDA-event timing in sisph_step. */
 int sisph_set_timing(sisph_t* s, int enable);
 
+/* Device milliseconds of the sweep-kernel launches of the last solve that
+ * were bracketed by CUDA events (timing enabled; the first sweep is fused into
+ * A11 and not counted), and their number.  Outputs may be NULL. */
+int sisph_sweep_timing(sisph_t* s, double* ms, int* n);
+
 /* Wait for all work queued on the handle's stream. */
 int sisph_sync(sisph_t* s);
 

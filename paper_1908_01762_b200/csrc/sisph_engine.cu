@@ -81,6 +81,7 @@ struct EngineBase {
                                  int64_t* total) = 0;
     virtual int owned_counts(int64_t* nfo, int64_t* nwo) = 0;
     virtual int next_dt(double* dtn, double* dtc, double* dtf) = 0;
+    virtual int sweep_timing(double* ms, int* n) = 0;
     virtual int sync() = 0;
     int timing = 0;
     int64_t nlaunch = 0;  // kernel launches issued (all entry points)
@@ -1874,6 +1875,13 @@ template <class T, int D> struct Engine : EngineBase {
         return SISPH_OK;
     }
 
+    int sweep_timing(double* ms, int* nn) override
+    {
+        if (ms) *ms = last_ms_sweeps;
+        if (nn) *nn = last_sweeps_timed;
+        return SISPH_OK;
+    }
+
     int owned_counts(int64_t* nfo, int64_t* nwo) override
     {
         if (nfo) *nfo = Nfo;
@@ -2240,6 +2248,11 @@ int sisph_next_dt(sisph_t* s, double* dt_next, double* dt_cfl, double* dt_force)
 {
     CHK_HANDLE(s);
     return s->e->next_dt(dt_next, dt_cfl, dt_force);
+}
+int sisph_sweep_timing(sisph_t* s, double* ms, int* n)
+{
+    CHK_HANDLE(s);
+    return s->e->sweep_timing(ms, n);
 }
 int sisph_set_timing(sisph_t* s, int enable)
 {

@@ -26,7 +26,7 @@ EXPORTED = ["sisph_params_default", "sisph_create", "sisph_destroy", "sisph_buil
             "sisph_predict", "sisph_ppe_solve", "sisph_correct", "sisph_step", "sisph_get_field",
             "sisph_set_field", "sisph_get_order", "sisph_get_neighbors", "sisph_get_neighbors_of",
             "sisph_get_counts", "sisph_get_owned_counts", "sisph_nccl_unique_id", "sisph_local_group_create",
-            "sisph_local_group_destroy", "sisph_slab_bounds", "sisph_slab_owner", "sisph_create_dist", "sisph_next_dt",
+            "sisph_local_group_destroy", "sisph_slab_bounds", "sisph_slab_owner", "sisph_create_dist", "sisph_next_dt", "sisph_sweep_timing",
             "sisph_set_timing", "sisph_sync", "sisph_last_error"]
 
 
@@ -96,6 +96,7 @@ def lib():
         L.sisph_get_counts.argtypes = [C.c_void_p, i64p, i64p, i64p]
         L.sisph_get_owned_counts.argtypes = [C.c_void_p, i64p, i64p]
         L.sisph_next_dt.argtypes = [C.c_void_p, dp, dp, dp]
+        L.sisph_sweep_timing.argtypes = [C.c_void_p, dp, C.POINTER(C.c_int)]
         L.sisph_nccl_unique_id.argtypes = [C.c_char_p, C.POINTER(C.c_uint8)]
         L.sisph_local_group_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
         L.sisph_local_group_destroy.argtypes = [C.c_void_p]
@@ -251,6 +252,12 @@ class Simulation:
         a, b, c = C.c_double(), C.c_double(), C.c_double()
         _check(lib().sisph_next_dt(self._h, C.byref(a), C.byref(b), C.byref(c)), self._h)
         return a.value, b.value, c.value
+
+    def sweep_timing(self):
+        """(device ms, launches) of the bracketed sweep launches of the last solve."""
+        ms, n = C.c_double(), C.c_int()
+        _check(lib().sisph_sweep_timing(self._h, C.byref(ms), C.byref(n)), self._h)
+        return ms.value, n.value
 
     def owned_counts(self):
         nf, nw = C.c_int64(), C.c_int64()
