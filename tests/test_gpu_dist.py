@@ -197,3 +197,31 @@ def test_adaptive_dt_over_slab_ranks():
         for a, b in zip(out[r], ref):
             assert a == pytest.approx(b, rel=1e-12)
     g.close()
+
+
+def test_full_size_two_slabs_equal_single_gpu():
+    """The bench's N = 2 weak-scaling problem at full size: BASELINE configs[4]
+    with two per-GPU slabs along the periodic y (4.2M fluid particles), as two
+    emulated ranks vs one handle holding the whole problem; fp32, 3 steps with
+    fixed sweeps so both sides do identical work."""
+    case = synth.dambreak3d(ranks=2)
+    over = {"tol": 0.0, "max_iter": 3}
+    single = gpu_sim(case, **over)
+    rs = [single.step(case.dt) for _ in range(3)]
+    sims, reps, g = run_ranks(case, 2, 1, 3, **over)
+    assert all(reps[r][s].iters == rs[s].iters == 3 for r in range(2) for s in range(3))
+    assert sum(s.owned_counts()[0] for s in sims) == case.n_fluid
+    rel, ab = TOL[32]
+    for fld in ("PRESSURE", "VELOCITY"):
+        a, b = gathered(sims, fld), single.get(fld)
+        scale = max(np.abs(b).max(), 1e-3)
+        assert np.abs(a - b).max() <= rel * scale + ab, fld
+    x, xs = gathered(sims, "POSITION"), single.get("POSITION")
+    d = x - xs
+    L = case.hi[1] - case.lo[1]
+    d[:, 1] = (d[:, 1] + 0.5 * L) % L - 0.5 * L
+    assert np.abs(d).max() <= rel * np.abs(case.x).max() + ab
+    assert all(reps[r][-1].n_ghost_fluid > 0 for r in range(2))
+    for s in sims:
+        s.close()
+    g.close()
