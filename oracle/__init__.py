@@ -45,6 +45,7 @@ class Cfg(C.Structure):
         ("clamp_wall_p", C.c_int), ("K", C.c_int), ("min_iter", C.c_int),
         ("max_iter", C.c_int), ("tol", C.c_double),
         ("wall_rho_summation", C.c_int),
+        ("ppe_mean_free", C.c_int),
     ]
 
 
@@ -134,6 +135,7 @@ def make_cfg(dim, lo, hi, periodic, h, params: dict | None = None) -> Cfg:
     c.max_iter = p.get("max_iter", 1000)
     c.tol = p.get("tol", 1e-2)
     c.wall_rho_summation = p.get("wall_rho_summation", 0)
+    c.ppe_mean_free = p.get("ppe_mean_free", 0)
     return c
 
 

@@ -786,6 +786,23 @@ void or_solve(or_sim* s, double tol, int max_iter, or_report* rep)
 #pragma omp parallel for schedule(static)
         for (int64_t i = 0; i < n; i++)
             pn[i] = s->tag[i] == FLUID ? sweep_one(s, pk, i) : pk[i];
+        if (s->c.ppe_mean_free) {
+            /* reading R32: without a Dirichlet row (no free surface) the PPE operator has the
+             * constant null space (its rows sum to zero, eq:coeff / eq:coeff1) and the Jacobi
+             * iterate drifts along it; remove the mean of the live rows, in id order */
+            double sum = 0.0;
+            int64_t cnt = 0;
+            for (int64_t i = 0; i < n; i++)
+                if (s->tag[i] == FLUID && s->fs[i] == 0.0 && s->diag[i] != 0.0) {
+                    sum += pn[i];
+                    cnt++;
+                }
+            if (cnt > 0) {
+                double m = sum / (double)cnt;
+                for (int64_t i = 0; i < n; i++)
+                    if (s->tag[i] == FLUID && s->fs[i] == 0.0 && s->diag[i] != 0.0) pn[i] -= m;
+            }
+        }
         double num = 0.0, den = 0.0;
         for (int64_t i = 0; i < n; i++) {
             if (s->tag[i] != FLUID) continue;

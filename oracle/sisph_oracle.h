@@ -31,6 +31,8 @@ typedef struct {
     int min_iter, max_iter;  /* P:545-546, P:770 */
     double tol;              /* epsilon of eq:convergence */
     int wall_rho_summation;  /* R4: 1 walls get summation density, 0 walls keep rho0 */
+    int ppe_mean_free;       /* R32: 1 = remove the mean of the live rows (not free surface, D_ii != 0)
+                                from every Jacobi iterate (null space of a PPE with no Dirichlet row) */
 } or_cfg;
 
 typedef struct or_sim or_sim;

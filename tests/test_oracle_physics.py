@@ -366,3 +366,39 @@ def test_adaptive_dt_unrestricted_at_rest(orc):
     s.step(1e-3)
     dtn, dtc, dtf = s.next_dt()
     assert np.isinf(dtc) and np.isinf(dtf) and np.isinf(dtn)
+
+
+# ---------------------------------------------------------------- reading R32 (null space of the PPE)
+def test_periodic_ppe_operator_has_the_constant_null_space(orc):
+    # eq:coeff / eq:coeff1: D_ii = sum_j fac_ij and OD_ij = -fac_ij, so every row of the
+    # operator sums to zero: a uniform pressure added to any iterate is a fixed point of the
+    # sweep (eq:p-sor with omega: omega (RHS + S) / D + (1 - omega) p shifts by the same c).
+    case, s = _resting_lattice(orc, 2, 16, jitter=0.15, p_ref=0.0)
+    rng = np.random.default_rng(3)
+    s.set("u", rng.uniform(-1, 1, (case.n, 2)))
+    s.predict(1e-3)
+    pk = rng.uniform(-1, 1, case.n)
+    a = s.sweep(pk)
+    b = s.sweep(pk + 7.5)
+    assert np.allclose(b - a, 7.5, rtol=0, atol=1e-9)
+
+
+def test_mean_free_jacobi_removes_the_drift(orc):
+    # On a periodic jittered lattice the source at r* is not in the range of the singular
+    # operator, so plain Jacobi drifts along the null space and its residual floors; with
+    # the mean removed (R32) the iterates converge (residual well below the floor) and the
+    # shape (p - mean) is the same as the drifting iterate's.
+    case = synth.tgv2d(n=24)
+    res = {}
+    pres = {}
+    for mf in (0, 1):
+        case.params["ppe_mean_free"] = mf
+        s = orc.Sim(case)
+        s.predict(case.dt)
+        it, r, _ = s.solve(1e-12, 3000)
+        res[mf] = r
+        p = s.get("p")
+        pres[mf] = p - p.mean()
+    case.params["ppe_mean_free"] = 0
+    assert res[1] < 1e-3 * res[0]
+    assert np.abs(pres[1] - pres[0]).max() < 2e-2 * np.abs(pres[1]).max()
