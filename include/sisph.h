@@ -91,6 +91,12 @@ typedef struct {
                                1 = host-polled speculative batches of sweep launches; 2 = a captured
                                CUDA graph with a device-decided WHILE node; 3 = one persistent
                                cooperative kernel for the whole loop (grid syncs between phases) */
+    int ppe_mean_free;      /* reading R32: 1 = after every Jacobi sweep subtract the
+                               mean of the live rows (fluid, not free surface, D_ii != 0) from
+                               p^{k+1} before eq:convergence -- the projection onto the range of
+                               a PPE with no Dirichlet row (fully periodic / enclosed flows, whose
+                               operator has the constant null space: eq:coeff rows sum to zero).
+                               0 (default) = eq:p-sor as printed.  Not with ppe_loop = 3. */
 } sisph_params;
 
 /* Per-step report (sisph_step).  Timings are device milliseconds measured

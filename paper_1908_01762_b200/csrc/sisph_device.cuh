@@ -66,6 +66,7 @@ template <class T> struct Params {
     T rho0, nu, alpha, c_ref, omega, fs_ratio, p_ref;
     T g[3];
     int pgrad, pref_external, ustar_noslip, clamp_wall_p, wall_rho_summation;
+    int mean_free;          // R32: remove the live-row mean of every Jacobi iterate
     // GTVF inner list (pairs with r* < 3 h~ + skin; used when h~ < h)
     int cap_in;
     float Rin2f;           // (3 h~ + skin)^2 (1 + 2^-10): generous inclusion

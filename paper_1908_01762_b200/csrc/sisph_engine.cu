@@ -313,6 +313,7 @@ template <class T, int D> struct Engine : EngineBase {
         rebuild_mode = prm->rebuild_mode;
         matrix_free = prm->matrix_free;
         ppe_loop = prm->ppe_loop;
+        P.mean_free = prm->ppe_mean_free ? 1 : 0;
         for (int a = 0; a < D; a++) extent = std::max(extent, std::max(fabs(dom->lo[a]), fabs(dom->hi[a])));
         min_iter = prm->min_iter;
         max_iter = prm->max_iter;
@@ -1300,10 +1301,12 @@ template <class T, int D> struct Engine : EngineBase {
         SCK(cudaStreamBeginCaptureToGraph(cst, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
         if (Nwo) k_ppe_wall<T, D><<<nblk(Nwo, 256), 256, 0, cst>>>(P, ddesc, cnt, P.cap, ctl);
         const int nb = std::max(nblk(Nfo, SWEEP_T), 1);
+        const int uh = P.mean_free ? 0 : 1;   // mean-free: k_mean_fix decides and sets the condition
         if (coef)
-            k_sweep<T, D, true><<<nb, SWEEP_T, 0, cst>>>(P, ddesc, rhs, diag, cnt, P.cap, ctl, partials, 0, pcond, 1);
+            k_sweep<T, D, true><<<nb, SWEEP_T, 0, cst>>>(P, ddesc, rhs, diag, cnt, P.cap, ctl, partials, 0, pcond, uh);
         else
-            k_sweep<T, D, false><<<nb, SWEEP_T, 0, cst>>>(P, ddesc, rhs, diag, cnt, P.cap, ctl, partials, 0, pcond, 1);
+            k_sweep<T, D, false><<<nb, SWEEP_T, 0, cst>>>(P, ddesc, rhs, diag, cnt, P.cap, ctl, partials, 0, pcond, uh);
+        if (P.mean_free) k_mean_fix<T><<<nb, SWEEP_T, 0, cst>>>(P, ddesc, diag, ctl, partials, 0, pcond, 1);
         cudaError_t le = cudaGetLastError();
         SCK(cudaStreamEndCapture(cst, &body));
         SCK(le);
@@ -1330,6 +1333,18 @@ template <class T, int D> struct Engine : EngineBase {
         return SISPH_OK;
     }
 
+    // R32: remove the live-row mean of the iterate the sweep just wrote
+    // (slab ranks: the live sum and count are allreduced first, the residual
+    // sums after) and reduce eq:convergence on the corrected iterate
+    int mean_fix()
+    {
+        if (dist()) SRET(xallreduce(ctl->red, 3, 0));
+        const int nb = std::max(nblk(Nfo, SWEEP_T), 1);
+        ++nlaunch, k_mean_fix<T><<<nb, SWEEP_T, 0, st>>>(P, ddesc, diag, ctl, partials, dist() ? 1 : 0, pcond, 0);
+        SCK(cudaGetLastError());
+        return SISPH_OK;
+    }
+
     int launch_sweeps(int count, double tl, int mi, int mx)
     {
         for (int c = 0; c < count; c++) {
@@ -1351,6 +1366,7 @@ template <class T, int D> struct Engine : EngineBase {
             else
                 ++nlaunch, k_sweep<T, D, false><<<nb, SWEEP_T, 0, st>>>(
                                P, ddesc, rhs, diag, cnt, P.cap, ctl, partials, defer, pcond, 0);
+            if (P.mean_free) SRET(mean_fix());
             if (rec) {
                 SCK(cudaEventRecord(sev[2 * nrec + 1], st));
                 nrec++;
@@ -1381,23 +1397,28 @@ template <class T, int D> struct Engine : EngineBase {
         nrec = 0;
         const bool pre = pre_swept;
         pre_swept = false;
+        SRET(write_desc(tl, mi, mx));
         if (pre) {
             // sweep 1 ran inside A11 as a deferred sweep: decide it now with this
-            // solve's tolerance and bounds (slab ranks: sums allreduced first)
-            if (dist()) SRET(xallreduce(ctl->red, 3, 0));
-            ++nlaunch, k_decide<<<1, 1, 0, st>>>(ctl, tl, mi, mx);
+            // solve's tolerance and bounds (slab ranks: sums allreduced first;
+            // mean-free: the mean is removed first, k_mean_fix decides one handle)
+            if (P.mean_free) SRET(mean_fix());
+            if (dist() || !P.mean_free) {
+                if (dist()) SRET(xallreduce(ctl->red, 3, 0));
+                ++nlaunch, k_decide<<<1, 1, 0, st>>>(ctl, tl, mi, mx);
+            }
             SCK(cudaGetLastError());
             if (dist()) SRET(halo_p(false));
             launched = 1;
         } else {
             SCK(cudaMemsetAsync(ctl, 0, 4 * sizeof(int), st));  // ticket, iter, done, nonfinite
         }
-        SRET(write_desc(tl, mi, mx));
         // the loop form: one handle with timing off may run the whole loop on the device
         // (0 = host batches: on B200 the three forms measured within 10 % of each other on
         // configs[0-1], where every form is bound by the ~10-25 us latency chain of one sweep)
         int mode = ppe_loop == 0 ? 1 : ppe_loop;
         if (dist() || timing || Nf == 0 || launched >= mx) mode = 1;
+        if (mode == 3 && P.mean_free) mode = 2;   // the persistent loop has no mean-free phase
         if (mode == 3) {
             // one cooperative launch: walls, sweep, fixed-order reduction and decision per
             // iteration, separated by grid syncs (small problems: no per-sweep launches)
@@ -1413,6 +1434,7 @@ template <class T, int D> struct Engine : EngineBase {
             SCK(cudaStreamSynchronize(st));
             // kernels the body ran: one (wall, sweep) pair per sweep + the one that saw done
             nlaunch += (Nwo ? 2 : 1) * (std::max(hctl->iter - launched, 0) + 1);
+            if (P.mean_free) nlaunch += std::max(hctl->iter - launched, 0) + 1;
         } else if (Nf > 0 || dist()) {
             // speculative batches: sweeps after convergence are no-ops on the device
             // (slab ranks take the same decisions, so they run the same batches)

@@ -1019,8 +1019,14 @@ __global__ void __launch_bounds__(RHS_T) k_rhs_diag(Params<T> P, T inv_dt, const
                 pnew = P.omega * (sr + sp) * frcp(sd) + (T(1) - P.omega) * pold;
             }
             pout[i] = pnew;
-            dn = fabs((double)pnew - (double)pold);
-            dd = fabs((double)pnew);
+            if (P.mean_free) {
+                // R32: reduce (sum, count) of the live rows; k_mean_fix removes the mean
+                dn = live ? (double)pnew : 0.0;
+                dd = live ? 1.0 : 0.0;
+            } else {
+                dn = fabs((double)pnew - (double)pold);
+                dd = fabs((double)pnew);
+            }
             bad = !isfinite((double)pnew);
         }
     }
@@ -1252,8 +1258,15 @@ __global__ void __launch_bounds__(SWEEP_T) k_sweep(Params<T> P, const PpeDesc<T>
         const T pold = pin[i];
         const T pnew = sweep_row<T, D, STORED>(P, i, pos, rho, fs, nbr, cnt, ncap, coef, rhs, diag, pin);
         pout[i] = pnew;
-        dn = fabs((double)pnew - (double)pold);
-        dd = fabs((double)pnew);
+        if (P.mean_free) {
+            // R32: (sum, count) of the live rows; k_mean_fix removes the mean and decides
+            const bool live = !fs[i] && diag[i] != T(0);
+            dn = live ? (double)pnew : 0.0;
+            dd = live ? 1.0 : 0.0;
+        } else {
+            dn = fabs((double)pnew - (double)pold);
+            dd = fabs((double)pnew);
+        }
         bad = !isfinite((double)pnew);
     }
     // block reduction (fixed order)
@@ -1303,8 +1316,9 @@ __global__ void __launch_bounds__(SWEEP_T) k_sweep(Params<T> P, const PpeDesc<T>
             num += sn[q];
             den += sd[q];
         }
-        if (defer) {
+        if (defer || P.mean_free) {
             // slab ranks: the local sums go through an allreduce, k_decide finishes
+            // (mean-free: the live-row sum and count go to k_mean_fix)
             ctl->red[0] = num;
             ctl->red[1] = den;
             ctl->red[2] = ctl->nonfinite ? 1.0 : 0.0;
@@ -1320,6 +1334,106 @@ __global__ void __launch_bounds__(SWEEP_T) k_sweep(Params<T> P, const PpeDesc<T>
         const int done = ((k1 >= dsc->min_it && res < dsc->tol) || k1 >= dsc->max_it || ctl->nonfinite) ? 1 : 0;
         ctl->done = done;
         ctl->ticket = 0;
+        if (use_h) cudaGraphSetConditional(hcond, done ? 0u : 1u);
+    }
+}
+
+// Reading R32 (ppe_mean_free): the sweep (or A11's fused first sweep) left
+// p^{k+1} in pout and (sum, count) of its live rows in ctl->red (allreduced
+// on slab ranks).  Subtract the mean from the live rows, then the fused
+// eq:convergence reduction of k_sweep on the corrected iterate: decide (one
+// handle; in the solve's graph it sets the WHILE condition) or defer the two
+// sums to an allreduce + k_decide (slab ranks).
+template <class T>
+__global__ void __launch_bounds__(SWEEP_T) k_mean_fix(Params<T> P, const PpeDesc<T>* __restrict__ dsc,
+                                                      const T* __restrict__ diag, Ctl* ctl,
+                                                      double* __restrict__ partials, int defer,
+                                                      cudaGraphConditionalHandle hcond, int use_h)
+{
+    if (ctl->done) {
+        if (use_h && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(hcond, 0u);
+        return;
+    }
+    const uint8_t* __restrict__ fs = dsc->fs;
+    const int kit = ctl->iter;
+    const T* __restrict__ pin = (kit & 1) ? dsc->pB : dsc->pA;
+    T* __restrict__ pout = (kit & 1) ? dsc->pA : dsc->pB;
+    const double sum = ctl->red[0], count = ctl->red[1], bad_in = ctl->red[2];
+    const double mean = count > 0.0 ? sum / count : 0.0;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    double dn = 0.0, dd = 0.0;
+    bool bad = false;
+    if (i < P.Nfo) {
+        T v = pout[i];
+        if (!fs[i] && diag[i] != T(0)) {
+            v = (T)((double)v - mean);
+            pout[i] = v;
+        }
+        dn = fabs((double)v - (double)pin[i]);
+        dd = fabs((double)v);
+        bad = !isfinite((double)v);
+    }
+    __shared__ double sn[SWEEP_T / 32], sd[SWEEP_T / 32];
+    __shared__ int last;
+    dn = warp_sum(dn);
+    dd = warp_sum(dd);
+    const int anybad = __any_sync(0xffffffffu, bad);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) {
+        sn[w] = dn;
+        sd[w] = dd;
+        if (anybad) atomicExch(&ctl->nonfinite, 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0, b = 0;
+        for (int q = 0; q < SWEEP_T / 32; q++) {
+            a += sn[q];
+            b += sd[q];
+        }
+        partials[2 * blockIdx.x] = a;
+        partials[2 * blockIdx.x + 1] = b;
+        __threadfence();
+        const unsigned t = atomicAdd(&ctl->ticket, 1u);
+        last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double a = 0, b = 0;
+    for (int q = threadIdx.x; q < (int)gridDim.x; q += blockDim.x) {
+        a += ((volatile double*)partials)[2 * q];
+        b += ((volatile double*)partials)[2 * q + 1];
+    }
+    a = warp_sum(a);
+    b = warp_sum(b);
+    if (lane == 0) {
+        sn[w] = a;
+        sd[w] = b;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double num = 0, den = 0;
+        for (int q = 0; q < SWEEP_T / 32; q++) {
+            num += sn[q];
+            den += sd[q];
+        }
+        if (bad_in > 0.0) ctl->nonfinite = 1;
+        ctl->ticket = 0;
+        if (defer) {
+            ctl->red[0] = num;
+            ctl->red[1] = den;
+            ctl->red[2] = ctl->nonfinite ? 1.0 : 0.0;
+            return;
+        }
+        const double lam = __longlong_as_double((long long)ctl->lambda_bits);
+        const double dmax = den > lam ? den : lam;
+        const double res = num == 0.0 ? 0.0 : (dmax > 0.0 ? num / dmax : INFINITY);
+        const int k1 = kit + 1;
+        ctl->residual = res;
+        ctl->iter = k1;
+        const int done = ((k1 >= dsc->min_it && res < dsc->tol) || k1 >= dsc->max_it || ctl->nonfinite) ? 1 : 0;
+        ctl->done = done;
         if (use_h) cudaGraphSetConditional(hcond, done ? 0u : 1u);
     }
 }

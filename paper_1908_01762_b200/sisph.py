@@ -44,7 +44,7 @@ class sisph_params(C.Structure):
         ("clamp_wall_p", C.c_int), ("K", C.c_int), ("min_iter", C.c_int), ("max_iter", C.c_int),
         ("tol", C.c_double), ("wall_rho_summation", C.c_int), ("nbr_cap", C.c_int),
         ("device", C.c_int), ("stream", C.c_void_p), ("rebuild_mode", C.c_int),
-        ("matrix_free", C.c_int), ("ppe_loop", C.c_int),
+        ("matrix_free", C.c_int), ("ppe_loop", C.c_int), ("ppe_mean_free", C.c_int),
     ]
 
 

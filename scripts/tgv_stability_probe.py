@@ -21,6 +21,11 @@ def run(n, label, re=100.0, **over):
     sim.close()
 if __name__ != "__main__":
     pass
+elif len(sys.argv) > 1 and sys.argv[1] == "meanfree":
+    # reading R32: the same tolerance study with the live-row mean removed every sweep
+    for tol in (1e-2, 1e-3, 1e-4):
+        run(100, f"asymm tol {tol:g} as printed", tol=tol)
+        run(100, f"asymm tol {tol:g} mean-free", tol=tol, ppe_mean_free=1)
 elif len(sys.argv) > 1 and sys.argv[1] == "tol":
     # the paper's tolerance study: 100 x 100, asymm + GTVF
     for tol in (0.1, 0.05, 1e-2, 5e-3, 1e-3, 5e-4, 2e-4, 1e-4):

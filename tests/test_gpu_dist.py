@@ -225,3 +225,22 @@ def test_full_size_two_slabs_equal_single_gpu():
     for s in sims:
         s.close()
     g.close()
+
+
+def test_mean_free_over_slab_ranks():
+    """R32 on slab ranks: the live sum and count are allreduced before the
+    mean is removed, the residual sums after: same sweep counts as one handle."""
+    case = synth.tgv2d()
+    over = {"ppe_mean_free": 1, "tol": 1e-6}
+    single = gpu_sim(case, **over)
+    rs = [single.step(case.dt) for _ in range(3)]
+    sims, reps, g = run_ranks(case, 3, 0, 3, **over)
+    for s in range(3):
+        assert {reps[r][s].iters for r in range(3)} == {rs[s].iters}
+    rel, ab = TOL[64]
+    for fld in ("PRESSURE", "VELOCITY"):
+        a, b = gathered(sims, fld), single.get(fld)
+        assert np.abs(a - b).max() <= rel * max(np.abs(b).max(), 1e-3) + ab, fld
+    for s in sims:
+        s.close()
+    g.close()

@@ -423,3 +423,67 @@ def test_ppe_loop_forms_agree(name):
     assert its[1] == its[2] == its[3]
     assert np.array_equal(sims[2].get("PRESSURE"), sims[1].get("PRESSURE"))
     assert np.array_equal(sims[3].get("PRESSURE"), sims[1].get("PRESSURE"))
+
+
+# ------------------------------------------------------------------ reading R32: mean-free Jacobi
+@pytest.mark.parametrize("name", ["tgv2d_f64", "tgv3d_f64", "hydro_f64", "db2d_f64", "tgv3d_f32"])
+def test_mean_free_solve_parity(name):
+    """ppe_mean_free = 1 (R32): every iterate has the live-row mean removed
+    (k_mean_fix; fused first sweep included).  A tight tolerance runs well into
+    the regime where plain Jacobi drifts on the periodic cases."""
+    case = CASES[name]
+    prec = _prec(case)
+    over = {"ppe_mean_free": 1}
+    sim = gpu_sim(case, **over)
+    o = oracle_from_gpu(case, sim, params=over)
+    sim.predict(case.dt)
+    o.predict(case.dt)
+    tol, mx = (1e-7, 400) if prec == 64 else (0.0, 9)
+    it_g, res_g = sim.ppe_solve(tol, mx)
+    it_o, res_o, _ = o.solve(tol, mx)
+    if prec == 64 and abs(res_o - tol) > 1e-9 * tol:
+        assert it_g == it_o, (it_g, it_o, res_g, res_o)
+        assert res_g == pytest.approx(res_o, rel=1e-6, abs=1e-14)
+    assert_close("p", sim.get("PRESSURE"), o.get("p"), prec)
+    f = case.tag == 0
+    live = f & (sim.get("FREE_SURFACE") == 0)
+    p = sim.get("PRESSURE")
+    assert abs(p[live].mean()) <= 1e-9 * np.abs(p[live]).max() * (1 if prec == 64 else 1e5)
+
+
+@pytest.mark.parametrize("name", ["tgv2d_f64", "db3d_f32"])
+def test_mean_free_loop_forms_agree(name):
+    """Host batches and the graph WHILE node (whose body ends with k_mean_fix
+    setting the condition) run identical kernels: bitwise-equal results; the
+    persistent form falls back to the graph for mean-free."""
+    case = CASES[name]
+    sims = {m: gpu_sim(case, ppe_loop=m, ppe_mean_free=1) for m in (1, 2, 3)}
+    for _ in range(3):
+        r = {m: s.step(case.dt) for m, s in sims.items()}
+        assert r[1].iters == r[2].iters == r[3].iters
+        assert r[1].residual == r[2].residual == r[3].residual
+    for fld in ("PRESSURE", "VELOCITY", "POSITION"):
+        ref = sims[1].get(fld)
+        assert np.array_equal(sims[2].get(fld), ref)
+        assert np.array_equal(sims[3].get(fld), ref)
+
+
+def test_mean_free_steps_parity_resynced():
+    case = CASES["tgv2d_f64"]
+    over = {"ppe_mean_free": 1, "tol": 1e-6}
+    sim = gpu_sim(case, **over)
+    o = oracle_from_gpu(case, sim, params=over)
+    f = case.tag == 0
+    for s in range(3):
+        resync(case, sim, o)
+        sim.predict(case.dt)
+        o.predict(case.dt)
+        it_g, _ = sim.ppe_solve(1e-6, 500)
+        it_o, res_o, _ = o.solve(1e-6, 500)
+        if abs(res_o - 1e-6) > 1e-9 * 1e-6:
+            assert it_g == it_o, (s, it_g, it_o)
+        sim.correct(case.dt)
+        o.correct(case.dt)
+        assert_close(f"p step {s}", sim.get("PRESSURE")[f], o.get("p")[f], 64)
+        assert_close(f"u step {s}", sim.get("VELOCITY")[f], o.get("u")[f], 64,
+                     scale=max(np.abs(o.get("u")[f]).max(), 1e-3))
