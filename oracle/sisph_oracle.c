@@ -304,6 +304,8 @@ struct or_sim {
     int64_t n;
     int32_t* tag;
     double *x, *u, *ut, *m, *rho, *p;   /* state; u of a wall = its ghost velocity */
+    double* uw;                         /* prescribed wall velocity u_i of eq:vg-adami (walls; 0 fluid) */
+    int pref_set;                       /* R33: p_ref already taken */
     double *xs, *us;                    /* r*, u* (walls: xs = x, us = wall u*) */
     double *rhs, *diag, *fs;            /* PPE scratch */
     double* nrm;                        /* wall unit normals */
@@ -442,7 +444,7 @@ or_sim* or_create(const or_cfg* c, int64_t n, const double* x3, const double* u3
     s->xs = dalloc(3 * n); s->us = dalloc(3 * n); s->nrm = dalloc(3 * n); s->xk = dalloc(3 * n);
     s->m = dalloc(n); s->rho = dalloc(n); s->p = dalloc(n);
     s->rhs = dalloc(n); s->diag = dalloc(n); s->fs = dalloc(n);
-    s->anp = dalloc(3 * n); s->ftot = dalloc(3 * n);
+    s->anp = dalloc(3 * n); s->ftot = dalloc(3 * n); s->uw = dalloc(3 * n);
     memcpy(s->x, x3, (size_t)(3 * n) * sizeof(double));
     memcpy(s->xs, x3, (size_t)(3 * n) * sizeof(double));
     memcpy(s->u, u3, (size_t)(3 * n) * sizeof(double));
@@ -450,8 +452,14 @@ or_sim* or_create(const or_cfg* c, int64_t n, const double* x3, const double* u3
     memcpy(s->m, m, (size_t)n * sizeof(double));
     memcpy(s->rho, rho, (size_t)n * sizeof(double));
     if (p) memcpy(s->p, p, (size_t)n * sizeof(double));
+    /* a wall's creation velocity is its physical velocity (eq:vg-adami);
+     * walls never move (R24): a moving lid slides along itself */
     for (int64_t i = 0; i < n; i++)
-        if (tag[i] == WALL) for (int a = 0; a < 3; a++) s->ut[3 * i + a] = 0.0;
+        if (tag[i] == WALL)
+            for (int a = 0; a < 3; a++) {
+                s->uw[3 * i + a] = u3[3 * i + a];
+                s->ut[3 * i + a] = 0.0;
+            }
     csr_build(s, 0, s->x, 0, NULL);
     compute_normals(s);
     return s;
@@ -465,7 +473,7 @@ void or_destroy(or_sim* s)
     free(s->tag); free(s->x); free(s->u); free(s->ut); free(s->xs); free(s->us);
     free(s->nrm); free(s->xk); free(s->m); free(s->rho); free(s->p);
     free(s->rhs); free(s->diag); free(s->fs);
-    free(s->anp); free(s->ftot);
+    free(s->anp); free(s->ftot); free(s->uw);
     free(s);
 }
 
@@ -486,6 +494,7 @@ static double* field_ptr(or_sim* s, const char* f, int* ncomp)
     if (!strcmp(f, "diag")) return s->diag;
     if (!strcmp(f, "fs")) return s->fs;
     if (!strcmp(f, "ftot")) { *ncomp = 3; return s->ftot; }
+    if (!strcmp(f, "uwall")) { *ncomp = 3; return s->uw; }
     if (!strcmp(f, "lambda")) return &s->lambda;
     return NULL;
 }
@@ -537,7 +546,8 @@ void or_pass_density(or_sim* s)
     }
 }
 
-/* Shepard average of a fluid vector field with W(r, h/2) (eq:vf) */
+/* Shepard average of a fluid vector field with W(r, h/2) (eq:vf);
+ * no fluid within the support: the wall's own velocity (reading R15a) */
 static void shepard_half(or_sim* s, const csr_t* b, const double* xpos, const double* f,
                          int64_t i, double* out)
 {
@@ -552,11 +562,12 @@ static void shepard_half(or_sim* s, const csr_t* b, const double* xpos, const do
         for (int a = 0; a < c->dim; a++) acc[a] += f[3 * j + a] * w;
         sw += w;
     }
-    for (int a = 0; a < 3; a++) out[a] = sw > 0.0 ? acc[a] / sw : 0.0;
+    for (int a = 0; a < 3; a++) out[a] = sw > 0.0 ? acc[a] / sw : s->uw[3 * i + a];
 }
 
 /* Ghost velocity (eq:vf, eq:vg-adami, eq:vg-no-normal, R15):
- * u_w = 2 u_wall - Shepard_{h/2}(u_f), u_wall = 0, then clip. */
+ * u_w = 2 u_wall - Shepard_{h/2}(u_f) with u_wall the wall's prescribed
+ * velocity (s->uw), then clip. */
 void or_pass_ghost_velocity(or_sim* s)
 {
     const or_cfg* c = &s->c;
@@ -565,7 +576,8 @@ void or_pass_ghost_velocity(or_sim* s)
         if (s->tag[i] != WALL) continue;
         double ut[3];
         shepard_half(s, &s->nb[0], s->x, s->u, i, ut);
-        double uw[3] = {-ut[0], -ut[1], -ut[2]};
+        const double* uwall = s->uw + 3 * i;
+        double uw[3] = {2.0 * uwall[0] - ut[0], 2.0 * uwall[1] - ut[1], 2.0 * uwall[2] - ut[2]};
         clip_normal(c->dim, uw, s->nrm + 3 * i);
         for (int a = 0; a < 3; a++) s->u[3 * i + a] = a < c->dim ? uw[a] : 0.0;
     }
@@ -649,7 +661,7 @@ static void pass_wall_ustar(or_sim* s)
         double ut[3];
         shepard_half(s, &s->nb[1], s->xs, s->us, i, ut);
         double uw[3];
-        for (int a = 0; a < 3; a++) uw[a] = c->ustar_noslip ? -ut[a] : ut[a];
+        for (int a = 0; a < 3; a++) uw[a] = c->ustar_noslip ? 2.0 * s->uw[3 * i + a] - ut[a] : ut[a];
         clip_normal(c->dim, uw, s->nrm + 3 * i);
         for (int a = 0; a < 3; a++) s->us[3 * i + a] = a < c->dim ? uw[a] : 0.0;
     }
@@ -857,6 +869,15 @@ void or_correct(or_sim* s, double dt)
         }
     }
     s->stepped = 1;
+    if (c->pref_auto && !s->pref_set) {
+        /* reading R33: internal flows take p_ref = 2 max(p_i) "after the first iteration"
+         * -- here: over the fluid, from this first solve */
+        double mx = -INFINITY;
+        for (int64_t i = 0; i < n; i++)
+            if (s->tag[i] == FLUID && s->p[i] > mx) mx = s->p[i];
+        s->c.p_ref = n > 0 && mx > -INFINITY ? 2.0 * mx : 0.0;
+        s->pref_set = 1;
+    }
     /* GTVF background pressure p0 (R22) and K sub-steps */
     double* p0 = dalloc(n);
     for (int64_t i = 0; i < n; i++) {

@@ -214,6 +214,86 @@ def dambreak2d(nx: int = 500, ny: int = 1000, dx: float = 0.002, tank: float = 4
 
 
 # --------------------------------------------------------------------------
+# NEXT-4 moving walls: plane Couette flow and the lid-driven cavity
+# --------------------------------------------------------------------------
+def couette_velocity(y, t, U, H, nu, terms: int = 200):
+    """Start-up plane Couette flow, lower plate at rest, upper plate impulsively
+    moved at U (a textbook closed form; the test's reference, not part of the
+    method): u(y, t) = U y/H - (2U/pi) sum_n (-1)^(n+1)/n sin(n pi y/H) exp(-n^2 pi^2 nu t/H^2)."""
+    y = np.asarray(y, np.float64)
+    u = U * y / H
+    for k in range(1, terms + 1):
+        u -= 2.0 * U / np.pi * (-1) ** (k + 1) / k * np.sin(k * np.pi * y / H) * np.exp(
+            -(k * np.pi) ** 2 * nu * t / (H * H))
+    return u
+
+
+def couette(nx: int = 10, ny: int = 20, H: float = 1.0, U: float = 1.0, re: float = 10.0,
+            layers: int = 3, steps: int = 100, tol: float = 1e-3, K: int = 10,
+            precision: int = 64) -> Case:
+    """Channel of height H = ny dx between two wall blocks of `layers` rows,
+    periodic in x (length nx dx); the upper wall moves at +U along x (its
+    creation velocity is its prescribed velocity, eq:vg-adami P:845-846), the
+    lower wall is at rest; fluid at rest, p = 0, no body force.  Internal flow:
+    symm gradient without GTVF (p_ref = 0: P:1244-1246 says "symm" works
+    without it), no-slip u* on the walls."""
+    rho0 = 1.0
+    dx = H / ny
+    h = dx
+    nu = U * H / re
+    L = nx * dx
+    fluid = _lattice((nx, ny), dx, (0.0, 0.0))
+    xs = (np.arange(nx) + 0.5) * dx
+    low = [np.stack([xs, np.full_like(xs, -(l + 0.5) * dx)], 1) for l in range(layers)]
+    top = [np.stack([xs, np.full_like(xs, H + (l + 0.5) * dx)], 1) for l in range(layers)]
+    wall = np.concatenate(low + top)
+    x = np.concatenate([fluid, wall])
+    nf, nw = fluid.shape[0], wall.shape[0]
+    tag = np.concatenate([np.zeros(nf, np.int32), np.ones(nw, np.int32)])
+    u = np.zeros((nf + nw, 2))
+    u[nf + nw // 2:, 0] = U                      # the upper wall block slides at U
+    dt = min(0.25 * h / U, 0.25 * h * h / nu)    # PAPER.md:655-673
+    params = default_params(rho0=rho0, nu=nu, pgrad=PGRAD_SYMM, h_tilde_factor=1.0, pref_external=0,
+                            p_ref=0.0, ustar_noslip=1, tol=tol, K=K, precision=precision)
+    lo = [0.0, -(layers + 0.5) * dx, 0.0]
+    hi = [L, H + (layers + 0.5) * dx, 0.0]
+    n = nf + nw
+    return Case("couette", 2, h, dx, dt, steps, lo, hi, [1, 0, 0], x, u,
+                np.full(n, rho0 * dx * dx), np.full(n, rho0), np.zeros(n), tag, params)
+
+
+def cavity(n: int = 50, re: float = 100.0, U: float = 1.0, layers: int = 3, t_end: float = 10.0,
+           tol: float = 1e-2, K: int = 10, precision: int = 64, ustar_noslip: int = 0) -> Case:
+    """Lid-driven cavity (§4.3): unit square of n x n fluid
+    particles, h/dx = 1, Re = U L / nu; the lid (every wall particle above the
+    fluid, corners included) moves at +U along x, the other walls are at rest.
+    Internal flow: symm gradient, GTVF with p_ref = 2 max(p_i) after the first
+    solve (reading R33); u* slip by default."""
+    rho0, L = 1.0, 1.0
+    dx = L / n
+    h = dx
+    nu = U * L / re
+    fluid, wall = _tank2d(n, n, n, n, layers, dx)
+    xs = (np.arange(-layers, n + layers) + 0.5) * dx
+    lid = np.concatenate([np.stack([xs, np.full_like(xs, L + (l + 0.5) * dx)], 1) for l in range(layers)])
+    wall = np.concatenate([wall, lid])
+    x = np.concatenate([fluid, wall])
+    nf, nw = fluid.shape[0], wall.shape[0]
+    tag = np.concatenate([np.zeros(nf, np.int32), np.ones(nw, np.int32)])
+    u = np.zeros((nf + nw, 2))
+    u[nf + nw - lid.shape[0]:, 0] = U
+    dt = min(0.25 * h / U, 0.25 * h * h / nu)
+    params = default_params(rho0=rho0, nu=nu, pgrad=PGRAD_SYMM, h_tilde_factor=1.0, pref_external=0,
+                            p_ref=0.0, pref_auto=1, ustar_noslip=ustar_noslip, tol=tol, K=K,
+                            precision=precision)
+    lo = [-(layers + 0.5) * dx, -(layers + 0.5) * dx, 0.0]
+    hi = [L + (layers + 0.5) * dx, L + (layers + 0.5) * dx, 0.0]
+    nn = nf + nw
+    return Case("cavity", 2, h, dx, dt, int(round(t_end / dt)), lo, hi, [0, 0, 0], x, u,
+                np.full(nn, rho0 * dx * dx), np.full(nn, rho0), np.zeros(nn), tag, params)
+
+
+# --------------------------------------------------------------------------
 # C4  3D Taylor-Green vortex (BASELINE configs[3])
 # --------------------------------------------------------------------------
 def tgv3d(n: int = 128, re: float = 100.0, jitter: float = 0.05, seed: int = 104,

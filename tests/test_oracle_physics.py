@@ -402,3 +402,83 @@ def test_mean_free_jacobi_removes_the_drift(orc):
     case.params["ppe_mean_free"] = 0
     assert res[1] < 1e-3 * res[0]
     assert np.abs(pres[1] - pres[0]).max() < 2e-2 * np.abs(pres[1]).max()
+
+
+# ---------------------------------------------------------------- NEXT-4: moving walls
+def test_ghost_velocity_of_a_moving_wall(orc):
+    # eq:vg-adami: u_w = 2 u_wall - Shepard(u_f).  Fluid at rest -> the first
+    # layer of the sliding block (fluid within 3 h/2) gets exactly 2U along the wall (the clip
+    # only removes into-solid normal components; this one is tangential); the outer layers see
+    # no fluid and keep u_wall (R15a); the resting wall stays exactly 0.
+    case = synth.couette(nx=8, ny=10, U=0.7)
+    s = orc.Sim(case)
+    s.density()
+    s.ghost_velocity()
+    u = s.get("u")
+    w = np.flatnonzero(case.tag == 1)
+    top = w[case.x[w, 1] > 0.5]
+    low = w[case.x[w, 1] < 0.5]
+    first = top[case.x[top, 1] < 1.0 + case.dx]
+    outer = top[case.x[top, 1] > 1.0 + case.dx]
+    assert len(first) == 8 and len(outer) == 16
+    # (the into-solid clip of eq:vg-no-normal sees u_w.n ~ 1e-16 from rounding in n)
+    assert np.abs(u[first, 0] - 1.4).max() < 1e-12
+    assert np.abs(u[outer, 0] - 0.7).max() < 1e-12
+    assert np.abs(u[top, 1]).max() < 1e-12
+    assert np.all(u[low] == 0.0)
+    assert np.array_equal(s.get("uwall")[top, 0], np.full(len(top), 0.7))
+
+
+def test_uniform_flow_between_walls_moving_with_it_stays_uniform(orc):
+    # a uniform stream between two walls sliding at the same velocity is the resting
+    # state seen from a moving frame: no shear, no divergence, p stays 0
+    case = synth.couette(nx=8, ny=12, U=0.9)
+    case.u[:, 0] = 0.9
+    s = orc.Sim(case)
+    for _ in range(4):
+        s.step(case.dt)
+    f = case.tag == 0
+    u = s.get("u")
+    assert np.abs(u[f, 0] - 0.9).max() < 1e-12
+    assert np.abs(u[f, 1]).max() < 1e-12
+    assert np.abs(s.get("p")[f]).max() < 1e-9
+
+
+@pytest.mark.parametrize("t_end", [1.0, 4.0])
+def test_couette_start_up_matches_the_closed_form(orc, t_end):
+    # impulsively started plane Couette flow (Re = U H / nu = 10, 20 particles across):
+    # the series solution decays to the linear profile U y / H.  A wrong factor in
+    # eq:vg-adami (u_w = U - u~, or + u~) or a wrong sign of the viscous term moves the
+    # profile by tens of percent of U.
+    case = synth.couette(nx=10, ny=20, re=10.0)
+    s = orc.Sim(case)
+    steps = int(round(t_end / case.dt))
+    for _ in range(steps):
+        s.step(case.dt)
+    f = case.tag == 0
+    x, u = s.get("x"), s.get("u")
+    ue = synth.couette_velocity(x[f, 1], steps * case.dt, 1.0, 1.0, case.params["nu"])
+    err = np.abs(u[f, 0] - ue)
+    assert err.max() < 0.01
+    assert err.mean() < 0.005
+    assert np.abs(u[f, 1]).max() < 1e-3
+
+
+def test_pref_auto_takes_twice_the_first_solve_max(orc):
+    # R33: p_ref = 2 max(p_i) over fluid after the first solve, then constant
+    case = synth.cavity(n=16, t_end=0.1)
+    a = orc.Sim(case)
+    a.predict(case.dt)
+    a.solve(case.params["tol"], case.params["max_iter"])
+    pmax = a.get("p")[case.tag == 0].max()
+    a.correct(case.dt)
+    case2 = synth.cavity(n=16, t_end=0.1)
+    case2.params.update(pref_auto=0, p_ref=2.0 * pmax)
+    b = orc.Sim(case2)
+    b.step(case.dt)
+    for _ in range(3):
+        a.step(case.dt)
+        b.step(case.dt)
+    assert pmax > 0
+    assert np.array_equal(a.get("x"), b.get("x"))
+    assert np.array_equal(a.get("u"), b.get("u"))
