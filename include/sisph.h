@@ -97,6 +97,9 @@ typedef struct {
                                a PPE with no Dirichlet row (fully periodic / enclosed flows, whose
                                operator has the constant null space: eq:coeff rows sum to zero).
                                0 (default) = eq:p-sor as printed.  Not with ppe_loop = 3. */
+    int pref_auto;          /* reading R33: 1 = the GTVF background pressure p_ref is set to
+                               2 max_i p_i over fluid from the handle's first solve (internal
+                               flows), then kept; 0 (default) = p_ref as given */
 } sisph_params;
 
 /* Per-step report (sisph_step).  Timings are device milliseconds measured
@@ -132,7 +135,12 @@ typedef enum {
     SISPH_FIELD_DIAG = 9,               /* n; D_ii of eq:coeff (walls: 0) */
     SISPH_FIELD_NORMAL = 10,            /* n x dim; wall unit normals (fluid: 0) */
     SISPH_FIELD_FREE_SURFACE = 11,      /* n; 1 if free-surface fluid particle */
-    SISPH_FIELD_TAG = 12                /* n; 0 fluid, 1 wall (read only) */
+    SISPH_FIELD_TAG = 12,               /* n; 0 fluid, 1 wall (read only) */
+    SISPH_FIELD_WALL_VELOCITY = 13      /* n x dim; the prescribed (physical) velocity u_i of a wall
+                                           in eq:vg-adami, initially the creation
+                                           velocity of the wall particle (fluid: 0; set ignores
+                                           fluid entries).  Walls never move (R24): a sliding
+                                           wall (a lid) moves along itself */
 } sisph_field;
 
 /* Fill *p with the paper's defaults (precision 64, omega 0.5, eta 0.01,

@@ -18,6 +18,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <chrono>
 #include <condition_variable>
 #include <cstring>
 #include <mutex>
@@ -149,27 +150,41 @@ struct LocalHub {
     std::condition_variable cv;
     int arrived = 0;
     long generation = 0;
+    bool aborted = false;   // a rank gave up waiting: every later barrier fails at once
     // per rank, per face: posted send buffer / size
     std::vector<const void*> sptr;
     std::vector<size_t> ssz;
     std::vector<double*> rptr;
     explicit LocalHub(int n) : nranks(n), sptr(2 * n), ssz(2 * n), rptr(n) {}
-    void barrier()
+    // false if a rank did not arrive within the timeout (it failed: its
+    // caller reports the error instead of hanging) or the hub was aborted
+    bool barrier()
     {
         std::unique_lock<std::mutex> lk(mu);
+        if (aborted) return false;
         long g = generation;
         if (++arrived == nranks) {
             arrived = 0;
             generation++;
             cv.notify_all();
-        } else {
-            cv.wait(lk, [&] { return generation != g; });
+            return true;
         }
+        if (!cv.wait_for(lk, std::chrono::seconds(120), [&] { return generation != g || aborted; }) || aborted) {
+            aborted = true;
+            cv.notify_all();
+            return false;
+        }
+        return true;
     }
 };
 
 struct LocalTransport : Transport {
     LocalHub* hub = nullptr;
+    int fail_barrier()
+    {
+        err = "local transport: another rank did not reach the exchange (it failed or hung)";
+        return 1;
+    }
     int sync(cudaStream_t st)
     {
         cudaError_t e = cudaStreamSynchronize(st);
@@ -187,7 +202,7 @@ struct LocalTransport : Transport {
             hub->sptr[2 * rank + f] = nb[f] >= 0 ? sbuf[f] : nullptr;
             hub->ssz[2 * rank + f] = nb[f] >= 0 ? sn[f] : 0;
         }
-        hub->barrier();
+        if (!hub->barrier()) return fail_barrier();
         int rc = 0;
         for (int f = 0; f < 2 && !rc; f++) {
             if (nb[f] < 0 || rn[f] == 0) continue;
@@ -205,7 +220,7 @@ struct LocalTransport : Transport {
             }
         }
         if (!rc) rc = sync(st);
-        hub->barrier();   // senders' buffers stay valid until every copy is done
+        if (!hub->barrier()) return fail_barrier();   // senders' buffers stay valid until every copy is done
         return rc;
     }
     int allreduce(double* buf, int count, int op, cudaStream_t st) override
@@ -213,7 +228,7 @@ struct LocalTransport : Transport {
         if (nranks == 1) return 0;
         if (sync(st)) return 1;
         hub->rptr[rank] = buf;
-        hub->barrier();
+        if (!hub->barrier()) return fail_barrier();
         // every rank reduces all ranks' values in rank order (identical bits everywhere)
         std::vector<double> acc(count), tmp(count);
         int rc = 0;
@@ -225,7 +240,7 @@ struct LocalTransport : Transport {
             for (int q = 0; q < count; q++)
                 acc[q] = r == 0 ? tmp[q] : (op == 0 ? acc[q] + tmp[q] : (tmp[q] > acc[q] ? tmp[q] : acc[q]));
         }
-        hub->barrier();   // all reads done before anyone overwrites its buffer
+        if (!hub->barrier()) return fail_barrier();   // all reads done before anyone overwrites its buffer
         if (!rc && cudaMemcpy(buf, acc.data(), count * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess) {
             err = "local transport: allreduce write-back failed";
             rc = 1;

@@ -116,6 +116,10 @@ template <class T, int D> struct Engine : EngineBase {
     // device state
     V *pos = nullptr, *pos_alt = nullptr, *vel = nullptr, *vel_alt = nullptr, *us = nullptr, *us_alt = nullptr;
     V *vt = nullptr, *vt_alt = nullptr, *rn = nullptr, *rstar = nullptr, *nrm = nullptr, *nstmp = nullptr;
+    V* uwl = nullptr;         // prescribed wall velocity per relative wall slot (eq:vg-adami)
+    bool uwl_set = false;     // uwl holds the walls' values (after the first wall sort)
+    int pref_auto = 0;        // R33: p_ref from the first solve
+    bool pref_done = false;
     V *rkA = nullptr, *rkB = nullptr, *vk = nullptr, *dk = nullptr;
     V* fnp = nullptr;       // non-pressure acceleration of A8 (adaptive dt)
     int* dcnt_w = nullptr;  // device flag of set_field's wall check
@@ -174,7 +178,7 @@ template <class T, int D> struct Engine : EngineBase {
 
     ~Engine() override
     {
-        void* ptrs[] = {pos, pos_alt, vel, vel_alt, us, us_alt, vt, vt_alt, rn, rstar, nrm, nstmp, rkA, rkB, vk, dk,
+        void* ptrs[] = {pos, pos_alt, vel, vel_alt, us, us_alt, vt, vt_alt, rn, rstar, nrm, nstmp, uwl, rkA, rkB, vk, dk,
                         p, p_alt, rho, rho_alt, rhs, diag, fs, fs_alt, pid, pid_alt, keys, rank, perm0, perm,
                         ccount, fstart, wstart, bsum, nbr, cnt, ctl, partials, dtmp, nbr_in, cnt_in,
                         nbs, cnt_s, wperm_s, wstart_s, coef, dflag, dflag2, dpre, dlist[0], dlist[1], dlist[2],
@@ -314,6 +318,7 @@ template <class T, int D> struct Engine : EngineBase {
         matrix_free = prm->matrix_free;
         ppe_loop = prm->ppe_loop;
         P.mean_free = prm->ppe_mean_free ? 1 : 0;
+        pref_auto = prm->pref_auto;
         for (int a = 0; a < D; a++) extent = std::max(extent, std::max(fabs(dom->lo[a]), fabs(dom->hi[a])));
         min_iter = prm->min_iter;
         max_iter = prm->max_iter;
@@ -359,7 +364,7 @@ template <class T, int D> struct Engine : EngineBase {
     ptr = dalloc<Ty>((cntx), err, rc);       \
     if (rc) return rc;
         AL(pos, V, NT) AL(pos_alt, V, NT) AL(vel, V, NT) AL(vel_alt, V, NT) AL(us, V, NT) AL(us_alt, V, NT)
-        AL(vt, V, NF) AL(vt_alt, V, NF) AL(rn, V, NT) AL(rstar, V, NT) AL(nrm, V, NW) AL(nstmp, V, NW)
+        AL(vt, V, NF) AL(vt_alt, V, NF) AL(rn, V, NT) AL(rstar, V, NT) AL(nrm, V, NW) AL(nstmp, V, NW) AL(uwl, V, NW)
         AL(rkA, V, NT) AL(rkB, V, NT) AL(vk, V, NF) AL(dk, V, NF) AL(fnp, V, NF) AL(dcnt_w, int, 4)
         AL(p, T, NT) AL(p_alt, T, NT) AL(rho, T, NT) AL(rho_alt, T, NT) AL(rhs, T, NF) AL(diag, T, NF)
         AL(fs, uint8_t, NF) AL(fs_alt, uint8_t, NF) AL(pid, int, NT) AL(pid_alt, int, NT)
@@ -384,6 +389,7 @@ template <class T, int D> struct Engine : EngineBase {
         SCK(cudaMemsetAsync(us, 0, NT * sizeof(V), st));
         SCK(cudaMemsetAsync(us_alt, 0, NT * sizeof(V), st));
         SCK(cudaMemsetAsync(nrm, 0, NW * sizeof(V), st));
+        SCK(cudaMemsetAsync(uwl, 0, NW * sizeof(V), st));
         SCK(cudaMemsetAsync(rhs, 0, NF * sizeof(T), st));
         SCK(cudaMemsetAsync(diag, 0, NF * sizeof(T), st));
         // ------------------------------------------------ upload (fluid, then owned walls, given order)
@@ -952,7 +958,11 @@ template <class T, int D> struct Engine : EngineBase {
             gl_add(G, rho + Nf, rho_alt + Nf, sizeof(T), Nw);
             gl_add(G, pid + Nf, pid_alt + Nf, sizeof(int), Nw);
             gl_add(G, p + Nf, p_alt + Nf, sizeof(T), Nw);
+            if (uwl_set) gl_add(G, uwl, nstmp, sizeof(V), Nw);   // re-sort: carry the prescribed velocities
             SRET(gather(G, wp, Nw));
+            // first sort: the walls' creation velocities are their prescribed velocities
+            SCK(cudaMemcpyAsync(uwl, uwl_set ? nstmp : vel_alt + Nf, Nw * sizeof(V), cudaMemcpyDeviceToDevice, st));
+            uwl_set = true;
             SCK(cudaMemcpyAsync(pos + Nf, pos_alt + Nf, Nw * sizeof(V), cudaMemcpyDeviceToDevice, st));
             SCK(cudaMemcpyAsync(vel + Nf, vel_alt + Nf, Nw * sizeof(V), cudaMemcpyDeviceToDevice, st));
             SCK(cudaMemcpyAsync(rho + Nf, rho_alt + Nf, Nw * sizeof(T), cudaMemcpyDeviceToDevice, st));
@@ -1156,7 +1166,7 @@ template <class T, int D> struct Engine : EngineBase {
             }
         }
         // A7
-        if (Nwo) ++nlaunch, k_wall_velocity<T, D><<<nblk(Nwo, 256), 256, 0, st>>>(P, pos, nb1, cn1, cap1, nrm, rho, vel, 0);
+        if (Nwo) ++nlaunch, k_wall_velocity<T, D><<<nblk(Nwo, 256), 256, 0, st>>>(P, pos, nb1, cn1, cap1, nrm, rho, uwl, vel, 0);
         SCK(cudaGetLastError());
         if (dist()) {
             PackList W{};
@@ -1204,7 +1214,7 @@ template <class T, int D> struct Engine : EngineBase {
             SRET(build_list_grow(true));   // + GTVF inner list
         }
         // A10
-        if (Nwo) ++nlaunch, k_wall_velocity<T, D><<<nblk(Nwo, 256), 256, 0, st>>>(P, pos, nbr, cnt, P.cap, nrm, rho, us, P.ustar_noslip ? 0 : 1);
+        if (Nwo) ++nlaunch, k_wall_velocity<T, D><<<nblk(Nwo, 256), 256, 0, st>>>(P, pos, nbr, cnt, P.cap, nrm, rho, uwl, us, P.ustar_noslip ? 0 : 1);
         SCK(cudaGetLastError());
         if (dist()) {
             PackList W{};
@@ -1525,6 +1535,20 @@ template <class T, int D> struct Engine : EngineBase {
             SRET(halo_walls(W));
         }
         SCK(cudaMemsetAsync(&ctl->fmax2_bits, 0, 2 * sizeof(unsigned long long), st));
+        if (pref_auto && !pref_done) {
+            // R33: p_ref = 2 max p over the fluid of this first solve (all ranks), then constant
+            double* dm = reinterpret_cast<double*>(&ctl->red[3]);
+            ++nlaunch, k_fluid_pmax<T><<<1, 1024, 0, st>>>(p, Nfo, dm);
+            SCK(cudaGetLastError());
+            if (dist()) SRET(xallreduce(dm, 1, 1));
+            double mx = 0;
+            SCK(cudaMemcpyAsync(&mx, dm, sizeof(double), cudaMemcpyDeviceToHost, st));
+            SCK(cudaStreamSynchronize(st));
+            const double pr = std::isfinite(mx) ? 2.0 * mx : 0.0;
+            P.p_ref = (T)pr;
+            PS.p_ref = (T)pr;
+            pref_done = true;
+        }
         if (Nfo) ++nlaunch, k_pgrad_correct<T, D><<<nblk(Nfo, 128), 128, 0, st>>>(P, (T)dt, pos, rho, p, us, nbr, cnt, P.cap, vel, fnp, ctl);
         // A14: K sub-steps (p0 = 0 everywhere when p_ref == 0: the shift is exactly zero)
         const V* rK = nullptr;   // GTVF displacement r^K - r^0 (none when p0 = 0)
@@ -1612,7 +1636,8 @@ template <class T, int D> struct Engine : EngineBase {
             case SISPH_FIELD_TRANSPORT_VELOCITY:
             case SISPH_FIELD_USTAR:
             case SISPH_FIELD_RSTAR:
-            case SISPH_FIELD_NORMAL: return D;
+            case SISPH_FIELD_NORMAL:
+            case SISPH_FIELD_WALL_VELOCITY: return D;
             case SISPH_FIELD_PRESSURE:
             case SISPH_FIELD_DENSITY:
             case SISPH_FIELD_MASS:
@@ -1669,6 +1694,9 @@ template <class T, int D> struct Engine : EngineBase {
                 break;
             case SISPH_FIELD_NORMAL:
                 if (Nwo) ++nlaunch, k_to_ids_vec<T><<<nblk(Nwo, B), B, 0, st>>>(nrm, pid + Nf, Nwo, D, dtmp);
+                break;
+            case SISPH_FIELD_WALL_VELOCITY:
+                if (Nwo) ++nlaunch, k_to_ids_vec<T><<<nblk(Nwo, B), B, 0, st>>>(uwl, pid + Nf, Nwo, D, dtmp);
                 break;
             case SISPH_FIELD_PRESSURE:
                 sc(p, 0, Nfo);
@@ -1744,6 +1772,10 @@ template <class T, int D> struct Engine : EngineBase {
                 break;
             case SISPH_FIELD_NORMAL:
                 if (Nwo) ++nlaunch, k_from_ids_vec<T><<<nblk(Nwo, B), B, 0, st>>>(dtmp, pid + Nf, Nwo, D, nrm, 0);
+                break;
+            case SISPH_FIELD_WALL_VELOCITY:
+                // owned walls (ghost walls take their ghost velocities from the owner's halo)
+                if (Nwo) ++nlaunch, k_from_ids_vec<T><<<nblk(Nwo, B), B, 0, st>>>(dtmp, pid + Nf, Nwo, D, uwl, 0);
                 break;
             case SISPH_FIELD_PRESSURE:
                 sc(p, 0, Nfo);

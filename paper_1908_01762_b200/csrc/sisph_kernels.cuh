@@ -815,7 +815,8 @@ template <class T, int D>
 __global__ void __launch_bounds__(256) k_wall_velocity(Params<T> P, const V4<T>* __restrict__ pos,
                                                        const int* __restrict__ nbr, const int* __restrict__ cnt, int ncap,
                                                        const V4<T>* __restrict__ nrm, const T* __restrict__ rho,
-                                                       V4<T>* __restrict__ vel, int mode)
+                                                       const V4<T>* __restrict__ uwl, V4<T>* __restrict__ vel,
+                                                       int mode)
 {
     int w = blockIdx.x * blockDim.x + threadIdx.x;
     if (w >= P.Nwo) return;
@@ -837,16 +838,19 @@ __global__ void __launch_bounds__(256) k_wall_velocity(Params<T> P, const V4<T>*
         if (D == 3) az += uj.z * wv;
         sw += wv;
     });
-    T ux = 0, uy = 0, uz = 0;
+    // eq:vg-adami with the wall's prescribed velocity u_wall (uwl); an empty
+    // Shepard sum gives u~ = u_wall (R15a)
+    const V4<T> uw = ld4(uwl + w);
+    T ux = uw.x, uy = uw.y, uz = D == 3 ? uw.z : T(0);
     if (sw > 0) {
         ux = ax / sw;
         uy = ay / sw;
         uz = D == 3 ? az / sw : T(0);
     }
     if (mode == 0) {
-        ux = -ux;
-        uy = -uy;
-        uz = -uz;
+        ux = T(2) * uw.x - ux;
+        uy = T(2) * uw.y - uy;
+        uz = D == 3 ? T(2) * uw.z - uz : T(0);
     }
     V4<T> nn = ld4(nrm + w);
     T un = ux * nn.x + uy * nn.y;
@@ -1435,6 +1439,23 @@ __global__ void __launch_bounds__(SWEEP_T) k_mean_fix(Params<T> P, const PpeDesc
         const int done = ((k1 >= dsc->min_it && res < dsc->tol) || k1 >= dsc->max_it || ctl->nonfinite) ? 1 : 0;
         ctl->done = done;
         if (use_h) cudaGraphSetConditional(hcond, done ? 0u : 1u);
+    }
+}
+
+// R33: max_i p_i over the owned fluid (one block, fixed order; once per handle)
+template <class T>
+__global__ void __launch_bounds__(1024) k_fluid_pmax(const T* __restrict__ p, int nf, double* out)
+{
+    __shared__ double sm[32];
+    double m = -INFINITY;
+    for (int i = threadIdx.x; i < nf; i += blockDim.x) m = fmax(m, (double)p[i]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int q = 1; q < (int)(blockDim.x >> 5); q++) m = fmax(m, sm[q]);
+        *out = fmax(m, sm[0]);
     }
 }
 

@@ -19,8 +19,8 @@ ERROR_NAMES = {1: "SISPH_EINVAL", 2: "SISPH_ENOMEM", 3: "SISPH_ECUDA", 4: "SISPH
                5: "SISPH_ENONFINITE", 6: "SISPH_EOVERFLOW"}
 
 FIELDS = dict(POSITION=0, VELOCITY=1, TRANSPORT_VELOCITY=2, PRESSURE=3, DENSITY=4, MASS=5,
-              USTAR=6, RSTAR=7, RHS=8, DIAG=9, NORMAL=10, FREE_SURFACE=11, TAG=12)
-VECTOR_FIELDS = {"POSITION", "VELOCITY", "TRANSPORT_VELOCITY", "USTAR", "RSTAR", "NORMAL"}
+              USTAR=6, RSTAR=7, RHS=8, DIAG=9, NORMAL=10, FREE_SURFACE=11, TAG=12, WALL_VELOCITY=13)
+VECTOR_FIELDS = {"POSITION", "VELOCITY", "TRANSPORT_VELOCITY", "USTAR", "RSTAR", "NORMAL", "WALL_VELOCITY"}
 
 EXPORTED = ["sisph_params_default", "sisph_create", "sisph_destroy", "sisph_build_neighbors",
             "sisph_predict", "sisph_ppe_solve", "sisph_correct", "sisph_step", "sisph_get_field",
@@ -45,6 +45,7 @@ class sisph_params(C.Structure):
         ("tol", C.c_double), ("wall_rho_summation", C.c_int), ("nbr_cap", C.c_int),
         ("device", C.c_int), ("stream", C.c_void_p), ("rebuild_mode", C.c_int),
         ("matrix_free", C.c_int), ("ppe_loop", C.c_int), ("ppe_mean_free", C.c_int),
+        ("pref_auto", C.c_int),
     ]
 
 

@@ -28,6 +28,9 @@ def oracle_from_gpu(case, sim, params=None):
     cfg = oracle.make_cfg(case.dim, case.lo, case.hi, case.periodic, case.h, prm)
     x = sim.get("POSITION")
     u = sim.get("VELOCITY")
+    w = case.tag == 1
+    # a wall's creation velocity is its prescribed velocity (VELOCITY of a wall is its ghost velocity)
+    u[w] = sim.get("WALL_VELOCITY")[w]
     m = sim.get("MASS")
     rho = sim.get("DENSITY")
     p = sim.get("PRESSURE")

@@ -487,3 +487,87 @@ def test_mean_free_steps_parity_resynced():
         assert_close(f"p step {s}", sim.get("PRESSURE")[f], o.get("p")[f], 64)
         assert_close(f"u step {s}", sim.get("VELOCITY")[f], o.get("u")[f], 64,
                      scale=max(np.abs(o.get("u")[f]).max(), 1e-3))
+
+
+# ------------------------------------------------------------------ NEXT-4: moving walls
+def _moving_cases():
+    return {
+        "couette_f64": synth.couette(nx=10, ny=20, re=10.0),
+        "couette_f32": synth.couette(nx=10, ny=20, re=10.0, precision=32),
+        "cavity_slip_f64": synth.cavity(n=24, t_end=0.1),
+        "cavity_noslip_f64": synth.cavity(n=24, t_end=0.1, ustar_noslip=1),
+        "cavity_f32": synth.cavity(n=24, t_end=0.1, precision=32),
+    }
+
+
+@pytest.mark.parametrize("name", list(_moving_cases()))
+def test_moving_wall_step_parity(name):
+    """Sliding walls (eq:vg-adami with u_wall != 0, R15a) and the first-solve
+    background pressure (R33, cavity): resynced full steps vs the oracle."""
+    case = _moving_cases()[name]
+    prec = case.params["precision"]
+    sim = gpu_sim(case)
+    assert np.array_equal(sim.get("WALL_VELOCITY")[case.tag == 1], case.u[case.tag == 1].astype(
+        np.float32 if prec == 32 else np.float64))
+    o = oracle_from_gpu(case, sim)
+    uw = case.u.copy()
+    uw[case.tag == 0] = 0
+    o.set("uwall", uw)
+    f = case.tag == 0
+    over = {} if prec == 64 else {"tol": 0.0, "max_iter": 5}
+    tol = over.get("tol", case.params["tol"])
+    mx = over.get("max_iter", case.params["max_iter"])
+    for s in range(4):
+        resync(case, sim, o)
+        sim.predict(case.dt)
+        o.predict(case.dt)
+        it_g, _ = sim.ppe_solve(tol, mx)
+        it_o, res_o, _ = o.solve(tol, mx)
+        if prec == 64 and abs(res_o - tol) > 1e-9 * tol:
+            assert it_g == it_o, (s, it_g, it_o)
+        sim.correct(case.dt)
+        o.correct(case.dt)
+        w = case.tag == 1
+        assert_close(f"wall u {s}", sim.get("VELOCITY")[w], o.get("u")[w], prec, scale=1.0)
+        assert_close(f"p step {s}", sim.get("PRESSURE")[f], o.get("p")[f], prec,
+                     scale=max(np.abs(o.get("p")[f]).max(), 1e-3))
+        assert_close(f"u step {s}", sim.get("VELOCITY")[f], o.get("u")[f], prec,
+                     scale=max(np.abs(o.get("u")[f]).max(), 1e-3))
+        dxg = sim.get("POSITION")[f] - o.get("x")[f]
+        for a in range(case.dim):
+            if case.periodic[a]:
+                L = case.hi[a] - case.lo[a]
+                dxg[:, a] = (dxg[:, a] + 0.5 * L) % L - 0.5 * L
+        assert_close(f"x step {s}", dxg, np.zeros_like(dxg), prec, scale=1.0)
+
+
+@pytest.mark.parametrize("prec", [64, 32])
+def test_couette_start_up_closed_form_gpu(prec):
+    """The CUDA path against the start-up Couette series (same bound as the oracle's pin)."""
+    case = synth.couette(nx=10, ny=20, re=10.0, precision=prec)
+    sim = gpu_sim(case)
+    steps = int(round(4.0 / case.dt))
+    for _ in range(steps):
+        sim.step(case.dt)
+    f = case.tag == 0
+    x, u = sim.get("POSITION"), sim.get("VELOCITY")
+    ue = synth.couette_velocity(x[f, 1], steps * case.dt, 1.0, 1.0, case.params["nu"])
+    err = np.abs(u[f, 0] - ue)
+    assert err.max() < 0.01 and err.mean() < 0.005
+
+
+def test_wall_velocity_field_roundtrip():
+    case = synth.cavity(n=16, t_end=0.1)
+    sim = gpu_sim(case)
+    uw = np.zeros_like(case.u)
+    w = case.tag == 1
+    uw[w, 0] = np.linspace(-1, 1, w.sum())
+    sim.set("WALL_VELOCITY", uw)
+    assert np.array_equal(sim.get("WALL_VELOCITY"), uw)
+    # the ghost velocity of a wall far from the fluid is its own velocity (R15a)
+    sim.step(case.dt)
+    x = case.x
+    far = w & ((x[:, 1] > 1 + 2 * case.dx) | (x[:, 1] < -2 * case.dx))
+    far &= (x[:, 0] > 3 * case.dx) & (x[:, 0] < 1 - 3 * case.dx)
+    assert far.sum() > 0
+    assert np.abs(sim.get("VELOCITY")[far, 0] - uw[far, 0]).max() < 1e-12
