@@ -97,6 +97,10 @@ typedef struct {
                                a PPE with no Dirichlet row (fully periodic / enclosed flows, whose
                                operator has the constant null space: eq:coeff rows sum to zero).
                                0 (default) = eq:p-sor as printed.  Not with ppe_loop = 3. */
+    int conv_mean;          /* reading R12b: 1 = eq:convergence compares means over the fluid,
+                               mean|p^{k+1} - p^k| / max(Lambda, mean|p^{k+1}|) (the text calls the
+                               denominator "the mean pressure" and Lambda "a measure of the mean
+                               pressure"); 0 (default) = the sums as printed */
     int pref_auto;          /* reading R33: 1 = the GTVF background pressure p_ref is set to
                                2 max_i p_i over fluid from the handle's first solve (internal
                                flows), then kept; 0 (default) = p_ref as given */

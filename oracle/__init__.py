@@ -46,6 +46,7 @@ class Cfg(C.Structure):
         ("max_iter", C.c_int), ("tol", C.c_double),
         ("wall_rho_summation", C.c_int),
         ("ppe_mean_free", C.c_int),
+        ("conv_mean", C.c_int),
         ("pref_auto", C.c_int),
     ]
 
@@ -137,6 +138,7 @@ def make_cfg(dim, lo, hi, periodic, h, params: dict | None = None) -> Cfg:
     c.tol = p.get("tol", 1e-2)
     c.wall_rho_summation = p.get("wall_rho_summation", 0)
     c.ppe_mean_free = p.get("ppe_mean_free", 0)
+    c.conv_mean = p.get("conv_mean", 0)
     c.pref_auto = p.get("pref_auto", 0)
     return c
 

@@ -816,10 +816,18 @@ void or_solve(or_sim* s, double tol, int max_iter, or_report* rep)
             }
         }
         double num = 0.0, den = 0.0;
+        int64_t nfl = 0;
         for (int64_t i = 0; i < n; i++) {
             if (s->tag[i] != FLUID) continue;
             num += fabs(pn[i] - pk[i]);
             den += fabs(pn[i]);
+            nfl++;
+        }
+        if (s->c.conv_mean && nfl > 0) {
+            /* reading R12b: the text calls the denominator "the mean pressure" and Lambda "a
+             * measure of the mean pressure": compare means, not sums */
+            num /= (double)nfl;
+            den /= (double)nfl;
         }
         double dd = den > s->lambda ? den : s->lambda;
         if (num == 0.0) res = 0.0;

@@ -33,6 +33,9 @@ typedef struct {
     int wall_rho_summation;  /* R4: 1 walls get summation density, 0 walls keep rho0 */
     int ppe_mean_free;       /* R32: 1 = remove the mean of the live rows (not free surface, D_ii != 0)
                                 from every Jacobi iterate (null space of a PPE with no Dirichlet row) */
+    int conv_mean;           /* R12b: 1 = eq:convergence on means over the fluid, mean|dp| / max(Lambda,
+                                mean|p|) ("Lambda ... as a measure of the mean pressure");
+                                0 = the sums as printed */
     int pref_auto;           /* R33: 1 = internal-flow p_ref := 2 max_i p_i over fluid, taken once from
                                 the pressure of the first solve, then constant */
 } or_cfg;

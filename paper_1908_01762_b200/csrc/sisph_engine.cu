@@ -319,6 +319,9 @@ template <class T, int D> struct Engine : EngineBase {
         ppe_loop = prm->ppe_loop;
         P.mean_free = prm->ppe_mean_free ? 1 : 0;
         pref_auto = prm->pref_auto;
+        conv_mean = prm->conv_mean;
+        nf_glob = 0;
+        for (int64_t k = 0; k < n; k++) nf_glob += tags_glob[k] == SISPH_TAG_FLUID ? 1 : 0;
         for (int a = 0; a < D; a++) extent = std::max(extent, std::max(fabs(dom->lo[a]), fabs(dom->hi[a])));
         min_iter = prm->min_iter;
         max_iter = prm->max_iter;
@@ -1261,6 +1264,11 @@ template <class T, int D> struct Engine : EngineBase {
     cudaGraphConditionalHandle pcond = 0;
     long long gkey[5] = {-1, -1, -1, -1, -1};
 
+    // R12b: eq:convergence on means (1 / global fluid count) or on the printed sums (1)
+    int conv_mean = 0;
+    int64_t nf_glob = 0;
+    double cscale() const { return conv_mean && nf_glob > 0 ? 1.0 / (double)nf_glob : 1.0; }
+
     int write_desc(double tl, int mi, int mx)
     {
         if (!ddesc) {
@@ -1277,6 +1285,7 @@ template <class T, int D> struct Engine : EngineBase {
         hdesc->pA = p;
         hdesc->pB = p_alt;
         hdesc->tol = tl;
+        hdesc->cscale = cscale();
         hdesc->min_it = mi;
         hdesc->max_it = mx;
         SCK(cudaMemcpyAsync(ddesc, hdesc, sizeof(PpeDesc<T>), cudaMemcpyHostToDevice, st));
@@ -1384,7 +1393,7 @@ template <class T, int D> struct Engine : EngineBase {
             if (dist()) {
                 // eq:convergence over all ranks: allreduce the local sums, decide, refresh p^{k+1}
                 SRET(xallreduce(ctl->red, 3, 0));
-                ++nlaunch, k_decide<<<1, 1, 0, st>>>(ctl, tl, mi, mx);
+                ++nlaunch, k_decide<<<1, 1, 0, st>>>(ctl, tl, mi, mx, cscale());
                 SRET(halo_p(false));
             }
         }
@@ -1415,7 +1424,7 @@ template <class T, int D> struct Engine : EngineBase {
             if (P.mean_free) SRET(mean_fix());
             if (dist() || !P.mean_free) {
                 if (dist()) SRET(xallreduce(ctl->red, 3, 0));
-                ++nlaunch, k_decide<<<1, 1, 0, st>>>(ctl, tl, mi, mx);
+                ++nlaunch, k_decide<<<1, 1, 0, st>>>(ctl, tl, mi, mx, cscale());
             }
             SCK(cudaGetLastError());
             if (dist()) SRET(halo_p(false));

@@ -1109,6 +1109,7 @@ template <class T> struct PpeDesc {
     T* pA;
     T* pB;
     double tol;
+    double cscale;      // R12b: 1 / (global fluid count) for means, 1 for the printed sums
     int min_it, max_it;
 };
 
@@ -1329,6 +1330,8 @@ __global__ void __launch_bounds__(SWEEP_T) k_sweep(Params<T> P, const PpeDesc<T>
             ctl->ticket = 0;
             return;
         }
+        num *= dsc->cscale;
+        den *= dsc->cscale;
         double lam = __longlong_as_double((long long)ctl->lambda_bits);
         double dmax = den > lam ? den : lam;
         double res = num == 0.0 ? 0.0 : (dmax > 0.0 ? num / dmax : INFINITY);
@@ -1430,6 +1433,8 @@ __global__ void __launch_bounds__(SWEEP_T) k_mean_fix(Params<T> P, const PpeDesc
             ctl->red[2] = ctl->nonfinite ? 1.0 : 0.0;
             return;
         }
+        num *= dsc->cscale;
+        den *= dsc->cscale;
         const double lam = __longlong_as_double((long long)ctl->lambda_bits);
         const double dmax = den > lam ? den : lam;
         const double res = num == 0.0 ? 0.0 : (dmax > 0.0 ? num / dmax : INFINITY);
@@ -1461,10 +1466,10 @@ __global__ void __launch_bounds__(1024) k_fluid_pmax(const T* __restrict__ p, in
 
 // eq:convergence on the allreduced sums (slab ranks; every rank takes the
 // same decision from the same bits).  A no-op once the solve is done.
-__global__ void k_decide(Ctl* ctl, double tol, int min_it, int max_it)
+__global__ void k_decide(Ctl* ctl, double tol, int min_it, int max_it, double cscale)
 {
     if (ctl->done) return;
-    const double num = ctl->red[0], den = ctl->red[1];
+    const double num = ctl->red[0] * cscale, den = ctl->red[1] * cscale;
     const double lam = __longlong_as_double((long long)ctl->lambda_bits);
     const double dmax = den > lam ? den : lam;
     const double res = num == 0.0 ? 0.0 : (dmax > 0.0 ? num / dmax : INFINITY);
@@ -1560,6 +1565,8 @@ __global__ void __launch_bounds__(SWEEP_T) k_ppe_persistent(Params<T> P, const P
                     num += sn[q];
                     den += sd[q];
                 }
+                num *= dsc->cscale;
+                den *= dsc->cscale;
                 const double lam = __longlong_as_double((long long)vc->lambda_bits);
                 const double dmax = den > lam ? den : lam;
                 const double res = num == 0.0 ? 0.0 : (dmax > 0.0 ? num / dmax : INFINITY);

@@ -45,7 +45,7 @@ class sisph_params(C.Structure):
         ("tol", C.c_double), ("wall_rho_summation", C.c_int), ("nbr_cap", C.c_int),
         ("device", C.c_int), ("stream", C.c_void_p), ("rebuild_mode", C.c_int),
         ("matrix_free", C.c_int), ("ppe_loop", C.c_int), ("ppe_mean_free", C.c_int),
-        ("pref_auto", C.c_int),
+        ("conv_mean", C.c_int), ("pref_auto", C.c_int),
     ]
 
 

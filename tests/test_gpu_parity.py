@@ -571,3 +571,24 @@ def test_wall_velocity_field_roundtrip():
     far &= (x[:, 0] > 3 * case.dx) & (x[:, 0] < 1 - 3 * case.dx)
     assert far.sum() > 0
     assert np.abs(sim.get("VELOCITY")[far, 0] - uw[far, 0]).max() < 1e-12
+
+
+@pytest.mark.parametrize("name", ["tgv2d_f64", "hydro_f64", "db2d_f64"])
+def test_conv_mean_solve_parity(name):
+    """Reading R12b (eq:convergence on means, scaled by the global fluid count):
+    same stopping sweep and residual as the oracle, from p^0 = 0 where Lambda
+    decides the first sweeps."""
+    case = CASES[name]
+    over = {"conv_mean": 1}
+    sim = gpu_sim(case, **over)
+    sim.set("PRESSURE", np.zeros(case.n))
+    o = oracle_from_gpu(case, sim, params=over)
+    sim.predict(case.dt)
+    o.predict(case.dt)
+    for tol in (1e-2, 1e-4):
+        it_g, res_g = sim.ppe_solve(tol, 300)
+        it_o, res_o, _ = o.solve(tol, 300)
+        if abs(res_o - tol) > 1e-9 * tol:
+            assert it_g == it_o, (tol, it_g, it_o, res_g, res_o)
+        assert res_g == pytest.approx(res_o, rel=1e-8, abs=1e-14)
+        assert_close("p", sim.get("PRESSURE")[case.tag == 0], o.get("p")[case.tag == 0], 64)

@@ -482,3 +482,46 @@ def test_pref_auto_takes_twice_the_first_solve_max(orc):
     assert pmax > 0
     assert np.array_equal(a.get("x"), b.get("x"))
     assert np.array_equal(a.get("u"), b.get("u"))
+
+
+def _tiled_kick(orc, reps, conv_mean):
+    # a 16 x 16 jittered periodic cell at rest except ONE particle moving (a localised
+    # divergence source, so the pressure is a localised bump and Lambda ~ its peak), p^0 = 0,
+    # tiled reps x reps into a periodic box of side reps
+    case = synth.tgv2d(n=16)
+    x0 = case.x
+    u0 = np.zeros_like(case.u)
+    u0[37] = [1.0, 0.5]
+    xs, us = [], []
+    for a in range(reps):
+        for b in range(reps):
+            xs.append(x0 + np.array([a, b]))
+            us.append(u0)
+    x, u = np.concatenate(xs), np.concatenate(us)
+    n = x.shape[0]
+    prm = dict(case.params, conv_mean=conv_mean)
+    cfg = orc.make_cfg(2, [0, 0, 0], [reps, reps, 0], [1, 1, 0], case.h, prm)
+    s = orc.Sim(cfg=cfg, x=x, u=u, m=np.full(n, case.m[0]), rho=np.ones(n), p=np.zeros(n),
+                tag=np.zeros(n, np.int32))
+    s.predict(case.dt)
+    return s
+
+
+def test_mean_convergence_measure_is_tiling_invariant(orc):
+    # R12b: with means, Lambda is compared with "the mean pressure".  A periodic
+    # problem tiled 2 x 2 is the same problem: it stops at the same sweep with the same
+    # residual.  And mean|dp| / max(Lambda, mean|p|) = sum|dp| / max(N Lambda, sum|p|) is never
+    # above the printed ratio, so the mean reading never needs more sweeps.
+    r = {}
+    for cm in (0, 1):
+        for reps in (1, 2):
+            for tol in (3e-2, 1e-2):
+                s = _tiled_kick(orc, reps, cm)
+                r[cm, reps, tol] = s.solve(tol, 500)[:2]
+    for tol in (3e-2, 1e-2):
+        assert r[1, 1, tol][0] == r[1, 2, tol][0]
+        assert r[1, 1, tol][1] == pytest.approx(r[1, 2, tol][1], rel=1e-9)
+        assert r[1, 1, tol][0] <= r[0, 1, tol][0]
+    # here Lambda dominates the mean |p| at the minimum two sweeps: the mean reading stops
+    # there, the printed sums run on (25 and 100 sweeps)
+    assert r[1, 1, 1e-2][0] == 2 and r[0, 1, 1e-2][0] > 2
