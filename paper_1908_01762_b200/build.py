@@ -13,7 +13,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsisph.so")
 SOURCES = ["sisph_engine.cu"]
-DEPS = SOURCES + ["sisph_kernels.cuh", "sisph_device.cuh"]
+DEPS = SOURCES + ["sisph_kernels.cuh", "sisph_device.cuh", "sisph_comm.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 FLAGS = [
@@ -34,23 +34,30 @@ def _stale() -> bool:
     return any(os.path.getmtime(s) > t for s in srcs)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    """out / defines: an A/B variant library (e.g. libsisph_v1.so built with -DSISPH_X),
+    loaded by the binding when SISPH_LIB names it; the default build is libsisph.so."""
+    lib_out = out or LIB
+    if out is None and not force and not _stale():
         return LIB
-    cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp",
+    cmd = [NVCC, *FLAGS, *defines, "-I", os.path.join(ROOT, "include"), "-o", lib_out + ".tmp",
            *[os.path.join(CSRC, s) for s in SOURCES]]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed building libsisph.so")
-    with open(os.path.join(HERE, "ptxas_info.txt"), "w") as f:
-        f.write(r.stderr)
+    if out is None:
+        with open(os.path.join(HERE, "ptxas_info.txt"), "w") as f:
+            f.write(r.stderr)
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib_out + ".tmp", lib_out)
+    return lib_out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
-    print(LIB)
+    # python -m paper_1908_01762_b200.build [--force] [--out PATH] [-DNAME ...]
+    args = sys.argv[1:]
+    out = args[args.index("--out") + 1] if "--out" in args else None
+    defs = [a for a in args if a.startswith("-D")]
+    print(build(force="--force" in args, verbose=True, out=out, defines=defs))

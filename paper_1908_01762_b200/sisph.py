@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsisph.so")
+# SISPH_LIB: an A/B variant of the library built in-tree (build.py --out); default libsisph.so
+LIB_PATH = os.environ.get("SISPH_LIB") or os.path.join(_HERE, "libsisph.so")
 
 SISPH_OK, SISPH_EINVAL, SISPH_ENOMEM, SISPH_ECUDA, SISPH_ENCCL, SISPH_ENONFINITE, SISPH_EOVERFLOW = range(7)
 ERROR_NAMES = {1: "SISPH_EINVAL", 2: "SISPH_ENOMEM", 3: "SISPH_ECUDA", 4: "SISPH_ENCCL",
