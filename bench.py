@@ -347,12 +347,15 @@ def run_sisph(args):
     # end to end through the public API with host buffers
     if not args.no_e2e:
         dim = case.dim
-        pin = lambda shape: torch.empty(shape, dtype=torch.float64, pin_memory=True)
+        # host buffers at the handle's precision (fp32 handles: sisph_{get,set}_field_f32)
+        f32 = case.params["precision"] == 32
+        hdt, hb = (torch.float32, 4) if f32 else (torch.float64, 8)
+        pin = lambda shape: torch.empty(shape, dtype=hdt, pin_memory=True)
         hx, hu, hut, hp = pin((n, dim)), pin((n, dim)), pin((n, dim)), pin((n,))
-        sim.get_ptr("POSITION", hx.data_ptr(), n * dim)
-        sim.get_ptr("VELOCITY", hu.data_ptr(), n * dim)
-        sim.get_ptr("TRANSPORT_VELOCITY", hut.data_ptr(), n * dim)
-        sim.get_ptr("PRESSURE", hp.data_ptr(), n)
+        sim.get_ptr("POSITION", hx.data_ptr(), n * dim, f32)
+        sim.get_ptr("VELOCITY", hu.data_ptr(), n * dim, f32)
+        sim.get_ptr("TRANSPORT_VELOCITY", hut.data_ptr(), n * dim, f32)
+        sim.get_ptr("PRESSURE", hp.data_ptr(), n, f32)
         if world > 1:
             # each rank filled its own particles: sum the ranks' arrays into the whole state,
             # so that every rank can feed any particle it comes to own
@@ -367,18 +370,19 @@ def run_sisph(args):
         sw2 = 0
         t0 = time.perf_counter()
         for _ in range(K2):
-            sim.set_ptr("POSITION", hx.data_ptr(), n * dim)
-            sim.set_ptr("VELOCITY", hu.data_ptr(), n * dim)
-            sim.set_ptr("TRANSPORT_VELOCITY", hut.data_ptr(), n * dim)
-            sim.set_ptr("PRESSURE", hp.data_ptr(), n)
+            sim.set_ptr("POSITION", hx.data_ptr(), n * dim, f32)
+            sim.set_ptr("VELOCITY", hu.data_ptr(), n * dim, f32)
+            sim.set_ptr("TRANSPORT_VELOCITY", hut.data_ptr(), n * dim, f32)
+            sim.set_ptr("PRESSURE", hp.data_ptr(), n, f32)
             sw2 += sim.step(case.dt).iters
-            sim.get_ptr("PRESSURE", out_p.data_ptr(), n)
+            sim.get_ptr("PRESSURE", out_p.data_ptr(), n, f32)
         torch.cuda.synchronize()
         t = time.perf_counter() - t0
         if world > 1:
             t = D.max_over_ranks(t, dev)
-        out["e2e"] = {"value": sw2 * nf / t, "unit": UNIT, "h2d_bytes_per_step": 8 * n * (3 * dim + 1),
-                      "d2h_bytes_per_step": 8 * n, "steps": K2, "ms_per_step": 1e3 * t / K2}
+        out["e2e"] = {"value": sw2 * nf / t, "unit": UNIT, "h2d_bytes_per_step": hb * n * (3 * dim + 1),
+                      "d2h_bytes_per_step": hb * n, "host_dtype": "f32" if f32 else "f64", "steps": K2,
+                      "ms_per_step": 1e3 * t / K2}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args.workload)
     del np

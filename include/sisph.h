@@ -219,6 +219,14 @@ int sisph_next_dt(sisph_t* s, double* dt_next, double* dt_cfl, double* dt_force)
 int sisph_get_field(sisph_t* s, sisph_field f, double* out, int64_t count);
 int sisph_set_field(sisph_t* s, sisph_field f, const double* in, int64_t count);
 
+/* The same with fp32 host buffers (half the host<->device bytes: the I/O of an
+ * fp32 handle's state at its own precision).  An fp64 handle widens on set and
+ * rounds on get.  Buffers may be pageable or pinned host memory, or device
+ * memory (cudaMemcpyDefault); the call is stream-ordered and returns after the
+ * copy (get) / the device-side scatter is enqueued (set).  Errors as above. */
+int sisph_get_field_f32(sisph_t* s, sisph_field f, float* out, int64_t count);
+int sisph_set_field_f32(sisph_t* s, sisph_field f, const float* in, int64_t count);
+
 /* Creation ids in internal order: ids[0 .. n_fluid) are the fluid particles
  * in cell-sorted order, ids[n_fluid .. n) the walls.  n must equal the
  * particle count. */

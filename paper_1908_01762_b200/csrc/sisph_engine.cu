@@ -75,6 +75,8 @@ struct EngineBase {
     virtual int step(double dt, sisph_step_report* rep) = 0;
     virtual int get_field(int f, double* out, int64_t count) = 0;
     virtual int set_field(int f, const double* in, int64_t count) = 0;
+    virtual int get_field_f32(int f, float* out, int64_t count) = 0;
+    virtual int set_field_f32(int f, const float* in, int64_t count) = 0;
     virtual int get_order(int64_t* ids) = 0;
     virtual int get_neighbors(int64_t* off, int64_t* ids, int64_t cap, int64_t* total) = 0;
     virtual int get_neighbors_of(const int64_t* which, int64_t m, int64_t* off, int64_t* ids, int64_t cap,
@@ -1659,8 +1661,16 @@ template <class T, int D> struct Engine : EngineBase {
     }
 
     // owned particles only (slab ranks: the entries of other ranks' particles stay 0)
-    int get_field(int f, double* out, int64_t count) override
+    int get_field(int f, double* out, int64_t count) override { return get_field_t(f, out, count); }
+    int get_field_f32(int f, float* out, int64_t count) override { return get_field_t(f, out, count); }
+    int set_field(int f, const double* in, int64_t count) override { return set_field_t(f, in, count); }
+    int set_field_f32(int f, const float* in, int64_t count) override { return set_field_t(f, in, count); }
+
+    // H: the host element type of the caller's buffer (double, or float for the _f32 calls)
+    template <class H>
+    int get_field_t(int f, H* out, int64_t count)
     {
+        H* htmp = reinterpret_cast<H*>(dtmp);   // device staging (3 n doubles >= count H)
         int nc = ncomp(f);
         if (nc < 0 || count != (int64_t)nc * n) {
             err = "get_field: unknown field or count != n * components";
@@ -1675,13 +1685,13 @@ template <class T, int D> struct Engine : EngineBase {
             err = "RSTAR is only defined between sisph_predict and sisph_correct";
             return SISPH_EINVAL;
         }
-        SCK(cudaMemsetAsync(dtmp, 0, (size_t)count * sizeof(double), st));
+        SCK(cudaMemsetAsync(dtmp, 0, (size_t)count * sizeof(H), st));
         const int B = 256;
         auto vec = [&](const V* src, int base, int cntx) {
-            if (cntx > 0) ++nlaunch, k_to_ids_vec<T><<<nblk(cntx, B), B, 0, st>>>(src + base, pid + base, cntx, D, dtmp);
+            if (cntx > 0) ++nlaunch, k_to_ids_vec<T, H><<<nblk(cntx, B), B, 0, st>>>(src + base, pid + base, cntx, D, htmp);
         };
         auto sc = [&](const auto* src, int base, int cntx) {
-            if (cntx > 0) ++nlaunch, k_to_ids_sc<<<nblk(cntx, B), B, 0, st>>>(src + base, pid + base, cntx, dtmp);
+            if (cntx > 0) ++nlaunch, k_to_ids_sc<<<nblk(cntx, B), B, 0, st>>>(src + base, pid + base, cntx, htmp);
         };
         switch (f) {
             case SISPH_FIELD_POSITION:
@@ -1702,10 +1712,10 @@ template <class T, int D> struct Engine : EngineBase {
                 vec(us, Nf, Nwo);
                 break;
             case SISPH_FIELD_NORMAL:
-                if (Nwo) ++nlaunch, k_to_ids_vec<T><<<nblk(Nwo, B), B, 0, st>>>(nrm, pid + Nf, Nwo, D, dtmp);
+                if (Nwo) ++nlaunch, k_to_ids_vec<T, H><<<nblk(Nwo, B), B, 0, st>>>(nrm, pid + Nf, Nwo, D, htmp);
                 break;
             case SISPH_FIELD_WALL_VELOCITY:
-                if (Nwo) ++nlaunch, k_to_ids_vec<T><<<nblk(Nwo, B), B, 0, st>>>(uwl, pid + Nf, Nwo, D, dtmp);
+                if (Nwo) ++nlaunch, k_to_ids_vec<T, H><<<nblk(Nwo, B), B, 0, st>>>(uwl, pid + Nf, Nwo, D, htmp);
                 break;
             case SISPH_FIELD_PRESSURE:
                 sc(p, 0, Nfo);
@@ -1719,32 +1729,34 @@ template <class T, int D> struct Engine : EngineBase {
             case SISPH_FIELD_DIAG: sc(diag, 0, Nfo); break;
             case SISPH_FIELD_FREE_SURFACE: sc(fs, 0, Nfo); break;
             case SISPH_FIELD_MASS:
-                if (Nfo) ++nlaunch, k_to_ids_w<T><<<nblk(Nfo, B), B, 0, st>>>(pos, pid, Nfo, dtmp);
-                if (Nwo) ++nlaunch, k_to_ids_w<T><<<nblk(Nwo, B), B, 0, st>>>(pos + Nf, pid + Nf, Nwo, dtmp);
+                if (Nfo) ++nlaunch, k_to_ids_w<T, H><<<nblk(Nfo, B), B, 0, st>>>(pos, pid, Nfo, htmp);
+                if (Nwo) ++nlaunch, k_to_ids_w<T, H><<<nblk(Nwo, B), B, 0, st>>>(pos + Nf, pid + Nf, Nwo, htmp);
                 break;
         }
         SCK(cudaGetLastError());
-        SCK(cudaMemcpyAsync(out, dtmp, (size_t)count * sizeof(double), cudaMemcpyDefault, st));
+        SCK(cudaMemcpyAsync(out, dtmp, (size_t)count * sizeof(H), cudaMemcpyDefault, st));
         SCK(cudaStreamSynchronize(st));
         return SISPH_OK;
     }
 
-    int set_field(int f, const double* in, int64_t count) override
+    template <class H>
+    int set_field_t(int f, const H* in, int64_t count)
     {
+        const H* htmp = reinterpret_cast<const H*>(dtmp);
         int nc = ncomp(f);
         if (nc < 0 || count != (int64_t)nc * n || f == SISPH_FIELD_TAG || f == SISPH_FIELD_RSTAR) {
             err = "set_field: unknown or read-only field, or count != n * components";
             return SISPH_EINVAL;
         }
         pre_swept = false;   // the sweep fused into A11 used the old state: the solve redoes it
-        SCK(cudaMemcpyAsync(dtmp, in, (size_t)count * sizeof(double), cudaMemcpyDefault, st));
+        SCK(cudaMemcpyAsync(dtmp, in, (size_t)count * sizeof(H), cudaMemcpyDefault, st));
         const int B = 256;
         auto vec = [&](V* dst, int base, int cntx, int keep_w) {
-            if (cntx > 0) ++nlaunch, k_from_ids_vec<T><<<nblk(cntx, B), B, 0, st>>>(dtmp, pid + base, cntx, D, dst + base, keep_w);
+            if (cntx > 0) ++nlaunch, k_from_ids_vec<T, H><<<nblk(cntx, B), B, 0, st>>>(htmp, pid + base, cntx, D, dst + base, keep_w);
         };
         auto sc = [&](auto* dst, int base, int cntx) {
             using S = std::remove_pointer_t<decltype(dst)>;
-            if (cntx > 0) ++nlaunch, k_from_ids_sc<T, S><<<nblk(cntx, B), B, 0, st>>>(dtmp, pid + base, cntx, dst + base);
+            if (cntx > 0) ++nlaunch, k_from_ids_sc<T, S, H><<<nblk(cntx, B), B, 0, st>>>(htmp, pid + base, cntx, dst + base);
         };
         switch (f) {
             case SISPH_FIELD_POSITION: {
@@ -1754,7 +1766,7 @@ template <class T, int D> struct Engine : EngineBase {
                     // wall geometry is static; re-sort walls + normals only if it changed
                     // (compared on the device against the input, in working precision)
                     SCK(cudaMemsetAsync(dcnt_w, 0, sizeof(int), st));
-                    ++nlaunch, k_walls_changed<T><<<nblk(Nwo, B), B, 0, st>>>(dtmp, pid + Nf, Nwo, D, pos + Nf, dcnt_w);
+                    ++nlaunch, k_walls_changed<T, H><<<nblk(Nwo, B), B, 0, st>>>(htmp, pid + Nf, Nwo, D, pos + Nf, dcnt_w);
                     int changed = 0;
                     SCK(cudaMemcpyAsync(&changed, dcnt_w, sizeof(int), cudaMemcpyDeviceToHost, st));
                     SCK(cudaStreamSynchronize(st));
@@ -1780,11 +1792,11 @@ template <class T, int D> struct Engine : EngineBase {
                 vec(us, Nf, Nwo, 0);
                 break;
             case SISPH_FIELD_NORMAL:
-                if (Nwo) ++nlaunch, k_from_ids_vec<T><<<nblk(Nwo, B), B, 0, st>>>(dtmp, pid + Nf, Nwo, D, nrm, 0);
+                if (Nwo) ++nlaunch, k_from_ids_vec<T, H><<<nblk(Nwo, B), B, 0, st>>>(htmp, pid + Nf, Nwo, D, nrm, 0);
                 break;
             case SISPH_FIELD_WALL_VELOCITY:
                 // owned walls (ghost walls take their ghost velocities from the owner's halo)
-                if (Nwo) ++nlaunch, k_from_ids_vec<T><<<nblk(Nwo, B), B, 0, st>>>(dtmp, pid + Nf, Nwo, D, uwl, 0);
+                if (Nwo) ++nlaunch, k_from_ids_vec<T, H><<<nblk(Nwo, B), B, 0, st>>>(htmp, pid + Nf, Nwo, D, uwl, 0);
                 break;
             case SISPH_FIELD_PRESSURE:
                 sc(p, 0, Nfo);
@@ -1798,8 +1810,8 @@ template <class T, int D> struct Engine : EngineBase {
             case SISPH_FIELD_DIAG: sc(diag, 0, Nfo); break;
             case SISPH_FIELD_FREE_SURFACE: sc(fs, 0, Nfo); break;
             case SISPH_FIELD_MASS:
-                if (Nfo) ++nlaunch, k_from_ids_w<T><<<nblk(Nfo, B), B, 0, st>>>(dtmp, pid, Nfo, pos);
-                if (Nwo) ++nlaunch, k_from_ids_w<T><<<nblk(Nwo, B), B, 0, st>>>(dtmp, pid + Nf, Nwo, pos + Nf);
+                if (Nfo) ++nlaunch, k_from_ids_w<T, H><<<nblk(Nfo, B), B, 0, st>>>(htmp, pid, Nfo, pos);
+                if (Nwo) ++nlaunch, k_from_ids_w<T, H><<<nblk(Nwo, B), B, 0, st>>>(htmp, pid + Nf, Nwo, pos + Nf);
                 break;
         }
         SCK(cudaGetLastError());
@@ -1810,7 +1822,7 @@ template <class T, int D> struct Engine : EngineBase {
     int get_field_walls_pos(double* out)
     {
         SCK(cudaMemsetAsync(dtmp, 0, (size_t)n * D * sizeof(double), st));
-        if (Nwo) ++nlaunch, k_to_ids_vec<T><<<nblk(Nwo, 256), 256, 0, st>>>(pos + Nf, pid + Nf, Nwo, D, dtmp);
+        if (Nwo) ++nlaunch, k_to_ids_vec<T, double><<<nblk(Nwo, 256), 256, 0, st>>>(pos + Nf, pid + Nf, Nwo, D, dtmp);
         SCK(cudaGetLastError());
         SCK(cudaMemcpyAsync(out, dtmp, (size_t)n * D * sizeof(double), cudaMemcpyDefault, st));
         SCK(cudaStreamSynchronize(st));
@@ -2271,6 +2283,18 @@ int sisph_set_field(sisph_t* s, sisph_field f, const double* in, int64_t count)
     CHK_HANDLE(s);
     if (!in) return fail_thread(SISPH_EINVAL, "NULL in");
     return s->e->set_field((int)f, in, count);
+}
+int sisph_get_field_f32(sisph_t* s, sisph_field f, float* out, int64_t count)
+{
+    CHK_HANDLE(s);
+    if (!out) return fail_thread(SISPH_EINVAL, "NULL out");
+    return s->e->get_field_f32((int)f, out, count);
+}
+int sisph_set_field_f32(sisph_t* s, sisph_field f, const float* in, int64_t count)
+{
+    CHK_HANDLE(s);
+    if (!in) return fail_thread(SISPH_EINVAL, "NULL in");
+    return s->e->set_field_f32((int)f, in, count);
 }
 int sisph_get_order(sisph_t* s, int64_t* ids, int64_t n)
 {

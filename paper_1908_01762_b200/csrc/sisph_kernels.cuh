@@ -1919,13 +1919,13 @@ __global__ void k_unpack(PackList L, const int* __restrict__ map, int base, int 
 // host <-> device marshalling in creation-id order
 // ===========================================================================
 // vector field: dst[slot] = src[id[slot]] (id order -> internal order)
-template <class T>
-__global__ void k_from_ids_vec(const double* __restrict__ src, const int* __restrict__ id, int n, int dim,
+template <class T, class H>
+__global__ void k_from_ids_vec(const H* __restrict__ src, const int* __restrict__ id, int n, int dim,
                                V4<T>* __restrict__ dst, int keep_w)
 {
     int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n) return;
-    const double* v = src + (size_t)id[s] * dim;
+    const H* v = src + (size_t)id[s] * dim;
     V4<T> o = dst[s];
     o.x = (T)v[0];
     o.y = (T)v[1];
@@ -1933,56 +1933,56 @@ __global__ void k_from_ids_vec(const double* __restrict__ src, const int* __rest
     if (!keep_w) o.w = T(0);
     dst[s] = o;
 }
-template <class T>
+template <class T, class H>
 __global__ void k_to_ids_vec(const V4<T>* __restrict__ src, const int* __restrict__ id, int n, int dim,
-                             double* __restrict__ dst)
+                             H* __restrict__ dst)
 {
     int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n) return;
     V4<T> o = src[s];
-    double* v = dst + (size_t)id[s] * dim;
-    v[0] = (double)o.x;
-    v[1] = (double)o.y;
-    if (dim == 3) v[2] = (double)o.z;
+    H* v = dst + (size_t)id[s] * dim;
+    v[0] = (H)o.x;
+    v[1] = (H)o.y;
+    if (dim == 3) v[2] = (H)o.z;
 }
-template <class T>
-__global__ void k_from_ids_w(const double* __restrict__ src, const int* __restrict__ id, int n,
+template <class T, class H>
+__global__ void k_from_ids_w(const H* __restrict__ src, const int* __restrict__ id, int n,
                              V4<T>* __restrict__ dst)
 {
     int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n) return;
     dst[s].w = (T)src[id[s]];
 }
-template <class T>
-__global__ void k_to_ids_w(const V4<T>* __restrict__ src, const int* __restrict__ id, int n, double* __restrict__ dst)
+template <class T, class H>
+__global__ void k_to_ids_w(const V4<T>* __restrict__ src, const int* __restrict__ id, int n, H* __restrict__ dst)
 {
     int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n) return;
-    dst[id[s]] = (double)src[s].w;
+    dst[id[s]] = (H)src[s].w;
 }
-template <class T, class S>
-__global__ void k_from_ids_sc(const double* __restrict__ src, const int* __restrict__ id, int n, S* __restrict__ dst)
+template <class T, class S, class H>
+__global__ void k_from_ids_sc(const H* __restrict__ src, const int* __restrict__ id, int n, S* __restrict__ dst)
 {
     int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n) return;
     dst[s] = (S)src[id[s]];
 }
-template <class S>
-__global__ void k_to_ids_sc(const S* __restrict__ src, const int* __restrict__ id, int n, double* __restrict__ dst)
+template <class S, class H>
+__global__ void k_to_ids_sc(const S* __restrict__ src, const int* __restrict__ id, int n, H* __restrict__ dst)
 {
     int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n) return;
-    dst[id[s]] = (double)src[s];
+    dst[id[s]] = (H)src[s];
 }
 // has any owned wall's position (creation-id order input, working precision)
 // changed?  (set_field(POSITION): the wall geometry is static unless it does)
-template <class T>
-__global__ void k_walls_changed(const double* __restrict__ src, const int* __restrict__ id, int n, int dim,
+template <class T, class H>
+__global__ void k_walls_changed(const H* __restrict__ src, const int* __restrict__ id, int n, int dim,
                                 const V4<T>* __restrict__ wpos, int* __restrict__ flag)
 {
     int s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= n) return;
-    const double* v = src + (size_t)id[s] * dim;
+    const H* v = src + (size_t)id[s] * dim;
     const V4<T> o = wpos[s];
     bool ch = (T)v[0] != o.x || (T)v[1] != o.y;
     if (dim == 3) ch = ch || (T)v[2] != o.z;

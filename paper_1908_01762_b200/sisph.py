@@ -25,7 +25,7 @@ VECTOR_FIELDS = {"POSITION", "VELOCITY", "TRANSPORT_VELOCITY", "USTAR", "RSTAR",
 
 EXPORTED = ["sisph_params_default", "sisph_create", "sisph_destroy", "sisph_build_neighbors",
             "sisph_predict", "sisph_ppe_solve", "sisph_correct", "sisph_step", "sisph_get_field",
-            "sisph_set_field", "sisph_get_order", "sisph_get_neighbors", "sisph_get_neighbors_of",
+            "sisph_set_field", "sisph_get_field_f32", "sisph_set_field_f32", "sisph_get_order", "sisph_get_neighbors", "sisph_get_neighbors_of",
             "sisph_get_counts", "sisph_get_owned_counts", "sisph_nccl_unique_id", "sisph_local_group_create",
             "sisph_local_group_destroy", "sisph_slab_bounds", "sisph_slab_owner", "sisph_create_dist", "sisph_next_dt", "sisph_sweep_timing",
             "sisph_set_timing", "sisph_sync", "sisph_last_error"]
@@ -299,23 +299,34 @@ class Simulation:
     def sync(self):
         _check(lib().sisph_sync(self._h), self._h)
 
-    def get(self, field: str, out: np.ndarray | None = None):
+    def get(self, field: str, out: np.ndarray | None = None, dtype=np.float64):
+        """sisph_get_field (float64) or sisph_get_field_f32 (dtype / out float32)."""
         nc = self.dim if field in VECTOR_FIELDS else 1
         if out is None:
-            out = np.empty((self.n, nc) if nc > 1 else self.n, np.float64)
-        _check(lib().sisph_get_field(self._h, FIELDS[field], out.ctypes.data, out.size), self._h)
+            out = np.empty((self.n, nc) if nc > 1 else self.n, dtype)
+        fn = lib().sisph_get_field_f32 if out.dtype == np.float32 else lib().sisph_get_field
+        if out.dtype not in (np.float32, np.float64) or not out.flags.c_contiguous:
+            raise ValueError("out must be a C-contiguous float32 or float64 array")
+        _check(fn(self._h, FIELDS[field], out.ctypes.data, out.size), self._h)
         return out
 
     def set(self, field: str, value):
+        """sisph_set_field; float32 arrays go through sisph_set_field_f32."""
+        if isinstance(value, np.ndarray) and value.dtype == np.float32:
+            v = np.ascontiguousarray(value)
+            _check(lib().sisph_set_field_f32(self._h, FIELDS[field], v.ctypes.data, v.size), self._h)
+            return
         v = np.ascontiguousarray(value, np.float64)
         _check(lib().sisph_set_field(self._h, FIELDS[field], v.ctypes.data, v.size), self._h)
 
-    def set_ptr(self, field: str, ptr: int, count: int):
-        """set_field from a raw host pointer (e.g. pinned torch memory)."""
-        _check(lib().sisph_set_field(self._h, FIELDS[field], C.c_void_p(ptr), count), self._h)
+    def set_ptr(self, field: str, ptr: int, count: int, f32: bool = False):
+        """set_field from a raw host pointer (e.g. pinned torch memory); f32: float buffer."""
+        fn = lib().sisph_set_field_f32 if f32 else lib().sisph_set_field
+        _check(fn(self._h, FIELDS[field], C.c_void_p(ptr), count), self._h)
 
-    def get_ptr(self, field: str, ptr: int, count: int):
-        _check(lib().sisph_get_field(self._h, FIELDS[field], C.c_void_p(ptr), count), self._h)
+    def get_ptr(self, field: str, ptr: int, count: int, f32: bool = False):
+        fn = lib().sisph_get_field_f32 if f32 else lib().sisph_get_field
+        _check(fn(self._h, FIELDS[field], C.c_void_p(ptr), count), self._h)
 
     def order(self):
         ids = np.empty(self.n, np.int64)
