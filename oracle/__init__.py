@@ -47,6 +47,8 @@ class Cfg(C.Structure):
         ("wall_rho_summation", C.c_int),
         ("ppe_mean_free", C.c_int),
         ("conv_mean", C.c_int),
+        ("open_x", C.c_int),
+        ("x_inlet", C.c_double), ("x_outlet", C.c_double), ("x_end", C.c_double), ("inlet_length", C.c_double),
         ("pref_auto", C.c_int),
     ]
 
@@ -88,6 +90,9 @@ def lib():
         L.or_num_pairs.restype = C.c_int64
         L.or_num_pairs.argtypes = [C.c_void_p, C.c_int]
         L.or_next_dt.argtypes = [C.c_void_p, dp, dp, dp]
+        L.or_get_tags.argtypes = [C.c_void_p, i32p]
+        L.or_get_tags.restype = None
+        L.or_error.argtypes = [C.c_void_p]
         _lib = L
     return _lib
 
@@ -139,6 +144,11 @@ def make_cfg(dim, lo, hi, periodic, h, params: dict | None = None) -> Cfg:
     c.wall_rho_summation = p.get("wall_rho_summation", 0)
     c.ppe_mean_free = p.get("ppe_mean_free", 0)
     c.conv_mean = p.get("conv_mean", 0)
+    c.open_x = p.get("open_x", 0)
+    c.x_inlet = p.get("x_inlet", 0.0)
+    c.x_outlet = p.get("x_outlet", 0.0)
+    c.x_end = p.get("x_end", 0.0)
+    c.inlet_length = p.get("inlet_length", 0.0)
     c.pref_auto = p.get("pref_auto", 0)
     return c
 
@@ -223,6 +233,15 @@ class Sim:
         if lib().or_get(self._h, f.encode(), _dp(out)) != 0:
             raise KeyError(f)
         return out[:, : self.dim] if f in self.VEC else out
+
+    def tags(self):
+        """current tags (open boundaries change them: R34)"""
+        out = np.zeros(self.n, np.int32)
+        lib().or_get_tags(self._h, out.ctypes.data_as(C.POINTER(C.c_int32)))
+        return out
+
+    def error(self):
+        return int(lib().or_error(self._h))
 
     def set(self, f, v):
         if f in self.VEC:

@@ -22,6 +22,11 @@
 
 #define FLUID 0
 #define WALL 1
+#define INLET 2     /* open boundaries (R34): prescribed velocity, PPE unknowns */
+#define OUTLET 3    /* u, p frozen, advected with the Shepard-extrapolated fluid u_x */
+#define DORMANT 4   /* not in the flow: parked far outside the domain */
+#define LIQ(t) ((t) == FLUID || (t) == INLET || (t) == OUTLET)
+#define UNKNOWN(t) ((t) == FLUID || (t) == INLET)   /* PPE rows */
 
 /* ------------------------------------------------------------------------ */
 /* Kernel: reading R1 (the paper only says "quintic spline"). */
@@ -306,6 +311,7 @@ struct or_sim {
     double *x, *u, *ut, *m, *rho, *p;   /* state; u of a wall = its ghost velocity */
     double* uw;                         /* prescribed wall velocity u_i of eq:vg-adami (walls; 0 fluid) */
     int pref_set;                       /* R33: p_ref already taken */
+    int error;                          /* R34: dormant pool exhausted */
     double *xs, *us;                    /* r*, u* (walls: xs = x, us = wall u*) */
     double *rhs, *diag, *fs;            /* PPE scratch */
     double* nrm;                        /* wall unit normals */
@@ -432,6 +438,19 @@ static void compute_normals(or_sim* s)
     free(ns);
 }
 
+/* R34: a dormant particle sits far below the domain in x (bounded axis), where
+ * no distance test can accept it; its fields are zeroed */
+static void park(or_sim* s, int64_t i)
+{
+    const or_cfg* c = &s->c;
+    s->x[3 * i] = c->lo[0] - 1.0e3 * (c->hi[0] - c->lo[0] + 1.0);
+    for (int a = 0; a < 3; a++) {
+        s->u[3 * i + a] = s->ut[3 * i + a] = s->us[3 * i + a] = 0.0;
+        s->xs[3 * i + a] = s->x[3 * i + a];
+    }
+    s->p[i] = 0.0;
+}
+
 or_sim* or_create(const or_cfg* c, int64_t n, const double* x3, const double* u3,
                   const double* m, const double* rho, const double* p, const int32_t* tag)
 {
@@ -460,6 +479,8 @@ or_sim* or_create(const or_cfg* c, int64_t n, const double* x3, const double* u3
                 s->uw[3 * i + a] = u3[3 * i + a];
                 s->ut[3 * i + a] = 0.0;
             }
+    for (int64_t i = 0; i < n; i++)
+        if (tag[i] == DORMANT) park(s, i);
     csr_build(s, 0, s->x, 0, NULL);
     compute_normals(s);
     return s;
@@ -540,6 +561,7 @@ void or_pass_density(or_sim* s)
             double r = sqrt(rij(c, s->x + 3 * i, s->x + 3 * j, d));
             rho += s->m[j] * or_W(c->dim, r, c->h);
         }
+        if (s->tag[i] == DORMANT) continue;
         if (s->tag[i] == WALL && !c->wall_rho_summation) rho = c->rho0;
         s->rho[i] = rho;
         s->fs[i] = (s->tag[i] == FLUID && rho / c->rho0 < c->fs_ratio) ? 1.0 : 0.0;
@@ -555,7 +577,7 @@ static void shepard_half(or_sim* s, const csr_t* b, const double* xpos, const do
     double sw = 0.0, acc[3] = {0, 0, 0};
     for (int64_t t = b->off[i]; t < b->off[i + 1]; t++) {
         int64_t j = b->nbr[t];
-        if (s->tag[j] != FLUID) continue;
+        if (!LIQ(s->tag[j])) continue;
         double d[3];
         double r = sqrt(rij(c, xpos + 3 * i, xpos + 3 * j, d));
         double w = or_W(c->dim, r, 0.5 * c->h);
@@ -600,6 +622,16 @@ static void pass_forces_predict(or_sim* s, double dt)
     csr_t* b = &s->nb[0];
 #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < s->n; i++) {
+        if (s->tag[i] == INLET || s->tag[i] == OUTLET) {
+            /* R34: prescribed / frozen velocity (no momentum update), moved like fluid to r* */
+            for (int a = 0; a < 3; a++) {
+                s->us[3 * i + a] = s->u[3 * i + a];
+                s->xs[3 * i + a] = a < dim ? s->x[3 * i + a] + dt * s->ut[3 * i + a] : 0.0;
+                s->anp[3 * i + a] = 0.0;
+            }
+            wrap_pos(c, s->xs + 3 * i);
+            continue;
+        }
         if (s->tag[i] != FLUID) {
             for (int a = 0; a < 3; a++) s->xs[3 * i + a] = s->x[3 * i + a];
             continue;
@@ -633,7 +665,7 @@ static void pass_forces_predict(or_sim* s, double dt)
                     for (int a = 0; a < dim; a++) acc[a] -= mj * Pi * gw[a];
                 }
             }
-            if (s->tag[j] == FLUID) {
+            if (LIQ(s->tag[j])) {
                 const double* utj = s->ut + 3 * j;
                 double duj[3] = {utj[0] - uj[0], utj[1] - uj[1], utj[2] - uj[2]};
                 double ai = dot(dim, dui, gw) / rhoi;
@@ -685,7 +717,7 @@ static void pass_rhs_diag(or_sim* s, double dt)
     csr_t* b = &s->nb[1];
 #pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < s->n; i++) {
-        if (s->tag[i] != FLUID) { s->rhs[i] = 0.0; s->diag[i] = 0.0; continue; }
+        if (!UNKNOWN(s->tag[i])) { s->rhs[i] = 0.0; s->diag[i] = 0.0; continue; }
         double rhs = 0.0, diag = 0.0, rhoi = s->rho[i];
         const double* usi = s->us + 3 * i;
         for (int64_t t = b->off[i]; t < b->off[i + 1]; t++) {
@@ -704,7 +736,7 @@ static void pass_rhs_diag(or_sim* s, double dt)
     }
     double lam = 0.0;
     for (int64_t i = 0; i < s->n; i++) {
-        if (s->tag[i] != FLUID || s->fs[i] != 0.0 || s->diag[i] == 0.0) continue;
+        if (!UNKNOWN(s->tag[i]) || s->fs[i] != 0.0 || s->diag[i] == 0.0) continue;
         double v = fabs(s->rhs[i] / s->diag[i]);
         if (v > lam) lam = v;
     }
@@ -720,7 +752,7 @@ static double wall_pressure_one(or_sim* s, const double* pk, int64_t i)
     double sw = 0.0, sp = 0.0, sr[3] = {0, 0, 0};
     for (int64_t t = b->off[i]; t < b->off[i + 1]; t++) {
         int64_t j = b->nbr[t];
-        if (s->tag[j] != FLUID) continue;
+        if (!LIQ(s->tag[j])) continue;
         double d[3];
         double r = sqrt(rij(c, s->xs + 3 * i, s->xs + 3 * j, d));
         double w = or_W(c->dim, r, c->h);
@@ -766,7 +798,7 @@ void or_pass_sweep(or_sim* s, const double* pk, int64_t nd, const int64_t* dests
     } else {
         int64_t t = 0;
         for (int64_t i = 0; i < s->n; i++)
-            if (s->tag[i] == FLUID) out[t++] = sweep_one(s, pk, i);
+            if (UNKNOWN(s->tag[i])) out[t++] = sweep_one(s, pk, i);
     }
 }
 
@@ -797,7 +829,7 @@ void or_solve(or_sim* s, double tol, int max_iter, or_report* rep)
         or_pass_wall_pressure(s, pk, pk);
 #pragma omp parallel for schedule(static)
         for (int64_t i = 0; i < n; i++)
-            pn[i] = s->tag[i] == FLUID ? sweep_one(s, pk, i) : pk[i];
+            pn[i] = UNKNOWN(s->tag[i]) ? sweep_one(s, pk, i) : pk[i];
         if (s->c.ppe_mean_free) {
             /* reading R32: without a Dirichlet row (no free surface) the PPE operator has the
              * constant null space (its rows sum to zero, eq:coeff / eq:coeff1) and the Jacobi
@@ -805,20 +837,20 @@ void or_solve(or_sim* s, double tol, int max_iter, or_report* rep)
             double sum = 0.0;
             int64_t cnt = 0;
             for (int64_t i = 0; i < n; i++)
-                if (s->tag[i] == FLUID && s->fs[i] == 0.0 && s->diag[i] != 0.0) {
+                if (UNKNOWN(s->tag[i]) && s->fs[i] == 0.0 && s->diag[i] != 0.0) {
                     sum += pn[i];
                     cnt++;
                 }
             if (cnt > 0) {
                 double m = sum / (double)cnt;
                 for (int64_t i = 0; i < n; i++)
-                    if (s->tag[i] == FLUID && s->fs[i] == 0.0 && s->diag[i] != 0.0) pn[i] -= m;
+                    if (UNKNOWN(s->tag[i]) && s->fs[i] == 0.0 && s->diag[i] != 0.0) pn[i] -= m;
             }
         }
         double num = 0.0, den = 0.0;
         int64_t nfl = 0;
         for (int64_t i = 0; i < n; i++) {
-            if (s->tag[i] != FLUID) continue;
+            if (!UNKNOWN(s->tag[i])) continue;
             num += fabs(pn[i] - pk[i]);
             den += fabs(pn[i]);
             nfl++;
@@ -846,6 +878,46 @@ void or_solve(or_sim* s, double tol, int max_iter, or_report* rep)
  * GTVF sub-steps (eq:int:gtvf:pos, eq:int:gtvf:vel:tmp) with the pair set
  * frozen at r* (P:454-456), transport velocity (eq:int:vhatnp2) and position
  * update (eq:int:rnp2) from r^n (R24). */
+/* R34 conversions after the position update, each in id order:
+ *   outlet with x >= x_end     -> dormant (its id returns to the pool)
+ *   fluid with x >= x_outlet   -> outlet (u, p frozen from now on)
+ *   inlet with x >= x_inlet    -> fluid; the lowest dormant id becomes a new inlet
+ *                                 particle at x - inlet_length (same y, z, u, m, rho, p) */
+static void open_boundaries(or_sim* s)
+{
+    const or_cfg* c = &s->c;
+    int64_t n = s->n;
+    for (int64_t i = 0; i < n; i++)
+        if (s->tag[i] == OUTLET && s->x[3 * i] >= c->x_end) {
+            s->tag[i] = DORMANT;
+            park(s, i);
+        }
+    for (int64_t i = 0; i < n; i++)
+        if (s->tag[i] == FLUID && s->x[3 * i] >= c->x_outlet) s->tag[i] = OUTLET;
+    int64_t pool = 0;   /* next candidate dormant id (ids only increase within a step) */
+    for (int64_t i = 0; i < n; i++) {
+        if (s->tag[i] != INLET || s->x[3 * i] < c->x_inlet) continue;
+        s->tag[i] = FLUID;
+        while (pool < n && s->tag[pool] != DORMANT) pool++;
+        if (pool == n) { s->error = 1; continue; }
+        int64_t k = pool++;
+        s->tag[k] = INLET;
+        for (int a = 0; a < 3; a++) {
+            s->x[3 * k + a] = s->x[3 * i + a];
+            s->u[3 * k + a] = s->ut[3 * k + a] = s->u[3 * i + a];
+            s->xs[3 * k + a] = s->us[3 * k + a] = 0.0;
+        }
+        s->x[3 * k] -= c->inlet_length;
+        s->m[k] = s->m[i];
+        s->rho[k] = s->rho[i];
+        s->p[k] = s->p[i];
+    }
+}
+
+int or_error(or_sim* s) { return s->error; }
+
+void or_get_tags(or_sim* s, int32_t* out) { memcpy(out, s->tag, (size_t)s->n * sizeof(int32_t)); }
+
 void or_correct(or_sim* s, double dt)
 {
     const or_cfg* c = &s->c;
@@ -929,8 +1001,44 @@ void or_correct(or_sim* s, double dt)
         }
         memcpy(rk, rn, (size_t)(3 * n) * sizeof(double));
     }
+    /* R34: the outlet's advection velocity, Shepard_h of the fluid's u_x^{n+1} at r^n
+     * (fluid sources of the r^n list; none in the support: the frozen u_x) */
+    double* uout = dalloc(n);
+    if (c->open_x) {
+        const csr_t* b0 = &s->nb[0];
+#pragma omp parallel for schedule(static)
+        for (int64_t i = 0; i < n; i++) {
+            if (s->tag[i] != OUTLET) continue;
+            double sw = 0.0, su = 0.0;
+            for (int64_t t = b0->off[i]; t < b0->off[i + 1]; t++) {
+                int64_t j = b0->nbr[t];
+                if (s->tag[j] != FLUID) continue;
+                double d[3];
+                double w = or_W(dim, sqrt(rij(c, s->x + 3 * i, s->x + 3 * j, d)), c->h);
+                su += unew[3 * j] * w;
+                sw += w;
+            }
+            uout[i] = sw > 0.0 ? su / sw : s->u[3 * i];
+        }
+    }
     /* transport velocity and positions */
     for (int64_t i = 0; i < n; i++) {
+        if (s->tag[i] == INLET) {
+            /* prescribed velocity: r^{n+1} = r^n + dt u, u~ = u */
+            for (int a = 0; a < dim; a++) {
+                s->x[3 * i + a] += dt * s->u[3 * i + a];
+                s->ut[3 * i + a] = s->u[3 * i + a];
+            }
+            wrap_pos(c, s->x + 3 * i);
+            continue;
+        }
+        if (s->tag[i] == OUTLET) {
+            /* u, p frozen; moved along x with the extrapolated fluid u_x */
+            s->x[3 * i] += dt * uout[i];
+            s->ut[3 * i] = uout[i];
+            for (int a = 1; a < 3; a++) s->ut[3 * i + a] = 0.0;
+            continue;
+        }
         if (s->tag[i] != FLUID) continue;
         for (int a = 0; a < dim; a++) {
             double utn = unew[3 * i + a] + (rk[3 * i + a] - s->xs[3 * i + a]) / dt;
@@ -940,7 +1048,8 @@ void or_correct(or_sim* s, double dt)
         }
         wrap_pos(c, s->x + 3 * i);
     }
-    free(unew); free(p0); free(rn); free(vk); free(fk);
+    if (c->open_x) open_boundaries(s);
+    free(unew); free(p0); free(rn); free(vk); free(fk); free(uout);
 }
 
 /* Adaptive time step:

@@ -36,6 +36,13 @@ typedef struct {
     int conv_mean;           /* R12b: 1 = eq:convergence on means over the fluid, mean|dp| / max(Lambda,
                                 mean|p|) ("Lambda ... as a measure of the mean pressure");
                                 0 = the sums as printed */
+    /* NEXT-4b open boundaries along x (§3.5, reading R34): tags 2 inlet, 3 outlet,
+     * 4 dormant (the id pool new inlet particles are drawn from).  After each step, in id
+     * order: outlet with x >= x_end -> dormant; fluid with x >= x_outlet -> outlet (u, p
+     * frozen); inlet with x >= x_inlet -> fluid, and the lowest dormant id becomes a new
+     * inlet particle at x - inlet_length with the same velocity. */
+    int open_x;
+    double x_inlet, x_outlet, x_end, inlet_length;
     int pref_auto;           /* R33: 1 = internal-flow p_ref := 2 max_i p_i over fluid, taken once from
                                 the pressure of the first solve, then constant */
 } or_cfg;
@@ -70,6 +77,8 @@ or_sim* or_create(const or_cfg* c, int64_t n, const double* x3, const double* u3
                   const double* m, const double* rho, const double* p, const int32_t* tag);
 void or_destroy(or_sim* s);
 int or_get(or_sim* s, const char* field, double* out);
+void or_get_tags(or_sim* s, int32_t* out);
+int or_error(or_sim* s);   /* 1: the dormant pool ran out during an inlet spawn */
 int or_set(or_sim* s, const char* field, const double* in);
 
 /* Algorithm 1 split as the C ABI splits it */

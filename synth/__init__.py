@@ -296,6 +296,70 @@ def cavity(n: int = 50, re: float = 100.0, U: float = 1.0, layers: int = 3, t_en
 
 
 # --------------------------------------------------------------------------
+# NEXT-4b open boundaries: channel with an inlet and an outlet
+# --------------------------------------------------------------------------
+INLET = 2
+OUTLET = 3
+DORMANT = 4
+
+
+def poiseuille_velocity(y, U, H):
+    """fully developed plane channel flow with mean velocity U (textbook closed form):
+    u(y) = 6 U y (H - y) / H^2"""
+    y = np.asarray(y, np.float64)
+    return 6.0 * U * y * (H - y) / (H * H)
+
+
+def channel(nx: int = 40, ny: int = 10, H: float = 1.0, U: float = 1.0, re: float = 10.0, n_in: int = 4,
+            n_out: int = 4, n_pool: int | None = None, layers: int = 3, t_end: float = 10.0, tol: float = 1e-3,
+            precision: int = 64) -> Case:
+    """Plane channel of height H (ny particles across) between two resting walls.
+    Inlet region x in [-n_in dx, 0): tag 2 with the developed (parabolic, mean U)
+    profile as prescribed velocity; fluid x in [0, nx dx) and the outlet region
+    [nx dx, (nx + n_out) dx) (tag 3, frozen until they leave at x_end) start
+    with the same profile.  n_pool dormant particles (tag 4)
+    hold the ids new inlet particles are drawn from (reading R34).  Re = U H / nu,
+    asymm gradient (the frozen outlet pressures ratchet the absolute level
+    upward with the flow; eq:mom:sph:press:pij is blind to it), no GTVF
+    (p_ref = 0), no-slip u* on the walls."""
+    rho0 = 1.0
+    dx = H / ny
+    h = dx
+    nu = U * H / re
+    Lf = nx * dx
+    L_in, L_out = n_in * dx, n_out * dx
+    fluid = _lattice((nx, ny), dx, (0.0, 0.0))
+    inlet = _lattice((n_in, ny), dx, (-L_in, 0.0))
+    outlet = _lattice((n_out, ny), dx, (Lf, 0.0))
+    n_pool = 2 * n_in * ny if n_pool is None else n_pool
+    pool = _lattice((n_in, ny), dx, (-L_in, 0.0))
+    pool = np.concatenate([pool] * (n_pool // len(pool) + 1))[:n_pool]
+    xs = (np.arange(-n_in - layers, nx + n_out + layers) + 0.5) * dx
+    walls = [np.stack([xs, np.full_like(xs, -(l + 0.5) * dx)], 1) for l in range(layers)]
+    walls += [np.stack([xs, np.full_like(xs, H + (l + 0.5) * dx)], 1) for l in range(layers)]
+    wall = np.concatenate(walls)
+    x = np.concatenate([fluid, inlet, outlet, wall, pool])
+    tag = np.concatenate([np.zeros(len(fluid), np.int32), np.full(len(inlet), INLET, np.int32),
+                          np.full(len(outlet), OUTLET, np.int32), np.ones(len(wall), np.int32),
+                          np.full(len(pool), DORMANT, np.int32)])
+    n = len(x)
+    u = np.zeros((n, 2))
+    # the developed profile everywhere (inlet prescribed, fluid and outlet initial): the
+    # steady state is the initial state, and the open boundaries must keep it
+    liq = (tag == INLET) | (tag == OUTLET) | (tag == FLUID)
+    u[liq, 0] = poiseuille_velocity(x[liq, 1], U, H)
+    umax = 1.5 * U
+    dt = min(0.25 * h / umax, 0.25 * h * h / nu)
+    params = default_params(rho0=rho0, nu=nu, pgrad=PGRAD_ASYMM, h_tilde_factor=1.0, pref_external=0, p_ref=0.0,
+                            ustar_noslip=1, tol=tol, precision=precision, open_x=1, x_inlet=0.0, x_outlet=Lf,
+                            x_end=Lf + L_out, inlet_length=L_in)
+    lo = [-L_in - (layers + 0.5) * dx, -(layers + 0.5) * dx, 0.0]
+    hi = [Lf + L_out + (layers + 0.5) * dx, H + (layers + 0.5) * dx, 0.0]
+    return Case("channel", 2, h, dx, dt, int(round(t_end / dt)), lo, hi, [0, 0, 0], x, u,
+                np.full(n, rho0 * dx * dx), np.full(n, rho0), np.zeros(n), tag, params)
+
+
+# --------------------------------------------------------------------------
 # C4  3D Taylor-Green vortex (BASELINE configs[3])
 # --------------------------------------------------------------------------
 def tgv3d(n: int = 128, re: float = 100.0, jitter: float = 0.05, seed: int = 104,

@@ -525,3 +525,66 @@ def test_mean_convergence_measure_is_tiling_invariant(orc):
     # here Lambda dominates the mean |p| at the minimum two sweeps: the mean reading stops
     # there, the printed sums run on (25 and 100 sweeps)
     assert r[1, 1, 1e-2][0] == 2 and r[0, 1, 1e-2][0] > 2
+
+
+# ---------------------------------------------------------------- NEXT-4b: open boundaries (R34)
+def test_open_boundary_bookkeeping(orc):
+    """Inlet -> fluid -> outlet -> dormant -> inlet: every conversion follows R34.
+    The inlet keeps its population (each conversion spawns one), prescribed and
+    frozen velocities never change, spawned inlet particles come from the lowest
+    dormant ids, and the particle count is conserved."""
+    case = synth.channel(nx=20, ny=8)
+    s = orc.Sim(case)
+    n_in = int((case.tag == synth.INLET).sum())
+    prm = case.params
+    prev_tag, prev_u, prev_x = s.tags(), s.get("u"), s.get("x")
+    seen_spawn = seen_delete = 0
+    for _ in range(40):
+        s.step(case.dt)
+        tag, u, x = s.tags(), s.get("u"), s.get("x")
+        assert s.error() == 0
+        assert (tag == synth.INLET).sum() == n_in
+        assert set(np.unique(tag)) <= {0, 1, 2, 3, 4}
+        # walls never change
+        assert np.array_equal(tag == 1, case.tag == 1)
+        # prescribed inlet velocity and frozen outlet velocity
+        stay_in = (prev_tag == synth.INLET) & (tag == synth.INLET)
+        assert np.array_equal(u[stay_in], prev_u[stay_in])
+        stay_out = (prev_tag == synth.OUTLET) & (tag == synth.OUTLET)
+        assert np.array_equal(u[stay_out], prev_u[stay_out])
+        # conversions happen at the thresholds
+        to_fluid = (prev_tag == synth.INLET) & (tag == 0)
+        assert np.all(x[to_fluid, 0] >= prm["x_inlet"])
+        to_out = (prev_tag == 0) & (tag == synth.OUTLET)
+        assert np.all(x[to_out, 0] >= prm["x_outlet"])
+        # deleted this step (some ids are drawn again by this step's spawns)
+        deleted = (prev_tag == synth.OUTLET) & ((tag == synth.DORMANT) | (tag == synth.INLET))
+        spawned = (prev_tag != synth.INLET) & (tag == synth.INLET)   # from the pool (incl. just-deleted ids)
+        assert spawned.sum() == to_fluid.sum()
+        if spawned.any():
+            # the lowest dormant ids (dormant after this step's deletions) are drawn first
+            pool = np.flatnonzero((prev_tag == synth.DORMANT) | deleted)
+            assert np.array_equal(np.flatnonzero(spawned), pool[:spawned.sum()])
+            # each new inlet particle sits one inlet length behind the one that left
+            src = np.flatnonzero(to_fluid)
+            assert np.allclose(x[spawned, 0], x[src, 0] - prm["inlet_length"], rtol=0, atol=1e-12)
+            assert np.array_equal(u[spawned], u[src])
+        seen_spawn += int(spawned.sum())
+        seen_delete += int(deleted.sum())
+        prev_tag, prev_u, prev_x = tag, u, x
+    assert seen_spawn > 0 and seen_delete > 0
+
+
+def test_channel_keeps_the_poiseuille_profile(orc):
+    """Developed plane channel flow with a parabolic inlet and a do-nothing outlet
+    (P:891-910): starting from the closed-form profile, the open boundaries keep it
+    (textbook u = 6 U y (H - y) / H^2; mid-channel, t = 2 H / U)."""
+    case = synth.channel()
+    s = orc.Sim(case)
+    for _ in range(int(round(2.0 / case.dt))):
+        s.step(case.dt)
+    tag, x, u = s.tags(), s.get("x"), s.get("u")
+    sel = (tag == 0) & (x[:, 0] > 2.0) & (x[:, 0] < 3.0)
+    err = np.abs(u[sel, 0] - synth.poiseuille_velocity(x[sel, 1], 1.0, 1.0))
+    assert err.mean() < 0.025 and err.max() < 0.06
+    assert np.abs(u[sel, 1]).max() < 0.05
