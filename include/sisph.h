@@ -40,6 +40,10 @@ extern "C" {
 
 #define SISPH_TAG_FLUID 0
 #define SISPH_TAG_WALL 1
+/* open boundaries along x (sisph_params.open_x, reading R34): */
+#define SISPH_TAG_INLET 2    /* prescribed velocity (its creation velocity), PPE unknown */
+#define SISPH_TAG_OUTLET 3   /* u and p frozen, advected with the extrapolated fluid u_x */
+#define SISPH_TAG_DORMANT 4  /* not in the flow: the id pool new inlet particles come from */
 
 typedef struct sisph sisph_t;
 
@@ -101,6 +105,14 @@ typedef struct {
                                mean|p^{k+1} - p^k| / max(Lambda, mean|p^{k+1}|) (the text calls the
                                denominator "the mean pressure" and Lambda "a measure of the mean
                                pressure"); 0 (default) = the sums as printed */
+    int open_x;             /* reading R34: 1 = open boundaries along x (single GPU,
+                               bounded x).  After every step, in id order: outlet particles with
+                               x >= x_end become dormant; fluid with x >= x_outlet become outlet
+                               (u, p frozen); inlet with x >= x_inlet become fluid, and the lowest
+                               dormant id becomes a new inlet particle at x - inlet_length with
+                               the same velocity.  TAG reads the current types; fields of dormant
+                               particles read 0.  SISPH_ENOMEM when the dormant pool runs out. */
+    double x_inlet, x_outlet, x_end, inlet_length;
     int pref_auto;          /* reading R33: 1 = the GTVF background pressure p_ref is set to
                                2 max_i p_i over fluid from the handle's first solve (internal
                                flows), then kept; 0 (default) = p_ref as given */

@@ -67,6 +67,10 @@ template <class T> struct Params {
     T g[3];
     int pgrad, pref_external, ustar_noslip, clamp_wall_p, wall_rho_summation;
     int mean_free;          // R32: remove the live-row mean of every Jacobi iterate
+    // R34 open boundaries along x: particle type of each fluid-block slot
+    // (0 fluid, 2 inlet, 3 outlet; nullptr without open boundaries)
+    const uint8_t* ptype;
+    T x_inlet, x_outlet, x_end, inlet_length;
     // GTVF inner list (pairs with r* < 3 h~ + skin; used when h~ < h)
     int cap_in;
     float Rin2f;           // (3 h~ + skin)^2 (1 + 2^-10): generous inclusion

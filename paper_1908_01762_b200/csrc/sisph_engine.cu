@@ -29,6 +29,7 @@
 #include <string>
 #include <type_traits>
 #include <utility>
+#include <set>
 #include <vector>
 
 #include "../../include/sisph.h"
@@ -121,6 +122,15 @@ template <class T, int D> struct Engine : EngineBase {
     V* uwl = nullptr;         // prescribed wall velocity per relative wall slot (eq:vg-adami)
     bool uwl_set = false;     // uwl holds the walls' values (after the first wall sort)
     int pref_auto = 0;        // R33: p_ref from the first solve
+    // R34 open boundaries: particle types of the fluid block, the dormant id pool
+    int open_x = 0;
+    std::set<int> pool;
+    uint8_t *ptype = nullptr, *ptype_alt = nullptr;
+    T* uout = nullptr;
+    int* oflag = nullptr;
+    int* olist = nullptr;
+    int* onew = nullptr;
+    int open_spawned = 0, open_deleted = 0;
     bool pref_done = false;
     V *rkA = nullptr, *rkB = nullptr, *vk = nullptr, *dk = nullptr;
     V* fnp = nullptr;       // non-pressure acceleration of A8 (adaptive dt)
@@ -185,7 +195,8 @@ template <class T, int D> struct Engine : EngineBase {
                         ccount, fstart, wstart, bsum, nbr, cnt, ctl, partials, dtmp, nbr_in, cnt_in,
                         nbs, cnt_s, wperm_s, wstart_s, coef, dflag, dflag2, dpre, dlist[0], dlist[1], dlist[2],
                         dcnt, fsend[0], fsend[1], fsend_pre[0], fsend_pre[1], grecv, wsend[0], wsend[1], wrecv,
-                        inv, sbuf[0], sbuf[1], rbuf[0], rbuf[1], wtmp, fnp, dcnt_w};
+                        inv, sbuf[0], sbuf[1], rbuf[0], rbuf[1], wtmp, fnp, dcnt_w, ptype, ptype_alt, uout,
+                        oflag, olist, onew};
         if (st) cudaStreamSynchronize(st);
         for (void* q : ptrs)
             if (q) cudaFree(q);
@@ -216,7 +227,13 @@ template <class T, int D> struct Engine : EngineBase {
         dim = D;
         tags_host.assign(tags_glob, tags_glob + n);
         std::vector<int> fid, wid;
-        for (int64_t k = 0; k < nloc; k++) (tags[k] == SISPH_TAG_FLUID ? fid : wid).push_back((int)k);
+        open_x = prm->open_x;
+        for (int64_t k = 0; k < nloc; k++) {
+            const int tg = tags[k];
+            if (tg == SISPH_TAG_DORMANT) pool.insert(gid ? (int)gid[k] : (int)k);   // R34 id pool
+            else if (tg == SISPH_TAG_WALL) wid.push_back((int)k);
+            else fid.push_back((int)k);                                             // fluid, inlet, outlet
+        }
         Nf = Nfo = (int)fid.size();
         Nw = (int)wid.size();
         Nwo = Nw;
@@ -322,8 +339,17 @@ template <class T, int D> struct Engine : EngineBase {
         P.mean_free = prm->ppe_mean_free ? 1 : 0;
         pref_auto = prm->pref_auto;
         conv_mean = prm->conv_mean;
-        nf_glob = 0;
-        for (int64_t k = 0; k < n; k++) nf_glob += tags_glob[k] == SISPH_TAG_FLUID ? 1 : 0;
+        nf_glob = 0;   // PPE unknowns: fluid (+ inlet, R34)
+        for (int64_t k = 0; k < n; k++)
+            nf_glob += (tags_glob[k] == SISPH_TAG_FLUID || tags_glob[k] == SISPH_TAG_INLET) ? 1 : 0;
+        P.x_inlet = (T)prm->x_inlet;
+        P.x_outlet = (T)prm->x_outlet;
+        P.x_end = (T)prm->x_end;
+        P.inlet_length = (T)prm->inlet_length;
+        if (open_x && rebuild_mode != 0) {
+            err = "open boundaries (open_x) need the single per-step build (rebuild_mode 0)";
+            return SISPH_EINVAL;
+        }
         for (int a = 0; a < D; a++) extent = std::max(extent, std::max(fabs(dom->lo[a]), fabs(dom->hi[a])));
         min_iter = prm->min_iter;
         max_iter = prm->max_iter;
@@ -341,11 +367,13 @@ template <class T, int D> struct Engine : EngineBase {
         // arithmetic as k_halo_flags on the working-precision positions) so that
         // the ghost-wall count is known before the allocation
         std::vector<int> hws[2];
-        if (dist()) {
+        if (dist() || open_x) {
             SCK(cudaHostAlloc((void**)&hcnt, 8 * sizeof(int), cudaHostAllocDefault));
             int rc = 0;
             dcnt = dalloc<int>(8, err, rc);
             if (rc) return rc;
+        }
+        if (dist()) {
             for (int w = 0; w < Nw; w++) {
                 const double y = (double)(T)x[(size_t)wid[w] * D + axis];
                 if (tp->nb[0] >= 0 && y < slab_lo + Gw) hws[0].push_back(w);
@@ -359,6 +387,7 @@ template <class T, int D> struct Engine : EngineBase {
         nf = Nfo;
         nw = Nwo;
         capF = dist() ? (int)(1.6 * Nfo) + 4096 : Nf;
+        if (open_x) capF = Nf + (int)pool.size() + 64;   // R34: every dormant particle may enter
         capT = capF + Nw;
         SRET(sync_counts());
         // ------------------------------------------------ allocation
@@ -375,9 +404,17 @@ template <class T, int D> struct Engine : EngineBase {
         AL(fs, uint8_t, NF) AL(fs_alt, uint8_t, NF) AL(pid, int, NT) AL(pid_alt, int, NT)
         AL(keys, int, NT) AL(rank, int, NT) AL(perm0, int, NT) AL(perm, int, NT)
         AL(ccount, int, NCT) AL(fstart, int, NCT) AL(wstart, int, NCT)
-        AL(bsum, int, (size_t)nblk(NCT, SCAN_B) + 1) AL(cnt, int, NT) AL(ctl, Ctl, 1) AL(cnt_in, int, NF)
+        // scan block sums: cell tables (NCT) and the particle compactions (NT items)
+        AL(bsum, int, (size_t)nblk(std::max(NCT, NT), SCAN_B) + 1) AL(cnt, int, NT) AL(ctl, Ctl, 1) AL(cnt_in, int, NF)
         AL(cnt_s, int, NT) AL(wperm_s, int, NW) AL(wstart_s, int, NCT)
         AL(partials, double, 2 * std::max((size_t)nblk(NF, RHS_T), (size_t)8192) + 2) AL(dtmp, double, 3 * (size_t)n)
+        if (open_x) {
+            AL(ptype, uint8_t, NF) AL(ptype_alt, uint8_t, NF) AL(uout, T, NF) AL(oflag, int, NF) AL(olist, int, NF)
+            AL(onew, int, NF)
+            if (!dist()) {
+                AL(wtmp, V, NW)   // wall-block relocation staging (the slab path allocates it too)
+            }
+        }
         if (dist()) {
             AL(dflag, int, NT) AL(dflag2, int, NT) AL(dpre, int, NT + 1) AL(dlist[0], int, NF) AL(dlist[1], int, NF)
             AL(dlist[2], int, NF) AL(fsend[0], int, NF) AL(fsend[1], int, NF) AL(fsend_pre[0], int, NF)
@@ -416,6 +453,14 @@ template <class T, int D> struct Engine : EngineBase {
         SCK(cudaMemcpyAsync(vt, hvel.data(), (size_t)Nf * sizeof(V), cudaMemcpyHostToDevice, st));  // R23
         SCK(cudaMemcpyAsync(rho, hrho.data(), nup * sizeof(T), cudaMemcpyHostToDevice, st));
         SCK(cudaMemcpyAsync(pid, hid.data(), nup * sizeof(int), cudaMemcpyHostToDevice, st));
+        std::vector<uint8_t> hty;
+        if (open_x) {
+            // R34: particle types of the fluid block (0 fluid, 2 inlet, 3 outlet)
+            hty.resize(std::max(Nf, 1));
+            for (int s = 0; s < Nf; s++) hty[s] = (uint8_t)tags[fid[s]];
+            SCK(cudaMemcpyAsync(ptype, hty.data(), Nf, cudaMemcpyHostToDevice, st));
+            P.ptype = ptype;
+        }
         if (dist())
             for (int f = 0; f < 2; f++)
                 if (nws[f]) SCK(cudaMemcpyAsync(wsend[f], hws[f].data(), nws[f] * sizeof(int), cudaMemcpyHostToDevice, st));
@@ -910,6 +955,99 @@ template <class T, int D> struct Engine : EngineBase {
         SRET(relocate_walls(Nfo));
         return sync_counts();
     }
+    // R34 conversions after the position update.  The device
+    // classifies each fluid-block row on its pre-step type; the host does the
+    // id bookkeeping in the oracle's order (deletions return ids to the pool,
+    // spawning rows draw the lowest dormant ids in ascending id order of the
+    // rows that left the inlet); the device compacts the kept rows and appends
+    // the new inlet rows behind them; the walls move to the new block end.
+    int open_boundaries()
+    {
+        open_spawned = open_deleted = 0;
+        if (Nfo == 0) return SISPH_OK;
+        ++nlaunch, k_open_classify<T><<<nblk(Nfo, 256), 256, 0, st>>>(P, pos, ptype, oflag);
+        SCK(cudaGetLastError());
+        std::vector<int> hf(Nfo), hp(Nfo);
+        std::vector<uint8_t> ht(Nfo);
+        SCK(cudaMemcpyAsync(hf.data(), oflag, Nfo * sizeof(int), cudaMemcpyDeviceToHost, st));
+        SCK(cudaMemcpyAsync(hp.data(), pid, Nfo * sizeof(int), cudaMemcpyDeviceToHost, st));
+        SCK(cudaMemcpyAsync(ht.data(), ptype, Nfo, cudaMemcpyDeviceToHost, st));
+        SCK(cudaStreamSynchronize(st));
+        std::vector<int> keep, src;
+        keep.reserve(Nfo);
+        for (int s = 0; s < Nfo; s++) {
+            if (hf[s] == 1) {
+                pool.insert(hp[s]);          // outlet -> dormant: the id returns to the pool
+                open_deleted++;
+            } else {
+                keep.push_back(s);
+                if (hf[s] == 2) src.push_back(s);
+            }
+        }
+        std::sort(src.begin(), src.end(), [&](int a, int b) { return hp[a] < hp[b]; });
+        std::vector<int> nid(src.size());
+        for (size_t q = 0; q < src.size(); q++) {
+            if (pool.empty()) {
+                err = "open boundaries: the dormant pool is exhausted (add particles with tag SISPH_TAG_DORMANT)";
+                return SISPH_ENOMEM;
+            }
+            nid[q] = *pool.begin();
+            pool.erase(pool.begin());
+        }
+        open_spawned = (int)src.size();
+        const int nkeep = (int)keep.size(), nsp = (int)src.size(), nnew = nkeep + nsp;
+        if (nnew + Nw > capT) {
+            err = "open boundaries: fluid slot capacity exceeded";
+            return SISPH_ENOMEM;
+        }
+        // a growing block first moves the walls up, so that the new rows never overlap them
+        const int nf_old = Nf;
+        if (nnew > nf_old) SRET(relocate_walls(nnew));
+        if (nkeep) SCK(cudaMemcpyAsync(perm, keep.data(), nkeep * sizeof(int), cudaMemcpyHostToDevice, st));
+        if (nsp) {
+            SCK(cudaMemcpyAsync(olist, src.data(), nsp * sizeof(int), cudaMemcpyHostToDevice, st));
+            SCK(cudaMemcpyAsync(onew, nid.data(), nsp * sizeof(int), cudaMemcpyHostToDevice, st));
+        }
+        GatherList G{};
+        gl_add(G, pos, pos_alt, sizeof(V), nkeep);
+        gl_add(G, vel, vel_alt, sizeof(V), nkeep);
+        gl_add(G, vt, vt_alt, sizeof(V), nkeep);
+        gl_add(G, p, p_alt, sizeof(T), nkeep);
+        gl_add(G, pid, pid_alt, sizeof(int), nkeep);
+        gl_add(G, rho, rho_alt, sizeof(T), nkeep);
+        gl_add(G, ptype, ptype_alt, 1, nkeep);
+        SRET(gather(G, perm, nkeep));
+        if (nsp)
+            ++nlaunch, k_open_spawn<T><<<nblk(nsp, 256), 256, 0, st>>>(P, nkeep, nsp, olist, onew, pos, vel, p, rho,
+                                                                         pos_alt, vel_alt, vt_alt, p_alt, rho_alt,
+                                                                         pid_alt, ptype_alt);
+        SCK(cudaGetLastError());
+        SRET(copy_walls_to_alt());
+        std::swap(pos, pos_alt);
+        std::swap(vel, vel_alt);
+        std::swap(vt, vt_alt);
+        std::swap(p, p_alt);
+        std::swap(pid, pid_alt);
+        std::swap(rho, rho_alt);
+        std::swap(ptype, ptype_alt);
+        P.ptype = PS.ptype = ptype;
+        SRET(copy_pos_walls(pos_alt, pos));
+        // host view of the types (TAG field) and the PPE unknown count (R12b means)
+        for (int64_t k = 0; k < n; k++)
+            if (tags_host[k] != SISPH_TAG_WALL) tags_host[k] = SISPH_TAG_DORMANT;
+        int64_t unk = 0;
+        for (int q = 0; q < nkeep; q++) {
+            const int t = ht[keep[q]];
+            tags_host[hp[keep[q]]] = t;
+            unk += (t == 0 || t == 2);
+        }
+        for (int q = 0; q < nsp; q++) tags_host[nid[q]] = SISPH_TAG_INLET;
+        nf_glob = unk + nsp;
+        Nfo = nnew;
+        if (nnew < nf_old) SRET(relocate_walls(nnew));   // a shrinking block: walls move down after
+        return sync_counts();
+    }
+
     int copy_pos_walls(V* dst, const V* src)
     {
         if (Nw) SCK(cudaMemcpyAsync(dst + Nf, src + Nf, Nw * sizeof(V), cudaMemcpyDeviceToDevice, st));
@@ -1022,6 +1160,7 @@ template <class T, int D> struct Engine : EngineBase {
         gl_add(L, pid, pid_alt, sizeof(int), Nf);
         gl_add(L, rho, rho_alt, sizeof(T), Nf);
         gl_add(L, fs, fs_alt, 1, Nf);
+        if (ptype) gl_add(L, ptype, ptype_alt, 1, Nf);
         SRET(gather(L, perm, Nf));
         // wall parts of the alternates
         SRET(copy_walls_to_alt());
@@ -1032,6 +1171,10 @@ template <class T, int D> struct Engine : EngineBase {
         std::swap(pid, pid_alt);
         std::swap(rho, rho_alt);
         std::swap(fs, fs_alt);
+        if (ptype) {
+            std::swap(ptype, ptype_alt);
+            P.ptype = PS.ptype = ptype;
+        }
         if (dist() && Nf) {
             ++nlaunch, k_invperm<<<nblk(Nf, 256), 256, 0, st>>>(perm, Nf, inv);
             for (int f = 0; f < 2; f++)
@@ -1150,6 +1293,10 @@ template <class T, int D> struct Engine : EngineBase {
             SRET(build_loose_grow());
         } else {
             SRET(plan_skin(dt, single));
+            if (open_x && !single) {
+                err = "open boundaries need the single per-step build: 2 dt max|u~| exceeds 0.3 x 3h (reduce dt)";
+                return SISPH_EINVAL;
+            }
             // A1-A5 at r^n (single build: the loose list on the skin grid)
             SRET(build_fluid(single));
         }
@@ -1206,7 +1353,12 @@ template <class T, int D> struct Engine : EngineBase {
             gl_add(G, fs, fs_alt, 1, Nf);
             gl_add(G, p, p_alt, sizeof(T), Nf);
             gl_add(G, pid, pid_alt, sizeof(int), Nf);
+            if (ptype) gl_add(G, ptype, ptype_alt, 1, Nf);
             SRET(gather(G, perm, Nf));
+            if (ptype) {
+                std::swap(ptype, ptype_alt);
+                P.ptype = PS.ptype = ptype;
+            }
             SRET(copy_walls_to_alt());
             std::swap(pos, pos_alt);
             std::swap(vel, vel_alt);
@@ -1585,9 +1737,12 @@ template <class T, int D> struct Engine : EngineBase {
                 }
             }
         }
-        // A15
-        if (Nfo) ++nlaunch, k_advance<T, D><<<nblk(Nfo, 256), 256, 0, st>>>(P, (T)dt, rK, rn, vel, pos, vt, ctl);
+        // A15 (R34: the outlet's advection velocity first, from the fluid's u^{n+1} at r^n)
+        if (open_x && Nfo)
+            ++nlaunch, k_outlet_velocity<T, D><<<nblk(Nfo, 256), 256, 0, st>>>(P, rn, vel, nbs, cnt_s, cap_s, uout);
+        if (Nfo) ++nlaunch, k_advance<T, D><<<nblk(Nfo, 256), 256, 0, st>>>(P, (T)dt, rK, rn, vel, pos, vt, ctl, uout);
         SCK(cudaGetLastError());
+        if (open_x) SRET(open_boundaries());
         phase = IDLE;
         stepped = true;
         return SISPH_OK;
@@ -2030,7 +2185,8 @@ static int validate(const double* positions, const double* velocities, const dou
     }
     int64_t nfl = 0;
     for (int64_t k = 0; k < n; k++) {
-        if (tags[k] != 0 && tags[k] != 1) return fail_thread(SISPH_EINVAL, "tag must be 0 (fluid) or 1 (wall)");
+        if (tags[k] < 0 || tags[k] > (prm.open_x ? 4 : 1))
+            return fail_thread(SISPH_EINVAL, "tag must be 0 (fluid) or 1 (wall) (2-4 with open_x)");
         nfl += tags[k] == 0;
         if (!(masses[k] > 0) || !(densities[k] > 0) || !std::isfinite(masses[k]) || !std::isfinite(densities[k]))
             return fail_thread(SISPH_EINVAL, "masses and densities must be finite and > 0");
@@ -2048,6 +2204,9 @@ static int validate(const double* positions, const double* velocities, const dou
         }
     }
     if (nfl == 0) return fail_thread(SISPH_EINVAL, "no fluid particle");
+    if (prm.open_x && (domain->periodic[0] || !(prm.inlet_length > 0) || !(prm.x_inlet <= prm.x_outlet) ||
+                       !(prm.x_outlet <= prm.x_end)))
+        return fail_thread(SISPH_EINVAL, "open_x needs a bounded x axis, inlet_length > 0 and x_inlet <= x_outlet <= x_end");
     return SISPH_OK;
 }
 
@@ -2166,6 +2325,7 @@ int sisph_create_dist(const double* positions, const double* velocities, const d
     if (P_ < 1 || r < 0 || r >= P_ || ax < 0 || ax >= dim) return fail_thread(SISPH_EINVAL, "bad nranks / rank / slab_axis");
     if (P_ == 1 && !dist->always_slab)
         return sisph_create(positions, velocities, masses, densities, tags, n, h, domain, params, out);
+    if (prm.open_x) return fail_thread(SISPH_EINVAL, "open boundaries (open_x) run on a single handle");
     const double L = domain->hi[ax] - domain->lo[ax];
     if (L / P_ < 1.3 * 3.0 * h * 1.01)
         return fail_thread(SISPH_EINVAL, "slabs thinner than the halo width 1.3 x 3h");

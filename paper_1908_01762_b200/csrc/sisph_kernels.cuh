@@ -798,7 +798,9 @@ __global__ void __launch_bounds__(256) k_density(Params<T> P, const V4<T>* __res
     s = xi.w * P.w0 + P.sig * s;
     rho[i] = s;
     if (i < P.Nf) {
-        fs[i] = (s / P.rho0 < P.fs_ratio) ? 1 : 0;
+        const int ty = P.ptype ? P.ptype[i] : 0;
+        // fs: 1 free surface (fluid only, R11); 2 outlet row (R34: p frozen, not a PPE unknown)
+        fs[i] = ty == 3 ? 2 : (ty == 0 && s / P.rho0 < P.fs_ratio ? 1 : 0);
         // rho_i rides in the 4th lane of u_i: the force pass gathers one vector less per pair
         reinterpret_cast<T*>(vel + i)[3] = s;
     }
@@ -945,6 +947,11 @@ __global__ void __launch_bounds__(128) k_forces_predict(Params<T> P, T dt, const
     T dux = uti.x - ui.x, duy = uti.y - ui.y, duz = D == 3 ? uti.z - ui.z : T(0);
     const T irhoi = frcp(rhoi);
     int n = cnt[i];
+    if (P.ptype && P.ptype[i] != 0) {
+        // R34: inlet (prescribed) / outlet (frozen) velocity: u* = u, only r* = r + dt u~
+        ax = ay = az = T(0);
+        n = 0;
+    }
     for_nbrs(nbr, ncap, i, n, [&](int j) {
         // (loose-list pairs beyond 3h contribute exactly 0: dW/dr = 0 for q >= 3)
         V4<T> xj = ld4(pos + j), uj = ld4(vel + j);
@@ -1010,14 +1017,15 @@ __global__ void __launch_bounds__(RHS_T) k_rhs_diag(Params<T> P, T inv_dt, const
         sr *= -P.dwk * inv_dt;
         const T scale = T(4) * P.dwk * frcp(rhoi);
         sd *= scale;
-        rhs[i] = sr;
-        diag[i] = sd;
+        const bool frozen = fs[i] == 2;                 // R34 outlet row: not a PPE unknown
+        rhs[i] = frozen ? T(0) : sr;
+        diag[i] = frozen ? T(0) : sd;
         const bool live = !fs[i] && sd != T(0);
         if (live) lam = (double)fabs(sr / sd);
         if (pin) {
             // eq:p-sor with p^k = p^0, exactly as k_sweep (same expression order)
             const T pold = pin[i];
-            T pnew = T(0);
+            T pnew = frozen ? pold : T(0);
             if (live) {
                 sp *= scale;
                 pnew = P.omega * (sr + sp) * frcp(sd) + (T(1) - P.omega) * pold;
@@ -1029,7 +1037,7 @@ __global__ void __launch_bounds__(RHS_T) k_rhs_diag(Params<T> P, T inv_dt, const
                 dd = live ? 1.0 : 0.0;
             } else {
                 dn = fabs((double)pnew - (double)pold);
-                dd = fabs((double)pnew);
+                dd = frozen ? 0.0 : fabs((double)pnew);
             }
             bad = !isfinite((double)pnew);
         }
@@ -1187,7 +1195,7 @@ __device__ __forceinline__ T sweep_row(const Params<T>& P, int i, const V4<T>* _
                                        const T* __restrict__ diag, const T* pin)
 {
     const T pold = pin[i];
-    T pnew = T(0);
+    T pnew = fs[i] == 2 ? pold : T(0);                 // R34 outlet rows keep their frozen p
     const T di = diag[i];
     if (!fs[i] && di != T(0)) {
         const T rhoi = rho[i];
@@ -1270,7 +1278,7 @@ __global__ void __launch_bounds__(SWEEP_T) k_sweep(Params<T> P, const PpeDesc<T>
             dd = live ? 1.0 : 0.0;
         } else {
             dn = fabs((double)pnew - (double)pold);
-            dd = fabs((double)pnew);
+            dd = fs[i] == 2 ? 0.0 : fabs((double)pnew);   // eq:convergence over the unknown rows
         }
         bad = !isfinite((double)pnew);
     }
@@ -1377,7 +1385,7 @@ __global__ void __launch_bounds__(SWEEP_T) k_mean_fix(Params<T> P, const PpeDesc
             pout[i] = v;
         }
         dn = fabs((double)v - (double)pin[i]);
-        dd = fabs((double)v);
+        dd = fs[i] == 2 ? 0.0 : fabs((double)v);
         bad = !isfinite((double)v);
     }
     __shared__ double sn[SWEEP_T / 32], sd[SWEEP_T / 32];
@@ -1523,7 +1531,7 @@ __global__ void __launch_bounds__(SWEEP_T) k_ppe_persistent(Params<T> P, const P
             const T pnew = sweep_row<T, D, STORED>(P, i, pos, rho, fs, nbr, cnt, ncap, coef, rhs, diag, pin);
             pout[i] = pnew;
             dn += fabs((double)pnew - (double)pold);
-            dd += fabs((double)pnew);
+            dd += fs[i] == 2 ? 0.0 : fabs((double)pnew);
             bad = bad || !isfinite((double)pnew);
         }
         dn = warp_sum(dn);
@@ -1600,6 +1608,7 @@ __global__ void __launch_bounds__(128) k_pgrad_correct(Params<T> P, T dt, const 
         T pir = pi * irhoi * irhoi;
         T ax = 0, ay = 0, az = 0;
         int n = cnt[i];
+        if (P.ptype && P.ptype[i] != 0) n = 0;       // R34: inlet / outlet keep u* = u
         for_nbrs(nbr, ncap, i, n, [&](int j) {
             V4<T> xj = ld4(pos + j);
             T rhoj = __ldg(rho + j), pj = __ldg(p + j);
@@ -1667,6 +1676,7 @@ __global__ void __launch_bounds__(128) k_gtvf_substep(Params<T> P, T dtau, const
     V4<T> xi = ld4(rk + i);
     T ax = 0, ay = 0, az = 0;
     int n = cnt[i];
+    if (P.ptype && P.ptype[i] != 0) n = 0;           // R34: no GTVF shift for inlet / outlet
     for_nbrs(nbr, ncap, i, n, [&](int j) {
         V4<T> xj = ld4(rk + j);
         T d[3], r, ri;
@@ -1704,11 +1714,27 @@ __global__ void __launch_bounds__(128) k_gtvf_substep(Params<T> P, T dtau, const
 // ===========================================================================
 template <class T, int D>
 __global__ void k_advance(Params<T> P, T dt, const V4<T>* __restrict__ dK, const V4<T>* __restrict__ rn,
-                          const V4<T>* __restrict__ vel, V4<T>* __restrict__ pos, V4<T>* __restrict__ vt, Ctl* ctl)
+                          const V4<T>* __restrict__ vel, V4<T>* __restrict__ pos, V4<T>* __restrict__ vt, Ctl* ctl,
+                          const T* __restrict__ uout)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     double v2 = 0.0;
-    if (i < P.Nfo) {
+    const int ptp = (P.ptype && i < P.Nfo) ? P.ptype[i] : 0;
+    if (ptp == 2) {
+        // R34 inlet: r^{n+1} = r^n + dt u (prescribed), u~ = u
+        const V4<T> x = ld4(rn + i), u = ld4(vel + i);
+        T X = x.x + dt * u.x, Y = x.y + dt * u.y, Z = D == 3 ? x.z + dt * u.z : x.z;
+        if (P.per[1]) { if (Y >= P.hi[1]) Y -= P.L[1]; else if (Y < P.lo[1]) Y += P.L[1]; }
+        if (D == 3 && P.per[2]) { if (Z >= P.hi[2]) Z -= P.L[2]; else if (Z < P.lo[2]) Z += P.L[2]; }
+        pos[i] = mk4<T>(X, Y, Z, x.w);
+        vt[i] = mk4<T>(u.x, u.y, D == 3 ? u.z : T(0), T(0));
+    } else if (ptp == 3) {
+        // R34 outlet: moved along x with the extrapolated fluid u_x; u, p frozen
+        const V4<T> x = ld4(rn + i);
+        const T ux = uout[i];
+        pos[i] = mk4<T>(x.x + dt * ux, x.y, x.z, x.w);
+        vt[i] = mk4<T>(ux, T(0), T(0), T(0));
+    } else if (i < P.Nfo) {
         V4<T> x = ld4(rn + i), u = ld4(vel + i), ut = ld4(vt + i);
         V4<T> dl = dK ? ld4(dK + i) : mk4<T>(T(0), T(0), T(0), T(0));   // r^K - r^0
         T tx = u.x + dl.x / dt, ty = u.y + dl.y / dt;
@@ -1723,6 +1749,80 @@ __global__ void k_advance(Params<T> P, T dt, const V4<T>* __restrict__ dK, const
         v2 = (double)u.x * u.x + (double)u.y * u.y + (D == 3 ? (double)u.z * u.z : 0.0);   // |u^{n+1}|^2
     }
     warp_max_to(v2, &ctl->vmax2_bits);
+}
+
+// ===========================================================================
+// R34 open boundaries
+// ===========================================================================
+// the outlet's advection velocity: Shepard_h of the fluid's u_x^{n+1} at r^n
+// (fluid sources of the r^n list; none in the support: the frozen u_x)
+template <class T, int D>
+__global__ void k_outlet_velocity(Params<T> P, const V4<T>* __restrict__ rn, const V4<T>* __restrict__ vel,
+                                  const int* __restrict__ nbr, const int* __restrict__ cnt, int ncap,
+                                  T* __restrict__ uout)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.Nfo || P.ptype[i] != 3) return;
+    const V4<T> xi = ld4(rn + i);
+    T sw = 0, su = 0;
+    for_nbrs(nbr, cnt ? ncap : 0, i, cnt ? cnt[i] : 0, [&](int j) {
+        if (j >= P.Nf || P.ptype[j] != 0) return;
+        T d[3], r, ri;
+        const T r2 = pair_vec<T, D>(P, xi, ld4(rn + j), d);
+        if (r2 >= P.R2cut) return;                    // W = 0 beyond 3h (loose list)
+        r_of(r2, r, ri);
+        const T w = P.sig * quintic5(r * P.inv_h);
+        su += vel[j].x * w;
+        sw += w;
+    });
+    uout[i] = sw > T(0) ? su / sw : vel[i].x;
+}
+
+// conversions after the position update, on the pre-step types:
+//   outlet with x >= x_end -> deleted (flag 1); fluid with x >= x_outlet -> outlet;
+//   inlet with x >= x_inlet -> fluid and spawns one inlet particle (flag 2)
+template <class T>
+__global__ void k_open_classify(Params<T> P, const V4<T>* __restrict__ pos, uint8_t* __restrict__ ptype,
+                                int* __restrict__ flag)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.Nfo) return;
+    const int ty = ptype[i];
+    const T x = pos[i].x;
+    int f = 0;
+    if (ty == 3 && x >= P.x_end) {
+        f = 1;
+    } else if (ty == 0 && x >= P.x_outlet) {
+        ptype[i] = 3;
+    } else if (ty == 2 && x >= P.x_inlet) {
+        ptype[i] = 0;
+        f = 2;
+    }
+    flag[i] = f;
+}
+
+// new inlet rows [base, base + n): copies of the spawning rows src[k] (pre-compaction
+// arrays), one inlet length upstream, with the ids drawn from the pool
+template <class T>
+__global__ void k_open_spawn(Params<T> P, int base, int n, const int* __restrict__ src,
+                             const int* __restrict__ newid, const V4<T>* __restrict__ pos0,
+                             const V4<T>* __restrict__ vel0, const T* __restrict__ p0, const T* __restrict__ rho0,
+                             V4<T>* __restrict__ pos, V4<T>* __restrict__ vel, V4<T>* __restrict__ vt,
+                             T* __restrict__ p, T* __restrict__ rho, int* __restrict__ pid, uint8_t* __restrict__ ptype)
+{
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const int s = src[k], d = base + k;
+    V4<T> x = pos0[s];
+    x.x = x.x - P.inlet_length;
+    pos[d] = x;
+    const V4<T> u = vel0[s];
+    vel[d] = u;
+    vt[d] = mk4<T>(u.x, u.y, u.z, T(0));
+    p[d] = p0[s];
+    rho[d] = rho0[s];
+    pid[d] = newid[k];
+    ptype[d] = 2;
 }
 
 // ===========================================================================

@@ -46,7 +46,8 @@ class sisph_params(C.Structure):
         ("tol", C.c_double), ("wall_rho_summation", C.c_int), ("nbr_cap", C.c_int),
         ("device", C.c_int), ("stream", C.c_void_p), ("rebuild_mode", C.c_int),
         ("matrix_free", C.c_int), ("ppe_loop", C.c_int), ("ppe_mean_free", C.c_int),
-        ("conv_mean", C.c_int), ("pref_auto", C.c_int),
+        ("conv_mean", C.c_int), ("open_x", C.c_int), ("x_inlet", C.c_double), ("x_outlet", C.c_double),
+        ("x_end", C.c_double), ("inlet_length", C.c_double), ("pref_auto", C.c_int),
     ]
 
 

@@ -615,3 +615,55 @@ def test_fp32_host_io_matches_fp64_io():
     assert rb.iters == rc.iters
     for fld in ("POSITION", "VELOCITY", "PRESSURE"):
         assert np.array_equal(b.get(fld), c.get(fld)), fld
+
+
+# ------------------------------------------------------------------ NEXT-4b: open boundaries (R34)
+def test_open_boundary_parity_fp64():
+    """Inlet / outlet / dormant conversions and the id pool (reading R34): the CUDA
+    path and the oracle, free running from the same inputs, agree on every type
+    change and id draw (bit-exact TAG field), on the sweep counts, and on the
+    fields of the active particles (fp64 tolerance)."""
+    import oracle
+    case = synth.channel(nx=20, ny=8)
+    sim = gpu_sim(case)
+    o = oracle.Sim(case)
+    moved = 0
+    for s in range(40):
+        rg = sim.step(case.dt)
+        it_o, res_o, _ = o.step(case.dt)
+        if abs(res_o - case.params["tol"]) > 1e-9 * case.params["tol"]:
+            assert rg.iters == it_o, (s, rg.iters, it_o)
+        tg, to = sim.get("TAG").astype(np.int32), o.tags()
+        assert np.array_equal(tg, to), s
+        act = (to == 0) | (to == synth.INLET) | (to == synth.OUTLET)
+        assert_close(f"x {s}", sim.get("POSITION")[act], o.get("x")[act], 64, scale=1.0)
+        assert_close(f"u {s}", sim.get("VELOCITY")[act], o.get("u")[act], 64, scale=1.5)
+        assert_close(f"p {s}", sim.get("PRESSURE")[act], o.get("p")[act], 64,
+                     scale=max(np.abs(o.get("p")[act]).max(), 1e-3))
+        moved += int((to != case.tag).sum())
+    assert moved > 0
+    # dormant ids read zero
+    dorm = o.tags() == synth.DORMANT
+    assert np.all(sim.get("POSITION")[dorm] == 0)
+
+
+def test_open_boundary_pool_exhaustion_is_an_error():
+    from paper_1908_01762_b200 import SisphError
+    case = synth.channel(nx=20, ny=8, n_pool=0)
+    sim = gpu_sim(case)
+    with pytest.raises(SisphError) as e:
+        for _ in range(200):
+            sim.step(case.dt)
+    assert "dormant pool" in str(e.value)
+
+
+def test_channel_keeps_the_poiseuille_profile_gpu():
+    """The oracle's closed-form pin on the CUDA path (same bound)."""
+    case = synth.channel()
+    sim = gpu_sim(case)
+    for _ in range(int(round(2.0 / case.dt))):
+        sim.step(case.dt)
+    tag, x, u = sim.get("TAG"), sim.get("POSITION"), sim.get("VELOCITY")
+    sel = (tag == 0) & (x[:, 0] > 2.0) & (x[:, 0] < 3.0)
+    err = np.abs(u[sel, 0] - synth.poiseuille_velocity(x[sel, 1], 1.0, 1.0))
+    assert err.mean() < 0.025 and err.max() < 0.06
