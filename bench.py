@@ -268,13 +268,17 @@ def run_sisph(args):
     barrier()
     reps = []
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # one event per step boundary as well (the median step)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
         e0.record(stream)
-        for _ in range(args.steps):
+        for k in range(args.steps):
             reps.append(sim.step(case.dt))
+            ev[k].record(stream)
         e1.record(stream)
         barrier()
     ms_rank = e0.elapsed_time(e1)
+    step_ms = [e0.elapsed_time(ev[0])] + [ev[k - 1].elapsed_time(ev[k]) for k in range(1, args.steps)]
     ms = D.max_over_ranks(ms_rank, dev) if world > 1 else ms_rank   # the job's time: its slowest rank
     sweeps = sum(r.iters for r in reps)   # identical on every rank (allreduced decision)
     value = sweeps * nf / (ms / 1e3)      # all ranks' fluid particles
@@ -322,6 +326,7 @@ def run_sisph(args):
                          % (4 * pairs / 1e9, 24 * n_loc / 1e6),
                    "parallelism": f"slab x{world}" + (f" along axis {SLAB_AXIS[args.workload]}, NCCL halos + "
                                                       "per-sweep allreduce" if world > 1 else "")},
+        "ms_per_step_median": float(np.median(step_ms)),
         "ppe_phase_particle_sweeps_per_s": sweeps_i * nf / (ms_solve_i / 1e3),
         "sweeps_per_step": sweeps / args.steps,
         "single_build_steps": sum(r.single_build for r in reps),
@@ -336,6 +341,10 @@ def run_sisph(args):
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": sweep_traffic(), "bytes_per_launch": b_per, "pairs_per_launch": pairs,
                      "avg_launch_us": avg_s * 1e6, "launches_timed": n_sw,
+                     # interactions/s and the logical gather bandwidth (the
+                     # p_j each interaction gathers; served by L1/L2, not an HBM fraction)
+                     "interactions_per_s": pairs / avg_s,
+                     "gather_logical_GBs": tb * pairs / avg_s / 1e9,
                      "how": "20 sweep launches of a fixed-sweep solve after the timed region, CUDA events",
                      "peak_source": peak_src},
         "gpu_launches": int(sum(r.launches for r in reps)),
