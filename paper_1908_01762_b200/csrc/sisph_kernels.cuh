@@ -1185,6 +1185,18 @@ __global__ void __launch_bounds__(256) k_ppe_wall(Params<T> P, const PpeDesc<T>*
 // takes the stop decision (R12, R13) on the device.
 // ===========================================================================
 constexpr int SWEEP_T = 256;
+// stored sweep: prefetch distance (chunks of 4 entries; 0 = none) and the minimum
+// resident blocks per SM of the fp32 kernel (a 64-register cap: 4 x 256 threads).
+// Tuned on B200 with A/B builds (build.py --out ... -DSISPH_SWEEP_PF=...):
+// PD 0 / 2 / 3 / 4 / 4 capped -> 0.79 / 0.88 / 0.89 / 0.89 / 0.92 of the measured HBM
+// bandwidth on C5; PD 5-8 fall off the occupancy cliff (2 blocks per SM).
+#ifndef SISPH_SWEEP_PF
+#define SISPH_SWEEP_PF 4
+#endif
+#ifndef SISPH_SWEEP_MINB
+#define SISPH_SWEEP_MINB 4
+#endif
+template <class T> constexpr int sweep_minb() { return sizeof(T) == 4 ? SISPH_SWEEP_MINB : 1; }
 
 // eq:p-sor for row i from p^k = pin (the stored or the recomputed fac_ij)
 template <class T, int D, bool STORED>
@@ -1204,6 +1216,41 @@ __device__ __forceinline__ T sweep_row(const Params<T>& P, int i, const V4<T>* _
         if (STORED) {
             const size_t b = nb_base(i, ncap);
             const int4* __restrict__ qi = reinterpret_cast<const int4*>(nbr + b);
+#if SISPH_SWEEP_PF > 0
+            // software pipelining: a register ring keeps the index + factor loads of the next
+            // PD chunks in flight while this chunk's p_j are gathered (B200: the streamed
+            // HBM traffic needs more bytes in flight per SM than one chunk per row gives;
+            // PD = 4 at a 64-register cap measured best, 0.92 of the measured HBM bandwidth)
+            constexpr int PD = SISPH_SWEEP_PF;
+            int4 vr[PD];
+            T fr[PD][4];
+#pragma unroll
+            for (int q = 0; q < PD; q++) {
+                const int c = 4 * q;
+                vr[q] = c < n ? __ldcs(qi + (size_t)(c >> 2) * 32) : make_int4(i, i, i, i);
+                if (c < n) ld_chunk4(coef + b + ((size_t)(c >> 2) * 32 << 2), fr[q]);
+                else fr[q][0] = fr[q][1] = fr[q][2] = fr[q][3] = T(0);
+            }
+            for (int c = 0; c < n; c += 4) {
+                const int cn = c + 4 * PD;
+                const int4 vnew = cn < n ? __ldcs(qi + (size_t)(cn >> 2) * 32) : make_int4(i, i, i, i);
+                T fnew[4] = {T(0), T(0), T(0), T(0)};
+                if (cn < n) ld_chunk4(coef + b + ((size_t)(cn >> 2) * 32 << 2), fnew);
+                s += fr[0][0] * __ldg(pin + vr[0].x);
+                if (c + 1 < n) s += fr[0][1] * __ldg(pin + vr[0].y);
+                if (c + 2 < n) s += fr[0][2] * __ldg(pin + vr[0].z);
+                if (c + 3 < n) s += fr[0][3] * __ldg(pin + vr[0].w);
+#pragma unroll
+                for (int q = 0; q < PD - 1; q++) {
+                    vr[q] = vr[q + 1];
+#pragma unroll
+                    for (int e = 0; e < 4; e++) fr[q][e] = fr[q + 1][e];
+                }
+                vr[PD - 1] = vnew;
+#pragma unroll
+                for (int e = 0; e < 4; e++) fr[PD - 1][e] = fnew[e];
+            }
+#else
             for (int c = 0; c < n; c += 4) {
                 const size_t o = (size_t)(c >> 2) * 32;
                 const int4 v = __ldcs(qi + o);
@@ -1214,6 +1261,7 @@ __device__ __forceinline__ T sweep_row(const Params<T>& P, int i, const V4<T>* _
                 if (c + 2 < n) s += f[2] * pin[v.z];
                 if (c + 3 < n) s += f[3] * pin[v.w];
             }
+#endif
         } else {
             const V4<T> xi = ld4(pos + i);
             for_nbrs(nbr, ncap, i, n, [&](int j) {
@@ -1244,7 +1292,7 @@ __device__ __forceinline__ T sweep_row(const Params<T>& P, int i, const V4<T>* _
 // graph and sets the loop condition (continue = not done) from the last
 // block; a sweep launched after the decision only clears it.
 template <class T, int D, bool STORED>
-__global__ void __launch_bounds__(SWEEP_T) k_sweep(Params<T> P, const PpeDesc<T>* __restrict__ dsc,
+__global__ void __launch_bounds__(SWEEP_T, sweep_minb<T>()) k_sweep(Params<T> P, const PpeDesc<T>* __restrict__ dsc,
                                                    const T* __restrict__ rhs, const T* __restrict__ diag,
                                                    const int* __restrict__ cnt, int ncap, Ctl* ctl,
                                                    double* __restrict__ partials, int defer,
