@@ -277,6 +277,28 @@ __device__ __forceinline__ void for_nbrs(const int* __restrict__ nbr, int cap, i
     }
 }
 
+// same, with the index chunks of the next PD chunks in flight (register ring)
+template <int PD, class F>
+__device__ __forceinline__ void for_nbrs_pf(const int* __restrict__ nbr, int cap, int i, int n, F&& f)
+{
+    const int4* __restrict__ q = reinterpret_cast<const int4*>(nbr + nb_base(i, cap));
+    int4 r[PD];
+#pragma unroll
+    for (int k = 0; k < PD; k++) r[k] = 4 * k < n ? __ldcs(q + (size_t)k * 32) : make_int4(0, 0, 0, 0);
+    for (int c = 0; c < n; c += 4) {
+        const int cn = c + 4 * PD;
+        const int4 nx = cn < n ? __ldcs(q + (size_t)(cn >> 2) * 32) : make_int4(0, 0, 0, 0);
+        const int4 v = r[0];
+        f(v.x);
+        if (c + 1 < n) f(v.y);
+        if (c + 2 < n) f(v.z);
+        if (c + 3 < n) f(v.w);
+#pragma unroll
+        for (int k = 0; k < PD - 1; k++) r[k] = r[k + 1];
+        r[PD - 1] = nx;
+    }
+}
+
 // same, also passing the entry number k
 template <class F>
 __device__ __forceinline__ void for_nbrs_k(const int* __restrict__ nbr, int cap, int i, int n, F&& f)
@@ -1725,7 +1747,10 @@ __global__ void __launch_bounds__(128) k_gtvf_substep(Params<T> P, T dtau, const
     T ax = 0, ay = 0, az = 0;
     int n = cnt[i];
     if (P.ptype && P.ptype[i] != 0) n = 0;           // R34: no GTVF shift for inlet / outlet
-    for_nbrs(nbr, ncap, i, n, [&](int j) {
+#ifndef SISPH_GTVF_PF
+#define SISPH_GTVF_PF 1   // B200, C5: PD 0 / 1 / 2 / 3 -> 113 / 107 / 125 / 120 us per sub-step
+#endif
+    for_nbrs_pf<SISPH_GTVF_PF>(nbr, ncap, i, n, [&](int j) {
         V4<T> xj = ld4(rk + j);
         T d[3], r, ri;
         r_of(pair_vec<T, D>(P, xi, xj, d), r, ri);
