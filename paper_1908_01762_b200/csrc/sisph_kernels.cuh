@@ -299,6 +299,28 @@ __device__ __forceinline__ void for_nbrs_pf(const int* __restrict__ nbr, int cap
     }
 }
 
+// PD = 0: for_nbrs; PD > 0: for_nbrs_pf<PD> (per-pass prefetch switches, tuned by A/B builds)
+template <int PD, class F>
+__device__ __forceinline__ void for_nbrs_pfx(const int* __restrict__ nbr, int cap, int i, int n, F&& f)
+{
+    if constexpr (PD == 0) for_nbrs(nbr, cap, i, n, f);
+    else for_nbrs_pf<PD>(nbr, cap, i, n, f);
+}
+// B200, C5 (us per launch, PD 0 / 1 / 2): density 435 / 415 / 430, forces 1350 / 1367 / 1278,
+// f_p 513 / 500 / 504, wall pressure 46.7 / 42.9 / 41.4
+#ifndef SISPH_DENS_PF
+#define SISPH_DENS_PF 1
+#endif
+#ifndef SISPH_FORCES_PF
+#define SISPH_FORCES_PF 2
+#endif
+#ifndef SISPH_WALLP_PF
+#define SISPH_WALLP_PF 2
+#endif
+#ifndef SISPH_PGRAD_PF
+#define SISPH_PGRAD_PF 1
+#endif
+
 // same, also passing the entry number k
 template <class F>
 __device__ __forceinline__ void for_nbrs_k(const int* __restrict__ nbr, int cap, int i, int n, F&& f)
@@ -811,7 +833,7 @@ __global__ void __launch_bounds__(256) k_density(Params<T> P, const V4<T>* __res
     }
     T s = 0;
     int n = cnt[i];
-    for_nbrs(nbr, ncap, i, n, [&](int j) {
+    for_nbrs_pfx<SISPH_DENS_PF>(nbr, ncap, i, n, [&](int j) {
         V4<T> xj = ld4(pos + j);
         T d[3], r, ri;
         r_of(pair_vec<T, D>(P, xi, xj, d), r, ri);
@@ -974,7 +996,7 @@ __global__ void __launch_bounds__(128) k_forces_predict(Params<T> P, T dt, const
         ax = ay = az = T(0);
         n = 0;
     }
-    for_nbrs(nbr, ncap, i, n, [&](int j) {
+    for_nbrs_pfx<SISPH_FORCES_PF>(nbr, ncap, i, n, [&](int j) {
         // (loose-list pairs beyond 3h contribute exactly 0: dW/dr = 0 for q >= 3)
         V4<T> xj = ld4(pos + j), uj = ld4(vel + j);
         const bool fl = j < P.Nf;
@@ -1152,7 +1174,7 @@ __device__ __forceinline__ void wall_pressure_row(const Params<T>& P, int w, con
     V4<T> xi = ld4(pos + i);
     T sw = 0, sp = 0, sx = 0, sy = 0, sz = 0;
     int n = cnt[i];
-    for_nbrs(nbr, ncap, i, n, [&](int j) {
+    for_nbrs_pfx<SISPH_WALLP_PF>(nbr, ncap, i, n, [&](int j) {
         if (j >= P.Nf) return;
         V4<T> xj = ld4(pos + j);
         T d[3], r, ri;
@@ -1679,7 +1701,7 @@ __global__ void __launch_bounds__(128) k_pgrad_correct(Params<T> P, T dt, const 
         T ax = 0, ay = 0, az = 0;
         int n = cnt[i];
         if (P.ptype && P.ptype[i] != 0) n = 0;       // R34: inlet / outlet keep u* = u
-        for_nbrs(nbr, ncap, i, n, [&](int j) {
+        for_nbrs_pfx<SISPH_PGRAD_PF>(nbr, ncap, i, n, [&](int j) {
             V4<T> xj = ld4(pos + j);
             T rhoj = __ldg(rho + j), pj = __ldg(p + j);
             T d[3], r, ri;
