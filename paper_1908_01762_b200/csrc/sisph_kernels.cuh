@@ -299,6 +299,39 @@ __device__ __forceinline__ void for_nbrs_pf(const int* __restrict__ nbr, int cap
     }
 }
 
+// for_nbrs_k with the index chunks of the next PD chunks in flight
+template <int PD, class F>
+__device__ __forceinline__ void for_nbrs_k_pf(const int* __restrict__ nbr, int cap, int i, int n, F&& f)
+{
+    if constexpr (PD == 0) {
+        for_nbrs_k(nbr, cap, i, n, f);
+    } else {
+        const int4* __restrict__ q = reinterpret_cast<const int4*>(nbr + nb_base(i, cap));
+        int4 r[PD];
+#pragma unroll
+        for (int k = 0; k < PD; k++) r[k] = 4 * k < n ? __ldcs(q + (size_t)k * 32) : make_int4(0, 0, 0, 0);
+        for (int c = 0; c < n; c += 4) {
+            const int cn = c + 4 * PD;
+            const int4 nx = cn < n ? __ldcs(q + (size_t)(cn >> 2) * 32) : make_int4(0, 0, 0, 0);
+            const int4 v = r[0];
+            f(v.x, c);
+            if (c + 1 < n) f(v.y, c + 1);
+            if (c + 2 < n) f(v.z, c + 2);
+            if (c + 3 < n) f(v.w, c + 3);
+#pragma unroll
+            for (int k = 0; k < PD - 1; k++) r[k] = r[k + 1];
+            r[PD - 1] = nx;
+        }
+    }
+}
+// B200, C5 (us per launch, PD 0 / 1 / 2): A11 1105 / 1100 / 1059, wall velocity 46.7 / 39.3 / 39.5
+#ifndef SISPH_RHS_PF
+#define SISPH_RHS_PF 2
+#endif
+#ifndef SISPH_WALLV_PF
+#define SISPH_WALLV_PF 1
+#endif
+
 // PD = 0: for_nbrs; PD > 0: for_nbrs_pf<PD> (per-pass prefetch switches, tuned by A/B builds)
 template <int PD, class F>
 __device__ __forceinline__ void for_nbrs_pfx(const int* __restrict__ nbr, int cap, int i, int n, F&& f)
@@ -870,7 +903,7 @@ __global__ void __launch_bounds__(256) k_wall_velocity(Params<T> P, const V4<T>*
     V4<T> xi = ld4(pos + i);
     T sw = 0, ax = 0, ay = 0, az = 0;
     int n = cnt[i];
-    for_nbrs(nbr, ncap, i, n, [&](int j) {
+    for_nbrs_pfx<SISPH_WALLV_PF>(nbr, ncap, i, n, [&](int j) {
         if (j >= P.Nf) return;
         V4<T> xj = ld4(pos + j);
         T d[3], r, ri;
@@ -1040,7 +1073,7 @@ __global__ void __launch_bounds__(RHS_T) k_rhs_diag(Params<T> P, T inv_dt, const
         T sr = 0, sd = 0, sp = 0;
         int n = cnt[i];
         T* __restrict__ crow = coef ? coef + nb_base(i, ncap) : nullptr;
-        for_nbrs_k(nbr, ncap, i, n, [&](int j, int k) {
+        for_nbrs_k_pf<SISPH_RHS_PF>(nbr, ncap, i, n, [&](int j, int k) {
             V4<T> xj = ld4(pos + j), uj = ld4(us + j);
             T rhoj = uj.w;                           // rho_j rides in u*_j's 4th lane
             T d[3], r, ri;
