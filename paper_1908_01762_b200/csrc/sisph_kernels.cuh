@@ -761,11 +761,22 @@ __global__ void __launch_bounds__(128) k_filter(Params<T> P, int row0, int nrows
         crow = coef ? coef + nb_base(i, cap) : nullptr;
     }
     const int4* __restrict__ src = reinterpret_cast<const int4*>(nbs + nb_base(i, cap_s));
-    int4 vnext = n > 0 ? __ldcs(src) : make_int4(i, i, i, i);
+#ifndef SISPH_FILTER_PF
+#define SISPH_FILTER_PF 1   // B200, C5: PD 1 / 2 / 3 -> 1214 / 1204 / 1201 us
+#endif
+    // the index chunks of the next SISPH_FILTER_PF chunks stay in flight while one is tested
+    int4 vr[SISPH_FILTER_PF];
+#pragma unroll
+    for (int q = 0; q < SISPH_FILTER_PF; q++) vr[q] = 4 * q < n ? __ldcs(src + (size_t)q * 32) : make_int4(i, i, i, i);
     for (int c = 0; c < nmax; c += 4) {
-        const int4 v = vnext;
-        // prefetch the next chunk of indices while this one is tested
-        vnext = c + 4 < n ? __ldcs(src + (size_t)((c + 4) >> 2) * 32) : make_int4(i, i, i, i);
+        const int4 v = vr[0];
+        {
+            const int cn = c + 4 * SISPH_FILTER_PF;
+            const int4 nx = cn < n ? __ldcs(src + (size_t)(cn >> 2) * 32) : make_int4(i, i, i, i);
+#pragma unroll
+            for (int q = 0; q < SISPH_FILTER_PF - 1; q++) vr[q] = vr[q + 1];
+            vr[SISPH_FILTER_PF - 1] = nx;
+        }
         V4<T> xj4[4];
         int j4[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
