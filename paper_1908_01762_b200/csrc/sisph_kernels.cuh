@@ -368,6 +368,16 @@ __device__ __forceinline__ void for_nbrs_k(const int* __restrict__ nbr, int cap,
     }
 }
 __device__ __forceinline__ size_t nb_off(int k) { return ((size_t)(k >> 2) << 7) + (k & 3); }
+// store one 4-entry chunk of a per-pair array (16 / 32 bytes, aligned)
+__device__ __forceinline__ void st_chunk4(float* p, const float (&f)[4])
+{
+    *reinterpret_cast<float4*>(p) = make_float4(f[0], f[1], f[2], f[3]);
+}
+__device__ __forceinline__ void st_chunk4(double* p, const double (&f)[4])
+{
+    reinterpret_cast<double2*>(p)[0] = make_double2(f[0], f[1]);
+    reinterpret_cast<double2*>(p)[1] = make_double2(f[2], f[3]);
+}
 // one 4-entry chunk of a per-pair array in the same layout (16 / 32 bytes)
 __device__ __forceinline__ void ld_chunk4(const float* p, float (&f)[4])
 {
@@ -1084,6 +1094,10 @@ __global__ void __launch_bounds__(RHS_T) k_rhs_diag(Params<T> P, T inv_dt, const
         T sr = 0, sd = 0, sp = 0;
         int n = cnt[i];
         T* __restrict__ crow = coef ? coef + nb_base(i, ncap) : nullptr;
+#ifndef SISPH_RHS_VST
+#define SISPH_RHS_VST 1   // B200, C5: 1061 -> 904 us per launch
+#endif
+        T fb[4] = {T(0), T(0), T(0), T(0)};             // SISPH_RHS_VST: one 16/32-byte store per chunk
         for_nbrs_k_pf<SISPH_RHS_PF>(nbr, ncap, i, n, [&](int j, int k) {
             V4<T> xj = ld4(pos + j), uj = ld4(us + j);
             T rhoj = uj.w;                           // rho_j rides in u*_j's 4th lane
@@ -1099,7 +1113,16 @@ __global__ void __launch_bounds__(RHS_T) k_rhs_diag(Params<T> P, T inv_dt, const
             sd += f;
             // stored per-pair part of fac_ij (particles do not move during the solve):
             // the sweep then reads it instead of recomputing it (same value, same layout as nbr)
+#if SISPH_RHS_VST
+            const int e = k & 3;
+            fb[0] = e == 0 ? f : fb[0];
+            fb[1] = e == 1 ? f : fb[1];
+            fb[2] = e == 2 ? f : fb[2];
+            fb[3] = e == 3 ? f : fb[3];
+            if (crow && (e == 3 || k == n - 1)) st_chunk4(crow + nb_off(k & ~3), fb);
+#else
             if (crow) crow[nb_off(k)] = f;
+#endif
             if (pin) sp += f * pin[j];                   // first sweep: sum_j fac_ij p^0_j
         });
         sr *= -P.dwk * inv_dt;
