@@ -418,6 +418,35 @@ struct NbCursor {
     }
 };
 
+// an append cursor that collects 4 entries in registers and writes them as one
+// 16-byte chunk (the blocked-ELL chunk of its row); flush() writes a partial tail
+// chunk (entries past the count are never read)
+struct NbCursorV {
+    int* row;
+    int k;
+    int b0, b1, b2, b3;
+    __device__ __forceinline__ void init(int* nbr, int cap, int i)
+    {
+        row = nbr + nb_base(i, cap);
+        k = 0;
+        b0 = b1 = b2 = b3 = 0;
+    }
+    __device__ __forceinline__ void push(bool acc, int j, int cap)
+    {
+        const int s = k & 3;
+        b0 = (acc && s == 0) ? j : b0;
+        b1 = (acc && s == 1) ? j : b1;
+        b2 = (acc && s == 2) ? j : b2;
+        b3 = (acc && s == 3) ? j : b3;
+        if (acc && s == 3 && k < cap) *reinterpret_cast<int4*>(row + ((k >> 2) << 7)) = make_int4(b0, b1, b2, b3);
+        k += acc ? 1 : 0;
+    }
+    __device__ __forceinline__ void flush(int cap)
+    {
+        if ((k & 3) != 0 && k < cap) *reinterpret_cast<int4*>(row + ((k >> 2) << 7)) = make_int4(b0, b1, b2, b3);
+    }
+};
+
 // One warp per cell: the lanes are the cell's destinations; candidates of
 // each stencil row are staged 32 at a time in shared memory (with the range's
 // periodic image shift applied) and read back as broadcasts, so every lane
@@ -630,9 +659,9 @@ __global__ void __launch_bounds__(32 * BL_WARPS) k_build_cells(Params<T> P, int 
 }
 
 // loose candidate loop over one staged chunk for DPL destinations per lane
-template <class T, int D, int DPL>
+template <class T, int D, int DPL, class Cur>
 __device__ __forceinline__ void loose_chunk(const V4<T>* sm, const int* smj, int nn, const V4<T> (&xi)[2],
-                                            const int (&i)[2], const bool (&act)[2], NbCursor (&A)[2], T Rs2, int cap)
+                                            const int (&i)[2], const bool (&act)[2], Cur (&A)[2], T Rs2, int cap)
 {
 #pragma unroll 4
     for (int u = 0; u < nn; u++) {
@@ -681,7 +710,14 @@ __global__ void __launch_bounds__(32 * BL_WARPS) k_build_loose(Params<T> P, int 
         V4<T> xi[2];
         int i[2];
         bool act[2];
+#ifndef SISPH_BUILD_VST
+#define SISPH_BUILD_VST 0   // B200, C5: 1770 -> 2355 us with the register-buffered append: off
+#endif
+#if SISPH_BUILD_VST
+        NbCursorV A[2];
+#else
         NbCursor A[2];
+#endif
 #pragma unroll
         for (int d = 0; d < 2; d++) {
             const int t = base + 32 * d + lane;
@@ -707,11 +743,15 @@ __global__ void __launch_bounds__(32 * BL_WARPS) k_build_loose(Params<T> P, int 
             }
         }
 #pragma unroll
-        for (int d = 0; d < 2; d++)
+        for (int d = 0; d < 2; d++) {
+#if SISPH_BUILD_VST
+            A[d].flush(cap);
+#endif
             if (act[d]) {
                 cnt[i[d]] = min(A[d].k, cap);
                 mmax = max(mmax, A[d].k);
             }
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mmax = max(mmax, __shfl_xor_sync(0xffffffffu, mmax, o));
@@ -758,7 +798,14 @@ __global__ void __launch_bounds__(128) k_filter(Params<T> P, int row0, int nrows
     for (int o = 16; o > 0; o >>= 1) nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
     const float Rin2 = inner ? P.Rin2f : -1.f;
     const int pmask = P.per[0] | (P.per[1] << 1) | (P.per[2] << 2);
+    #ifndef SISPH_FILTER_VST
+#define SISPH_FILTER_VST 1   // B200, C5: 1213 -> 1196 us
+#endif
+#if SISPH_FILTER_VST
+    NbCursorV A, B;
+#else
     NbCursor A, B;
+#endif
     A.init(nbr, cap, i);
     B.init(nbr_in ? nbr_in : nbr, cap_in, inner ? i : 0);
     // A11 state
@@ -838,6 +885,10 @@ __global__ void __launch_bounds__(128) k_filter(Params<T> P, int row0, int nrows
         }
     }
     double lam = 0.0;
+#if SISPH_FILTER_VST
+    A.flush(cap);
+    B.flush(cap_in);
+#endif
     if (act) {
         cnt[i] = min(A.k, cap);
         if (inner) cnt_in[i] = min(B.k, cap_in);
