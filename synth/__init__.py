@@ -312,7 +312,7 @@ def poiseuille_velocity(y, U, H):
 
 def channel(nx: int = 40, ny: int = 10, H: float = 1.0, U: float = 1.0, re: float = 10.0, n_in: int = 4,
             n_out: int = 4, n_pool: int | None = None, layers: int = 3, t_end: float = 10.0, tol: float = 1e-3,
-            precision: int = 64) -> Case:
+            precision: int = 64, nz: int = 0) -> Case:
     """Plane channel of height H (ny particles across) between two resting walls.
     Inlet region x in [-n_in dx, 0): tag 2 with the developed (parabolic, mean U)
     profile as prescribed velocity; fluid x in [0, nx dx) and the outlet region
@@ -321,29 +321,37 @@ def channel(nx: int = 40, ny: int = 10, H: float = 1.0, U: float = 1.0, re: floa
     hold the ids new inlet particles are drawn from (reading R34).  Re = U H / nu,
     asymm gradient (the frozen outlet pressures ratchet the absolute level
     upward with the flow; eq:mom:sph:press:pij is blind to it), no GTVF
-    (p_ref = 0), no-slip u* on the walls."""
+    (p_ref = 0), no-slip u* on the walls.  nz > 0: a 3D channel, periodic in z
+    over nz particles (the same plane flow in every z layer)."""
     rho0 = 1.0
     dx = H / ny
     h = dx
     nu = U * H / re
     Lf = nx * dx
     L_in, L_out = n_in * dx, n_out * dx
-    fluid = _lattice((nx, ny), dx, (0.0, 0.0))
-    inlet = _lattice((n_in, ny), dx, (-L_in, 0.0))
-    outlet = _lattice((n_out, ny), dx, (Lf, 0.0))
-    n_pool = 2 * n_in * ny if n_pool is None else n_pool
-    pool = _lattice((n_in, ny), dx, (-L_in, 0.0))
+    d3 = nz > 0
+    ext = (nz,) if d3 else ()
+    org = (0.0,) if d3 else ()
+    fluid = _lattice((nx, ny) + ext, dx, (0.0, 0.0) + org)
+    inlet = _lattice((n_in, ny) + ext, dx, (-L_in, 0.0) + org)
+    outlet = _lattice((n_out, ny) + ext, dx, (Lf, 0.0) + org)
+    n_pool = 2 * n_in * ny * max(nz, 1) if n_pool is None else n_pool
+    pool = _lattice((n_in, ny) + ext, dx, (-L_in, 0.0) + org)
     pool = np.concatenate([pool] * (n_pool // len(pool) + 1))[:n_pool]
-    xs = (np.arange(-n_in - layers, nx + n_out + layers) + 0.5) * dx
-    walls = [np.stack([xs, np.full_like(xs, -(l + 0.5) * dx)], 1) for l in range(layers)]
-    walls += [np.stack([xs, np.full_like(xs, H + (l + 0.5) * dx)], 1) for l in range(layers)]
+    nwx = n_in + nx + n_out + 2 * layers
+    walls = []
+    for l in range(layers):
+        for yl in (-(l + 0.5) * dx, H + (l + 0.5) * dx):
+            w = _lattice((nwx, 1) + ext, dx, (-(n_in + layers) * dx, 0.0) + org)
+            w[:, 1] = yl
+            walls.append(w)
     wall = np.concatenate(walls)
     x = np.concatenate([fluid, inlet, outlet, wall, pool])
     tag = np.concatenate([np.zeros(len(fluid), np.int32), np.full(len(inlet), INLET, np.int32),
                           np.full(len(outlet), OUTLET, np.int32), np.ones(len(wall), np.int32),
                           np.full(len(pool), DORMANT, np.int32)])
     n = len(x)
-    u = np.zeros((n, 2))
+    u = np.zeros((n, 3 if d3 else 2))
     # the developed profile everywhere (inlet prescribed, fluid and outlet initial): the
     # steady state is the initial state, and the open boundaries must keep it
     liq = (tag == INLET) | (tag == OUTLET) | (tag == FLUID)
@@ -354,9 +362,10 @@ def channel(nx: int = 40, ny: int = 10, H: float = 1.0, U: float = 1.0, re: floa
                             ustar_noslip=1, tol=tol, precision=precision, open_x=1, x_inlet=0.0, x_outlet=Lf,
                             x_end=Lf + L_out, inlet_length=L_in)
     lo = [-L_in - (layers + 0.5) * dx, -(layers + 0.5) * dx, 0.0]
-    hi = [Lf + L_out + (layers + 0.5) * dx, H + (layers + 0.5) * dx, 0.0]
-    return Case("channel", 2, h, dx, dt, int(round(t_end / dt)), lo, hi, [0, 0, 0], x, u,
-                np.full(n, rho0 * dx * dx), np.full(n, rho0), np.zeros(n), tag, params)
+    hi = [Lf + L_out + (layers + 0.5) * dx, H + (layers + 0.5) * dx, nz * dx if d3 else 0.0]
+    dim = 3 if d3 else 2
+    return Case("channel", dim, h, dx, dt, int(round(t_end / dt)), lo, hi, [0, 0, 1 if d3 else 0], x, u,
+                np.full(n, rho0 * dx ** dim), np.full(n, rho0), np.zeros(n), tag, params)
 
 
 # --------------------------------------------------------------------------

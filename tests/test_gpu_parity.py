@@ -618,17 +618,19 @@ def test_fp32_host_io_matches_fp64_io():
 
 
 # ------------------------------------------------------------------ NEXT-4b: open boundaries (R34)
-def test_open_boundary_parity_fp64():
+@pytest.mark.parametrize("dim", [2, 3])
+def test_open_boundary_parity_fp64(dim):
     """Inlet / outlet / dormant conversions and the id pool (reading R34): the CUDA
     path and the oracle, free running from the same inputs, agree on every type
     change and id draw (bit-exact TAG field), on the sweep counts, and on the
-    fields of the active particles (fp64 tolerance)."""
+    fields of the active particles (fp64 tolerance).  3D: the same channel, periodic
+    in z."""
     import oracle
-    case = synth.channel(nx=20, ny=8)
+    case = synth.channel(nx=20, ny=8) if dim == 2 else synth.channel(nx=12, ny=8, nz=12)
     sim = gpu_sim(case)
     o = oracle.Sim(case)
     moved = 0
-    for s in range(40):
+    for s in range(40 if dim == 2 else 25):
         rg = sim.step(case.dt)
         it_o, res_o, _ = o.step(case.dt)
         if abs(res_o - case.params["tol"]) > 1e-9 * case.params["tol"]:

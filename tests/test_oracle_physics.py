@@ -528,12 +528,13 @@ def test_mean_convergence_measure_is_tiling_invariant(orc):
 
 
 # ---------------------------------------------------------------- NEXT-4b: open boundaries (R34)
-def test_open_boundary_bookkeeping(orc):
+@pytest.mark.parametrize("dim", [2, 3])
+def test_open_boundary_bookkeeping(orc, dim):
     """Inlet -> fluid -> outlet -> dormant -> inlet: every conversion follows R34.
     The inlet keeps its population (each conversion spawns one), prescribed and
     frozen velocities never change, spawned inlet particles come from the lowest
     dormant ids, and the particle count is conserved."""
-    case = synth.channel(nx=20, ny=8)
+    case = synth.channel(nx=20, ny=8) if dim == 2 else synth.channel(nx=12, ny=8, nz=12)
     s = orc.Sim(case)
     n_in = int((case.tag == synth.INLET).sum())
     prm = case.params
