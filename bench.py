@@ -25,6 +25,12 @@ import sys
 import threading
 import time
 
+# stdout carries exactly one JSON line: the real stdout is kept aside for it and file
+# descriptor 1 points at stderr, so that whatever libraries print there (NCCL's "NCCL version"
+# banner, CUDA / torch notices) cannot interleave with the result
+_JSON_FD = os.dup(1)
+os.dup2(2, 1)
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -189,7 +195,8 @@ def cpu_baseline(name, max_seconds=20.0):
 
 
 def emit(d):
-    print(json.dumps(d), flush=True)
+    sys.stdout.flush()
+    os.write(_JSON_FD, (json.dumps(d) + "\n").encode())
 
 
 def run_reference(args):
