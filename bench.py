@@ -28,8 +28,7 @@ import time
 # stdout carries exactly one JSON line: the real stdout is kept aside for it and file
 # descriptor 1 points at stderr, so that whatever libraries print there (NCCL's "NCCL version"
 # banner, CUDA / torch notices) cannot interleave with the result
-_JSON_FD = os.dup(1)
-os.dup2(2, 1)
+_JSON_FD = None   # set by main()
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -195,6 +194,9 @@ def cpu_baseline(name, max_seconds=20.0):
 
 
 def emit(d):
+    if _JSON_FD is None:
+        print(json.dumps(d), flush=True)
+        return
     sys.stdout.flush()
     os.write(_JSON_FD, (json.dumps(d) + "\n").encode())
 
@@ -412,6 +414,9 @@ def run_sisph(args):
 
 
 def main():
+    global _JSON_FD
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
     args = parse()
     if args.impl == "reference":
         run_reference(args)
