@@ -357,7 +357,12 @@ template <class T, int D> struct Engine : EngineBase {
         K = prm->K;
         // GTVF inner list: worth it when the GTVF kernel support 3 h~ is well inside 3 h
         {
-            const double ht = prm->h_tilde_factor * h, skin = 0.25 * h;
+#ifndef SISPH_GTVF_SKIN
+#define SISPH_GTVF_SKIN 0.1   // B200, C5: 0.25 h -> 0.1 h: 107 -> 81 us per sub-step (fewer dead pairs)
+#endif
+            // the inner list's skin covers the K sub-steps' displacement (checked per step:
+            // a particle moving more than skin / 2 sends the step back to the full list)
+            const double ht = prm->h_tilde_factor * h, skin = SISPH_GTVF_SKIN * h;
             const double rin = 3.0 * ht + skin;
             use_inner = rin < 0.85 * R && prm->p_ref != 0.0 && prm->K > 0;
             P.Rin2f = (float)(rin * rin * (1.0 + 1.0 / 1024.0));
@@ -1701,7 +1706,7 @@ template <class T, int D> struct Engine : EngineBase {
         if (pref_auto && !pref_done) {
             // R33: p_ref = 2 max p over the fluid of this first solve (all ranks), then constant
             double* dm = reinterpret_cast<double*>(&ctl->red[3]);
-            ++nlaunch, k_fluid_pmax<T><<<1, 1024, 0, st>>>(p, Nfo, dm);
+            ++nlaunch, k_fluid_pmax<T><<<1, 1024, 0, st>>>(p, Nfo, ptype, dm);
             SCK(cudaGetLastError());
             if (dist()) SRET(xallreduce(dm, 1, 1));
             double mx = 0;

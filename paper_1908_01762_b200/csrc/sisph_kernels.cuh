@@ -1665,13 +1665,16 @@ __global__ void __launch_bounds__(SWEEP_T) k_mean_fix(Params<T> P, const PpeDesc
     }
 }
 
-// R33: max_i p_i over the owned fluid (one block, fixed order; once per handle)
+// R33: max_i p_i over the owned fluid (one block, fixed order; once per handle);
+// with open boundaries (R34) over the fluid proper (not inlet / outlet rows)
 template <class T>
-__global__ void __launch_bounds__(1024) k_fluid_pmax(const T* __restrict__ p, int nf, double* out)
+__global__ void __launch_bounds__(1024) k_fluid_pmax(const T* __restrict__ p, int nf, const uint8_t* __restrict__ ptype,
+                                                     double* out)
 {
     __shared__ double sm[32];
     double m = -INFINITY;
-    for (int i = threadIdx.x; i < nf; i += blockDim.x) m = fmax(m, (double)p[i]);
+    for (int i = threadIdx.x; i < nf; i += blockDim.x)
+        if (!ptype || ptype[i] == 0) m = fmax(m, (double)p[i]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
     if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
