@@ -1,7 +1,7 @@
-"""A few steps of every workload family on the CUDA path, small sizes: run under
-compute-sanitizer (memcheck / racecheck) to catch out-of-bounds and races.
+"""A few steps of every workload family and PPE-loop form on the CUDA path, small sizes
+(meant to run under compute-sanitizer where that is available; this build's GPU pool disables it).
 
-    compute-sanitizer --tool memcheck python scripts/all_families_smoke.py
+    python scripts/all_families_smoke.py
 """
 import os
 import sys
