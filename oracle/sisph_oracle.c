@@ -1001,11 +1001,12 @@ void or_correct(or_sim* s, double dt)
         }
         memcpy(rk, rn, (size_t)(3 * n) * sizeof(double));
     }
-    /* R34: the outlet's advection velocity, Shepard_h of the fluid's u_x^{n+1} at r^n
-     * (fluid sources of the r^n list; none in the support: the frozen u_x) */
+    /* R34: the outlet's advection velocity, Shepard_h of the fluid's u_x^{n+1} at r*, the
+     * positions of the pressure solve (fluid sources of the r* list; none in the
+     * support: the frozen u_x) */
     double* uout = dalloc(n);
     if (c->open_x) {
-        const csr_t* b0 = &s->nb[0];
+        const csr_t* b0 = &s->nb[1];
 #pragma omp parallel for schedule(static)
         for (int64_t i = 0; i < n; i++) {
             if (s->tag[i] != OUTLET) continue;
@@ -1014,7 +1015,7 @@ void or_correct(or_sim* s, double dt)
                 int64_t j = b0->nbr[t];
                 if (s->tag[j] != FLUID) continue;
                 double d[3];
-                double w = or_W(dim, sqrt(rij(c, s->x + 3 * i, s->x + 3 * j, d)), c->h);
+                double w = or_W(dim, sqrt(rij(c, s->xs + 3 * i, s->xs + 3 * j, d)), c->h);
                 su += unew[3 * j] * w;
                 sw += w;
             }

@@ -346,10 +346,6 @@ template <class T, int D> struct Engine : EngineBase {
         P.x_outlet = (T)prm->x_outlet;
         P.x_end = (T)prm->x_end;
         P.inlet_length = (T)prm->inlet_length;
-        if (open_x && rebuild_mode != 0) {
-            err = "open boundaries (open_x) need the single per-step build (rebuild_mode 0)";
-            return SISPH_EINVAL;
-        }
         for (int a = 0; a < D; a++) extent = std::max(extent, std::max(fabs(dom->lo[a]), fabs(dom->hi[a])));
         min_iter = prm->min_iter;
         max_iter = prm->max_iter;
@@ -1298,10 +1294,6 @@ template <class T, int D> struct Engine : EngineBase {
             SRET(build_loose_grow());
         } else {
             SRET(plan_skin(dt, single));
-            if (open_x && !single) {
-                err = "open boundaries need the single per-step build: 2 dt max|u~| exceeds 0.3 x 3h (reduce dt)";
-                return SISPH_EINVAL;
-            }
             // A1-A5 at r^n (single build: the loose list on the skin grid)
             SRET(build_fluid(single));
         }
@@ -1742,9 +1734,9 @@ template <class T, int D> struct Engine : EngineBase {
                 }
             }
         }
-        // A15 (R34: the outlet's advection velocity first, from the fluid's u^{n+1} at r^n)
+        // A15 (R34: the outlet's advection velocity first, from the fluid's u^{n+1} at r*)
         if (open_x && Nfo)
-            ++nlaunch, k_outlet_velocity<T, D><<<nblk(Nfo, 256), 256, 0, st>>>(P, rn, vel, nbs, cnt_s, cap_s, uout);
+            ++nlaunch, k_outlet_velocity<T, D><<<nblk(Nfo, 256), 256, 0, st>>>(P, pos, vel, nbr, cnt, P.cap, uout);
         if (Nfo) ++nlaunch, k_advance<T, D><<<nblk(Nfo, 256), 256, 0, st>>>(P, (T)dt, rK, rn, vel, pos, vt, ctl, uout);
         SCK(cudaGetLastError());
         if (open_x) SRET(open_boundaries());

@@ -1970,8 +1970,8 @@ __global__ void k_advance(Params<T> P, T dt, const V4<T>* __restrict__ dK, const
 // ===========================================================================
 // R34 open boundaries
 // ===========================================================================
-// the outlet's advection velocity: Shepard_h of the fluid's u_x^{n+1} at r^n
-// (fluid sources of the r^n list; none in the support: the frozen u_x)
+// the outlet's advection velocity: Shepard_h of the fluid's u_x^{n+1} at r* (the
+// exact r* list; none in the support: the frozen u_x)
 template <class T, int D>
 __global__ void k_outlet_velocity(Params<T> P, const V4<T>* __restrict__ rn, const V4<T>* __restrict__ vel,
                                   const int* __restrict__ nbr, const int* __restrict__ cnt, int ncap,

@@ -370,6 +370,66 @@ def channel(nx: int = 40, ny: int = 10, H: float = 1.0, U: float = 1.0, re: floa
                 np.full(n, rho0 * dx ** dim), np.full(n, rho0), np.zeros(n), tag, params)
 
 
+def cylinder(D: float = 2.0, re: float = 200.0, U: float = 1.0, ppd: int = 30, h_ratio: float = 1.2,
+             up: float = 5.0, down: float = 10.0, half_width: float = 7.5, n_in: int = 4, n_out: int = 4,
+             layers: int = 4, t_end: float = 200.0, tol: float = 1e-2, precision: int = 64,
+             n_pool: int | None = None) -> Case:
+    """Flow past a circular cylinder (§4.7): D = 2, Re = U D / nu = 200,
+    dx = D / ppd (30: 200 k fluid particles), h / dx = 1.2, cylinder centre 5D behind
+    the inlet (uniform U, tag 2), outlet (tag 3) 10D behind the centre, eps = 0.01,
+    symm, no artificial viscosity, external
+    GTVF with p_ref = rho c^2, c = 10 |U|max, h~ = h / 2.  The cylinder is
+    `layers` rings of wall particles inside the circumference, the outer ring dx/2
+    inside it, each ring evenly spaced at about dx.  Reading
+    R35: the slip side walls at +-7.5D become a periodic y axis of width
+    15D (no slip-wall construction for the viscous ghost velocity here); the same
+    blockage ratio D / 15D.  And the fluid starts as the uniform stream U instead of
+    impulsively from rest: with the fluid at rest the inlet's first pressure spike
+    drives a GTVF shift (p0 = min(10|p|, rho c^2)) past the single build's skin."""
+    rho0 = 1.0
+    dx = D / ppd
+    h = h_ratio * dx
+    nu = U * D / re
+    R = 0.5 * D
+    xc = up * D
+    L_in, L_out = n_in * dx, n_out * dx
+    x_out = xc + down * D
+    W = 2.0 * half_width * D
+    nx = int(round(x_out / dx))
+    ny = int(round(W / dx))
+    fl = _lattice((nx, ny), dx, (0.0, -half_width * D))
+    outside = (fl[:, 0] - xc) ** 2 + fl[:, 1] ** 2 >= (R + 0.5 * dx) ** 2 - 1e-12   # dx/2 gap to the surface
+    fl = fl[outside]
+    inlet = _lattice((n_in, ny), dx, (-L_in, -half_width * D))
+    n_pool = 2 * n_in * ny if n_pool is None else n_pool
+    pool = np.concatenate([inlet] * (n_pool // len(inlet) + 1))[:n_pool]
+    rings = []
+    for l in range(layers):
+        r = R - (l + 0.5) * dx
+        if r <= 0:
+            break
+        m = max(int(round(2 * np.pi * r / dx)), 3)
+        th = 2 * np.pi * (np.arange(m) + 0.5) / m
+        rings.append(np.stack([xc + r * np.cos(th), r * np.sin(th)], 1))
+    wall = np.concatenate(rings)
+    x = np.concatenate([fl, inlet, wall, pool])
+    tag = np.concatenate([np.zeros(len(fl), np.int32), np.full(len(inlet), INLET, np.int32),
+                          np.ones(len(wall), np.int32), np.full(len(pool), DORMANT, np.int32)])
+    n = len(x)
+    u = np.zeros((n, 2))
+    u[(tag == INLET) | (tag == 0), 0] = U     # R35: a uniform stream at t = 0 (see below)
+    umax = 1.5 * U
+    dt = min(0.25 * h / umax, 0.25 * h * h / nu)
+    c_ref = 10.0 * umax
+    params = default_params(rho0=rho0, nu=nu, pgrad=PGRAD_SYMM, h_tilde_factor=0.5, pref_external=1,
+                            p_ref=rho0 * c_ref * c_ref, c_ref=c_ref, ustar_noslip=0, tol=tol, precision=precision,
+                            open_x=1, x_inlet=0.0, x_outlet=x_out, x_end=x_out + L_out, inlet_length=L_in)
+    lo = [-L_in - 4 * h, -half_width * D, 0.0]
+    hi = [x_out + L_out + 4 * h, half_width * D, 0.0]
+    return Case("cylinder", 2, h, dx, dt, int(round(t_end / dt)), lo, hi, [0, 1, 0], x, u,
+                np.full(n, rho0 * dx * dx), np.full(n, rho0), np.zeros(n), tag, params)
+
+
 # --------------------------------------------------------------------------
 # C4  3D Taylor-Green vortex (BASELINE configs[3])
 # --------------------------------------------------------------------------
