@@ -71,8 +71,13 @@ def main():
     ap.add_argument("--ppd", type=int, default=30)
     ap.add_argument("--t-end", type=float, default=200.0)
     ap.add_argument("--every", type=float, default=0.5)
+    ap.add_argument("--max-wall", type=float, default=1200.0, help="stop after this many seconds")
+    ap.add_argument("--set", nargs="*", default=[], help="parameter overrides key=value")
     args = ap.parse_args()
     case = synth.cylinder(ppd=args.ppd, t_end=args.t_end)
+    for kv in args.set:
+        k, v = kv.split("=")
+        case.params[k] = float(v) if ("." in v or "e" in v) else int(v)
     sim = Simulation.from_case(case)
     cyl = np.flatnonzero(case.tag == 1)
     D, U = 2.0, 1.0
@@ -82,6 +87,9 @@ def main():
     k_every = max(1, int(round(args.every / case.dt)))
     try:
         for k in range(case.steps):
+            if time.perf_counter() - t0 > args.max_wall:
+                status = f"stopped at the wall-clock limit ({args.max_wall:g} s)"
+                break
             its.append(sim.step(case.dt).iters)
             t += case.dt
             if (k + 1) % k_every == 0:
