@@ -1346,7 +1346,10 @@ __global__ void __launch_bounds__(256) k_ppe_wall(Params<T> P, const PpeDesc<T>*
 // (sum |p^{k+1} - p^k|, sum |p^{k+1}|) finished by the last block, which also
 // takes the stop decision (R12, R13) on the device.
 // ===========================================================================
-constexpr int SWEEP_T = 256;
+#ifndef SISPH_SWEEP_T
+#define SISPH_SWEEP_T 256   // B200, C5: 128 / 256 / 512 -> 298 / 274 / 272 us
+#endif
+constexpr int SWEEP_T = SISPH_SWEEP_T;
 // stored sweep: prefetch distance (chunks of 4 entries; 0 = none) and the minimum
 // resident blocks per SM of the fp32 kernel (a 64-register cap: 4 x 256 threads).
 // Tuned on B200 with A/B builds (build.py --out ... -DSISPH_SWEEP_PF=...):
