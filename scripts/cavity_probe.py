@@ -38,6 +38,14 @@ def probe(label, n=100, re=100.0, **over):
     print(f"{label:40s} | " + " | ".join(out), flush=True)
 
 
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "htilde":
+    probe("base (h~ = h)")
+    probe("h~ = h/2", h_tilde_factor=0.5)
+    probe("h~ = h/2, sums", h_tilde_factor=0.5, conv_mean=0)
+    probe("h~ = h/2, tol 1e-3", h_tilde_factor=0.5, tol=1e-3)
+    probe("h~ = h/2, no-slip u*", h_tilde_factor=0.5, ustar_noslip=1)
+    probe("h~ = h/2, Re 10^4", re=10000.0, h_tilde_factor=0.5)
+    sys.exit(0)
 if __name__ == "__main__":
     which = sys.argv[1] if len(sys.argv) > 1 else "all"
     probe("base (slip, means, GTVF 2max p)")

@@ -5,7 +5,7 @@ sys.path.insert(0, "."); sys.path.insert(0, "scripts")
 import synth
 from paper_1908_01762_b200 import Simulation
 from variants import tgv_error
-T_OUT = (0.25, 0.5, 1.0, 2.0)
+T_OUT = (0.25, 0.5, 1.0, 2.0, 5.0)
 def run(n, label, re=100.0, **over):
     case = synth.tgv2d(n=n, re=re)
     sim = Simulation.from_case(case, **over)
@@ -21,6 +21,13 @@ def run(n, label, re=100.0, **over):
     sim.close()
 if __name__ != "__main__":
     pass
+elif len(sys.argv) > 1 and sys.argv[1] == "htilde":
+    # the GTVF kernel length: h~ = h (the paper's internal-flow choice) pairs particles on an
+    # h/dx = 1 lattice; h~ = h/2 with the mean-free PPE (R32), over the paper's tolerance range
+    for tol in (0.1, 0.05, 1e-2, 5e-3, 1e-3, 5e-4, 1e-4):
+        run(100, f"asymm tol {tol:g} h~=h/2 mean-free", tol=tol, h_tilde_factor=0.5, ppe_mean_free=1)
+    run(100, "asymm tol 0.0001 h~=h mean-free", tol=1e-4, ppe_mean_free=1)
+    run(100, "asymm tol 0.0001 h~=h/2 printed", tol=1e-4, h_tilde_factor=0.5)
 elif len(sys.argv) > 1 and sys.argv[1] == "meanfree":
     # reading R32: the same tolerance study with the live-row mean removed every sweep
     for tol in (1e-2, 1e-3, 1e-4):

@@ -589,3 +589,35 @@ def test_channel_keeps_the_poiseuille_profile(orc):
     err = np.abs(u[sel, 0] - synth.poiseuille_velocity(x[sel, 1], 1.0, 1.0))
     assert err.mean() < 0.025 and err.max() < 0.06
     assert np.abs(u[sel, 1]).max() < 0.05
+
+
+# ---------------------------------------------------------------- GTVF: regularisation vs pairing
+def _gtvf_lattice_std(orc, h_tilde_factor, p_ref, steps=40):
+    # a jittered periodic lattice at rest (h = dx): only the GTVF shift moves the particles
+    case = synth.tgv2d(n=24, jitter=0.2)
+    case.u[:] = 0
+    case.p[:] = 0
+    case.params.update(nu=0.01, p_ref=p_ref, h_tilde_factor=h_tilde_factor, tol=1e-3)
+    s = orc.Sim(case)
+    s.density()
+    std0 = s.get("rho").std()
+    for _ in range(steps):
+        s.step(case.dt)
+    s.density()
+    assert np.abs(s.get("u")).max() == 0.0      # the shift moves positions only (eq:int:vhatnp2)
+    return std0, s.get("rho").std()
+
+
+def test_gtvf_regularises_with_half_h_and_pairs_with_h(orc):
+    """eq:mom:sph:gtvf repels along -p0 grad W(r, h~); the quintic's |dW/dr| peaks near q = 1,
+    so on an h/dx = 1 lattice with h~ = h nearest neighbours sit at the peak and a pair that
+    closes in is pushed apart LESS: the lattice pairs up (the density spread grows), whereas
+    with h~ = h/2 the neighbours sit beyond the peak and the spread shrinks.  Too strong a
+    background pressure (dt sqrt(p0 / rho) / h~ >~ 1) overshoots within the step and clusters
+    even with h~ = h/2 (R22c)."""
+    s0, s1 = _gtvf_lattice_std(orc, 0.5, 1.0)
+    assert s1 < 0.7 * s0
+    s0, s1 = _gtvf_lattice_std(orc, 1.0, 1.0)
+    assert s1 > s0
+    s0, s1 = _gtvf_lattice_std(orc, 0.5, 10.0)
+    assert s1 > 2.0 * s0
