@@ -373,7 +373,8 @@ def channel(nx: int = 40, ny: int = 10, H: float = 1.0, U: float = 1.0, re: floa
 def cylinder(D: float = 2.0, re: float = 200.0, U: float = 1.0, ppd: int = 30, h_ratio: float = 1.2,
              up: float = 5.0, down: float = 10.0, half_width: float = 7.5, n_in: int = 4, n_out: int = 4,
              layers: int = 4, t_end: float = 200.0, tol: float = 1e-2, precision: int = 64,
-             n_pool: int | None = None) -> Case:
+             n_pool: int | None = None, jitter: float = 0.05, seed: int = 1504,
+             p_ref: float | None = None) -> Case:
     """Flow past a circular cylinder (§4.7): D = 2, Re = U D / nu = 200,
     dx = D / ppd (30: 200 k fluid particles), h / dx = 1.2, cylinder centre 5D behind
     the inlet (uniform U, tag 2), outlet (tag 3) 10D behind the centre, eps = 0.01,
@@ -400,6 +401,9 @@ def cylinder(D: float = 2.0, re: float = 200.0, U: float = 1.0, ppd: int = 30, h
     fl = _lattice((nx, ny), dx, (0.0, -half_width * D))
     outside = (fl[:, 0] - xc) ** 2 + fl[:, 1] ** 2 >= (R + 0.5 * dx) ** 2 - 1e-12   # dx/2 gap to the surface
     fl = fl[outside]
+    # a seeded jitter breaks the set-up's mirror symmetry about y = 0 (a perfectly symmetric,
+    # deterministic start delays the shedding indefinitely)
+    fl = _jitter(fl, jitter * dx, seed, [0.0, -half_width * D], [x_out, half_width * D], [0, 1])
     inlet = _lattice((n_in, ny), dx, (-L_in, -half_width * D))
     n_pool = 2 * n_in * ny if n_pool is None else n_pool
     pool = np.concatenate([inlet] * (n_pool // len(inlet) + 1))[:n_pool]
@@ -421,8 +425,11 @@ def cylinder(D: float = 2.0, re: float = 200.0, U: float = 1.0, ppd: int = 30, h
     umax = 1.5 * U
     dt = min(0.25 * h / umax, 0.25 * h * h / nu)
     c_ref = 10.0 * umax
+    # p_ref: the paper's rho c^2 unless given; R22c: the GTVF sub-steps are an
+    # undamped oscillator over one step and need dt sqrt(p0 / rho) / h~ <~ 1 (here p0 <~ 9)
     params = default_params(rho0=rho0, nu=nu, pgrad=PGRAD_SYMM, h_tilde_factor=0.5, pref_external=1,
-                            p_ref=rho0 * c_ref * c_ref, c_ref=c_ref, ustar_noslip=0, tol=tol, precision=precision,
+                            p_ref=rho0 * c_ref * c_ref if p_ref is None else p_ref, c_ref=c_ref, ustar_noslip=0,
+                            tol=tol, precision=precision,
                             open_x=1, x_inlet=0.0, x_outlet=x_out, x_end=x_out + L_out, inlet_length=L_in)
     lo = [-L_in - 4 * h, -half_width * D, 0.0]
     hi = [x_out + L_out + 4 * h, half_width * D, 0.0]
