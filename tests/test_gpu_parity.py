@@ -696,3 +696,17 @@ def test_cylinder_steps_parity_fp64():
         assert_close(f"u {s}", sim.get("VELOCITY")[act], o.get("u")[act], 64, scale=2.0)
         assert_close(f"p {s}", sim.get("PRESSURE")[act], o.get("p")[act], 64,
                      scale=max(np.abs(o.get("p")[act]).max(), 1e-3))
+
+
+def test_tgv_tight_tolerance_with_half_h_gtvf_and_mean_free():
+    """R22c + R32 on the CUDA path: at eps = 1e-4 the 50^2 Taylor-Green vortex follows the
+    exact decay exp(-8 pi^2 t / Re) to t = 1 (with h~ = h and the printed iteration it
+    goes unstable there; profiles/r1_variants.md §6-8)."""
+    case = synth.tgv2d()
+    sim = gpu_sim(case, tol=1e-4, h_tilde_factor=0.5, ppe_mean_free=1)
+    steps = int(round(1.0 / case.dt))
+    for _ in range(steps):
+        sim.step(case.dt)
+    u = sim.get("VELOCITY")
+    decay = np.abs(u).max() / np.exp(-8 * np.pi ** 2 * case.params["nu"] * steps * case.dt)
+    assert abs(decay - 1.0) < 0.03, decay
