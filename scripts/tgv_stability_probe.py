@@ -21,6 +21,13 @@ def run(n, label, re=100.0, **over):
     sim.close()
 if __name__ != "__main__":
     pass
+elif len(sys.argv) > 1 and sys.argv[1] == "re10k":
+    # EISPH vs SISPH at Re = 10^4 with the stable GTVF / PPE settings (R22c, R32)
+    st = dict(h_tilde_factor=0.5, ppe_mean_free=1)
+    run(100, "SISPH tol 1e-2 h~=h/2 mean-free", re=10000.0, tol=1e-2, **st)
+    run(100, "SISPH tol 1e-3 h~=h/2 mean-free", re=10000.0, tol=1e-3, **st)
+    run(100, "EISPH (1 sweep) h~=h/2 mean-free", re=10000.0, max_iter=1, min_iter=1, **st)
+    run(100, "SISPH tol 1e-2 h~=h (printed)", re=10000.0, tol=1e-2)
 elif len(sys.argv) > 1 and sys.argv[1] == "htilde":
     # the GTVF kernel length: h~ = h (the paper's internal-flow choice) pairs particles on an
     # h/dx = 1 lattice; h~ = h/2 with the mean-free PPE (R32), over the paper's tolerance range
