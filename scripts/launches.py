@@ -1,7 +1,10 @@
 """Per-kernel totals and shares from an `ncu --metrics gpu__time_duration.sum --csv` launch list."""
 import collections
 import csv
+import signal
 import sys
+
+signal.signal(signal.SIGPIPE, signal.SIG_DFL)   # `| head` closes the pipe early: exit quietly
 
 rows = list(csv.reader(open(sys.argv[1])))
 hdr = next(i for i, r in enumerate(rows) if 'Kernel Name' in r)
