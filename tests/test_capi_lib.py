@@ -59,7 +59,7 @@ def _create(sl, x, u, m, rho, tag, h, dom, prm=None):
 
 
 @pytest.mark.parametrize("case", ["h", "dim", "tag", "mass", "nan", "periodic_cells", "outside", "nofluid",
-                                  "precision"])
+                                  "precision", "open_tag_without_open_x", "open_x_periodic", "open_x_order"])
 def test_create_rejects_invalid_arguments(sl, case):
     n = 16
     x = np.random.default_rng(0).uniform(0.1, 0.9, (n, 2))
@@ -88,6 +88,13 @@ def test_create_rejects_invalid_arguments(sl, case):
         tag[:] = 1
     elif case == "precision":
         prm = sl.params_from_dict({"precision": 16})
+    elif case == "open_tag_without_open_x":
+        tag[4] = 2           # an inlet tag needs open_x (R34)
+    elif case == "open_x_periodic":
+        prm = sl.params_from_dict({"open_x": 1, "inlet_length": 0.1, "x_inlet": 0.1, "x_outlet": 0.8, "x_end": 0.9})
+    elif case == "open_x_order":
+        dom = sl.domain(2, [0, 0], [1, 1], [0, 1])
+        prm = sl.params_from_dict({"open_x": 1, "inlet_length": 0.1, "x_inlet": 0.8, "x_outlet": 0.2, "x_end": 0.9})
     rc, msg = _create(sl, x, u, m, rho, tag, h, dom, prm)
     assert rc == sl.SISPH_EINVAL, (rc, msg)
     assert msg
