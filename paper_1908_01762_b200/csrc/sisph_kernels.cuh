@@ -447,6 +447,37 @@ struct NbCursorV {
     }
 };
 
+// the same 16-byte append with the entries shifted in (b3 newest): four
+// selects per push and no slot compares
+struct NbCursorS {
+    int* row;
+    int k;
+    int b0, b1, b2, b3;
+    __device__ __forceinline__ void init(int* nbr, int cap, int i)
+    {
+        row = nbr + nb_base(i, cap);
+        k = 0;
+        b0 = b1 = b2 = b3 = 0;
+    }
+    __device__ __forceinline__ void push(bool acc, int j, int cap)
+    {
+        b0 = acc ? b1 : b0;
+        b1 = acc ? b2 : b1;
+        b2 = acc ? b3 : b2;
+        b3 = acc ? j : b3;
+        if (acc && (k & 3) == 3 && k < cap) *reinterpret_cast<int4*>(row + ((k >> 2) << 7)) = make_int4(b0, b1, b2, b3);
+        k += acc ? 1 : 0;
+    }
+    __device__ __forceinline__ void flush(int cap)
+    {
+        const int s = k & 3;
+        if (s != 0 && k < cap) {
+            const int4 v = s == 1 ? make_int4(b3, 0, 0, 0) : s == 2 ? make_int4(b2, b3, 0, 0) : make_int4(b1, b2, b3, 0);
+            *reinterpret_cast<int4*>(row + ((k >> 2) << 7)) = v;
+        }
+    }
+};
+
 // One warp per cell: the lanes are the cell's destinations; candidates of
 // each stencil row are staged 32 at a time in shared memory (with the range's
 // periodic image shift applied) and read back as broadcasts, so every lane
@@ -658,6 +689,41 @@ __global__ void __launch_bounds__(32 * BL_WARPS) k_build_cells(Params<T> P, int 
     }
 }
 
+// stage one chunk of candidates for the loose build (positions already in
+// registers, ok = the lane holds a candidate), keeping only those within
+// sqrt(Rc2) of the box [lo, hi] that holds the warp's destinations (order
+// preserved): a culled candidate has r^2 >= its box distance^2 >= Rc2 > Rs2
+// for every destination, so the loose list is the same set in the same
+// order.  Returns the kept count.
+template <class T, int D>
+__device__ __forceinline__ int cull_compact(V4<T> v, int slot, bool ok, T sx, T sy, T sz, const V4<T>& lo,
+                                            const V4<T>& hi, T Rc2, V4<T>* sm, int* smj)
+{
+    const int lane = threadIdx.x & 31;
+    bool keep = false;
+    if (ok) {
+        v.x += sx;
+        v.y += sy;
+        if (D == 3) v.z += sz;
+        const T bx = max(max(lo.x - v.x, v.x - hi.x), (T)0);
+        const T by = max(max(lo.y - v.y, v.y - hi.y), (T)0);
+        T d2 = bx * bx + by * by;
+        if (D == 3) {
+            const T bz = max(max(lo.z - v.z, v.z - hi.z), (T)0);
+            d2 += bz * bz;
+        }
+        keep = d2 < Rc2;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (keep) {
+        const int q = __popc(m & ((1u << lane) - 1u));
+        sm[q] = v;
+        smj[q] = slot;
+    }
+    __syncwarp();
+    return __popc(m);
+}
+
 // loose candidate loop over one staged chunk for DPL destinations per lane
 template <class T, int D, int DPL, class Cur>
 __device__ __forceinline__ void loose_chunk(const V4<T>* sm, const int* smj, int nn, const V4<T> (&xi)[2],
@@ -680,8 +746,22 @@ __device__ __forceinline__ void loose_chunk(const V4<T>* sm, const int* smj, int
     }
 }
 
+#ifndef SISPH_BUILD_CULL
+// B200, C5 k_build_loose (profiles/r1_variants.md §11): plain 1766 us; culled 1788 us
+// (36 % fewer instructions, the staging load latency exposed); culled + 16-byte
+// appends 1642 us (adopted); + next-chunk prefetch 1664 us; shift-in appends 1767 us
+#define SISPH_BUILD_CULL 1   // cull staged candidates against the destinations' box
+#endif
+#ifndef SISPH_BUILD_PF
+#define SISPH_BUILD_PF 0     // load the next chunk's candidates while testing this one
+#endif
+#ifdef SISPH_BUILD_MINB
+#define BL_LOOSE_BOUNDS __launch_bounds__(32 * BL_WARPS, SISPH_BUILD_MINB)
+#else
+#define BL_LOOSE_BOUNDS __launch_bounds__(32 * BL_WARPS)
+#endif
 template <class T, int D>
-__global__ void __launch_bounds__(32 * BL_WARPS) k_build_loose(Params<T> P, int ncells, const V4<T>* __restrict__ pos,
+__global__ void BL_LOOSE_BOUNDS k_build_loose(Params<T> P, int ncells, const V4<T>* __restrict__ pos,
                                                               const int* __restrict__ fstart,
                                                               const int* __restrict__ wstart,
                                                               const int* __restrict__ wperm, int* __restrict__ nbr,
@@ -711,9 +791,11 @@ __global__ void __launch_bounds__(32 * BL_WARPS) k_build_loose(Params<T> P, int 
         int i[2];
         bool act[2];
 #ifndef SISPH_BUILD_VST
-#define SISPH_BUILD_VST 0   // B200, C5: 1770 -> 2355 us with the register-buffered append: off
+#define SISPH_BUILD_VST 1   // unculled: 1770 -> 2355 us with the register-buffered append; culled: 1788 -> 1642 us
 #endif
-#if SISPH_BUILD_VST
+#if SISPH_BUILD_VST == 2
+        NbCursorS A[2];
+#elif SISPH_BUILD_VST
         NbCursorV A[2];
 #else
         NbCursor A[2];
@@ -726,6 +808,88 @@ __global__ void __launch_bounds__(32 * BL_WARPS) k_build_loose(Params<T> P, int 
             xi[d] = ld4(pos + (act[d] ? i[d] : fa));
             A[d].init(nbr, cap, act[d] ? i[d] : 0);
         }
+#if SISPH_BUILD_CULL
+        // box of this pass's destinations (warp-wide)
+        V4<T> lo, hi;
+        {
+            const T big = (T)3.0e38;
+            lo.x = lo.y = lo.z = big;
+            hi.x = hi.y = hi.z = -big;
+#pragma unroll
+            for (int d = 0; d < 2; d++)
+                if (act[d]) {
+                    lo.x = min(lo.x, xi[d].x); lo.y = min(lo.y, xi[d].y); lo.z = min(lo.z, xi[d].z);
+                    hi.x = max(hi.x, xi[d].x); hi.y = max(hi.y, xi[d].y); hi.z = max(hi.z, xi[d].z);
+                }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                lo.x = min(lo.x, __shfl_xor_sync(0xffffffffu, lo.x, o));
+                lo.y = min(lo.y, __shfl_xor_sync(0xffffffffu, lo.y, o));
+                hi.x = max(hi.x, __shfl_xor_sync(0xffffffffu, hi.x, o));
+                hi.y = max(hi.y, __shfl_xor_sync(0xffffffffu, hi.y, o));
+                if (D == 3) {
+                    lo.z = min(lo.z, __shfl_xor_sync(0xffffffffu, lo.z, o));
+                    hi.z = max(hi.z, __shfl_xor_sync(0xffffffffu, hi.z, o));
+                }
+            }
+        }
+        // margin over Rs2 for the rounding of the two distance evaluations
+        const T Rc2 = Rs2 * (T)(1.0 + 1.0 / 4096.0);
+#endif
+#if SISPH_BUILD_CULL
+        // flattened walk over the 32-candidate chunks of the stencil ranges; the
+        // next chunk's slots and positions are loaded while this one is tested
+        int q = -1, j0 = 0, b = 0, code = 0;
+        auto advance = [&]() -> bool {
+            j0 += 32;
+            if (j0 < b) return true;
+            while (++q < NRNG) {
+                const int4 ab = rng[warp][q];
+                if (ab.x < ab.y) {
+                    j0 = ab.x;
+                    b = ab.y;
+                    code = ab.z;
+                    return true;
+                }
+            }
+            return false;
+        };
+        V4<T> vn;
+        vn.x = vn.y = vn.z = vn.w = (T)0;
+        int sn = 0;
+        auto fetch = [&]() {
+            if (j0 + lane < b) {
+                sn = wslot(wperm, Nf, j0 + lane);
+                vn = ld4(pos + sn);
+            }
+        };
+        bool more = advance();
+#if SISPH_BUILD_PF
+        if (more) fetch();
+#endif
+#pragma unroll 1
+        while (more) {
+#if !SISPH_BUILD_PF
+            fetch();
+#endif
+            const V4<T> v0 = vn;
+            const int s0 = sn, code0 = code;
+            const bool ok0 = j0 + lane < b;
+            more = advance();
+#if SISPH_BUILD_PF
+            if (more) fetch();
+#endif
+            T sx, sy, sz;
+            shift_of(P, code0, sx, sy, sz);
+            const int nn = cull_compact<T, D>(v0, s0, ok0, sx, sy, sz, lo, hi, Rc2, sm, smj);
+            if (nn == 0) continue;
+            if (two)
+                loose_chunk<T, D, 2>(sm, smj, nn, xi, i, act, A, Rs2, cap);
+            else
+                loose_chunk<T, D, 1>(sm, smj, nn, xi, i, act, A, Rs2, cap);
+            __syncwarp();
+        }
+#else
 #pragma unroll 1
         for (int q = 0; q < NRNG; q++) {
             const int4 ab = rng[warp][q];
@@ -742,6 +906,7 @@ __global__ void __launch_bounds__(32 * BL_WARPS) k_build_loose(Params<T> P, int 
                 __syncwarp();
             }
         }
+#endif
 #pragma unroll
         for (int d = 0; d < 2; d++) {
 #if SISPH_BUILD_VST
@@ -801,7 +966,9 @@ __global__ void __launch_bounds__(128) k_filter(Params<T> P, int row0, int nrows
     #ifndef SISPH_FILTER_VST
 #define SISPH_FILTER_VST 1   // B200, C5: 1213 -> 1196 us
 #endif
-#if SISPH_FILTER_VST
+#if SISPH_FILTER_VST == 2
+    NbCursorS A, B;
+#elif SISPH_FILTER_VST
     NbCursorV A, B;
 #else
     NbCursor A, B;
