@@ -401,8 +401,8 @@ def run_sisph(args):
         out["e2e"] = {"value": sw2 * nf / t, "unit": UNIT, "h2d_bytes_per_step": hb * n * (3 * dim + 1),
                       "d2h_bytes_per_step": hb * n, "host_dtype": "f32" if f32 else "f64", "steps": K2,
                       "ms_per_step": 1e3 * t / K2,
-                      # every e2e step restarts from the one uploaded state, so its sweep count can
-                      # differ from the timed steps' (same on C5; not on the PPE-heavy small configs)
+                      # every e2e step repeats the step from the uploaded state (the one after the
+                      # timed steps), so its sweep count can differ from theirs (same on C5)
                       "sweeps_per_step": sw2 / K2}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args.workload)
