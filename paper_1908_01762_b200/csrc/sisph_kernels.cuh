@@ -941,8 +941,13 @@ __global__ void BL_LOOSE_BOUNDS k_build_loose(Params<T> P, int ncells, const V4<
 // k_rhs_diag).  Measured on C5 it is SLOWER than filter + k_rhs_diag (96
 // registers: occupancy halves), so the engine runs RHS = false; kept for
 // the record.
+#ifdef SISPH_FILTER_MINB
+#define FILTER_BOUNDS __launch_bounds__(128, SISPH_FILTER_MINB)
+#else
+#define FILTER_BOUNDS __launch_bounds__(128)
+#endif
 template <class T, int D, bool RHS>
-__global__ void __launch_bounds__(128) k_filter(Params<T> P, int row0, int nrows, const V4<T>* __restrict__ pos,
+__global__ void FILTER_BOUNDS k_filter(Params<T> P, int row0, int nrows, const V4<T>* __restrict__ pos,
                                                 const int* __restrict__ nbs, const int* __restrict__ cnts, int cap_s,
                                                 int* __restrict__ nbr, int* __restrict__ cnt,
                                                 int* __restrict__ nbr_in, int* __restrict__ cnt_in,
