@@ -621,3 +621,39 @@ def test_gtvf_regularises_with_half_h_and_pairs_with_h(orc):
     assert s1 > s0
     s0, s1 = _gtvf_lattice_std(orc, 0.5, 10.0)
     assert s1 > 2.0 * s0
+
+
+@pytest.mark.parametrize("noslip", [0, 1])
+def test_wall_ustar_of_a_uniform_tangential_stream(orc, noslip):
+    # R16: slip u*_w = Shepard_{h/2}(u*_f), no-slip u*_w = 2 u_wall - Shepard_{h/2}(u*_f),
+    # then the normal clip (eq:vg-no-normal).  With g = 0, alpha = 0 and a uniform fluid
+    # velocity U along the floor, u*_f = U exactly (every pair difference is zero), the Shepard
+    # average of a constant is that constant, and the clip leaves a tangential vector alone:
+    # the floor's top wall layer gets +U (slip) or -U (no-slip).  The deeper layers have no
+    # fluid within the h/2 support (1.5 dx < 2 dx) and keep their own velocity, 0 (R15a).
+    # A missing Shepard normalisation, a wrong support or sign, or a clip of tangential
+    # components fails this.
+    import dataclasses
+    base = synth.hydrostatic(nx=20, ny=20, layers=3)
+    prm = dict(base.params, g=[0.0, 0.0, 0.0], alpha=0.0, nu=0.0, ustar_noslip=noslip)
+    U = 0.37
+    u = np.zeros_like(base.u)
+    u[base.tag == 0, 0] = U
+    case = dataclasses.replace(base, u=u, params=prm)
+    s = orc.Sim(case)
+    s.predict(case.dt)
+    us, x = s.get("us"), case.x
+    f = case.tag == 0
+    assert np.abs(us[f, 0] - U).max() < 1e-12 and np.abs(us[f, 1]).max() < 1e-12
+    dx = case.dx
+    w = case.tag == 1
+    # away from the corners (the smoothed normals of the 3 dx next to a side wall tilt)
+    inner = w & (x[:, 0] > 5 * dx) & (x[:, 0] < 20 * dx - 5 * dx)
+    top = inner & np.isclose(x[:, 1], -0.5 * dx)
+    deep = inner & (x[:, 1] < -1.0 * dx)
+    assert top.sum() == 10 and deep.sum() == 20
+    assert np.abs(s.get("normal")[top, 0]).max() < 1e-12
+    want = -U if noslip else U
+    assert np.abs(us[top, 0] - want).max() < 1e-12
+    assert np.abs(us[top, 1]).max() < 1e-12
+    assert np.abs(us[deep]).max() == 0.0
