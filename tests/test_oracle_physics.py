@@ -657,3 +657,25 @@ def test_wall_ustar_of_a_uniform_tangential_stream(orc, noslip):
     assert np.abs(us[top, 0] - want).max() < 1e-12
     assert np.abs(us[top, 1]).max() < 1e-12
     assert np.abs(us[deep]).max() == 0.0
+
+
+def test_wall_normals_of_a_flat_three_layer_wall(orc):
+    # R17 (eq:normal-approx / eq:normal): away from corners a flat 3-layer wall is
+    # symmetric about its middle layer, so the normals are exact: the layer next to the fluid
+    # points into it, the outermost layer out of it, and the middle layer's sums cancel to
+    # rounding noise, which the 1/(4h) threshold and the 0.01 rule must turn into exactly 0
+    # (normalising it would give an arbitrary direction).  Floor and side walls both.
+    case = synth.hydrostatic(nx=20, ny=20, layers=3)
+    s = orc.Sim(case)
+    s.predict(case.dt)
+    n, x, dx = s.get("normal"), case.x, case.dx
+    w = case.tag == 1
+    for axis, other in ((1, 0), (0, 1)):          # floor (normal along y), left wall (along x)
+        band = w & (x[:, other] > 5 * dx) & (x[:, other] < 15 * dx)
+        for layer, sign in ((-0.5, 1.0), (-1.5, 0.0), (-2.5, -1.0)):
+            sel = band & np.isclose(x[:, axis], layer * dx)
+            assert sel.sum() == 10
+            want = np.zeros(2)
+            want[axis] = sign
+            err = np.abs(n[sel][:, :2] - want).max()
+            assert (err == 0.0) if sign == 0.0 else (err < 1e-12)
