@@ -679,3 +679,32 @@ def test_wall_normals_of_a_flat_three_layer_wall(orc):
             want[axis] = sign
             err = np.abs(n[sel][:, :2] - want).max()
             assert (err == 0.0) if sign == 0.0 else (err < 1e-12)
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_tgv_initial_pressure_solves_the_pressure_poisson_equation(dim):
+    # R29: the TGV initial pressures (2D: the exact p(0); 3D: rho/16 (cos 2x + cos 2y)
+    # (cos 2z + 2)) are the pressures of the initial velocity fields, i.e. they satisfy
+    # lap p = -rho d_i u_j d_j u_i (incompressible Euler / Navier-Stokes at t = 0).  Checked with
+    # spectral derivatives on the unjittered periodic lattice (exact for these trigonometric
+    # fields up to rounding); a wrong factor, sign or wavenumber fails.
+    n = 16
+    case = synth.tgv2d(n=n, jitter=0.0) if dim == 2 else synth.tgv3d(n=n, jitter=0.0, precision=64)
+    L = case.hi[0] - case.lo[0]
+    shape = (n,) * dim                                   # slowest axis first, x fastest
+    f = case.tag == 0
+    assert f.sum() == n ** dim
+    u = [case.u[f, a].reshape(shape) for a in range(dim)]
+    p = case.p[f].reshape(shape)
+    rho = case.rho[f][0]
+    k = 2.0 * np.pi / L * np.fft.fftfreq(n, 1.0 / n)
+
+    def deriv(g, a):                                     # d/dx_a; array axis dim-1-a
+        ax = dim - 1 - a
+        kk = k.reshape([-1 if b == ax else 1 for b in range(dim)])
+        return np.real(np.fft.ifftn(1j * kk * np.fft.fftn(g)))
+
+    lap = sum(deriv(deriv(p, a), a) for a in range(dim))
+    rhs = -rho * sum(deriv(u[j], i) * deriv(u[i], j) for i in range(dim) for j in range(dim))
+    assert np.abs(p).max() > 0.1
+    assert np.abs(lap - rhs).max() < 1e-10 * np.abs(rhs).max()
