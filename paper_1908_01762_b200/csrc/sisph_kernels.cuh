@@ -6,6 +6,7 @@
 // DESIGN.md readings (Rn).
 #pragma once
 #include <cooperative_groups.h>
+#include <type_traits>
 
 #include "sisph_device.cuh"
 
@@ -755,6 +756,18 @@ __device__ __forceinline__ void loose_chunk(const V4<T>* sm, const int* smj, int
 #ifndef SISPH_BUILD_PF
 #define SISPH_BUILD_PF 0     // load the next chunk's candidates while testing this one
 #endif
+#ifndef SISPH_BUILD_VST
+#define SISPH_BUILD_VST 1   // unculled: 1770 -> 2355 us with the register-buffered append; culled: 1788 -> 1642 us
+#endif
+// 3D only: on C3 (2D, a 3 x 3 stencil, short candidate loops) the loose build takes 192 us with
+// the cull and 16-byte appends against 155 us without
+template <int D>
+struct BlCfg {
+    static constexpr bool cull = SISPH_BUILD_CULL && D == 3;
+    static constexpr bool vst = SISPH_BUILD_VST != 0 && D == 3;
+    using Cur = typename std::conditional<!vst, NbCursor,
+                                          typename std::conditional<SISPH_BUILD_VST == 2, NbCursorS, NbCursorV>::type>::type;
+};
 #ifdef SISPH_BUILD_MINB
 #define BL_LOOSE_BOUNDS __launch_bounds__(32 * BL_WARPS, SISPH_BUILD_MINB)
 #else
@@ -790,16 +803,7 @@ __global__ void BL_LOOSE_BOUNDS k_build_loose(Params<T> P, int ncells, const V4<
         V4<T> xi[2];
         int i[2];
         bool act[2];
-#ifndef SISPH_BUILD_VST
-#define SISPH_BUILD_VST 1   // unculled: 1770 -> 2355 us with the register-buffered append; culled: 1788 -> 1642 us
-#endif
-#if SISPH_BUILD_VST == 2
-        NbCursorS A[2];
-#elif SISPH_BUILD_VST
-        NbCursorV A[2];
-#else
-        NbCursor A[2];
-#endif
+        typename BlCfg<D>::Cur A[2];
 #pragma unroll
         for (int d = 0; d < 2; d++) {
             const int t = base + 32 * d + lane;
@@ -808,7 +812,7 @@ __global__ void BL_LOOSE_BOUNDS k_build_loose(Params<T> P, int ncells, const V4<
             xi[d] = ld4(pos + (act[d] ? i[d] : fa));
             A[d].init(nbr, cap, act[d] ? i[d] : 0);
         }
-#if SISPH_BUILD_CULL
+        if constexpr (BlCfg<D>::cull) {
         // box of this pass's destinations (warp-wide)
         V4<T> lo, hi;
         {
@@ -835,8 +839,6 @@ __global__ void BL_LOOSE_BOUNDS k_build_loose(Params<T> P, int ncells, const V4<
         }
         // margin over Rs2 for the rounding of the two distance evaluations
         const T Rc2 = Rs2 * (T)(1.0 + 1.0 / 4096.0);
-#endif
-#if SISPH_BUILD_CULL
         // flattened walk over the 32-candidate chunks of the stencil ranges; the
         // next chunk's slots and positions are loaded while this one is tested
         int q = -1, j0 = 0, b = 0, code = 0;
@@ -889,7 +891,7 @@ __global__ void BL_LOOSE_BOUNDS k_build_loose(Params<T> P, int ncells, const V4<
                 loose_chunk<T, D, 1>(sm, smj, nn, xi, i, act, A, Rs2, cap);
             __syncwarp();
         }
-#else
+        } else {
 #pragma unroll 1
         for (int q = 0; q < NRNG; q++) {
             const int4 ab = rng[warp][q];
@@ -906,12 +908,10 @@ __global__ void BL_LOOSE_BOUNDS k_build_loose(Params<T> P, int ncells, const V4<
                 __syncwarp();
             }
         }
-#endif
+        }
 #pragma unroll
         for (int d = 0; d < 2; d++) {
-#if SISPH_BUILD_VST
-            A[d].flush(cap);
-#endif
+            if constexpr (BlCfg<D>::vst) A[d].flush(cap);
             if (act[d]) {
                 cnt[i[d]] = min(A[d].k, cap);
                 mmax = max(mmax, A[d].k);
