@@ -311,24 +311,35 @@ def test_tgv3d_kinetic_energy_decay(orc):
 
 
 def test_hydrostatic_column(orc):
-    # PPE with wall BCs reaches p = rho0 g (H - y) (BASELINE configs[1])
+    # PPE with wall BCs reaches p = rho0 g (H - y) (BASELINE configs[1], 500 steps)
     case = synth.hydrostatic(nx=20, ny=40, dx=0.05, precision=64)
     s = orc.Sim(case)
     f = case.tag == 0
     H, rg = 2.0, 1000.0 * 9.81
     errs = []
-    for k in range(300):
+    P = Y = 0.0
+    navg = 0
+    for k in range(500):
         s.step(case.dt)
         if k % 50 == 49:
             x = s.get("x")
             sel = x[f, 1] < H - 3 * case.h
             err = np.abs(s.get("p")[f][sel] - rg * (H - x[f, 1][sel]))
             errs.append((err.max() / (rg * H), err.mean() / (rg * H)))
+        if k >= 200:
+            P = P + s.get("p")[f]
+            Y = Y + s.get("x")[f, 1]
+            navg += 1
     errs = np.array(errs)
-    # the column settles from p = 0 with a decaying slosh: every sample within
-    # 8 % of rho0 g H (max) / 5 % (mean); the last one within 6 % / 2 %
-    assert errs[:, 0].max() < 0.08 and errs[:, 1].max() < 0.05
-    assert errs[-1, 0] < 0.06 and errs[-1, 1] < 0.02
+    # the column settles from p = 0 and keeps a small undamped slosh of the pressure about
+    # the hydrostatic field: every sample within 6.5 % of rho0 g H (max) / 4.5 % (mean) ...
+    assert errs[:, 0].max() < 0.065 and errs[:, 1].max() < 0.045
+    # ... and the pressure averaged over steps 200-500 within 2 % (max) / 1 % (mean) of
+    # rho0 g H (SURVEY §8(c) asks 5 %; measured 0.73 % / 0.32 %)
+    P, Y = P / navg, Y / navg
+    sel = Y < H - 3 * case.h
+    err = np.abs(P[sel] - rg * (H - Y[sel]))
+    assert err.max() < 0.02 * rg * H and err.mean() < 0.01 * rg * H
     assert np.abs(s.get("u")[f]).max() < 0.1
 
 
