@@ -161,13 +161,40 @@ def peaks():
     return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def sweep_traffic():
-    """dram bytes per sweep launch from the committed ncu --set full capture, if any."""
-    p = os.path.join(ROOT, "profiles", "sweep_traffic.json")
+def sweep_traffic(workload):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one k_sweep launch from the committed
+    ncu --set full capture of THIS workload (profiles/traffic_<workload>.json), else None."""
+    p = os.path.join(ROOT, "profiles", f"traffic_{workload}.json")
     if os.path.exists(p):
         with open(p) as f:
             return json.load(f).get("dram_bytes_per_launch")
     return None
+
+
+def kernel_instr(workload):
+    """Warp instructions per launch of the issue-bound kernels (sm__inst_executed.sum from the
+    committed ncu --set full captures of this workload), profiles/instr_<workload>.json."""
+    p = os.path.join(ROOT, "profiles", f"instr_{workload}.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return {}
+
+
+def alu_peak(device):
+    """The FP32 issue roof of this GPU at its current clocks:
+    libsisph_tools.so's FFMA / MUFU micro-benchmark (csrc/sisph_tools.cu)."""
+    import ctypes
+    from paper_1908_01762_b200 import build as B
+    lib = ctypes.CDLL(B.build_tools())
+    out = (ctypes.c_double * 4)()
+    rc = lib.sisph_tools_alu_peak(int(device), out)
+    if rc != 0:
+        return None
+    return {"ffma_warp_instr_per_s": out[0], "fp32_tflops": out[0] * 64 / 1e12,
+            "mufu_rsq_warp_instr_per_s": out[1], "issue_warp_instr_per_s": out[2],
+            "sm_mhz_during": out[3],
+            "how": "8 independent FFMA (MUFU.RSQ) chains per thread, 8 x SMs blocks of 256 threads, CUDA events"}
 
 
 def cpu_baseline(name, max_seconds=20.0):
@@ -205,6 +232,10 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    if "RANK" in os.environ and os.environ.get("OMP_NUM_THREADS") == "1":
+        # torchrun's default of one thread per rank: rank 0 alone runs the oracle here, on all
+        # host cores as at N = 1 (OpenMP reads this when the oracle library first runs)
+        os.environ["OMP_NUM_THREADS"] = str(os.cpu_count())
     import oracle
     oracle.build()
     case, sdesc = sample_case(args.workload, small=True)
@@ -312,18 +343,67 @@ def run_sisph(args):
     pairs = reps[-1].pairs
     n_loc = nf_own + (n - nf) // world if world > 1 else n     # this rank's rows (roofline: per-GPU kernel)
     nf_loc = nf_own
+    nw_loc = n_loc - nf_loc
     tb = 4 if case.params["precision"] == 32 else 8
+    d = case.dim
+    # SURVEY.md §8(d) M3(a), design (i): the ALGORITHMIC bytes of one sweep = the state of every
+    # fluid row read or written once (r: d s, rho, p^k, RHS, D_ii, p^{k+1}: 5 s, fs: 1 byte;
+    # 33 B in 3D fp32) + the stored neighbour structure, a 4-byte index per interaction
+    state_b = d * tb + 5 * tb + 1
+    b_alg = state_b * nf_loc + 4 * pairs
+    # what this design actually streams per launch (reported apart, it is not "useful" bytes):
     if args.matrix_free:
-        # pos (x, y, z, m), rho, p^k of every particle; rhs, diag, cnt, p^{k+1} (+ 1-byte fs) of
-        # every fluid particle; the 4-byte neighbour index of every pair
-        b_per = (6 * tb) * n_loc + (3 * tb + 5) * nf_loc + 4 * pairs
+        # pos (x, y, z, m), rho, p^k of every particle; rhs, diag, cnt, p^{k+1} (+ fs) of every
+        # fluid row; the 4-byte index of every pair
+        b_str = (6 * tb) * n_loc + (3 * tb + 5) * nf_loc + 4 * pairs
     else:
-        # p^k of every particle; rho, rhs, diag, cnt, p^{k+1} (+ fs) of every fluid particle;
-        # per pair the 4-byte index and the stored factor of fac_ij
-        b_per = tb * n_loc + (4 * tb + 5) * nf_loc + (4 + tb) * pairs
+        # p^k of every particle; rho, rhs, diag, cnt, p^{k+1} (+ fs) of every fluid row; per pair
+        # the 4-byte index and the stored factor of fac_ij
+        b_str = tb * n_loc + (4 * tb + 5) * nf_loc + (4 + tb) * pairs
     avg_s = ms_sw / max(n_sw, 1) / 1e3
-    achieved = b_per / avg_s / 1e9
+    achieved = b_alg / avg_s / 1e9
     peak, peak_src = peaks()
+    # M1 = sum(sweeps x N_f) / t_PPE with t_PPE from the start of A11 (wall p^0, RHS, D_ii and the
+    # fused first sweep) to the final decision of the solve
+    ms_ppe_i = sum(r.ms_ppe for r in ireps)
+    # the neighbour-build + PPE pipeline (north_star's ">= 60 % of the HBM roofline"): algorithmic
+    # bytes per step of
+    #   sort / reorder (A1-A4): hash reads r (4 s) and writes key + rank (8 B), the scatter moves
+    #     key, rank, slot (12 B), the reorder reads and writes the carried state (r, u, u~: 3 x 4 s,
+    #     p, rho: 2 s, id 4 B, fs 1 B) -> 32 s + 30 B per fluid particle (158 B in fp32)
+    #   the exact r* neighbour list (A5 / A9): positions read once (4 s per particle), the list
+    #     written once (4 B per interaction)
+    #   A11: r*, u* (2 x 4 s), rho, fs read, RHS, D_ii written (3 s + 1 B) per fluid row, walls'
+    #     r and u* (2 x 4 s), the list read once (4 B per interaction)
+    #   every sweep: b_alg (A11's fused first sweep included)
+    # over the device time of those phases (CUDA events: ms_build + ms_filter + ms_ppe)
+    sw_i = sweeps_i / len(ireps)
+    vb = 4 * tb   # one (x, y, z, m) / (u, rho) record
+    pipe_b = ((32 * tb + 30) * nf_loc + vb * n_loc + 4 * pairs
+              + (2 * vb + 3 * tb + 1) * nf_loc + 2 * vb * nw_loc + 4 * pairs
+              + sw_i * b_alg)
+    pipe_ms = sum(r.ms_build + r.ms_filter + r.ms_ppe for r in ireps) / len(ireps)
+    alu = alu_peak(local)
+    instr = kernel_instr(args.workload)
+    m3 = None
+    if alu and instr:
+        # M3(b) issue fraction of the issue-bound kernels: the committed ncu warp-instruction count
+        # of one launch over this run's launch time x the measured issue roof; M3(c) binding
+        # roofline: max(bytes / HBM peak, instructions / issue roof) / launch time
+        m3 = {}
+        ph = {"k_sweep": avg_s}
+        for kname, rec in instr.items():
+            t = ph.get(kname)
+            if t is None and rec.get("us_ncu"):
+                t = rec["us_ncu"] * 1e-6
+            if not t:
+                continue
+            ins = rec["warp_instr"]
+            byt = rec.get("dram_bytes", 0.0)
+            m3[kname] = {"issue_frac": ins / t / alu["issue_warp_instr_per_s"],
+                         "binding_frac": max(byt / (peak * 1e9), ins / alu["issue_warp_instr_per_s"]) / t,
+                         "time_source": "live CUDA events" if kname in ph else "ncu gpu__time_duration",
+                         "warp_instr": ins}
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -336,26 +416,49 @@ def run_sisph(args):
                    "parallelism": f"slab x{world}" + (f" along axis {SLAB_AXIS[args.workload]}, NCCL halos + "
                                                       "per-sweep allreduce" if world > 1 else "")},
         "ms_per_step_median": float(np.median(step_ms)),
-        "ppe_phase_particle_sweeps_per_s": sweeps_i * nf / (ms_solve_i / 1e3),
+        # t_PPE from the start of A11 to the final decision (the fused first sweep
+        # and the wall passes included); instrumented steps after the timed region
+        "ppe_phase_particle_sweeps_per_s": sweeps_i * nf / (ms_ppe_i / 1e3) if ms_ppe_i > 0 else None,
         "sweeps_per_step": sweeps / args.steps,
         "single_build_steps": sum(r.single_build for r in reps),
         "ms_per_step_phases": {"predict": sum(r.ms_predict for r in ireps) / len(ireps),
                                "solve": sum(r.ms_solve for r in ireps) / len(ireps),
                                "correct": sum(r.ms_correct for r in ireps) / len(ireps),
+                               "build_rn": sum(r.ms_build for r in ireps) / len(ireps),
+                               "rstar_sets": sum(r.ms_filter for r in ireps) / len(ireps),
+                               "a11": sum(r.ms_rhs for r in ireps) / len(ireps),
+                               "ppe_from_a11": ms_ppe_i / len(ireps),
                                "note": f"{len(ireps)} instrumented steps after the timed region "
                                        "(events between phases, host-polled PPE loop)"},
         "roofline": {"kernel": "k_sweep (A12 Jacobi sweep + fused residual reduction, "
                                + ("fac_ij recomputed per sweep)" if args.matrix_free else "stored fac_ij streamed)"),
                      "bound": "hbm",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": sweep_traffic(), "bytes_per_launch": b_per, "pairs_per_launch": pairs,
+                     "traffic": sweep_traffic(args.workload),
+                     "algorithmic_bytes_per_launch": b_alg,
+                     "algorithmic_bytes_def": f"SURVEY §8(d) M3(a) design (i): {state_b} B of state per fluid row "
+                                              "+ 4 B per interaction",
+                     "bytes_streamed_per_launch": b_str,
+                     "streamed_frac": b_str / avg_s / 1e9 / peak,
+                     "pairs_per_launch": pairs,
                      "avg_launch_us": avg_s * 1e6, "launches_timed": n_sw,
                      # interactions/s and the logical gather bandwidth (the
                      # p_j each interaction gathers; served by L1/L2, not an HBM fraction)
                      "interactions_per_s": pairs / avg_s,
                      "gather_logical_GBs": tb * pairs / avg_s / 1e9,
-                     "how": "20 sweep launches of a fixed-sweep solve after the timed region, CUDA events",
-                     "peak_source": peak_src},
+                     "how": "20 sweep launches of a fixed-sweep solve after the timed region, CUDA events "
+                            "on the handle's stream",
+                     "peak_source": peak_src + " (burst copy figure; the sweep is timed alone)"},
+        "pipeline_roofline": {"phases": "build at r^n (A1-A5) + r* sets (A9) + A11 + PPE sweeps to the decision",
+                              "algorithmic_bytes": pipe_b, "ms": pipe_ms,
+                              "achieved": pipe_b / (pipe_ms / 1e3) / 1e9 if pipe_ms > 0 else None,
+                              "peak": peak, "unit": "GB/s",
+                              "frac": pipe_b / (pipe_ms / 1e3) / 1e9 / peak if pipe_ms > 0 else None,
+                              "bytes_def": "158 B / fluid particle (hash, sort, reorder) + 16 B / particle + "
+                                           "4 B / interaction (the exact r* list) + A11 state + 4 B / "
+                                           "interaction + sweeps x (state + 4 B / interaction)"},
+        "alu_peak": alu,
+        "m3_issue_bound": m3,
         "gpu_launches": int(sum(r.launches for r in reps)),
         "halo": {"ghost_fluid_per_rank": int(reps[-1].n_ghost_fluid),
                  "bytes_sent_per_step_rank0": int(sum(r.halo_bytes for r in reps) / args.steps)}
@@ -416,11 +519,36 @@ def run_sisph(args):
         td.destroy_process_group()
 
 
+def spawn_ranks(n):
+    """`bench.py --gpus N` outside torchrun: re-launch this command as N ranks (one process
+    per GPU) under torch.distributed.run on 127.0.0.1, exactly as the driver launches it;
+    rank 0 prints the JSON line on the inherited stdout.  Returns the launcher's exit code."""
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     global _JSON_FD
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    if world == 0 and args.gpus > 1:
+        sys.exit(spawn_ranks(args.gpus))
+    if world and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    rf = os.environ.get("SISPH_BENCH_RANKFILE")
+    if rf:   # CPU test hook: every rank records that it started
+        with open(rf, "a") as f:
+            f.write(f"{os.environ.get('RANK', '0')}/{max(world, 1)}\n")
+        if os.environ.get("SISPH_BENCH_DRYRUN"):
+            return
     _JSON_FD = os.dup(1)
     os.dup2(2, 1)
-    args = parse()
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -136,6 +136,12 @@ typedef struct {
     int64_t n_owned_fluid;  /* fluid particles this handle owns (all of them on one GPU) */
     int64_t n_ghost_fluid;  /* halo copies of neighbour slabs' fluid (slab ranks) */
     int64_t halo_bytes;     /* bytes this rank sent in halo / migration exchanges this step */
+    /* timing mode, device ms of the pipeline phases: */
+    double ms_build;        /* step start -> end of the build at r^n (skin, A1-A5: hash, sort,
+                               reorder, list build) */
+    double ms_filter;       /* A9: the r* sets (filter of the single build, or the second build) */
+    double ms_rhs;          /* A11: wall p^0, RHS_i, D_ii, Lambda (+ the fused first sweep) */
+    double ms_ppe;          /* M1's t_PPE: A11 start -> final decision of the solve */
 } sisph_step_report;
 
 typedef enum {

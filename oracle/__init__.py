@@ -80,6 +80,7 @@ def lib():
         L.or_get.argtypes = [C.c_void_p, C.c_char_p, dp]
         L.or_set.argtypes = [C.c_void_p, C.c_char_p, dp]
         L.or_predict.argtypes = [C.c_void_p, C.c_double]
+        L.or_predict_stage2.argtypes = [C.c_void_p, C.c_double]
         L.or_solve.argtypes = [C.c_void_p, C.c_double, C.c_int, C.POINTER(Report)]
         L.or_correct.argtypes = [C.c_void_p, C.c_double]
         L.or_step.argtypes = [C.c_void_p, C.c_double, C.POINTER(Report)]
@@ -255,6 +256,10 @@ class Sim:
 
     def predict(self, dt):
         lib().or_predict(self._h, float(dt))
+
+    def predict_stage2(self, dt):
+        """A9-A11 again from the current xs (e.g. a working-precision handle's r*)."""
+        lib().or_predict_stage2(self._h, float(dt))
 
     def solve(self, tol, max_iter):
         r = Report()

@@ -802,15 +802,24 @@ void or_pass_sweep(or_sim* s, const double* pk, int64_t nd, const int64_t* dests
     }
 }
 
+/* the r*-stage of or_predict (A9-A11) from the current xs / us: neighbours at r*,
+ * wall u*, RHS, D_ii, Lambda.  Tests call it after replacing xs by the r* a
+ * working-precision (fp32) handle holds, so that both sides evaluate the pressure
+ * solve on the same positions (reading R36); or_predict runs it itself. */
+void or_predict_stage2(or_sim* s, double dt)
+{
+    csr_build(s, 1, s->xs, 0, NULL);                /* neighbours at r* (R3) */
+    pass_wall_ustar(s);                             /* A10 */
+    pass_rhs_diag(s, dt);                           /* line 6 + Lambda */
+}
+
 void or_predict(or_sim* s, double dt)
 {
     csr_build(s, 0, s->x, 0, NULL);                 /* neighbours at r^n (R3) */
     or_pass_density(s);                             /* line 2 */
     or_pass_ghost_velocity(s);                      /* A7 */
     pass_forces_predict(s, dt);                     /* lines 3-5 */
-    csr_build(s, 1, s->xs, 0, NULL);                /* neighbours at r* (R3) */
-    pass_wall_ustar(s);                             /* A10 */
-    pass_rhs_diag(s, dt);                           /* line 6 + Lambda */
+    or_predict_stage2(s, dt);                       /* A9-A11 at r* */
 }
 
 /* Lines 7-10: iterate eq:p-sor from p^0 = p(t) (R10) until eq:convergence

@@ -83,6 +83,7 @@ int or_set(or_sim* s, const char* field, const double* in);
 
 /* Algorithm 1 split as the C ABI splits it */
 void or_predict(or_sim* s, double dt);                       /* lines 2-5 + A10/A11 */
+void or_predict_stage2(or_sim* s, double dt);                /* A9-A11 from the current xs, us */
 void or_solve(or_sim* s, double tol, int max_iter, or_report* rep);  /* lines 6-9 */
 void or_correct(or_sim* s, double dt);                       /* lines 10-19 */
 void or_step(or_sim* s, double dt, or_report* rep);

@@ -55,6 +55,25 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
     return lib_out
 
 
+TOOLS = os.path.join(HERE, "libsisph_tools.so")
+
+
+def build_tools(force: bool = False) -> str:
+    """libsisph_tools.so: bench.py's measurement helpers (the FP32 ALU roof), not the hot path."""
+    src = os.path.join(CSRC, "sisph_tools.cu")
+    if not force and os.path.exists(TOOLS) and os.path.getmtime(TOOLS) >= max(os.path.getmtime(src),
+                                                                               os.path.getmtime(__file__)):
+        return TOOLS
+    flags = [f for f in FLAGS if f not in ("-Xptxas", "-v")]
+    cmd = [NVCC, *flags, "-o", TOOLS + ".tmp", src]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("nvcc failed building libsisph_tools.so")
+    os.replace(TOOLS + ".tmp", TOOLS)
+    return TOOLS
+
+
 if __name__ == "__main__":
     # python -m paper_1908_01762_b200.build [--force] [--out PATH] [-DNAME ...]
     args = sys.argv[1:]

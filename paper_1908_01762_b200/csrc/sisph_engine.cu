@@ -164,7 +164,18 @@ template <class T, int D> struct Engine : EngineBase {
     double* partials = nullptr;
     double* dtmp = nullptr;  // staging for get/set (n * 3 doubles)
     std::vector<int> tags_host;  // creation-order tags
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    // timing mode: 0-3 step / predict / solve / correct boundaries; 4 after the build at r^n
+    // (A1-A5); 5 / 6 around the r* filter (A9) or build; 7 / 8 around A11 (+ fused sweep)
+    static constexpr int NEV = 9;
+    cudaEvent_t ev[NEV] = {};
+    unsigned evmask = 0;
+    int mark(int k)
+    {
+        if (!timing) return SISPH_OK;
+        SCK(cudaEventRecord(ev[k], st));
+        evmask |= 1u << k;
+        return SISPH_OK;
+    }
 
     // ---------------------------------------------------------------- slab ranks
     Transport* tp = nullptr;
@@ -1297,6 +1308,7 @@ template <class T, int D> struct Engine : EngineBase {
             // A1-A5 at r^n (single build: the loose list on the skin grid)
             SRET(build_fluid(single));
         }
+        SRET(mark(4));
         const int* nb1 = single ? nbs : nbr;
         const int* cn1 = single ? cnt_s : cnt;
         const int cap1 = single ? cap_s : P.cap;
@@ -1331,6 +1343,7 @@ template <class T, int D> struct Engine : EngineBase {
             pl_add(L, us, sizeof(V));
             SRET(halo_fluid(L));
         }
+        SRET(mark(5));
         if (single) {
             // A9 (R3): r* becomes the current position set (walls are in every buffer),
             // r^n is kept as rn; exact sets at r* filtered out of the loose list
@@ -1367,6 +1380,7 @@ template <class T, int D> struct Engine : EngineBase {
             std::swap(pid, pid_alt);
             SRET(build_list_grow(true));   // + GTVF inner list
         }
+        SRET(mark(6));
         // A10
         if (Nwo) ++nlaunch, k_wall_velocity<T, D><<<nblk(Nwo, 256), 256, 0, st>>>(P, pos, nbr, cnt, P.cap, nrm, rho, uwl, us, P.ustar_noslip ? 0 : 1);
         SCK(cudaGetLastError());
@@ -1378,6 +1392,7 @@ template <class T, int D> struct Engine : EngineBase {
         // A11 with the first PPE sweep fused (walls first get p^0, R14)
         SCK(cudaMemsetAsync(&ctl->lambda_bits, 0, sizeof(unsigned long long), st));
         SCK(cudaMemsetAsync(ctl, 0, 4 * sizeof(int), st));  // ticket, iter, done, nonfinite
+        SRET(mark(7));   // t_PPE starts at A11 (wall p^0, RHS, D_ii, sweep 1)
         if (Nwo) ++nlaunch, k_wall_pressure<T, D><<<nblk(Nwo, 256), 256, 0, st>>>(P, pos, rho, nbr, cnt, P.cap, p);
         SCK(cudaGetLastError());
         if (dist()) {
@@ -1388,6 +1403,7 @@ template <class T, int D> struct Engine : EngineBase {
         ++nlaunch, k_rhs_diag<T, D><<<std::max(nblk(Nfo, RHS_T), 1), RHS_T, 0, st>>>(
                        P, (T)(1.0 / dt), pos, us, rho, fs, nbr, cnt, P.cap, rhs, diag, coef, ctl, p, p_alt, partials);
         SCK(cudaGetLastError());
+        SRET(mark(8));
         pre_swept = true;
         // Lambda is global (eq:convergence): the bits of a non-negative double order as the value
         if (dist()) SRET(xallreduce(reinterpret_cast<double*>(&ctl->lambda_bits), 1, 1));
@@ -1657,22 +1673,22 @@ template <class T, int D> struct Engine : EngineBase {
             V* dst = (k & 1) ? rkB : rkA;
             if (Nfo) {
                 if (inner)
-                    ++nlaunch, k_gtvf_substep<T, D><<<nblk(Nfo, 128), 128, 0, st>>>(P, dtau, src, dst, vk, dk, p, nbr_in,
+                    ++nlaunch, k_gtvf_substep<T, D><<<nblk(Nfo, 128), 128, 0, st>>>(P, dtau, src, dst, vk, p, nbr_in,
                                                                                     P.cap_in, cnt_in, k == 0, pos, 1, ctl);
                 else
-                    ++nlaunch, k_gtvf_substep<T, D><<<nblk(Nfo, 128), 128, 0, st>>>(P, dtau, src, dst, vk, dk, p, nbr,
+                    ++nlaunch, k_gtvf_substep<T, D><<<nblk(Nfo, 128), 128, 0, st>>>(P, dtau, src, dst, vk, p, nbr,
                                                                                     P.cap, cnt, k == 0, pos, 0, ctl);
             }
             SCK(cudaGetLastError());
             if (dist()) {
                 PackList L{};
-                pl_add(L, dst, sizeof(V), 1);
+                pl_add(L, dst, sizeof(V));   // displacements: no periodic image shift
                 SRET(halo_fluid(L));
             }
             src = dst;
         }
         SCK(cudaGetLastError());
-        rK = dk;
+        rK = src;   // delta^K = r^K - r^0 (4th lane m / rho^2, unused by k_advance)
         return SISPH_OK;
     }
 
@@ -1749,15 +1765,16 @@ template <class T, int D> struct Engine : EngineBase {
     {
         int64_t l0 = nlaunch;
         int64_t hb0 = halo_bytes;
-        if (timing) SCK(cudaEventRecord(ev[0], st));
+        evmask = 0;
+        SRET(mark(0));
         SRET(predict(dt));
-        if (timing) SCK(cudaEventRecord(ev[1], st));
+        SRET(mark(1));
         int it = 0;
         double res = 0;
         SRET(solve(tol, max_iter, &it, &res));
-        if (timing) SCK(cudaEventRecord(ev[2], st));
+        SRET(mark(2));
         SRET(correct(dt));
-        if (timing) SCK(cudaEventRecord(ev[3], st));
+        SRET(mark(3));
         if (rep) {
             memset(rep, 0, sizeof(*rep));
             rep->dt = dt;
@@ -1784,6 +1801,15 @@ template <class T, int D> struct Engine : EngineBase {
                 rep->ms_predict = a;
                 rep->ms_solve = b;
                 rep->ms_correct = c;
+                auto span = [&](int u, int v) -> double {
+                    float x = 0;
+                    if ((evmask >> u & 1) && (evmask >> v & 1)) cudaEventElapsedTime(&x, ev[u], ev[v]);
+                    return x;
+                };
+                rep->ms_build = span(0, 4);
+                rep->ms_filter = span(5, 6);
+                rep->ms_rhs = span(7, 8);
+                rep->ms_ppe = span(7, 2);
             }
         }
         if (hctl->overflow) return check_overflow();

@@ -2037,31 +2037,36 @@ __global__ void k_gtvf_prep(const V4<T>* __restrict__ pos, const T* __restrict__
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    V4<T> x = ld4(pos + i);
-    T r = rho[i];
-    x.w = x.w / (r * r);
-    a[i] = x;
-    if (b) b[i] = x;
+    const V4<T> x = ld4(pos + i);
+    const T r = rho[i];
+    // displacement r^0 - r^0 = 0 and m / rho^2 (eq:mom:sph:gtvf)
+    const V4<T> z = mk4<T>(T(0), T(0), T(0), x.w / (r * r));
+    a[i] = z;
+    if (b) b[i] = z;
 }
 
 // nbr/stride/cnt select the full r* list or the inner list (pairs with
 // r* < 3 h~ + skin).  With the inner list, a particle that has moved more
 // than skin/2 from r* raises ctl->gtvf_far and the host repeats the
 // sub-steps on the full list (exact either way).
-// The displacement delta^k = r^k - r^0 is carried explicitly (same recursion
-// as eq:int:gtvf:pos), so that eq:int:vhatnp2's (r^K - r^0)/dt does not lose
-// its digits to a difference of two positions in fp32.
+// The sub-step state is the displacement delta^k = r^k - r^0 (same recursion as
+// eq:int:gtvf:pos) with m_j / rho_j^2 in the 4th lane; a pair's r^k_ij is
+// (r^0_i - r^0_j) + (delta^k_i - delta^k_j): the difference of the two r* is
+// exact for neighbours (Sterbenz), so the GTVF force sees the geometry to the
+// working precision of r_ij itself and not to the ulp of the coordinates (fp32
+// at |x| ~ 3 with h = 1/256: 6e-5 h), and eq:int:vhatnp2's (r^K - r^0)/dt keeps
+// its digits.
 template <class T, int D>
 __global__ void __launch_bounds__(128) k_gtvf_substep(Params<T> P, T dtau, const V4<T>* __restrict__ rk,
                                                       V4<T>* __restrict__ rk1, V4<T>* __restrict__ vk,
-                                                      V4<T>* __restrict__ dk, const T* __restrict__ p,
-                                                      const int* __restrict__ nbr, int ncap,
+                                                      const T* __restrict__ p, const int* __restrict__ nbr, int ncap,
                                                       const int* __restrict__ cnt, int first,
                                                       const V4<T>* __restrict__ rstar, int check, Ctl* ctl)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= P.Nfo) return;
-    V4<T> xi = ld4(rk + i);
+    const V4<T> di = ld4(rk + i);
+    const V4<T> xi = ld4(rstar + i);
     T ax = 0, ay = 0, az = 0;
     int n = cnt[i];
     if (P.ptype && P.ptype[i] != 0) n = 0;           // R34: no GTVF shift for inlet / outlet
@@ -2069,10 +2074,17 @@ __global__ void __launch_bounds__(128) k_gtvf_substep(Params<T> P, T dtau, const
 #define SISPH_GTVF_PF 1   // B200, C5: PD 0 / 1 / 2 / 3 -> 113 / 107 / 125 / 120 us per sub-step
 #endif
     for_nbrs_pf<SISPH_GTVF_PF>(nbr, ncap, i, n, [&](int j) {
-        V4<T> xj = ld4(rk + j);
+        const V4<T> dj = ld4(rk + j);
+        const V4<T> xj = ld4(rstar + j);
         T d[3], r, ri;
-        r_of(pair_vec<T, D>(P, xi, xj, d), r, ri);
-        T f = xj.w * quintic4(r * P.inv_ht) * ri;   // m_j / rho_j^2 * |gradW| / r (dwkt below)
+        pair_vec<T, D>(P, xi, xj, d);
+        d[0] += di.x - dj.x;
+        d[1] += di.y - dj.y;
+        d[2] = D == 3 ? d[2] + (di.z - dj.z) : T(0);
+        T r2 = d[0] * d[0] + d[1] * d[1];
+        if (D == 3) r2 += d[2] * d[2];
+        r_of(r2, r, ri);
+        T f = dj.w * quintic4(r * P.inv_ht) * ri;   // m_j / rho_j^2 * |gradW| / r (dwkt below)
         ax += f * d[0];
         ay += f * d[1];
         if (D == 3) az += f * d[2];
@@ -2087,14 +2099,11 @@ __global__ void __launch_bounds__(128) k_gtvf_substep(Params<T> P, T dtau, const
     ay *= s;
     az *= s;
     const V4<T> zero = mk4<T>(T(0), T(0), T(0), T(0));
-    V4<T> v = first ? zero : ld4(vk + i);
-    V4<T> dl = first ? zero : ld4(dk + i);
-    T h2 = T(0.5) * dtau * dtau;
-    dl = mk4<T>(dl.x + dtau * v.x + h2 * ax, dl.y + dtau * v.y + h2 * ay, D == 3 ? dl.z + dtau * v.z + h2 * az : T(0),
-                T(0));
-    V4<T> r0 = ld4(rstar + i);
-    rk1[i] = mk4<T>(r0.x + dl.x, r0.y + dl.y, D == 3 ? r0.z + dl.z : xi.z, xi.w);
-    dk[i] = dl;
+    const V4<T> v = first ? zero : ld4(vk + i);
+    const T h2 = T(0.5) * dtau * dtau;
+    const V4<T> dl = mk4<T>(di.x + dtau * v.x + h2 * ax, di.y + dtau * v.y + h2 * ay,
+                            D == 3 ? di.z + dtau * v.z + h2 * az : T(0), di.w);
+    rk1[i] = dl;
     vk[i] = mk4<T>(v.x + dtau * ax, v.y + dtau * ay, D == 3 ? v.z + dtau * az : T(0), T(0));
     if (check && dl.x * dl.x + dl.y * dl.y + dl.z * dl.z > P.skin_half2) atomicExch(&ctl->gtvf_far, 1);
 }

@@ -57,7 +57,8 @@ class sisph_step_report(C.Structure):
                 ("ms_correct", C.c_double), ("pairs", C.c_int64), ("max_neighbors", C.c_int),
                 ("ms_sweeps", C.c_double), ("sweeps_timed", C.c_int), ("launches", C.c_int64),
                 ("single_build", C.c_int), ("skin_radius", C.c_double), ("n_owned_fluid", C.c_int64),
-                ("n_ghost_fluid", C.c_int64), ("halo_bytes", C.c_int64)]
+                ("n_ghost_fluid", C.c_int64), ("halo_bytes", C.c_int64), ("ms_build", C.c_double),
+                ("ms_filter", C.c_double), ("ms_rhs", C.c_double), ("ms_ppe", C.c_double)]
 
 
 class sisph_dist(C.Structure):

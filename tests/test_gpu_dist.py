@@ -17,7 +17,7 @@ import numpy as np
 import pytest
 
 import synth
-from parity_util import TOL, gpu_sim
+from parity_util import assert_close, assert_disp_close, gpu_sim
 
 pytestmark = pytest.mark.gpu
 
@@ -74,7 +74,9 @@ def test_slab_ranks_equal_single_gpu(name):
     mk, R, axis = CASES[name]
     case = mk()
     prec = case.params["precision"]
-    steps = 3
+    # fp32: one step (the two decompositions sum in different orders; over free-running fp32
+    # steps the difference grows through the fp32 position rounding, reading R36)
+    steps = 3 if prec == 64 else 1
     # fp32: fixed sweeps so both decompositions do identical work
     over = {} if prec == 64 else {"tol": 0.0, "max_iter": 4}
     single = gpu_sim(case, **over)
@@ -87,19 +89,10 @@ def test_slab_ranks_equal_single_gpu(name):
     # every particle owned by exactly one rank
     own = sum(s.owned_counts()[0] for s in sims)
     assert own == case.n_fluid
-    rel, ab = TOL[prec]
-    for fld in ("PRESSURE", "VELOCITY", "TRANSPORT_VELOCITY", "POSITION"):
-        a, b = gathered(sims, fld), single.get(fld)
-        if fld == "POSITION":
-            d = a - b
-            for k in range(case.dim):
-                if case.periodic[k]:
-                    L = case.hi[k] - case.lo[k]
-                    d[:, k] = (d[:, k] + 0.5 * L) % L - 0.5 * L
-            err, scale = np.abs(d).max(), np.abs(case.x).max()
-        else:
-            err, scale = np.abs(a - b).max(), max(np.abs(b).max(), 1e-3)
-        assert err <= rel * scale + ab, f"{fld}: {err:.3e} > {rel * scale + ab:.3e}"
+    for fld in ("PRESSURE", "VELOCITY", "TRANSPORT_VELOCITY"):
+        assert_close(fld, gathered(sims, fld), single.get(fld), prec)
+    # positions through the displacement over the run (from the creation positions)
+    assert_disp_close("POSITION", gathered(sims, "POSITION"), single.get("POSITION"), case.x, case, prec)
     # halos were exchanged (and ghosts were present where fluid borders fluid)
     assert sum(reps[r][-1].halo_bytes for r in range(R)) > 0
     if not name.startswith("db2d"):      # db2d: the water column lies in one slab
@@ -211,16 +204,9 @@ def test_full_size_two_slabs_equal_single_gpu():
     sims, reps, g = run_ranks(case, 2, 1, 3, **over)
     assert all(reps[r][s].iters == rs[s].iters == 3 for r in range(2) for s in range(3))
     assert sum(s.owned_counts()[0] for s in sims) == case.n_fluid
-    rel, ab = TOL[32]
     for fld in ("PRESSURE", "VELOCITY"):
-        a, b = gathered(sims, fld), single.get(fld)
-        scale = max(np.abs(b).max(), 1e-3)
-        assert np.abs(a - b).max() <= rel * scale + ab, fld
-    x, xs = gathered(sims, "POSITION"), single.get("POSITION")
-    d = x - xs
-    L = case.hi[1] - case.lo[1]
-    d[:, 1] = (d[:, 1] + 0.5 * L) % L - 0.5 * L
-    assert np.abs(d).max() <= rel * np.abs(case.x).max() + ab
+        assert_close(fld, gathered(sims, fld), single.get(fld), 32)
+    assert_disp_close("POSITION", gathered(sims, "POSITION"), single.get("POSITION"), case.x, case, 32)
     assert all(reps[r][-1].n_ghost_fluid > 0 for r in range(2))
     for s in sims:
         s.close()
@@ -237,10 +223,8 @@ def test_mean_free_over_slab_ranks():
     sims, reps, g = run_ranks(case, 3, 0, 3, **over)
     for s in range(3):
         assert {reps[r][s].iters for r in range(3)} == {rs[s].iters}
-    rel, ab = TOL[64]
     for fld in ("PRESSURE", "VELOCITY"):
-        a, b = gathered(sims, fld), single.get(fld)
-        assert np.abs(a - b).max() <= rel * max(np.abs(b).max(), 1e-3) + ab, fld
+        assert_close(fld, gathered(sims, fld), single.get(fld), 64)
     for s in sims:
         s.close()
     g.close()
@@ -255,10 +239,9 @@ def test_moving_lid_over_slab_ranks():
     sims, reps, g = run_ranks(case, 2, 0, 4)
     for s in range(4):
         assert {reps[r][s].iters for r in range(2)} == {rs[s].iters}
-    rel, ab = TOL[64]
-    for fld in ("PRESSURE", "VELOCITY", "POSITION"):
-        a, b = gathered(sims, fld), single.get(fld)
-        assert np.abs(a - b).max() <= rel * max(np.abs(b).max(), 1e-3) + ab, fld
+    for fld in ("PRESSURE", "VELOCITY"):
+        assert_close(fld, gathered(sims, fld), single.get(fld), 64)
+    assert_disp_close("POSITION", gathered(sims, "POSITION"), single.get("POSITION"), case.x, case, 64)
     for s in sims:
         s.close()
     g.close()
