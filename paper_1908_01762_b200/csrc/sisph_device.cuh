@@ -38,6 +38,34 @@ template <> __device__ __forceinline__ dbl4 mk4<double>(double x, double y, doub
     return dbl4{x, y, z, w};
 }
 
+// 8-element records with one 256-bit access (sm_100: LDG.E.ENL2.256 / STG.E.ENL2.256);
+// fp64 records are two 256-bit halves.  Read-only (.nc) loads: callers never read a
+// record array the same kernel writes.
+__device__ __forceinline__ void ld8(const float* p, float (&r)[8])
+{
+    asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7])
+        : "l"(p));
+}
+__device__ __forceinline__ void ld8(const double* p, double (&r)[8])
+{
+    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3]) : "l"(p));
+    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(r[4]), "=d"(r[5]), "=d"(r[6]), "=d"(r[7]) : "l"(p + 4));
+}
+__device__ __forceinline__ void st8(float* p, const float (&r)[8])
+{
+    asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(r[0]), "f"(r[1]), "f"(r[2]),
+                 "f"(r[3]), "f"(r[4]), "f"(r[5]), "f"(r[6]), "f"(r[7])
+                 : "memory");
+}
+__device__ __forceinline__ void st8(double* p, const double (&r)[8])
+{
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(r[0]), "d"(r[1]), "d"(r[2]), "d"(r[3])
+                 : "memory");
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p + 4), "d"(r[4]), "d"(r[5]), "d"(r[6]), "d"(r[7])
+                 : "memory");
+}
+
 // ---------------------------------------------------------------------------
 // Kernel-argument block: geometry + scheme constants, passed by value.
 // ---------------------------------------------------------------------------

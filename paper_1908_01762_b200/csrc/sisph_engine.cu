@@ -132,7 +132,9 @@ template <class T, int D> struct Engine : EngineBase {
     int* onew = nullptr;
     int open_spawned = 0, open_deleted = 0;
     bool pref_done = false;
-    V *rkA = nullptr, *rkB = nullptr, *vk = nullptr, *dk = nullptr;
+    // GTVF sub-step records (A14): per particle {r*, m / rho^2, r^k - r^0, 0} (two V4), ping-pong
+    V *gtA = nullptr, *gtB = nullptr, *vk = nullptr;
+    V *recF = nullptr, *recS = nullptr;   // joint {r, m, u, rho} records of A8 / A11 (k_pack_rec)
     V* fnp = nullptr;       // non-pressure acceleration of A8 (adaptive dt)
     int* dcnt_w = nullptr;  // device flag of set_field's wall check
     bool stepped = false;   // a correct has completed: next_dt is defined
@@ -201,7 +203,7 @@ template <class T, int D> struct Engine : EngineBase {
 
     ~Engine() override
     {
-        void* ptrs[] = {pos, pos_alt, vel, vel_alt, us, us_alt, vt, vt_alt, rn, rstar, nrm, nstmp, uwl, rkA, rkB, vk, dk,
+        void* ptrs[] = {pos, pos_alt, vel, vel_alt, us, us_alt, vt, vt_alt, rn, rstar, nrm, nstmp, uwl, gtA, gtB, vk, recF, recS,
                         p, p_alt, rho, rho_alt, rhs, diag, fs, fs_alt, pid, pid_alt, keys, rank, perm0, perm,
                         ccount, fstart, wstart, bsum, nbr, cnt, ctl, partials, dtmp, nbr_in, cnt_in,
                         nbs, cnt_s, wperm_s, wstart_s, coef, dflag, dflag2, dpre, dlist[0], dlist[1], dlist[2],
@@ -411,7 +413,7 @@ template <class T, int D> struct Engine : EngineBase {
     if (rc) return rc;
         AL(pos, V, NT) AL(pos_alt, V, NT) AL(vel, V, NT) AL(vel_alt, V, NT) AL(us, V, NT) AL(us_alt, V, NT)
         AL(vt, V, NF) AL(vt_alt, V, NF) AL(rn, V, NT) AL(rstar, V, NT) AL(nrm, V, NW) AL(nstmp, V, NW) AL(uwl, V, NW)
-        AL(rkA, V, NT) AL(rkB, V, NT) AL(vk, V, NF) AL(dk, V, NF) AL(fnp, V, NF) AL(dcnt_w, int, 4)
+        AL(gtA, V, 2 * NT) AL(gtB, V, 2 * NT) AL(recF, V, 2 * NT) AL(recS, V, 2 * NT) AL(vk, V, NF) AL(fnp, V, NF) AL(dcnt_w, int, 4)
         AL(p, T, NT) AL(p_alt, T, NT) AL(rho, T, NT) AL(rho_alt, T, NT) AL(rhs, T, NF) AL(diag, T, NF)
         AL(fs, uint8_t, NF) AL(fs_alt, uint8_t, NF) AL(pid, int, NT) AL(pid_alt, int, NT)
         AL(keys, int, NT) AL(rank, int, NT) AL(perm0, int, NT) AL(perm, int, NT)
@@ -879,7 +881,7 @@ template <class T, int D> struct Engine : EngineBase {
             SCK(cudaMemcpyAsync(b + (size_t)newNf * esz, wtmp, (size_t)Nw * esz, cudaMemcpyDeviceToDevice, st));
             return SISPH_OK;
         };
-        void* vecs[] = {pos, pos_alt, rn, rstar, rkA, rkB, vel, vel_alt, us, us_alt};
+        void* vecs[] = {pos, pos_alt, rn, rstar, vel, vel_alt, us, us_alt};
         for (void* q : vecs) SRET(mv(q, sizeof(V)));
         void* scs[] = {p, p_alt, rho, rho_alt};
         for (void* q : scs) SRET(mv(q, sizeof(T)));
@@ -1123,7 +1125,7 @@ template <class T, int D> struct Engine : EngineBase {
             SCK(cudaMemcpyAsync(rho + Nf, rho_alt + Nf, Nw * sizeof(T), cudaMemcpyDeviceToDevice, st));
             SCK(cudaMemcpyAsync(pid + Nf, pid_alt + Nf, Nw * sizeof(int), cudaMemcpyDeviceToDevice, st));
             SCK(cudaMemcpyAsync(p + Nf, p_alt + Nf, Nw * sizeof(T), cudaMemcpyDeviceToDevice, st));
-            V* bufs[] = {pos_alt, rkA, rkB, rn, rstar};
+            V* bufs[] = {pos_alt, rn, rstar};
             for (V* q : bufs) SCK(cudaMemcpyAsync(q + Nf, pos + Nf, Nw * sizeof(V), cudaMemcpyDeviceToDevice, st));
             if (dist()) {
                 // new relative slot of every pre-sort wall slot
@@ -1334,8 +1336,10 @@ template <class T, int D> struct Engine : EngineBase {
             pl_add(W, vel + Nf, sizeof(V));
             SRET(halo_walls(W));
         }
-        // A8
-        if (Nfo) ++nlaunch, k_forces_predict<T, D><<<nblk(Nfo, 128), 128, 0, st>>>(P, (T)dt, pos, vel, vt, rho, nb1, cn1, cap1, us, rstar, fnp);
+        // A8 (neighbours' {r, m, u, rho} packed into one 256-bit record)
+        if (Ntot) ++nlaunch, k_pack_rec<T><<<nblk(Ntot, 256), 256, 0, st>>>(pos, vel, Ntot, reinterpret_cast<T*>(recF));
+        if (Nfo) ++nlaunch, k_forces_predict<T, D><<<nblk(Nfo, 128), 128, 0, st>>>(P, (T)dt, pos, vel, vt, rho, nb1, cn1, cap1, us, rstar, fnp,
+                                                                                   reinterpret_cast<const T*>(recF));
         SCK(cudaGetLastError());
         if (dist()) {
             PackList L{};
@@ -1389,7 +1393,9 @@ template <class T, int D> struct Engine : EngineBase {
             pl_add(W, us + Nf, sizeof(V));
             SRET(halo_walls(W));
         }
-        // A11 with the first PPE sweep fused (walls first get p^0, R14)
+        // A11 with the first PPE sweep fused (walls first get p^0, R14); neighbours' {r*, m, u*, rho}
+        // packed into one 256-bit record
+        if (Ntot) ++nlaunch, k_pack_rec<T><<<nblk(Ntot, 256), 256, 0, st>>>(pos, us, Ntot, reinterpret_cast<T*>(recS));
         SCK(cudaMemsetAsync(&ctl->lambda_bits, 0, sizeof(unsigned long long), st));
         SCK(cudaMemsetAsync(ctl, 0, 4 * sizeof(int), st));  // ticket, iter, done, nonfinite
         SRET(mark(7));   // t_PPE starts at A11 (wall p^0, RHS, D_ii, sweep 1)
@@ -1401,7 +1407,8 @@ template <class T, int D> struct Engine : EngineBase {
             SRET(halo_walls(W));
         }
         ++nlaunch, k_rhs_diag<T, D><<<std::max(nblk(Nfo, RHS_T), 1), RHS_T, 0, st>>>(
-                       P, (T)(1.0 / dt), pos, us, rho, fs, nbr, cnt, P.cap, rhs, diag, coef, ctl, p, p_alt, partials);
+                       P, (T)(1.0 / dt), pos, us, rho, fs, nbr, cnt, P.cap, rhs, diag, coef, ctl, p, p_alt, partials,
+                       reinterpret_cast<const T*>(recS));
         SCK(cudaGetLastError());
         SRET(mark(8));
         pre_swept = true;
@@ -1663,32 +1670,36 @@ template <class T, int D> struct Engine : EngineBase {
         return SISPH_OK;
     }
 
-    // K modified-GTVF sub-steps (A14) from r* = pos; returns the final positions in rK
-    int gtvf_substeps(T dtau, bool inner, const V*& rK)
+    // K modified-GTVF sub-steps (A14) from r* = pos; returns the final records (delta^K = r^K - r^0
+    // in the second V4 of each particle's record)
+    int gtvf_substeps(T dtau, bool inner, const T*& rK)
     {
-        if (Ntot) ++nlaunch, k_gtvf_prep<T><<<nblk(Ntot, 256), 256, 0, st>>>(pos, rho, Ntot, rkA, rkB);
+        T* a = reinterpret_cast<T*>(gtA);
+        T* b = reinterpret_cast<T*>(gtB);
+        if (Ntot) ++nlaunch, k_gtvf_prep<T><<<nblk(Ntot, 256), 256, 0, st>>>(pos, rho, Ntot, a, b);
         if (inner) SCK(cudaMemsetAsync(&ctl->gtvf_far, 0, sizeof(int), st));
-        const V* src = rkB;
+        const T* src = b;
         for (int k = 0; k < K; k++) {
-            V* dst = (k & 1) ? rkB : rkA;
+            T* dst = (k & 1) ? b : a;
             if (Nfo) {
                 if (inner)
                     ++nlaunch, k_gtvf_substep<T, D><<<nblk(Nfo, 128), 128, 0, st>>>(P, dtau, src, dst, vk, p, nbr_in,
-                                                                                    P.cap_in, cnt_in, k == 0, pos, 1, ctl);
+                                                                                    P.cap_in, cnt_in, k == 0, 1, ctl);
                 else
                     ++nlaunch, k_gtvf_substep<T, D><<<nblk(Nfo, 128), 128, 0, st>>>(P, dtau, src, dst, vk, p, nbr,
-                                                                                    P.cap, cnt, k == 0, pos, 0, ctl);
+                                                                                    P.cap, cnt, k == 0, 0, ctl);
             }
             SCK(cudaGetLastError());
             if (dist()) {
+                // the record's r* carries the periodic image shift of the ghost, delta does not
                 PackList L{};
-                pl_add(L, dst, sizeof(V));   // displacements: no periodic image shift
+                pl_add(L, dst, 2 * sizeof(V), 1);
                 SRET(halo_fluid(L));
             }
             src = dst;
         }
         SCK(cudaGetLastError());
-        rK = src;   // delta^K = r^K - r^0 (4th lane m / rho^2, unused by k_advance)
+        rK = src;
         return SISPH_OK;
     }
 
@@ -1727,7 +1738,7 @@ template <class T, int D> struct Engine : EngineBase {
         }
         if (Nfo) ++nlaunch, k_pgrad_correct<T, D><<<nblk(Nfo, 128), 128, 0, st>>>(P, (T)dt, pos, rho, p, us, nbr, cnt, P.cap, vel, fnp, ctl);
         // A14: K sub-steps (p0 = 0 everywhere when p_ref == 0: the shift is exactly zero)
-        const V* rK = nullptr;   // GTVF displacement r^K - r^0 (none when p0 = 0)
+        const T* rK = nullptr;   // GTVF records with delta^K = r^K - r^0 (none when p0 = 0)
         if (P.p_ref != T(0) && K > 0 && (Nf || dist())) {
             SRET(gtvf_substeps((T)(dt / K), inner_valid, rK));
             if (inner_valid) {

@@ -1091,6 +1091,23 @@ __global__ void FILTER_BOUNDS k_filter(Params<T> P, int row0, int nrows, const V
 }
 
 // ===========================================================================
+// Joint per-particle records for the pair passes: rec[i] = {a[i], b[i]} (8 working-
+// precision values), so that a neighbour's position + mass and velocity + density
+// arrive with ONE 256-bit gather instead of two 128-bit ones from two arrays (the
+// pair passes are bound by L1 requests).  A8 reads {r^n, m, u, rho}
+// (packed after A7), A11 reads {r*, m, u*, rho} (packed after A10).
+// ===========================================================================
+template <class T>
+__global__ void k_pack_rec(const V4<T>* __restrict__ a, const V4<T>* __restrict__ b, int n, T* __restrict__ rec)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const V4<T> x = ld4(a + i), u = ld4(b + i);
+    const T r[8] = {x.x, x.y, x.z, x.w, u.x, u.y, u.z, u.w};
+    st8(rec + 8 * (size_t)i, r);
+}
+
+// ===========================================================================
 // A6: summation density, eq:summation_density, self included;
 // walls keep rho0 unless wall_rho_summation (R4).  Free surface flag
 // rho_i / rho0 < 0.8 for fluid.
@@ -1258,7 +1275,8 @@ __global__ void __launch_bounds__(128) k_forces_predict(Params<T> P, T dt, const
                                                         const V4<T>* __restrict__ vel, const V4<T>* __restrict__ vt,
                                                         const T* __restrict__ rho, const int* __restrict__ nbr,
                                                         const int* __restrict__ cnt, int ncap, V4<T>* __restrict__ us,
-                                                        V4<T>* __restrict__ rstar, V4<T>* __restrict__ fnp)
+                                                        V4<T>* __restrict__ rstar, V4<T>* __restrict__ fnp,
+                                                        const T* __restrict__ rec)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= P.Nfo) return;
@@ -1275,7 +1293,9 @@ __global__ void __launch_bounds__(128) k_forces_predict(Params<T> P, T dt, const
     }
     for_nbrs_pfx<SISPH_FORCES_PF>(nbr, ncap, i, n, [&](int j) {
         // (loose-list pairs beyond 3h contribute exactly 0: dW/dr = 0 for q >= 3)
-        V4<T> xj = ld4(pos + j), uj = ld4(vel + j);
+        T q[8];
+        ld8(rec + 8 * (size_t)j, q);                 // {r_j, m_j, u_j, rho_j} (k_pack_rec)
+        const V4<T> xj = mk4<T>(q[0], q[1], q[2], q[3]), uj = mk4<T>(q[4], q[5], q[6], q[7]);
         const bool fl = j < P.Nf;
         V4<T> utj = fl ? ld4(vt + j) : uj;
         T d[3];
@@ -1306,7 +1326,7 @@ __global__ void __launch_bounds__(RHS_T) k_rhs_diag(Params<T> P, T inv_dt, const
                                                     const int* __restrict__ cnt, int ncap, T* __restrict__ rhs,
                                                     T* __restrict__ diag, T* __restrict__ coef, Ctl* ctl,
                                                     const T* __restrict__ pin, T* __restrict__ pout,
-                                                    double* __restrict__ partials)
+                                                    double* __restrict__ partials, const T* __restrict__ rec)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     double lam = 0.0, dn = 0.0, dd = 0.0;
@@ -1322,7 +1342,9 @@ __global__ void __launch_bounds__(RHS_T) k_rhs_diag(Params<T> P, T inv_dt, const
 #endif
         T fb[4] = {T(0), T(0), T(0), T(0)};             // SISPH_RHS_VST: one 16/32-byte store per chunk
         for_nbrs_k_pf<SISPH_RHS_PF>(nbr, ncap, i, n, [&](int j, int k) {
-            V4<T> xj = ld4(pos + j), uj = ld4(us + j);
+            T q[8];
+            ld8(rec + 8 * (size_t)j, q);             // {r*_j, m_j, u*_j, rho_j} (k_pack_rec)
+            const V4<T> xj = mk4<T>(q[0], q[1], q[2], q[3]), uj = mk4<T>(q[4], q[5], q[6], q[7]);
             T rhoj = uj.w;                           // rho_j rides in u*_j's 4th lane
             T d[3], r, ri;
             T r2 = pair_vec<T, D>(P, xi, xj, d);
@@ -2032,41 +2054,41 @@ __global__ void __launch_bounds__(128) k_pgrad_correct(Params<T> P, T dt, const 
 // constant through the sub-steps (rho frozen at stage 1, R5), so it rides in
 // the position vector's 4th lane and costs no extra gather.
 template <class T>
-__global__ void k_gtvf_prep(const V4<T>* __restrict__ pos, const T* __restrict__ rho, int n, V4<T>* __restrict__ a,
-                            V4<T>* __restrict__ b)
+__global__ void k_gtvf_prep(const V4<T>* __restrict__ pos, const T* __restrict__ rho, int n, T* __restrict__ a,
+                            T* __restrict__ b)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const V4<T> x = ld4(pos + i);
     const T r = rho[i];
-    // displacement r^0 - r^0 = 0 and m / rho^2 (eq:mom:sph:gtvf)
-    const V4<T> z = mk4<T>(T(0), T(0), T(0), x.w / (r * r));
-    a[i] = z;
-    if (b) b[i] = z;
+    // {r^0 = r*, m / rho^2 (eq:mom:sph:gtvf), delta^0 = 0, 0}
+    const T z[8] = {x.x, x.y, x.z, x.w / (r * r), T(0), T(0), T(0), T(0)};
+    st8(a + 8 * (size_t)i, z);
+    if (b) st8(b + 8 * (size_t)i, z);
 }
 
 // nbr/stride/cnt select the full r* list or the inner list (pairs with
 // r* < 3 h~ + skin).  With the inner list, a particle that has moved more
 // than skin/2 from r* raises ctl->gtvf_far and the host repeats the
 // sub-steps on the full list (exact either way).
-// The sub-step state is the displacement delta^k = r^k - r^0 (same recursion as
-// eq:int:gtvf:pos) with m_j / rho_j^2 in the 4th lane; a pair's r^k_ij is
-// (r^0_i - r^0_j) + (delta^k_i - delta^k_j): the difference of the two r* is
-// exact for neighbours (Sterbenz), so the GTVF force sees the geometry to the
-// working precision of r_ij itself and not to the ulp of the coordinates (fp32
-// at |x| ~ 3 with h = 1/256: 6e-5 h), and eq:int:vhatnp2's (r^K - r^0)/dt keeps
-// its digits.
+// A particle's sub-step record is {r^0 = r*, m / rho^2, delta^k = r^k - r^0, 0}
+// (the recursion of eq:int:gtvf:pos carried on delta), read with ONE 256-bit
+// load per neighbour.  A pair's r^k_ij is (r^0_i - r^0_j) + (delta^k_i - delta^k_j):
+// the difference of the two r* is exact for neighbours (Sterbenz), so the GTVF
+// force sees the geometry to the working precision of r_ij itself, not to the
+// ulp of the coordinates (fp32 at |x| ~ 3 with h = 1/256: 6e-5 h), and
+// eq:int:vhatnp2's (r^K - r^0)/dt keeps its digits.
 template <class T, int D>
-__global__ void __launch_bounds__(128) k_gtvf_substep(Params<T> P, T dtau, const V4<T>* __restrict__ rk,
-                                                      V4<T>* __restrict__ rk1, V4<T>* __restrict__ vk,
+__global__ void __launch_bounds__(128) k_gtvf_substep(Params<T> P, T dtau, const T* __restrict__ rk,
+                                                      T* __restrict__ rk1, V4<T>* __restrict__ vk,
                                                       const T* __restrict__ p, const int* __restrict__ nbr, int ncap,
-                                                      const int* __restrict__ cnt, int first,
-                                                      const V4<T>* __restrict__ rstar, int check, Ctl* ctl)
+                                                      const int* __restrict__ cnt, int first, int check, Ctl* ctl)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= P.Nfo) return;
-    const V4<T> di = ld4(rk + i);
-    const V4<T> xi = ld4(rstar + i);
+    T ri8[8];
+    ld8(rk + 8 * (size_t)i, ri8);
+    const V4<T> xi = mk4<T>(ri8[0], ri8[1], ri8[2], ri8[3]);
     T ax = 0, ay = 0, az = 0;
     int n = cnt[i];
     if (P.ptype && P.ptype[i] != 0) n = 0;           // R34: no GTVF shift for inlet / outlet
@@ -2074,17 +2096,18 @@ __global__ void __launch_bounds__(128) k_gtvf_substep(Params<T> P, T dtau, const
 #define SISPH_GTVF_PF 1   // B200, C5: PD 0 / 1 / 2 / 3 -> 113 / 107 / 125 / 120 us per sub-step
 #endif
     for_nbrs_pf<SISPH_GTVF_PF>(nbr, ncap, i, n, [&](int j) {
-        const V4<T> dj = ld4(rk + j);
-        const V4<T> xj = ld4(rstar + j);
+        T rj8[8];
+        ld8(rk + 8 * (size_t)j, rj8);
+        const V4<T> xj = mk4<T>(rj8[0], rj8[1], rj8[2], rj8[3]);
         T d[3], r, ri;
         pair_vec<T, D>(P, xi, xj, d);
-        d[0] += di.x - dj.x;
-        d[1] += di.y - dj.y;
-        d[2] = D == 3 ? d[2] + (di.z - dj.z) : T(0);
+        d[0] += ri8[4] - rj8[4];
+        d[1] += ri8[5] - rj8[5];
+        d[2] = D == 3 ? d[2] + (ri8[6] - rj8[6]) : T(0);
         T r2 = d[0] * d[0] + d[1] * d[1];
         if (D == 3) r2 += d[2] * d[2];
         r_of(r2, r, ri);
-        T f = dj.w * quintic4(r * P.inv_ht) * ri;   // m_j / rho_j^2 * |gradW| / r (dwkt below)
+        T f = rj8[3] * quintic4(r * P.inv_ht) * ri;   // m_j / rho_j^2 * |gradW| / r (dwkt below)
         ax += f * d[0];
         ay += f * d[1];
         if (D == 3) az += f * d[2];
@@ -2101,11 +2124,11 @@ __global__ void __launch_bounds__(128) k_gtvf_substep(Params<T> P, T dtau, const
     const V4<T> zero = mk4<T>(T(0), T(0), T(0), T(0));
     const V4<T> v = first ? zero : ld4(vk + i);
     const T h2 = T(0.5) * dtau * dtau;
-    const V4<T> dl = mk4<T>(di.x + dtau * v.x + h2 * ax, di.y + dtau * v.y + h2 * ay,
-                            D == 3 ? di.z + dtau * v.z + h2 * az : T(0), di.w);
-    rk1[i] = dl;
+    const T o8[8] = {ri8[0], ri8[1], ri8[2], ri8[3], ri8[4] + dtau * v.x + h2 * ax, ri8[5] + dtau * v.y + h2 * ay,
+                     D == 3 ? ri8[6] + dtau * v.z + h2 * az : T(0), T(0)};
+    st8(rk1 + 8 * (size_t)i, o8);
     vk[i] = mk4<T>(v.x + dtau * ax, v.y + dtau * ay, D == 3 ? v.z + dtau * az : T(0), T(0));
-    if (check && dl.x * dl.x + dl.y * dl.y + dl.z * dl.z > P.skin_half2) atomicExch(&ctl->gtvf_far, 1);
+    if (check && o8[4] * o8[4] + o8[5] * o8[5] + o8[6] * o8[6] > P.skin_half2) atomicExch(&ctl->gtvf_far, 1);
 }
 
 // ===========================================================================
@@ -2113,7 +2136,7 @@ __global__ void __launch_bounds__(128) k_gtvf_substep(Params<T> P, T dtau, const
 // (eq:int:rnp2, R24), periodic wrap.
 // ===========================================================================
 template <class T, int D>
-__global__ void k_advance(Params<T> P, T dt, const V4<T>* __restrict__ dK, const V4<T>* __restrict__ rn,
+__global__ void k_advance(Params<T> P, T dt, const T* __restrict__ dK, const V4<T>* __restrict__ rn,
                           const V4<T>* __restrict__ vel, V4<T>* __restrict__ pos, V4<T>* __restrict__ vt, Ctl* ctl,
                           const T* __restrict__ uout)
 {
@@ -2136,7 +2159,8 @@ __global__ void k_advance(Params<T> P, T dt, const V4<T>* __restrict__ dK, const
         vt[i] = mk4<T>(ux, T(0), T(0), T(0));
     } else if (i < P.Nfo) {
         V4<T> x = ld4(rn + i), u = ld4(vel + i), ut = ld4(vt + i);
-        V4<T> dl = dK ? ld4(dK + i) : mk4<T>(T(0), T(0), T(0), T(0));   // r^K - r^0
+        // r^K - r^0: the second half of the GTVF record (k_gtvf_substep)
+        const V4<T> dl = dK ? ld4(reinterpret_cast<const V4<T>*>(dK + 8 * (size_t)i + 4)) : mk4<T>(T(0), T(0), T(0), T(0));
         T tx = u.x + dl.x / dt, ty = u.y + dl.y / dt;
         T tz = D == 3 ? u.z + dl.z / dt : T(0);
         T hd = T(0.5) * dt;
