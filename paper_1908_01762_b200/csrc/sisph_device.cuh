@@ -157,9 +157,10 @@ __device__ __forceinline__ T pair_vec(const Params<T>& P, const V4<T>& a, const 
 // ---------------------------------------------------------------------------
 // Exact neighbour decision (R2): r^2 < R^2 evaluated in fp64 exactly as the
 // definition is written (difference, minimum image, products and sums in
-// order, no contraction).  Working in fp32, a cheap prefilter with a
-// relative band of 2^-12 decides all pairs whose fp32 r^2 is clearly inside
-// or outside; only the band goes to fp64 (it is also the whole decision in
+// order, no contraction).  Working in fp32, a cheap prefilter decides all
+// pairs whose fp32 r^2 is outside a band [R2lo, R2hi] around R^2 that bounds
+// the fp32 rounding (a few 2^-24 relative plus the periodic shift terms, set in
+// the engine); only the band goes to fp64 (it is also the whole decision in
 // fp64 mode).
 // ---------------------------------------------------------------------------
 // the rare fp32 band case, out of line so the candidate loop stays small;

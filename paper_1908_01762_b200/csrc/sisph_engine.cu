@@ -314,8 +314,22 @@ template <class T, int D> struct Engine : EngineBase {
         }
         ncells = (int)nc_tot;
         P.R2d = R * R;
-        P.R2lo = (float)(R * R * (1.0 - 1.0 / 4096.0));
-        P.R2hi = (float)(R * R * (1.0 + 1.0 / 4096.0));
+        // fp32 prefilter band of the exact neighbour decision (R2): |fl32(r^2) - r^2| <= band R^2
+        // for every pair near R with fp32 coordinates: each component difference carries <= u |d|
+        // (u = 2^-24), a periodic image shift <= u 2 L_a (the shifted coordinate) + |L_f - L_d|
+        // (the fp32 box length), the squares and sums <= 4 u r^2; doubled for safety.  Pairs
+        // outside the band are decided by the fp32 comparison (it cannot disagree with the fp64
+        // one there), pairs inside it in fp64 (exact_band): a narrow band keeps the lattices'
+        // near-ties (C5: ~30 per particle at 3h) out of the fp64 path once they have moved
+        {
+            const double u = 1.0 / 16777216.0;
+            double b = 10.0 * u;
+            for (int a = 0; a < D; a++)
+                if (P.per[a]) b += 2.0 * (2.0 * u * P.Ld[a] + fabs((double)P.Lf[a] - P.Ld[a])) / R;
+            b *= 2.0;
+            P.R2lo = nextafterf((float)(R * R * (1.0 - b)), 0.0f);
+            P.R2hi = nextafterf((float)(R * R * (1.0 + b)), 1e30f);
+        }
         P.R2cut = (T)(R * R * (1.0 + 1.0 / 1024.0));
         const double sigd = D == 2 ? 7.0 / (478.0 * M_PI) : 1.0 / (120.0 * M_PI);
         auto hd = [&](double hh, T& sig, T& dwk, T& inv_) {

@@ -486,7 +486,7 @@ struct NbCursorS {
 //
 // Two kernels:
 //  * k_build_cells (exact): N(i) = { j != i : r_ij^2 < (3h)^2 } decided as R2
-//    prescribes (fp32 prefilter with a +-2^-12 band decided in fp64 from the
+//    prescribes (fp32 prefilter with a rounding-bound band [R2lo, R2hi] decided in fp64 from the
 //    unshifted positions with the oracle's minimum-image arithmetic; every
 //    pair in fp64 mode), optionally also the GTVF inner list (fluid rows;
 //    pairs with r^2 < Rin2f);

@@ -1,6 +1,11 @@
 """Summarise ncu reports (--page details + raw dram bytes) into profiles/.
 
-    python scripts/ncu_summary.py <out.txt> <rep1.ncu-rep> [<rep2> ...]
+    python scripts/ncu_summary.py [--workload NAME] <out.txt> <rep1.ncu-rep> [<rep2> ...]
+
+With --workload, also writes the per-workload records bench.py reads:
+profiles/traffic_NAME.json (dram bytes of one k_sweep launch, its roofline
+`traffic`) and profiles/instr_NAME.json (warp instructions, dram bytes and ncu
+duration per captured kernel launch).
 """
 import csv
 import io
@@ -51,20 +56,41 @@ def to_bytes(v, u):
     return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
 
 
+def to_us(v, u):
+    v = float(v.replace(",", ""))
+    return v * {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}.get(u, 1.0)
+
+
+def short(name):
+    return name.split("(")[0].replace("void ", "").split("<")[0].replace("sb::", "")
+
+
 if __name__ == "__main__":
-    out = sys.argv[1]
+    args = sys.argv[1:]
+    wl = None
+    if args and args[0] == "--workload":
+        wl, args = args[1], args[2:]
+    out = args[0]
     allines = []
-    for rep in sys.argv[2:]:
+    instr = {}
+    for rep in args[1:]:
         try:
             name, lines, extra = summarise(rep)
         except (ValueError, IndexError) as e:
             print(f"skip {rep}: {e}", file=sys.stderr)
             continue
         allines += [f"# {rep}"] + lines + [""]
-        if "k_sweep" in name and "dram__bytes_read.sum" in extra:
+        if "dram__bytes_read.sum" in extra and "sm__sass_inst_executed.sum" in extra:
             b = to_bytes(*extra["dram__bytes_read.sum"]) + to_bytes(*extra["dram__bytes_write.sum"])
-            with open("profiles/sweep_traffic.json", "w") as f:
-                json.dump({"kernel": name, "dram_bytes_per_launch": b, "source": rep}, f, indent=1)
+            instr[short(name)] = {"warp_instr": float(extra["sm__sass_inst_executed.sum"][0].replace(",", "")),
+                                  "dram_bytes": b, "us_ncu": to_us(*extra["gpu__time_duration.sum"]),
+                                  "source": rep}
+            if wl and "k_sweep" in name:
+                with open(f"profiles/traffic_{wl}.json", "w") as f:
+                    json.dump({"kernel": name, "dram_bytes_per_launch": b, "source": rep}, f, indent=1)
+    if wl and instr:
+        with open(f"profiles/instr_{wl}.json", "w") as f:
+            json.dump(instr, f, indent=1)
     with open(out, "w") as f:
         f.write("\n".join(allines) + "\n")
     print("\n".join(allines))
