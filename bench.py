@@ -44,7 +44,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="sisph", choices=["sisph", "reference"])
-    ap.add_argument("--workload", default="dambreak3d", choices=["dambreak3d", "tgv3d", "dambreak2d", "hydrostatic"])
+    ap.add_argument("--workload", default="dambreak3d",
+                    choices=["dambreak3d", "tgv3d", "dambreak2d", "hydrostatic", "tgv2d"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
@@ -69,6 +70,9 @@ def workload(name, ranks=1):
     elif name == "dambreak2d":
         c = synth.dambreak2d()
         desc = "2D dam break 500x1000 fluid in a 4x4 tank (BASELINE configs[2]), fp32, tol 1e-2"
+    elif name == "tgv2d":
+        c = synth.tgv2d()
+        desc = "2D Taylor-Green 50x50 periodic (BASELINE configs[0]), fp64, tol 1e-4, 10 steps as configured"
     else:
         c = synth.hydrostatic()
         desc = "2D hydrostatic column 200x400 (BASELINE configs[1]), fp32, tol 1e-3"
@@ -90,6 +94,8 @@ def sample_case(name, small=False):
         return synth.tgv3d(n=64), "64^3 instance of the same TGV-3D recipe"
     if name == "dambreak2d":
         return synth.dambreak2d(nx=250, ny=500, dx=0.004), "dx=0.004 instance of the same dam break"
+    if name == "tgv2d":
+        return synth.tgv2d(), "the full workload"
     return synth.hydrostatic(), "the full workload"
 
 
@@ -261,7 +267,7 @@ def run_reference(args):
           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
 
 
-SLAB_AXIS = {"dambreak3d": 1, "tgv3d": 0, "dambreak2d": 0, "hydrostatic": 0}
+SLAB_AXIS = {"dambreak3d": 1, "tgv3d": 0, "dambreak2d": 0, "hydrostatic": 0, "tgv2d": 0}
 
 
 def run_sisph(args):
