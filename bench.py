@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--slab-self", action="store_true",
                     help="ablation on one GPU: the slab path (halos over NCCL to itself across the periodic y)")
+    ap.add_argument("--ppe-loop", type=int, default=0,
+                    help="PPE loop form: 0 auto, 1 host-polled batches, 2 CUDA-graph WHILE node, 3 persistent kernel")
     ap.add_argument("--matrix-free", action="store_true",
                     help="ablation: the sweep recomputes fac_ij every sweep (PAPER.md:785-801)")
     return ap.parse_args()
@@ -284,6 +286,8 @@ def run_sisph(args):
     case, desc = workload(args.workload, ranks=world)
     stream = torch.cuda.current_stream()
     over = dict(stream=stream.cuda_stream, device=local, matrix_free=1 if args.matrix_free else 0)
+    if args.ppe_loop:
+        over["ppe_loop"] = args.ppe_loop
     if world > 1:
         # one process per GPU: torch.distributed (NCCL) carries the NCCL id; the halo
         # exchanges and per-sweep allreduce run inside libsisph over NCCL

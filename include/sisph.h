@@ -101,10 +101,11 @@ typedef struct {
                                a PPE with no Dirichlet row (fully periodic / enclosed flows, whose
                                operator has the constant null space: eq:coeff rows sum to zero).
                                0 (default) = eq:p-sor as printed.  Not with ppe_loop = 3. */
-    int conv_mean;          /* reading R12b: 1 = eq:convergence compares means over the fluid,
-                               mean|p^{k+1} - p^k| / max(Lambda, mean|p^{k+1}|) (the text calls the
-                               denominator "the mean pressure" and Lambda "a measure of the mean
-                               pressure"); 0 (default) = the sums as printed */
+    int conv_mean;          /* reading R12b: 1 (default) = eq:convergence compares means over the
+                               fluid, mean|p^{k+1} - p^k| / max(Lambda, mean|p^{k+1}|) (the text calls
+                               the denominator "the mean pressure" and Lambda "a measure of the mean
+                               pressure"; with means the paper's Table 1 sweep counts are
+                               reproduced); 0 = the sums as printed */
     int open_x;             /* reading R34: 1 = open boundaries along x (single GPU,
                                bounded x).  After every step, in id order: outlet particles with
                                x >= x_end become dormant; fluid with x >= x_outlet become outlet

@@ -144,7 +144,7 @@ def make_cfg(dim, lo, hi, periodic, h, params: dict | None = None) -> Cfg:
     c.tol = p.get("tol", 1e-2)
     c.wall_rho_summation = p.get("wall_rho_summation", 0)
     c.ppe_mean_free = p.get("ppe_mean_free", 0)
-    c.conv_mean = p.get("conv_mean", 0)
+    c.conv_mean = p.get("conv_mean", 1)   # reading R12b
     c.open_x = p.get("open_x", 0)
     c.x_inlet = p.get("x_inlet", 0.0)
     c.x_outlet = p.get("x_outlet", 0.0)

@@ -650,7 +650,20 @@ template <class T, int D> struct Engine : EngineBase {
         return SISPH_OK;
     }
 
-    // exact sets at the current positions out of the loose list (+ GTVF inner list)
+    // r* of the fluid slots (eq:int:rnp1); slab ranks: the ghosts' from their owners
+    int compute_rstar(double dt)
+    {
+        if (Nfo) ++nlaunch, k_rstar<T, D><<<nblk(Nfo, 256), 256, 0, st>>>(P, (T)dt, Nfo, pos, vt, rstar);
+        SCK(cudaGetLastError());
+        if (dist()) {
+            PackList L{};
+            pl_add(L, rstar, sizeof(V), 1);
+            SRET(halo_fluid(L));
+        }
+        return SISPH_OK;
+    }
+
+    // exact sets at r* out of the loose list (+ GTVF inner list)
     int filter_list()
     {
         // keep the overflow flag of the loose build; reset the statistics
@@ -659,9 +672,8 @@ template <class T, int D> struct Engine : EngineBase {
         int* ni = nbr_in;
         const int rows = Nfo + Nwo;
         if (rows)
-            ++nlaunch, k_filter<T, D, false><<<nblk(rows, 128), 128, 0, st>>>(
-                           P, -1, rows, pos, nbs, cnt_s, cap_s, nbr, cnt, ni, cnt_in, us, fs, T(0), nullptr, nullptr,
-                           nullptr, ctl);
+            ++nlaunch, k_filter<T, D><<<nblk(rows, 128), 128, 0, st>>>(P, rows, rstar, nbs, cnt_s, cap_s, nbr, cnt, ni,
+                                                                        cnt_in, ctl);
         SCK(cudaGetLastError());
         inner_valid = ni != nullptr;
         return SISPH_OK;
@@ -1325,6 +1337,13 @@ template <class T, int D> struct Engine : EngineBase {
             SRET(build_fluid(single));
         }
         SRET(mark(4));
+        if (single) {
+            // A9 (R3): r* = r^n + dt u~^n is known now: the exact sets at r* out of the loose list
+            SRET(mark(5));
+            SRET(compute_rstar(dt));
+            SRET(filter_list_grow());
+            SRET(mark(6));
+        }
         const int* nb1 = single ? nbs : nbr;
         const int* cn1 = single ? cnt_s : cnt;
         const int cap1 = single ? cap_s : P.cap;
@@ -1352,23 +1371,22 @@ template <class T, int D> struct Engine : EngineBase {
         }
         // A8 (neighbours' {r, m, u, rho} packed into one 256-bit record)
         if (Ntot) ++nlaunch, k_pack_rec<T><<<nblk(Ntot, 256), 256, 0, st>>>(pos, vel, Ntot, reinterpret_cast<T*>(recF));
-        if (Nfo) ++nlaunch, k_forces_predict<T, D><<<nblk(Nfo, 128), 128, 0, st>>>(P, (T)dt, pos, vel, vt, rho, nb1, cn1, cap1, us, rstar, fnp,
+        if (Nfo) ++nlaunch, k_forces_predict<T, D><<<nblk(Nfo, 128), 128, 0, st>>>(P, (T)dt, pos, vel, vt, rho, nb1, cn1, cap1, us,
+                                                                                   single ? nullptr : rstar, fnp,
                                                                                    reinterpret_cast<const T*>(recF));
         SCK(cudaGetLastError());
         if (dist()) {
             PackList L{};
-            pl_add(L, rstar, sizeof(V), 1);
+            if (!single) pl_add(L, rstar, sizeof(V), 1);   // single build: compute_rstar did
             pl_add(L, us, sizeof(V));
             SRET(halo_fluid(L));
         }
-        SRET(mark(5));
         if (single) {
-            // A9 (R3): r* becomes the current position set (walls are in every buffer),
-            // r^n is kept as rn; exact sets at r* filtered out of the loose list
+            // r* becomes the current position set (walls are in every buffer), r^n is kept as rn
             std::swap(pos, rstar);
             std::swap(rn, rstar);
-            SRET(filter_list_grow());
         } else {
+            SRET(mark(5));
             // A9: build at r*; carry r^n along as rn
             SRET(sort_set(P, rstar, Nf, Nf, fstart, perm));
             GatherList G{};
@@ -1397,8 +1415,8 @@ template <class T, int D> struct Engine : EngineBase {
             std::swap(p, p_alt);
             std::swap(pid, pid_alt);
             SRET(build_list_grow(true));   // + GTVF inner list
+            SRET(mark(6));
         }
-        SRET(mark(6));
         // A10
         if (Nwo) ++nlaunch, k_wall_velocity<T, D><<<nblk(Nwo, 256), 256, 0, st>>>(P, pos, nbr, cnt, P.cap, nrm, rho, uwl, us, P.ustar_noslip ? 0 : 1);
         SCK(cudaGetLastError());
@@ -1413,7 +1431,7 @@ template <class T, int D> struct Engine : EngineBase {
         SCK(cudaMemsetAsync(&ctl->lambda_bits, 0, sizeof(unsigned long long), st));
         SCK(cudaMemsetAsync(ctl, 0, 4 * sizeof(int), st));  // ticket, iter, done, nonfinite
         SRET(mark(7));   // t_PPE starts at A11 (wall p^0, RHS, D_ii, sweep 1)
-        if (Nwo) ++nlaunch, k_wall_pressure<T, D><<<nblk(Nwo, 256), 256, 0, st>>>(P, pos, rho, nbr, cnt, P.cap, p);
+        if (Nwo) ++nlaunch, k_wall_pressure<T, D><<<nblk((long)Nwo * WL, 256), 256, 0, st>>>(P, pos, rho, nbr, cnt, P.cap, p);
         SCK(cudaGetLastError());
         if (dist()) {
             PackList W{};
@@ -1506,7 +1524,7 @@ template <class T, int D> struct Engine : EngineBase {
         SCK(cudaGraphAddNode(&node, pgraph, nullptr, 0, &cp));
         cudaGraph_t body = cp.conditional.phGraph_out[0];
         SCK(cudaStreamBeginCaptureToGraph(cst, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-        if (Nwo) k_ppe_wall<T, D><<<nblk(Nwo, 256), 256, 0, cst>>>(P, ddesc, cnt, P.cap, ctl);
+        if (Nwo) k_ppe_wall<T, D><<<nblk((long)Nwo * WL, 256), 256, 0, cst>>>(P, ddesc, cnt, P.cap, ctl);
         const int nb = std::max(nblk(Nfo, SWEEP_T), 1);
         const int uh = P.mean_free ? 0 : 1;   // mean-free: k_mean_fix decides and sets the condition
         if (coef)
@@ -1532,7 +1550,7 @@ template <class T, int D> struct Engine : EngineBase {
             SCK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
             pgrid_max = std::max(1, std::min(per * sms, 8192));
         }
-        const int grid = std::max(1, std::min(pgrid_max, nblk(std::max(Nfo, Nwo), SWEEP_T)));
+        const int grid = std::max(1, std::min(pgrid_max, nblk(std::max((long)Nfo, (long)Nwo * WL), SWEEP_T)));
         int cap = P.cap;
         void* args[] = {&P, &ddesc, &rhs, &diag, &cnt, &cap, &ctl, &partials};
         ++nlaunch;
@@ -1555,7 +1573,7 @@ template <class T, int D> struct Engine : EngineBase {
     int launch_sweeps(int count, double tl, int mi, int mx)
     {
         for (int c = 0; c < count; c++) {
-            if (Nwo) ++nlaunch, k_ppe_wall<T, D><<<nblk(Nwo, 256), 256, 0, st>>>(P, ddesc, cnt, P.cap, ctl);
+            if (Nwo) ++nlaunch, k_ppe_wall<T, D><<<nblk((long)Nwo * WL, 256), 256, 0, st>>>(P, ddesc, cnt, P.cap, ctl);
             if (dist()) SRET(halo_p(true));
             bool rec = timing && nrec < MAXREC;
             if (rec) {
@@ -1728,7 +1746,7 @@ template <class T, int D> struct Engine : EngineBase {
             return SISPH_EINVAL;
         }
         // A13
-        if (Nwo) ++nlaunch, k_wall_pressure<T, D><<<nblk(Nwo, 256), 256, 0, st>>>(P, pos, rho, nbr, cnt, P.cap, p);
+        if (Nwo) ++nlaunch, k_wall_pressure<T, D><<<nblk((long)Nwo * WL, 256), 256, 0, st>>>(P, pos, rho, nbr, cnt, P.cap, p);
         SCK(cudaGetLastError());
         if (dist()) {
             PackList W{};
@@ -2201,6 +2219,7 @@ extern "C" void sisph_params_default(sisph_params* p)
     p->min_iter = 2;
     p->max_iter = 1000;
     p->tol = 1e-2;
+    p->conv_mean = 1;   // reading R12b
     p->device = -1;
 }
 

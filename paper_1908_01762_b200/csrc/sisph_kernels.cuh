@@ -348,9 +348,6 @@ __device__ __forceinline__ void for_nbrs_pfx(const int* __restrict__ nbr, int ca
 #ifndef SISPH_FORCES_PF
 #define SISPH_FORCES_PF 2
 #endif
-#ifndef SISPH_WALLP_PF
-#define SISPH_WALLP_PF 2
-#endif
 #ifndef SISPH_PGRAD_PF
 #define SISPH_PGRAD_PF 1
 #endif
@@ -926,40 +923,53 @@ __global__ void BL_LOOSE_BOUNDS k_build_loose(Params<T> P, int ncells, const V4<
     }
 }
 
+// r* = r^n + dt u~^n (eq:int:rnp1) of the slots [0, n): known at the start of the step, so the
+// single per-step build takes the r* sets before the stage-1 passes (same expression as
+// forces_finish, bit-identical r*)
+template <class T, int D>
+__global__ void k_rstar(Params<T> P, T dt, int n, const V4<T>* __restrict__ pos, const V4<T>* __restrict__ vt,
+                        V4<T>* __restrict__ rstar)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const V4<T> xi = ld4(pos + i), uti = ld4(vt + i);
+    T rx = xi.x + dt * uti.x, ry = xi.y + dt * uti.y, rz = D == 3 ? xi.z + dt * uti.z : xi.z;
+    if (P.per[0]) { if (rx >= P.hi[0]) rx -= P.L[0]; else if (rx < P.lo[0]) rx += P.L[0]; }
+    if (P.per[1]) { if (ry >= P.hi[1]) ry -= P.L[1]; else if (ry < P.lo[1]) ry += P.L[1]; }
+    if (D == 3 && P.per[2]) { if (rz >= P.hi[2]) rz -= P.L[2]; else if (rz < P.lo[2]) rz += P.L[2]; }
+    rstar[i] = mk4<T>(rx, ry, rz, xi.w);
+}
+
 // ===========================================================================
 // A9 (single-build form, R3): the exact neighbour sets at r* filtered out of
 // the loose list built at r^n.  Every pair with |r*_ij| < 3h has
 // |r^n_ij| < 3h + dt|u~_i| + dt|u~_j| <= Rs, so it is in the loose list; the
 // decision itself is R2's (fp32 prefilter + fp64 band, as the exact build).
-// The filtered rows keep the loose list's order (deterministic).  Also
-// writes the GTVF inner list of fluid rows.  The warp walks to its longest
-// row so that the fp64 band decision can be taken warp-wide.
+// r* = r^n + dt u~^n is known at the start of the step (eq:int:rnp1, k_rstar),
+// so the filter runs right after the build.  The filtered rows keep the loose
+// list's order (deterministic; band cases last); also writes the GTVF inner
+// list of fluid rows.  The warp walks to its longest row so that the fp64
+// band decision can be taken warp-wide.
 // ===========================================================================
-//
-// RHS = true (fluid rows): A11 fused in (the contributions to RHS_i, D_ii
-// and the stored factor of fac_ij computed for every kept pair, as
-// k_rhs_diag).  Measured on C5 it is SLOWER than filter + k_rhs_diag (96
-// registers: occupancy halves), so the engine runs RHS = false; kept for
-// the record.
 #ifdef SISPH_FILTER_MINB
 #define FILTER_BOUNDS __launch_bounds__(128, SISPH_FILTER_MINB)
 #else
 #define FILTER_BOUNDS __launch_bounds__(128)
 #endif
-template <class T, int D, bool RHS>
-__global__ void FILTER_BOUNDS k_filter(Params<T> P, int row0, int nrows, const V4<T>* __restrict__ pos,
-                                                const int* __restrict__ nbs, const int* __restrict__ cnts, int cap_s,
-                                                int* __restrict__ nbr, int* __restrict__ cnt,
-                                                int* __restrict__ nbr_in, int* __restrict__ cnt_in,
-                                                const V4<T>* __restrict__ us, const uint8_t* __restrict__ fs, T inv_dt,
-                                                T* __restrict__ rhs, T* __restrict__ diag, T* __restrict__ coef,
-                                                Ctl* ctl)
+#ifndef SISPH_FILTER_PF
+#define SISPH_FILTER_PF 1   // B200, C5: PD 1 / 2 / 3 -> 1214 / 1204 / 1201 us
+#endif
+template <class T, int D>
+__global__ void FILTER_BOUNDS k_filter(Params<T> P, int nrows, const V4<T>* __restrict__ pos,
+                                       const int* __restrict__ nbs, const int* __restrict__ cnts, int cap_s,
+                                       int* __restrict__ nbr, int* __restrict__ cnt, int* __restrict__ nbr_in,
+                                       int* __restrict__ cnt_in, Ctl* ctl)
 {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     const int Nf = P.Nf, cap = P.cap, cap_in = P.cap_in;
-    // rows row0 + t; row0 < 0: every owned row (fluid [0, Nfo), then walls [Nf, Nf + Nwo))
+    // every owned row: fluid [0, Nfo), then walls [Nf, Nf + Nwo)
     const bool act = t < nrows;
-    const int i = row0 >= 0 ? row0 + (act ? t : 0) : (!act ? 0 : (t < P.Nfo ? t : Nf + (t - P.Nfo)));
+    const int i = !act ? 0 : (t < P.Nfo ? t : Nf + (t - P.Nfo));
     const bool inner = act && nbr_in && i < Nf;
     const V4<T> xi = ld4(pos + i);
     const int n = act ? cnts[i] : 0;
@@ -967,32 +977,19 @@ __global__ void FILTER_BOUNDS k_filter(Params<T> P, int row0, int nrows, const V
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
     const float Rin2 = inner ? P.Rin2f : -1.f;
+    // fp32 band cases (|r^2 - R^2| within the prefilter's rounding bound, R37: lattice
+    // near-ties) are queued per lane and decided in fp64 after the row, so the warp runs the
+    // fp64 path max-over-lanes times instead of once per entry any lane has in the band; they
+    // are appended after the row's other entries (the set is the same).  Band pairs lie at
+    // ~3h, beyond every inner-list radius (3 h~ + 0.1 h <= 0.85 x 3h).
+    constexpr int FQ = 48;
+    __shared__ int bq[FQ][128];
+    int nq = 0;
     const int pmask = P.per[0] | (P.per[1] << 1) | (P.per[2] << 2);
-    #ifndef SISPH_FILTER_VST
-#define SISPH_FILTER_VST 1   // B200, C5: 1213 -> 1196 us
-#endif
-#if SISPH_FILTER_VST == 2
-    NbCursorS A, B;
-#elif SISPH_FILTER_VST
     NbCursorV A, B;
-#else
-    NbCursor A, B;
-#endif
     A.init(nbr, cap, i);
     B.init(nbr_in ? nbr_in : nbr, cap_in, inner ? i : 0);
-    // A11 state
-    V4<T> ui;
-    T rhoi = T(1), sr = T(0), sd = T(0);
-    T* __restrict__ crow = nullptr;
-    if (RHS) {
-        ui = ld4(us + i);
-        rhoi = ui.w;                    // rho_i rides in u*'s 4th lane (k_forces_predict)
-        crow = coef ? coef + nb_base(i, cap) : nullptr;
-    }
     const int4* __restrict__ src = reinterpret_cast<const int4*>(nbs + nb_base(i, cap_s));
-#ifndef SISPH_FILTER_PF
-#define SISPH_FILTER_PF 1   // B200, C5: PD 1 / 2 / 3 -> 1214 / 1204 / 1201 us
-#endif
     // the index chunks of the next SISPH_FILTER_PF chunks stay in flight while one is tested
     int4 vr[SISPH_FILTER_PF];
 #pragma unroll
@@ -1026,51 +1023,35 @@ __global__ void FILTER_BOUNDS k_filter(Params<T> P, int row0, int nrows, const V
                 if (D == 3) r2 += d2 * d2;
                 in = r2 < P.R2lo;
                 const bool band = valid && !in && r2 <= P.R2hi;
-                if (__any_sync(0xffffffffu, band)) {
+                const bool queued = band && nq < FQ;
+                if (queued) bq[nq++][threadIdx.x] = j;
+                const bool now = band && !queued;   // queue full: decide here
+                if (__any_sync(0xffffffffu, now)) {
                     const bool ex = exact_band((double)xi.x, (double)xi.y, (double)xi.z, (double)xj.x, (double)xj.y,
                                                (double)xj.z, P.Ld[0], P.Ld[1], P.Ld[2], pmask, D == 3, P.R2d);
-                    in = band ? ex : in;
+                    in = now ? ex : in;
                 }
             } else {
                 in = nb_test<D>(P, xi, xj, r2);
             }
             in = in && valid;
-            if (RHS) {
-                // eq:sph-ppe right side (R8) and eq:coeff (R6/R7), as k_rhs_diag
-                const V4<T> uj = in ? ld4(us + j) : ui;
-                const T rhoj = in ? uj.w : T(1);
-                T d[3], r, ri;
-                const T rr2 = pair_vec<T, D>(P, xi, xj, d);
-                r_of(rr2, r, ri);
-                const T p4 = quintic4(r * P.inv_h);
-                const T mj = xj.w;
-                T ud = (ui.x - uj.x) * d[0] + (ui.y - uj.y) * d[1];
-                if (D == 3) ud += (ui.z - uj.z) * d[2];
-                const T fr = mj * frcp(rhoj) * (ud * p4 * ri);
-                const T f = mj * (r * p4) * frcp((rhoi + rhoj) * (rr2 + P.eta_h2));
-                sr += in ? fr : T(0);
-                sd += in ? f : T(0);
-                if (crow && in && A.k < cap) crow[nb_off(A.k)] = f;
-            }
             A.push(in, j, cap);
             B.push(in && r2 < Rin2, j, cap_in);
         }
     }
-    double lam = 0.0;
-#if SISPH_FILTER_VST
+    // the queued band cases, in fp64 (R2)
+    for (int q = 0; q < nq; q++) {
+        const int j = bq[q][threadIdx.x];
+        const V4<T> xj = ld4(pos + j);
+        const bool ex = exact_band((double)xi.x, (double)xi.y, (double)xi.z, (double)xj.x, (double)xj.y, (double)xj.z,
+                                   P.Ld[0], P.Ld[1], P.Ld[2], pmask, D == 3, P.R2d);
+        A.push(ex, j, cap);
+    }
     A.flush(cap);
     B.flush(cap_in);
-#endif
     if (act) {
         cnt[i] = min(A.k, cap);
         if (inner) cnt_in[i] = min(B.k, cap_in);
-        if (RHS) {
-            sr *= -P.dwk * inv_dt;
-            sd *= T(4) * P.dwk * frcp(rhoi);
-            rhs[i] = sr;
-            diag[i] = sd;
-            if (!fs[i] && sd != T(0)) lam = (double)fabs(sr / sd);
-        }
     }
     int mmax = act ? max(A.k, inner && B.k > cap_in ? cap + 1 : 0) : 0;
     unsigned sfl = act && i < Nf ? (unsigned)min(A.k, cap) : 0u, sin_ = inner ? (unsigned)B.k : 0u;
@@ -1080,13 +1061,11 @@ __global__ void FILTER_BOUNDS k_filter(Params<T> P, int row0, int nrows, const V
         sfl += __shfl_xor_sync(0xffffffffu, sfl, o);
         sin_ += __shfl_xor_sync(0xffffffffu, sin_, o);
     }
-    if (RHS) lam = warp_max(lam);
     if ((threadIdx.x & 31) == 0) {
         atomicMax(&ctl->max_count, mmax);
         if (mmax > cap) atomicExch(&ctl->overflow, 1);
         if (sfl) atomicAdd(&ctl->pairs_fluid, (unsigned long long)sfl);
         if (sin_) atomicAdd(&ctl->pairs_inner, (unsigned long long)sin_);
-        if (RHS && lam > 0.0) atomicMax(&ctl->lambda_bits, (unsigned long long)__double_as_longlong(lam));
     }
 }
 
@@ -1263,6 +1242,7 @@ __device__ __forceinline__ void forces_finish(const Params<T>& P, int i, T dt, c
 {
     us[i] = mk4<T>(ui.x + dt * ax, ui.y + dt * ay, D == 3 ? ui.z + dt * az : T(0), rhoi);   // rho_i in lane 4
     fnp[i] = mk4<T>(ax, ay, D == 3 ? az : T(0), T(0));   // f_visc + f_avisc + f_astress + f_body (adaptive dt)
+    if (!rstar) return;                                  // single build: k_rstar computed r* (same expression)
     T rx = xi.x + dt * uti.x, ry = xi.y + dt * uti.y, rz = D == 3 ? xi.z + dt * uti.z : xi.z;
     if (P.per[0]) { if (rx >= P.hi[0]) rx -= P.L[0]; else if (rx < P.lo[0]) rx += P.L[0]; }
     if (P.per[1]) { if (ry >= P.hi[1]) ry -= P.L[1]; else if (ry < P.lo[1]) ry += P.L[1]; }
@@ -1477,16 +1457,21 @@ template <class T> struct PpeDesc {
     int min_it, max_it;
 };
 
+// WL lanes share a wall row (lane `sub` takes its chunks sub, sub + WL, ...; the sums
+// meet by shuffles): walls are few (configs[1]: 3.1k) and each row is long, so one
+// lane per row left the pass bound by a ~45-deep chain of dependent loads
+constexpr int WL = 8;
 template <class T, int D>
 __device__ __forceinline__ void wall_pressure_row(const Params<T>& P, int w, const V4<T>* __restrict__ pos,
                                                   const T* __restrict__ rho, const int* __restrict__ nbr,
-                                                  const int* __restrict__ cnt, int ncap, T* p)
+                                                  const int* __restrict__ cnt, int ncap, T* p, int sub)
 {
     int i = P.Nf + w;
     V4<T> xi = ld4(pos + i);
     T sw = 0, sp = 0, sx = 0, sy = 0, sz = 0;
     int n = cnt[i];
-    for_nbrs_pfx<SISPH_WALLP_PF>(nbr, ncap, i, n, [&](int j) {
+    const int4* __restrict__ q = reinterpret_cast<const int4*>(nbr + nb_base(i, ncap));
+    auto one = [&](int j) {
         if (j >= P.Nf) return;
         V4<T> xj = ld4(pos + j);
         T d[3], r, ri;
@@ -1498,7 +1483,24 @@ __device__ __forceinline__ void wall_pressure_row(const Params<T>& P, int w, con
         sy += rw * d[1];
         if (D == 3) sz += rw * d[2];
         sw += wv;
-    });
+    };
+    for (int c = 4 * sub; c < n; c += 4 * WL) {
+        const int4 v = __ldcs(q + (size_t)(c >> 2) * 32);
+        one(v.x);
+        if (c + 1 < n) one(v.y);
+        if (c + 2 < n) one(v.z);
+        if (c + 3 < n) one(v.w);
+    }
+    const unsigned gm = ((1u << WL) - 1u) << ((threadIdx.x & 31) & ~(WL - 1));
+#pragma unroll
+    for (int o = WL / 2; o > 0; o >>= 1) {
+        sw += __shfl_xor_sync(gm, sw, o, WL);
+        sp += __shfl_xor_sync(gm, sp, o, WL);
+        sx += __shfl_xor_sync(gm, sx, o, WL);
+        sy += __shfl_xor_sync(gm, sy, o, WL);
+        if (D == 3) sz += __shfl_xor_sync(gm, sz, o, WL);
+    }
+    if (sub) return;
     T pw = 0;
     if (sw > T(0)) {
         T gr = P.g[0] * sx + P.g[1] * sy;
@@ -1515,9 +1517,9 @@ __global__ void __launch_bounds__(256) k_wall_pressure(Params<T> P, const V4<T>*
                                                        const T* __restrict__ rho, const int* __restrict__ nbr,
                                                        const int* __restrict__ cnt, int ncap, T* p)
 {
-    int w = blockIdx.x * blockDim.x + threadIdx.x;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x, w = t / WL;
     if (w >= P.Nwo) return;
-    wall_pressure_row<T, D>(P, w, pos, rho, nbr, cnt, ncap, p);
+    wall_pressure_row<T, D>(P, w, pos, rho, nbr, cnt, ncap, p, t % WL);
 }
 
 // in a solve: from p^k, the buffer selected by the device iteration counter
@@ -1526,10 +1528,10 @@ __global__ void __launch_bounds__(256) k_ppe_wall(Params<T> P, const PpeDesc<T>*
                                                   const int* __restrict__ cnt, int ncap, const Ctl* ctl)
 {
     if (ctl->done) return;
-    int w = blockIdx.x * blockDim.x + threadIdx.x;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x, w = t / WL;
     if (w >= P.Nwo) return;
     T* p = (ctl->iter & 1) ? dsc->pB : dsc->pA;
-    wall_pressure_row<T, D>(P, w, dsc->pos, dsc->rho, dsc->nbr, cnt, ncap, p);
+    wall_pressure_row<T, D>(P, w, dsc->pos, dsc->rho, dsc->nbr, cnt, ncap, p, t % WL);
 }
 
 // ===========================================================================
@@ -1932,7 +1934,7 @@ __global__ void __launch_bounds__(SWEEP_T) k_ppe_persistent(Params<T> P, const P
         const int kit = vc->iter;
         T* pin = (kit & 1) ? pB : pA;
         T* pout = (kit & 1) ? pA : pB;
-        for (int q = gt; q < P.Nwo; q += gs) wall_pressure_row<T, D>(P, q, pos, rho, nbr, cnt, ncap, pin);
+        for (int q = gt / WL; q < P.Nwo; q += gs / WL) wall_pressure_row<T, D>(P, q, pos, rho, nbr, cnt, ncap, pin, gt % WL);
         grid.sync();
         double dn = 0.0, dd = 0.0;
         bool bad = false;
