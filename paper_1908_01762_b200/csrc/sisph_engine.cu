@@ -1638,10 +1638,11 @@ template <class T, int D> struct Engine : EngineBase {
         } else {
             SCK(cudaMemsetAsync(ctl, 0, 4 * sizeof(int), st));  // ticket, iter, done, nonfinite
         }
-        // the loop form: one handle with timing off may run the whole loop on the device
-        // (0 = host batches: on B200 the three forms measured within 10 % of each other on
-        // configs[0-1], where every form is bound by the ~10-25 us latency chain of one sweep)
-        int mode = ppe_loop == 0 ? 1 : ppe_loop;
+        // the loop form: one handle with timing off may run the whole loop on the device.
+        // Auto (0): the CUDA-graph WHILE node for small problems, whose solves run tens of
+        // latency-bound sweeps (configs[1]: 2.63 vs 2.88 ms per step with host-polled batches,
+        // no host round trip per batch); host batches for large ones (a few HBM-bound sweeps)
+        int mode = ppe_loop == 0 ? (Nfo <= 400000 ? 2 : 1) : ppe_loop;
         if (dist() || timing || Nf == 0 || launched >= mx) mode = 1;
         if (mode == 3 && P.mean_free) mode = 2;   // the persistent loop has no mean-free phase
         if (mode == 3) {

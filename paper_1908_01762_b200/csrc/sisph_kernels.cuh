@@ -254,6 +254,11 @@ __global__ void k_gather(GatherList G, const int* __restrict__ perm, int n)
 // 16-byte chunk is written by one lane and every 512-byte block by one warp
 // (the L2 merges them before write-back: no partial-sector traffic).
 // ===========================================================================
+#ifdef SISPH_LIST_LDG
+#define LDLIST __ldg      // A/B: the default read-only path (lists stay L2-resident on small problems)
+#else
+#define LDLIST __ldcs
+#endif
 // List (and stored-coefficient) loads use the streaming cache policy
 // (__ldcs: evict-first in L1 and L2): each list is read once per pass and is
 // far larger than L2, so it must not evict the gathered per-particle arrays.
@@ -270,7 +275,7 @@ __device__ __forceinline__ void for_nbrs(const int* __restrict__ nbr, int cap, i
 {
     const int4* __restrict__ q = reinterpret_cast<const int4*>(nbr + nb_base(i, cap));
     for (int c = 0; c < n; c += 4) {
-        const int4 v = __ldcs(q + (size_t)(c >> 2) * 32);
+        const int4 v = LDLIST(q + (size_t)(c >> 2) * 32);
         f(v.x);
         if (c + 1 < n) f(v.y);
         if (c + 2 < n) f(v.z);
@@ -285,10 +290,10 @@ __device__ __forceinline__ void for_nbrs_pf(const int* __restrict__ nbr, int cap
     const int4* __restrict__ q = reinterpret_cast<const int4*>(nbr + nb_base(i, cap));
     int4 r[PD];
 #pragma unroll
-    for (int k = 0; k < PD; k++) r[k] = 4 * k < n ? __ldcs(q + (size_t)k * 32) : make_int4(0, 0, 0, 0);
+    for (int k = 0; k < PD; k++) r[k] = 4 * k < n ? LDLIST(q + (size_t)k * 32) : make_int4(0, 0, 0, 0);
     for (int c = 0; c < n; c += 4) {
         const int cn = c + 4 * PD;
-        const int4 nx = cn < n ? __ldcs(q + (size_t)(cn >> 2) * 32) : make_int4(0, 0, 0, 0);
+        const int4 nx = cn < n ? LDLIST(q + (size_t)(cn >> 2) * 32) : make_int4(0, 0, 0, 0);
         const int4 v = r[0];
         f(v.x);
         if (c + 1 < n) f(v.y);
@@ -310,10 +315,10 @@ __device__ __forceinline__ void for_nbrs_k_pf(const int* __restrict__ nbr, int c
         const int4* __restrict__ q = reinterpret_cast<const int4*>(nbr + nb_base(i, cap));
         int4 r[PD];
 #pragma unroll
-        for (int k = 0; k < PD; k++) r[k] = 4 * k < n ? __ldcs(q + (size_t)k * 32) : make_int4(0, 0, 0, 0);
+        for (int k = 0; k < PD; k++) r[k] = 4 * k < n ? LDLIST(q + (size_t)k * 32) : make_int4(0, 0, 0, 0);
         for (int c = 0; c < n; c += 4) {
             const int cn = c + 4 * PD;
-            const int4 nx = cn < n ? __ldcs(q + (size_t)(cn >> 2) * 32) : make_int4(0, 0, 0, 0);
+            const int4 nx = cn < n ? LDLIST(q + (size_t)(cn >> 2) * 32) : make_int4(0, 0, 0, 0);
             const int4 v = r[0];
             f(v.x, c);
             if (c + 1 < n) f(v.y, c + 1);
@@ -358,7 +363,7 @@ __device__ __forceinline__ void for_nbrs_k(const int* __restrict__ nbr, int cap,
 {
     const int4* __restrict__ q = reinterpret_cast<const int4*>(nbr + nb_base(i, cap));
     for (int c = 0; c < n; c += 4) {
-        const int4 v = __ldcs(q + (size_t)(c >> 2) * 32);
+        const int4 v = LDLIST(q + (size_t)(c >> 2) * 32);
         f(v.x, c);
         if (c + 1 < n) f(v.y, c + 1);
         if (c + 2 < n) f(v.z, c + 2);
@@ -379,7 +384,7 @@ __device__ __forceinline__ void st_chunk4(double* p, const double (&f)[4])
 // one 4-entry chunk of a per-pair array in the same layout (16 / 32 bytes)
 __device__ __forceinline__ void ld_chunk4(const float* p, float (&f)[4])
 {
-    const float4 v = __ldcs(reinterpret_cast<const float4*>(p));
+    const float4 v = LDLIST(reinterpret_cast<const float4*>(p));
     f[0] = v.x;
     f[1] = v.y;
     f[2] = v.z;
@@ -387,7 +392,7 @@ __device__ __forceinline__ void ld_chunk4(const float* p, float (&f)[4])
 }
 __device__ __forceinline__ void ld_chunk4(const double* p, double (&f)[4])
 {
-    const double2 a = __ldcs(reinterpret_cast<const double2*>(p)), b = __ldcs(reinterpret_cast<const double2*>(p) + 1);
+    const double2 a = LDLIST(reinterpret_cast<const double2*>(p)), b = LDLIST(reinterpret_cast<const double2*>(p) + 1);
     f[0] = a.x;
     f[1] = a.y;
     f[2] = b.x;
@@ -993,12 +998,12 @@ __global__ void FILTER_BOUNDS k_filter(Params<T> P, int nrows, const V4<T>* __re
     // the index chunks of the next SISPH_FILTER_PF chunks stay in flight while one is tested
     int4 vr[SISPH_FILTER_PF];
 #pragma unroll
-    for (int q = 0; q < SISPH_FILTER_PF; q++) vr[q] = 4 * q < n ? __ldcs(src + (size_t)q * 32) : make_int4(i, i, i, i);
+    for (int q = 0; q < SISPH_FILTER_PF; q++) vr[q] = 4 * q < n ? LDLIST(src + (size_t)q * 32) : make_int4(i, i, i, i);
     for (int c = 0; c < nmax; c += 4) {
         const int4 v = vr[0];
         {
             const int cn = c + 4 * SISPH_FILTER_PF;
-            const int4 nx = cn < n ? __ldcs(src + (size_t)(cn >> 2) * 32) : make_int4(i, i, i, i);
+            const int4 nx = cn < n ? LDLIST(src + (size_t)(cn >> 2) * 32) : make_int4(i, i, i, i);
 #pragma unroll
             for (int q = 0; q < SISPH_FILTER_PF - 1; q++) vr[q] = vr[q + 1];
             vr[SISPH_FILTER_PF - 1] = nx;
@@ -1485,7 +1490,7 @@ __device__ __forceinline__ void wall_pressure_row(const Params<T>& P, int w, con
         sw += wv;
     };
     for (int c = 4 * sub; c < n; c += 4 * WL) {
-        const int4 v = __ldcs(q + (size_t)(c >> 2) * 32);
+        const int4 v = LDLIST(q + (size_t)(c >> 2) * 32);
         one(v.x);
         if (c + 1 < n) one(v.y);
         if (c + 2 < n) one(v.z);
@@ -1588,13 +1593,13 @@ __device__ __forceinline__ T sweep_row(const Params<T>& P, int i, const V4<T>* _
 #pragma unroll
             for (int q = 0; q < PD; q++) {
                 const int c = 4 * q;
-                vr[q] = c < n ? __ldcs(qi + (size_t)(c >> 2) * 32) : make_int4(i, i, i, i);
+                vr[q] = c < n ? LDLIST(qi + (size_t)(c >> 2) * 32) : make_int4(i, i, i, i);
                 if (c < n) ld_chunk4(coef + b + ((size_t)(c >> 2) * 32 << 2), fr[q]);
                 else fr[q][0] = fr[q][1] = fr[q][2] = fr[q][3] = T(0);
             }
             for (int c = 0; c < n; c += 4) {
                 const int cn = c + 4 * PD;
-                const int4 vnew = cn < n ? __ldcs(qi + (size_t)(cn >> 2) * 32) : make_int4(i, i, i, i);
+                const int4 vnew = cn < n ? LDLIST(qi + (size_t)(cn >> 2) * 32) : make_int4(i, i, i, i);
                 T fnew[4] = {T(0), T(0), T(0), T(0)};
                 if (cn < n) ld_chunk4(coef + b + ((size_t)(cn >> 2) * 32 << 2), fnew);
                 s += fr[0][0] * __ldg(pin + vr[0].x);
@@ -1614,7 +1619,7 @@ __device__ __forceinline__ T sweep_row(const Params<T>& P, int i, const V4<T>* _
 #else
             for (int c = 0; c < n; c += 4) {
                 const size_t o = (size_t)(c >> 2) * 32;
-                const int4 v = __ldcs(qi + o);
+                const int4 v = LDLIST(qi + o);
                 T f[4];
                 ld_chunk4(coef + b + (o << 2), f);
                 s += f[0] * pin[v.x];
