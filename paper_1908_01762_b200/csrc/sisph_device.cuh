@@ -109,6 +109,11 @@ template <class T> struct Params {
     // (3h)^2 (1 + 2^-10): a pair at or beyond it contributes exactly 0 to every
     // kernel sum (W, dW/dr vanish for q >= 3): passes over the loose list skip it
     T R2cut;
+    // fixed-point coordinates of the fp32 GTVF sub-steps: x_fix = (x - lo) / fxs (mod 2^32),
+    // fxs = L / 2^32 per axis (7.5e-10 m on C5's 3.2 m tank: 2e-7 h); a pair difference is an
+    // exact int32 subtraction (the minimum image on a periodic axis for free)
+    double fxs[3];
+    float fxf[3];
 };
 
 // ---------------------------------------------------------------------------

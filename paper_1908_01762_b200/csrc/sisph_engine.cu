@@ -134,6 +134,7 @@ template <class T, int D> struct Engine : EngineBase {
     bool pref_done = false;
     // GTVF sub-step records (A14): per particle {r*, m / rho^2, r^k - r^0, 0} (two V4), ping-pong
     V *gtA = nullptr, *gtB = nullptr, *vk = nullptr;
+    V *fx0 = nullptr, *dk = nullptr;   // fp32 GTVF: fixed-point r* (int4) and delta^k per slot
     V *recF = nullptr, *recS = nullptr;   // joint {r, m, u, rho} records of A8 / A11 (k_pack_rec)
     V* fnp = nullptr;       // non-pressure acceleration of A8 (adaptive dt)
     int* dcnt_w = nullptr;  // device flag of set_field's wall check
@@ -203,7 +204,7 @@ template <class T, int D> struct Engine : EngineBase {
 
     ~Engine() override
     {
-        void* ptrs[] = {pos, pos_alt, vel, vel_alt, us, us_alt, vt, vt_alt, rn, rstar, nrm, nstmp, uwl, gtA, gtB, vk, recF, recS,
+        void* ptrs[] = {pos, pos_alt, vel, vel_alt, us, us_alt, vt, vt_alt, rn, rstar, nrm, nstmp, uwl, gtA, gtB, vk, fx0, dk, recF, recS,
                         p, p_alt, rho, rho_alt, rhs, diag, fs, fs_alt, pid, pid_alt, keys, rank, perm0, perm,
                         ccount, fstart, wstart, bsum, nbr, cnt, ctl, partials, dtmp, nbr_in, cnt_in,
                         nbs, cnt_s, wperm_s, wstart_s, coef, dflag, dflag2, dpre, dlist[0], dlist[1], dlist[2],
@@ -306,6 +307,10 @@ template <class T, int D> struct Engine : EngineBase {
             P.halfLf[a] = (float)(0.5 * L);
             P.L[a] = (T)L;
             P.halfL[a] = (T)(0.5 * L);
+        }
+        for (int a = 0; a < 3; a++) {
+            P.fxs[a] = a < D ? P.Ld[a] / 4294967296.0 : 1.0;
+            P.fxf[a] = (float)P.fxs[a];
         }
         long long nc_tot = (long long)P.nc[0] * P.nc[1] * P.nc[2];
         if (nc_tot > (1ll << 29)) {
@@ -427,7 +432,7 @@ template <class T, int D> struct Engine : EngineBase {
     if (rc) return rc;
         AL(pos, V, NT) AL(pos_alt, V, NT) AL(vel, V, NT) AL(vel_alt, V, NT) AL(us, V, NT) AL(us_alt, V, NT)
         AL(vt, V, NF) AL(vt_alt, V, NF) AL(rn, V, NT) AL(rstar, V, NT) AL(nrm, V, NW) AL(nstmp, V, NW) AL(uwl, V, NW)
-        AL(gtA, V, 2 * NT) AL(gtB, V, 2 * NT) AL(recF, V, 2 * NT) AL(recS, V, 2 * NT) AL(vk, V, NF) AL(fnp, V, NF) AL(dcnt_w, int, 4)
+        AL(gtA, V, 2 * NT) AL(gtB, V, 2 * NT) AL(fx0, V, NT) AL(dk, V, NT) AL(recF, V, 2 * NT) AL(recS, V, 2 * NT) AL(vk, V, NF) AL(fnp, V, NF) AL(dcnt_w, int, 4)
         AL(p, T, NT) AL(p_alt, T, NT) AL(rho, T, NT) AL(rho_alt, T, NT) AL(rhs, T, NF) AL(diag, T, NF)
         AL(fs, uint8_t, NF) AL(fs_alt, uint8_t, NF) AL(pid, int, NT) AL(pid_alt, int, NT)
         AL(keys, int, NT) AL(rank, int, NT) AL(perm0, int, NT) AL(perm, int, NT)
@@ -1703,36 +1708,72 @@ template <class T, int D> struct Engine : EngineBase {
         return SISPH_OK;
     }
 
-    // K modified-GTVF sub-steps (A14) from r* = pos; returns the final records (delta^K = r^K - r^0
-    // in the second V4 of each particle's record)
-    int gtvf_substeps(T dtau, bool inner, const T*& rK)
+    // K modified-GTVF sub-steps (A14) from r* = pos; returns delta^K = r^K - r^0 in rK (stride
+    // rstride working-precision values per slot, delta in the last four)
+    int gtvf_substeps(T dtau, bool inner, const T*& rK, int& rstride)
     {
-        T* a = reinterpret_cast<T*>(gtA);
-        T* b = reinterpret_cast<T*>(gtB);
-        if (Ntot) ++nlaunch, k_gtvf_prep<T><<<nblk(Ntot, 256), 256, 0, st>>>(pos, rho, Ntot, a, b);
         if (inner) SCK(cudaMemsetAsync(&ctl->gtvf_far, 0, sizeof(int), st));
-        const T* src = b;
-        for (int k = 0; k < K; k++) {
-            T* dst = (k & 1) ? b : a;
-            if (Nfo) {
-                if (inner)
-                    ++nlaunch, k_gtvf_substep<T, D><<<nblk(Nfo, 128), 128, 0, st>>>(P, dtau, src, dst, vk, p, nbr_in,
-                                                                                    P.cap_in, cnt_in, k == 0, 1, ctl);
-                else
-                    ++nlaunch, k_gtvf_substep<T, D><<<nblk(Nfo, 128), 128, 0, st>>>(P, dtau, src, dst, vk, p, nbr,
-                                                                                    P.cap, cnt, k == 0, 0, ctl);
+        if constexpr (std::is_same<T, float>::value) {
+            // fp32: 16-byte fixed-point records (k_gtvf_substep_fx)
+            int4* a = reinterpret_cast<int4*>(gtA);
+            int4* b = reinterpret_cast<int4*>(gtB);
+            int4* f0 = reinterpret_cast<int4*>(fx0);
+            float4* dl = reinterpret_cast<float4*>(dk);
+            float4* vv = reinterpret_cast<float4*>(vk);
+            if (Ntot) ++nlaunch, k_gtvf_prep_fx<D><<<nblk(Ntot, 256), 256, 0, st>>>(P, pos, rho, Ntot, a, b, f0, dl);
+            const int4* src = b;
+            for (int k = 0; k < K; k++) {
+                int4* dst = (k & 1) ? b : a;
+                if (Nfo) {
+                    if (inner)
+                        ++nlaunch, k_gtvf_substep_fx<D><<<nblk(Nfo, 128), 128, 0, st>>>(
+                                       P, dtau, src, dst, f0, dl, vv, p, nbr_in, P.cap_in, cnt_in, k == 0, 1, ctl);
+                    else
+                        ++nlaunch, k_gtvf_substep_fx<D><<<nblk(Nfo, 128), 128, 0, st>>>(
+                                       P, dtau, src, dst, f0, dl, vv, p, nbr, P.cap, cnt, k == 0, 0, ctl);
+                }
+                SCK(cudaGetLastError());
+                if (dist()) {
+                    // the ghosts' delta^k from their owners (no image shift), then their records
+                    PackList L{};
+                    pl_add(L, dk, sizeof(V));
+                    SRET(halo_fluid(L));
+                    const int ng = Nf - Nfo;
+                    if (ng) ++nlaunch, k_gtvf_ghost_fx<<<nblk(ng, 256), 256, 0, st>>>(Nfo, ng, f0, dl, src, dst, P.fxf[0],
+                                                                                       P.fxf[1], P.fxf[2], D == 3);
+                    SCK(cudaGetLastError());
+                }
+                src = dst;
             }
-            SCK(cudaGetLastError());
-            if (dist()) {
-                // the record's r* carries the periodic image shift of the ghost, delta does not
-                PackList L{};
-                pl_add(L, dst, 2 * sizeof(V), 1);
-                SRET(halo_fluid(L));
+            rK = reinterpret_cast<const T*>(dk);
+            rstride = 4;
+        } else {
+            T* a = reinterpret_cast<T*>(gtA);
+            T* b = reinterpret_cast<T*>(gtB);
+            if (Ntot) ++nlaunch, k_gtvf_prep<T><<<nblk(Ntot, 256), 256, 0, st>>>(pos, rho, Ntot, a, b);
+            const T* src = b;
+            for (int k = 0; k < K; k++) {
+                T* dst = (k & 1) ? b : a;
+                if (Nfo) {
+                    if (inner)
+                        ++nlaunch, k_gtvf_substep<T, D><<<nblk(Nfo, 128), 128, 0, st>>>(P, dtau, src, dst, vk, p, nbr_in,
+                                                                                        P.cap_in, cnt_in, k == 0, 1, ctl);
+                    else
+                        ++nlaunch, k_gtvf_substep<T, D><<<nblk(Nfo, 128), 128, 0, st>>>(P, dtau, src, dst, vk, p, nbr,
+                                                                                        P.cap, cnt, k == 0, 0, ctl);
+                }
+                SCK(cudaGetLastError());
+                if (dist()) {
+                    // the record's r* carries the periodic image shift of the ghost, delta does not
+                    PackList L{};
+                    pl_add(L, dst, 2 * sizeof(V), 1);
+                    SRET(halo_fluid(L));
+                }
+                src = dst;
             }
-            src = dst;
+            rK = src;   // delta^K in the second V4 of each record
+            rstride = 8;
         }
-        SCK(cudaGetLastError());
-        rK = src;
         return SISPH_OK;
     }
 
@@ -1771,9 +1812,10 @@ template <class T, int D> struct Engine : EngineBase {
         }
         if (Nfo) ++nlaunch, k_pgrad_correct<T, D><<<nblk(Nfo, 128), 128, 0, st>>>(P, (T)dt, pos, rho, p, us, nbr, cnt, P.cap, vel, fnp, ctl);
         // A14: K sub-steps (p0 = 0 everywhere when p_ref == 0: the shift is exactly zero)
-        const T* rK = nullptr;   // GTVF records with delta^K = r^K - r^0 (none when p0 = 0)
+        const T* rK = nullptr;   // delta^K = r^K - r^0 of the GTVF sub-steps (none when p0 = 0)
+        int rstride = 4;
         if (P.p_ref != T(0) && K > 0 && (Nf || dist())) {
-            SRET(gtvf_substeps((T)(dt / K), inner_valid, rK));
+            SRET(gtvf_substeps((T)(dt / K), inner_valid, rK, rstride));
             if (inner_valid) {
                 // the inner list is exact only while no particle moved more than skin/2
                 // (slab ranks: if any rank's did, all repeat)
@@ -1790,14 +1832,14 @@ template <class T, int D> struct Engine : EngineBase {
                 }
                 if (hctl->gtvf_far) {
                     gtvf_fallbacks++;
-                    SRET(gtvf_substeps((T)(dt / K), false, rK));
+                    SRET(gtvf_substeps((T)(dt / K), false, rK, rstride));
                 }
             }
         }
         // A15 (R34: the outlet's advection velocity first, from the fluid's u^{n+1} at r*)
         if (open_x && Nfo)
             ++nlaunch, k_outlet_velocity<T, D><<<nblk(Nfo, 256), 256, 0, st>>>(P, pos, vel, nbr, cnt, P.cap, uout);
-        if (Nfo) ++nlaunch, k_advance<T, D><<<nblk(Nfo, 256), 256, 0, st>>>(P, (T)dt, rK, rn, vel, pos, vt, ctl, uout);
+        if (Nfo) ++nlaunch, k_advance<T, D><<<nblk(Nfo, 256), 256, 0, st>>>(P, (T)dt, rK, rstride, rn, vel, pos, vt, ctl, uout);
         SCK(cudaGetLastError());
         if (open_x) SRET(open_boundaries());
         phase = IDLE;

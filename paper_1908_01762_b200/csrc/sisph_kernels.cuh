@@ -2074,6 +2074,101 @@ __global__ void k_gtvf_prep(const V4<T>* __restrict__ pos, const T* __restrict__
     if (b) st8(b + 8 * (size_t)i, z);
 }
 
+#ifndef SISPH_GTVF_PF
+#define SISPH_GTVF_PF 1   // B200, C5: PD 0 / 1 / 2 / 3 -> 113 / 107 / 125 / 120 us per sub-step
+#endif
+// fp32 GTVF sub-steps on fixed-point positions (round 2): the sub-step record is 16 bytes,
+// {x, y, z as 32-bit fixed point of the local box, m / rho^2}, so a neighbour costs one 128-bit
+// gather; the pair difference is an exact integer subtraction of the fixed-point r^k converted
+// with the axis scale (quantisation 2e-7 h on C5: the GTVF force sums, which cancel to ~1e-3
+// of their terms on near-lattices, keep ~1e-6 relative).  r^k_fix = r*_fix + round(delta^k /
+// fxs); delta^k (fp32, the recursion of eq:int:gtvf:pos) and the velocity live per particle.
+__device__ __forceinline__ unsigned fix_coord(double x, double lo, double s)
+{
+    return (unsigned)(unsigned long long)(long long)llrint((x - lo) / s);
+}
+
+template <int D>
+__global__ void k_gtvf_prep_fx(Params<float> P, const float4* __restrict__ pos, const float* __restrict__ rho, int n,
+                               int4* __restrict__ a, int4* __restrict__ b, int4* __restrict__ fix0,
+                               float4* __restrict__ dk)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float4 x = ld4(pos + i);
+    const float r = rho[i];
+    const int4 f = make_int4((int)fix_coord(x.x, P.lo[0], P.fxs[0]), (int)fix_coord(x.y, P.lo[1], P.fxs[1]),
+                             D == 3 ? (int)fix_coord(x.z, P.lo[2], P.fxs[2]) : 0, __float_as_int(x.w / (r * r)));
+    a[i] = f;
+    b[i] = f;
+    fix0[i] = f;
+    dk[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+template <int D>
+__global__ void __launch_bounds__(128) k_gtvf_substep_fx(Params<float> P, float dtau, const int4* __restrict__ rk,
+                                                         int4* __restrict__ rk1, const int4* __restrict__ fix0,
+                                                         float4* __restrict__ dk, float4* __restrict__ vk,
+                                                         const float* __restrict__ p, const int* __restrict__ nbr,
+                                                         int ncap, const int* __restrict__ cnt, int first, int check,
+                                                         Ctl* ctl)
+{
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.Nfo) return;
+    const int4 ri = __ldg(rk + i);
+    float ax = 0.f, ay = 0.f, az = 0.f;
+    int n = cnt[i];
+    if (P.ptype && P.ptype[i] != 0) n = 0;           // R34: no GTVF shift for inlet / outlet
+    const float s0 = P.fxf[0], s1 = P.fxf[1], s2 = P.fxf[2];
+    for_nbrs_pf<SISPH_GTVF_PF>(nbr, ncap, i, n, [&](int j) {
+        const int4 rj = __ldg(rk + j);
+        const float d0 = (float)(ri.x - rj.x) * s0, d1 = (float)(ri.y - rj.y) * s1;
+        const float d2 = D == 3 ? (float)(ri.z - rj.z) * s2 : 0.f;
+        float r2 = d0 * d0 + d1 * d1;
+        if (D == 3) r2 += d2 * d2;
+        float r, rinv;
+        r_of(r2, r, rinv);
+        const float f = __int_as_float(rj.w) * quintic4(r * P.inv_ht) * rinv;   // m_j / rho_j^2 |gradW| / r
+        ax += f * d0;
+        ay += f * d1;
+        if (D == 3) az += f * d2;
+    });
+    float p0 = P.p_ref;
+    if (P.pref_external) {
+        const float v = 10.f * fabsf(p[i]);
+        p0 = v < P.p_ref ? v : P.p_ref;
+    }
+    const float sc = -p0 * P.dwkt;
+    ax *= sc;
+    ay *= sc;
+    az *= sc;
+    const float4 v = first ? make_float4(0.f, 0.f, 0.f, 0.f) : ld4(vk + i);
+    const float4 dl = ld4(dk + i);
+    const float h2 = 0.5f * dtau * dtau;
+    const float4 dn = make_float4(dl.x + dtau * v.x + h2 * ax, dl.y + dtau * v.y + h2 * ay,
+                                  D == 3 ? dl.z + dtau * v.z + h2 * az : 0.f, 0.f);
+    dk[i] = dn;
+    vk[i] = make_float4(v.x + dtau * ax, v.y + dtau * ay, D == 3 ? v.z + dtau * az : 0.f, 0.f);
+    const int4 f0 = __ldg(fix0 + i);
+    rk1[i] = make_int4(f0.x + __float2int_rn(dn.x / s0), f0.y + __float2int_rn(dn.y / s1),
+                       D == 3 ? f0.z + __float2int_rn(dn.z / s2) : 0, ri.w);
+    if (check && dn.x * dn.x + dn.y * dn.y + dn.z * dn.z > P.skin_half2) atomicExch(&ctl->gtvf_far, 1);
+}
+
+// slab ranks: the ghosts' fixed-point r^k from their owners' delta^k (halo-exchanged)
+__global__ void k_gtvf_ghost_fx(int base, int n, const int4* __restrict__ fix0, const float4* __restrict__ dk,
+                                const int4* __restrict__ rk, int4* __restrict__ rk1, float s0, float s1, float s2,
+                                int three)
+{
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n) return;
+    const int i = base + q;
+    const int4 f0 = fix0[i];
+    const float4 dn = dk[i];
+    rk1[i] = make_int4(f0.x + __float2int_rn(dn.x / s0), f0.y + __float2int_rn(dn.y / s1),
+                       three ? f0.z + __float2int_rn(dn.z / s2) : 0, rk[i].w);
+}
+
 // nbr/stride/cnt select the full r* list or the inner list (pairs with
 // r* < 3 h~ + skin).  With the inner list, a particle that has moved more
 // than skin/2 from r* raises ctl->gtvf_far and the host repeats the
@@ -2099,9 +2194,6 @@ __global__ void __launch_bounds__(128) k_gtvf_substep(Params<T> P, T dtau, const
     T ax = 0, ay = 0, az = 0;
     int n = cnt[i];
     if (P.ptype && P.ptype[i] != 0) n = 0;           // R34: no GTVF shift for inlet / outlet
-#ifndef SISPH_GTVF_PF
-#define SISPH_GTVF_PF 1   // B200, C5: PD 0 / 1 / 2 / 3 -> 113 / 107 / 125 / 120 us per sub-step
-#endif
     for_nbrs_pf<SISPH_GTVF_PF>(nbr, ncap, i, n, [&](int j) {
         T rj8[8];
         ld8(rk + 8 * (size_t)j, rj8);
@@ -2143,7 +2235,7 @@ __global__ void __launch_bounds__(128) k_gtvf_substep(Params<T> P, T dtau, const
 // (eq:int:rnp2, R24), periodic wrap.
 // ===========================================================================
 template <class T, int D>
-__global__ void k_advance(Params<T> P, T dt, const T* __restrict__ dK, const V4<T>* __restrict__ rn,
+__global__ void k_advance(Params<T> P, T dt, const T* __restrict__ dK, int dstride, const V4<T>* __restrict__ rn,
                           const V4<T>* __restrict__ vel, V4<T>* __restrict__ pos, V4<T>* __restrict__ vt, Ctl* ctl,
                           const T* __restrict__ uout)
 {
@@ -2167,7 +2259,9 @@ __global__ void k_advance(Params<T> P, T dt, const T* __restrict__ dK, const V4<
     } else if (i < P.Nfo) {
         V4<T> x = ld4(rn + i), u = ld4(vel + i), ut = ld4(vt + i);
         // r^K - r^0: the second half of the GTVF record (k_gtvf_substep)
-        const V4<T> dl = dK ? ld4(reinterpret_cast<const V4<T>*>(dK + 8 * (size_t)i + 4)) : mk4<T>(T(0), T(0), T(0), T(0));
+        // r^K - r^0: fp32 the delta array (stride 4), fp64 the second half of the GTVF record (stride 8)
+        const V4<T> dl = dK ? ld4(reinterpret_cast<const V4<T>*>(dK + (size_t)dstride * i + (dstride - 4)))
+                            : mk4<T>(T(0), T(0), T(0), T(0));
         T tx = u.x + dl.x / dt, ty = u.y + dl.y / dt;
         T tz = D == 3 ? u.z + dl.z / dt : T(0);
         T hd = T(0.5) * dt;
