@@ -127,13 +127,18 @@ struct NcclTransport : Transport {
                  cudaStream_t st) override
     {
         if (check(api->GroupStart(), "ncclGroupStart")) return 1;
-        for (int f = 1; f >= 0; f--)
+        // a failed Send / Recv inside the group still closes the group (keeping the first
+        // error): an open group would leave this thread's later collectives undefined
+        int bad = 0;
+        for (int f = 1; f >= 0 && !bad; f--)
             if (nb[f] >= 0 && sn[f] > 0 && check(api->Send(sbuf[f], sn[f], ncclChar, nb[f], comm, st), "ncclSend"))
-                return 1;
-        for (int f = 0; f < 2; f++)
+                bad = 1;
+        for (int f = 0; f < 2 && !bad; f++)
             if (nb[f] >= 0 && rn[f] > 0 && check(api->Recv(rbuf[f], rn[f], ncclChar, nb[f], comm, st), "ncclRecv"))
-                return 1;
-        return check(api->GroupEnd(), "ncclGroupEnd");
+                bad = 1;
+        const ncclResult_t ge = api->GroupEnd();
+        if (bad) return 1;
+        return check(ge, "ncclGroupEnd");
     }
     int allreduce(double* buf, int count, int op, cudaStream_t st) override
     {
