@@ -481,43 +481,6 @@ struct NbCursorS {
     }
 };
 
-// the predicated append staged through a per-lane ring of 8 shared-memory slots (slot-major:
-// lane l's slot q is word q * 32 + l, so the lanes' stores never share a bank): one predicated
-// shared store per candidate instead of four register selects; every 4th accepted entry the
-// chunk leaves as one 16-byte global store
-struct NbCursorR {
-    int* ring;
-    int* row;
-    int k;
-    __device__ __forceinline__ void init(int* ring_, int* nbr, int cap, int i)
-    {
-        ring = ring_;
-        row = nbr + nb_base(i, cap);
-        k = 0;
-    }
-    __device__ __forceinline__ void push(bool acc, int j, int cap)
-    {
-        if (acc) {
-            ring[(k & 7) << 5] = j;
-            k++;
-            if ((k & 3) == 0 && k <= cap) {
-                const int q = (k - 4) & 7;
-                *reinterpret_cast<int4*>(row + (((k - 4) >> 2) << 7)) =
-                    make_int4(ring[q << 5], ring[(q + 1) << 5], ring[(q + 2) << 5], ring[(q + 3) << 5]);
-            }
-        }
-    }
-    __device__ __forceinline__ void flush(int cap)
-    {
-        const int s = k & 3;
-        if (s != 0 && k < cap) {
-            const int q = (k - s) & 7;
-            *reinterpret_cast<int4*>(row + (((k - s) >> 2) << 7)) =
-                make_int4(ring[q << 5], s > 1 ? ring[(q + 1) << 5] : 0, s > 2 ? ring[(q + 2) << 5] : 0, 0);
-        }
-    }
-};
-
 // One warp per cell: the lanes are the cell's destinations; candidates of
 // each stencil row are staged 32 at a time in shared memory (with the range's
 // periodic image shift applied) and read back as broadcasts, so every lane
@@ -804,10 +767,8 @@ template <int D>
 struct BlCfg {
     static constexpr bool cull = SISPH_BUILD_CULL && D == 3;
     static constexpr bool vst = SISPH_BUILD_VST != 0 && D == 3;
-    static constexpr bool ring = vst && SISPH_BUILD_VST == 3;
     using Cur = typename std::conditional<!vst, NbCursor,
-                typename std::conditional<SISPH_BUILD_VST == 2, NbCursorS,
-                typename std::conditional<SISPH_BUILD_VST == 3, NbCursorR, NbCursorV>::type>::type>::type;
+                                          typename std::conditional<SISPH_BUILD_VST == 2, NbCursorS, NbCursorV>::type>::type;
 };
 #ifdef SISPH_BUILD_MINB
 #define BL_LOOSE_BOUNDS __launch_bounds__(32 * BL_WARPS, SISPH_BUILD_MINB)
@@ -825,7 +786,6 @@ __global__ void BL_LOOSE_BOUNDS k_build_loose(Params<T> P, int ncells, const V4<
     constexpr int NRNG = NROW * RNG_PER_ROW;
     __shared__ V4<T> smem[BL_WARPS][32];
     __shared__ int smemj[BL_WARPS][32];
-    __shared__ int bring[BlCfg<D>::ring ? BL_WARPS : 1][2][8 * 32];   // NbCursorR rings
     __shared__ int4 rng[BL_WARPS][NRNG];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c = blockIdx.x * BL_WARPS + warp;
@@ -852,8 +812,7 @@ __global__ void BL_LOOSE_BOUNDS k_build_loose(Params<T> P, int ncells, const V4<
             act[d] = t < nd;
             i[d] = !act[d] ? -1 : (t < nfc ? fa + t : wslot(wperm, Nf, Nf + wa + (t - nfc)));
             xi[d] = ld4(pos + (act[d] ? i[d] : fa));
-            if constexpr (BlCfg<D>::ring) A[d].init(&bring[warp][d][lane], nbr, cap, act[d] ? i[d] : 0);
-            else A[d].init(nbr, cap, act[d] ? i[d] : 0);
+            A[d].init(nbr, cap, act[d] ? i[d] : 0);
         }
         if constexpr (BlCfg<D>::cull) {
         // box of this pass's destinations (warp-wide)
@@ -1032,21 +991,9 @@ __global__ void FILTER_BOUNDS k_filter(Params<T> P, int nrows, const V4<T>* __re
     __shared__ int bq[FQ][128];
     int nq = 0;
     const int pmask = P.per[0] | (P.per[1] << 1) | (P.per[2] << 2);
-#ifndef SISPH_FILTER_RING
-#define SISPH_FILTER_RING 0
-#endif
-#if SISPH_FILTER_RING
-    // append rings (NbCursorR): [cursor][warp][8 slots][32 lanes]
-    __shared__ int fring[2][4][8 * 32];
-    const int wq = threadIdx.x >> 5, ln = threadIdx.x & 31;
-    NbCursorR A, B;
-    A.init(&fring[0][wq][ln], nbr, cap, i);
-    B.init(&fring[1][wq][ln], nbr_in ? nbr_in : nbr, cap_in, inner ? i : 0);
-#else
     NbCursorV A, B;
     A.init(nbr, cap, i);
     B.init(nbr_in ? nbr_in : nbr, cap_in, inner ? i : 0);
-#endif
     const int4* __restrict__ src = reinterpret_cast<const int4*>(nbs + nb_base(i, cap_s));
     // the index chunks of the next SISPH_FILTER_PF chunks stay in flight while one is tested
     int4 vr[SISPH_FILTER_PF];

@@ -27,4 +27,13 @@ for w in tgv3d dambreak2d hydrostatic tgv2d; do
     timeout 900 ncu --set full --clock-control none --import-source on -k "regex:${re}" -s ${skip} -c 1 -o gpurun_out/${TAG}_${w}_${name} $CMD > gpurun_out/${TAG}_ncu_${w}_${name}.log 2>&1
   done
 done
+# summaries on the box (gpurun copies back at most 64 MiB): keep the C5 sweep and build reports
+for w in dambreak3d tgv3d dambreak2d hydrostatic tgv2d; do
+  python scripts/ncu_summary.py --workload $w --outdir gpurun_out gpurun_out/${TAG}_ncu_${w}.txt gpurun_out/${TAG}_${w}_*.ncu-rep > /dev/null 2>&1
+  python scripts/launches.py gpurun_out/${TAG}_${w}_launches.csv > gpurun_out/${TAG}_${w}_launches.txt 2>/dev/null
+done
+for r in gpurun_out/${TAG}_*.ncu-rep; do
+  case $r in *dambreak3d_sweep*|*dambreak3d_build*) ;; *) rm -f $r;; esac
+done
+rm -f gpurun_out/${TAG}_*_launches.csv
 echo done

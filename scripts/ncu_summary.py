@@ -1,6 +1,6 @@
 """Summarise ncu reports (--page details + raw dram bytes) into profiles/.
 
-    python scripts/ncu_summary.py [--workload NAME] <out.txt> <rep1.ncu-rep> [<rep2> ...]
+    python scripts/ncu_summary.py [--workload NAME] [--outdir DIR] <out.txt> <rep1.ncu-rep> [<rep2> ...]
 
 With --workload, also writes the per-workload records bench.py reads:
 profiles/traffic_NAME.json (dram bytes of one k_sweep launch, its roofline
@@ -68,8 +68,14 @@ def short(name):
 if __name__ == "__main__":
     args = sys.argv[1:]
     wl = None
-    if args and args[0] == "--workload":
-        wl, args = args[1], args[2:]
+    outdir = "profiles"
+    while args and args[0].startswith("--"):
+        if args[0] == "--workload":
+            wl, args = args[1], args[2:]
+        elif args[0] == "--outdir":
+            outdir, args = args[1], args[2:]
+        else:
+            break
     out = args[0]
     allines = []
     instr = {}
@@ -86,10 +92,10 @@ if __name__ == "__main__":
                                   "dram_bytes": b, "us_ncu": to_us(*extra["gpu__time_duration.sum"]),
                                   "source": rep}
             if wl and "k_sweep" in name:
-                with open(f"profiles/traffic_{wl}.json", "w") as f:
+                with open(f"{outdir}/traffic_{wl}.json", "w") as f:
                     json.dump({"kernel": name, "dram_bytes_per_launch": b, "source": rep}, f, indent=1)
     if wl and instr:
-        with open(f"profiles/instr_{wl}.json", "w") as f:
+        with open(f"{outdir}/instr_{wl}.json", "w") as f:
             json.dump(instr, f, indent=1)
     with open(out, "w") as f:
         f.write("\n".join(allines) + "\n")
