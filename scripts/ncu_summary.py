@@ -86,9 +86,13 @@ if __name__ == "__main__":
             print(f"skip {rep}: {e}", file=sys.stderr)
             continue
         allines += [f"# {rep}"] + lines + [""]
-        if "dram__bytes_read.sum" in extra and "sm__sass_inst_executed.sum" in extra:
+        ins = None
+        for ln in lines:
+            if ln.strip().startswith("Executed Instructions"):
+                ins = float(ln.split()[2].replace(",", ""))
+        if "dram__bytes_read.sum" in extra and ins is not None:
             b = to_bytes(*extra["dram__bytes_read.sum"]) + to_bytes(*extra["dram__bytes_write.sum"])
-            instr[short(name)] = {"warp_instr": float(extra["sm__sass_inst_executed.sum"][0].replace(",", "")),
+            instr[short(name)] = {"warp_instr": ins,
                                   "dram_bytes": b, "us_ncu": to_us(*extra["gpu__time_duration.sum"]),
                                   "source": rep}
             if wl and "k_sweep" in name:
