@@ -90,11 +90,14 @@ typedef struct {
                                during the iterations); 1: every sweep recomputes it from
                                the positions, as the paper's listing */
     int ppe_loop;           /* form of the PPE loop (one handle, timing off; slab ranks and timing
-                               always use 1): 0 (default) = 1 (the forms measured within 10 % of
-                               each other on B200: a sweep is latency-bound at these sizes);
-                               1 = host-polled speculative batches of sweep launches; 2 = a captured
-                               CUDA graph with a device-decided WHILE node; 3 = one persistent
-                               cooperative kernel for the whole loop (grid syncs between phases) */
+                               always use 1): 0 (default) = auto: 4 for <= 16384 fluid particles,
+                               2 for <= 400000, 1 above; 1 = host-polled speculative batches of
+                               sweep launches; 2 = a captured CUDA graph with a device-decided WHILE
+                               node; 3 = one persistent cooperative kernel for the whole loop (grid
+                               syncs between phases); 4 = one thread-block cluster (<= 16 SMs) for
+                               the whole loop, hardware cluster barriers between phases.  Every form
+                               runs the same row arithmetic (equal sweep counts and pressures; forms
+                               3 and 4 reduce the residual and the R32 mean in another order) */
     int ppe_mean_free;      /* reading R32: 1 = after every Jacobi sweep subtract the
                                mean of the live rows (fluid, not free surface, D_ii != 0) from
                                p^{k+1} before eq:convergence -- the projection onto the range of

@@ -1545,6 +1545,47 @@ template <class T, int D> struct Engine : EngineBase {
         return SISPH_OK;
     }
 
+    // the whole PPE loop in one thread-block cluster (k_ppe_cluster): up to 16 blocks of 1024
+    // threads (non-portable cluster size; 8 if the device refuses 16)
+    int cluster_max = 16;
+    int launch_cluster()
+    {
+        void* fn = coef ? (void*)k_ppe_cluster<T, D, true> : (void*)k_ppe_cluster<T, D, false>;
+        const long need = std::max((long)Nfo, (long)Nwo * WL);
+        for (;;) {
+            int nbk = (int)std::min<long>(cluster_max, std::max<long>(1, (need + CLUSTER_T - 1) / CLUSTER_T));
+            if (nbk > 8) SCK(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(nbk);
+            cfg.blockDim = dim3(CLUSTER_T);
+            cfg.stream = st;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = nbk;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            int cap = P.cap;
+            cudaError_t le;
+            if (coef)
+                le = cudaLaunchKernelEx(&cfg, k_ppe_cluster<T, D, true>, P, (const PpeDesc<T>*)ddesc, (const T*)rhs,
+                                        (const T*)diag, (const int*)cnt, cap, ctl);
+            else
+                le = cudaLaunchKernelEx(&cfg, k_ppe_cluster<T, D, false>, P, (const PpeDesc<T>*)ddesc, (const T*)rhs,
+                                        (const T*)diag, (const int*)cnt, cap, ctl);
+            if (le == cudaSuccess) break;
+            (void)cudaGetLastError();
+            if (cluster_max <= 1) {
+                err = std::string("cluster PPE launch: ") + cudaGetErrorString(le);
+                return SISPH_ECUDA;
+            }
+            cluster_max /= 2;   // e.g. no 16-SM cluster available: retry smaller
+        }
+        ++nlaunch;
+        return SISPH_OK;
+    }
+
     int launch_persistent()
     {
         void* fn = coef ? (void*)k_ppe_persistent<T, D, true> : (void*)k_ppe_persistent<T, D, false>;
@@ -1647,10 +1688,16 @@ template <class T, int D> struct Engine : EngineBase {
         // Auto (0): the CUDA-graph WHILE node for small problems, whose solves run tens of
         // latency-bound sweeps (configs[1]: 2.63 vs 2.88 ms per step with host-polled batches,
         // no host round trip per batch); host batches for large ones (a few HBM-bound sweeps)
-        int mode = ppe_loop == 0 ? (Nfo <= 400000 ? 2 : 1) : ppe_loop;
+        int mode = ppe_loop == 0 ? (Nfo <= 16384 ? 4 : (Nfo <= 400000 ? 2 : 1)) : ppe_loop;
         if (dist() || timing || Nf == 0 || launched >= mx) mode = 1;
         if (mode == 3 && P.mean_free) mode = 2;   // the persistent loop has no mean-free phase
-        if (mode == 3) {
+        if (mode == 4) {
+            // one thread-block cluster runs the loop (walls, sweep, mean, reduction, decision),
+            // separated by hardware cluster barriers
+            SRET(launch_cluster());
+            SCK(cudaMemcpyAsync(hctl, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+            SCK(cudaStreamSynchronize(st));
+        } else if (mode == 3) {
             // one cooperative launch: walls, sweep, fixed-order reduction and decision per
             // iteration, separated by grid syncs (small problems: no per-sweep launches)
             SRET(launch_persistent());

@@ -1462,11 +1462,16 @@ template <class T> struct PpeDesc {
     int min_it, max_it;
 };
 
+// a pressure read inside a kernel that also writes p (the persistent and cluster PPE loops:
+// other SMs' writes of the previous iteration): L2-coherent (ld.global.cg) instead of the
+// read-only path, whose L1 lines could still hold an older iterate
+template <bool COH, class T> __device__ __forceinline__ T ldp(const T* p) { return COH ? __ldcg(p) : __ldg(p); }
+
 // WL lanes share a wall row (lane `sub` takes its chunks sub, sub + WL, ...; the sums
 // meet by shuffles): walls are few (configs[1]: 3.1k) and each row is long, so one
 // lane per row left the pass bound by a ~45-deep chain of dependent loads
 constexpr int WL = 8;
-template <class T, int D>
+template <class T, int D, bool COH = false>
 __device__ __forceinline__ void wall_pressure_row(const Params<T>& P, int w, const V4<T>* __restrict__ pos,
                                                   const T* __restrict__ rho, const int* __restrict__ nbr,
                                                   const int* __restrict__ cnt, int ncap, T* p, int sub)
@@ -1483,7 +1488,7 @@ __device__ __forceinline__ void wall_pressure_row(const Params<T>& P, int w, con
         r_of(pair_vec<T, D>(P, xi, xj, d), r, ri);
         T wv = P.sig * quintic5(r * P.inv_h);
         T rw = __ldg(rho + j) * wv;
-        sp += p[j] * wv;
+        sp += ldp<COH>(p + j) * wv;
         sx += rw * d[0];
         sy += rw * d[1];
         if (D == 3) sz += rw * d[2];
@@ -1565,7 +1570,7 @@ constexpr int SWEEP_T = SISPH_SWEEP_T;
 template <class T> constexpr int sweep_minb() { return sizeof(T) == 4 ? SISPH_SWEEP_MINB : 1; }
 
 // eq:p-sor for row i from p^k = pin (the stored or the recomputed fac_ij)
-template <class T, int D, bool STORED>
+template <class T, int D, bool STORED, bool COH = false, int PFD = SISPH_SWEEP_PF>
 __device__ __forceinline__ T sweep_row(const Params<T>& P, int i, const V4<T>* __restrict__ pos,
                                        const T* __restrict__ rho, const uint8_t* __restrict__ fs,
                                        const int* __restrict__ nbr, const int* __restrict__ cnt, int ncap,
@@ -1582,12 +1587,12 @@ __device__ __forceinline__ T sweep_row(const Params<T>& P, int i, const V4<T>* _
         if (STORED) {
             const size_t b = nb_base(i, ncap);
             const int4* __restrict__ qi = reinterpret_cast<const int4*>(nbr + b);
-#if SISPH_SWEEP_PF > 0
+            if constexpr (PFD > 0) {
             // software pipelining: a register ring keeps the index + factor loads of the next
             // PD chunks in flight while this chunk's p_j are gathered (B200: the streamed
             // HBM traffic needs more bytes in flight per SM than one chunk per row gives;
             // PD = 4 at a 64-register cap measured best, 0.92 of the measured HBM bandwidth)
-            constexpr int PD = SISPH_SWEEP_PF;
+            constexpr int PD = PFD;
             int4 vr[PD];
             T fr[PD][4];
 #pragma unroll
@@ -1602,10 +1607,10 @@ __device__ __forceinline__ T sweep_row(const Params<T>& P, int i, const V4<T>* _
                 const int4 vnew = cn < n ? LDLIST(qi + (size_t)(cn >> 2) * 32) : make_int4(i, i, i, i);
                 T fnew[4] = {T(0), T(0), T(0), T(0)};
                 if (cn < n) ld_chunk4(coef + b + ((size_t)(cn >> 2) * 32 << 2), fnew);
-                s += fr[0][0] * __ldg(pin + vr[0].x);
-                if (c + 1 < n) s += fr[0][1] * __ldg(pin + vr[0].y);
-                if (c + 2 < n) s += fr[0][2] * __ldg(pin + vr[0].z);
-                if (c + 3 < n) s += fr[0][3] * __ldg(pin + vr[0].w);
+                s += fr[0][0] * ldp<COH>(pin + vr[0].x);
+                if (c + 1 < n) s += fr[0][1] * ldp<COH>(pin + vr[0].y);
+                if (c + 2 < n) s += fr[0][2] * ldp<COH>(pin + vr[0].z);
+                if (c + 3 < n) s += fr[0][3] * ldp<COH>(pin + vr[0].w);
 #pragma unroll
                 for (int q = 0; q < PD - 1; q++) {
                     vr[q] = vr[q + 1];
@@ -1616,24 +1621,24 @@ __device__ __forceinline__ T sweep_row(const Params<T>& P, int i, const V4<T>* _
 #pragma unroll
                 for (int e = 0; e < 4; e++) fr[PD - 1][e] = fnew[e];
             }
-#else
+            } else {
             for (int c = 0; c < n; c += 4) {
                 const size_t o = (size_t)(c >> 2) * 32;
                 const int4 v = LDLIST(qi + o);
                 T f[4];
                 ld_chunk4(coef + b + (o << 2), f);
-                s += f[0] * pin[v.x];
-                if (c + 1 < n) s += f[1] * pin[v.y];
-                if (c + 2 < n) s += f[2] * pin[v.z];
-                if (c + 3 < n) s += f[3] * pin[v.w];
+                s += f[0] * ldp<COH>(pin + v.x);
+                if (c + 1 < n) s += f[1] * ldp<COH>(pin + v.y);
+                if (c + 2 < n) s += f[2] * ldp<COH>(pin + v.z);
+                if (c + 3 < n) s += f[3] * ldp<COH>(pin + v.w);
             }
-#endif
+            }
         } else {
             const V4<T> xi = ld4(pos + i);
             for_nbrs(nbr, ncap, i, n, [&](int j) {
                 V4<T> xj = ld4(pos + j);
                 T rhoj = __ldg(rho + j);
-                T pj = pin[j];
+                T pj = ldp<COH>(pin + j);
                 T d[3], r, ri;
                 T r2 = pair_vec<T, D>(P, xi, xj, d);
                 r_of(r2, r, ri);
@@ -1939,13 +1944,14 @@ __global__ void __launch_bounds__(SWEEP_T) k_ppe_persistent(Params<T> P, const P
         const int kit = vc->iter;
         T* pin = (kit & 1) ? pB : pA;
         T* pout = (kit & 1) ? pA : pB;
-        for (int q = gt / WL; q < P.Nwo; q += gs / WL) wall_pressure_row<T, D>(P, q, pos, rho, nbr, cnt, ncap, pin, gt % WL);
+        for (int q = gt / WL; q < P.Nwo; q += gs / WL)
+            wall_pressure_row<T, D, true>(P, q, pos, rho, nbr, cnt, ncap, pin, gt % WL);
         grid.sync();
         double dn = 0.0, dd = 0.0;
         bool bad = false;
         for (int i = gt; i < P.Nfo; i += gs) {
             const T pold = pin[i];
-            const T pnew = sweep_row<T, D, STORED>(P, i, pos, rho, fs, nbr, cnt, ncap, coef, rhs, diag, pin);
+            const T pnew = sweep_row<T, D, STORED, true>(P, i, pos, rho, fs, nbr, cnt, ncap, coef, rhs, diag, pin);
             pout[i] = pnew;
             dn += fabs((double)pnew - (double)pold);
             dd += fs[i] == 2 ? 0.0 : fabs((double)pnew);
@@ -2002,6 +2008,151 @@ __global__ void __launch_bounds__(SWEEP_T) k_ppe_persistent(Params<T> P, const P
             }
         }
         grid.sync();
+    }
+}
+
+// ===========================================================================
+// A12 for small problems: ONE thread-block cluster (up to 16 SMs, one launch per solve)
+// runs the whole PPE loop — wall pressures, the sweep, (R32) the live-row mean, the
+// fixed-order reduction and the stop decision (R12/R12b, R13) — separated by hardware
+// cluster barriers instead of kernel boundaries or a software grid barrier.  The block
+// partials meet through distributed shared memory in block-rank order (deterministic);
+// the pressures of other SMs are read L2-coherent (ldp<true>).  The row arithmetic is
+// sweep_row / wall_pressure_row, the same as every other loop form.
+// ===========================================================================
+constexpr int CLUSTER_T = 1024;
+template <class T, int D, bool STORED>
+__global__ void __launch_bounds__(CLUSTER_T) k_ppe_cluster(Params<T> P, const PpeDesc<T>* __restrict__ dsc,
+                                                           const T* __restrict__ rhs, const T* __restrict__ diag,
+                                                           const int* __restrict__ cnt, int ncap, Ctl* ctl)
+{
+    cg::cluster_group cl = cg::this_cluster();
+    const int nbk = (int)cl.num_blocks(), rk = (int)cl.block_rank();
+    const int gt = rk * blockDim.x + threadIdx.x, gs = nbk * blockDim.x;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    __shared__ double sa[32], sb[32];
+    __shared__ double bp[2][2][2];   // [iteration parity][phase: sweep / R32 pass][a, b]: this block's partials
+    __shared__ double red_s[2];      // the cluster sums, identical in every block
+    __shared__ int bad_s[2][2];      // [parity][phase]: a non-finite value in this block
+    __shared__ int badc_s;           // any block's (identical in every block)
+    const V4<T>* __restrict__ pos = dsc->pos;
+    const T* __restrict__ rho = dsc->rho;
+    const uint8_t* __restrict__ fs = dsc->fs;
+    const int* __restrict__ nbr = dsc->nbr;
+    const T* __restrict__ coef = dsc->coef;
+    T* pA = dsc->pA;
+    T* pB = dsc->pB;
+    volatile Ctl* vc = ctl;
+    if (threadIdx.x < 4) bad_s[threadIdx.x >> 1][threadIdx.x & 1] = 0;
+    // fixed-order block reduction of (a, b) into dst (thread 0 writes); bflag: this phase's flag
+    auto block_sum = [&](double a, double b, bool bad, double* dst, int* bflag) {
+        a = warp_sum(a);
+        b = warp_sum(b);
+        const int anyb = __any_sync(0xffffffffu, bad);
+        if (threadIdx.x == 0) *bflag = 0;
+        __syncthreads();
+        if (lane == 0) {
+            sa[w] = a;
+            sb[w] = b;
+            if (anyb) atomicOr(bflag, 1);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double x = 0, y = 0;
+            for (int q = 0; q < nw; q++) {
+                x += sa[q];
+                y += sb[q];
+            }
+            dst[0] = x;
+            dst[1] = y;
+        }
+    };
+    // after a cluster barrier: every block sums all blocks' partials in block-rank order (the
+    // same result everywhere), so every block takes the same decision without a broadcast
+    auto cluster_sum = [&](int par, int ph) {
+        if (threadIdx.x == 0) {
+            double A = 0, B = 0;
+            int bad = 0;
+            for (int r = 0; r < nbk; r++) {
+                const double* q = cl.map_shared_rank(&bp[par][ph][0], r);
+                A += q[0];
+                B += q[1];
+                bad |= *cl.map_shared_rank(&bad_s[par][ph], r);
+            }
+            red_s[0] = A;
+            red_s[1] = B;
+            badc_s |= bad;
+            if (bad && rk == 0) vc->nonfinite = 1;
+        }
+        __syncthreads();
+    };
+    int kit = vc->iter;
+    bool done = vc->done != 0;
+    const double lam = __longlong_as_double((long long)vc->lambda_bits);
+    if (threadIdx.x == 0) badc_s = vc->nonfinite ? 1 : 0;   // e.g. from A11's fused first sweep
+    __syncthreads();
+    while (!done) {
+        const int par = kit & 1;
+        const T* pin = par ? pB : pA;
+        T* pout = par ? pA : pB;
+        if (P.Nwo) {
+            for (int t = gt; t < P.Nwo * WL; t += gs)
+                wall_pressure_row<T, D, true>(P, t / WL, pos, rho, nbr, cnt, ncap, const_cast<T*>(pin), t % WL);
+            cl.sync();
+        }
+        double dn = 0.0, dd = 0.0;
+        bool bad = false;
+        for (int i = gt; i < P.Nfo; i += gs) {
+            const T pold = pin[i];
+            const T pnew =
+                sweep_row<T, D, STORED, true, 2>(P, i, pos, rho, fs, nbr, cnt, ncap, coef, rhs, diag, pin);
+            pout[i] = pnew;
+            if (P.mean_free) {
+                const bool live = !fs[i] && diag[i] != T(0);
+                dn += live ? (double)pnew : 0.0;
+                dd += live ? 1.0 : 0.0;
+            } else {
+                dn += fabs((double)pnew - (double)pold);
+                dd += fs[i] == 2 ? 0.0 : fabs((double)pnew);
+            }
+            bad = bad || !isfinite((double)pnew);
+        }
+        block_sum(dn, dd, bad, &bp[par][0][0], &bad_s[par][0]);
+        cl.sync();
+        cluster_sum(par, 0);
+        double num = red_s[0], den = red_s[1];
+        if (P.mean_free) {
+            // R32: remove the live-row mean, then the residual sums of the corrected iterate
+            const double mean = den > 0.0 ? num / den : 0.0;
+            dn = dd = 0.0;
+            bad = false;
+            for (int i = gt; i < P.Nfo; i += gs) {
+                T v = pout[i];
+                if (!fs[i] && diag[i] != T(0)) {
+                    v = (T)((double)v - mean);
+                    pout[i] = v;
+                }
+                dn += fabs((double)v - (double)pin[i]);
+                dd += fs[i] == 2 ? 0.0 : fabs((double)v);
+                bad = bad || !isfinite((double)v);
+            }
+            block_sum(dn, dd, bad, &bp[par][1][0], &bad_s[par][1]);
+            cl.sync();
+            cluster_sum(par, 1);
+            num = red_s[0];
+            den = red_s[1];
+        }
+        num *= dsc->cscale;
+        den *= dsc->cscale;
+        const double dmax = den > lam ? den : lam;
+        const double res = num == 0.0 ? 0.0 : (dmax > 0.0 ? num / dmax : INFINITY);
+        kit += 1;
+        done = (kit >= dsc->min_it && res < dsc->tol) || kit >= dsc->max_it || badc_s;
+        if (rk == 0 && threadIdx.x == 0) {
+            vc->residual = res;
+            vc->iter = kit;
+            vc->done = done ? 1 : 0;
+        }
     }
 }
 

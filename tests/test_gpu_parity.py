@@ -402,29 +402,40 @@ def test_square_patch_parity(prec):
 # ------------------------------------------------------------------ PPE loop forms
 @pytest.mark.parametrize("name", ["tgv2d_f64", "hydro_f64", "db3d_f32", "tgv3d_f64", "db2d_f64"])
 def test_ppe_loop_forms_agree(name):
-    """Host-polled batches (1), the CUDA-graph WHILE node (2) and the persistent
-    cooperative kernel (3) run the same row arithmetic: equal sweep counts and
-    bitwise-equal pressures; the graph runs the very same kernels, so its
-    residual is bitwise equal too (the persistent kernel groups the residual
-    sums per block of its grid-stride loop: equal to rounding)."""
+    """Host-polled batches (1), the CUDA-graph WHILE node (2), the persistent
+    cooperative kernel (3) and the thread-block cluster (4) run the same row
+    arithmetic: equal sweep counts and bitwise-equal pressures; the graph runs the
+    very same kernels, so its residual is bitwise equal too (forms 3 and 4 group the
+    residual sums -- and the R32 live-row mean of the periodic cases -- in another
+    order: equal to rounding there)."""
     case = CASES[name]
-    sims = {m: gpu_sim(case, ppe_loop=m) for m in (1, 2, 3)}
+    mf = bool(case.params.get("ppe_mean_free", 0))
+    sims = {m: gpu_sim(case, ppe_loop=m) for m in (1, 2, 3, 4)}
     for _ in range(3):
         r = {m: s.step(case.dt) for m, s in sims.items()}
-        assert r[1].iters == r[2].iters == r[3].iters
+        assert r[1].iters == r[2].iters == r[3].iters == r[4].iters
         assert r[1].residual == r[2].residual
         assert r[3].residual == pytest.approx(r[1].residual, rel=1e-9)
+        assert r[4].residual == pytest.approx(r[1].residual, rel=1e-9)
     for fld in ("PRESSURE", "VELOCITY", "POSITION"):
         ref = sims[1].get(fld)
         assert np.array_equal(sims[2].get(fld), ref)
-        assert np.array_equal(sims[3].get(fld), ref)
+        for m in (3, 4):
+            if mf:
+                assert_close(fld, sims[m].get(fld), ref, case.params["precision"])
+            else:
+                assert np.array_equal(sims[m].get(fld), ref), (m, fld)
     # split API with another tolerance than the parameters': read per solve
     for s in sims.values():
         s.predict(case.dt)
     its = {m: s.ppe_solve(1e-6, 50)[0] for m, s in sims.items()}
-    assert its[1] == its[2] == its[3]
+    assert its[1] == its[2] == its[3] == its[4]
     assert np.array_equal(sims[2].get("PRESSURE"), sims[1].get("PRESSURE"))
-    assert np.array_equal(sims[3].get("PRESSURE"), sims[1].get("PRESSURE"))
+    for m in (3, 4):
+        if mf:
+            assert_close("p", sims[m].get("PRESSURE"), sims[1].get("PRESSURE"), case.params["precision"])
+        else:
+            assert np.array_equal(sims[m].get("PRESSURE"), sims[1].get("PRESSURE")), m
 
 
 # ------------------------------------------------------------------ reading R32: mean-free Jacobi
@@ -458,17 +469,21 @@ def test_mean_free_solve_parity(name):
 def test_mean_free_loop_forms_agree(name):
     """Host batches and the graph WHILE node (whose body ends with k_mean_fix
     setting the condition) run identical kernels: bitwise-equal results; the
-    persistent form falls back to the graph for mean-free."""
+    persistent form falls back to the graph for mean-free; the cluster form (4)
+    reduces the live-row mean in block-rank order: equal sweep counts, fields equal
+    to rounding."""
     case = CASES[name]
-    sims = {m: gpu_sim(case, ppe_loop=m, ppe_mean_free=1) for m in (1, 2, 3)}
+    sims = {m: gpu_sim(case, ppe_loop=m, ppe_mean_free=1) for m in (1, 2, 3, 4)}
     for _ in range(3):
         r = {m: s.step(case.dt) for m, s in sims.items()}
-        assert r[1].iters == r[2].iters == r[3].iters
+        assert r[1].iters == r[2].iters == r[3].iters == r[4].iters
         assert r[1].residual == r[2].residual == r[3].residual
+        assert r[4].residual == pytest.approx(r[1].residual, rel=1e-6)
     for fld in ("PRESSURE", "VELOCITY", "POSITION"):
         ref = sims[1].get(fld)
         assert np.array_equal(sims[2].get(fld), ref)
         assert np.array_equal(sims[3].get(fld), ref)
+        assert_close(fld, sims[4].get(fld), ref, case.params["precision"])
 
 
 def test_mean_free_steps_parity_resynced():
