@@ -91,10 +91,11 @@ typedef struct {
                                the positions, as the paper's listing */
     int ppe_loop;           /* form of the PPE loop (one handle, timing off; slab ranks and timing
                                always use 1): 0 (default) = auto: 4 for <= 16384 fluid particles,
-                               2 for <= 400000, 1 above; 1 = host-polled speculative batches of
+                               3 for <= 400000 (2 with ppe_mean_free), 1 above; 1 = host-polled
+                               speculative batches of
                                sweep launches; 2 = a captured CUDA graph with a device-decided WHILE
-                               node; 3 = one persistent cooperative kernel for the whole loop (grid
-                               syncs between phases); 4 = one thread-block cluster (<= 16 SMs) for
+                               node; 3 = one persistent cooperative kernel for the whole loop (two
+                               grid syncs per sweep, every block takes the stop decision); 4 = one thread-block cluster (<= 16 SMs) for
                                the whole loop, hardware cluster barriers between phases.  Every form
                                runs the same row arithmetic (equal sweep counts and pressures; forms
                                3 and 4 reduce the residual and the R32 mean in another order) */

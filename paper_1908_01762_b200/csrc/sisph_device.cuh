@@ -230,6 +230,14 @@ __device__ __forceinline__ int cell_key(const Params<T>& P, const int c[3])
 // ---------------------------------------------------------------------------
 // warp / block reductions
 // ---------------------------------------------------------------------------
+// Programmatic dependent launch (PDL): a kernel launched with the programmatic
+// stream-serialization attribute may be scheduled while its predecessor runs;
+// pdl_wait blocks until the predecessor has completed and its writes are
+// visible (a no-op without the attribute), pdl_trigger lets the successor be
+// scheduled early.  Every PDL-launched kernel waits before it reads anything.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ double warp_sum(double v)
 {
 #pragma unroll

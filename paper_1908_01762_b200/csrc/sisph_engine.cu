@@ -24,6 +24,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -159,6 +160,10 @@ template <class T, int D> struct Engine : EngineBase {
     int rebuild_mode = 0;   // 0: single build + filter when the skin fits, 1: always two exact builds
     int matrix_free = 0;    // 1: the sweep recomputes fac_ij from positions; 0: A11 stores it per pair
     T* coef = nullptr;      // stored per-pair part of fac_ij, blocked-ELL layout of nbr (fluid rows)
+    uint4* code = nullptr;  // code mode: the sweep's 16-bit copy of the fluid rows' list (CodeWriter)
+    int* nslot = nullptr;   // with coef in slot order
+    int cc8 = 0;
+    int use_codes = 0;      // SISPH_SWEEP_CODES=1: code mode (measured: sweep +12 %, A11 -20 %)
     bool skin_used = false;
     double skin_radius = 0;
     double extent = 0;      // max |coordinate| of the domain (rounding margin of the skin)
@@ -210,7 +215,7 @@ template <class T, int D> struct Engine : EngineBase {
                         nbs, cnt_s, wperm_s, wstart_s, coef, dflag, dflag2, dpre, dlist[0], dlist[1], dlist[2],
                         dcnt, fsend[0], fsend[1], fsend_pre[0], fsend_pre[1], grecv, wsend[0], wsend[1], wrecv,
                         inv, sbuf[0], sbuf[1], rbuf[0], rbuf[1], wtmp, fnp, dcnt_w, ptype, ptype_alt, uout,
-                        oflag, olist, onew};
+                        oflag, olist, onew, code, nslot};
         if (st) cudaStreamSynchronize(st);
         for (void* q : ptrs)
             if (q) cudaFree(q);
@@ -367,6 +372,8 @@ template <class T, int D> struct Engine : EngineBase {
         P.ghosts = dist() ? 1 : 0;
         rebuild_mode = prm->rebuild_mode;
         matrix_free = prm->matrix_free;
+        if (const char* e = getenv("SISPH_SWEEP_CODES")) use_codes = atoi(e) != 0;
+        if (const char* e = getenv("SISPH_PDL")) pdl = atoi(e) != 0;
         ppe_loop = prm->ppe_loop;
         P.mean_free = prm->ppe_mean_free ? 1 : 0;
         pref_auto = prm->pref_auto;
@@ -553,14 +560,26 @@ template <class T, int D> struct Engine : EngineBase {
         if (nbr) cudaFree(nbr);
         if (nbr_in) cudaFree(nbr_in);
         if (coef) cudaFree(coef);
+        if (code) cudaFree(code);
+        if (nslot) cudaFree(nslot);
         nbr = nbr_in = nullptr;
         coef = nullptr;
+        code = nullptr;
+        nslot = nullptr;
         int rc = 0;
         nbr = dalloc<int>((size_t)cap * rows32(capT), err, rc);
         if (rc) return rc;
         if (!matrix_free) {
-            coef = dalloc<T>((size_t)cap * rows32(capF), err, rc);
+            // code mode: a long step takes two slots, so a row needs at most 2 cap slots
+            cc8 = use_codes ? (2 * cap + 7) / 8 : 0;
+            coef = dalloc<T>((size_t)(use_codes ? 8 * cc8 : cap) * rows32(capF), err, rc);
             if (rc) return rc;
+            if (use_codes) {
+                code = dalloc<uint4>((size_t)cc8 * rows32(capF), err, rc);
+                if (rc) return rc;
+                nslot = dalloc<int>(rows32(capF), err, rc);
+                if (rc) return rc;
+            }
         }
         P.cap = cap;
         if (use_inner) {
@@ -1445,7 +1464,7 @@ template <class T, int D> struct Engine : EngineBase {
         }
         ++nlaunch, k_rhs_diag<T, D><<<std::max(nblk(Nfo, RHS_T), 1), RHS_T, 0, st>>>(
                        P, (T)(1.0 / dt), pos, us, rho, fs, nbr, cnt, P.cap, rhs, diag, coef, ctl, p, p_alt, partials,
-                       reinterpret_cast<const T*>(recS));
+                       reinterpret_cast<const T*>(recS), code, nslot, cc8);
         SCK(cudaGetLastError());
         SRET(mark(8));
         pre_swept = true;
@@ -1493,6 +1512,9 @@ template <class T, int D> struct Engine : EngineBase {
         hdesc->fs = fs;
         hdesc->nbr = nbr;
         hdesc->coef = coef;
+        hdesc->code = code;
+        hdesc->nslot = nslot;
+        hdesc->cc8 = cc8;
         hdesc->pA = p;
         hdesc->pB = p_alt;
         hdesc->tol = tl;
@@ -1529,14 +1551,15 @@ template <class T, int D> struct Engine : EngineBase {
         SCK(cudaGraphAddNode(&node, pgraph, nullptr, 0, &cp));
         cudaGraph_t body = cp.conditional.phGraph_out[0];
         SCK(cudaStreamBeginCaptureToGraph(cst, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-        if (Nwo) k_ppe_wall<T, D><<<nblk((long)Nwo * WL, 256), 256, 0, cst>>>(P, ddesc, cnt, P.cap, ctl);
+        if (Nwo) SCK(klaunch(k_ppe_wall<T, D>, nblk((long)Nwo * WL, 256), 256, cst, P, (const PpeDesc<T>*)ddesc,
+                             (const int*)cnt, P.cap, (const Ctl*)ctl));
         const int nb = std::max(nblk(Nfo, SWEEP_T), 1);
         const int uh = P.mean_free ? 0 : 1;   // mean-free: k_mean_fix decides and sets the condition
-        if (coef)
-            k_sweep<T, D, true><<<nb, SWEEP_T, 0, cst>>>(P, ddesc, rhs, diag, cnt, P.cap, ctl, partials, 0, pcond, uh);
-        else
-            k_sweep<T, D, false><<<nb, SWEEP_T, 0, cst>>>(P, ddesc, rhs, diag, cnt, P.cap, ctl, partials, 0, pcond, uh);
-        if (P.mean_free) k_mean_fix<T><<<nb, SWEEP_T, 0, cst>>>(P, ddesc, diag, ctl, partials, 0, pcond, 1);
+        SCK(klaunch(coef ? k_sweep<T, D, true> : k_sweep<T, D, false>, nb, SWEEP_T, cst, P, (const PpeDesc<T>*)ddesc,
+                    (const T*)rhs, (const T*)diag, (const int*)cnt, P.cap, ctl, partials, 0, pcond, uh));
+        if (P.mean_free)
+            SCK(klaunch(k_mean_fix<T>, nb, SWEEP_T, cst, P, (const PpeDesc<T>*)ddesc, (const T*)diag, ctl, partials, 0,
+                        pcond, 1));
         cudaError_t le = cudaGetLastError();
         SCK(cudaStreamEndCapture(cst, &body));
         SCK(le);
@@ -1594,7 +1617,7 @@ template <class T, int D> struct Engine : EngineBase {
             SCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, SWEEP_T, 0));
             SCK(cudaGetDevice(&dev));
             SCK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-            pgrid_max = std::max(1, std::min(per * sms, 8192));
+            pgrid_max = std::max(1, std::min(per * sms, 4096));   // partials: 2 parities x 2 per block
         }
         const int grid = std::max(1, std::min(pgrid_max, nblk(std::max((long)Nfo, (long)Nwo * WL), SWEEP_T)));
         int cap = P.cap;
@@ -1611,15 +1634,40 @@ template <class T, int D> struct Engine : EngineBase {
     {
         if (dist()) SRET(xallreduce(ctl->red, 3, 0));
         const int nb = std::max(nblk(Nfo, SWEEP_T), 1);
-        ++nlaunch, k_mean_fix<T><<<nb, SWEEP_T, 0, st>>>(P, ddesc, diag, ctl, partials, dist() ? 1 : 0, pcond, 0);
+        ++nlaunch;
+        SCK(klaunch(k_mean_fix<T>, nb, SWEEP_T, st, P, (const PpeDesc<T>*)ddesc, (const T*)diag, ctl, partials,
+                    dist() ? 1 : 0, pcond, 0));
         SCK(cudaGetLastError());
         return SISPH_OK;
+    }
+
+    // the PPE loop's kernels (k_ppe_wall, k_sweep, k_mean_fix) with programmatic dependent
+    // launch on problems whose sweeps are launch-latency bound (each kernel waits on its
+    // predecessor before reading anything: griddepcontrol.wait)
+    int pdl = -1;   // -1: auto (Nfo <= 400000), SISPH_PDL=0/1 overrides
+    template <class... KArgs, class... Args>
+    cudaError_t klaunch(void (*k)(KArgs...), int grid, int block, cudaStream_t s, Args... args)
+    {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(block);
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = (pdl < 0 ? Nfo <= 400000 : pdl != 0) ? 1 : 0;
+        return cudaLaunchKernelEx(&cfg, k, args...);
     }
 
     int launch_sweeps(int count, double tl, int mi, int mx)
     {
         for (int c = 0; c < count; c++) {
-            if (Nwo) ++nlaunch, k_ppe_wall<T, D><<<nblk((long)Nwo * WL, 256), 256, 0, st>>>(P, ddesc, cnt, P.cap, ctl);
+            if (Nwo) {
+                ++nlaunch;
+                SCK(klaunch(k_ppe_wall<T, D>, nblk((long)Nwo * WL, 256), 256, st, P, (const PpeDesc<T>*)ddesc,
+                            (const int*)cnt, P.cap, (const Ctl*)ctl));
+            }
             if (dist()) SRET(halo_p(true));
             bool rec = timing && nrec < MAXREC;
             if (rec) {
@@ -1631,12 +1679,10 @@ template <class T, int D> struct Engine : EngineBase {
             }
             const int defer = dist() ? 1 : 0;
             const int nb = std::max(nblk(Nfo, SWEEP_T), 1);   // one block at least: the last block decides
-            if (coef)
-                ++nlaunch, k_sweep<T, D, true><<<nb, SWEEP_T, 0, st>>>(
-                               P, ddesc, rhs, diag, cnt, P.cap, ctl, partials, defer, pcond, 0);
-            else
-                ++nlaunch, k_sweep<T, D, false><<<nb, SWEEP_T, 0, st>>>(
-                               P, ddesc, rhs, diag, cnt, P.cap, ctl, partials, defer, pcond, 0);
+            ++nlaunch;
+            SCK(klaunch(coef ? k_sweep<T, D, true> : k_sweep<T, D, false>, nb, SWEEP_T, st, P,
+                        (const PpeDesc<T>*)ddesc, (const T*)rhs, (const T*)diag, (const int*)cnt, P.cap, ctl, partials,
+                        defer, pcond, 0));
             if (P.mean_free) SRET(mean_fix());
             if (rec) {
                 SCK(cudaEventRecord(sev[2 * nrec + 1], st));
@@ -1685,10 +1731,11 @@ template <class T, int D> struct Engine : EngineBase {
             SCK(cudaMemsetAsync(ctl, 0, 4 * sizeof(int), st));  // ticket, iter, done, nonfinite
         }
         // the loop form: one handle with timing off may run the whole loop on the device.
-        // Auto (0): the CUDA-graph WHILE node for small problems, whose solves run tens of
-        // latency-bound sweeps (configs[1]: 2.63 vs 2.88 ms per step with host-polled batches,
-        // no host round trip per batch); host batches for large ones (a few HBM-bound sweeps)
-        int mode = ppe_loop == 0 ? (Nfo <= 16384 ? 4 : (Nfo <= 400000 ? 2 : 1)) : ppe_loop;
+        // Auto (0): one thread-block cluster for <= 16k rows (C1: 2.37 -> 1.83 ms per step),
+        // the persistent cooperative kernel up to 400k rows (C2: 1.67 vs 2.15 ms with the
+        // graph's WHILE node, 10-step runs; the mean-free loop falls back to the graph), host
+        // batches for large ones (a few HBM-bound sweeps per step)
+        int mode = ppe_loop == 0 ? (Nfo <= 16384 ? 4 : (Nfo <= 400000 ? 3 : 1)) : ppe_loop;
         if (dist() || timing || Nf == 0 || launched >= mx) mode = 1;
         if (mode == 3 && P.mean_free) mode = 2;   // the persistent loop has no mean-free phase
         if (mode == 4) {

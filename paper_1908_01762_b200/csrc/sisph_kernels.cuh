@@ -1304,6 +1304,92 @@ __global__ void __launch_bounds__(128) k_forces_predict(Params<T> P, T dt, const
 // sweep (k_decide takes the decision in the solve, once Lambda is complete).
 constexpr int RHS_T = 128;
 
+// ---------------------------------------------------------------------------
+// The sweep's 16-bit list (round 2).  The stored sweep streams, per pair, the
+// neighbour index and the stored factor: 4 + 4 bytes.  In code mode A11
+// writes each fluid row's S list as SLOTS of (16-bit code, factor) instead:
+// the code is the difference to the previous entry (the row index i before
+// the first one).  The list runs through the stencil rows in cell order, so
+// inside a stencil row and between y-rows the steps fit in 15 bits; a longer
+// step (between z-rows, into the wall / halo ranges, across a periodic image)
+// takes two slots: A = high part, factor 0, gathers p_i; B = low 16 bits and
+// the factor.  Slot codes: bit 0 = 0: d = (short)c >> 1; bit 0 = 1: slot A,
+// hi = (short)c >> 1, and the next slot's 16 bits complete d = hi * 2^16 + lo.
+// Every slot is decoded and gathered without a branch (fixed rate: one code,
+// one factor); the row is padded with (0, 0) slots to a multiple of 8.
+// Layout: row group g = i / 32, chunk c of 8 codes at uint4 index
+// (g * cc8 + c) * 32 + i % 32 (coalesced like the 32-bit list); factors in
+// the blocked-ELL layout of the list with the slot capacity 8 cc8; the slot
+// count per row in nslot.  The decoded entries are the list's, in its order,
+// and a (0-factor) slot adds +-0: the results are bit-equal.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ size_t code_at(int i, int cc8, int c)
+{
+    return ((size_t)(i >> 5) * cc8 + c) * 32 + (i & 31);
+}
+
+// the factors of slots k .. k + 7 (two blocked-ELL chunks), zeros if !ok
+template <class T>
+__device__ __forceinline__ void ld_slots8(const T* __restrict__ crow, int k, bool ok, T (&f)[8])
+{
+    T a[4] = {T(0), T(0), T(0), T(0)}, b[4] = {T(0), T(0), T(0), T(0)};
+    if (ok) {
+        ld_chunk4(crow + nb_off(k), a);
+        ld_chunk4(crow + nb_off(k + 4), b);
+    }
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+        f[e] = a[e];
+        f[4 + e] = b[e];
+    }
+}
+
+template <class T> struct CodeWriter {
+    uint4* code;
+    T* crow;            // coef + nb_base(i, 8 cc8)
+    int cc8, i, prev, ns;
+    unsigned w0, w1, w2, w3;
+    T f0, f1, f2, f3;
+    __device__ CodeWriter(uint4* c, T* coef, int cc, int row)
+        : code(c), crow(coef ? coef + nb_base(row, 8 * cc) : nullptr), cc8(cc), i(row), prev(row), ns(0),
+          w0(0), w1(0), w2(0), w3(0), f0(0), f1(0), f2(0), f3(0)
+    {
+    }
+    __device__ __forceinline__ void emit(unsigned c, T f)
+    {
+        w0 = __funnelshift_r(w0, w1, 16);
+        w1 = __funnelshift_r(w1, w2, 16);
+        w2 = __funnelshift_r(w2, w3, 16);
+        w3 = (w3 >> 16) | (c << 16);
+        f0 = f1;
+        f1 = f2;
+        f2 = f3;
+        f3 = f;
+        ns++;
+        if ((ns & 3) == 0) {
+            const T fb[4] = {f0, f1, f2, f3};
+            st_chunk4(crow + nb_off(ns - 4), fb);
+        }
+        if ((ns & 7) == 0) code[code_at(i, cc8, (ns >> 3) - 1)] = make_uint4(w0, w1, w2, w3);
+    }
+    __device__ __forceinline__ void push(int j, T f)
+    {
+        const int d = j - prev;
+        prev = j;
+        if (d >= -16384 && d <= 16383) {
+            emit(((unsigned)d << 1) & 0xFFFFu, f);
+        } else {
+            emit((((unsigned)(d >> 16) << 1) | 1u) & 0xFFFFu, T(0));
+            emit((unsigned)d & 0xFFFFu, f);
+        }
+    }
+    __device__ __forceinline__ void finish(int* nslot)
+    {
+        nslot[i] = ns;
+        while (ns & 7) emit(0u, T(0));
+    }
+};
+
 template <class T, int D>
 __global__ void __launch_bounds__(RHS_T) k_rhs_diag(Params<T> P, T inv_dt, const V4<T>* __restrict__ pos,
                                                     const V4<T>* __restrict__ us, const T* __restrict__ rho,
@@ -1311,7 +1397,8 @@ __global__ void __launch_bounds__(RHS_T) k_rhs_diag(Params<T> P, T inv_dt, const
                                                     const int* __restrict__ cnt, int ncap, T* __restrict__ rhs,
                                                     T* __restrict__ diag, T* __restrict__ coef, Ctl* ctl,
                                                     const T* __restrict__ pin, T* __restrict__ pout,
-                                                    double* __restrict__ partials, const T* __restrict__ rec)
+                                                    double* __restrict__ partials, const T* __restrict__ rec,
+                                                    uint4* __restrict__ code, int* __restrict__ nslot, int cc8)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     double lam = 0.0, dn = 0.0, dd = 0.0;
@@ -1322,6 +1409,9 @@ __global__ void __launch_bounds__(RHS_T) k_rhs_diag(Params<T> P, T inv_dt, const
         T sr = 0, sd = 0, sp = 0;
         int n = cnt[i];
         T* __restrict__ crow = coef ? coef + nb_base(i, ncap) : nullptr;
+        // code mode (sweep_row): the factors go out as (code, factor) slots instead of in list order
+        CodeWriter<T> cw(code, coef, cc8, i);
+        if (code) crow = nullptr;
 #ifndef SISPH_RHS_VST
 #define SISPH_RHS_VST 1   // B200, C5: 1061 -> 904 us per launch
 #endif
@@ -1354,7 +1444,9 @@ __global__ void __launch_bounds__(RHS_T) k_rhs_diag(Params<T> P, T inv_dt, const
             if (crow) crow[nb_off(k)] = f;
 #endif
             if (pin) sp += f * pin[j];                   // first sweep: sum_j fac_ij p^0_j
+            if (code) cw.push(j, f);
         });
+        if (code) cw.finish(nslot);
         sr *= -P.dwk * inv_dt;
         const T scale = T(4) * P.dwk * frcp(rhoi);
         sd *= scale;
@@ -1455,6 +1547,9 @@ template <class T> struct PpeDesc {
     const uint8_t* fs;
     const int* nbr;
     const T* coef;      // stored per-pair factor (nullptr: matrix-free)
+    const uint4* code;  // the sweep's 16-bit list (CodeWriter; nullptr: the 32-bit list)
+    const int* nslot;   // its slot count per row
+    int cc8;            // 8-slot chunks per row
     T* pA;
     T* pB;
     double tol;
@@ -1537,6 +1632,8 @@ template <class T, int D>
 __global__ void __launch_bounds__(256) k_ppe_wall(Params<T> P, const PpeDesc<T>* __restrict__ dsc,
                                                   const int* __restrict__ cnt, int ncap, const Ctl* ctl)
 {
+    pdl_trigger();
+    pdl_wait();
     if (ctl->done) return;
     const int t = blockIdx.x * blockDim.x + threadIdx.x, w = t / WL;
     if (w >= P.Nwo) return;
@@ -1564,6 +1661,9 @@ constexpr int SWEEP_T = SISPH_SWEEP_T;
 #ifndef SISPH_SWEEP_PF
 #define SISPH_SWEEP_PF 4
 #endif
+#ifndef SISPH_SWEEP_G
+#define SISPH_SWEEP_G 1   // 2: measured slower on C2 (1.67 -> 1.88 ms), equal on C4 / C5
+#endif
 #ifndef SISPH_SWEEP_MINB
 #define SISPH_SWEEP_MINB 4
 #endif
@@ -1575,7 +1675,9 @@ __device__ __forceinline__ T sweep_row(const Params<T>& P, int i, const V4<T>* _
                                        const T* __restrict__ rho, const uint8_t* __restrict__ fs,
                                        const int* __restrict__ nbr, const int* __restrict__ cnt, int ncap,
                                        const T* __restrict__ coef, const T* __restrict__ rhs,
-                                       const T* __restrict__ diag, const T* pin)
+                                       const T* __restrict__ diag, const T* pin,
+                                       const uint4* __restrict__ code = nullptr,
+                                       const int* __restrict__ nslot = nullptr, int cc8 = 0)
 {
     const T pold = pin[i];
     T pnew = fs[i] == 2 ? pold : T(0);                 // R34 outlet rows keep their frozen p
@@ -1584,15 +1686,76 @@ __device__ __forceinline__ T sweep_row(const Params<T>& P, int i, const V4<T>* _
         const T rhoi = rho[i];
         T s = 0;
         const int n = cnt[i];
-        if (STORED) {
-            const size_t b = nb_base(i, ncap);
+        const size_t b = nb_base(i, ncap);
+        bool wide = true;
+        if constexpr (STORED) {
+            if (code) {
+            // code mode (CodeWriter): 2 + 4 bytes per slot instead of 4 + 4 per pair.  Each
+            // iteration decodes 8 slots without a branch, gathers their 8 p_j, then sums in
+            // slot order; the code chunk and the two factor chunks of the iteration DIST
+            // ahead are in flight meanwhile.
+            wide = false;
+            constexpr int DIST = (PFD >= 4 && sizeof(T) == 4) ? 2 : 1;
+            const int ns = nslot[i];
+            const T* __restrict__ crow = coef + nb_base(i, 8 * cc8);
+            uint4 cq[DIST];
+            T fq[DIST][8];
+#pragma unroll
+            for (int q = 0; q < DIST; q++) {
+                const bool ok = 8 * q < ns;
+                cq[q] = ok ? LDLIST(code + code_at(i, cc8, q)) : make_uint4(0, 0, 0, 0);
+                ld_slots8(crow, 8 * q, ok, fq[q]);
+            }
+            int prev = i, hi = 0;
+            bool pend = false;
+            for (int c = 0; c < ns; c += 8) {
+                const int cn = c + 8 * DIST;
+                const bool okn = cn < ns;
+                const uint4 cx = okn ? LDLIST(code + code_at(i, cc8, cn >> 3)) : make_uint4(0, 0, 0, 0);
+                T fx[8];
+                ld_slots8(crow, cn, okn, fx);
+                const unsigned wv[4] = {cq[0].x, cq[0].y, cq[0].z, cq[0].w};
+                int jj[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
+                    const unsigned cu = (wv[u >> 1] >> (16 * (u & 1))) & 0xFFFFu;
+                    const int v = (int)(short)cu >> 1;
+                    const bool isA = !pend && (cu & 1u);
+                    const int jr = prev + (pend ? (int)(((unsigned)hi << 16) | cu) : v);
+                    jj[u] = isA ? i : jr;
+                    prev = isA ? prev : jr;
+                    hi = v;
+                    pend = isA;
+                }
+                T pj[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++) pj[u] = ldp<COH>(pin + jj[u]);
+#pragma unroll
+                for (int u = 0; u < 8; u++) s += fq[0][u] * pj[u];
+#pragma unroll
+                for (int q = 0; q < DIST - 1; q++) {
+                    cq[q] = cq[q + 1];
+#pragma unroll
+                    for (int e = 0; e < 8; e++) fq[q][e] = fq[q + 1][e];
+                }
+                cq[DIST - 1] = cx;
+#pragma unroll
+                for (int e = 0; e < 8; e++) fq[DIST - 1][e] = fx[e];
+            }
+            }
+        }
+        if (STORED && wide) {
             const int4* __restrict__ qi = reinterpret_cast<const int4*>(nbr + b);
             if constexpr (PFD > 0) {
             // software pipelining: a register ring keeps the index + factor loads of the next
             // PD chunks in flight while this chunk's p_j are gathered (B200: the streamed
             // HBM traffic needs more bytes in flight per SM than one chunk per row gives;
             // PD = 4 at a 64-register cap measured best, 0.92 of the measured HBM bandwidth)
+            // G chunks per iteration: their 4G gathers are all issued before the sums
+            // consume them (in entry order, so the result is unchanged): the dependent
+            // chain of a row is n / 4G gather latencies, not n / 4
             constexpr int PD = PFD;
+            constexpr int G = (PD >= 4 && PD % SISPH_SWEEP_G == 0) ? SISPH_SWEEP_G : 1;
             int4 vr[PD];
             T fr[PD][4];
 #pragma unroll
@@ -1602,24 +1765,44 @@ __device__ __forceinline__ T sweep_row(const Params<T>& P, int i, const V4<T>* _
                 if (c < n) ld_chunk4(coef + b + ((size_t)(c >> 2) * 32 << 2), fr[q]);
                 else fr[q][0] = fr[q][1] = fr[q][2] = fr[q][3] = T(0);
             }
-            for (int c = 0; c < n; c += 4) {
-                const int cn = c + 4 * PD;
-                const int4 vnew = cn < n ? LDLIST(qi + (size_t)(cn >> 2) * 32) : make_int4(i, i, i, i);
-                T fnew[4] = {T(0), T(0), T(0), T(0)};
-                if (cn < n) ld_chunk4(coef + b + ((size_t)(cn >> 2) * 32 << 2), fnew);
-                s += fr[0][0] * ldp<COH>(pin + vr[0].x);
-                if (c + 1 < n) s += fr[0][1] * ldp<COH>(pin + vr[0].y);
-                if (c + 2 < n) s += fr[0][2] * ldp<COH>(pin + vr[0].z);
-                if (c + 3 < n) s += fr[0][3] * ldp<COH>(pin + vr[0].w);
+            for (int c = 0; c < n; c += 4 * G) {
+                int4 vnew[G];
+                T fnew[G][4];
 #pragma unroll
-                for (int q = 0; q < PD - 1; q++) {
-                    vr[q] = vr[q + 1];
-#pragma unroll
-                    for (int e = 0; e < 4; e++) fr[q][e] = fr[q + 1][e];
+                for (int g = 0; g < G; g++) {
+                    const int cn = c + 4 * (PD + g);
+                    vnew[g] = cn < n ? LDLIST(qi + (size_t)(cn >> 2) * 32) : make_int4(i, i, i, i);
+                    fnew[g][0] = fnew[g][1] = fnew[g][2] = fnew[g][3] = T(0);
+                    if (cn < n) ld_chunk4(coef + b + ((size_t)(cn >> 2) * 32 << 2), fnew[g]);
                 }
-                vr[PD - 1] = vnew;
+                T pv[G][4];
 #pragma unroll
-                for (int e = 0; e < 4; e++) fr[PD - 1][e] = fnew[e];
+                for (int g = 0; g < G; g++) {
+                    const int cg0 = c + 4 * g;
+                    pv[g][0] = cg0 < n ? ldp<COH>(pin + vr[g].x) : T(0);
+                    pv[g][1] = cg0 + 1 < n ? ldp<COH>(pin + vr[g].y) : T(0);
+                    pv[g][2] = cg0 + 2 < n ? ldp<COH>(pin + vr[g].z) : T(0);
+                    pv[g][3] = cg0 + 3 < n ? ldp<COH>(pin + vr[g].w) : T(0);
+                }
+#pragma unroll
+                for (int g = 0; g < G; g++) {
+                    const int cg0 = c + 4 * g;
+#pragma unroll
+                    for (int e = 0; e < 4; e++)
+                        if (cg0 + e < n) s += fr[g][e] * pv[g][e];
+                }
+#pragma unroll
+                for (int q = 0; q < PD - G; q++) {
+                    vr[q] = vr[q + G];
+#pragma unroll
+                    for (int e = 0; e < 4; e++) fr[q][e] = fr[q + G][e];
+                }
+#pragma unroll
+                for (int g = 0; g < G; g++) {
+                    vr[PD - G + g] = vnew[g];
+#pragma unroll
+                    for (int e = 0; e < 4; e++) fr[PD - G + g][e] = fnew[g][e];
+                }
             }
             } else {
             for (int c = 0; c < n; c += 4) {
@@ -1633,7 +1816,7 @@ __device__ __forceinline__ T sweep_row(const Params<T>& P, int i, const V4<T>* _
                 if (c + 3 < n) s += f[3] * ldp<COH>(pin + v.w);
             }
             }
-        } else {
+        } else if (!STORED) {
             const V4<T> xi = ld4(pos + i);
             for_nbrs(nbr, ncap, i, n, [&](int j) {
                 V4<T> xj = ld4(pos + j);
@@ -1669,6 +1852,8 @@ __global__ void __launch_bounds__(SWEEP_T, sweep_minb<T>()) k_sweep(Params<T> P,
                                                    double* __restrict__ partials, int defer,
                                                    cudaGraphConditionalHandle hcond, int use_h)
 {
+    pdl_trigger();
+    pdl_wait();
     if (ctl->done) {
         if (use_h && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(hcond, 0u);
         return;
@@ -1678,6 +1863,9 @@ __global__ void __launch_bounds__(SWEEP_T, sweep_minb<T>()) k_sweep(Params<T> P,
     const uint8_t* __restrict__ fs = dsc->fs;
     const int* __restrict__ nbr = dsc->nbr;
     const T* __restrict__ coef = dsc->coef;
+    const uint4* __restrict__ code = dsc->code;
+    const int* __restrict__ nslot = dsc->nslot;
+    const int cc8 = dsc->cc8;
     T* pA = dsc->pA;
     T* pB = dsc->pB;
     const int kit = ctl->iter;
@@ -1688,7 +1876,7 @@ __global__ void __launch_bounds__(SWEEP_T, sweep_minb<T>()) k_sweep(Params<T> P,
     bool bad = false;
     if (i < P.Nfo) {
         const T pold = pin[i];
-        const T pnew = sweep_row<T, D, STORED>(P, i, pos, rho, fs, nbr, cnt, ncap, coef, rhs, diag, pin);
+        const T pnew = sweep_row<T, D, STORED>(P, i, pos, rho, fs, nbr, cnt, ncap, coef, rhs, diag, pin, code, nslot, cc8);
         pout[i] = pnew;
         if (P.mean_free) {
             // R32: (sum, count) of the live rows; k_mean_fix removes the mean and decides
@@ -1784,6 +1972,8 @@ __global__ void __launch_bounds__(SWEEP_T) k_mean_fix(Params<T> P, const PpeDesc
                                                       double* __restrict__ partials, int defer,
                                                       cudaGraphConditionalHandle hcond, int use_h)
 {
+    pdl_trigger();
+    pdl_wait();
     if (ctl->done) {
         if (use_h && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(hcond, 0u);
         return;
@@ -1920,7 +2110,7 @@ __global__ void k_decide(Ctl* ctl, double tol, int min_it, int max_it, double cs
 // level differences in the residual only).
 // ===========================================================================
 template <class T, int D, bool STORED>
-__global__ void __launch_bounds__(SWEEP_T) k_ppe_persistent(Params<T> P, const PpeDesc<T>* __restrict__ dsc,
+__global__ void __launch_bounds__(SWEEP_T, 4) k_ppe_persistent(Params<T> P, const PpeDesc<T>* __restrict__ dsc,
                                                             const T* __restrict__ rhs, const T* __restrict__ diag,
                                                             const int* __restrict__ cnt, int ncap, Ctl* ctl,
                                                             double* __restrict__ partials)
@@ -1931,6 +2121,9 @@ __global__ void __launch_bounds__(SWEEP_T) k_ppe_persistent(Params<T> P, const P
     const uint8_t* __restrict__ fs = dsc->fs;
     const int* __restrict__ nbr = dsc->nbr;
     const T* __restrict__ coef = dsc->coef;
+    const uint4* __restrict__ code = dsc->code;
+    const int* __restrict__ nslot = dsc->nslot;
+    const int cc8 = dsc->cc8;
     T* pA = dsc->pA;
     T* pB = dsc->pB;
     const double tol = dsc->tol;
@@ -1939,11 +2132,16 @@ __global__ void __launch_bounds__(SWEEP_T) k_ppe_persistent(Params<T> P, const P
     const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     __shared__ double sn[SWEEP_T / 32], sd[SWEEP_T / 32];
-    for (;;) {
-        if (vc->done) break;                       // every block reads it after the same grid sync
-        const int kit = vc->iter;
-        T* pin = (kit & 1) ? pB : pA;
-        T* pout = (kit & 1) ? pA : pB;
+    __shared__ int done_s;
+    // two grid barriers per iteration: walls | sweep + block partials (per parity) | every
+    // block sums the partials in block order and takes the (identical) stop decision itself
+    int kit = vc->iter;
+    bool done = vc->done != 0;
+    const double lam = __longlong_as_double((long long)vc->lambda_bits);
+    while (!done) {
+        const int par = kit & 1;
+        T* pin = par ? pB : pA;
+        T* pout = par ? pA : pB;
         for (int q = gt / WL; q < P.Nwo; q += gs / WL)
             wall_pressure_row<T, D, true>(P, q, pos, rho, nbr, cnt, ncap, pin, gt % WL);
         grid.sync();
@@ -1951,7 +2149,7 @@ __global__ void __launch_bounds__(SWEEP_T) k_ppe_persistent(Params<T> P, const P
         bool bad = false;
         for (int i = gt; i < P.Nfo; i += gs) {
             const T pold = pin[i];
-            const T pnew = sweep_row<T, D, STORED, true>(P, i, pos, rho, fs, nbr, cnt, ncap, coef, rhs, diag, pin);
+            const T pnew = sweep_row<T, D, STORED, true>(P, i, pos, rho, fs, nbr, cnt, ncap, coef, rhs, diag, pin, code, nslot, cc8);
             pout[i] = pnew;
             dn += fabs((double)pnew - (double)pold);
             dd += fs[i] == 2 ? 0.0 : fabs((double)pnew);
@@ -1966,48 +2164,54 @@ __global__ void __launch_bounds__(SWEEP_T) k_ppe_persistent(Params<T> P, const P
             if (anybad) atomicExch(&ctl->nonfinite, 1);
         }
         __syncthreads();
+        double* part = partials + 2 * (size_t)gridDim.x * par;
         if (threadIdx.x == 0) {
             double a = 0, b = 0;
             for (int q = 0; q < SWEEP_T / 32; q++) {
                 a += sn[q];
                 b += sd[q];
             }
-            partials[2 * blockIdx.x] = a;
-            partials[2 * blockIdx.x + 1] = b;
+            part[2 * blockIdx.x] = a;
+            part[2 * blockIdx.x + 1] = b;
         }
         grid.sync();
-        if (blockIdx.x == 0) {
-            double a = 0, b = 0;
-            for (int q = threadIdx.x; q < (int)gridDim.x; q += blockDim.x) {
-                a += partials[2 * q];
-                b += partials[2 * q + 1];
+        // the partials of this parity are next written two iterations on, after two more barriers
+        double a = 0, b = 0;
+        for (int q = threadIdx.x; q < (int)gridDim.x; q += blockDim.x) {
+            a += __ldcg(part + 2 * q);
+            b += __ldcg(part + 2 * q + 1);
+        }
+        a = warp_sum(a);
+        b = warp_sum(b);
+        __syncthreads();                            // sn / sd of the sweep reduction are consumed
+        if (lane == 0) {
+            sn[w] = a;
+            sd[w] = b;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double num = 0, den = 0;
+            for (int q = 0; q < SWEEP_T / 32; q++) {
+                num += sn[q];
+                den += sd[q];
             }
-            a = warp_sum(a);
-            b = warp_sum(b);
-            __syncthreads();
-            if (lane == 0) {
-                sn[w] = a;
-                sd[w] = b;
-            }
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                double num = 0, den = 0;
-                for (int q = 0; q < SWEEP_T / 32; q++) {
-                    num += sn[q];
-                    den += sd[q];
-                }
-                num *= dsc->cscale;
-                den *= dsc->cscale;
-                const double lam = __longlong_as_double((long long)vc->lambda_bits);
-                const double dmax = den > lam ? den : lam;
-                const double res = num == 0.0 ? 0.0 : (dmax > 0.0 ? num / dmax : INFINITY);
-                const int k1 = kit + 1;
+            num *= dsc->cscale;
+            den *= dsc->cscale;
+            const double dmax = den > lam ? den : lam;
+            const double res = num == 0.0 ? 0.0 : (dmax > 0.0 ? num / dmax : INFINITY);
+            const int k1 = kit + 1;
+            const int nonf = __ldcg(&ctl->nonfinite);
+            const int dn_ = ((k1 >= min_it && res < tol) || k1 >= max_it || nonf) ? 1 : 0;
+            done_s = dn_;
+            if (blockIdx.x == 0) {
                 vc->residual = res;
                 vc->iter = k1;
-                vc->done = ((k1 >= min_it && res < tol) || k1 >= max_it || vc->nonfinite) ? 1 : 0;
+                vc->done = dn_;
             }
         }
-        grid.sync();
+        __syncthreads();
+        done = done_s != 0;
+        kit++;
     }
 }
 
@@ -2040,6 +2244,9 @@ __global__ void __launch_bounds__(CLUSTER_T) k_ppe_cluster(Params<T> P, const Pp
     const uint8_t* __restrict__ fs = dsc->fs;
     const int* __restrict__ nbr = dsc->nbr;
     const T* __restrict__ coef = dsc->coef;
+    const uint4* __restrict__ code = dsc->code;
+    const int* __restrict__ nslot = dsc->nslot;
+    const int cc8 = dsc->cc8;
     T* pA = dsc->pA;
     T* pB = dsc->pB;
     volatile Ctl* vc = ctl;
@@ -2105,7 +2312,7 @@ __global__ void __launch_bounds__(CLUSTER_T) k_ppe_cluster(Params<T> P, const Pp
         for (int i = gt; i < P.Nfo; i += gs) {
             const T pold = pin[i];
             const T pnew =
-                sweep_row<T, D, STORED, true, 2>(P, i, pos, rho, fs, nbr, cnt, ncap, coef, rhs, diag, pin);
+                sweep_row<T, D, STORED, true, 2>(P, i, pos, rho, fs, nbr, cnt, ncap, coef, rhs, diag, pin, code, nslot, cc8);
             pout[i] = pnew;
             if (P.mean_free) {
                 const bool live = !fs[i] && diag[i] != T(0);

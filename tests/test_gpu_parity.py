@@ -438,6 +438,27 @@ def test_ppe_loop_forms_agree(name):
             assert np.array_equal(sims[m].get("PRESSURE"), sims[1].get("PRESSURE")), m
 
 
+# ------------------------------------------------------------------ the sweep's 16-bit list
+@pytest.mark.parametrize("name", ["db3d_f32", "tgv3d_f64", "hydro_f64", "tgv2d_f64"])
+@pytest.mark.parametrize("loop", [1, 4])
+def test_sweep_codes_bit_equal(name, loop, monkeypatch):
+    """Code mode (SISPH_SWEEP_CODES=1, read at create): A11 writes each fluid row's
+    list as (16-bit step code, factor) slots with two-slot long steps (z-rows, walls,
+    periodic images) and the sweep decodes them -- the same entries in the same
+    order, so the solve is bitwise equal to the 32-bit sweep."""
+    case = CASES[name]
+    sims = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("SISPH_SWEEP_CODES", flag)
+        sims[flag] = gpu_sim(case, ppe_loop=loop)
+    for _ in range(3):
+        r = {k: s.step(case.dt) for k, s in sims.items()}
+        assert r["0"].iters == r["1"].iters
+        assert r["0"].residual == r["1"].residual
+    for fld in ("PRESSURE", "VELOCITY", "POSITION"):
+        assert np.array_equal(sims["1"].get(fld), sims["0"].get(fld)), fld
+
+
 # ------------------------------------------------------------------ reading R32: mean-free Jacobi
 @pytest.mark.parametrize("name", ["tgv2d_f64", "tgv3d_f64", "hydro_f64", "db2d_f64", "tgv3d_f32"])
 def test_mean_free_solve_parity(name):
