@@ -1622,6 +1622,7 @@ template <class T, int D> struct Engine : EngineBase {
         const int grid = std::max(1, std::min(pgrid_max, nblk(std::max((long)Nfo, (long)Nwo * WL), SWEEP_T)));
         int cap = P.cap;
         void* args[] = {&P, &ddesc, &rhs, &diag, &cnt, &cap, &ctl, &partials};
+        SCK(cudaMemsetAsync(&ctl->gbar, 0, sizeof(unsigned int), st));
         ++nlaunch;
         SCK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(SWEEP_T), args, 0, st));
         return SISPH_OK;
@@ -1750,6 +1751,24 @@ template <class T, int D> struct Engine : EngineBase {
             SRET(launch_persistent());
             SCK(cudaMemcpyAsync(hctl, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
             SCK(cudaStreamSynchronize(st));
+#ifdef SISPH_PERS_PROF
+            {
+                std::vector<unsigned long long> hp(4096 * 6);
+                SCK(cudaMemcpyFromSymbol(hp.data(), g_pers_prof, hp.size() * sizeof(unsigned long long)));
+                const int nb = std::max(1, std::min(pgrid_max, nblk(std::max((long)Nfo, (long)Nwo * WL), SWEEP_T)));
+                const int its = std::max(hctl->iter - launched, 1);
+                double mean[5] = {0}, mx[5] = {0};
+                for (int b = 0; b < nb; b++)
+                    for (int k = 0; k < 5; k++) {
+                        const double v = hp[b * 6 + k] * 1e-3 / its;
+                        mean[k] += v / nb;
+                        mx[k] = std::max(mx[k], v);
+                    }
+                fprintf(stderr, "pers its=%d blocks=%d us/it mean|max: sweep %.2f|%.2f bar2 %.2f|%.2f walls+decide %.2f|%.2f "
+                        "bar1 %.2f|%.2f - %.2f|%.2f\n", its, nb, mean[0], mx[0], mean[1], mx[1], mean[2], mx[2],
+                        mean[3], mx[3], mean[4], mx[4]);
+            }
+#endif
         } else if (mode == 2) {
             // one launch: WHILE (not done) { wall pressure; sweep }  (sweeps after the
             // decision never run; the host waits once)

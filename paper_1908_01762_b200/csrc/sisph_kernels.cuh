@@ -27,7 +27,7 @@ struct Ctl {
     unsigned long long pairs_fluid;  // sum of neighbour counts over fluid rows of the last build
     unsigned long long pairs_inner;  // sum of GTVF inner-list counts of the last build
     int gtvf_far;              // a particle moved more than skin/2 during the GTVF sub-steps
-    int pad2;
+    unsigned int gbar;         // arrivals at the persistent PPE kernel's grid barrier (reset per launch)
     unsigned long long umax2_bits;   // max |u~|^2 over fluid (ordered bits of a non-negative double)
     double red[4];             // slab ranks: local (sum |dp|, sum |p|, nonfinite) of a sweep, allreduced
     unsigned long long fmax2_bits;   // max |f^n|^2 of the last correct (adaptive dt)
@@ -389,6 +389,22 @@ __device__ __forceinline__ void ld_chunk4(const float* p, float (&f)[4])
     f[1] = v.y;
     f[2] = v.z;
     f[3] = v.w;
+}
+__device__ __forceinline__ void ld_chunk4_l1(const float* p, float (&f)[4])
+{
+    const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+    f[0] = v.x;
+    f[1] = v.y;
+    f[2] = v.z;
+    f[3] = v.w;
+}
+__device__ __forceinline__ void ld_chunk4_l1(const double* p, double (&f)[4])
+{
+    const double2 a = __ldg(reinterpret_cast<const double2*>(p)), b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+    f[0] = a.x;
+    f[1] = a.y;
+    f[2] = b.x;
+    f[3] = b.y;
 }
 __device__ __forceinline__ void ld_chunk4(const double* p, double (&f)[4])
 {
@@ -1661,6 +1677,15 @@ constexpr int SWEEP_T = SISPH_SWEEP_T;
 #ifndef SISPH_SWEEP_PF
 #define SISPH_SWEEP_PF 4
 #endif
+#ifndef SISPH_PERS_B
+#define SISPH_PERS_B -4   // the persistent loop's sweep_row form (< 0: batched gathers, no ring)
+#endif
+#ifndef SISPH_CLUSTER_B
+#define SISPH_CLUSTER_B -2
+#endif
+#ifndef SISPH_PERS_MINB
+#define SISPH_PERS_MINB 3
+#endif
 #ifndef SISPH_SWEEP_G
 #define SISPH_SWEEP_G 1   // 2: measured slower on C2 (1.67 -> 1.88 ms), equal on C4 / C5
 #endif
@@ -1746,7 +1771,40 @@ __device__ __forceinline__ T sweep_row(const Params<T>& P, int i, const V4<T>* _
         }
         if (STORED && wide) {
             const int4* __restrict__ qi = reinterpret_cast<const int4*>(nbr + b);
-            if constexpr (PFD > 0) {
+            if constexpr (PFD < 0) {
+            // latency-bound form (persistent / cluster loops, L2-resident lists): the list and
+            // factor chunks are read through L1 (__ldg: a block's rows are re-read every
+            // sweep and stay L1-resident on small problems); B = -PFD
+            // chunks per iteration, their 4B gathers all issued before the sums consume them
+            // in entry order; entries past the row end gather p_i with a zero factor
+            constexpr int B = -PFD;
+            for (int c = 0; c < n; c += 4 * B) {
+                int4 v[B];
+                T f[B][4];
+#pragma unroll
+                for (int g = 0; g < B; g++) {
+                    const int cg0 = c + 4 * g;
+                    v[g] = cg0 < n ? __ldg(qi + (size_t)(cg0 >> 2) * 32) : make_int4(i, i, i, i);
+                    f[g][0] = f[g][1] = f[g][2] = f[g][3] = T(0);
+                    if (cg0 < n) ld_chunk4_l1(coef + b + ((size_t)(cg0 >> 2) * 32 << 2), f[g]);
+                }
+                T pv[B][4];
+#pragma unroll
+                for (int g = 0; g < B; g++) {
+                    const int cg0 = c + 4 * g;
+                    pv[g][0] = ldp<COH>(pin + (cg0 < n ? v[g].x : i));
+                    pv[g][1] = ldp<COH>(pin + (cg0 + 1 < n ? v[g].y : i));
+                    pv[g][2] = ldp<COH>(pin + (cg0 + 2 < n ? v[g].z : i));
+                    pv[g][3] = ldp<COH>(pin + (cg0 + 3 < n ? v[g].w : i));
+                }
+#pragma unroll
+                for (int g = 0; g < B; g++) {
+                    const int cg0 = c + 4 * g;
+#pragma unroll
+                    for (int e = 0; e < 4; e++) s += (cg0 + e < n ? f[g][e] : T(0)) * pv[g][e];
+                }
+            }
+            } else if constexpr (PFD > 0) {
             // software pipelining: a register ring keeps the index + factor loads of the next
             // PD chunks in flight while this chunk's p_j are gathered (B200: the streamed
             // HBM traffic needs more bytes in flight per SM than one chunk per row gives;
@@ -1775,21 +1833,22 @@ __device__ __forceinline__ T sweep_row(const Params<T>& P, int i, const V4<T>* _
                     fnew[g][0] = fnew[g][1] = fnew[g][2] = fnew[g][3] = T(0);
                     if (cn < n) ld_chunk4(coef + b + ((size_t)(cn >> 2) * 32 << 2), fnew[g]);
                 }
+                // entries past the row end gather p_i (a valid slot) with a zero factor:
+                // adding +-0 leaves s unchanged, and the loads issue without predicates
                 T pv[G][4];
 #pragma unroll
                 for (int g = 0; g < G; g++) {
                     const int cg0 = c + 4 * g;
-                    pv[g][0] = cg0 < n ? ldp<COH>(pin + vr[g].x) : T(0);
-                    pv[g][1] = cg0 + 1 < n ? ldp<COH>(pin + vr[g].y) : T(0);
-                    pv[g][2] = cg0 + 2 < n ? ldp<COH>(pin + vr[g].z) : T(0);
-                    pv[g][3] = cg0 + 3 < n ? ldp<COH>(pin + vr[g].w) : T(0);
+                    pv[g][0] = ldp<COH>(pin + (cg0 < n ? vr[g].x : i));
+                    pv[g][1] = ldp<COH>(pin + (cg0 + 1 < n ? vr[g].y : i));
+                    pv[g][2] = ldp<COH>(pin + (cg0 + 2 < n ? vr[g].z : i));
+                    pv[g][3] = ldp<COH>(pin + (cg0 + 3 < n ? vr[g].w : i));
                 }
 #pragma unroll
                 for (int g = 0; g < G; g++) {
                     const int cg0 = c + 4 * g;
 #pragma unroll
-                    for (int e = 0; e < 4; e++)
-                        if (cg0 + e < n) s += fr[g][e] * pv[g][e];
+                    for (int e = 0; e < 4; e++) s += (cg0 + e < n ? fr[g][e] : T(0)) * pv[g][e];
                 }
 #pragma unroll
                 for (int q = 0; q < PD - G; q++) {
@@ -2103,19 +2162,44 @@ __global__ void k_decide(Ctl* ctl, double tol, int min_it, int max_it, double cs
 // ===========================================================================
 // The whole PPE loop in ONE cooperative launch (small problems, where the
 // per-sweep launches and their latency dominate: BASELINE configs[0-1]).
-// Per sweep: walls from p^k (grid-stride), grid sync, fluid rows (grid-
-// stride) + block partials, grid sync, block 0 sums the partials in a fixed
-// order and decides eq:convergence, grid sync.  Same row arithmetic as
+// Per sweep: walls from p^k (grid-stride), grid barrier, fluid rows (grid-
+// stride) + block partials (per parity), grid barrier, then every block sums
+// the partials in block order and takes the same eq:convergence decision (no
+// third barrier; block 0 publishes it to ctl).  Same row arithmetic as
 // k_sweep; the sums are grouped per block of the grid-stride loop (rounding-
 // level differences in the residual only).
 // ===========================================================================
+#ifdef SISPH_PERS_PROF
+__device__ unsigned long long g_pers_prof[4096 * 6];   // debug build: per-block phase times (ns)
+#endif
+// Grid barrier of the persistent PPE kernel: a monotone arrival counter (reset
+// before the launch), thread 0 of every block adds 1 with release semantics and
+// spins until the counter reaches (barrier number) x (blocks) with acquire
+// loads.  Unlike cg::grid_group::sync it does not invalidate L1: every value
+// another block wrote during the kernel (pressures, partials, the non-finite
+// flag) is read L2-coherent (ldp<true>, __ldcg), the rest is read-only.
+__device__ __forceinline__ void pgrid_sync(unsigned int* cnt, unsigned int target)
+{
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
+        unsigned int v;
+        for (;;) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+            if ((int)(v - target) >= 0) break;
+        }
+    }
+    __syncthreads();
+}
+
 template <class T, int D, bool STORED>
-__global__ void __launch_bounds__(SWEEP_T, 4) k_ppe_persistent(Params<T> P, const PpeDesc<T>* __restrict__ dsc,
+__global__ void __launch_bounds__(SWEEP_T, SISPH_PERS_MINB) k_ppe_persistent(Params<T> P, const PpeDesc<T>* __restrict__ dsc,
                                                             const T* __restrict__ rhs, const T* __restrict__ diag,
                                                             const int* __restrict__ cnt, int ncap, Ctl* ctl,
                                                             double* __restrict__ partials)
 {
-    cg::grid_group grid = cg::this_grid();
+    unsigned int* gbar = &ctl->gbar;
+    unsigned int nbar = 0;
     const V4<T>* __restrict__ pos = dsc->pos;
     const T* __restrict__ rho = dsc->rho;
     const uint8_t* __restrict__ fs = dsc->fs;
@@ -2131,6 +2215,9 @@ __global__ void __launch_bounds__(SWEEP_T, 4) k_ppe_persistent(Params<T> P, cons
     volatile Ctl* vc = ctl;
     const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    // wall rows block-cyclic (every block takes its share, WL lanes each): the wall phase
+    // runs beside the decision in every block instead of in the first blocks only
+    const int wq0 = (threadIdx.x / WL) * gridDim.x + blockIdx.x, wqs = (blockDim.x / WL) * gridDim.x;
     __shared__ double sn[SWEEP_T / 32], sd[SWEEP_T / 32];
     __shared__ int done_s;
     // two grid barriers per iteration: walls | sweep + block partials (per parity) | every
@@ -2138,18 +2225,31 @@ __global__ void __launch_bounds__(SWEEP_T, 4) k_ppe_persistent(Params<T> P, cons
     int kit = vc->iter;
     bool done = vc->done != 0;
     const double lam = __longlong_as_double((long long)vc->lambda_bits);
+#ifdef SISPH_PERS_PROF
+    unsigned long long tp[6] = {0, 0, 0, 0, 0, 0}, tq0 = 0, tq1 = 0;
+#define PPROF(k) if (threadIdx.x == 0) { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tq1)); if (k) tp[k - 1] += tq1 - tq0; tq0 = tq1; }
+#else
+#define PPROF(k)
+#endif
+    // prologue: the walls of p^kit; then per iteration: sweep | walls of p^{k+1} (speculative:
+    // after the last sweep they land in the final buffer's wall slots, which the solve's
+    // epilogue overwrites with the walls the last sweep used) overlapped with the decision |
+    if (!done) {
+        T* pin = (kit & 1) ? pB : pA;
+        for (int q = wq0; q < P.Nwo; q += wqs)
+            wall_pressure_row<T, D, true>(P, q, pos, rho, nbr, cnt, ncap, pin, threadIdx.x % WL);
+        pgrid_sync(gbar, (++nbar) * gridDim.x);
+    }
     while (!done) {
+        PPROF(0);
         const int par = kit & 1;
         T* pin = par ? pB : pA;
         T* pout = par ? pA : pB;
-        for (int q = gt / WL; q < P.Nwo; q += gs / WL)
-            wall_pressure_row<T, D, true>(P, q, pos, rho, nbr, cnt, ncap, pin, gt % WL);
-        grid.sync();
         double dn = 0.0, dd = 0.0;
         bool bad = false;
         for (int i = gt; i < P.Nfo; i += gs) {
             const T pold = pin[i];
-            const T pnew = sweep_row<T, D, STORED, true>(P, i, pos, rho, fs, nbr, cnt, ncap, coef, rhs, diag, pin, code, nslot, cc8);
+            const T pnew = sweep_row<T, D, STORED, true, SISPH_PERS_B>(P, i, pos, rho, fs, nbr, cnt, ncap, coef, rhs, diag, pin, code, nslot, cc8);
             pout[i] = pnew;
             dn += fabs((double)pnew - (double)pold);
             dd += fs[i] == 2 ? 0.0 : fabs((double)pnew);
@@ -2174,16 +2274,20 @@ __global__ void __launch_bounds__(SWEEP_T, 4) k_ppe_persistent(Params<T> P, cons
             part[2 * blockIdx.x] = a;
             part[2 * blockIdx.x + 1] = b;
         }
-        grid.sync();
+        __syncthreads();
+        PPROF(1);
+        pgrid_sync(gbar, (++nbar) * gridDim.x);
+        PPROF(2);
         // the partials of this parity are next written two iterations on, after two more barriers
         double a = 0, b = 0;
         for (int q = threadIdx.x; q < (int)gridDim.x; q += blockDim.x) {
             a += __ldcg(part + 2 * q);
             b += __ldcg(part + 2 * q + 1);
         }
+        for (int q = wq0; q < P.Nwo; q += wqs)
+            wall_pressure_row<T, D, true>(P, q, pos, rho, nbr, cnt, ncap, pout, threadIdx.x % WL);
         a = warp_sum(a);
         b = warp_sum(b);
-        __syncthreads();                            // sn / sd of the sweep reduction are consumed
         if (lane == 0) {
             sn[w] = a;
             sd[w] = b;
@@ -2212,7 +2316,15 @@ __global__ void __launch_bounds__(SWEEP_T, 4) k_ppe_persistent(Params<T> P, cons
         __syncthreads();
         done = done_s != 0;
         kit++;
+        PPROF(3);
+        if (!done) pgrid_sync(gbar, (++nbar) * gridDim.x);   // every block takes the same decision
+        PPROF(4);
     }
+#ifdef SISPH_PERS_PROF
+    if (threadIdx.x == 0)
+        for (int k = 0; k < 5; k++) g_pers_prof[blockIdx.x * 6 + k] = tp[k];
+#endif
+#undef PPROF
 }
 
 // ===========================================================================
@@ -2312,7 +2424,7 @@ __global__ void __launch_bounds__(CLUSTER_T) k_ppe_cluster(Params<T> P, const Pp
         for (int i = gt; i < P.Nfo; i += gs) {
             const T pold = pin[i];
             const T pnew =
-                sweep_row<T, D, STORED, true, 2>(P, i, pos, rho, fs, nbr, cnt, ncap, coef, rhs, diag, pin, code, nslot, cc8);
+                sweep_row<T, D, STORED, true, SISPH_CLUSTER_B>(P, i, pos, rho, fs, nbr, cnt, ncap, coef, rhs, diag, pin, code, nslot, cc8);
             pout[i] = pnew;
             if (P.mean_free) {
                 const bool live = !fs[i] && diag[i] != T(0);
