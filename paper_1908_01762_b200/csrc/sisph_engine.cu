@@ -203,6 +203,7 @@ template <class T, int D> struct Engine : EngineBase {
     char *sbuf[2] = {nullptr, nullptr}, *rbuf[2] = {nullptr, nullptr};
     size_t bufcap[2] = {0, 0};
     V* wtmp = nullptr;                                  // wall-block relocation staging
+    char* wstage = nullptr;                             // relocate_walls: every array's wall block
     int64_t halo_bytes = 0;                             // bytes sent by halo / migration exchanges
 
     bool dist() const { return tp != nullptr; }
@@ -215,7 +216,7 @@ template <class T, int D> struct Engine : EngineBase {
                         nbs, cnt_s, wperm_s, wstart_s, coef, dflag, dflag2, dpre, dlist[0], dlist[1], dlist[2],
                         dcnt, fsend[0], fsend[1], fsend_pre[0], fsend_pre[1], grecv, wsend[0], wsend[1], wrecv,
                         inv, sbuf[0], sbuf[1], rbuf[0], rbuf[1], wtmp, fnp, dcnt_w, ptype, ptype_alt, uout,
-                        oflag, olist, onew, code, nslot};
+                        oflag, olist, onew, code, nslot, wstage};
         if (st) cudaStreamSynchronize(st);
         for (void* q : ptrs)
             if (q) cudaFree(q);
@@ -408,9 +409,9 @@ template <class T, int D> struct Engine : EngineBase {
         // the ghost-wall count is known before the allocation
         std::vector<int> hws[2];
         if (dist() || open_x) {
-            SCK(cudaHostAlloc((void**)&hcnt, 8 * sizeof(int), cudaHostAllocDefault));
+            SCK(cudaHostAlloc((void**)&hcnt, 16 * sizeof(int), cudaHostAllocDefault));
             int rc = 0;
-            dcnt = dalloc<int>(8, err, rc);
+            dcnt = dalloc<int>(16, err, rc);
             if (rc) return rc;
         }
         if (dist()) {
@@ -453,6 +454,7 @@ template <class T, int D> struct Engine : EngineBase {
             AL(onew, int, NF)
             if (!dist()) {
                 AL(wtmp, V, NW)   // wall-block relocation staging (the slab path allocates it too)
+                AL(wstage, char, (8 * sizeof(V) + 4 * sizeof(T) + 8) * NW)
             }
         }
         if (dist()) {
@@ -460,6 +462,7 @@ template <class T, int D> struct Engine : EngineBase {
             AL(dlist[2], int, NF) AL(fsend[0], int, NF) AL(fsend[1], int, NF) AL(fsend_pre[0], int, NF)
             AL(fsend_pre[1], int, NF) AL(grecv, int, NF) AL(wsend[0], int, NW) AL(wsend[1], int, NW)
             AL(wrecv, int, NW) AL(inv, int, NT) AL(wtmp, V, NW)
+            AL(wstage, char, (8 * sizeof(V) + 4 * sizeof(T) + 8) * NW)
         }
 #undef AL
         SCK(cudaHostAlloc((void**)&hctl, sizeof(Ctl), cudaHostAllocDefault));
@@ -855,12 +858,18 @@ template <class T, int D> struct Engine : EngineBase {
         for (int f = 0; f < 2; f++) {
             SRET(ensure_buf(f, (size_t)std::max(ns[f], nr[f]) * L.rec));
         }
-        for (int f = 0; f < 2; f++) {
-            if (!ns[f]) continue;
-            PackList Lf = L;
-            Lf.shift = face_shift(f);
-            ++nlaunch, k_pack<T><<<nblk(ns[f], 256), 256, 0, st>>>(Lf, list[f], 0, ns[f], sbuf[f]);
-            halo_bytes += (int64_t)ns[f] * L.rec;
+        if (list[0] && list[1] && ns[0] + ns[1] > 0) {
+            ++nlaunch, k_pack2<T><<<nblk(ns[0] + ns[1], 256), 256, 0, st>>>(
+                           L, face_shift(0), face_shift(1), list[0], list[1], ns[0], ns[1], sbuf[0], sbuf[1]);
+            halo_bytes += (int64_t)(ns[0] + ns[1]) * L.rec;
+        } else {
+            for (int f = 0; f < 2; f++) {
+                if (!ns[f]) continue;
+                PackList Lf = L;
+                Lf.shift = face_shift(f);
+                ++nlaunch, k_pack<T><<<nblk(ns[f], 256), 256, 0, st>>>(Lf, list[f], 0, ns[f], sbuf[f]);
+                halo_bytes += (int64_t)ns[f] * L.rec;
+            }
         }
         SCK(cudaGetLastError());
         const void* sb[2] = {sbuf[0], sbuf[1]};
@@ -868,13 +877,9 @@ template <class T, int D> struct Engine : EngineBase {
         const size_t sz[2] = {(size_t)ns[0] * L.rec, (size_t)ns[1] * L.rec};
         const size_t rz[2] = {(size_t)nr[0] * L.rec, (size_t)nr[1] * L.rec};
         if (tp->sendrecv(sb, sz, rb, rz, st)) return tperr();
-        int off = 0;
-        for (int f = 0; f < 2; f++) {
-            if (nr[f])
-                ++nlaunch, k_unpack<T><<<nblk(nr[f], 256), 256, 0, st>>>(L, map ? map + off : nullptr, base_r + off,
-                                                                          nr[f], rbuf[f]);
-            off += nr[f];
-        }
+        if (nr[0] + nr[1] > 0)
+            ++nlaunch, k_unpack2<T><<<nblk(nr[0] + nr[1], 256), 256, 0, st>>>(L, map, base_r, nr[0], nr[1], rbuf[0],
+                                                                               rbuf[1]);
         SCK(cudaGetLastError());
         return SISPH_OK;
     }
@@ -912,6 +917,42 @@ template <class T, int D> struct Engine : EngineBase {
         return SISPH_OK;
     }
 
+    // stable compaction without a host wait: the count goes to dcnt[slot]
+    // (slots 8..15; read by counts_sync)
+    int compact_async(const int* flag, int nn, int v, int* out, int slot)
+    {
+        if (nn <= 0) {
+            SCK(cudaMemsetAsync(dcnt + slot, 0, sizeof(int), st));
+            return SISPH_OK;
+        }
+        const int* f01 = flag;
+        if (v >= 0) {
+            ++nlaunch, k_flag_eq<<<nblk(nn, 256), 256, 0, st>>>(flag, nn, v, dflag2);
+            f01 = dflag2;
+        }
+        SRET(scan(f01, dpre, nn));
+        ++nlaunch, k_compact<<<nblk(nn, 256), 256, 0, st>>>(f01, dpre, nn, out, dcnt + slot);
+        SCK(cudaGetLastError());
+        return SISPH_OK;
+    }
+    // send the counts in dcnt[s0] / dcnt[s1] to the face-0 / face-1 neighbours, receive
+    // theirs into dcnt[r0] / dcnt[r1] (0 without a neighbour), then ONE host wait for all
+    // of dcnt[8..15]
+    int counts_sync(int s0, int s1, int r0, int r1)
+    {
+        SCK(cudaMemsetAsync(dcnt + r0, 0, sizeof(int), st));
+        SCK(cudaMemsetAsync(dcnt + r1, 0, sizeof(int), st));
+        const void* sb[2] = {dcnt + s0, dcnt + s1};
+        void* rb[2] = {dcnt + r0, dcnt + r1};
+        const size_t sz[2] = {sizeof(int), sizeof(int)};
+        if (tp->sendrecv(sb, sz, rb, sz, st)) return tperr();
+        SCK(cudaMemcpyAsync(hcnt + 8, dcnt + 8, 8 * sizeof(int), cudaMemcpyDeviceToHost, st));
+        SCK(cudaStreamSynchronize(st));
+        if (tp->nb[0] < 0) hcnt[r0] = 0;
+        if (tp->nb[1] < 0) hcnt[r1] = 0;
+        return SISPH_OK;
+    }
+
     // move the wall block of every wall-carrying array from [Nf, ...) to [newNf, ...)
     int relocate_walls(int newNf)
     {
@@ -925,18 +966,26 @@ template <class T, int D> struct Engine : EngineBase {
             Ntot = Nf;
             return sync_counts();
         }
-        auto mv = [&](void* base, size_t esz) -> int {
-            char* b = (char*)base;
-            SCK(cudaMemcpyAsync(wtmp, b + (size_t)Nf * esz, (size_t)Nw * esz, cudaMemcpyDeviceToDevice, st));
-            SCK(cudaMemcpyAsync(b + (size_t)newNf * esz, wtmp, (size_t)Nw * esz, cudaMemcpyDeviceToDevice, st));
-            return SISPH_OK;
+        // every wall-carrying array in two launches (staged: the old and new blocks may overlap)
+        MoveList M{};
+        size_t off = 0;
+        auto add = [&](void* base, int esz) {
+            M.ptr[M.n] = (char*)base;
+            M.esz[M.n] = esz;
+            M.toff[M.n] = off;
+            off += (size_t)Nw * esz;
+            M.n++;
         };
         void* vecs[] = {pos, pos_alt, rn, rstar, vel, vel_alt, us, us_alt};
-        for (void* q : vecs) SRET(mv(q, sizeof(V)));
+        for (void* q : vecs) add(q, sizeof(V));
         void* scs[] = {p, p_alt, rho, rho_alt};
-        for (void* q : scs) SRET(mv(q, sizeof(T)));
-        SRET(mv(pid, sizeof(int)));
-        SRET(mv(pid_alt, sizeof(int)));
+        for (void* q : scs) add(q, sizeof(T));
+        add(pid, sizeof(int));
+        add(pid_alt, sizeof(int));
+        const dim3 g((unsigned)std::min(nblk((long)Nw * sizeof(V) / 4, 256), 148 * 8), (unsigned)M.n);
+        ++nlaunch, k_move_block<<<g, 256, 0, st>>>(M, Nf, Nw, wstage, 1);
+        ++nlaunch, k_move_block<<<g, 256, 0, st>>>(M, newNf, Nw, wstage, 0);
+        SCK(cudaGetLastError());
         Nf = newNf;
         Ntot = Nf + Nw;
         return sync_counts();
@@ -947,14 +996,21 @@ template <class T, int D> struct Engine : EngineBase {
     int migrate()
     {
         const int has[2] = {tp->nb[0] >= 0, tp->nb[1] >= 0};
+        // the classification counts the leavers per face; the counts are exchanged and read
+        // with one host wait; the stable compactions run only when someone moves
+        SCK(cudaMemsetAsync(dcnt + 9, 0, 2 * sizeof(int), st));
         if (Nfo) ++nlaunch, k_classify<T><<<nblk(Nfo, 256), 256, 0, st>>>(pos, Nfo, axis, slab_lo, slab_hi, glo, ghi, gper,
-                                                                          has[0], has[1], dflag);
+                                                                          has[0], has[1], dflag, dcnt + 9);
         SCK(cudaGetLastError());
-        int nstay = 0, nout[2] = {0, 0}, nin[2] = {0, 0};
-        SRET(compact(dflag, Nfo, 0, dlist[0], nstay));
-        SRET(compact(dflag, Nfo, 1, dlist[1], nout[0]));
-        SRET(compact(dflag, Nfo, 2, dlist[2], nout[1]));
-        SRET(exchange_counts(nout, nin));
+        SRET(counts_sync(9, 10, 11, 12));
+        const int nout[2] = {hcnt[9], hcnt[10]}, nin[2] = {hcnt[11], hcnt[12]};
+        const int nstay = Nfo - nout[0] - nout[1];
+        // nobody leaves or arrives: the stayers are the owned block in its order, and the
+        // ghosts of the previous step are dropped by the caller's relocation
+        if (nout[0] + nout[1] + nin[0] + nin[1] == 0) return sync_counts();
+        SRET(compact_async(dflag, Nfo, 0, dlist[0], 13));
+        SRET(compact_async(dflag, Nfo, 1, dlist[1], 14));
+        SRET(compact_async(dflag, Nfo, 2, dlist[2], 15));
         const int nnew = nstay + nin[0] + nin[1];
         // ghosts of the previous step are dropped: the fluid block is owned only
         if (nnew + Nw > capT) {
@@ -1127,9 +1183,13 @@ template <class T, int D> struct Engine : EngineBase {
         if (Nfo) ++nlaunch, k_halo_flags<T><<<nblk(Nfo, 256), 256, 0, st>>>(pos, Nfo, axis, slab_lo, slab_hi, Gw, has[0],
                                                                             has[1], dflag, dflag2);
         SCK(cudaGetLastError());
-        SRET(compact(dflag, Nfo, -1, fsend_pre[0], nfs[0]));
-        SRET(compact(dflag2, Nfo, -1, fsend_pre[1], nfs[1]));
-        SRET(exchange_counts(nfs, nfr));
+        SRET(compact_async(dflag, Nfo, -1, fsend_pre[0], 8));
+        SRET(compact_async(dflag2, Nfo, -1, fsend_pre[1], 9));
+        SRET(counts_sync(8, 9, 10, 11));
+        nfs[0] = hcnt[8];
+        nfs[1] = hcnt[9];
+        nfr[0] = hcnt[10];
+        nfr[1] = hcnt[11];
         const int ng = nfr[0] + nfr[1];
         SRET(relocate_walls(Nfo + ng));
         PackList L{};
@@ -1345,16 +1405,41 @@ template <class T, int D> struct Engine : EngineBase {
         bool single = false;
         if (dist()) {
             // migrate first: the skin is the max over the owned fluid of all ranks
+#ifdef SISPH_DIST_PROF
+            static cudaEvent_t pe[6];
+            static bool pe_init = false;
+            if (!pe_init) {
+                for (auto& e : pe) cudaEventCreate(&e);
+                pe_init = true;
+            }
+#define DPROF(k) cudaEventRecord(pe[k], st)
+#else
+#define DPROF(k)
+#endif
+            DPROF(0);
             SRET(migrate());
+            DPROF(1);
             SRET(plan_skin(dt, single));
             if (!single) {
                 err = "slab ranks need the single per-step build: 2 dt max|u~| exceeds 0.3 x 3h (reduce dt)";
                 return SISPH_EINVAL;
             }
+            DPROF(2);
             SRET(fetch_ghosts());
+            DPROF(3);
             SRET(bin_walls_skin());
             SRET(sort_fluid(PS));
+            DPROF(4);
             SRET(build_loose_grow());
+            DPROF(5);
+#ifdef SISPH_DIST_PROF
+            cudaEventSynchronize(pe[5]);
+            float t[5];
+            for (int k = 0; k < 5; k++) cudaEventElapsedTime(&t[k], pe[k], pe[k + 1]);
+            fprintf(stderr, "dist build ms: migrate %.3f plan_skin %.3f fetch_ghosts %.3f bin+sort %.3f loose %.3f\n",
+                    t[0], t[1], t[2], t[3], t[4]);
+#endif
+#undef DPROF
         } else {
             SRET(plan_skin(dt, single));
             // A1-A5 at r^n (single build: the loose list on the skin grid)
@@ -1847,13 +1932,28 @@ template <class T, int D> struct Engine : EngineBase {
                 }
                 SCK(cudaGetLastError());
                 if (dist()) {
-                    // the ghosts' delta^k from their owners (no image shift), then their records
+                    // the ghosts' delta^k from their owners (no image shift), unpacked straight
+                    // into their records (pack, send / receive, one fused unpack)
                     PackList L{};
                     pl_add(L, dk, sizeof(V));
-                    SRET(halo_fluid(L));
-                    const int ng = Nf - Nfo;
-                    if (ng) ++nlaunch, k_gtvf_ghost_fx<<<nblk(ng, 256), 256, 0, st>>>(Nfo, ng, f0, dl, src, dst, P.fxf[0],
-                                                                                       P.fxf[1], P.fxf[2], D == 3);
+                    L.rec = sizeof(V);
+                    L.axis = axis;
+                    for (int f = 0; f < 2; f++) SRET(ensure_buf(f, (size_t)std::max(nfs[f], nfr[f]) * L.rec));
+                    if (nfs[0] + nfs[1] > 0) {
+                        ++nlaunch, k_pack2<T><<<nblk(nfs[0] + nfs[1], 256), 256, 0, st>>>(
+                                       L, 0.0, 0.0, fsend[0], fsend[1], nfs[0], nfs[1], sbuf[0], sbuf[1]);
+                        halo_bytes += (int64_t)(nfs[0] + nfs[1]) * L.rec;
+                    }
+                    const void* sb[2] = {sbuf[0], sbuf[1]};
+                    void* rb[2] = {rbuf[0], rbuf[1]};
+                    const size_t sz[2] = {(size_t)nfs[0] * L.rec, (size_t)nfs[1] * L.rec};
+                    const size_t rz[2] = {(size_t)nfr[0] * L.rec, (size_t)nfr[1] * L.rec};
+                    if (tp->sendrecv(sb, sz, rb, rz, st)) return tperr();
+                    if (nfr[0] + nfr[1] > 0)
+                        ++nlaunch, k_unpack_gtvf_fx<<<nblk(nfr[0] + nfr[1], 256), 256, 0, st>>>(
+                                       grecv, nfr[0], nfr[1], reinterpret_cast<const float4*>(rbuf[0]),
+                                       reinterpret_cast<const float4*>(rbuf[1]), f0, dl, src, dst, P.fxf[0], P.fxf[1],
+                                       P.fxf[2], D == 3);
                     SCK(cudaGetLastError());
                 }
                 src = dst;

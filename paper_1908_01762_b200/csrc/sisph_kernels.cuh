@@ -2639,6 +2639,23 @@ __global__ void k_gtvf_ghost_fx(int base, int n, const int4* __restrict__ fix0, 
                        three ? f0.z + __float2int_rn(dn.z / s2) : 0, rk[i].w);
 }
 
+// slab ranks, fused: the received delta^k records of both faces (face 0 first,
+// slot grecv[t]) go to dk and straight into the ghosts' fixed-point r^k
+__global__ void k_unpack_gtvf_fx(const int* __restrict__ map, int n0, int n1, const float4* __restrict__ buf0,
+                                 const float4* __restrict__ buf1, const int4* __restrict__ fix0,
+                                 float4* __restrict__ dk, const int4* __restrict__ rk, int4* __restrict__ rk1, float s0,
+                                 float s1, float s2, int three)
+{
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n0 + n1) return;
+    const float4 dn = t < n0 ? buf0[t] : buf1[t - n0];
+    const int i = map[t];
+    dk[i] = dn;
+    const int4 f0 = fix0[i];
+    rk1[i] = make_int4(f0.x + __float2int_rn(dn.x / s0), f0.y + __float2int_rn(dn.y / s1),
+                       three ? f0.z + __float2int_rn(dn.z / s2) : 0, rk[i].w);
+}
+
 // nbr/stride/cnt select the full r* list or the inner list (pairs with
 // r* < 3 h~ + skin).  With the inner list, a particle that has moved more
 // than skin/2 from r* raises ctl->gtvf_far and the host repeats the
@@ -2898,16 +2915,28 @@ __global__ void k_normals_smooth(Params<T> P, const V4<T>* __restrict__ pos, con
 // and classify: 0 stays, 1 leaves across the low face, 2 across the high face
 template <class T>
 __global__ void k_classify(V4<T>* __restrict__ pos, int n, int axis, double slab_lo, double slab_hi, double glo,
-                           double ghi, int gper, int has_lo, int has_hi, int* __restrict__ flag)
+                           double ghi, int gper, int has_lo, int has_hi, int* __restrict__ flag,
+                           int* __restrict__ nout)
 {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
+    // nout[0] / nout[1]: how many leave through face 0 / 1 (warp-aggregated counts)
+    int fl = 0;
+    if (i < n) {
+        const double y = (double)reinterpret_cast<const T*>(pos + i)[axis];
+        fl = (has_lo && y < slab_lo) ? 1 : ((has_hi && y >= slab_hi) ? 2 : 0);
+    }
+    const unsigned m1 = __ballot_sync(0xffffffffu, fl == 1), m2 = __ballot_sync(0xffffffffu, fl == 2);
+    if ((threadIdx.x & 31) == 0) {
+        if (m1) atomicAdd(nout, __popc(m1));
+        if (m2) atomicAdd(nout + 1, __popc(m2));
+    }
     if (i >= n) return;
     V4<T> x = ld4(pos + i);
     T* c = reinterpret_cast<T*>(&x);
     // the face is decided on the unwrapped coordinate (a particle leaving the
     // first slab downwards goes to the last slab), the stored position is wrapped
     const double y = (double)c[axis];
-    flag[i] = (has_lo && y < slab_lo) ? 1 : ((has_hi && y >= slab_hi) ? 2 : 0);
+    flag[i] = fl;
     if (gper) {
         const T L = (T)(ghi - glo);
         if (y >= ghi) c[axis] -= L;
@@ -2985,6 +3014,81 @@ __global__ void k_pack(PackList L, const int* __restrict__ idx, int base, int n,
         } else {
             for (int w = 0; w < sz / 4; w++) reinterpret_cast<int*>(r + off)[w] = reinterpret_cast<const int*>(src)[w];
             if (L.sh[f]) reinterpret_cast<T*>(r + off)[L.axis] += (T)L.shift;
+        }
+        off += sz;
+    }
+}
+
+// the wall blocks of up to 16 arrays moved in two launches (to a staging
+// buffer and back at the new offset; the ranges may overlap): grid.y = array,
+// one thread per 4-byte word
+struct MoveList {
+    int n;
+    char* ptr[16];
+    int esz[16];
+    size_t toff[16];
+};
+__global__ void k_move_block(MoveList M, int from, int nw, char* __restrict__ tmp, int to_tmp)
+{
+    const int a = blockIdx.y;
+    if (a >= M.n) return;
+    const int words = nw * (M.esz[a] >> 2);
+    int* blk = reinterpret_cast<int*>(M.ptr[a] + (size_t)from * M.esz[a]);
+    int* stg = reinterpret_cast<int*>(tmp + M.toff[a]);
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < words; t += gridDim.x * blockDim.x) {
+        if (to_tmp) stg[t] = blk[t];
+        else blk[t] = stg[t];
+    }
+}
+
+// both faces of one exchange in one launch: records q < n0 go to face 0's buffer
+// (idx0, periodic shift sh0), the rest to face 1's
+template <class T>
+__global__ void k_pack2(PackList L, double sh0, double sh1, const int* __restrict__ idx0,
+                        const int* __restrict__ idx1, int n0, int n1, char* __restrict__ buf0,
+                        char* __restrict__ buf1)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n0 + n1) return;
+    const bool f1 = t >= n0;
+    const int q = f1 ? t - n0 : t;
+    const int* idx = f1 ? idx1 : idx0;
+    const int s = idx[q];
+    char* r = (f1 ? buf1 : buf0) + (size_t)q * L.rec;
+    const T shift = (T)(f1 ? sh1 : sh0);
+    int off = 0;
+    for (int f = 0; f < L.nf; f++) {
+        const int sz = L.size[f];
+        const char* src = (const char*)L.ptr[f] + (size_t)s * sz;
+        if (sz == 1) {
+            r[off] = *src;
+        } else {
+            for (int w = 0; w < sz / 4; w++) reinterpret_cast<int*>(r + off)[w] = reinterpret_cast<const int*>(src)[w];
+            if (L.sh[f]) reinterpret_cast<T*>(r + off)[L.axis] += shift;
+        }
+        off += sz;
+    }
+}
+
+// both faces' received records in one launch (face 0's first: slots map[t] or base + t)
+template <class T>
+__global__ void k_unpack2(PackList L, const int* __restrict__ map, int base, int n0, int n1,
+                          const char* __restrict__ buf0, const char* __restrict__ buf1)
+{
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n0 + n1) return;
+    const bool f1 = t >= n0;
+    const int q = f1 ? t - n0 : t;
+    const int s = map ? map[t] : base + t;
+    const char* r = (f1 ? buf1 : buf0) + (size_t)q * L.rec;
+    int off = 0;
+    for (int f = 0; f < L.nf; f++) {
+        const int sz = L.size[f];
+        char* dst = (char*)L.ptr[f] + (size_t)s * sz;
+        if (sz == 1) {
+            *dst = r[off];
+        } else {
+            for (int w = 0; w < sz / 4; w++) reinterpret_cast<int*>(dst)[w] = reinterpret_cast<const int*>(r + off)[w];
         }
         off += sz;
     }
