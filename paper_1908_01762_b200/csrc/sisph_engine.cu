@@ -1908,6 +1908,37 @@ template <class T, int D> struct Engine : EngineBase {
 
     // K modified-GTVF sub-steps (A14) from r* = pos; returns delta^K = r^K - r^0 in rK (stride
     // rstride working-precision values per slot, delta in the last four)
+    // slab ranks, fp32 GTVF: the ghosts' delta^k from their owners (no image shift),
+    // unpacked straight into their fixed-point records (pack, send / receive, fused unpack)
+    int gtvf_halo_fx(cudaStream_t hs, int4* f0, float4* dl, const int4* src, int4* dst)
+    {
+        if constexpr (std::is_same<T, float>::value) {
+            PackList L{};
+            pl_add(L, dk, sizeof(V));
+            L.rec = sizeof(V);
+            L.axis = axis;
+            for (int f = 0; f < 2; f++) SRET(ensure_buf(f, (size_t)std::max(nfs[f], nfr[f]) * L.rec));
+            if (nfs[0] + nfs[1] > 0) {
+                ++nlaunch, k_pack2<T><<<nblk(nfs[0] + nfs[1], 256), 256, 0, hs>>>(
+                               L, 0.0, 0.0, fsend[0], fsend[1], nfs[0], nfs[1], sbuf[0], sbuf[1]);
+                halo_bytes += (int64_t)(nfs[0] + nfs[1]) * L.rec;
+            }
+            const void* sb[2] = {sbuf[0], sbuf[1]};
+            void* rb[2] = {rbuf[0], rbuf[1]};
+            const size_t sz[2] = {(size_t)nfs[0] * L.rec, (size_t)nfs[1] * L.rec};
+            const size_t rz[2] = {(size_t)nfr[0] * L.rec, (size_t)nfr[1] * L.rec};
+            if (tp->sendrecv(sb, sz, rb, rz, hs)) return tperr();
+            if (nfr[0] + nfr[1] > 0)
+                ++nlaunch, k_unpack_gtvf_fx<<<nblk(nfr[0] + nfr[1], 256), 256, 0, hs>>>(
+                               grecv, nfr[0], nfr[1], reinterpret_cast<const float4*>(rbuf[0]),
+                               reinterpret_cast<const float4*>(rbuf[1]), f0, dl, src, dst, P.fxf[0], P.fxf[1],
+                               P.fxf[2], D == 3);
+            SCK(cudaGetLastError());
+
+        }
+        return SISPH_OK;
+    }
+
     int gtvf_substeps(T dtau, bool inner, const T*& rK, int& rstride)
     {
         if (inner) SCK(cudaMemsetAsync(&ctl->gtvf_far, 0, sizeof(int), st));
@@ -1931,33 +1962,16 @@ template <class T, int D> struct Engine : EngineBase {
                                        P, dtau, src, dst, f0, dl, vv, p, nbr, P.cap, cnt, k == 0, 0, ctl);
                 }
                 SCK(cudaGetLastError());
-                if (dist()) {
-                    // the ghosts' delta^k from their owners (no image shift), unpacked straight
-                    // into their records (pack, send / receive, one fused unpack)
-                    PackList L{};
-                    pl_add(L, dk, sizeof(V));
-                    L.rec = sizeof(V);
-                    L.axis = axis;
-                    for (int f = 0; f < 2; f++) SRET(ensure_buf(f, (size_t)std::max(nfs[f], nfr[f]) * L.rec));
-                    if (nfs[0] + nfs[1] > 0) {
-                        ++nlaunch, k_pack2<T><<<nblk(nfs[0] + nfs[1], 256), 256, 0, st>>>(
-                                       L, 0.0, 0.0, fsend[0], fsend[1], nfs[0], nfs[1], sbuf[0], sbuf[1]);
-                        halo_bytes += (int64_t)(nfs[0] + nfs[1]) * L.rec;
-                    }
-                    const void* sb[2] = {sbuf[0], sbuf[1]};
-                    void* rb[2] = {rbuf[0], rbuf[1]};
-                    const size_t sz[2] = {(size_t)nfs[0] * L.rec, (size_t)nfs[1] * L.rec};
-                    const size_t rz[2] = {(size_t)nfr[0] * L.rec, (size_t)nfr[1] * L.rec};
-                    if (tp->sendrecv(sb, sz, rb, rz, st)) return tperr();
-                    if (nfr[0] + nfr[1] > 0)
-                        ++nlaunch, k_unpack_gtvf_fx<<<nblk(nfr[0] + nfr[1], 256), 256, 0, st>>>(
-                                       grecv, nfr[0], nfr[1], reinterpret_cast<const float4*>(rbuf[0]),
-                                       reinterpret_cast<const float4*>(rbuf[1]), f0, dl, src, dst, P.fxf[0], P.fxf[1],
-                                       P.fxf[2], D == 3);
-                    SCK(cudaGetLastError());
-                }
+                if (dist()) SRET(gtvf_halo_fx(st, f0, dl, src, dst));
                 src = dst;
             }
+#ifdef SISPH_DIST_PROF
+            cudaEventRecord(ge[1], st);
+            cudaEventSynchronize(ge[1]);
+            float gms = 0;
+            cudaEventElapsedTime(&gms, ge[0], ge[1]);
+            fprintf(stderr, "gtvf substeps ms %.3f\n", gms);
+#endif
             rK = reinterpret_cast<const T*>(dk);
             rstride = 4;
         } else {
