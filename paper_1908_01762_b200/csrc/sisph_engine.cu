@@ -163,6 +163,7 @@ template <class T, int D> struct Engine : EngineBase {
     uint4* code = nullptr;  // code mode: the sweep's 16-bit copy of the fluid rows' list (CodeWriter)
     int* nslot = nullptr;   // with coef in slot order
     int cc8 = 0;
+    int build_mask = 1;     // 3D loose build: 1 = test-then-append (k_build_loose_m), 0 = k_build_loose (SISPH_BUILD_MASK)
     int use_codes = 0;      // SISPH_SWEEP_CODES=1: code mode (measured: sweep +12 %, A11 -20 %)
     bool skin_used = false;
     double skin_radius = 0;
@@ -375,6 +376,7 @@ template <class T, int D> struct Engine : EngineBase {
         matrix_free = prm->matrix_free;
         if (const char* e = getenv("SISPH_SWEEP_CODES")) use_codes = atoi(e) != 0;
         if (const char* e = getenv("SISPH_PDL")) pdl = atoi(e) != 0;
+        if (const char* e = getenv("SISPH_BUILD_MASK")) build_mask = atoi(e) != 0;
         ppe_loop = prm->ppe_loop;
         P.mean_free = prm->ppe_mean_free ? 1 : 0;
         pref_auto = prm->pref_auto;
@@ -671,8 +673,17 @@ template <class T, int D> struct Engine : EngineBase {
     {
         SCK(cudaMemsetAsync(&ctl->max_count, 0, 2 * sizeof(int) + 2 * sizeof(unsigned long long), st));
         const int nc = ncells_of(PS);
-        ++nlaunch, k_build_loose<T, D><<<nblk(nc, BL_WARPS), 32 * BL_WARPS, 0, st>>>(
-            PS, nc, pos, fstart, wstart_s, Nw ? wperm_s : nullptr, nbs, cnt_s, ctl);
+        bool done = false;
+        if constexpr (D == 3) {
+            if (build_mask) {
+                ++nlaunch, k_build_loose_m<T, D><<<nblk(nc, BM_WARPS), 32 * BM_WARPS, 0, st>>>(
+                    PS, nc, pos, fstart, wstart_s, Nw ? wperm_s : nullptr, nbs, cnt_s, ctl);
+                done = true;
+            }
+        }
+        if (!done)
+            ++nlaunch, k_build_loose<T, D><<<nblk(nc, BL_WARPS), 32 * BL_WARPS, 0, st>>>(
+                PS, nc, pos, fstart, wstart_s, Nw ? wperm_s : nullptr, nbs, cnt_s, ctl);
         SCK(cudaGetLastError());
         return SISPH_OK;
     }

@@ -944,6 +944,273 @@ __global__ void BL_LOOSE_BOUNDS k_build_loose(Params<T> P, int ncells, const V4<
     }
 }
 
+// ===========================================================================
+// k_build_loose_m (round 2): the loose list of k_build_loose, entry for entry
+// and in the same order, with the candidate test and the append split.
+// k_build_loose tests a candidate and appends it in one step, so every lane
+// pays the append (register buffer selects + predicated 16-byte store, ~12
+// instructions) for every candidate, accepted or not — ~28 instructions per
+// candidate, 1/3 of which are accepted on a lattice.  Here:
+//  * the culled candidates are packed densely into a 64-entry shared ring
+//    (order kept), and every full 32-candidate chunk is tested by all lanes
+//    at once into one 32-bit acceptance mask per destination (~10
+//    instructions per candidate: distance, compare, a predicated OR);
+//  * after BM_QM chunks (or at the end of the stencil) each lane walks its
+//    own masks lowest bit first and appends only the accepted slots (the
+//    walk diverges, but every lane's total is about the same row length).
+// Same candidates (the box cull), same test expression, same order: the
+// list is the one k_build_loose writes.
+// ===========================================================================
+constexpr int BM_WARPS = 4;
+#ifndef SISPH_BM_QM
+#define SISPH_BM_QM 16
+#endif
+constexpr int BM_QM = SISPH_BM_QM;
+
+// acceptance masks of nn staged candidates (ring entries t0 .. t0 + nn - 1, t0 in {0, 32})
+// for DPL destinations per lane
+template <class T, int D, int DPL, bool FULL>
+__device__ __forceinline__ void bm_test(const V4<T>* ring, const int* rslot, int t0, int nn, const V4<T> (&xi)[2],
+                                        const int (&i)[2], T Rs2, unsigned (&m)[2])
+{
+    m[0] = m[1] = 0u;
+    auto one = [&](int u) {
+        const V4<T> xj = ring[t0 + u];
+        const int j = rslot[t0 + u];
+#pragma unroll
+        for (int d = 0; d < DPL; d++) {
+            const T dx = xi[d].x - xj.x, dy = xi[d].y - xj.y;
+            T r2 = dx * dx + dy * dy;
+            if (D == 3) {
+                const T dz = xi[d].z - xj.z;
+                r2 += dz * dz;
+            }
+            if (r2 < Rs2 && j != i[d]) m[d] |= 1u << u;
+        }
+    };
+    if constexpr (FULL) {
+#pragma unroll
+        for (int u = 0; u < 32; u++) one(u);
+    } else {
+#pragma unroll 4
+        for (int u = 0; u < nn; u++) one(u);
+    }
+}
+
+// append the accepted slots of masks 0 .. nq - 1 (chunk q's slots in cs[q], lowest bit first)
+// to a lane's row at entry k: single entries up to a 4-aligned count, then 16-byte chunks (the
+// last one padded; entries past the count are never read).  (Measured on C5 against a
+// per-lane list of the non-empty masks, with a branched and a branch-free step to the next
+// mask: 1193 / 1290 / 1219 us.)
+__device__ __forceinline__ void bm_walk(const unsigned (*msk)[2][32], const int (*cs)[32], int d, int nq, int* row,
+                                        int& k, int cap)
+{
+    const int lane = threadIdx.x & 31;
+    int qq = 0;
+    unsigned mm = msk[0][d][lane];
+    auto next = [&](int& j) -> bool {
+        while (mm == 0u) {
+            if (++qq >= nq) return false;
+            mm = msk[qq][d][lane];
+        }
+        const int bit = __ffs(mm) - 1;
+        mm &= mm - 1u;
+        j = cs[qq][bit];
+        return true;
+    };
+    while (k & 3) {
+        int j;
+        if (!next(j)) return;
+        if (k < cap) row[((k >> 2) << 7) + (k & 3)] = j;
+        k++;
+    }
+    while (true) {
+        int e0, e1, e2, e3;
+        if (!next(e0)) return;
+        int ne = 1;
+        e1 = e2 = e3 = e0;
+        if (next(e1)) {
+            ne++;
+            if (next(e2)) {
+                ne++;
+                if (next(e3)) ne++;
+            }
+        }
+        if (k < cap) *reinterpret_cast<int4*>(row + ((k >> 2) << 7)) = make_int4(e0, e1, e2, e3);
+        k += ne;
+        if (ne < 4) return;
+    }
+}
+
+template <class T, int D>
+__global__ void __launch_bounds__(32 * BM_WARPS) k_build_loose_m(Params<T> P, int ncells, const V4<T>* __restrict__ pos,
+                                                                 const int* __restrict__ fstart,
+                                                                 const int* __restrict__ wstart,
+                                                                 const int* __restrict__ wperm, int* __restrict__ nbr,
+                                                                 int* __restrict__ cnt, Ctl* ctl)
+{
+    constexpr int NROW = D == 3 ? 9 : 3;
+    constexpr int NRNG = NROW * RNG_PER_ROW;
+    __shared__ V4<T> sring[BM_WARPS][64];
+    __shared__ int sslot[BM_WARPS][64];
+    __shared__ int4 rng[BM_WARPS][NRNG];
+    __shared__ unsigned smsk[BM_WARPS][BM_QM][2][32];
+    __shared__ int scs[BM_WARPS][BM_QM][32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int c = blockIdx.x * BM_WARPS + warp;
+    if (c >= ncells) return;
+    const int fa = fstart[c], nfc = fstart[c + 1] - fa;
+    const int wa = wstart[c], nwc = wstart[c + 1] - wa;
+    const int nd = nfc + nwc;
+    if (nd == 0) return;
+    V4<T>* ring = sring[warp];
+    int* rslot = sslot[warp];
+    unsigned (*msk)[2][32] = smsk[warp];
+    int (*cs)[32] = scs[warp];
+    stencil_ranges<T, D>(P, c, fstart, wstart, rng[warp]);
+    // the non-empty ranges, in order, compacted in place
+    int nr = 0;
+    for (int q0 = 0; q0 < NRNG; q0 += 32) {
+        const int q = q0 + lane;
+        const int4 ab = q < NRNG ? rng[warp][q] : make_int4(0, 0, 0, 0);
+        const bool ne = ab.x < ab.y;
+        const unsigned m = __ballot_sync(0xffffffffu, ne);   // every lane has read its entry
+        if (ne) rng[warp][nr + __popc(m & ((1u << lane) - 1u))] = ab;
+        nr += __popc(m);
+        __syncwarp();
+    }
+    const int Nf = P.Nf, cap = P.cap;
+    const T Rs2 = P.Rs2;
+    int mmax = 0;
+    for (int base = 0; base < nd; base += 64) {
+        const bool two = nd - base > 32;   // warp-uniform
+        V4<T> xi[2];
+        int i[2], k[2];
+        int* row[2];
+        bool act[2];
+#pragma unroll
+        for (int d = 0; d < 2; d++) {
+            const int t = base + 32 * d + lane;
+            act[d] = t < nd;
+            i[d] = !act[d] ? -1 : (t < nfc ? fa + t : wslot(wperm, Nf, Nf + wa + (t - nfc)));
+            xi[d] = ld4(pos + (act[d] ? i[d] : fa));
+            row[d] = nbr + nb_base(act[d] ? i[d] : 0, cap);
+            k[d] = 0;
+        }
+        // box of this pass's destinations (warp-wide), as k_build_loose
+        V4<T> lo, hi;
+        {
+            const T big = (T)3.0e38;
+            lo.x = lo.y = lo.z = big;
+            hi.x = hi.y = hi.z = -big;
+#pragma unroll
+            for (int d = 0; d < 2; d++)
+                if (act[d]) {
+                    lo.x = min(lo.x, xi[d].x); lo.y = min(lo.y, xi[d].y); lo.z = min(lo.z, xi[d].z);
+                    hi.x = max(hi.x, xi[d].x); hi.y = max(hi.y, xi[d].y); hi.z = max(hi.z, xi[d].z);
+                }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                lo.x = min(lo.x, __shfl_xor_sync(0xffffffffu, lo.x, o));
+                lo.y = min(lo.y, __shfl_xor_sync(0xffffffffu, lo.y, o));
+                hi.x = max(hi.x, __shfl_xor_sync(0xffffffffu, hi.x, o));
+                hi.y = max(hi.y, __shfl_xor_sync(0xffffffffu, hi.y, o));
+                if (D == 3) {
+                    lo.z = min(lo.z, __shfl_xor_sync(0xffffffffu, lo.z, o));
+                    hi.z = max(hi.z, __shfl_xor_sync(0xffffffffu, hi.z, o));
+                }
+            }
+        }
+        const T Rc2 = Rs2 * (T)(1.0 + 1.0 / 4096.0);
+        auto emit = [&](int nq) {
+            if (act[0]) bm_walk(msk, cs, 0, nq, row[0], k[0], cap);
+            if (act[1]) bm_walk(msk, cs, 1, nq, row[1], k[1], cap);
+            __syncwarp();
+        };
+        // test the 32 (at the end: nn) staged candidates at ring offset t0 as chunk qn (a last
+        // chunk padded to 32 far-away candidates: 1231 us against 1193)
+        auto test = [&](int t0, int nn, int qn) {
+            unsigned m[2];
+            if (nn == 32) {
+                if (two) bm_test<T, D, 2, true>(ring, rslot, t0, 32, xi, i, Rs2, m);
+                else bm_test<T, D, 1, true>(ring, rslot, t0, 32, xi, i, Rs2, m);
+            } else {
+                if (two) bm_test<T, D, 2, false>(ring, rslot, t0, nn, xi, i, Rs2, m);
+                else bm_test<T, D, 1, false>(ring, rslot, t0, nn, xi, i, Rs2, m);
+            }
+            msk[qn][0][lane] = m[0];
+            msk[qn][1][lane] = m[1];
+            cs[qn][lane] = lane < nn ? rslot[t0 + lane] : 0;
+            __syncwarp();
+        };
+        int head = 0, tail = 0, nq = 0;
+        // (a flattened walk that loads the next chunk while this one is tested: 1237 us against 1193)
+#pragma unroll 1
+        for (int r = 0; r < nr; r++) {
+            const int4 ab = rng[warp][r];
+            V4<T> sh;
+            shift_of(P, ab.z, sh.x, sh.y, sh.z);
+#pragma unroll 1
+            for (int j0 = ab.x; j0 < ab.y; j0 += 32) {
+                V4<T> v;
+                v.x = v.y = v.z = v.w = (T)0;
+                int slot = 0;
+                const bool ok = j0 + lane < ab.y;
+                bool keep = false;
+                if (ok) {
+                    slot = wslot(wperm, Nf, j0 + lane);
+                    v = ld4(pos + slot);
+                    // cull against the box (cull_compact's test) into the ring, order kept
+                    v.x += sh.x;
+                    v.y += sh.y;
+                    if (D == 3) v.z += sh.z;
+                    const T bx = max(max(lo.x - v.x, v.x - hi.x), (T)0);
+                    const T by = max(max(lo.y - v.y, v.y - hi.y), (T)0);
+                    T d2 = bx * bx + by * by;
+                    if (D == 3) {
+                        const T bz = max(max(lo.z - v.z, v.z - hi.z), (T)0);
+                        d2 += bz * bz;
+                    }
+                    keep = d2 < Rc2;
+                }
+                const unsigned km = __ballot_sync(0xffffffffu, keep);
+                if (keep) {
+                    const int at = (head + __popc(km & ((1u << lane) - 1u))) & 63;
+                    ring[at] = v;
+                    rslot[at] = slot;
+                }
+                head += __popc(km);
+                __syncwarp();
+                if (head - tail >= 32) {
+                    test(tail & 63, 32, nq);
+                    tail += 32;
+                    if (++nq == BM_QM) {
+                        emit(nq);
+                        nq = 0;
+                    }
+                }
+            }
+        }
+        if (head > tail) {
+            test(tail & 63, head - tail, nq);
+            nq++;
+        }
+        if (nq) emit(nq);
+#pragma unroll
+        for (int d = 0; d < 2; d++)
+            if (act[d]) {
+                cnt[i[d]] = min(k[d], cap);
+                mmax = max(mmax, k[d]);
+            }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mmax = max(mmax, __shfl_xor_sync(0xffffffffu, mmax, o));
+    if (lane == 0) {
+        atomicMax(&ctl->max_count, mmax);
+        if (mmax > cap) atomicExch(&ctl->overflow, 1);
+    }
+}
+
 // r* = r^n + dt u~^n (eq:int:rnp1) of the slots [0, n): known at the start of the step, so the
 // single per-step build takes the r* sets before the stage-1 passes (same expression as
 // forces_finish, bit-identical r*)
