@@ -1965,12 +1965,15 @@ template <class T, int D> struct Engine : EngineBase {
             for (int k = 0; k < K; k++) {
                 int4* dst = (k & 1) ? b : a;
                 if (Nfo) {
+                    bool iso = true;   // one fixed-point unit on every axis (k_gtvf_substep_fx<D, true>)
+                    for (int a = 1; a < D; a++) iso = iso && P.fxf[a] == P.fxf[0];
+                    auto kf = iso ? k_gtvf_substep_fx<D, true> : k_gtvf_substep_fx<D, false>;
                     if (inner)
-                        ++nlaunch, k_gtvf_substep_fx<D><<<nblk(Nfo, 128), 128, 0, st>>>(
-                                       P, dtau, src, dst, f0, dl, vv, p, nbr_in, P.cap_in, cnt_in, k == 0, 1, ctl);
+                        ++nlaunch, kf<<<nblk(Nfo, 128), 128, 0, st>>>(P, dtau, src, dst, f0, dl, vv, p, nbr_in,
+                                                                      P.cap_in, cnt_in, k == 0, 1, ctl);
                     else
-                        ++nlaunch, k_gtvf_substep_fx<D><<<nblk(Nfo, 128), 128, 0, st>>>(
-                                       P, dtau, src, dst, f0, dl, vv, p, nbr, P.cap, cnt, k == 0, 0, ctl);
+                        ++nlaunch, kf<<<nblk(Nfo, 128), 128, 0, st>>>(P, dtau, src, dst, f0, dl, vv, p, nbr, P.cap,
+                                                                      cnt, k == 0, 0, ctl);
                 }
                 SCK(cudaGetLastError());
                 if (dist()) SRET(gtvf_halo_fx(st, f0, dl, src, dst));
