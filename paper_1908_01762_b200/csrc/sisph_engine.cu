@@ -671,7 +671,7 @@ template <class T, int D> struct Engine : EngineBase {
     // loose list at the current positions on the skin geometry PS (R3)
     int build_loose()
     {
-        SCK(cudaMemsetAsync(&ctl->max_count, 0, 2 * sizeof(int) + 2 * sizeof(unsigned long long), st));
+        SCK(cudaMemsetAsync(&ctl->max_count_s, 0, 2 * sizeof(int), st));
         const int nc = ncells_of(PS);
         bool done = false;
         if constexpr (D == 3) {
@@ -704,8 +704,8 @@ template <class T, int D> struct Engine : EngineBase {
     // exact sets at r* out of the loose list (+ GTVF inner list)
     int filter_list()
     {
-        // keep the overflow flag of the loose build; reset the statistics
-        SCK(cudaMemsetAsync(&ctl->max_count, 0, sizeof(int), st));
+        // the loose build keeps its own count / overflow (max_count_s, overflow_s)
+        SCK(cudaMemsetAsync(&ctl->max_count, 0, 2 * sizeof(int), st));
         SCK(cudaMemsetAsync(&ctl->pairs_fluid, 0, 2 * sizeof(unsigned long long), st));
         int* ni = nbr_in;
         const int rows = Nfo + Nwo;
@@ -1331,6 +1331,7 @@ template <class T, int D> struct Engine : EngineBase {
         }
         if (loose) SRET(bin_walls_skin());
         SRET(sort_fluid(loose ? PS : P));
+        if (loose && defer_loose_check) return build_loose();
         return loose ? build_loose_grow() : build_list_grow();
     }
 
@@ -1357,22 +1358,53 @@ template <class T, int D> struct Engine : EngineBase {
         }
         return SISPH_OK;
     }
+    int regrow_loose(int mc)
+    {
+        const int want = grown(mc);
+        if (nbs) cudaFree(nbs);
+        nbs = nullptr;
+        int rc = 0;
+        nbs = dalloc<int>((size_t)want * rows32(capT), err, rc);
+        if (rc) return rc;
+        cap_s = PS.cap = want;
+        return SISPH_OK;
+    }
     int build_loose_grow()
     {
         SRET(build_loose());
-        int mc;
-        SRET(read_overflow(mc));
-        if (hctl->overflow) {
-            const int want = grown(mc);
-            if (nbs) cudaFree(nbs);
-            nbs = nullptr;
-            int rc = 0;
-            nbs = dalloc<int>((size_t)want * rows32(capT), err, rc);
-            if (rc) return rc;
-            cap_s = PS.cap = want;
+        SCK(cudaMemcpyAsync(&hctl->max_count_s, &ctl->max_count_s, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+        SCK(cudaStreamSynchronize(st));
+        if (hctl->overflow_s) {
+            SRET(regrow_loose(hctl->max_count_s));
             SRET(build_loose());
         }
         return SISPH_OK;
+    }
+    // single GPU, single build: the loose build's and the filter's capacities are checked with ONE
+    // host wait after the filter (a loose overflow leaves a truncated loose list, the filter of it
+    // is redone after the regrow; the positions neither pass reads have changed)
+    bool defer_loose_check = false;
+    int filter_checked()
+    {
+        for (int round = 0; round < 8; round++) {
+            SRET(filter_list());
+            SCK(cudaMemcpyAsync(&hctl->max_count, &ctl->max_count, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+            SCK(cudaMemcpyAsync(&hctl->max_count_s, &ctl->max_count_s, 2 * sizeof(int), cudaMemcpyDeviceToHost,
+                                st));
+            SCK(cudaStreamSynchronize(st));
+            if (hctl->overflow_s) {
+                SRET(regrow_loose(hctl->max_count_s));
+                SRET(build_loose());
+                continue;
+            }
+            if (hctl->overflow) {
+                SRET(alloc_list(grown(hctl->max_count)));
+                continue;
+            }
+            return SISPH_OK;
+        }
+        err = "neighbour list capacity: no fit after repeated growth";
+        return SISPH_EOVERFLOW;
     }
     int filter_list_grow()
     {
@@ -1453,15 +1485,18 @@ template <class T, int D> struct Engine : EngineBase {
 #undef DPROF
         } else {
             SRET(plan_skin(dt, single));
-            // A1-A5 at r^n (single build: the loose list on the skin grid)
+            // A1-A5 at r^n (single build: the loose list on the skin grid, its capacity checked
+            // together with the filter's)
+            defer_loose_check = single;
             SRET(build_fluid(single));
+            defer_loose_check = false;
         }
         SRET(mark(4));
         if (single) {
             // A9 (R3): r* = r^n + dt u~^n is known now: the exact sets at r* out of the loose list
             SRET(mark(5));
             SRET(compute_rstar(dt));
-            SRET(filter_list_grow());
+            SRET(dist() ? filter_list_grow() : filter_checked());
             SRET(mark(6));
         }
         const int* nb1 = single ? nbs : nbr;

@@ -32,6 +32,8 @@ struct Ctl {
     double red[4];             // slab ranks: local (sum |dp|, sum |p|, nonfinite) of a sweep, allreduced
     unsigned long long fmax2_bits;   // max |f^n|^2 of the last correct (adaptive dt)
     unsigned long long vmax2_bits;   // max |u^{n+1}|^2 of the last correct
+    int max_count_s;           // largest row of the last loose build (k_build_loose, k_build_loose_m)
+    int overflow_s;            // a loose row exceeded the loose capacity
 };
 
 // block max of a non-negative double, one atomic per block (every thread of
@@ -939,8 +941,8 @@ __global__ void BL_LOOSE_BOUNDS k_build_loose(Params<T> P, int ncells, const V4<
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mmax = max(mmax, __shfl_xor_sync(0xffffffffu, mmax, o));
     if (lane == 0) {
-        atomicMax(&ctl->max_count, mmax);
-        if (mmax > cap) atomicExch(&ctl->overflow, 1);
+        atomicMax(&ctl->max_count_s, mmax);
+        if (mmax > cap) atomicExch(&ctl->overflow_s, 1);
     }
 }
 
@@ -1206,8 +1208,8 @@ __global__ void __launch_bounds__(32 * BM_WARPS) k_build_loose_m(Params<T> P, in
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mmax = max(mmax, __shfl_xor_sync(0xffffffffu, mmax, o));
     if (lane == 0) {
-        atomicMax(&ctl->max_count, mmax);
-        if (mmax > cap) atomicExch(&ctl->overflow, 1);
+        atomicMax(&ctl->max_count_s, mmax);
+        if (mmax > cap) atomicExch(&ctl->overflow_s, 1);
     }
 }
 

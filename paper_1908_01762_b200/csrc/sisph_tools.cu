@@ -9,7 +9,8 @@
 //     out[1]  MUFU.RSQ warp-instructions / s
 //     out[2]  the warp-instruction issue roof (= the FFMA rate: on sm_100 the FP32 pipe takes
 //             one warp-instruction per scheduler per cycle, the issue limit itself)
-//     out[3]  SM clock in MHz during the FFMA run (clock64 cycles / event time)
+//     out[3]  SM clock in MHz during the FFMA run (block 0's clock64 cycles over its own
+//             %globaltimer span)
 // Each kernel runs 8 independent dependency chains per thread (enough ILP to
 // hide the 4-cycle FMA latency at 4 warps per scheduler) over a grid of
 // 8 x SM-count blocks of 256 threads, and is timed with CUDA events after a
@@ -21,11 +22,19 @@ namespace {
 
 constexpr int CHAINS = 8;
 
+__device__ __forceinline__ unsigned long long gtimer()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 __global__ void k_ffma(float* out, int iters, float a, float b, long long* cyc)
 {
     float x[CHAINS];
 #pragma unroll
     for (int c = 0; c < CHAINS; c++) x[c] = threadIdx.x * 1e-3f + c;
+    const unsigned long long g0 = gtimer();
     const long long t0 = clock64();
     for (int k = 0; k < iters; k++) {
 #pragma unroll
@@ -35,11 +44,15 @@ __global__ void k_ffma(float* out, int iters, float a, float b, long long* cyc)
         }
     }
     const long long t1 = clock64();
+    const unsigned long long g1 = gtimer();
     float s = 0.f;
 #pragma unroll
     for (int c = 0; c < CHAINS; c++) s += x[c];
     if (s == 12345.678f) out[0] = s;   // keep the chains live
-    if (threadIdx.x == 0 && blockIdx.x == 0) *cyc = t1 - t0;
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        cyc[0] = t1 - t0;
+        cyc[1] = (long long)(g1 - g0);   // ns
+    }
 }
 
 __global__ void k_mufu(float* out, int iters)
@@ -74,7 +87,7 @@ extern "C" int sisph_tools_alu_peak(int device, double* out)
     const int blocks = 8 * sms, threads = 256, iters = 4096;
     float* f = nullptr;
     long long* cyc = nullptr;
-    if (cudaMalloc(&f, 64) != cudaSuccess || cudaMalloc(&cyc, sizeof(long long)) != cudaSuccess) return 2;
+    if (cudaMalloc(&f, 64) != cudaSuccess || cudaMalloc(&cyc, 2 * sizeof(long long)) != cudaSuccess) return 2;
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
@@ -88,10 +101,10 @@ extern "C" int sisph_tools_alu_peak(int device, double* out)
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     cudaEventElapsedTime(&ms, e0, e1);
-    long long c = 0;
-    cudaMemcpy(&c, cyc, sizeof(c), cudaMemcpyDeviceToHost);
+    long long c[2] = {0, 0};
+    cudaMemcpy(c, cyc, sizeof(c), cudaMemcpyDeviceToHost);
     out[0] = warps * per_warp / (ms * 1e-3);
-    out[3] = (double)c / (ms * 1e-3) / 1e6;   // one block's cycles over the whole kernel: a lower bound
+    out[3] = c[1] > 0 ? (double)c[0] / (double)c[1] * 1e3 : 0.0;   // cycles per ns x 1000 = MHz
     // MUFU
     k_mufu<<<blocks, threads>>>(f, iters / 4);
     cudaEventRecord(e0);

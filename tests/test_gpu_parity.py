@@ -772,3 +772,22 @@ def test_tgv_tight_tolerance_with_half_h_gtvf_and_mean_free():
     u = sim.get("VELOCITY")
     decay = np.abs(u).max() / np.exp(-8 * np.pi ** 2 * case.params["nu"] * steps * case.dt)
     assert abs(decay - 1.0) < 0.03, decay
+
+
+# ------------------------------------------------------------------ A5 build kernels
+@pytest.mark.parametrize("name", ["db3d_f32", "db3d_f64", "tgv3d_f32"])
+def test_masked_loose_build_equals_fused(name, monkeypatch):
+    """k_build_loose_m (test into masks, then append) writes the loose list of k_build_loose
+    entry for entry, so whole steps are bit-identical (SISPH_BUILD_MASK=0 selects the fused
+    kernel; the switch is read when a handle is created)."""
+    case = CASES[name]
+    out = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("SISPH_BUILD_MASK", flag)
+        sim = gpu_sim(case)
+        sim.set("TRANSPORT_VELOCITY", _moving(case, 0.3))
+        its = [sim.step(case.dt).iters for _ in range(3)]
+        out[flag] = [np.array(its)] + [sim.get(f) for f in ("POSITION", "VELOCITY", "PRESSURE", "DENSITY")]
+        sim.close()
+    for a, b in zip(out["0"], out["1"]):
+        assert np.array_equal(a, b)
