@@ -206,6 +206,17 @@ template <class T, int D> struct Engine : EngineBase {
     V* wtmp = nullptr;                                  // wall-block relocation staging
     char* wstage = nullptr;                             // relocate_walls: every array's wall block
     int64_t halo_bytes = 0;                             // bytes sent by halo / migration exchanges
+    // fp32 GTVF sub-steps on slab ranks: the rows other ranks hold as ghosts (brow) are stepped
+    // first, their delta halo runs on hst while the other rows (irow) are stepped (gcnt: the two
+    // row counts on the device)
+    int *bflag = nullptr, *brow = nullptr, *irow = nullptr, *gcnt = nullptr;
+    cudaStream_t hst = nullptr;
+    cudaEvent_t gev[2] = {nullptr, nullptr};
+    // SISPH_GTVF_OVERLAP=1 (opt-in): measured on one B200 with the slab path talking to itself over
+    // NCCL (bench.py --slab-self, C5), the 10 sub-steps take 1.19 ms overlapped against 1.13 ms
+    // unsplit (an NCCL send to itself gains nothing from the overlap; the split costs a launch and
+    // a tail per sub-step); across GPUs the halo's NVLink time is what it would hide
+    int gtvf_overlap = 0;
 
     bool dist() const { return tp != nullptr; }
 
@@ -217,7 +228,7 @@ template <class T, int D> struct Engine : EngineBase {
                         nbs, cnt_s, wperm_s, wstart_s, coef, dflag, dflag2, dpre, dlist[0], dlist[1], dlist[2],
                         dcnt, fsend[0], fsend[1], fsend_pre[0], fsend_pre[1], grecv, wsend[0], wsend[1], wrecv,
                         inv, sbuf[0], sbuf[1], rbuf[0], rbuf[1], wtmp, fnp, dcnt_w, ptype, ptype_alt, uout,
-                        oflag, olist, onew, code, nslot, wstage};
+                        oflag, olist, onew, code, nslot, wstage, bflag, brow, irow, gcnt};
         if (st) cudaStreamSynchronize(st);
         for (void* q : ptrs)
             if (q) cudaFree(q);
@@ -230,6 +241,12 @@ template <class T, int D> struct Engine : EngineBase {
         delete tp;
         drop_graph();
         if (cst) cudaStreamDestroy(cst);
+        if (hst) {
+            cudaStreamSynchronize(hst);
+            cudaStreamDestroy(hst);
+        }
+        for (auto& e : gev)
+            if (e) cudaEventDestroy(e);
         if (hdesc) cudaFreeHost(hdesc);
         if (ddesc) cudaFree(ddesc);
         if (own_stream && st) cudaStreamDestroy(st);
@@ -377,6 +394,7 @@ template <class T, int D> struct Engine : EngineBase {
         if (const char* e = getenv("SISPH_SWEEP_CODES")) use_codes = atoi(e) != 0;
         if (const char* e = getenv("SISPH_PDL")) pdl = atoi(e) != 0;
         if (const char* e = getenv("SISPH_BUILD_MASK")) build_mask = atoi(e) != 0;
+        if (const char* e = getenv("SISPH_GTVF_OVERLAP")) gtvf_overlap = atoi(e) != 0;
         ppe_loop = prm->ppe_loop;
         P.mean_free = prm->ppe_mean_free ? 1 : 0;
         pref_auto = prm->pref_auto;
@@ -465,6 +483,7 @@ template <class T, int D> struct Engine : EngineBase {
             AL(fsend_pre[1], int, NF) AL(grecv, int, NF) AL(wsend[0], int, NW) AL(wsend[1], int, NW)
             AL(wrecv, int, NW) AL(inv, int, NT) AL(wtmp, V, NW)
             AL(wstage, char, (8 * sizeof(V) + 4 * sizeof(T) + 8) * NW)
+            AL(bflag, int, NF) AL(brow, int, NF) AL(irow, int, NF) AL(gcnt, int, 2)
         }
 #undef AL
         SCK(cudaHostAlloc((void**)&hctl, sizeof(Ctl), cudaHostAllocDefault));
@@ -1995,23 +2014,63 @@ template <class T, int D> struct Engine : EngineBase {
             int4* f0 = reinterpret_cast<int4*>(fx0);
             float4* dl = reinterpret_cast<float4*>(dk);
             float4* vv = reinterpret_cast<float4*>(vk);
+#ifdef SISPH_DIST_PROF
+            static cudaEvent_t ge[2] = {nullptr, nullptr};
+            if (!ge[0]) {
+                cudaEventCreate(&ge[0]);
+                cudaEventCreate(&ge[1]);
+            }
+            cudaEventRecord(ge[0], st);
+#endif
             if (Ntot) ++nlaunch, k_gtvf_prep_fx<D><<<nblk(Ntot, 256), 256, 0, st>>>(P, pos, rho, Ntot, a, b, f0, dl);
+            bool iso = true;   // one fixed-point unit on every axis (k_gtvf_substep_fx<D, true>)
+            for (int q = 1; q < D; q++) iso = iso && P.fxf[q] == P.fxf[0];
+            auto kf = iso ? k_gtvf_substep_fx<D, true> : k_gtvf_substep_fx<D, false>;
+            const int* lst = inner ? nbr_in : nbr;
+            const int lcap = inner ? P.cap_in : P.cap;
+            const int* lcnt = inner ? cnt_in : cnt;
+            const int chk = inner ? 1 : 0;
+            // slab ranks: rows other ranks hold as ghosts first, their halo overlapped with the rest
+            const int nbnd = dist() ? nfs[0] + nfs[1] : 0;
+            const bool ovl = dist() && gtvf_overlap && Nfo > 0 && nbnd > 0;
+            if (ovl) {
+                if (!hst) {
+                    // the halo stream's blocks go first whenever an SM frees up (the interior rows'
+                    // blocks are short), so the exchange does not wait for the whole interior kernel
+                    int lo = 0, hi = 0;
+                    SCK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+                    SCK(cudaStreamCreateWithPriority(&hst, cudaStreamNonBlocking, hi));
+                }
+                for (auto& e : gev)
+                    if (!e) SCK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                SCK(cudaMemsetAsync(bflag, 0, (size_t)Nfo * sizeof(int), st));
+                for (int f = 0; f < 2; f++)
+                    if (nfs[f]) ++nlaunch, k_set_flag<<<nblk(nfs[f], 256), 256, 0, st>>>(fsend[f], nfs[f], bflag);
+                SRET(scan(bflag, dpre, Nfo));
+                ++nlaunch, k_split_rows<<<nblk(Nfo, 256), 256, 0, st>>>(bflag, dpre, Nfo, brow, irow, gcnt);
+                SCK(cudaGetLastError());
+            }
             const int4* src = b;
             for (int k = 0; k < K; k++) {
                 int4* dst = (k & 1) ? b : a;
-                if (Nfo) {
-                    bool iso = true;   // one fixed-point unit on every axis (k_gtvf_substep_fx<D, true>)
-                    for (int a = 1; a < D; a++) iso = iso && P.fxf[a] == P.fxf[0];
-                    auto kf = iso ? k_gtvf_substep_fx<D, true> : k_gtvf_substep_fx<D, false>;
-                    if (inner)
-                        ++nlaunch, kf<<<nblk(Nfo, 128), 128, 0, st>>>(P, dtau, src, dst, f0, dl, vv, p, nbr_in,
-                                                                      P.cap_in, cnt_in, k == 0, 1, ctl);
-                    else
-                        ++nlaunch, kf<<<nblk(Nfo, 128), 128, 0, st>>>(P, dtau, src, dst, f0, dl, vv, p, nbr, P.cap,
-                                                                      cnt, k == 0, 0, ctl);
+                if (ovl) {
+                    ++nlaunch, kf<<<nblk(nbnd, 128), 128, 0, st>>>(P, dtau, src, dst, f0, dl, vv, p, lst, lcap, lcnt,
+                                                                   k == 0, chk, ctl, brow, gcnt);
+                    SCK(cudaEventRecord(gev[0], st));
+                    ++nlaunch, kf<<<nblk(Nfo, 128), 128, 0, st>>>(P, dtau, src, dst, f0, dl, vv, p, lst, lcap, lcnt,
+                                                                  k == 0, chk, ctl, irow, gcnt + 1);
+                    SCK(cudaGetLastError());
+                    SCK(cudaStreamWaitEvent(hst, gev[0], 0));
+                    SRET(gtvf_halo_fx(hst, f0, dl, src, dst));
+                    SCK(cudaEventRecord(gev[1], hst));
+                    SCK(cudaStreamWaitEvent(st, gev[1], 0));
+                } else {
+                    if (Nfo)
+                        ++nlaunch, kf<<<nblk(Nfo, 128), 128, 0, st>>>(P, dtau, src, dst, f0, dl, vv, p, lst, lcap,
+                                                                      lcnt, k == 0, chk, ctl, nullptr, nullptr);
+                    SCK(cudaGetLastError());
+                    if (dist()) SRET(gtvf_halo_fx(st, f0, dl, src, dst));
                 }
-                SCK(cudaGetLastError());
-                if (dist()) SRET(gtvf_halo_fx(st, f0, dl, src, dst));
                 src = dst;
             }
 #ifdef SISPH_DIST_PROF

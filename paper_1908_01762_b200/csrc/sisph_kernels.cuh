@@ -2855,10 +2855,13 @@ __global__ void __launch_bounds__(128) k_gtvf_substep_fx(Params<float> P, float 
                                                          float4* __restrict__ dk, float4* __restrict__ vk,
                                                          const float* __restrict__ p, const int* __restrict__ nbr,
                                                          int ncap, const int* __restrict__ cnt, int first, int check,
-                                                         Ctl* ctl)
+                                                         Ctl* ctl, const int* __restrict__ rows,
+                                                         const int* __restrict__ nrows)
 {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= P.Nfo) return;
+    // rows == nullptr: every owned fluid row; else the rows rows[0 .. *nrows) (slab ranks)
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (nrows ? *nrows : P.Nfo)) return;
+    const int i = rows ? rows[t] : t;
     const int4 ri = __ldg(rk + i);
     float ax = 0.f, ay = 0.f, az = 0.f;
     int n = cnt[i];
@@ -2910,6 +2913,27 @@ __global__ void __launch_bounds__(128) k_gtvf_substep_fx(Params<float> P, float 
     rk1[i] = make_int4(f0.x + __float2int_rn(dn.x / P.fxf[0]), f0.y + __float2int_rn(dn.y / P.fxf[1]),
                        D == 3 ? f0.z + __float2int_rn(dn.z / P.fxf[2]) : 0, ri.w);
     if (check && dn.x * dn.x + dn.y * dn.y + dn.z * dn.z > P.skin_half2) atomicExch(&ctl->gtvf_far, 1);
+}
+
+// slab ranks: flag[idx[t]] = 1 (the rows of the halo send lists)
+__global__ void k_set_flag(const int* __restrict__ idx, int n, int* __restrict__ flag)
+{
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n) flag[idx[t]] = 1;
+}
+// stable split of [0, n) by flag (pre = exclusive scan of flag): flagged rows to brow, the
+// others to irow; cnt = {#flagged, #others}
+__global__ void k_split_rows(const int* __restrict__ f, const int* __restrict__ pre, int n, int* __restrict__ brow,
+                             int* __restrict__ irow, int* __restrict__ cnt)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (f[i]) brow[pre[i]] = i;
+    else irow[i - pre[i]] = i;
+    if (i == n - 1) {
+        cnt[0] = pre[i] + f[i];
+        cnt[1] = n - cnt[0];
+    }
 }
 
 // slab ranks: the ghosts' fixed-point r^k from their owners' delta^k (halo-exchanged)
