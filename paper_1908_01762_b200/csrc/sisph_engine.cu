@@ -1895,6 +1895,16 @@ template <class T, int D> struct Engine : EngineBase {
             SRET(launch_cluster());
             SCK(cudaMemcpyAsync(hctl, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
             SCK(cudaStreamSynchronize(st));
+#ifdef SISPH_PERS_PROF
+            {
+                std::vector<unsigned long long> hp(4096 * 6);
+                SCK(cudaMemcpyFromSymbol(hp.data(), g_pers_prof, hp.size() * sizeof(unsigned long long)));
+                const int its = std::max(hctl->iter - launched, 1);
+                fprintf(stderr, "cluster its=%d us/it (block 0): walls %.2f sweep %.2f blocksum %.2f barrier %.2f "
+                        "clustersum %.2f r32+decide %.2f\n", its, hp[0] * 1e-3 / its, hp[1] * 1e-3 / its,
+                        hp[2] * 1e-3 / its, hp[3] * 1e-3 / its, hp[4] * 1e-3 / its, hp[5] * 1e-3 / its);
+            }
+#endif
         } else if (mode == 3) {
             // one cooperative launch: walls, sweep, fixed-order reduction and decision per
             // iteration, separated by grid syncs (small problems: no per-sweep launches)

@@ -2679,6 +2679,13 @@ __global__ void __launch_bounds__(CLUSTER_T) k_ppe_cluster(Params<T> P, const Pp
     const double lam = __longlong_as_double((long long)vc->lambda_bits);
     if (threadIdx.x == 0) badc_s = vc->nonfinite ? 1 : 0;   // e.g. from A11's fused first sweep
     __syncthreads();
+#ifdef SISPH_PERS_PROF
+    unsigned long long tp[6] = {0, 0, 0, 0, 0, 0}, tq0 = 0, tq1 = 0;
+#define CPROF(k) if (threadIdx.x == 0) { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tq1)); if (k) tp[k - 1] += tq1 - tq0; tq0 = tq1; }
+#else
+#define CPROF(k)
+#endif
+    CPROF(0);
     while (!done) {
         const int par = kit & 1;
         const T* pin = par ? pB : pA;
@@ -2688,12 +2695,10 @@ __global__ void __launch_bounds__(CLUSTER_T) k_ppe_cluster(Params<T> P, const Pp
                 wall_pressure_row<T, D, true>(P, t / WL, pos, rho, nbr, cnt, ncap, const_cast<T*>(pin), t % WL);
             cl.sync();
         }
+        CPROF(1);
         double dn = 0.0, dd = 0.0;
         bool bad = false;
-        for (int i = gt; i < P.Nfo; i += gs) {
-            const T pold = pin[i];
-            const T pnew =
-                sweep_row<T, D, STORED, true, SISPH_CLUSTER_B>(P, i, pos, rho, fs, nbr, cnt, ncap, coef, rhs, diag, pin, code, nslot, cc8);
+        auto row_done = [&](int i, T pold, T pnew) {
             pout[i] = pnew;
             if (P.mean_free) {
                 const bool live = !fs[i] && diag[i] != T(0);
@@ -2704,10 +2709,20 @@ __global__ void __launch_bounds__(CLUSTER_T) k_ppe_cluster(Params<T> P, const Pp
                 dd += fs[i] == 2 ? 0.0 : fabs((double)pnew);
             }
             bad = bad || !isfinite((double)pnew);
+        };
+        for (int i = gt; i < P.Nfo; i += gs) {
+            const T pold = pin[i];
+            const T pnew = sweep_row<T, D, STORED, true, SISPH_CLUSTER_B>(P, i, pos, rho, fs, nbr, cnt, ncap, coef, rhs,
+                                                                         diag, pin, code, nslot, cc8);
+            row_done(i, pold, pnew);
         }
+        CPROF(2);
         block_sum(dn, dd, bad, &bp[par][0][0], &bad_s[par][0]);
+        CPROF(3);
         cl.sync();
+        CPROF(4);
         cluster_sum(par, 0);
+        CPROF(5);
         double num = red_s[0], den = red_s[1];
         if (P.mean_free) {
             // R32: remove the live-row mean, then the residual sums of the corrected iterate
@@ -2741,7 +2756,14 @@ __global__ void __launch_bounds__(CLUSTER_T) k_ppe_cluster(Params<T> P, const Pp
             vc->iter = kit;
             vc->done = done ? 1 : 0;
         }
+        CPROF(6);
     }
+#ifdef SISPH_PERS_PROF
+    // phases per iteration: walls | sweep | block sum | cluster barrier | cluster sum | R32 + decision
+    if (threadIdx.x == 0)
+        for (int k = 0; k < 6; k++) g_pers_prof[rk * 6 + k] = tp[k];
+#endif
+#undef CPROF
 }
 
 // ===========================================================================
