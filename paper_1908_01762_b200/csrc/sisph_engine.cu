@@ -1612,7 +1612,8 @@ template <class T, int D> struct Engine : EngineBase {
             pl_add(W, p + Nf, sizeof(T));
             SRET(halo_walls(W));
         }
-        ++nlaunch, k_rhs_diag<T, D><<<std::max(nblk(Nfo, RHS_T), 1), RHS_T, 0, st>>>(
+        ++nlaunch, (code ? k_rhs_diag<T, D, true> : k_rhs_diag<T, D, false>)<<<std::max(nblk(Nfo, RHS_T), 1), RHS_T, 0,
+                                                                                  st>>>(
                        P, (T)(1.0 / dt), pos, us, rho, fs, nbr, cnt, P.cap, rhs, diag, coef, ctl, p, p_alt, partials,
                        reinterpret_cast<const T*>(recS), code, nslot, cc8);
         SCK(cudaGetLastError());
@@ -1705,7 +1706,7 @@ template <class T, int D> struct Engine : EngineBase {
                              (const int*)cnt, P.cap, (const Ctl*)ctl));
         const int nb = std::max(nblk(Nfo, SWEEP_T), 1);
         const int uh = P.mean_free ? 0 : 1;   // mean-free: k_mean_fix decides and sets the condition
-        SCK(klaunch(coef ? k_sweep<T, D, true> : k_sweep<T, D, false>, nb, SWEEP_T, cst, P, (const PpeDesc<T>*)ddesc,
+        SCK(klaunch(coef ? (code ? k_sweep<T, D, true, true> : k_sweep<T, D, true, false>) : k_sweep<T, D, false>, nb, SWEEP_T, cst, P, (const PpeDesc<T>*)ddesc,
                     (const T*)rhs, (const T*)diag, (const int*)cnt, P.cap, ctl, partials, 0, pcond, uh));
         if (P.mean_free)
             SCK(klaunch(k_mean_fix<T>, nb, SWEEP_T, cst, P, (const PpeDesc<T>*)ddesc, (const T*)diag, ctl, partials, 0,
@@ -1831,7 +1832,7 @@ template <class T, int D> struct Engine : EngineBase {
             const int defer = dist() ? 1 : 0;
             const int nb = std::max(nblk(Nfo, SWEEP_T), 1);   // one block at least: the last block decides
             ++nlaunch;
-            SCK(klaunch(coef ? k_sweep<T, D, true> : k_sweep<T, D, false>, nb, SWEEP_T, st, P,
+            SCK(klaunch(coef ? (code ? k_sweep<T, D, true, true> : k_sweep<T, D, true, false>) : k_sweep<T, D, false>, nb, SWEEP_T, st, P,
                         (const PpeDesc<T>*)ddesc, (const T*)rhs, (const T*)diag, (const int*)cnt, P.cap, ctl, partials,
                         defer, pcond, 0));
             if (P.mean_free) SRET(mean_fix());

@@ -1682,7 +1682,9 @@ template <class T> struct CodeWriter {
     }
 };
 
-template <class T, int D>
+// CODE: the opt-in 16-bit step-code list (SISPH_SWEEP_CODES) is written too; the plain instance
+// carries no CodeWriter state through the pair loop
+template <class T, int D, bool CODE = false>
 __global__ void __launch_bounds__(RHS_T) k_rhs_diag(Params<T> P, T inv_dt, const V4<T>* __restrict__ pos,
                                                     const V4<T>* __restrict__ us, const T* __restrict__ rho,
                                                     const uint8_t* __restrict__ fs, const int* __restrict__ nbr,
@@ -1702,8 +1704,8 @@ __global__ void __launch_bounds__(RHS_T) k_rhs_diag(Params<T> P, T inv_dt, const
         int n = cnt[i];
         T* __restrict__ crow = coef ? coef + nb_base(i, ncap) : nullptr;
         // code mode (sweep_row): the factors go out as (code, factor) slots instead of in list order
-        CodeWriter<T> cw(code, coef, cc8, i);
-        if (code) crow = nullptr;
+        CodeWriter<T> cw(CODE ? code : nullptr, coef, cc8, i);
+        if (CODE) crow = nullptr;
 #ifndef SISPH_RHS_VST
 #define SISPH_RHS_VST 1   // B200, C5: 1061 -> 904 us per launch
 #endif
@@ -1736,9 +1738,9 @@ __global__ void __launch_bounds__(RHS_T) k_rhs_diag(Params<T> P, T inv_dt, const
             if (crow) crow[nb_off(k)] = f;
 #endif
             if (pin) sp += f * pin[j];                   // first sweep: sum_j fac_ij p^0_j
-            if (code) cw.push(j, f);
+            if constexpr (CODE) cw.push(j, f);
         });
-        if (code) cw.finish(nslot);
+        if constexpr (CODE) cw.finish(nslot);
         sr *= -P.dwk * inv_dt;
         const T scale = T(4) * P.dwk * frcp(rhoi);
         sd *= scale;
@@ -1971,7 +1973,7 @@ constexpr int SWEEP_T = SISPH_SWEEP_T;
 template <class T> constexpr int sweep_minb() { return sizeof(T) == 4 ? SISPH_SWEEP_MINB : 1; }
 
 // eq:p-sor for row i from p^k = pin (the stored or the recomputed fac_ij)
-template <class T, int D, bool STORED, bool COH = false, int PFD = SISPH_SWEEP_PF>
+template <class T, int D, bool STORED, bool COH = false, int PFD = SISPH_SWEEP_PF, bool CODE = true>
 __device__ __forceinline__ T sweep_row(const Params<T>& P, int i, const V4<T>* __restrict__ pos,
                                        const T* __restrict__ rho, const uint8_t* __restrict__ fs,
                                        const int* __restrict__ nbr, const int* __restrict__ cnt, int ncap,
@@ -1989,7 +1991,7 @@ __device__ __forceinline__ T sweep_row(const Params<T>& P, int i, const V4<T>* _
         const int n = cnt[i];
         const size_t b = nb_base(i, ncap);
         bool wide = true;
-        if constexpr (STORED) {
+        if constexpr (STORED && CODE) {
             if (code) {
             // code mode (CodeWriter): 2 + 4 bytes per slot instead of 4 + 4 per pair.  Each
             // iteration decodes 8 slots without a branch, gathers their 8 p_j, then sums in
@@ -2180,7 +2182,9 @@ __device__ __forceinline__ T sweep_row(const Params<T>& P, int i, const V4<T>* _
 // memory).  use_h: the kernel runs inside the WHILE body of the solve's CUDA
 // graph and sets the loop condition (continue = not done) from the last
 // block; a sweep launched after the decision only clears it.
-template <class T, int D, bool STORED>
+// CODE: rows may come as the opt-in 16-bit step-code list (SISPH_SWEEP_CODES); the plain
+// instance has no code path
+template <class T, int D, bool STORED, bool CODE = false>
 __global__ void __launch_bounds__(SWEEP_T, sweep_minb<T>()) k_sweep(Params<T> P, const PpeDesc<T>* __restrict__ dsc,
                                                    const T* __restrict__ rhs, const T* __restrict__ diag,
                                                    const int* __restrict__ cnt, int ncap, Ctl* ctl,
@@ -2211,7 +2215,8 @@ __global__ void __launch_bounds__(SWEEP_T, sweep_minb<T>()) k_sweep(Params<T> P,
     bool bad = false;
     if (i < P.Nfo) {
         const T pold = pin[i];
-        const T pnew = sweep_row<T, D, STORED>(P, i, pos, rho, fs, nbr, cnt, ncap, coef, rhs, diag, pin, code, nslot, cc8);
+        const T pnew = sweep_row<T, D, STORED, false, SISPH_SWEEP_PF, CODE>(P, i, pos, rho, fs, nbr, cnt, ncap, coef, rhs,
+                                                                          diag, pin, code, nslot, cc8);
         pout[i] = pnew;
         if (P.mean_free) {
             // R32: (sum, count) of the live rows; k_mean_fix removes the mean and decides
