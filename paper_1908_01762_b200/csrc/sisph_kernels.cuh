@@ -1289,6 +1289,8 @@ __global__ void FILTER_BOUNDS k_filter(Params<T> P, int nrows, const V4<T>* __re
     auto chunk = [&](const int4 v, int nv) {
         const int c = 0;
         const int n = nv;
+        // the queue can take this chunk's band cases on every lane: no fp64 decision inside it
+        const bool roomy = __all_sync(0xffffffffu, nq <= FQ - 4);
         V4<T> xj4[4];
         int j4[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
@@ -1312,7 +1314,7 @@ __global__ void FILTER_BOUNDS k_filter(Params<T> P, int nrows, const V4<T>* __re
                 const bool queued = band && nq < FQ;
                 if (queued) bq[nq++][threadIdx.x] = j;
                 const bool now = band && !queued;   // queue full: decide here
-                if (__any_sync(0xffffffffu, now)) {
+                if (!roomy && __any_sync(0xffffffffu, now)) {
                     const bool ex = exact_band((double)xi.x, (double)xi.y, (double)xi.z, (double)xj.x, (double)xj.y,
                                                (double)xj.z, P.Ld[0], P.Ld[1], P.Ld[2], pmask, D == 3, P.R2d);
                     in = now ? ex : in;
