@@ -729,8 +729,8 @@ template <class T, int D> struct Engine : EngineBase {
         int* ni = nbr_in;
         const int rows = Nfo + Nwo;
         if (rows)
-            ++nlaunch, k_filter<T, D><<<nblk(rows, 128), 128, 0, st>>>(P, rows, rstar, nbs, cnt_s, cap_s, nbr, cnt, ni,
-                                                                        cnt_in, ctl);
+            ++nlaunch, (ni ? k_filter<T, D, true> : k_filter<T, D, false>)<<<nblk(rows, 128), 128, 0, st>>>(
+                           P, rows, rstar, nbs, cnt_s, cap_s, nbr, cnt, ni, cnt_in, ctl);
         SCK(cudaGetLastError());
         inner_valid = ni != nullptr;
         return SISPH_OK;

@@ -1249,7 +1249,9 @@ __global__ void k_rstar(Params<T> P, T dt, int n, const V4<T>* __restrict__ pos,
 #ifndef SISPH_FILTER_PF
 #define SISPH_FILTER_PF 1   // B200, C5: PD 1 / 2 / 3 -> 1214 / 1204 / 1201 us
 #endif
-template <class T, int D>
+// INNER: the GTVF inner list is written too (h~ well inside h); without it the instance has no
+// second append in the entry loop
+template <class T, int D, bool INNER = true>
 __global__ void FILTER_BOUNDS k_filter(Params<T> P, int nrows, const V4<T>* __restrict__ pos,
                                        const int* __restrict__ nbs, const int* __restrict__ cnts, int cap_s,
                                        int* __restrict__ nbr, int* __restrict__ cnt, int* __restrict__ nbr_in,
@@ -1324,7 +1326,7 @@ __global__ void FILTER_BOUNDS k_filter(Params<T> P, int nrows, const V4<T>* __re
             }
             in = in && valid;
             A.push(in, j, cap);
-            B.push(in && r2 < Rin2, j, cap_in);
+            if constexpr (INNER) B.push(in && r2 < Rin2, j, cap_in);
         }
     };
     for (int c = 0; c < nmax; c += 4) {
@@ -1347,13 +1349,13 @@ __global__ void FILTER_BOUNDS k_filter(Params<T> P, int nrows, const V4<T>* __re
         A.push(ex, j, cap);
     }
     A.flush(cap);
-    B.flush(cap_in);
+    if (INNER) B.flush(cap_in);
     if (act) {
         cnt[i] = min(A.k, cap);
-        if (inner) cnt_in[i] = min(B.k, cap_in);
+        if (INNER && inner) cnt_in[i] = min(B.k, cap_in);
     }
-    int mmax = act ? max(A.k, inner && B.k > cap_in ? cap + 1 : 0) : 0;
-    unsigned sfl = act && i < Nf ? (unsigned)min(A.k, cap) : 0u, sin_ = inner ? (unsigned)B.k : 0u;
+    int mmax = act ? max(A.k, INNER && inner && B.k > cap_in ? cap + 1 : 0) : 0;
+    unsigned sfl = act && i < Nf ? (unsigned)min(A.k, cap) : 0u, sin_ = INNER && inner ? (unsigned)B.k : 0u;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         mmax = max(mmax, __shfl_xor_sync(0xffffffffu, mmax, o));
