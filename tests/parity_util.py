@@ -149,12 +149,21 @@ def ut_floor(case, dt=None, prec=64, S=1.0):
     the coordinate, divided by dt (the GPU carries the displacement explicitly).  fp32: the
     GTVF force of eq:mom:sph:gtvf sums m_j / rho_j^2 grad W over a near-lattice
     neighbourhood whose terms cancel to ~1e-3 of their absolute sum, so the fp32 shift
-    carries up to ~1e-6 of the velocity scale on top of the generic bound (R36)."""
+    carries up to ~1e-6 of the velocity scale on top of the generic bound (R36).  That shift is
+    a cancelling sum over positions the handle stores in fp32 (r^{n+1} before the sub-steps),
+    so its rounding moves linearly with the coordinate quantum relative to h: the allowance is
+    GTVF_CANCEL * ulp32(x_max) / h of the velocity scale, GTVF_CANCEL = 1e-6 / (ulp32(3.2) * 256)
+    fixed on C5 (|x| <= 3.2, h = 1/256), and never below C5's 1e-6 (C3: |x| <= 4, h = 0.002,
+    about twice C5's quantum relative to h)."""
     xm = max(abs(float(np.max(case.hi))), abs(float(np.min(case.lo))), 1.0)
     fl = 2.0 * float(np.spacing(xm)) / (case.dt if dt is None else dt)
     if prec == 32:
-        fl += 1e-6 * max(S, 1.0)
+        q = float(np.spacing(np.float32(xm))) / case.h
+        fl += max(1e-6, GTVF_CANCEL * q) * max(S, 1.0)
     return fl
+
+
+GTVF_CANCEL = 1e-6 / (float(np.spacing(np.float32(3.2))) * 256.0)
 
 
 def inject_rstar(sim, o, case, prec, dt=None):
@@ -164,6 +173,19 @@ def inject_rstar(sim, o, case, prec, dt=None):
     if prec == 32:
         o.set("xs", sim.get("RSTAR"))
         o.predict_stage2(case.dt if dt is None else dt)
+
+
+def inject_stage1(sim, o, case, prec, dt=None):
+    """As inject_rstar, and the fluid u* too: an fp32 handle stores u* in fp32, and the RHS of
+    eq:sph-ppe is a divergence of u* that cancels on a smooth field (TGV-3D at full size: the
+    terms' absolute sum is ~1e3 times the result), so the storage rounding of u*, 6e-8 of |u|,
+    moves it by ~1e-4 of its scale (reading R36).  Call after u* itself was compared."""
+    if prec == 32:
+        f = case.tag == 0
+        us = o.get("us")
+        us[f] = sim.get("USTAR")[f]
+        o.set("us", us)
+    inject_rstar(sim, o, case, prec, dt)
 
 
 def fs_hazards(rho_o, params, width=1e-6):
