@@ -719,3 +719,37 @@ def test_tgv_initial_pressure_solves_the_pressure_poisson_equation(dim):
     rhs = -rho * sum(deriv(u[j], i) * deriv(u[i], j) for i in range(dim) for j in range(dim))
     assert np.abs(p).max() > 0.1
     assert np.abs(lap - rhs).max() < 1e-10 * np.abs(rhs).max()
+
+
+def test_outlet_advection_is_shepard_at_rstar(orc):
+    """Reading R34a (P:904-909 fixes neither r^n nor r*): the outlet's advection velocity
+    is Shepard_h of the fluid's u_x^{n+1} with weights W(|r*_i - r*_j|, h) over the rows that
+    were fluid during the step.  Recomputed here by brute force over every fluid particle
+    (W from the pinned kernel, zero beyond 3h) from the step's r* and u^{n+1}; the same
+    average at r^n differs by far more than the tolerance, so the pin tells the two apart."""
+    case = synth.channel()
+    s = orc.Sim(case)
+    for _ in range(30):
+        s.step(case.dt)
+    tag0, x0 = s.tags(), s.get("x")
+    s.step(case.dt)
+    xs, u, ut, tag1 = s.get("xs"), s.get("u"), s.get("ut"), s.tags()
+    fl = np.flatnonzero(tag0 == 0)
+    outl = np.flatnonzero((tag0 == synth.OUTLET) & (tag1 == synth.OUTLET))   # not deleted this step
+    assert outl.size > 0
+    Wv = np.vectorize(lambda r: orc.W(case.dim, float(r), case.h))
+    worst_at_rn, supported = 0.0, 0
+    for i in outl:
+        w = Wv(np.linalg.norm(xs[fl] - xs[i], axis=1))
+        if w.sum() == 0.0:                     # no fluid in the support: the frozen u_x
+            assert ut[i, 0] == u[i, 0]
+            continue
+        supported += 1
+        ref = (w * u[fl, 0]).sum() / w.sum()
+        assert abs(ut[i, 0] - ref) <= 1e-12 * max(abs(ref), 1.0), (i, ut[i, 0], ref)
+        w0 = Wv(np.linalg.norm(x0[fl] - x0[i], axis=1))
+        if w0.sum() > 0:
+            worst_at_rn = max(worst_at_rn, abs((w0 * u[fl, 0]).sum() / w0.sum() - ref))
+    assert supported > 0
+    print("outlet Shepard at r^n vs r*: max difference", worst_at_rn, "over", supported, "rows")
+    assert worst_at_rn > 1e-8
