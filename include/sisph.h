@@ -250,6 +250,23 @@ int sisph_set_field(sisph_t* s, sisph_field f, const double* in, int64_t count);
 int sisph_get_field_f32(sisph_t* s, sisph_field f, float* out, int64_t count);
 int sisph_set_field_f32(sisph_t* s, sisph_field f, const float* in, int64_t count);
 
+/* Pipelined input (the state a caller feeds for the NEXT step, uploaded while
+ * the current one computes): sisph_stage_field / _f32 enqueue the host->device
+ * copy of `in` (same fields, counts and layout as sisph_set_field) on the
+ * handle's upload stream and return at once; the handle's state is unchanged
+ * until sisph_commit_staged, which makes the handle's stream wait for the
+ * staged copies and scatters them in staging order (stream-ordered, like
+ * sisph_set_field; staging POSITION checks the wall geometry as set_field
+ * does).  A field can be staged once per commit.  Ownership: `in` must stay
+ * valid and unmodified until sisph_commit_staged returns; pinned host memory
+ * makes the copy overlap the handle's kernels (pageable memory is copied
+ * synchronously by the driver).  The next staging of a field waits on the
+ * device for the previous commit's scatters.  Errors: SISPH_EINVAL (field,
+ * count, NULL, or a field staged twice), SISPH_ECUDA. */
+int sisph_stage_field(sisph_t* s, sisph_field f, const double* in, int64_t count);
+int sisph_stage_field_f32(sisph_t* s, sisph_field f, const float* in, int64_t count);
+int sisph_commit_staged(sisph_t* s);
+
 /* Creation ids in internal order: ids[0 .. n_fluid) are the fluid particles
  * in cell-sorted order, ids[n_fluid .. n) the walls.  n must equal the
  * particle count. */

@@ -79,6 +79,8 @@ struct EngineBase {
     virtual int set_field(int f, const double* in, int64_t count) = 0;
     virtual int get_field_f32(int f, float* out, int64_t count) = 0;
     virtual int set_field_f32(int f, const float* in, int64_t count) = 0;
+    virtual int stage_field(int f, const void* in, int64_t count, bool f32) = 0;
+    virtual int commit_staged() = 0;
     virtual int get_order(int64_t* ids) = 0;
     virtual int get_neighbors(int64_t* off, int64_t* ids, int64_t cap, int64_t* total) = 0;
     virtual int get_neighbors_of(const int64_t* which, int64_t m, int64_t* off, int64_t* ids, int64_t cap,
@@ -172,6 +174,22 @@ template <class T, int D> struct Engine : EngineBase {
     Ctl* hctl = nullptr;  // pinned host mirror
     double* partials = nullptr;
     double* dtmp = nullptr;  // staging for get/set (n * 3 doubles)
+    // sisph_stage_field / sisph_commit_staged: per-field device staging filled on an upload
+    // stream (ust) while the handle's stream computes; commit scatters them on st
+    struct Staged {
+        void* buf = nullptr;
+        size_t cap = 0;
+        int64_t count = 0;
+        bool f32 = false, pending = false;
+        cudaEvent_t ev = nullptr;
+    };
+    static constexpr int NFIELD = 16;
+    Staged stg[NFIELD];
+    int stg_order[NFIELD] = {};
+    int nstg = 0;
+    cudaStream_t ust = nullptr;
+    cudaEvent_t ev_consumed = nullptr;   // the last commit's scatters are done with the buffers
+    bool consumed_rec = false;
     std::vector<int> tags_host;  // creation-order tags
     // timing mode: 0-3 step / predict / solve / correct boundaries; 4 after the build at r^n
     // (A1-A5); 5 / 6 around the r* filter (A9) or build; 7 / 8 around A11 (+ fused sweep)
@@ -241,6 +259,15 @@ template <class T, int D> struct Engine : EngineBase {
         delete tp;
         drop_graph();
         if (cst) cudaStreamDestroy(cst);
+        if (ust) {
+            cudaStreamSynchronize(ust);
+            cudaStreamDestroy(ust);
+        }
+        for (auto& g : stg) {
+            if (g.buf) cudaFree(g.buf);
+            if (g.ev) cudaEventDestroy(g.ev);
+        }
+        if (ev_consumed) cudaEventDestroy(ev_consumed);
         if (hst) {
             cudaStreamSynchronize(hst);
             cudaStreamDestroy(hst);
@@ -2349,17 +2376,32 @@ template <class T, int D> struct Engine : EngineBase {
         return SISPH_OK;
     }
 
-    template <class H>
-    int set_field_t(int f, const H* in, int64_t count)
+    bool settable(int f, int64_t count)
     {
-        const H* htmp = reinterpret_cast<const H*>(dtmp);
         int nc = ncomp(f);
         if (nc < 0 || count != (int64_t)nc * n || f == SISPH_FIELD_TAG || f == SISPH_FIELD_RSTAR) {
             err = "set_field: unknown or read-only field, or count != n * components";
-            return SISPH_EINVAL;
+            return false;
         }
-        pre_swept = false;   // the sweep fused into A11 used the old state: the solve redoes it
+        return true;
+    }
+
+    template <class H>
+    int set_field_t(int f, const H* in, int64_t count)
+    {
+        if (!settable(f, count)) return SISPH_EINVAL;
         SCK(cudaMemcpyAsync(dtmp, in, (size_t)count * sizeof(H), cudaMemcpyDefault, st));
+        SRET(scatter_field(f, reinterpret_cast<const H*>(dtmp)));
+        SCK(cudaStreamSynchronize(st));
+        return SISPH_OK;
+    }
+
+    // stream-ordered scatter of a creation-id-order device buffer into field f (set_field and
+    // commit_staged)
+    template <class H>
+    int scatter_field(int f, const H* htmp)
+    {
+        pre_swept = false;   // the sweep fused into A11 used the old state: the solve redoes it
         const int B = 256;
         auto vec = [&](V* dst, int base, int cntx, int keep_w) {
             if (cntx > 0) ++nlaunch, k_from_ids_vec<T, H><<<nblk(cntx, B), B, 0, st>>>(htmp, pid + base, cntx, D, dst + base, keep_w);
@@ -2425,7 +2467,65 @@ template <class T, int D> struct Engine : EngineBase {
                 break;
         }
         SCK(cudaGetLastError());
-        SCK(cudaStreamSynchronize(st));
+        return SISPH_OK;
+    }
+
+    // sisph_stage_field: the host->device copy of a field's next value runs on the upload stream
+    // (after the previous commit's scatters released the buffer) and overlaps whatever the
+    // handle's stream is computing; nothing changes until commit_staged
+    int stage_field(int f, const void* in, int64_t count, bool f32) override
+    {
+        if (!settable(f, count)) return SISPH_EINVAL;
+        if (f < 0 || f >= NFIELD) return SISPH_EINVAL;
+        Staged& g = stg[f];
+        if (g.pending) {
+            err = "stage_field: the field is already staged (sisph_commit_staged first)";
+            return SISPH_EINVAL;
+        }
+        const size_t bytes = (size_t)count * (f32 ? sizeof(float) : sizeof(double));
+        if (!ust) SCK(cudaStreamCreateWithFlags(&ust, cudaStreamNonBlocking));
+        if (!ev_consumed) SCK(cudaEventCreateWithFlags(&ev_consumed, cudaEventDisableTiming));
+        if (!g.ev) SCK(cudaEventCreateWithFlags(&g.ev, cudaEventDisableTiming));
+        if (g.cap < bytes) {
+            SCK(cudaStreamSynchronize(ust));
+            SCK(cudaStreamSynchronize(st));
+            if (g.buf) SCK(cudaFree(g.buf));
+            g.buf = nullptr;
+            g.cap = 0;
+            SCK(cudaMalloc(&g.buf, bytes));
+            g.cap = bytes;
+        }
+        if (consumed_rec) SCK(cudaStreamWaitEvent(ust, ev_consumed, 0));
+        SCK(cudaMemcpyAsync(g.buf, in, bytes, cudaMemcpyDefault, ust));
+        SCK(cudaEventRecord(g.ev, ust));
+        g.count = count;
+        g.f32 = f32;
+        g.pending = true;
+        stg_order[nstg++] = f;
+        return SISPH_OK;
+    }
+
+    // sisph_commit_staged: the handle's stream waits for each staged copy and scatters it, in
+    // staging order; stream-ordered (no host wait except POSITION's wall-geometry check)
+    int commit_staged() override
+    {
+        for (int q = 0; q < nstg; q++) {
+            Staged& g = stg[stg_order[q]];
+            SCK(cudaStreamWaitEvent(st, g.ev, 0));
+            int rc = g.f32 ? scatter_field(stg_order[q], reinterpret_cast<const float*>(g.buf))
+                           : scatter_field(stg_order[q], reinterpret_cast<const double*>(g.buf));
+            g.pending = false;
+            if (rc != SISPH_OK) {
+                for (int r = q + 1; r < nstg; r++) stg[stg_order[r]].pending = false;
+                nstg = 0;
+                return rc;
+            }
+        }
+        nstg = 0;
+        if (ev_consumed) {
+            SCK(cudaEventRecord(ev_consumed, st));
+            consumed_rec = true;
+        }
         return SISPH_OK;
     }
 
@@ -2911,6 +3011,23 @@ int sisph_set_field_f32(sisph_t* s, sisph_field f, const float* in, int64_t coun
     CHK_HANDLE(s);
     if (!in) return fail_thread(SISPH_EINVAL, "NULL in");
     return s->e->set_field_f32((int)f, in, count);
+}
+int sisph_stage_field(sisph_t* s, sisph_field f, const double* in, int64_t count)
+{
+    CHK_HANDLE(s);
+    if (!in) return fail_thread(SISPH_EINVAL, "NULL in");
+    return s->e->stage_field((int)f, in, count, false);
+}
+int sisph_stage_field_f32(sisph_t* s, sisph_field f, const float* in, int64_t count)
+{
+    CHK_HANDLE(s);
+    if (!in) return fail_thread(SISPH_EINVAL, "NULL in");
+    return s->e->stage_field((int)f, in, count, true);
+}
+int sisph_commit_staged(sisph_t* s)
+{
+    CHK_HANDLE(s);
+    return s->e->commit_staged();
 }
 int sisph_get_order(sisph_t* s, int64_t* ids, int64_t n)
 {

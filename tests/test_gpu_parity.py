@@ -631,6 +631,44 @@ def test_state_roundtrip_exact(make):
     assert np.array_equal(res[0][2], res[1][2])
 
 
+@pytest.mark.parametrize("make", [lambda: synth.tgv3d(n=16), lambda: synth.dambreak2d(nx=60, ny=120)],
+                         ids=["tgv3d", "db2d"])
+def test_staged_upload_equals_set_field(make):
+    """sisph_stage_field / sisph_commit_staged (bench.py's pipelined e2e): the staged state,
+    uploaded while steps run and committed afterwards, gives the same next step, bit for bit,
+    as sisph_set_field of the same buffers; a field staged twice before a commit is
+    rejected; a commit with nothing staged is a no-op."""
+    from paper_1908_01762_b200 import SisphError
+    case = make()
+    ref = gpu_sim(case)
+    for _ in range(2):
+        ref.step(case.dt)
+    state = {k: ref.get(k, dtype=np.float32) for k in ("POSITION", "VELOCITY", "TRANSPORT_VELOCITY", "PRESSURE")}
+    res = []
+    for staged in (False, True):
+        sim = gpu_sim(case)
+        if staged:
+            for k, v in state.items():
+                sim.stage_ptr(k, v.ctypes.data, v.size, True)
+            with pytest.raises(SisphError):
+                v = state["PRESSURE"]
+                sim.stage_ptr("PRESSURE", v.ctypes.data, v.size, True)
+            sim.step(case.dt)              # runs on the creation state; the upload overlaps it
+            sim.commit_staged()
+            sim.commit_staged()            # nothing staged: no-op
+        else:
+            sim.step(case.dt)
+            for k, v in state.items():
+                sim.set(k, v)
+        r = sim.step(case.dt)
+        res.append((r.iters, sim.get("PRESSURE"), sim.get("POSITION"), sim.get("VELOCITY")))
+        sim.close()
+    ref.close()
+    assert res[0][0] == res[1][0]
+    for a, b in zip(res[0][1:], res[1][1:]):
+        assert np.array_equal(a, b)
+
+
 @pytest.mark.parametrize("name", ["tgv2d_f64", "hydro_f64", "db2d_f64"])
 def test_conv_mean_solve_parity(name):
     """Reading R12b (eq:convergence on means, scaled by the global fluid count):
