@@ -7,7 +7,10 @@
  *
  * Conventions (all entry points):
  *   - Every pointer argument is a HOST pointer owned by the caller; the library
- *     copies in or out and never keeps it.  The handle owns all device memory,
+ *     copies in or out and never keeps it (exception: the pipelined
+ *     sisph_stage_field / sisph_fetch_field read / write the caller's buffer
+ *     asynchronously until sisph_commit_staged / sisph_fetch_wait returns).
+ *     The handle owns all device memory,
  *     its CUDA stream (unless one is supplied in sisph_params.stream), and its
  *     NCCL communicator (distributed handles).
  *   - Vectors are row-major n x dim (dim = domain->dim) doubles.
@@ -266,6 +269,20 @@ int sisph_set_field_f32(sisph_t* s, sisph_field f, const float* in, int64_t coun
 int sisph_stage_field(sisph_t* s, sisph_field f, const double* in, int64_t count);
 int sisph_stage_field_f32(sisph_t* s, sisph_field f, const float* in, int64_t count);
 int sisph_commit_staged(sisph_t* s);
+
+/* Pipelined output: sisph_fetch_field / _f32 enqueue, on the handle's stream,
+ * the gather of field f into creation-id order (as sisph_get_field) and its
+ * device->host copy on a download stream, and return at once; the handle's
+ * stream goes on (e.g. with the next step) while the copy runs.
+ * sisph_fetch_wait blocks until the copy is in `out` (returns at once if no
+ * fetch is pending).  One fetch at a time: a second fetch before the wait is
+ * SISPH_EINVAL.  Ownership: `out` (pinned host memory for an overlapped copy)
+ * must stay valid until sisph_fetch_wait returns.  The value is the field as
+ * of the point in the handle's stream where the fetch was enqueued.  Errors:
+ * SISPH_EINVAL (field, TAG, count, NULL, pending fetch), SISPH_ECUDA. */
+int sisph_fetch_field(sisph_t* s, sisph_field f, double* out, int64_t count);
+int sisph_fetch_field_f32(sisph_t* s, sisph_field f, float* out, int64_t count);
+int sisph_fetch_wait(sisph_t* s);
 
 /* Creation ids in internal order: ids[0 .. n_fluid) are the fluid particles
  * in cell-sorted order, ids[n_fluid .. n) the walls.  n must equal the

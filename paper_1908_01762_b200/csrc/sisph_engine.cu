@@ -81,6 +81,8 @@ struct EngineBase {
     virtual int set_field_f32(int f, const float* in, int64_t count) = 0;
     virtual int stage_field(int f, const void* in, int64_t count, bool f32) = 0;
     virtual int commit_staged() = 0;
+    virtual int fetch_field(int f, void* out, int64_t count, bool f32) = 0;
+    virtual int fetch_wait() = 0;
     virtual int get_order(int64_t* ids) = 0;
     virtual int get_neighbors(int64_t* off, int64_t* ids, int64_t cap, int64_t* total) = 0;
     virtual int get_neighbors_of(const int64_t* which, int64_t m, int64_t* off, int64_t* ids, int64_t cap,
@@ -190,6 +192,13 @@ template <class T, int D> struct Engine : EngineBase {
     cudaStream_t ust = nullptr;
     cudaEvent_t ev_consumed = nullptr;   // the last commit's scatters are done with the buffers
     bool consumed_rec = false;
+    // sisph_fetch_field / sisph_fetch_wait: one field gathered into fbuf on st, copied to the
+    // host on a download stream (dlst) while st goes on
+    void* fbuf = nullptr;
+    size_t fcap = 0;
+    cudaStream_t dlst = nullptr;
+    cudaEvent_t ev_fready = nullptr, ev_fdone = nullptr;
+    bool fpending = false, fdone_rec = false;
     std::vector<int> tags_host;  // creation-order tags
     // timing mode: 0-3 step / predict / solve / correct boundaries; 4 after the build at r^n
     // (A1-A5); 5 / 6 around the r* filter (A9) or build; 7 / 8 around A11 (+ fused sweep)
@@ -268,6 +277,13 @@ template <class T, int D> struct Engine : EngineBase {
             if (g.ev) cudaEventDestroy(g.ev);
         }
         if (ev_consumed) cudaEventDestroy(ev_consumed);
+        if (dlst) {
+            cudaStreamSynchronize(dlst);
+            cudaStreamDestroy(dlst);
+        }
+        if (fbuf) cudaFree(fbuf);
+        if (ev_fready) cudaEventDestroy(ev_fready);
+        if (ev_fdone) cudaEventDestroy(ev_fdone);
         if (hst) {
             cudaStreamSynchronize(hst);
             cudaStreamDestroy(hst);
@@ -2307,7 +2323,6 @@ template <class T, int D> struct Engine : EngineBase {
     template <class H>
     int get_field_t(int f, H* out, int64_t count)
     {
-        H* htmp = reinterpret_cast<H*>(dtmp);   // device staging (3 n doubles >= count H)
         int nc = ncomp(f);
         if (nc < 0 || count != (int64_t)nc * n) {
             err = "get_field: unknown field or count != n * components";
@@ -2317,12 +2332,68 @@ template <class T, int D> struct Engine : EngineBase {
             for (int64_t k = 0; k < n; k++) out[k] = tags_host[k];
             return SISPH_OK;
         }
+        SRET(gather_field(f, reinterpret_cast<H*>(dtmp), count));   // device staging (3 n doubles >= count H)
+        SCK(cudaMemcpyAsync(out, dtmp, (size_t)count * sizeof(H), cudaMemcpyDefault, st));
+        SCK(cudaStreamSynchronize(st));
+        return SISPH_OK;
+    }
+
+    // sisph_fetch_field: field f gathered on st into fbuf, then copied to `out` on the download
+    // stream; the host waits only in fetch_wait
+    int fetch_field(int f, void* out, int64_t count, bool f32) override
+    {
+        int nc = ncomp(f);
+        if (nc < 0 || count != (int64_t)nc * n || f == SISPH_FIELD_TAG) {
+            err = "fetch_field: unknown field, TAG, or count != n * components";
+            return SISPH_EINVAL;
+        }
+        if (fpending) {
+            err = "fetch_field: a fetch is pending (sisph_fetch_wait first)";
+            return SISPH_EINVAL;
+        }
+        const size_t bytes = (size_t)count * (f32 ? sizeof(float) : sizeof(double));
+        if (!dlst) SCK(cudaStreamCreateWithFlags(&dlst, cudaStreamNonBlocking));
+        if (!ev_fready) SCK(cudaEventCreateWithFlags(&ev_fready, cudaEventDisableTiming));
+        if (!ev_fdone) SCK(cudaEventCreateWithFlags(&ev_fdone, cudaEventDisableTiming));
+        if (fcap < bytes) {
+            SCK(cudaStreamSynchronize(dlst));
+            SCK(cudaStreamSynchronize(st));
+            if (fbuf) SCK(cudaFree(fbuf));
+            fbuf = nullptr;
+            fcap = 0;
+            SCK(cudaMalloc(&fbuf, bytes));
+            fcap = bytes;
+        }
+        if (fdone_rec) SCK(cudaStreamWaitEvent(st, ev_fdone, 0));   // the last download has read fbuf
+        if (f32) SRET(gather_field(f, reinterpret_cast<float*>(fbuf), count));
+        else SRET(gather_field(f, reinterpret_cast<double*>(fbuf), count));
+        SCK(cudaEventRecord(ev_fready, st));
+        SCK(cudaStreamWaitEvent(dlst, ev_fready, 0));
+        SCK(cudaMemcpyAsync(out, fbuf, bytes, cudaMemcpyDefault, dlst));
+        SCK(cudaEventRecord(ev_fdone, dlst));
+        fdone_rec = fpending = true;
+        return SISPH_OK;
+    }
+
+    int fetch_wait() override
+    {
+        if (!fpending) return SISPH_OK;
+        fpending = false;
+        SCK(cudaEventSynchronize(ev_fdone));
+        return SISPH_OK;
+    }
+
+    // stream-ordered gather of field f into a creation-id-order device buffer (get_field and
+    // fetch_field)
+    template <class H>
+    int gather_field(int f, H* htmp, int64_t count)
+    {
         bool mid = phase != IDLE;
         if (f == SISPH_FIELD_RSTAR && !mid) {
             err = "RSTAR is only defined between sisph_predict and sisph_correct";
             return SISPH_EINVAL;
         }
-        SCK(cudaMemsetAsync(dtmp, 0, (size_t)count * sizeof(H), st));
+        SCK(cudaMemsetAsync(htmp, 0, (size_t)count * sizeof(H), st));
         const int B = 256;
         auto vec = [&](const V* src, int base, int cntx) {
             if (cntx > 0) ++nlaunch, k_to_ids_vec<T, H><<<nblk(cntx, B), B, 0, st>>>(src + base, pid + base, cntx, D, htmp);
@@ -2371,8 +2442,6 @@ template <class T, int D> struct Engine : EngineBase {
                 break;
         }
         SCK(cudaGetLastError());
-        SCK(cudaMemcpyAsync(out, dtmp, (size_t)count * sizeof(H), cudaMemcpyDefault, st));
-        SCK(cudaStreamSynchronize(st));
         return SISPH_OK;
     }
 
@@ -3028,6 +3097,23 @@ int sisph_commit_staged(sisph_t* s)
 {
     CHK_HANDLE(s);
     return s->e->commit_staged();
+}
+int sisph_fetch_field(sisph_t* s, sisph_field f, double* out, int64_t count)
+{
+    CHK_HANDLE(s);
+    if (!out) return fail_thread(SISPH_EINVAL, "NULL out");
+    return s->e->fetch_field((int)f, out, count, false);
+}
+int sisph_fetch_field_f32(sisph_t* s, sisph_field f, float* out, int64_t count)
+{
+    CHK_HANDLE(s);
+    if (!out) return fail_thread(SISPH_EINVAL, "NULL out");
+    return s->e->fetch_field((int)f, out, count, true);
+}
+int sisph_fetch_wait(sisph_t* s)
+{
+    CHK_HANDLE(s);
+    return s->e->fetch_wait();
 }
 int sisph_get_order(sisph_t* s, int64_t* ids, int64_t n)
 {

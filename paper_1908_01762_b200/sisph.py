@@ -26,7 +26,8 @@ VECTOR_FIELDS = {"POSITION", "VELOCITY", "TRANSPORT_VELOCITY", "USTAR", "RSTAR",
 EXPORTED = ["sisph_params_default", "sisph_create", "sisph_destroy", "sisph_build_neighbors",
             "sisph_predict", "sisph_ppe_solve", "sisph_correct", "sisph_step", "sisph_get_field",
             "sisph_set_field", "sisph_get_field_f32", "sisph_set_field_f32", "sisph_stage_field",
-            "sisph_stage_field_f32", "sisph_commit_staged", "sisph_get_order", "sisph_get_neighbors", "sisph_get_neighbors_of",
+            "sisph_stage_field_f32", "sisph_commit_staged", "sisph_fetch_field", "sisph_fetch_field_f32",
+            "sisph_fetch_wait", "sisph_get_order", "sisph_get_neighbors", "sisph_get_neighbors_of",
             "sisph_get_counts", "sisph_get_owned_counts", "sisph_nccl_unique_id", "sisph_local_group_create",
             "sisph_local_group_destroy", "sisph_slab_bounds", "sisph_slab_owner", "sisph_create_dist", "sisph_next_dt", "sisph_sweep_timing",
             "sisph_set_timing", "sisph_sync", "sisph_last_error"]
@@ -98,6 +99,9 @@ def lib():
         L.sisph_stage_field.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64]
         L.sisph_stage_field_f32.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64]
         L.sisph_commit_staged.argtypes = [C.c_void_p]
+        L.sisph_fetch_field.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64]
+        L.sisph_fetch_field_f32.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int64]
+        L.sisph_fetch_wait.argtypes = [C.c_void_p]
         L.sisph_get_order.argtypes = [C.c_void_p, i64p, C.c_int64]
         L.sisph_get_neighbors.argtypes = [C.c_void_p, i64p, i64p, C.c_int64, i64p]
         L.sisph_get_neighbors_of.argtypes = [C.c_void_p, i64p, C.c_int64, i64p, i64p, C.c_int64, i64p]
@@ -339,6 +343,16 @@ class Simulation:
     def commit_staged(self):
         """sisph_commit_staged: the staged fields become the handle's state (stream-ordered)."""
         _check(lib().sisph_commit_staged(self._h), self._h)
+
+    def fetch_ptr(self, field: str, ptr: int, count: int, f32: bool = False):
+        """sisph_fetch_field(_f32): enqueue the read of a field into a raw host pointer (pinned
+        memory overlaps the handle's next work); the data is there after fetch_wait()."""
+        fn = lib().sisph_fetch_field_f32 if f32 else lib().sisph_fetch_field
+        _check(fn(self._h, FIELDS[field], C.c_void_p(ptr), count), self._h)
+
+    def fetch_wait(self):
+        """sisph_fetch_wait: block until the pending fetch's copy has landed."""
+        _check(lib().sisph_fetch_wait(self._h), self._h)
 
     def get_ptr(self, field: str, ptr: int, count: int, f32: bool = False):
         fn = lib().sisph_get_field_f32 if f32 else lib().sisph_get_field

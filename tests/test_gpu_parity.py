@@ -669,6 +669,34 @@ def test_staged_upload_equals_set_field(make):
         assert np.array_equal(a, b)
 
 
+def test_fetch_field_equals_get_field():
+    """sisph_fetch_field / sisph_fetch_wait (bench.py's pipelined e2e): the value fetched right
+    after a step, read while the next step runs, equals sisph_get_field's after that step; a
+    second fetch before the wait is rejected; a wait with nothing pending is a no-op."""
+    from paper_1908_01762_b200 import SisphError
+    case = synth.dambreak2d(nx=60, ny=120)
+    sim = gpu_sim(case)
+    sim.step(case.dt)
+    ref = sim.get("PRESSURE", dtype=np.float32)
+    ref_x = sim.get("POSITION")
+    out = np.zeros(ref.size, np.float32)
+    sim.fetch_ptr("PRESSURE", out.ctypes.data, out.size, True)
+    with pytest.raises(SisphError):
+        sim.fetch_ptr("PRESSURE", out.ctypes.data, out.size, True)
+    sim.step(case.dt)                  # the copy of the previous p overlaps this step
+    sim.fetch_wait()
+    sim.fetch_wait()
+    assert np.array_equal(out, ref)
+    x64 = np.zeros(ref_x.size)
+    sim2 = gpu_sim(case)
+    sim2.step(case.dt)
+    sim2.fetch_ptr("POSITION", x64.ctypes.data, x64.size, False)
+    sim2.fetch_wait()
+    assert np.array_equal(x64.reshape(ref_x.shape), ref_x)
+    sim.close()
+    sim2.close()
+
+
 @pytest.mark.parametrize("name", ["tgv2d_f64", "hydro_f64", "db2d_f64"])
 def test_conv_mean_solve_parity(name):
     """Reading R12b (eq:convergence on means, scaled by the global fluid count):
