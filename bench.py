@@ -535,6 +535,14 @@ def run_sisph(args):
                 t = D.max_over_ranks(t, dev)
             return t, sw
 
+        # untimed warm-up of the pipelined calls: their staging / download buffers and streams are
+        # allocated on first use
+        for f, buf, cnt in fields:
+            sim.stage_ptr(f, buf.data_ptr(), cnt, f32)
+        sim.commit_staged()
+        sim.fetch_ptr("PRESSURE", out_p.data_ptr(), n, f32)
+        sim.fetch_wait()
+        torch.cuda.synchronize()
         t_s, sw_s = e2e(False)
         t, sw2 = e2e(True)
         out["e2e"] = {"value": sw2 * nf / t, "unit": UNIT, "h2d_bytes_per_step": hb * n * (3 * dim + 1),

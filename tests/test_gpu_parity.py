@@ -669,6 +669,32 @@ def test_staged_upload_equals_set_field(make):
         assert np.array_equal(a, b)
 
 
+def test_staged_positions_with_moved_walls():
+    """A staged POSITION whose wall particles moved takes set_field's re-sort path (the wall
+    check ran on the upload stream): the next step equals the set_field one bit for bit."""
+    case = synth.dambreak2d(nx=60, ny=120)
+    x = None
+    res = []
+    for staged in (False, True):
+        sim = gpu_sim(case)
+        sim.step(case.dt)
+        if x is None:
+            x = sim.get("POSITION", dtype=np.float32)
+            w = case.tag == 1
+            x[w, 0] += np.float32(0.25 * case.dx)
+        if staged:
+            sim.stage_ptr("POSITION", x.ctypes.data, x.size, True)
+            sim.commit_staged()
+        else:
+            sim.set("POSITION", x)
+        r = sim.step(case.dt)
+        res.append((r.iters, sim.get("PRESSURE"), sim.get("POSITION")))
+        sim.close()
+    assert res[0][0] == res[1][0]
+    assert np.array_equal(res[0][1], res[1][1])
+    assert np.array_equal(res[0][2], res[1][2])
+
+
 def test_fetch_field_equals_get_field():
     """sisph_fetch_field / sisph_fetch_wait (bench.py's pipelined e2e): the value fetched right
     after a step, read while the next step runs, equals sisph_get_field's after that step; a
