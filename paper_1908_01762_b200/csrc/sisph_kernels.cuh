@@ -2565,6 +2565,9 @@ __global__ void __launch_bounds__(SWEEP_T, SISPH_PERS_MINB) k_ppe_persistent(Par
         PPROF(2);
         // the partials of this parity are next written two iterations on, after two more barriers
         double a = 0, b = 0;
+        // the non-finite flag was raised (if at all) before the barrier: its L2 round trip runs
+        // beside the wall rows instead of in front of the decision
+        const int nonf = threadIdx.x == 0 ? __ldcg(&ctl->nonfinite) : 0;
         for (int q = threadIdx.x; q < (int)gridDim.x; q += blockDim.x) {
             a += __ldcg(part + 2 * q);
             b += __ldcg(part + 2 * q + 1);
@@ -2589,7 +2592,6 @@ __global__ void __launch_bounds__(SWEEP_T, SISPH_PERS_MINB) k_ppe_persistent(Par
             const double dmax = den > lam ? den : lam;
             const double res = num == 0.0 ? 0.0 : (dmax > 0.0 ? num / dmax : INFINITY);
             const int k1 = kit + 1;
-            const int nonf = __ldcg(&ctl->nonfinite);
             const int dn_ = ((k1 >= min_it && res < tol) || k1 >= max_it || nonf) ? 1 : 0;
             done_s = dn_;
             if (blockIdx.x == 0) {
