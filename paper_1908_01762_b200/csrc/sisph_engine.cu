@@ -1682,6 +1682,7 @@ template <class T, int D> struct Engine : EngineBase {
     PpeDesc<T>* hdesc = nullptr;   // pinned
     int ppe_loop = 0;              // 0 auto, 1 host-polled batches, 2 graph WHILE node, 3 persistent
     int pgrid_max = 0;             // co-resident blocks of the persistent PPE kernel
+    int pgrid_cache = -1;          // ... with the row cache's dynamic shared memory (-1: not asked yet)
     cudaStream_t cst = nullptr;    // capture stream (the handle's stream may be the legacy default)
     cudaGraph_t pgraph = nullptr;
     cudaGraphExec_t pexec = nullptr;
@@ -1813,12 +1814,35 @@ template <class T, int D> struct Engine : EngineBase {
             SCK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
             pgrid_max = std::max(1, std::min(per * sms, 4096));   // partials: 2 parities x 2 per block
         }
-        const int grid = std::max(1, std::min(pgrid_max, nblk(std::max((long)Nfo, (long)Nwo * WL), SWEEP_T)));
+        const int want = nblk(std::max((long)Nfo, (long)Nwo * WL), SWEEP_T);
+        // the row cache (k_ppe_persistent): csm chunks per thread of dynamic shared memory, when
+        // the blocks that give every thread at most one row are still co-resident with it
+        int csm_try = coef ? (sizeof(T) == 4 ? 8 : 4) : 0;
+        if (const char* e = getenv("SISPH_PERS_CACHE")) csm_try = coef ? std::max(0, std::min(atoi(e), 8)) : 0;   // A/B
+        const size_t dyn_try = (size_t)csm_try * SWEEP_T * (4 * sizeof(T) + 4 * sizeof(unsigned short));
+        if (pgrid_cache < 0) {
+            pgrid_cache = 0;
+            {
+                int per = 0, dev = 0, sms = 0;
+                if (csm_try && cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_try) == cudaSuccess &&
+                    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, SWEEP_T, dyn_try) == cudaSuccess) {
+                    SCK(cudaGetDevice(&dev));
+                    SCK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+                    pgrid_cache = std::min(per * sms, 4096);
+                } else {
+                    cudaGetLastError();
+                }
+            }
+        }
+        const bool use_cache = csm_try && want <= pgrid_cache;
+        int csm = use_cache ? csm_try : 0;
+        const size_t dyn = use_cache ? dyn_try : 0;
+        const int grid = std::max(1, std::min(use_cache ? pgrid_cache : pgrid_max, want));
         int cap = P.cap;
-        void* args[] = {&P, &ddesc, &rhs, &diag, &cnt, &cap, &ctl, &partials};
+        void* args[] = {&P, &ddesc, &rhs, &diag, &cnt, &cap, &ctl, &partials, &csm};
         SCK(cudaMemsetAsync(&ctl->gbar, 0, sizeof(unsigned int), st));
         ++nlaunch;
-        SCK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(SWEEP_T), args, 0, st));
+        SCK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(SWEEP_T), args, dyn, st));
         return SISPH_OK;
     }
 
@@ -1962,6 +1986,13 @@ template <class T, int D> struct Engine : EngineBase {
                 const int nb = std::max(1, std::min(pgrid_max, nblk(std::max((long)Nfo, (long)Nwo * WL), SWEEP_T)));
                 const int its = std::max(hctl->iter - launched, 1);
                 double mean[5] = {0}, mx[5] = {0};
+                int ntiled = 0;
+                unsigned long long tmax = 0;
+                for (int b = 0; b < nb; b++) {
+                    ntiled += hp[b * 6 + 5] != 0;
+                    tmax = std::max(tmax, hp[b * 6 + 5]);
+                }
+                fprintf(stderr, "pers tiled blocks %d of %d, largest span %llu\n", ntiled, nb, tmax);
                 for (int b = 0; b < nb; b++)
                     for (int k = 0; k < 5; k++) {
                         const double v = hp[b * 6 + k] * 1e-3 / its;

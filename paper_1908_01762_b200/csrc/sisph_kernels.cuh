@@ -400,6 +400,22 @@ __device__ __forceinline__ void ld_chunk4_l1(const float* p, float (&f)[4])
     f[2] = v.z;
     f[3] = v.w;
 }
+__device__ __forceinline__ void ld_chunk4_s(const float* p, float (&f)[4])
+{
+    const float4 v = *reinterpret_cast<const float4*>(p);
+    f[0] = v.x;
+    f[1] = v.y;
+    f[2] = v.z;
+    f[3] = v.w;
+}
+__device__ __forceinline__ void ld_chunk4_s(const double* p, double (&f)[4])
+{
+    const double2 a = reinterpret_cast<const double2*>(p)[0], b = reinterpret_cast<const double2*>(p)[1];
+    f[0] = a.x;
+    f[1] = a.y;
+    f[2] = b.x;
+    f[3] = b.y;
+}
 __device__ __forceinline__ void ld_chunk4_l1(const double* p, double (&f)[4])
 {
     const double2 a = __ldg(reinterpret_cast<const double2*>(p)), b = __ldg(reinterpret_cast<const double2*>(p) + 1);
@@ -1977,6 +1993,21 @@ constexpr int SWEEP_T = SISPH_SWEEP_T;
 template <class T> constexpr int sweep_minb() { return sizeof(T) == 4 ? SISPH_SWEEP_MINB : 1; }
 
 // eq:p-sor for row i from p^k = pin (the stored or the recomputed fac_ij)
+// eq:p-sor for one row from its neighbour sum s = sum_j (stored factor)_ij p_j:
+// p_i^{k+1} = omega (rhs_i + 4 dwk s / rho_i) / D_ii + (1 - omega) p_i^k.  The fused
+// multiply-adds are written out (the grouping the compiler chose for k_sweep's expression in
+// either precision), so every loop form -- and the persistent loop's cached rows, whose
+// operands are loop invariants -- rounds identically whatever the surrounding code.
+template <class T>
+__device__ __forceinline__ T ppe_update(const Params<T>& P, T rhs_i, T s, T di, T rhoi, T pold)
+{
+    const T k = T(4) * P.dwk * frcp(rhoi);
+    const T t = P.omega * fma(s, k, rhs_i);
+    const T om1 = T(1) - P.omega;
+    if constexpr (sizeof(T) == 4) return fma(frcp(di), t, pold * om1);
+    else return fma(pold, om1, frcp(di) * t);
+}
+
 template <class T, int D, bool STORED, bool COH = false, int PFD = SISPH_SWEEP_PF, bool CODE = true>
 __device__ __forceinline__ T sweep_row(const Params<T>& P, int i, const V4<T>* __restrict__ pos,
                                        const T* __restrict__ rho, const uint8_t* __restrict__ fs,
@@ -2171,8 +2202,7 @@ __device__ __forceinline__ T sweep_row(const Params<T>& P, int i, const V4<T>* _
                 s += xj.w * (r * quintic4(r * P.inv_h)) * frcp((rhoi + rhoj) * (r2 + P.eta_h2)) * pj;
             });
         }
-        s *= T(4) * P.dwk * frcp(rhoi);       // S_i = sum_j fac_ij p_j = -sum_j OD_ij p_j
-        pnew = P.omega * (rhs[i] + s) * frcp(di) + (T(1) - P.omega) * pold;
+        pnew = ppe_update(P, rhs[i], s, di, rhoi, pold);   // S_i = 4 dwk s / rho_i = -sum_j OD_ij p_j
     }
     return pnew;
 }
@@ -2444,6 +2474,65 @@ __global__ void k_decide(Ctl* ctl, double tol, int min_it, int max_it, double cs
     ctl->done = ((k1 >= min_it && res < tol) || k1 >= max_it || ctl->nonfinite) ? 1 : 0;
 }
 
+// sweep_row's batched-gather form with p^k of the block's neighbour span staged in shared
+// memory (persistent loop, stored factors): the same loads of the list and the factors, the
+// same sums in entry order (pads gather p_i with a zero factor) -- only the p_j come from the
+// tile instead of one L2 request per pair.  Slot of particle j in the tile: fluid j - f0,
+// wall j - wsh (the wall span follows the fluid span).
+#ifndef SISPH_PERS_TILE
+#define SISPH_PERS_TILE 2048
+#endif
+constexpr int PERS_TILE = SISPH_PERS_TILE;
+template <class T, int B>
+__device__ __forceinline__ T sweep_row_tile(const Params<T>& P, int i, const T* __restrict__ rho,
+                                            const uint8_t* __restrict__ fs, const int* __restrict__ nbr,
+                                            const int* __restrict__ cnt, int ncap, const T* __restrict__ coef,
+                                            const T* __restrict__ rhs, const T* __restrict__ diag,
+                                            const T* tile, int f0, int wsh)
+{
+    const int nf = P.Nf;
+    const T pold = tile[i - f0];
+    T pnew = fs[i] == 2 ? pold : T(0);                 // R34 outlet rows keep their frozen p
+    const T di = diag[i];
+    if (!fs[i] && di != T(0)) {
+        const T rhoi = rho[i];
+        T s = 0;
+        const int n = cnt[i];
+        const size_t b = nb_base(i, ncap);
+        const int4* __restrict__ qi = reinterpret_cast<const int4*>(nbr + b);
+        for (int c = 0; c < n; c += 4 * B) {
+            int4 v[B];
+            T f[B][4];
+#pragma unroll
+            for (int g = 0; g < B; g++) {
+                const int cg0 = c + 4 * g;
+                v[g] = cg0 < n ? __ldg(qi + (size_t)(cg0 >> 2) * 32) : make_int4(i, i, i, i);
+                f[g][0] = f[g][1] = f[g][2] = f[g][3] = T(0);
+                if (cg0 < n) ld_chunk4_l1(coef + b + ((size_t)(cg0 >> 2) * 32 << 2), f[g]);
+            }
+            T pv[B][4];
+#pragma unroll
+            for (int g = 0; g < B; g++) {
+                const int cg0 = c + 4 * g;
+                const int j0 = cg0 < n ? v[g].x : i, j1 = cg0 + 1 < n ? v[g].y : i;
+                const int j2 = cg0 + 2 < n ? v[g].z : i, j3 = cg0 + 3 < n ? v[g].w : i;
+                pv[g][0] = tile[j0 - (j0 < nf ? f0 : wsh)];
+                pv[g][1] = tile[j1 - (j1 < nf ? f0 : wsh)];
+                pv[g][2] = tile[j2 - (j2 < nf ? f0 : wsh)];
+                pv[g][3] = tile[j3 - (j3 < nf ? f0 : wsh)];
+            }
+#pragma unroll
+            for (int g = 0; g < B; g++) {
+                const int cg0 = c + 4 * g;
+#pragma unroll
+                for (int e = 0; e < 4; e++) s += (cg0 + e < n ? f[g][e] : T(0)) * pv[g][e];
+            }
+        }
+        pnew = ppe_update(P, rhs[i], s, di, rhoi, pold);   // S_i = 4 dwk s / rho_i = -sum_j OD_ij p_j
+    }
+    return pnew;
+}
+
 // ===========================================================================
 // The whole PPE loop in ONE cooperative launch (small problems, where the
 // per-sweep launches and their latency dominate: BASELINE configs[0-1]).
@@ -2481,7 +2570,7 @@ template <class T, int D, bool STORED>
 __global__ void __launch_bounds__(SWEEP_T, SISPH_PERS_MINB) k_ppe_persistent(Params<T> P, const PpeDesc<T>* __restrict__ dsc,
                                                             const T* __restrict__ rhs, const T* __restrict__ diag,
                                                             const int* __restrict__ cnt, int ncap, Ctl* ctl,
-                                                            double* __restrict__ partials)
+                                                            double* __restrict__ partials, int csm)
 {
     unsigned int* gbar = &ctl->gbar;
     unsigned int nbar = 0;
@@ -2516,6 +2605,96 @@ __global__ void __launch_bounds__(SWEEP_T, SISPH_PERS_MINB) k_ppe_persistent(Par
 #else
 #define PPROF(k)
 #endif
+    // the neighbour span of this block's rows (once per solve: the lists do not change): when the
+    // fluid span [f0, f0 + nfs) and the wall span [w0, w0 + nws) fit the tile, every sweep stages
+    // their p^k in shared memory (one coalesced L2 read per value instead of one L2 request per
+    // pair: the gathers bypass L1, and on configs[1] their sectors were the sweep phase's bound)
+    __shared__ T tile[STORED ? PERS_TILE : 1];
+    __shared__ int span_s[4];
+    int f0 = 0, w0 = 0, nfs = 0, nws = 0;
+    bool tiled = false;
+    if constexpr (STORED) {
+        if (!done && code == nullptr) {
+            if (threadIdx.x == 0) {
+                span_s[0] = span_s[2] = 0x7fffffff;
+                span_s[1] = span_s[3] = -1;
+            }
+            __syncthreads();
+            int fmn = 0x7fffffff, fmx = -1, wmn = 0x7fffffff, wmx = -1;
+            for (int i = gt; i < P.Nfo; i += gs) {
+                fmn = min(fmn, i);
+                fmx = max(fmx, i);
+                if (!fs[i] && diag[i] != T(0))
+                    for_nbrs(nbr, ncap, i, cnt[i], [&](int j) {
+                        if (j < P.Nf) {
+                            fmn = min(fmn, j);
+                            fmx = max(fmx, j);
+                        } else {
+                            wmn = min(wmn, j);
+                            wmx = max(wmx, j);
+                        }
+                    });
+            }
+            fmn = __reduce_min_sync(0xffffffffu, fmn);
+            fmx = __reduce_max_sync(0xffffffffu, fmx);
+            wmn = __reduce_min_sync(0xffffffffu, wmn);
+            wmx = __reduce_max_sync(0xffffffffu, wmx);
+            if (lane == 0) {
+                atomicMin(&span_s[0], fmn);
+                atomicMax(&span_s[1], fmx);
+                atomicMin(&span_s[2], wmn);
+                atomicMax(&span_s[3], wmx);
+            }
+            __syncthreads();
+            f0 = span_s[0];
+            nfs = span_s[1] >= f0 ? span_s[1] - f0 + 1 : 0;
+            w0 = span_s[2];
+            nws = span_s[3] >= w0 ? span_s[3] - w0 + 1 : 0;
+            tiled = nfs > 0 && (long long)nfs + nws <= PERS_TILE;
+        }
+    }
+    const int wsh = w0 - nfs;
+    // the row cache (csm > 0: the launch carries csm 4-entry chunks per thread of dynamic shared
+    // memory): the first row of every thread keeps its first csm chunks -- tile slots as 16-bit
+    // values and the stored factors, pads as (own slot, 0) -- and its row constants in registers
+    // for the whole solve.  On configs[1] the lists of an SM's rows exceed its L1 (ncu: 2 % hit
+    // rate), so every sweep re-read them from L2; now a sweep reads the tile and nothing else.
+    extern __shared__ __align__(16) unsigned char pers_dsm[];
+    T* const cfac = reinterpret_cast<T*>(pers_dsm);                                    // [csm][SWEEP_T][4]
+    unsigned short* const cidx = reinterpret_cast<unsigned short*>(cfac + (size_t)csm * SWEEP_T * 4);
+    const bool cached = STORED && tiled && csm > 0 && gt < P.Nfo;
+    int cn = 0;                // entries of the cached row that are summed (0: the row does not sum)
+    T c_di = 0, c_rhs = 0, c_rhoi = 0;
+    int c_fs = 0;
+    if constexpr (STORED) {
+        if (cached) {
+            const int i = gt;
+            c_fs = fs[i];
+            c_di = diag[i];
+            c_rhs = rhs[i];
+            c_rhoi = rho[i];
+            cn = (!c_fs && c_di != T(0)) ? cnt[i] : 0;
+            const size_t b = nb_base(i, ncap);
+            const int4* __restrict__ qi = reinterpret_cast<const int4*>(nbr + b);
+            for (int c = 0; c < csm && 4 * c < cn; c++) {
+                const int4 v = __ldg(qi + (size_t)c * 32);
+                T f[4];
+                ld_chunk4_l1(coef + b + ((size_t)c * 32 << 2), f);
+                const int jv[4] = {v.x, v.y, v.z, v.w};
+                ushort4 lv;
+                unsigned short* lp = &lv.x;
+#pragma unroll
+                for (int e = 0; e < 4; e++) {
+                    const bool ok = 4 * c + e < cn;
+                    const int j = ok ? jv[e] : i;
+                    lp[e] = (unsigned short)(j - (j < P.Nf ? f0 : wsh));
+                    if (!ok) f[e] = T(0);
+                }
+                *reinterpret_cast<ushort4*>(cidx + ((size_t)c * SWEEP_T + threadIdx.x) * 4) = lv;
+                st_chunk4(cfac + ((size_t)c * SWEEP_T + threadIdx.x) * 4, f);
+            }
+        }
+    }
     // prologue: the walls of p^kit; then per iteration: sweep | walls of p^{k+1} (speculative:
     // after the last sweep they land in the final buffer's wall slots, which the solve's
     // epilogue overwrites with the walls the last sweep used) overlapped with the decision |
@@ -2532,9 +2711,64 @@ __global__ void __launch_bounds__(SWEEP_T, SISPH_PERS_MINB) k_ppe_persistent(Par
         T* pout = par ? pA : pB;
         double dn = 0.0, dd = 0.0;
         bool bad = false;
-        for (int i = gt; i < P.Nfo; i += gs) {
+        if (tiled) {
+            for (int t = threadIdx.x; t < nfs; t += blockDim.x) tile[t] = __ldcg(pin + f0 + t);
+            for (int t = threadIdx.x; t < nws; t += blockDim.x) tile[nfs + t] = __ldcg(pin + w0 + t);
+            __syncthreads();
+        }
+        int ifirst = gt;
+        if constexpr (STORED) {
+            if (cached) {
+                // the cached row: same sums in entry order as sweep_row (pads add 0 x p_i)
+                const int i = gt;
+                const T pold = tile[i - f0];
+                T pnew = c_fs == 2 ? pold : T(0);
+                if (cn > 0) {
+                    T s = 0;
+                    const int nc = min(csm, (cn + 3) >> 2);
+                    for (int c = 0; c < nc; c++) {
+                        const ushort4 lv = *reinterpret_cast<const ushort4*>(cidx + ((size_t)c * SWEEP_T + threadIdx.x) * 4);
+                        T f[4];
+                        ld_chunk4_s(cfac + ((size_t)c * SWEEP_T + threadIdx.x) * 4, f);
+                        const T p0 = tile[lv.x], p1 = tile[lv.y], p2 = tile[lv.z], p3 = tile[lv.w];
+                        s += f[0] * p0;
+                        s += f[1] * p1;
+                        s += f[2] * p2;
+                        s += f[3] * p3;
+                    }
+                    if (4 * csm < cn) {
+                        // the rest of a long row from the list (tile gathers)
+                        const size_t b = nb_base(i, ncap);
+                        const int4* __restrict__ qi = reinterpret_cast<const int4*>(nbr + b);
+                        for (int c = 4 * csm; c < cn; c += 4) {
+                            const int4 v = __ldg(qi + (size_t)(c >> 2) * 32);
+                            T f[4];
+                            ld_chunk4_l1(coef + b + ((size_t)(c >> 2) * 32 << 2), f);
+                            const int j0 = v.x, j1 = c + 1 < cn ? v.y : i, j2 = c + 2 < cn ? v.z : i, j3 = c + 3 < cn ? v.w : i;
+                            s += f[0] * tile[j0 - (j0 < P.Nf ? f0 : wsh)];
+                            s += (c + 1 < cn ? f[1] : T(0)) * tile[j1 - (j1 < P.Nf ? f0 : wsh)];
+                            s += (c + 2 < cn ? f[2] : T(0)) * tile[j2 - (j2 < P.Nf ? f0 : wsh)];
+                            s += (c + 3 < cn ? f[3] : T(0)) * tile[j3 - (j3 < P.Nf ? f0 : wsh)];
+                        }
+                    }
+                    pnew = ppe_update(P, c_rhs, s, c_di, c_rhoi, pold);
+                }
+                pout[i] = pnew;
+                dn += fabs((double)pnew - (double)pold);
+                dd += c_fs == 2 ? 0.0 : fabs((double)pnew);
+                bad = bad || !isfinite((double)pnew);
+                ifirst = gt + gs;
+            }
+        }
+        for (int i = ifirst; i < P.Nfo; i += gs) {
             const T pold = pin[i];
-            const T pnew = sweep_row<T, D, STORED, true, SISPH_PERS_B>(P, i, pos, rho, fs, nbr, cnt, ncap, coef, rhs, diag, pin, code, nslot, cc8);
+            T pnew;
+            if constexpr (STORED && SISPH_PERS_B < 0) {
+                pnew = tiled ? sweep_row_tile<T, -SISPH_PERS_B>(P, i, rho, fs, nbr, cnt, ncap, coef, rhs, diag, tile, f0, wsh)
+                             : sweep_row<T, D, STORED, true, SISPH_PERS_B>(P, i, pos, rho, fs, nbr, cnt, ncap, coef, rhs, diag, pin, code, nslot, cc8);
+            } else {
+                pnew = sweep_row<T, D, STORED, true, SISPH_PERS_B>(P, i, pos, rho, fs, nbr, cnt, ncap, coef, rhs, diag, pin, code, nslot, cc8);
+            }
             pout[i] = pnew;
             dn += fabs((double)pnew - (double)pold);
             dd += fs[i] == 2 ? 0.0 : fabs((double)pnew);
@@ -2609,7 +2843,10 @@ __global__ void __launch_bounds__(SWEEP_T, SISPH_PERS_MINB) k_ppe_persistent(Par
     }
 #ifdef SISPH_PERS_PROF
     if (threadIdx.x == 0)
+    {
         for (int k = 0; k < 5; k++) g_pers_prof[blockIdx.x * 6 + k] = tp[k];
+        g_pers_prof[blockIdx.x * 6 + 5] = tiled ? (unsigned long long)(nfs + nws) : 0ull;
+    }
 #endif
 #undef PPROF
 }
