@@ -1817,9 +1817,10 @@ template <class T, int D> struct Engine : EngineBase {
         const int want = nblk(std::max((long)Nfo, (long)Nwo * WL), SWEEP_T);
         // the row cache (k_ppe_persistent): csm chunks per thread of dynamic shared memory, when
         // the blocks that give every thread at most one row are still co-resident with it
-        int csm_try = coef ? (sizeof(T) == 4 ? 8 : 4) : 0;
+        int csm_try = coef ? (sizeof(T) == 4 ? 8 : 3) : 0;
         if (const char* e = getenv("SISPH_PERS_CACHE")) csm_try = coef ? std::max(0, std::min(atoi(e), 8)) : 0;   // A/B
-        const size_t dyn_try = (size_t)csm_try * SWEEP_T * (4 * sizeof(T) + 4 * sizeof(unsigned short));
+        const size_t dyn_try = (size_t)csm_try * SWEEP_T * (4 * sizeof(T) + 4 * sizeof(unsigned short)) +
+                               (size_t)WCE * SWEEP_T * (sizeof(int) + sizeof(T));   // + the wall cache
         if (pgrid_cache < 0) {
             pgrid_cache = 0;
             {

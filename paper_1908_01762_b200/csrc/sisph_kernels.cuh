@@ -1880,6 +1880,15 @@ template <bool COH, class T> __device__ __forceinline__ T ldp(const T* p) { retu
 // meet by shuffles): walls are few (configs[1]: 3.1k) and each row is long, so one
 // lane per row left the pass bound by a ~45-deep chain of dependent loads
 constexpr int WL = 8;
+// the body-force part of eq:p-shepard's numerator, g . sum_f rho_f W (r_w - r_f), with its fused
+// multiply-adds written out (the grouping the compiler chose in k_ppe_wall, either precision)
+template <class T, int D>
+__device__ __forceinline__ T wall_gr(const Params<T>& P, T sx, T sy, T sz)
+{
+    T gr = fma(sx, P.g[0], sy * P.g[1]);
+    if (D == 3) gr = fma(sz, P.g[2], gr);
+    return gr;
+}
 template <class T, int D, bool COH = false>
 __device__ __forceinline__ void wall_pressure_row(const Params<T>& P, int w, const V4<T>* __restrict__ pos,
                                                   const T* __restrict__ rho, const int* __restrict__ nbr,
@@ -1922,12 +1931,87 @@ __device__ __forceinline__ void wall_pressure_row(const Params<T>& P, int w, con
     if (sub) return;
     T pw = 0;
     if (sw > T(0)) {
-        T gr = P.g[0] * sx + P.g[1] * sy;
-        if (D == 3) gr += P.g[2] * sz;
+        const T gr = wall_gr<T, D>(P, sx, sy, sz);
         pw = (sp + gr) / sw;
     }
     if (P.clamp_wall_p && pw < T(0)) pw = T(0);
     p[i] = pw;
+}
+
+// The persistent loop's wall cache: positions do not move during the solve, so a wall row's
+// Shepard weights W_wf, their sum and the body-force term are constants of the solve; only
+// sum_f p_f W_wf changes per sweep.  Lane `sub` of wall row w stores its fluid entries (index,
+// weight; at most WCE, slot e of thread t at [e * SWEEP_T + t]) in list order and the row's
+// constants; returns the number of entries, or -1 when its share of the row is longer.
+// Same expressions and order as wall_pressure_row.
+constexpr int WCE = 8;
+template <class T, int D, int NT>
+__device__ __forceinline__ int wall_row_cache(const Params<T>& P, int w, const V4<T>* __restrict__ pos,
+                                              const T* __restrict__ rho, const int* __restrict__ nbr,
+                                              const int* __restrict__ cnt, int ncap, int sub, int* cj, T* cwv,
+                                              T& c_sw, T& c_gr)
+{
+    const int i = P.Nf + w;
+    const int n = cnt[i];
+    if (n > WCE * WL) return -1;          // a lane would take more than WCE / 4 chunks
+    V4<T> xi = ld4(pos + i);
+    T sw = 0, sx = 0, sy = 0, sz = 0;
+    int m = 0;
+    const int4* __restrict__ q = reinterpret_cast<const int4*>(nbr + nb_base(i, ncap));
+    auto one = [&](int j) {
+        if (j >= P.Nf) return;
+        V4<T> xj = ld4(pos + j);
+        T d[3], r, ri;
+        r_of(pair_vec<T, D>(P, xi, xj, d), r, ri);
+        T wv = P.sig * quintic5(r * P.inv_h);
+        T rw = __ldg(rho + j) * wv;
+        cj[m * NT] = j;
+        cwv[m * NT] = wv;
+        m++;
+        sx += rw * d[0];
+        sy += rw * d[1];
+        if (D == 3) sz += rw * d[2];
+        sw += wv;
+    };
+    for (int c = 4 * sub; c < n; c += 4 * WL) {
+        const int4 v = LDLIST(q + (size_t)(c >> 2) * 32);
+        one(v.x);
+        if (c + 1 < n) one(v.y);
+        if (c + 2 < n) one(v.z);
+        if (c + 3 < n) one(v.w);
+    }
+    const unsigned gm = ((1u << WL) - 1u) << ((threadIdx.x & 31) & ~(WL - 1));
+#pragma unroll
+    for (int o = WL / 2; o > 0; o >>= 1) {
+        sw += __shfl_xor_sync(gm, sw, o, WL);
+        sx += __shfl_xor_sync(gm, sx, o, WL);
+        sy += __shfl_xor_sync(gm, sy, o, WL);
+        if (D == 3) sz += __shfl_xor_sync(gm, sz, o, WL);
+    }
+    c_sw = sw;
+    c_gr = wall_gr<T, D>(P, sx, sy, sz);
+    return m;
+}
+// one sweep's wall pressure of a cached row from the pressures in p (L2-coherent reads)
+template <class T, int NT>
+__device__ __forceinline__ void wall_row_cached(const Params<T>& P, int w, int m, const int* cj, const T* cwv, T c_sw,
+                                                T c_gr, T* p, int sub)
+{
+    T pj[WCE];
+#pragma unroll
+    for (int e = 0; e < WCE; e++) pj[e] = e < m ? __ldcg(p + cj[e * NT]) : T(0);
+    T sp = 0;
+#pragma unroll
+    for (int e = 0; e < WCE; e++)
+        if (e < m) sp = fma(pj[e], cwv[e * NT], sp);
+    const unsigned gm = ((1u << WL) - 1u) << ((threadIdx.x & 31) & ~(WL - 1));
+#pragma unroll
+    for (int o = WL / 2; o > 0; o >>= 1) sp += __shfl_xor_sync(gm, sp, o, WL);
+    if (sub) return;
+    T pw = 0;
+    if (c_sw > T(0)) pw = (sp + c_gr) / c_sw;
+    if (P.clamp_wall_p && pw < T(0)) pw = T(0);
+    p[P.Nf + w] = pw;
 }
 
 // standalone wall pressure from the pressures in p (before A11's fused sweep, A13)
@@ -2695,13 +2779,28 @@ __global__ void __launch_bounds__(SWEEP_T, SISPH_PERS_MINB) k_ppe_persistent(Par
             }
         }
     }
+    // the wall cache (wall_row_cache): this thread's lane of its first wall row
+    int* const wcj = reinterpret_cast<int*>(cidx + (size_t)csm * SWEEP_T * 4) + threadIdx.x;
+    T* const wcw = reinterpret_cast<T*>(wcj - threadIdx.x + WCE * SWEEP_T) + threadIdx.x;
+    int wm = -1;
+    T c_wsw = 0, c_wgr = 0;
+    if (csm > 0 && !done && wq0 < P.Nwo)
+        wm = wall_row_cache<T, D, SWEEP_T>(P, wq0, pos, rho, nbr, cnt, ncap, threadIdx.x % WL, wcj, wcw, c_wsw, c_wgr);
+    auto walls = [&](T* pbuf) {
+        int q = wq0;
+        if (wm >= 0) {
+            wall_row_cached<T, SWEEP_T>(P, q, wm, wcj, wcw, c_wsw, c_wgr, pbuf, threadIdx.x % WL);
+            q += wqs;
+        }
+        for (; q < P.Nwo; q += wqs)
+            wall_pressure_row<T, D, true>(P, q, pos, rho, nbr, cnt, ncap, pbuf, threadIdx.x % WL);
+    };
     // prologue: the walls of p^kit; then per iteration: sweep | walls of p^{k+1} (speculative:
     // after the last sweep they land in the final buffer's wall slots, which the solve's
     // epilogue overwrites with the walls the last sweep used) overlapped with the decision |
     if (!done) {
         T* pin = (kit & 1) ? pB : pA;
-        for (int q = wq0; q < P.Nwo; q += wqs)
-            wall_pressure_row<T, D, true>(P, q, pos, rho, nbr, cnt, ncap, pin, threadIdx.x % WL);
+        walls(pin);
         pgrid_sync(gbar, (++nbar) * gridDim.x);
     }
     while (!done) {
@@ -2806,8 +2905,7 @@ __global__ void __launch_bounds__(SWEEP_T, SISPH_PERS_MINB) k_ppe_persistent(Par
             a += __ldcg(part + 2 * q);
             b += __ldcg(part + 2 * q + 1);
         }
-        for (int q = wq0; q < P.Nwo; q += wqs)
-            wall_pressure_row<T, D, true>(P, q, pos, rho, nbr, cnt, ncap, pout, threadIdx.x % WL);
+        walls(pout);
         a = warp_sum(a);
         b = warp_sum(b);
         if (lane == 0) {
