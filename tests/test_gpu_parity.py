@@ -459,6 +459,40 @@ def test_sweep_codes_bit_equal(name, loop, monkeypatch):
         assert np.array_equal(sims["1"].get(fld), sims["0"].get(fld)), fld
 
 
+# ------------------------------------------------------------------ the persistent loop's caches
+@pytest.mark.parametrize("name", ["hydro_f64", "db2d_f64", "db3d_f32", "db3d_f64"])
+def test_persistent_loop_caches_bit_equal(name, monkeypatch):
+    """The persistent PPE loop keeps, for the whole solve, p^k of a block's neighbour span
+    in a shared-memory tile, every thread's row (tile slots + stored factors) and every
+    wall lane's Shepard weights (SISPH_PERS_CACHE = cached chunks per row, read at each
+    launch; 0 = the plain form, 1 = almost every row finishes from the list).  Same
+    entries, same order, same fused multiply-adds: bitwise-equal solves, with walls whose
+    rows fit the wall cache (2D) and walls that fall back to the list (3D)."""
+    case = CASES[name]
+    sims = {}
+    for flag in ("0", "1", "8"):
+        monkeypatch.setenv("SISPH_PERS_CACHE", flag)
+        sims[flag] = gpu_sim(case, ppe_loop=3)
+        its = []
+        for _ in range(3):
+            r = sims[flag].step(case.dt)
+            its.append((r.iters, r.residual))
+        sims[flag + "its"] = its
+    for flag in ("1", "8"):
+        assert sims[flag + "its"] == sims["0its"]
+        for fld in ("PRESSURE", "VELOCITY", "POSITION"):
+            assert np.array_equal(sims[flag].get(fld), sims["0"].get(fld)), (flag, fld)
+    # a tight solve: many sweeps on the cached rows
+    monkeypatch.setenv("SISPH_PERS_CACHE", "0")
+    for s in (sims["0"], sims["8"]):
+        s.predict(case.dt)
+    it0 = sims["0"].ppe_solve(1e-7, 60)[0]
+    monkeypatch.setenv("SISPH_PERS_CACHE", "8")
+    it8 = sims["8"].ppe_solve(1e-7, 60)[0]
+    assert it0 == it8
+    assert np.array_equal(sims["8"].get("PRESSURE"), sims["0"].get("PRESSURE"))
+
+
 # ------------------------------------------------------------------ reading R32: mean-free Jacobi
 @pytest.mark.parametrize("name", ["tgv2d_f64", "tgv3d_f64", "hydro_f64", "db2d_f64", "tgv3d_f32"])
 def test_mean_free_solve_parity(name):
