@@ -2698,7 +2698,8 @@ __global__ void __launch_bounds__(SWEEP_T, SISPH_PERS_MINB) k_ppe_persistent(Par
     int f0 = 0, w0 = 0, nfs = 0, nws = 0;
     bool tiled = false;
     if constexpr (STORED) {
-        if (!done && code == nullptr) {
+        // (only with the row cache, csm > 0: the tile alone measured slower than plain gathers)
+        if (!done && code == nullptr && csm > 0) {
             if (threadIdx.x == 0) {
                 span_s[0] = span_s[2] = 0x7fffffff;
                 span_s[1] = span_s[3] = -1;
