@@ -1683,6 +1683,7 @@ template <class T, int D> struct Engine : EngineBase {
     int ppe_loop = 0;              // 0 auto, 1 host-polled batches, 2 graph WHILE node, 3 persistent
     int pgrid_max = 0;             // co-resident blocks of the persistent PPE kernel
     int pgrid_cache = -1;          // ... with the row cache's dynamic shared memory (-1: not asked yet)
+    int pcache_csm = -1;           // the cached chunks per row pgrid_cache was computed for
     cudaStream_t cst = nullptr;    // capture stream (the handle's stream may be the legacy default)
     cudaGraph_t pgraph = nullptr;
     cudaGraphExec_t pexec = nullptr;
@@ -1821,8 +1822,9 @@ template <class T, int D> struct Engine : EngineBase {
         if (const char* e = getenv("SISPH_PERS_CACHE")) csm_try = coef ? std::max(0, std::min(atoi(e), 8)) : 0;   // A/B
         const size_t dyn_try = (size_t)csm_try * SWEEP_T * (4 * sizeof(T) + 4 * sizeof(unsigned short)) +
                                (size_t)WCE * SWEEP_T * (sizeof(int) + sizeof(T));   // + the wall cache
-        if (pgrid_cache < 0) {
+        if (pgrid_cache < 0 || pcache_csm != csm_try) {   // (the A/B switch may change between launches)
             pgrid_cache = 0;
+            pcache_csm = csm_try;
             {
                 int per = 0, dev = 0, sms = 0;
                 if (csm_try && cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_try) == cudaSuccess &&
